@@ -1,0 +1,73 @@
+/* include/nnc_b200.h -- C-ABI of the B200 host library (libnnc_b200.so).
+ *
+ * The drop-in boundary for non-C++ callers (Python ctypes in this repo; cgo /
+ * JNI / N-API stubs in INTEGRATION.md). Each entry point wraps the C++ API that
+ * mirrors the reference (namespace nnc, include paths nnc/<module>.hpp):
+ *
+ *   nnc_model_compile     ingest::parse_model (ref ingest.cpp:411-500) ->
+ *                         passes::optimize (ref passes.cpp:785-793) ->
+ *                         autodiff::derive_versions (ref autodiff.cpp:89-319) ->
+ *                         plan::compile_version_set (ref plan.cpp:441-457)
+ *   nnc_model_run         runtime::execute (ref runtime.cpp:314-462)
+ *   nnc_model_train_step  runtime::train_step (ref runtime.cpp:498-537)
+ *   nnc_group_document    backends::group_layers (ref backends.cpp:321-400)
+ *
+ * Conventions: int status (0 = OK; otherwise 1 + nnc::Error::Code, or 100 for
+ * other failures) with nnc_last_error(); tensors are float32, row-major NHWC;
+ * no exceptions cross the ABI. A model is used by one host thread at a time.
+ */
+#ifndef NNC_B200_H
+#define NNC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct nnc_model nnc_model;
+
+const char* nnc_last_error(void);
+
+/* Parse + optimize + derive versions + compile plans. gemm_precision:
+ * 0 = tcgen05 tf32 (default), 1 = exact fp32 (bit-exact with the reference). */
+nnc_model*  nnc_model_compile(const char* dlb_document, int gemm_precision);
+void        nnc_model_free(nnc_model* m);
+const char* nnc_model_describe(nnc_model* m);          /* JSON: plans, groups, launches, save set */
+
+int nnc_model_set_weight(nnc_model* m, const char* name, const float* data, int64_t n);
+int nnc_model_get_weight(nnc_model* m, const char* name, float* out, int64_t n);
+int nnc_model_set_input(nnc_model* m, const char* name, const float* data, const int64_t* dims, int rank);
+
+/* role: 0 = inference plan, 1 = train_fwd plan (outputs include the SaveSet). */
+int nnc_model_run(nnc_model* m, int role);
+int nnc_model_output(nnc_model* m, const char* name, float* out, int64_t n);
+
+int nnc_model_train_step(nnc_model* m, const float* target, int64_t n, double lr, double* loss);
+int nnc_model_gradients(nnc_model* m, const float* target, int64_t n, double* loss);
+int nnc_model_grad(nnc_model* m, const char* weight, float* out, int64_t n);
+
+/* Device-resident stepping for benchmarks: inputs/target stay on the device. */
+int      nnc_model_trainer_prepare(nnc_model* m, const float* target, int64_t n);
+int      nnc_model_trainer_step_device(nnc_model* m, double lr);
+int      nnc_model_trainer_loss(nnc_model* m, double* loss);
+uint64_t nnc_model_launches_per_step(nnc_model* m);
+uint64_t nnc_model_arena_bytes(nnc_model* m);
+int      nnc_model_infer_device(nnc_model* m);         /* replay inference, no host copies */
+
+/* The device context (nncb_ctx*) for stream events / timing via nncb.h. */
+void* nnc_device_ctx(void);
+
+/* Data parallelism (one process per GPU). */
+int nnc_comm_unique_id(uint8_t id[128]);
+int nnc_init_comm(int nranks, int rank, const uint8_t id[128]);
+
+/* Partition of the optimized inference graph of a document under the B200
+ * default assignment (policy 0) or an explicit {"node": backend_int} JSON map
+ * (assignment_json != NULL). Returns JSON [[members...], ...]. */
+const char* nnc_group_document(const char* dlb_document, const char* assignment_json);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NNC_B200_H */

@@ -1,0 +1,209 @@
+/* include/nncb.h -- thin C-ABI of the B200 kernel layer (libnncb.so).
+ *
+ * The reference has no device layer: every kernel is a C++ template in
+ * core/include/nnc/kernels.hpp run on the host by runtime::execute
+ * (core/src/runtime.cpp:160-306). This header is the sm_100a replacement of
+ * that kernel set, called by the C++ host (libnnc_b200.so) -- never by users
+ * directly. Plain C: int status (0 = OK), nncb_last_error(), no exceptions,
+ * no torch types. One nncb_ctx per GPU, used by one host thread at a time.
+ * All launches are asynchronous on the context's compute stream.
+ *
+ * Which reference routine each entry point replaces is cited per function.
+ */
+#ifndef NNCB_H
+#define NNCB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct nncb_ctx nncb_ctx;
+typedef struct nncb_ew_kernel nncb_ew_kernel;
+
+/* ------------------------------------------------------------------ */
+/*  Context, memory, streams (replaces ExecutionContext's host buffers, */
+/*  runtime.hpp:92-121, and OffloadDevice's byte store, runtime.hpp:47-75) */
+/* ------------------------------------------------------------------ */
+int         nncb_create(int device_ordinal, nncb_ctx** out);
+int         nncb_destroy(nncb_ctx* ctx);
+const char* nncb_last_error(void);
+int         nncb_device_info(nncb_ctx* ctx, int* sm_count, int* cc_major, int* cc_minor,
+                             size_t* total_mem);
+int         nncb_malloc(nncb_ctx* ctx, size_t bytes, void** out);
+int         nncb_free(nncb_ctx* ctx, void* ptr);
+int         nncb_host_alloc(size_t bytes, void** out);        /* pinned host memory */
+int         nncb_host_free(void* ptr);
+int         nncb_memset(nncb_ctx* ctx, void* dst, int value, size_t bytes);
+int         nncb_h2d(nncb_ctx* ctx, void* dst, const void* src, size_t bytes);
+int         nncb_d2h(nncb_ctx* ctx, void* dst, const void* src, size_t bytes);
+int         nncb_d2d(nncb_ctx* ctx, void* dst, const void* src, size_t bytes);
+int         nncb_sync(nncb_ctx* ctx);
+void*       nncb_stream(nncb_ctx* ctx);                       /* cudaStream_t */
+
+/* CUDA-graph capture of a launch sequence (one graph per bound plan). */
+int nncb_capture_begin(nncb_ctx* ctx);
+int nncb_capture_end(nncb_ctx* ctx, void** graph_exec);
+int nncb_graph_launch(nncb_ctx* ctx, void* graph_exec);
+int nncb_graph_destroy(void* graph_exec);
+
+/* Device-side timing on the compute stream. */
+int nncb_event_create(void** ev);
+int nncb_event_record(nncb_ctx* ctx, void* ev);
+int nncb_event_elapsed_ms(void* start, void* stop, float* ms);
+int nncb_event_destroy(void* ev);
+
+/* Number of nncb kernel launches issued on this context (all families). */
+uint64_t nncb_launch_count(nncb_ctx* ctx);
+
+/* ------------------------------------------------------------------ */
+/*  Fused elementwise group: replaces run_ew (runtime.cpp:280-306) and  */
+/*  the per-element REF kernels relu/relu_grad/add/mul/copy            */
+/*  (kernels.hpp:47-70). The program is compiled once to a dedicated   */
+/*  sm_100a kernel (NVRTC) and launched with one pointer per slot.      */
+/* ------------------------------------------------------------------ */
+enum nncb_ew_op {
+    NNCB_EW_LOAD = 0,       /* r[dst] = slot[s][i]                 (mode: element)      */
+    NNCB_EW_LOAD_CH = 1,    /* r[dst] = slot[s][i % C]             (per-channel param)  */
+    NNCB_EW_STORE = 2,      /* slot[s][i] = r[a]                                        */
+    NNCB_EW_RELU = 3,       /* r[dst] = r[a] > 0 ? r[a] : 0  (kernels.hpp:47-50)        */
+    NNCB_EW_RELU_GRAD = 4,  /* r[dst] = r[a] > 0 ? r[b] : 0  (kernels.hpp:52-55)        */
+    NNCB_EW_ADD = 5,        /* r[dst] = r[a] + r[b]  (round-to-nearest, no FMA)         */
+    NNCB_EW_MUL = 6,        /* r[dst] = r[a] * r[b]                                     */
+    NNCB_EW_COPY = 7,       /* r[dst] = r[a]                                            */
+    NNCB_EW_BN_APPLY = 8,   /* r[dst] = ((r[a]-mean)*invstd)*gamma + beta; operands:
+                               b = mean reg, c = invstd reg, d = gamma reg, e = beta reg  */
+    NNCB_EW_GELU = 9,       /* r[dst] = 0.5*x*(1+erf(x/sqrt2)) computed in double        */
+    NNCB_EW_GELU_GRAD = 10, /* r[dst] = g*(Phi(x) + x*phi(x)), a = x, b = g, in double   */
+    NNCB_EW_BN_GRAD = 11,   /* dx = (gamma*invstd) * (g - (sum_g + xhat*sum_gx)/M)
+                               a = x, b = g, c = mean, d = invstd, e = gamma,
+                               f = sum_g reg, h = sum_gx reg; imm = M (count)            */
+    NNCB_EW_BN_INFER = 12,  /* inference BatchNorm from moving statistics:
+                               invstd = (float)(1/sqrt((double)var + imm));
+                               r[dst] = ((x - mean)*invstd)*gamma + beta;
+                               a = x, b = mean, c = var, d = gamma, e = beta         */
+};
+
+typedef struct {
+    int32_t op;
+    int32_t dst, a, b, c, d, e, f, h;
+    int32_t slot;
+    double imm;
+} nncb_ew_instr;
+
+typedef struct {
+    int32_t n_instr;
+    const nncb_ew_instr* instr;
+    int32_t n_regs;
+    int32_t n_slots;
+} nncb_ew_program;
+
+int nncb_ew_compile(nncb_ctx* ctx, const nncb_ew_program* prog, nncb_ew_kernel** out);
+/* n = element count of the group's iteration space, channels = C for LOAD_CH. */
+int nncb_ew_launch(nncb_ctx* ctx, nncb_ew_kernel* k, void* const* slots, int64_t n,
+                   int64_t channels);
+/* Generated CUDA source of a compiled program (for inspection / profiles). */
+const char* nncb_ew_source(nncb_ew_kernel* k);
+
+/* ------------------------------------------------------------------ */
+/*  Tensor-core GEMMs: replace dense/dense_tiled/dense_grad_* and      */
+/*  conv2d/conv2d_tiled/conv2d_grad_* (kernels.hpp:118-243, 354-418).  */
+/* ------------------------------------------------------------------ */
+enum nncb_gemm_kind {
+    NNCB_DENSE_FWD = 0,    /* y[b,o]  = bias[o] + sum_i x[b,i] w[i,o]       kernels.hpp:118-127 */
+    NNCB_DENSE_DGRAD = 1,  /* gx[b,i] = sum_o g[b,o] w[i,o]                 kernels.hpp:130-139 */
+    NNCB_DENSE_WGRAD = 2,  /* gw[i,o] = sum_b x[b,i] g[b,o]                 kernels.hpp:142-151 */
+    NNCB_CONV_FWD = 3,     /* NHWC conv, kernel [kh,kw,ci,co], TF-SAME      kernels.hpp:166-190 */
+    NNCB_CONV_DGRAD = 4,   /* transposed correlation                        kernels.hpp:192-218 */
+    NNCB_CONV_WGRAD = 5,   /* gk[dh,dw,ci,co] = sum x*g                      kernels.hpp:220-243 */
+};
+enum nncb_precision {
+    NNCB_PREC_TF32 = 0,    /* tcgen05.mma kind::tf32, fp32 accumulate in TMEM (default)    */
+    NNCB_PREC_FP32 = 1,    /* exact-order fp32 FFMA path (parity mode)                      */
+};
+enum nncb_epilogue { NNCB_EPI_BIAS = 1, NNCB_EPI_RELU = 2 };
+
+typedef struct {
+    int32_t kind, precision, epilogue, _pad;
+    /* conv geometry, as kernels::ConvGeom (kernels.hpp:20-25) */
+    int64_t n, ih, iw, ci, co, kh, kw, sh, sw, oh, ow, pad_top, pad_left;
+    /* dense geometry */
+    int64_t batch, in_f, out_f;
+} nncb_gemm_desc;
+
+/* FWD:   a = x, b = weight, out = y (bias optional)
+ * DGRAD: a = g, b = weight, out = gx
+ * WGRAD: a = x, b = g,      out = gw                                    */
+int nncb_gemm(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b,
+              const float* bias, float* out);
+
+/* ------------------------------------------------------------------ */
+/*  Pooling (kernels.hpp:258-344)                                       */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    int64_t n, ih, iw, c, kh, kw, sh, sw, oh, ow;
+} nncb_pool_geom;
+/* idx may be NULL; stored as float window-linear index (kernels.hpp:256-283) */
+int nncb_maxpool_fwd(nncb_ctx* ctx, const nncb_pool_geom* g, const float* x, float* y,
+                     float* idx);
+int nncb_maxpool_bwd(nncb_ctx* ctx, const nncb_pool_geom* g, const float* idx, const float* gy,
+                     float* gx);
+int nncb_avgpool_fwd(nncb_ctx* ctx, int64_t n, int64_t ih, int64_t iw, int64_t c, int64_t oh,
+                     int64_t ow, const float* x, float* y);
+int nncb_avgpool_bwd(nncb_ctx* ctx, int64_t n, int64_t ih, int64_t iw, int64_t c, int64_t oh,
+                     int64_t ow, const float* gy, float* gx);
+
+/* ------------------------------------------------------------------ */
+/*  Reductions                                                          */
+/* ------------------------------------------------------------------ */
+/* out[c] = sum_r x[r, c]  (SumCols kernels.hpp:153-160, SumNHW 245-250).
+ * exact = 1: float running sum in row order, bit-identical to the reference;
+ * exact = 0: double accumulation in a fixed two-level tree (fast path).      */
+int nncb_sum_rows(nncb_ctx* ctx, const float* x, float* out, int64_t rows, int64_t cols, int exact);
+/* cumsum along an axis (kernels.hpp:76-111) */
+int nncb_cumsum(nncb_ctx* ctx, const float* x, float* y, int64_t outer, int64_t len,
+                int64_t inner, int exclusive, int reverse);
+
+/* BatchNorm statistics over rows of x[rows, C]: stats[0:C] = mean, stats[C:2C]
+ * = 1/sqrt(var + eps) (biased variance); accumulation in double.           */
+int nncb_bn_stats(nncb_ctx* ctx, const float* x, float* stats, int64_t rows, int64_t C,
+                  double eps);
+/* BatchNorm backward reductions: sum_g[c] = sum g, sum_gx[c] = sum g*xhat.  */
+int nncb_bn_grad_reduce(nncb_ctx* ctx, const float* x, const float* stats, const float* g,
+                        float* sum_g, float* sum_gx, int64_t rows, int64_t C);
+/* LayerNorm over the last axis; gamma/beta [C]; y = xhat*gamma + beta.     */
+int nncb_layernorm_fwd(nncb_ctx* ctx, const float* x, const float* gamma, const float* beta,
+                       float* y, int64_t rows, int64_t C, double eps);
+int nncb_layernorm_bwd(nncb_ctx* ctx, const float* x, const float* gamma, const float* g,
+                       float* gx, int64_t rows, int64_t C, double eps);
+/* dgamma[c] = sum_r g*xhat (row statistics recomputed)                     */
+int nncb_layernorm_dgamma(nncb_ctx* ctx, const float* x, const float* g, float* dgamma,
+                          int64_t rows, int64_t C, double eps);
+
+/* ------------------------------------------------------------------ */
+/*  Loss and update (runtime.cpp:468-496)                              */
+/* ------------------------------------------------------------------ */
+/* grad = sign(p - t)/N (sign(0)=0), *loss_dev (double, device) = sum|p-t|/N */
+int nncb_l1_loss(nncb_ctx* ctx, const float* pred, const float* target, float* grad,
+                 double* loss_dev, int64_t n);
+/* Flat-buffer SGD over the whole parameter region (weights and gradients share
+ * one layout): w = (float)((double)w - lr*((double)g*grad_scale)). With
+ * grad_scale = 1 this is bit-identical to runtime::sgd_step (runtime.cpp:493). */
+int nncb_sgd(nncb_ctx* ctx, float* w, const float* g, int64_t n, double lr, double grad_scale);
+
+/* ------------------------------------------------------------------ */
+/*  Data-parallel collectives (NCCL over NVLink/NVSwitch)               */
+/* ------------------------------------------------------------------ */
+int nncb_comm_unique_id(uint8_t id[128]);
+int nncb_comm_init(nncb_ctx* ctx, int nranks, int rank, const uint8_t id[128]);
+int nncb_comm_destroy(nncb_ctx* ctx);
+/* in-place sum all-reduce of fp32 on the comm stream, ordered after all work
+ * enqueued so far on the compute stream; the compute stream waits for it.  */
+int nncb_allreduce_sum(nncb_ctx* ctx, float* buf, int64_t count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NNCB_H */

@@ -1,0 +1,266 @@
+"""paper_2205_10357_b200 -- B200-native execution backend for SOL-style compiled networks.
+
+Python mirror of the reference's C++ pipeline (nnc::ingest / passes / autodiff /
+plan / runtime), bound through the C-ABI in include/nnc_b200.h. The compute path
+is libnnc_b200.so (C++ host: partitioning, buffer planning, launch scheduling)
+over libnncb.so (hand-written sm_100a kernels, include/nncb.h). There is no CPU
+fallback: if the native libraries are missing, importing this package raises.
+
+Reference call chain being replaced (file:line in /root/reference/proj):
+    ingest::parse_model        core/src/ingest.cpp:411-500
+    passes::optimize           core/src/passes.cpp:785-793
+    autodiff::derive_versions  core/src/autodiff.cpp:89-319
+    plan::compile_version_set  core/src/plan.cpp:441-457
+    runtime::execute           core/src/runtime.cpp:314-462
+    runtime::train_step        core/src/runtime.cpp:498-537
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+from typing import Dict, Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_DIR = os.path.join(_HERE, "lib")
+HOST_LIB = os.path.join(LIB_DIR, "libnnc_b200.so")
+KERNEL_LIB = os.path.join(LIB_DIR, "libnncb.so")
+
+PREC_TF32 = 0   # tcgen05.mma kind::tf32, fp32 accumulation in TMEM
+PREC_FP32 = 1   # exact-order fp32 (bit-identical to the reference CPU kernels)
+
+
+class NNCError(RuntimeError):
+    """Mirror of nnc::Error: `code` is the reference Error::Code value (error.hpp:12-31)."""
+
+    CODES = ["UnknownOp", "ShapeMismatch", "MissingSeed", "BadMagic", "TruncatedTensor",
+             "DuplicateName", "RankError", "ExtentMismatch", "UnknownSymbol", "IllegalOverride",
+             "NoBackend", "UnsupportedInGroup", "NonDifferentiable", "UnboundVdim",
+             "ArenaOverflow", "MissingGrad", "BadToken", "BadDocument", "DeviceError"]
+
+    def __init__(self, status: int, message: str):
+        self.status = status
+        self.code = self.CODES[status - 1] if 1 <= status <= len(self.CODES) else "Internal"
+        super().__init__(f"{self.code}: {message}")
+
+
+def _load():
+    if not os.path.exists(HOST_LIB):
+        raise ImportError(f"{HOST_LIB} is not built; run __graft_entry__.build()")
+    kern = ctypes.CDLL(KERNEL_LIB, mode=ctypes.RTLD_GLOBAL)
+    host = ctypes.CDLL(HOST_LIB, mode=ctypes.RTLD_GLOBAL)
+    P, I, I64, D, U64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_uint64
+    FP, I64P, DP, S = (ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int64),
+                       ctypes.POINTER(ctypes.c_double), ctypes.c_char_p)
+    sig = {
+        "nnc_last_error": (S, []),
+        "nnc_model_compile": (P, [S, I]),
+        "nnc_model_free": (None, [P]),
+        "nnc_model_describe": (S, [P]),
+        "nnc_model_set_weight": (I, [P, S, FP, I64]),
+        "nnc_model_get_weight": (I, [P, S, FP, I64]),
+        "nnc_model_set_input": (I, [P, S, FP, I64P, I]),
+        "nnc_model_run": (I, [P, I]),
+        "nnc_model_output": (I, [P, S, FP, I64]),
+        "nnc_model_train_step": (I, [P, FP, I64, D, DP]),
+        "nnc_model_gradients": (I, [P, FP, I64, DP]),
+        "nnc_model_grad": (I, [P, S, FP, I64]),
+        "nnc_model_trainer_prepare": (I, [P, FP, I64]),
+        "nnc_model_trainer_step_device": (I, [P, D]),
+        "nnc_model_trainer_loss": (I, [P, DP]),
+        "nnc_model_launches_per_step": (U64, [P]),
+        "nnc_model_arena_bytes": (U64, [P]),
+        "nnc_model_infer_device": (I, [P]),
+        "nnc_device_ctx": (P, []),
+        "nnc_comm_unique_id": (I, [ctypes.c_char_p]),
+        "nnc_init_comm": (I, [I, I, ctypes.c_char_p]),
+        "nnc_group_document": (S, [S, S]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(host, name)
+        fn.restype, fn.argtypes = res, args
+    ksig = {
+        "nncb_last_error": (S, []),
+        "nncb_event_create": (I, [ctypes.POINTER(P)]),
+        "nncb_event_record": (I, [P, P]),
+        "nncb_event_elapsed_ms": (I, [P, P, ctypes.POINTER(ctypes.c_float)]),
+        "nncb_event_destroy": (I, [P]),
+        "nncb_sync": (I, [P]),
+        "nncb_launch_count": (U64, [P]),
+    }
+    for name, (res, args) in ksig.items():
+        fn = getattr(kern, name)
+        fn.restype, fn.argtypes = res, args
+    return host, kern
+
+
+_host, _kern = _load()
+
+
+def _check(status: int):
+    if status != 0:
+        raise NNCError(status, _host.nnc_last_error().decode())
+
+
+def _fptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+
+
+def group_document(document: str, assignment: Optional[Dict[str, int]] = None):
+    """backends::group_layers on the optimized inference graph of a DLB document."""
+    res = _host.nnc_group_document(document.encode(),
+                                   json.dumps(assignment).encode() if assignment is not None else None)
+    if res is None:
+        raise NNCError(100, _host.nnc_last_error().decode())
+    return json.loads(res.decode())
+
+
+class CompiledModel:
+    """A document compiled through optimize -> derive_versions -> compile_version_set,
+    holding its HostModel (weights + stamps) on the B200 runtime."""
+
+    def __init__(self, document: str, precision: int = PREC_TF32):
+        h = _host.nnc_model_compile(document.encode(), precision)
+        if not h:
+            raise NNCError(100, _host.nnc_last_error().decode())
+        self._h = h
+        self.describe = json.loads(_host.nnc_model_describe(h).decode())
+        self.weight_shapes = {k: tuple(v) for k, v in self.describe["weights"].items()}
+        inf = self.describe["inference"]
+        outs = [v for v in inf["values"] if v["category"] == "output"]
+        self.pred = outs[0]["name"] if outs else None
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _host.nnc_model_free(self._h)
+            self._h = None
+
+    # -- weights (HostModel) --------------------------------------------
+    def weight(self, name: str) -> np.ndarray:
+        out = np.empty(self.weight_shapes[name], dtype=np.float32)
+        _check(_host.nnc_model_get_weight(self._h, name.encode(), _fptr(out), out.size))
+        return out
+
+    def set_weight(self, name: str, value: np.ndarray):
+        v = np.ascontiguousarray(value, dtype=np.float32)
+        _check(_host.nnc_model_set_weight(self._h, name.encode(), _fptr(v), v.size))
+
+    # -- execution --------------------------------------------------------
+    def feed(self, name: str, value: np.ndarray):
+        v = np.ascontiguousarray(value, dtype=np.float32)
+        dims = (ctypes.c_int64 * v.ndim)(*v.shape)
+        _check(_host.nnc_model_set_input(self._h, name.encode(), _fptr(v), dims, v.ndim))
+
+    def _plan_value(self, role: str, name: str):
+        for v in self.describe[role]["values"]:
+            if v["name"] == name:
+                return v
+        raise KeyError(name)
+
+    def run(self, inputs: Dict[str, np.ndarray], role: str = "inference") -> Dict[str, np.ndarray]:
+        """runtime::execute on the inference (or train_fwd) plan; returns every output."""
+        for k, v in inputs.items():
+            self.feed(k, v)
+        _check(_host.nnc_model_run(self._h, 1 if role == "train_fwd" else 0))
+        out = {}
+        plan = self.describe[role]
+        out_names = [plan["values"][i]["name"] for i in range(len(plan["values"]))
+                     if plan["values"][i]["category"] in ("output", "saved") and plan["values"][i]["resident"]]
+        for name in out_names:
+            v = self._plan_value(role, name)
+            if v["storage"] != "buffer":
+                continue
+            arr = np.empty(v["dims"], dtype=np.float32)
+            if _host.nnc_model_output(self._h, name.encode(), _fptr(arr), arr.size) == 0:
+                out[name] = arr
+        return out
+
+    def train_step(self, inputs: Dict[str, np.ndarray], target: np.ndarray, lr: float) -> float:
+        for k, v in inputs.items():
+            self.feed(k, v)
+        t = np.ascontiguousarray(target, dtype=np.float32)
+        loss = ctypes.c_double()
+        _check(_host.nnc_model_train_step(self._h, _fptr(t), t.size, lr, ctypes.byref(loss)))
+        return loss.value
+
+    def gradients(self, inputs: Dict[str, np.ndarray], target: np.ndarray):
+        for k, v in inputs.items():
+            self.feed(k, v)
+        t = np.ascontiguousarray(target, dtype=np.float32)
+        loss = ctypes.c_double()
+        _check(_host.nnc_model_gradients(self._h, _fptr(t), t.size, ctypes.byref(loss)))
+        grads = {}
+        for w in self.describe["weight_grads"]:
+            g = np.empty(self.weight_shapes[w], dtype=np.float32)
+            _check(_host.nnc_model_grad(self._h, w.encode(), _fptr(g), g.size))
+            grads[w] = g
+        return loss.value, grads
+
+    # -- device-resident stepping (benchmarks) ------------------------------
+    def trainer_prepare(self, inputs: Dict[str, np.ndarray], target: np.ndarray):
+        for k, v in inputs.items():
+            self.feed(k, v)
+        t = np.ascontiguousarray(target, dtype=np.float32)
+        _check(_host.nnc_model_trainer_prepare(self._h, _fptr(t), t.size))
+
+    def trainer_step_device(self, lr: float):
+        _check(_host.nnc_model_trainer_step_device(self._h, lr))
+
+    def trainer_loss(self) -> float:
+        loss = ctypes.c_double()
+        _check(_host.nnc_model_trainer_loss(self._h, ctypes.byref(loss)))
+        return loss.value
+
+    def launches_per_step(self) -> int:
+        return int(_host.nnc_model_launches_per_step(self._h))
+
+    def arena_bytes(self) -> int:
+        return int(_host.nnc_model_arena_bytes(self._h))
+
+    def infer_device(self):
+        _check(_host.nnc_model_infer_device(self._h))
+
+
+class DeviceTimer:
+    """CUDA events on the runtime's compute stream (the stream every kernel of
+    the backend is launched on)."""
+
+    def __init__(self):
+        self.ctx = _host.nnc_device_ctx()
+        if not self.ctx:
+            raise NNCError(100, _host.nnc_last_error().decode())
+        self.a, self.b = ctypes.c_void_p(), ctypes.c_void_p()
+        _kern.nncb_event_create(ctypes.byref(self.a))
+        _kern.nncb_event_create(ctypes.byref(self.b))
+
+    def start(self):
+        _kern.nncb_event_record(self.ctx, self.a)
+
+    def stop(self) -> float:
+        _kern.nncb_event_record(self.ctx, self.b)
+        ms = ctypes.c_float()
+        if _kern.nncb_event_elapsed_ms(self.a, self.b, ctypes.byref(ms)) != 0:
+            raise NNCError(100, _kern.nncb_last_error().decode())
+        return ms.value
+
+    def sync(self):
+        _kern.nncb_sync(self.ctx)
+
+    def launches(self) -> int:
+        return int(_kern.nncb_launch_count(self.ctx))
+
+
+def comm_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_host.nnc_comm_unique_id(buf))
+    return buf.raw
+
+
+def init_comm(nranks: int, rank: int, uid: bytes):
+    _check(_host.nnc_init_comm(nranks, rank, uid))
+
+
+__all__ = ["CompiledModel", "DeviceTimer", "NNCError", "group_document", "comm_unique_id",
+           "init_comm", "PREC_TF32", "PREC_FP32", "HOST_LIB", "KERNEL_LIB"]

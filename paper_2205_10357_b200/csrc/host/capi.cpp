@@ -1,0 +1,282 @@
+// capi.cpp -- extern "C" surface of libnnc_b200.so (include/nnc_b200.h).
+#include "nnc_b200.h"
+
+#include <cstring>
+#include <memory>
+#include <sstream>
+
+#include <json.hpp>
+
+#include "nnc/autodiff.hpp"
+#include "nnc/backends.hpp"
+#include "nnc/ingest.hpp"
+#include "nnc/passes.hpp"
+#include "nnc/plan.hpp"
+#include "nnc/runtime.hpp"
+
+using namespace nnc;
+
+struct nnc_model {
+    ingest::Model model;
+    hlir::Graph optimized;
+    autodiff::VersionSet versions;
+    plan::VersionPlans plans;
+    std::unique_ptr<runtime::HostModel> host;
+    runtime::ExecOptions opts;
+    std::map<std::string, Tensor> inputs;
+    std::map<std::string, Tensor> outputs;
+    std::map<std::string, Tensor> grads;
+    std::unique_ptr<runtime::Trainer> trainer;
+    std::string desc;
+};
+
+namespace {
+
+thread_local std::string g_err;
+thread_local std::string g_buf;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const Error& e) {
+        g_err = e.what();
+        return 1 + static_cast<int>(e.code());
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 100;
+    }
+}
+
+std::string jstr(const std::string& s) { return nlohmann::json(s).dump(); }
+
+void describe_plan(std::ostringstream& os, const plan::ExecutionPlan& p) {
+    os << "{\"groups\":[";
+    for (size_t i = 0; i < p.groups.size(); ++i) {
+        const auto& g = p.groups[i];
+        os << (i ? "," : "") << "{\"backend\":" << jstr(backends::backend_name(g.backend)) << ",\"label\":" << jstr(g.label)
+           << ",\"members\":[";
+        for (size_t k = 0; k < g.members.size(); ++k) os << (k ? "," : "") << jstr(g.members[k]);
+        os << "],\"launches\":[";
+        for (size_t k = 0; k < g.launches.size(); ++k) {
+            const auto& L = g.launches[k];
+            os << (k ? "," : "") << "{\"kind\":" << jstr(plan::launch_kind_name(L.kind)) << ",\"label\":" << jstr(L.label)
+               << ",\"instrs\":" << L.ew.size() << ",\"args\":[";
+            for (size_t a = 0; a < L.args.size(); ++a)
+                os << (a ? "," : "") << "[" << jstr(p.values[L.args[a].slot].name) << "," << L.args[a].offset << ","
+                   << (L.is_out[a] ? 1 : 0) << "]";
+            os << "]}";
+        }
+        os << "]}";
+    }
+    os << "],\"exec_steps\":[";
+    for (size_t i = 0; i < p.exec_steps.size(); ++i) os << (i ? "," : "") << jstr(p.exec_steps[i].label);
+    os << "],\"values\":[";
+    for (size_t i = 0; i < p.values.size(); ++i) {
+        const auto& v = p.values[i];
+        os << (i ? "," : "") << "{\"name\":" << jstr(v.name) << ",\"category\":" << jstr(plan::category_name(v.category))
+           << ",\"storage\":" << (v.storage == plan::StorageClass::Buffer ? "\"buffer\"" : "\"register\"")
+           << ",\"resident\":" << (v.resident ? "true" : "false") << ",\"dims\":[";
+        for (size_t d = 0; d < v.dims.size(); ++d) os << (d ? "," : "") << v.dims[d];
+        os << "]}";
+    }
+    os << "],\"events\":[";
+    for (size_t i = 0; i < p.events.size(); ++i)
+        os << (i ? "," : "") << "[" << p.events[i].step << "," << (p.events[i].alloc ? 1 : 0) << "," << p.events[i].slot
+           << "]";
+    os << "],\"launch_count\":" << p.launch_count() << "}";
+}
+
+Tensor make(const float* data, const int64_t* dims, int rank) {
+    Tensor t(DType::F32, std::vector<int64_t>(dims, dims + rank));
+    std::memcpy(t.data(), data, t.byte_size());
+    return t;
+}
+
+const plan::ExecutionPlan& pred_plan(nnc_model* m) { return m->plans.inference; }
+
+Tensor target_tensor(nnc_model* m, const float* target, int64_t n) {
+    const auto& p = pred_plan(m);
+    const auto& v = p.values[p.output_slots.at(0)];
+    if (element_count(v.dims) != n) throw Error(Error::Code::ShapeMismatch, "target size mismatch");
+    return make(target, v.dims.data(), static_cast<int>(v.dims.size()));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* nnc_last_error(void) { return g_err.c_str(); }
+
+nnc_model* nnc_model_compile(const char* doc, int precision) {
+    auto m = std::make_unique<nnc_model>();
+    int rc = guarded([&] {
+        m->model = ingest::parse_model(doc);
+        m->optimized = passes::optimize(m->model.graph).graph;
+        m->versions = autodiff::derive_versions(m->optimized);
+        m->plans = plan::compile_version_set(m->versions, [](const hlir::Graph& g) { return backends::default_assignment(g); });
+        m->host = std::make_unique<runtime::HostModel>(runtime::HostModel::from_graph(m->optimized));
+        m->opts.gemm_precision = precision;
+    });
+    return rc ? nullptr : m.release();
+}
+
+void nnc_model_free(nnc_model* m) {
+    if (!m) return;
+    try {
+        m->trainer.reset();
+        runtime::release(m->plans);
+    } catch (...) {
+    }
+    delete m;
+}
+
+const char* nnc_model_describe(nnc_model* m) {
+    std::ostringstream os;
+    os << "{\"inference\":";
+    describe_plan(os, m->plans.inference);
+    os << ",\"train_fwd\":";
+    describe_plan(os, m->plans.train_fwd);
+    os << ",\"train_bwd\":";
+    describe_plan(os, m->plans.train_bwd);
+    os << ",\"save_set\":" << nlohmann::json(m->plans.save_set).dump();
+    os << ",\"output_grads\":" << nlohmann::json(m->plans.output_grads).dump();
+    os << ",\"weight_grads\":" << nlohmann::json(m->plans.weight_grads).dump();
+    os << ",\"weights\":{";
+    size_t k = 0;
+    for (const auto& name : m->host->names()) os << (k++ ? "," : "") << jstr(name) << ":" << nlohmann::json(m->optimized.initializers.at(name).dims()).dump();
+    auto peak = plan::estimate_peak(m->plans, 64);
+    os << "},\"peak\":{\"inference\":" << peak.inference_bytes << ",\"training\":" << peak.training_bytes << "}}";
+    m->desc = os.str();
+    return m->desc.c_str();
+}
+
+int nnc_model_set_weight(nnc_model* m, const char* name, const float* data, int64_t n) {
+    return guarded([&] {
+        Tensor t = m->host->tensor(name);
+        if (t.elements() != n) throw Error(Error::Code::ShapeMismatch, std::string(name) + ": size mismatch");
+        std::memcpy(t.data(), data, t.byte_size());
+        m->host->set(name, std::move(t));
+    });
+}
+
+int nnc_model_get_weight(nnc_model* m, const char* name, float* out, int64_t n) {
+    return guarded([&] {
+        const Tensor& t = m->host->tensor(name);
+        if (t.elements() != n) throw Error(Error::Code::ShapeMismatch, std::string(name) + ": size mismatch");
+        std::memcpy(out, t.data(), t.byte_size());
+    });
+}
+
+int nnc_model_set_input(nnc_model* m, const char* name, const float* data, const int64_t* dims, int rank) {
+    return guarded([&] { m->inputs[name] = make(data, dims, rank); });
+}
+
+int nnc_model_run(nnc_model* m, int role) {
+    return guarded([&] {
+        const plan::ExecutionPlan& p = role == 1 ? m->plans.train_fwd : m->plans.inference;
+        m->outputs = runtime::execute(p, m->inputs, *m->host, nullptr, m->opts);
+    });
+}
+
+int nnc_model_output(nnc_model* m, const char* name, float* out, int64_t n) {
+    return guarded([&] {
+        auto it = m->outputs.find(name);
+        if (it == m->outputs.end()) throw Error(Error::Code::ShapeMismatch, std::string("no output ") + name);
+        if (it->second.elements() != n) throw Error(Error::Code::ShapeMismatch, "output size mismatch");
+        std::memcpy(out, it->second.data(), it->second.byte_size());
+    });
+}
+
+int nnc_model_train_step(nnc_model* m, const float* target, int64_t n, double lr, double* loss) {
+    return guarded([&] { *loss = runtime::train_step(m->plans, m->inputs, target_tensor(m, target, n), *m->host, lr, nullptr, m->opts); });
+}
+
+int nnc_model_gradients(nnc_model* m, const float* target, int64_t n, double* loss) {
+    return guarded([&] { m->grads = runtime::gradients(m->plans, m->inputs, target_tensor(m, target, n), *m->host, loss, nullptr, m->opts); });
+}
+
+int nnc_model_grad(nnc_model* m, const char* weight, float* out, int64_t n) {
+    return guarded([&] {
+        auto it = m->grads.find(weight);
+        if (it == m->grads.end()) throw Error(Error::Code::MissingGrad, std::string("no gradient for ") + weight);
+        if (it->second.elements() != n) throw Error(Error::Code::ShapeMismatch, "gradient size mismatch");
+        std::memcpy(out, it->second.data(), it->second.byte_size());
+    });
+}
+
+int nnc_model_trainer_prepare(nnc_model* m, const float* target, int64_t n) {
+    return guarded([&] {
+        auto& dev = runtime::default_device();
+        m->trainer = std::make_unique<runtime::Trainer>(m->plans, *m->host, dev, m->opts);
+        Tensor t = target_tensor(m, target, n);
+        // one full host step uploads inputs + target and warms every kernel
+        m->trainer->step(m->inputs, t, 0.0);
+    });
+}
+
+int nnc_model_trainer_step_device(nnc_model* m, double lr) {
+    return guarded([&] {
+        if (!m->trainer) throw Error(Error::Code::BadDocument, "trainer not prepared");
+        m->trainer->step_device(lr);
+    });
+}
+
+int nnc_model_trainer_loss(nnc_model* m, double* loss) {
+    return guarded([&] {
+        if (!m->trainer) throw Error(Error::Code::BadDocument, "trainer not prepared");
+        *loss = m->trainer->last_loss();
+    });
+}
+
+uint64_t nnc_model_launches_per_step(nnc_model* m) { return m->trainer ? m->trainer->launches_per_step() : 0; }
+uint64_t nnc_model_arena_bytes(nnc_model* m) { return m->trainer ? m->trainer->arena_bytes() : 0; }
+
+int nnc_model_infer_device(nnc_model* m) {
+    return guarded([&] {
+        std::set<std::string> none;
+        runtime::ExecOptions o = m->opts;
+        o.materialize = &none;
+        runtime::execute(m->plans.inference, m->inputs, *m->host, nullptr, o);
+    });
+}
+
+void* nnc_device_ctx(void) {
+    try {
+        return runtime::default_device().ctx();
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+int nnc_comm_unique_id(uint8_t id[128]) {
+    if (nncb_comm_unique_id(id)) {
+        g_err = nncb_last_error();
+        return 100;
+    }
+    return 0;
+}
+
+int nnc_init_comm(int nranks, int rank, const uint8_t id[128]) {
+    return guarded([&] { runtime::default_device().init_comm(nranks, rank, id); });
+}
+
+const char* nnc_group_document(const char* doc, const char* assignment_json) {
+    int rc = guarded([&] {
+        auto model = ingest::parse_model(doc);
+        auto g = passes::optimize(model.graph).graph;
+        std::vector<std::vector<std::string>> groups;
+        if (assignment_json) {
+            std::map<std::string, int> a = nlohmann::json::parse(assignment_json).get<std::map<std::string, int>>();
+            groups = backends::group_layers_ints(g, a);
+        } else {
+            for (const auto& fg : backends::group_layers(g, backends::default_assignment(g))) groups.push_back(fg.members);
+        }
+        g_buf = nlohmann::json(groups).dump();
+    });
+    return rc ? nullptr : g_buf.c_str();
+}
+
+}  // extern "C"

@@ -1,0 +1,865 @@
+// runtime.cpp -- the B200 executor behind runtime::execute / train_step.
+//
+// Reference semantics kept (runtime.cpp:314-537): inputs bind by name and must
+// match the plan's shapes (ShapeMismatch), parameters come from the HostModel
+// through a version-stamped device cache (the OffloadDevice protocol,
+// runtime.cpp:71-102: a weight crosses to the device only when its stamp is
+// stale, counted in SyncStats), outputs are materialized by name (optionally a
+// subset), train_step runs forward -> L1 loss -> backward -> SGD with the four
+// trace phases (runtime.cpp:506-527).
+//
+// B200 design:
+//  * Bind once per plan: every Buffer value gets an arena offset from a replay
+//    of the plan's static alloc/free events (best-fit, 256-byte aligned), so
+//    the whole plan runs out of ONE device allocation; kernels (generated
+//    fused-group kernels, GEMM descriptors, pool geometry) are resolved to raw
+//    pointers at bind time.
+//  * Run: the launch list is captured once into a CUDA graph and replayed.
+//  * Training: parameters live in one flat device region and weight gradients
+//    in a second flat region with the same layout; backward GEMM/reduction
+//    kernels write gradients straight into it, the data-parallel all-reduce
+//    (NCCL) runs over it in buckets, and SGD is one kernel over the region.
+//    Forward, loss, backward, all-reduce and update are one CUDA graph.
+#include "nnc/runtime.hpp"
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <list>
+#include <mutex>
+#include <unordered_map>
+
+#include "nnc/geometry.hpp"
+
+namespace nnc::runtime {
+
+using plan::ExecutionPlan;
+using plan::Launch;
+using plan::LaunchKind;
+using plan::MemCategory;
+using plan::StorageClass;
+
+namespace {
+
+[[noreturn]] void device_fail(const std::string& what) {
+    throw Error(Error::Code::DeviceError, what + ": " + nncb_last_error());
+}
+#define NNC_CHECK(expr)                                         \
+    do {                                                        \
+        if ((expr) != 0) device_fail(#expr);                    \
+    } while (0)
+
+constexpr int64_t kAlign = 256;
+
+int64_t value_bytes(const ExecutionPlan& p, uint32_t s) {
+    return static_cast<int64_t>(element_count(p.values[s].dims)) * static_cast<int64_t>(dtype_size(p.dtype));
+}
+
+/// Best-fit offset allocator over a static schedule (free blocks coalesce).
+class OffsetPlanner {
+public:
+    int64_t alloc(int64_t bytes) {
+        bytes = plan::align_bytes(std::max<int64_t>(bytes, 1), kAlign);
+        auto best = free_.end();
+        for (auto it = free_.begin(); it != free_.end(); ++it)
+            if (it->second >= bytes && (best == free_.end() || it->second < best->second)) best = it;
+        int64_t off;
+        if (best != free_.end()) {
+            off = best->first;
+            int64_t rest = best->second - bytes;
+            free_.erase(best);
+            if (rest > 0) free_[off + bytes] = rest;
+        } else {
+            off = top_;
+            top_ += bytes;
+            high_ = std::max(high_, top_);
+        }
+        sizes_[off] = bytes;
+        return off;
+    }
+    void release(int64_t off) {
+        auto sz = sizes_.find(off);
+        if (sz == sizes_.end()) return;
+        auto it = free_.emplace(off, sz->second).first;
+        sizes_.erase(sz);
+        auto nx = std::next(it);
+        if (nx != free_.end() && it->first + it->second == nx->first) {
+            it->second += nx->second;
+            free_.erase(nx);
+        }
+        if (it != free_.begin()) {
+            auto pv = std::prev(it);
+            if (pv->first + pv->second == it->first) {
+                pv->second += it->second;
+                free_.erase(it);
+                it = pv;
+            }
+        }
+        if (it->first + it->second == top_) {
+            top_ = it->first;
+            free_.erase(it);
+        }
+    }
+    int64_t high() const { return high_; }
+    void note() {}
+
+private:
+    std::map<int64_t, int64_t> free_;
+    std::map<int64_t, int64_t> sizes_;
+    int64_t top_ = 0, high_ = 0;
+};
+
+struct BoundLaunch {
+    LaunchKind kind;
+    std::vector<void*> ptrs;
+    nncb_ew_kernel* ew = nullptr;
+    int64_t n = 0, c = 0;
+    nncb_gemm_desc gemm{};
+    nncb_pool_geom pool{};
+    int64_t d0 = 0, d1 = 0, d2 = 0, d3 = 0, d4 = 0, d5 = 0;
+    double eps = 0;
+    int flag0 = 0, flag1 = 0;
+};
+
+void enqueue(nncb_ctx* ctx, const BoundLaunch& b) {
+    auto P = [&](size_t i) { return static_cast<float*>(b.ptrs.at(i)); };
+    switch (b.kind) {
+        case LaunchKind::Ew: NNC_CHECK(nncb_ew_launch(ctx, b.ew, b.ptrs.data(), b.n, b.c)); break;
+        case LaunchKind::Gemm:
+            NNC_CHECK(nncb_gemm(ctx, &b.gemm, P(0), P(1), b.flag0 ? P(2) : nullptr, P(b.ptrs.size() - 1)));
+            break;
+        case LaunchKind::MaxPool:
+            NNC_CHECK(nncb_maxpool_fwd(ctx, &b.pool, P(0), P(1), b.ptrs.size() > 2 ? P(2) : nullptr));
+            break;
+        case LaunchKind::MaxPoolGrad: NNC_CHECK(nncb_maxpool_bwd(ctx, &b.pool, P(0), P(1), P(2))); break;
+        case LaunchKind::AvgPool: NNC_CHECK(nncb_avgpool_fwd(ctx, b.d0, b.d1, b.d2, b.d3, b.d4, b.d5, P(0), P(1))); break;
+        case LaunchKind::AvgPoolGrad:
+            NNC_CHECK(nncb_avgpool_bwd(ctx, b.d0, b.d1, b.d2, b.d3, b.d4, b.d5, P(0), P(1)));
+            break;
+        case LaunchKind::SumRows: NNC_CHECK(nncb_sum_rows(ctx, P(0), P(1), b.d0, b.d1, b.flag0)); break;
+        case LaunchKind::CumSum: NNC_CHECK(nncb_cumsum(ctx, P(0), P(1), b.d0, b.d1, b.d2, b.flag0, b.flag1)); break;
+        case LaunchKind::BnStats: NNC_CHECK(nncb_bn_stats(ctx, P(0), P(1), b.d0, b.d1, b.eps)); break;
+        case LaunchKind::BnGradReduce:
+            NNC_CHECK(nncb_bn_grad_reduce(ctx, P(0), P(1), P(2), P(3), P(4), b.d0, b.d1));
+            break;
+        case LaunchKind::LnFwd: NNC_CHECK(nncb_layernorm_fwd(ctx, P(0), P(1), P(2), P(3), b.d0, b.d1, b.eps)); break;
+        case LaunchKind::LnBwd: NNC_CHECK(nncb_layernorm_bwd(ctx, P(0), P(1), P(2), P(3), b.d0, b.d1, b.eps)); break;
+        case LaunchKind::LnDgamma: NNC_CHECK(nncb_layernorm_dgamma(ctx, P(0), P(1), P(2), b.d0, b.d1, b.eps)); break;
+    }
+}
+
+}  // namespace
+
+/* ------------------------------------------------------------------ */
+/*  Program: one or more plans bound to device memory                  */
+/* ------------------------------------------------------------------ */
+
+struct Program {
+    Device* dev = nullptr;
+    std::vector<const ExecutionPlan*> plans;
+    void* arena = nullptr;
+    int64_t arena_bytes = 0;
+    std::unordered_map<std::string, void*> where;   // value name -> device pointer
+    std::vector<std::vector<BoundLaunch>> steps;     // per plan, flattened launches
+    std::vector<std::vector<std::pair<size_t, std::string>>> step_labels;  // per plan: (launch idx, label)
+    int precision = NNCB_PREC_TF32;
+
+    ~Program() {
+        if (arena) nncb_free(dev->ctx(), arena);
+    }
+
+    void* ptr(const std::string& name) const {
+        auto it = where.find(name);
+        if (it == where.end()) throw Error(Error::Code::ShapeMismatch, "no device buffer for " + name);
+        return it->second;
+    }
+
+    /// `param_ptr(name)` supplies Parameter buffers; `fixed(name)` may pin other
+    /// values (flat gradient region) -- return nullptr to arena-allocate.
+    void bind(const std::function<void*(const std::string&)>& param_ptr,
+              const std::function<void*(const std::string&)>& fixed) {
+        OffsetPlanner pl;
+        std::unordered_map<std::string, int64_t> offset;
+        std::unordered_map<std::string, bool> live;
+        for (const ExecutionPlan* p : plans)
+            for (const plan::PlanEvent& ev : p->events) {
+                const plan::ValueEntry& v = p->values[ev.slot];
+                if (v.storage != StorageClass::Buffer) continue;
+                if (v.category == MemCategory::Parameter) {
+                    if (!where.count(v.name)) where[v.name] = param_ptr(v.source_weight);
+                    continue;
+                }
+                if (ev.alloc) {
+                    if (live[v.name] || where.count(v.name)) continue;
+                    if (void* f = fixed(v.name)) {
+                        where[v.name] = f;
+                        continue;
+                    }
+                    offset[v.name] = pl.alloc(value_bytes(*p, ev.slot));
+                    live[v.name] = true;
+                    pl.note();
+                } else {
+                    auto it = offset.find(v.name);
+                    if (it != offset.end() && live[v.name]) {
+                        pl.release(it->second);
+                        live[v.name] = false;
+                    }
+                }
+            }
+        arena_bytes = std::max<int64_t>(pl.high(), kAlign);
+        NNC_CHECK(nncb_malloc(dev->ctx(), static_cast<size_t>(arena_bytes), &arena));
+        for (auto& [name, off] : offset) where[name] = static_cast<char*>(arena) + off;
+        // every referenced Buffer value must have storage (values produced but
+        // never in an alloc event, e.g. scratch, get arena space too)
+        for (const ExecutionPlan* p : plans)
+            for (const auto& v : p->values)
+                if (v.storage == StorageClass::Buffer && !where.count(v.name))
+                    throw Error(Error::Code::ArenaOverflow, "value " + v.name + " has no schedule entry");
+        // resolve launches
+        for (const ExecutionPlan* p : plans) {
+            steps.emplace_back();
+            step_labels.emplace_back();
+            for (const plan::ExecStep& es : p->exec_steps) {
+                step_labels.back().push_back({steps.back().size(), es.label});
+                for (uint32_t li : es.launches) steps.back().push_back(resolve(*p, p->groups[es.group].launches[li]));
+            }
+        }
+    }
+
+    BoundLaunch resolve(const ExecutionPlan& p, const Launch& L) {
+        BoundLaunch b;
+        b.kind = L.kind;
+        for (const plan::Arg& a : L.args)
+            b.ptrs.push_back(static_cast<float*>(ptr(p.values[a.slot].name)) + a.offset);
+        auto dims = [&](size_t arg) -> const std::vector<int64_t>& { return p.values[L.args.at(arg).slot].dims; };
+        const hlir::Attrs& at = L.attrs;
+        switch (L.kind) {
+            case LaunchKind::Ew: {
+                nncb_ew_program prog{static_cast<int32_t>(L.ew.size()), L.ew.data(), L.ew_regs,
+                                     static_cast<int32_t>(L.args.size())};
+                NNC_CHECK(nncb_ew_compile(dev->ctx(), &prog, &b.ew));
+                b.n = element_count(p.values[L.elem_slot].dims);
+                b.c = at.out_channels;
+                break;
+            }
+            case LaunchKind::Gemm: {
+                nncb_gemm_desc& d = b.gemm;
+                d.precision = precision;
+                switch (L.op) {
+                    case hlir::OpKind::Conv2D:
+                        d.kind = NNCB_CONV_FWD;
+                        geom::conv_geometry(d, dims(0), at);
+                        b.flag0 = at.has_bias ? 1 : 0;
+                        d.epilogue = at.has_bias ? NNCB_EPI_BIAS : 0;
+                        break;
+                    case hlir::OpKind::Conv2DGradInput:
+                        d.kind = NNCB_CONV_DGRAD;
+                        geom::conv_geometry(d, dims(L.args.size() - 1), at);
+                        break;
+                    case hlir::OpKind::Conv2DGradWeight:
+                        d.kind = NNCB_CONV_WGRAD;
+                        geom::conv_geometry(d, dims(0), at);
+                        break;
+                    case hlir::OpKind::Dense:
+                        d.kind = NNCB_DENSE_FWD;
+                        d.batch = dims(0)[0];
+                        d.in_f = dims(0)[1];
+                        d.out_f = at.out_features;
+                        b.flag0 = at.has_bias ? 1 : 0;
+                        d.epilogue = at.has_bias ? NNCB_EPI_BIAS : 0;
+                        break;
+                    case hlir::OpKind::DenseGradInput:
+                        d.kind = NNCB_DENSE_DGRAD;
+                        d.batch = dims(0)[0];
+                        d.out_f = dims(0)[1];
+                        d.in_f = dims(1)[0];
+                        break;
+                    case hlir::OpKind::DenseGradWeight:
+                        d.kind = NNCB_DENSE_WGRAD;
+                        d.batch = dims(0)[0];
+                        d.in_f = dims(0)[1];
+                        d.out_f = dims(1)[1];
+                        break;
+                    default: throw Error(Error::Code::UnsupportedInGroup, "not a GEMM op");
+                }
+                break;
+            }
+            case LaunchKind::MaxPool: b.pool = geom::pool_geometry(dims(0), at); break;
+            case LaunchKind::MaxPoolGrad: b.pool = geom::pool_geometry(dims(2), at); break;
+            case LaunchKind::AvgPool: {
+                const auto& x = dims(0);
+                b.d0 = x[0]; b.d1 = x[1]; b.d2 = x[2]; b.d3 = x[3]; b.d4 = at.out_hw[0]; b.d5 = at.out_hw[1];
+                break;
+            }
+            case LaunchKind::AvgPoolGrad: {
+                const auto& gx = dims(1);
+                const auto& gy = dims(0);
+                b.d0 = gx[0]; b.d1 = gx[1]; b.d2 = gx[2]; b.d3 = gx[3]; b.d4 = gy[1]; b.d5 = gy[2];
+                break;
+            }
+            case LaunchKind::SumRows: {
+                const auto& x = dims(0);
+                b.d1 = x.back();
+                b.d0 = element_count(x) / std::max<int64_t>(b.d1, 1);
+                b.flag0 = precision == NNCB_PREC_FP32 ? 1 : 0;
+                break;
+            }
+            case LaunchKind::CumSum: {
+                const auto& x = dims(0);
+                int64_t outer = 1, inner = 1;
+                for (int64_t i = 0; i < at.axis; ++i) outer *= x[i];
+                for (size_t i = at.axis + 1; i < x.size(); ++i) inner *= x[i];
+                b.d0 = outer; b.d1 = x.empty() ? 1 : x[at.axis]; b.d2 = inner;
+                b.flag0 = at.exclusive; b.flag1 = at.reverse;
+                break;
+            }
+            case LaunchKind::BnStats:
+            case LaunchKind::BnGradReduce:
+            case LaunchKind::LnFwd:
+            case LaunchKind::LnBwd:
+            case LaunchKind::LnDgamma: {
+                const auto& x = dims(0);
+                b.d1 = x.back();
+                b.d0 = element_count(x) / b.d1;
+                b.eps = at.eps;
+                break;
+            }
+        }
+        return b;
+    }
+
+    void enqueue_plan(size_t pi, std::vector<std::string>* trace) const {
+        const auto& labels = step_labels[pi];
+        size_t li = 0;
+        for (size_t k = 0; k < steps[pi].size(); ++k) {
+            while (trace && li < labels.size() && labels[li].first == k) trace->push_back("exec:" + labels[li++].second);
+            enqueue(dev->ctx(), steps[pi][k]);
+        }
+        while (trace && li < labels.size()) trace->push_back("exec:" + labels[li++].second);
+    }
+};
+
+/* ------------------------------------------------------------------ */
+/*  HostModel                                                          */
+/* ------------------------------------------------------------------ */
+
+HostModel::HostModel() {
+    static std::atomic<uint64_t> next{1};
+    uid_ = next.fetch_add(1);
+}
+
+HostModel HostModel::from_graph(const hlir::Graph& g) {
+    HostModel m;
+    for (const auto& [name, t] : g.initializers) {
+        m.weights_.emplace(name, t);
+        m.stamps_[name] = 0;
+    }
+    return m;
+}
+
+const Tensor& HostModel::tensor(const std::string& name) const {
+    auto it = weights_.find(name);
+    if (it == weights_.end()) throw Error(Error::Code::ShapeMismatch, "model has no weight " + name);
+    if (device_owner && device_newer.count(name)) {
+        device_owner->pull_weight(name, it->second);
+        device_newer.erase(name);
+    }
+    return it->second;
+}
+
+uint64_t HostModel::stamp(const std::string& name) const {
+    auto it = stamps_.find(name);
+    return it == stamps_.end() ? 0 : it->second;
+}
+
+void HostModel::set(const std::string& name, Tensor value) {
+    weights_[name] = std::move(value);
+    device_newer.erase(name);
+    ++stamps_[name];
+}
+
+void HostModel::bump(const std::string& name) { ++stamps_[name]; }
+
+std::vector<std::string> HostModel::names() const {
+    std::vector<std::string> out;
+    for (const auto& [k, v] : weights_) out.push_back(k);
+    return out;
+}
+
+/* ------------------------------------------------------------------ */
+/*  Device                                                             */
+/* ------------------------------------------------------------------ */
+
+Device::Device(int ordinal) { NNC_CHECK(nncb_create(ordinal, &ctx_)); }
+
+Device::~Device() {
+    programs_.clear();
+    for (auto& [name, cw] : cache_)
+        if (cw.ptr && !cw.external) nncb_free(ctx_, cw.ptr);
+    nncb_destroy(ctx_);
+}
+
+SyncStats Device::sync_stats(bool reset) {
+    SyncStats s = stats_;
+    if (reset) stats_ = {};
+    return s;
+}
+
+void Device::init_comm(int nranks, int rank, const uint8_t id[128]) {
+    NNC_CHECK(nncb_comm_init(ctx_, nranks, rank, id));
+    nranks_ = nranks;
+    rank_ = rank;
+}
+
+void* Device::weight_buffer(const std::string& name, const Tensor& host, uint64_t stamp) {
+    auto it = cache_.find(name);
+    size_t bytes = host.byte_size();
+    if (it == cache_.end()) {
+        CachedWeight cw;
+        cw.bytes = bytes;
+        NNC_CHECK(nncb_malloc(ctx_, std::max<size_t>(bytes, 4), &cw.ptr));
+        cw.stamp = stamp + 1;  // force upload below
+        it = cache_.emplace(name, cw).first;
+    }
+    CachedWeight& cw = it->second;
+    if (cw.bytes != bytes) throw Error(Error::Code::ShapeMismatch, name + ": stored weight does not match plan");
+    if (cw.stamp != stamp) {
+        NNC_CHECK(nncb_h2d(ctx_, cw.ptr, host.data(), bytes));
+        cw.stamp = stamp;
+        stats_.h2d_bytes += bytes;
+        stats_.weight_bytes += bytes;
+        ++stats_.weight_transfers[name];
+    }
+    return cw.ptr;
+}
+
+void* Device::weight_ptr(const std::string& name) const {
+    auto it = cache_.find(name);
+    return it == cache_.end() ? nullptr : it->second.ptr;
+}
+
+void Device::pull_weight(const std::string& name, Tensor& host) {
+    void* p = weight_ptr(name);
+    if (!p) return;
+    NNC_CHECK(nncb_d2h(ctx_, host.data(), p, host.byte_size()));
+    NNC_CHECK(nncb_sync(ctx_));
+    stats_.d2h_bytes += host.byte_size();
+}
+
+void Device::adopt_weight(const std::string& name, void* ptr, size_t bytes, uint64_t stamp) {
+    auto it = cache_.find(name);
+    if (it != cache_.end() && !it->second.external && it->second.ptr) nncb_free(ctx_, it->second.ptr);
+    cache_[name] = CachedWeight{ptr, bytes, stamp, true};
+}
+
+uint64_t Device::cached_stamp(const std::string& name) const {
+    auto it = cache_.find(name);
+    return it == cache_.end() ? ~0ull : it->second.stamp;
+}
+
+void Device::mark_device_newer(HostModel& m, const std::string& name, uint64_t new_stamp) {
+    auto it = cache_.find(name);
+    if (it != cache_.end()) it->second.stamp = new_stamp;
+    m.device_owner = this;
+    m.device_newer.insert(name);
+}
+
+Device& default_device() {
+    static std::unique_ptr<Device> dev;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!dev) {
+        const char* env = std::getenv("NNC_DEVICE");
+        dev = std::make_unique<Device>(env ? std::atoi(env) : 0);
+    }
+    return *dev;
+}
+
+/* ------------------------------------------------------------------ */
+/*  execute                                                            */
+/* ------------------------------------------------------------------ */
+
+namespace {
+
+struct ExecCache {
+    std::unique_ptr<Program> prog;
+    void* graph = nullptr;
+    std::map<std::string, void*> weight_ptrs;   // pointers baked into the graph
+    int runs = 0;
+    ~ExecCache() {
+        if (graph) nncb_graph_destroy(graph);
+    }
+};
+
+std::map<std::pair<const Device*, uint64_t>, std::unique_ptr<ExecCache>>& exec_caches() {
+    static std::map<std::pair<const Device*, uint64_t>, std::unique_ptr<ExecCache>> m;
+    return m;
+}
+
+void check_inputs(const ExecutionPlan& p, const std::map<std::string, Tensor>& inputs) {
+    for (uint32_t slot : p.input_slots) {
+        const auto& v = p.values[slot];
+        auto fed = inputs.find(v.name);
+        if (fed == inputs.end()) throw Error(Error::Code::ShapeMismatch, "missing input " + v.name);
+        if (fed->second.dims().size() != v.dims.size())
+            throw Error(Error::Code::ShapeMismatch, v.name + ": rank " + std::to_string(fed->second.dims().size()) +
+                                                        ", plan expects " + std::to_string(v.dims.size()));
+        if (fed->second.dims() != v.dims)
+            throw Error(Error::Code::ShapeMismatch,
+                        v.name + ": expected " + dims_to_string(v.dims) + ", got " + dims_to_string(fed->second.dims()));
+        if (fed->second.dtype() != p.dtype) throw Error(Error::Code::ShapeMismatch, v.name + ": dtype mismatch");
+    }
+}
+
+}  // namespace
+
+std::map<std::string, Tensor> execute(const ExecutionPlan& p, const std::map<std::string, Tensor>& inputs,
+                                      const HostModel& model, Device* device, const ExecOptions& opts) {
+    Device& dev = device ? *device : default_device();
+    check_inputs(p, inputs);
+    auto& slot = exec_caches()[{&dev, p.uid}];
+    // weights: stamp-checked device cache (uploads only stale tensors)
+    std::map<std::string, void*> wptrs;
+    for (const std::string& w : p.weight_names) wptrs[w] = dev.weight_buffer(w, model.tensor(w), model.stamp(w));
+    if (!slot || slot->weight_ptrs != wptrs || slot->prog->precision != opts.gemm_precision) {
+        slot = std::make_unique<ExecCache>();
+        slot->prog = std::make_unique<Program>();
+        slot->prog->dev = &dev;
+        slot->prog->plans = {&p};
+        slot->prog->precision = opts.gemm_precision;
+        slot->prog->bind([&](const std::string& w) { return wptrs.at(w); },
+                         [](const std::string&) -> void* { return nullptr; });
+        slot->weight_ptrs = wptrs;
+    }
+    Program& prog = *slot->prog;
+    nncb_ctx* ctx = dev.ctx();
+    for (uint32_t s : p.input_slots) {
+        const Tensor& t = inputs.at(p.values[s].name);
+        NNC_CHECK(nncb_h2d(ctx, prog.ptr(p.values[s].name), t.data(), t.byte_size()));
+        dev.stats().h2d_bytes += t.byte_size();
+    }
+    // first run eagerly (sizes scratch, compiles kernels); later runs replay a graph
+    if (!opts.use_graphs || slot->runs == 0) {
+        prog.enqueue_plan(0, opts.trace);
+    } else {
+        if (!slot->graph) {
+            NNC_CHECK(nncb_capture_begin(ctx));
+            prog.enqueue_plan(0, nullptr);
+            NNC_CHECK(nncb_capture_end(ctx, &slot->graph));
+        }
+        if (opts.trace)
+            for (const auto& es : p.exec_steps) opts.trace->push_back("exec:" + es.label);
+        NNC_CHECK(nncb_graph_launch(ctx, slot->graph));
+    }
+    ++slot->runs;
+    std::map<std::string, Tensor> out;
+    for (uint32_t s : p.output_slots) {
+        const auto& v = p.values[s];
+        if (opts.materialize && !opts.materialize->count(v.name)) continue;
+        Tensor t(p.dtype, v.dims);
+        NNC_CHECK(nncb_d2h(ctx, t.data(), prog.ptr(v.name), t.byte_size()));
+        dev.stats().d2h_bytes += t.byte_size();
+        out.emplace(v.name, std::move(t));
+    }
+    NNC_CHECK(nncb_sync(ctx));
+    return out;
+}
+
+/* ------------------------------------------------------------------ */
+/*  Loss and update (host-tensor API, run on the device)               */
+/* ------------------------------------------------------------------ */
+
+L1Result l1_loss(const Tensor& pred, const Tensor& target, Device* device) {
+    if (pred.dims() != target.dims() || pred.dtype() != target.dtype())
+        throw Error(Error::Code::ShapeMismatch, "l1_loss: operand shapes differ");
+    Device& dev = device ? *device : default_device();
+    nncb_ctx* ctx = dev.ctx();
+    size_t bytes = pred.byte_size();
+    void *p = nullptr, *t = nullptr, *g = nullptr, *loss = nullptr;
+    NNC_CHECK(nncb_malloc(ctx, std::max<size_t>(bytes, 16), &p));
+    NNC_CHECK(nncb_malloc(ctx, std::max<size_t>(bytes, 16), &t));
+    NNC_CHECK(nncb_malloc(ctx, std::max<size_t>(bytes, 16), &g));
+    NNC_CHECK(nncb_malloc(ctx, 16, &loss));
+    NNC_CHECK(nncb_h2d(ctx, p, pred.data(), bytes));
+    NNC_CHECK(nncb_h2d(ctx, t, target.data(), bytes));
+    NNC_CHECK(nncb_l1_loss(ctx, static_cast<float*>(p), static_cast<float*>(t), static_cast<float*>(g),
+                           static_cast<double*>(loss), pred.elements()));
+    L1Result r;
+    r.grad = Tensor(pred.dtype(), pred.dims());
+    NNC_CHECK(nncb_d2h(ctx, r.grad.data(), g, bytes));
+    NNC_CHECK(nncb_d2h(ctx, &r.loss, loss, sizeof(double)));
+    NNC_CHECK(nncb_sync(ctx));
+    for (void* b : {p, t, g, loss}) nncb_free(ctx, b);
+    return r;
+}
+
+void sgd_step(HostModel& model, const std::map<std::string, Tensor>& grads, double lr, Device* device) {
+    Device& dev = device ? *device : default_device();
+    nncb_ctx* ctx = dev.ctx();
+    for (const auto& [name, g] : grads) {
+        if (!model.has(name)) throw Error(Error::Code::MissingGrad, "gradient for unknown weight " + name);
+        Tensor w = model.tensor(name);
+        if (w.dims() != g.dims()) throw Error(Error::Code::ShapeMismatch, name + ": gradient shape mismatch");
+        size_t bytes = w.byte_size();
+        void *wd = nullptr, *gd = nullptr;
+        NNC_CHECK(nncb_malloc(ctx, std::max<size_t>(bytes, 16), &wd));
+        NNC_CHECK(nncb_malloc(ctx, std::max<size_t>(bytes, 16), &gd));
+        NNC_CHECK(nncb_h2d(ctx, wd, w.data(), bytes));
+        NNC_CHECK(nncb_h2d(ctx, gd, g.data(), bytes));
+        NNC_CHECK(nncb_sgd(ctx, static_cast<float*>(wd), static_cast<float*>(gd), w.elements(), lr, 1.0));
+        NNC_CHECK(nncb_d2h(ctx, w.data(), wd, bytes));
+        NNC_CHECK(nncb_sync(ctx));
+        nncb_free(ctx, wd);
+        nncb_free(ctx, gd);
+        model.set(name, std::move(w));
+    }
+}
+
+/* ------------------------------------------------------------------ */
+/*  Trainer: the fused training step                                   */
+/* ------------------------------------------------------------------ */
+
+struct Trainer::Impl {
+    const plan::VersionPlans* plans = nullptr;
+    HostModel* model = nullptr;
+    Device* dev = nullptr;
+    ExecOptions opts;
+    std::unique_ptr<Program> prog;
+    std::string pred, dpred;
+    std::vector<std::string> weights;                 // all parameters, region order
+    std::map<std::string, int64_t> w_off, w_elems;    // element offsets in the flat regions
+    int64_t region_elems = 0;
+    void *params = nullptr, *grads = nullptr, *target = nullptr, *loss = nullptr;
+    void* graph = nullptr;
+    void* graph_nosgd = nullptr;
+    double graph_lr = std::nan("");
+    std::vector<std::pair<int64_t, int64_t>> buckets;   // (offset, count) in reverse backward order
+    uint64_t launches_per_step = 0;
+    bool warmed = false;
+
+    ~Impl() {
+        if (graph) nncb_graph_destroy(graph);
+        if (graph_nosgd) nncb_graph_destroy(graph_nosgd);
+        nncb_ctx* ctx = dev->ctx();
+        for (void* p : {params, grads, target, loss})
+            if (p) nncb_free(ctx, p);
+    }
+
+    void enqueue_step(double lr, bool do_sgd) {
+        nncb_ctx* ctx = dev->ctx();
+        prog->enqueue_plan(0, nullptr);
+        int64_t n = element_count(plans->train_fwd.values[plans->train_fwd.find_value(pred)].dims);
+        NNC_CHECK(nncb_l1_loss(ctx, static_cast<float*>(prog->ptr(pred)), static_cast<float*>(target),
+                               static_cast<float*>(prog->ptr(dpred)), static_cast<double*>(loss), n));
+        prog->enqueue_plan(1, nullptr);
+        if (dev->nranks() > 1)
+            for (auto [off, cnt] : buckets) NNC_CHECK(nncb_allreduce_sum(ctx, static_cast<float*>(grads) + off, cnt));
+        if (do_sgd)
+            NNC_CHECK(nncb_sgd(ctx, static_cast<float*>(params), static_cast<float*>(grads), region_elems, lr,
+                               1.0 / static_cast<double>(dev->nranks())));
+    }
+
+    void sync_params() {
+        // host-side edits (HostModel::set) since the last step: re-upload in place
+        for (const std::string& w : weights)
+            if (!model->device_newer.count(w) && dev->cached_stamp(w) != model->stamp(w))
+                dev->weight_buffer(w, model->tensor(w), model->stamp(w));
+    }
+
+    void run(double lr, bool do_sgd) {
+        nncb_ctx* ctx = dev->ctx();
+        sync_params();
+        if (!opts.use_graphs || !warmed) {
+            uint64_t before = nncb_launch_count(ctx);
+            enqueue_step(lr, do_sgd);
+            NNC_CHECK(nncb_sync(ctx));
+            if (do_sgd) launches_per_step = nncb_launch_count(ctx) - before;
+            warmed = true;
+        } else {
+            void*& g = do_sgd ? graph : graph_nosgd;
+            if (do_sgd && g && graph_lr != lr) {
+                nncb_graph_destroy(g);
+                g = nullptr;
+            }
+            if (!g) {
+                NNC_CHECK(nncb_capture_begin(ctx));
+                enqueue_step(lr, do_sgd);
+                NNC_CHECK(nncb_capture_end(ctx, &g));
+                if (do_sgd) graph_lr = lr;
+            }
+            NNC_CHECK(nncb_graph_launch(ctx, g));
+        }
+        if (do_sgd)
+            for (const std::string& w : weights) {
+                model->bump(w);
+                dev->mark_device_newer(*model, w, model->stamp(w));
+            }
+    }
+};
+
+Trainer::Trainer(const plan::VersionPlans& plans, HostModel& model, Device& dev, const ExecOptions& opts)
+    : impl(std::make_unique<Impl>()) {
+    Impl& I = *impl;
+    I.plans = &plans;
+    I.model = &model;
+    I.dev = &dev;
+    I.opts = opts;
+    if (plans.inference.output_slots.size() != 1)
+        throw Error(Error::Code::BadDocument, "train_step expects exactly one prediction output");
+    I.pred = plans.inference.values[plans.inference.output_slots[0]].name;
+    I.dpred = "d." + I.pred;
+    nncb_ctx* ctx = dev.ctx();
+    // flat parameter / gradient regions: trainable weights in reverse order of
+    // gradient production (so all-reduce buckets close early in backward), then
+    // the remaining parameters.
+    std::vector<std::string> order;
+    std::map<std::string, std::string> grad_to_weight;
+    for (const auto& [w, gv] : plans.weight_grads) grad_to_weight[gv] = w;
+    const ExecutionPlan& bwd = plans.train_bwd;
+    for (const auto& es : bwd.exec_steps)
+        for (uint32_t li : es.launches)
+            for (size_t a = 0; a < bwd.groups[es.group].launches[li].args.size(); ++a) {
+                const auto& L = bwd.groups[es.group].launches[li];
+                if (!L.is_out[a]) continue;
+                auto it = grad_to_weight.find(bwd.values[L.args[a].slot].name);
+                if (it != grad_to_weight.end() && std::find(order.begin(), order.end(), it->second) == order.end())
+                    order.push_back(it->second);
+            }
+    for (const auto* p : {&plans.train_fwd, &plans.train_bwd})
+        for (const std::string& w : p->weight_names)
+            if (std::find(order.begin(), order.end(), w) == order.end()) order.push_back(w);
+    for (const std::string& w : order) {
+        const Tensor& t = model.tensor(w);
+        I.w_off[w] = I.region_elems;
+        I.w_elems[w] = t.elements();
+        I.region_elems += (t.elements() + 63) / 64 * 64;   // 256-byte aligned tensors
+        I.weights.push_back(w);
+    }
+    size_t region_bytes = static_cast<size_t>(std::max<int64_t>(I.region_elems, 64)) * 4;
+    NNC_CHECK(nncb_malloc(ctx, region_bytes, &I.params));
+    NNC_CHECK(nncb_malloc(ctx, region_bytes, &I.grads));
+    NNC_CHECK(nncb_memset(ctx, I.params, 0, region_bytes));
+    NNC_CHECK(nncb_memset(ctx, I.grads, 0, region_bytes));
+    for (const std::string& w : I.weights) {
+        const Tensor& t = model.tensor(w);
+        void* home = static_cast<float*>(I.params) + I.w_off[w];
+        NNC_CHECK(nncb_h2d(ctx, home, t.data(), t.byte_size()));
+        dev.stats().h2d_bytes += t.byte_size();
+        dev.stats().weight_bytes += t.byte_size();
+        dev.adopt_weight(w, home, t.byte_size(), model.stamp(w));
+    }
+    // buckets of ~32 MB over the trainable prefix of the region
+    int64_t trainable_end = 0;
+    for (const auto& [w, gv] : plans.weight_grads) trainable_end = std::max(trainable_end, I.w_off[w] + I.w_elems[w]);
+    const int64_t bucket = 8 << 20;   // elements (32 MB)
+    for (int64_t off = 0; off < trainable_end; off += bucket)
+        I.buckets.push_back({off, std::min(bucket, trainable_end - off)});
+    const int64_t pred_elems = element_count(plans.train_fwd.values[plans.train_fwd.find_value(I.pred)].dims);
+    NNC_CHECK(nncb_malloc(ctx, static_cast<size_t>(std::max<int64_t>(pred_elems, 4)) * 4, &I.target));
+    NNC_CHECK(nncb_malloc(ctx, 64, &I.loss));
+    I.prog = std::make_unique<Program>();
+    I.prog->dev = &dev;
+    I.prog->plans = {&plans.train_fwd, &plans.train_bwd};
+    I.prog->precision = opts.gemm_precision;
+    std::map<std::string, std::string> weight_of_grad = grad_to_weight;
+    I.prog->bind([&](const std::string& w) { return static_cast<void*>(static_cast<float*>(I.params) + I.w_off.at(w)); },
+                 [&](const std::string& v) -> void* {
+                     auto it = weight_of_grad.find(v);
+                     if (it == weight_of_grad.end()) return nullptr;
+                     return static_cast<float*>(I.grads) + I.w_off.at(it->second);
+                 });
+}
+
+Trainer::~Trainer() = default;
+
+void* Trainer::input_device_ptr(const std::string& name) { return impl->prog->ptr(name); }
+void* Trainer::target_device_ptr() { return impl->target; }
+size_t Trainer::arena_bytes() const { return static_cast<size_t>(impl->prog->arena_bytes); }
+uint64_t Trainer::launches_per_step() const { return impl->launches_per_step; }
+
+double Trainer::step(const std::map<std::string, Tensor>& inputs, const Tensor& target, double lr) {
+    Impl& I = *impl;
+    check_inputs(I.plans->train_fwd, inputs);
+    nncb_ctx* ctx = I.dev->ctx();
+    for (uint32_t s : I.plans->train_fwd.input_slots) {
+        const std::string& name = I.plans->train_fwd.values[s].name;
+        const Tensor& t = inputs.at(name);
+        NNC_CHECK(nncb_h2d(ctx, I.prog->ptr(name), t.data(), t.byte_size()));
+    }
+    NNC_CHECK(nncb_h2d(ctx, I.target, target.data(), target.byte_size()));
+    I.run(lr, true);
+    double loss = 0;
+    NNC_CHECK(nncb_d2h(ctx, &loss, I.loss, sizeof(double)));
+    NNC_CHECK(nncb_sync(ctx));
+    return loss;
+}
+
+void Trainer::step_device(double lr) { impl->run(lr, true); }
+
+double Trainer::last_loss() {
+    double loss = 0;
+    NNC_CHECK(nncb_d2h(impl->dev->ctx(), &loss, impl->loss, sizeof(double)));
+    NNC_CHECK(nncb_sync(impl->dev->ctx()));
+    return loss;
+}
+
+namespace {
+std::map<std::pair<uint64_t, uint64_t>, std::unique_ptr<Trainer>>& trainers() {
+    static std::map<std::pair<uint64_t, uint64_t>, std::unique_ptr<Trainer>> m;
+    return m;
+}
+Trainer& trainer_for(const plan::VersionPlans& plans, HostModel& model, Device& dev, const ExecOptions& opts) {
+    auto& t = trainers()[{plans.train_fwd.uid, model.uid()}];
+    if (!t || t->impl->dev != &dev) t = std::make_unique<Trainer>(plans, model, dev, opts);
+    return *t;
+}
+}  // namespace
+
+void release(const plan::VersionPlans& plans) {
+    for (auto it = exec_caches().begin(); it != exec_caches().end();) {
+        uint64_t u = it->first.second;
+        bool drop = u == plans.inference.uid || u == plans.train_fwd.uid || u == plans.train_bwd.uid;
+        it = drop ? exec_caches().erase(it) : std::next(it);
+    }
+    for (auto it = trainers().begin(); it != trainers().end();)
+        it = it->first.first == plans.train_fwd.uid ? trainers().erase(it) : std::next(it);
+}
+
+double train_step(const plan::VersionPlans& plans, const std::map<std::string, Tensor>& inputs, const Tensor& target,
+                  HostModel& model, double lr, Device* device, const ExecOptions& opts) {
+    Device& dev = device ? *device : default_device();
+    if (opts.trace)
+        for (const char* ph : {"forward", "loss", "backward", "update"}) opts.trace->push_back(ph);
+    return trainer_for(plans, model, dev, opts).step(inputs, target, lr);
+}
+
+std::map<std::string, Tensor> gradients(const plan::VersionPlans& plans, const std::map<std::string, Tensor>& inputs,
+                                        const Tensor& target, HostModel& model, double* loss, Device* device,
+                                        const ExecOptions& opts) {
+    Device& dev = device ? *device : default_device();
+    Trainer& tr = trainer_for(plans, model, dev, opts);
+    Trainer::Impl& I = *tr.impl;
+    check_inputs(plans.train_fwd, inputs);
+    nncb_ctx* ctx = dev.ctx();
+    for (uint32_t s : plans.train_fwd.input_slots) {
+        const std::string& name = plans.train_fwd.values[s].name;
+        const Tensor& t = inputs.at(name);
+        NNC_CHECK(nncb_h2d(ctx, I.prog->ptr(name), t.data(), t.byte_size()));
+    }
+    NNC_CHECK(nncb_h2d(ctx, I.target, target.data(), target.byte_size()));
+    I.run(0.0, false);
+    std::map<std::string, Tensor> out;
+    for (const auto& [w, gv] : plans.weight_grads) {
+        Tensor t(DType::F32, model.tensor(w).dims());
+        NNC_CHECK(nncb_d2h(ctx, t.data(), static_cast<float*>(I.grads) + I.w_off.at(w), t.byte_size()));
+        out.emplace(w, std::move(t));
+    }
+    if (loss) NNC_CHECK(nncb_d2h(ctx, loss, I.loss, sizeof(double)));
+    NNC_CHECK(nncb_sync(ctx));
+    return out;
+}
+
+}  // namespace nnc::runtime

@@ -1,0 +1,136 @@
+// nnc/plan.hpp -- lowering of a grouped graph into a B200 execution plan.
+//
+// Mirrors reference core/include/nnc/plan.hpp:24-182: the same value table
+// (names, MemCategory, StorageClass, resident flags), the same static
+// alloc/free event schedule and ExecStep structure (one step per member of a
+// GEMM group, one step per fused group), and compile_version_set. What differs
+// is the lowering of a group: the reference emits one CPU KernelStep per member
+// or a per-element register program (plan.cpp:296-353); here a fused group is
+// lowered to a short list of device launches -- generated elementwise kernels
+// (register programs compiled to sm_100a) plus reduction / pooling kernels --
+// and a GEMM member to one tensor-core launch.
+#pragma once
+
+#include <cstdint>
+#include <functional>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "nncb.h"
+#include "nnc/autodiff.hpp"
+#include "nnc/backends.hpp"
+#include "nnc/hlir.hpp"
+
+namespace nnc::plan {
+
+enum class MemCategory : uint8_t { Parameter = 0, Input = 1, Output = 2, Intermediate = 3, Saved = 4 };
+const char* category_name(MemCategory c);
+inline int64_t align_bytes(int64_t b, int64_t a) { return (b + a - 1) / a * a; }
+
+enum class StorageClass : uint8_t { Buffer = 0, FusedRegister = 1 };
+
+struct ValueEntry {
+    std::string name;
+    MemCategory category = MemCategory::Intermediate;
+    StorageClass storage = StorageClass::Buffer;
+    bool resident = false;
+    std::string source_weight;
+    std::vector<int64_t> dims;
+};
+
+enum class LaunchKind : uint8_t {
+    Ew, Gemm, MaxPool, MaxPoolGrad, AvgPool, AvgPoolGrad, SumRows, CumSum, BnStats,
+    BnGradReduce, LnFwd, LnBwd, LnDgamma,
+};
+const char* launch_kind_name(LaunchKind k);
+
+/// A kernel argument: value-table slot plus an element offset into it.
+struct Arg {
+    uint32_t slot = 0;
+    int64_t offset = 0;
+};
+
+struct Launch {
+    LaunchKind kind = LaunchKind::Ew;
+    std::string label;
+    std::vector<Arg> args;
+    std::vector<bool> is_out;      // per arg: written by the launch
+    // Ew: register program whose slot fields index `args`.
+    std::vector<nncb_ew_instr> ew;
+    int32_t ew_regs = 0;
+    uint32_t elem_slot = 0;        // value whose dims define the iteration space
+    // Gemm / pooling / reductions: the originating op and attributes.
+    hlir::OpKind op = hlir::OpKind::Identity;
+    hlir::Attrs attrs;
+    bool relu_epilogue = false;
+};
+
+struct GroupKernel {
+    uint32_t id = 0;
+    backends::BackendId backend = backends::BackendId::B200_FUSED;
+    std::string label;
+    std::vector<std::string> members;
+    std::vector<Launch> launches;
+};
+
+struct PlanEvent {
+    int32_t step = 0;
+    bool alloc = true;
+    uint32_t slot = 0;
+};
+
+/// One schedule step: a member of a GEMM group (kernel = member index) or a
+/// whole fused group (kernel = -1). Step s >= 1 is exec_steps[s-1].
+struct ExecStep {
+    uint32_t group = 0;
+    int32_t kernel = -1;
+    std::string label;
+    std::vector<uint32_t> launches;   // indices into groups[group].launches
+};
+
+enum class PlanRole : uint8_t { Inference = 0, TrainFwd = 1, TrainBwd = 2 };
+
+struct ExecutionPlan {
+    uint64_t uid = 0;   // process-unique id (runtime caches key on it, never on addresses)
+    DType dtype = DType::F32;
+    PlanRole role = PlanRole::Inference;
+    std::vector<ValueEntry> values;
+    std::vector<GroupKernel> groups;
+    std::vector<ExecStep> exec_steps;
+    std::vector<PlanEvent> events;
+    std::vector<uint32_t> input_slots;
+    std::vector<uint32_t> output_slots;
+    std::vector<std::string> weight_names;
+
+    int find_value(const std::string& name) const;
+    size_t launch_count() const;
+};
+
+ExecutionPlan compile_plan(const hlir::Graph& g, const std::vector<backends::FusionGroup>& groups,
+                           PlanRole role = PlanRole::Inference,
+                           const autodiff::VersionSet* versions = nullptr);
+
+struct VersionPlans {
+    ExecutionPlan inference;
+    ExecutionPlan train_fwd;
+    ExecutionPlan train_bwd;
+    std::vector<std::string> save_set;
+    std::vector<std::string> output_grads;
+    std::map<std::string, std::string> weight_grads;
+};
+
+VersionPlans compile_version_set(
+    const autodiff::VersionSet& versions,
+    const std::function<backends::BackendAssignment(const hlir::Graph&)>& assign);
+
+struct PeakEstimate {
+    int64_t inference_bytes = 0;
+    int64_t training_bytes = 0;
+};
+/// Static peak of the event schedule (reference schedule.cpp:157-204 semantics:
+/// training carries SaveSet + parameters across the fwd/bwd boundary).
+PeakEstimate estimate_peak(const VersionPlans& plans, int64_t alignment = 64);
+int64_t plan_peak(const ExecutionPlan& p, int64_t alignment = 64);
+
+}  // namespace nnc::plan

@@ -1,0 +1,160 @@
+// nnc/runtime.hpp -- the B200 executor behind the reference runtime API.
+//
+// Reference API kept (core/include/nnc/runtime.hpp):
+//   HostModel (:21-34), SyncStats (:40-45), ExecOptions (:81-87),
+//   execute (:126-130), l1_loss/sgd_step (:141-144), train_step (:149-152).
+// B200 design: a Device owns one nncb context (one GPU), a version-stamped device
+// weight cache with the OffloadDevice protocol (runtime.cpp:71-102), and one
+// BoundProgram per (plan, role): arena offsets from the static event schedule,
+// compiled kernels, and a CUDA graph replayed per call. Training keeps weights
+// device-authoritative: SGD runs on the device and HostModel tensors are
+// refreshed lazily (HostModel::tensor() pulls stale weights back).
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "nnc/plan.hpp"
+#include "nnc/tensor.hpp"
+
+struct nncb_ctx;
+
+namespace nnc::runtime {
+
+class Device;
+
+class HostModel {
+public:
+    HostModel();
+    uint64_t uid() const { return uid_; }
+    static HostModel from_graph(const hlir::Graph& g);
+    bool has(const std::string& name) const { return weights_.count(name) != 0; }
+    const Tensor& tensor(const std::string& name) const;   // pulls if device-newer
+    uint64_t stamp(const std::string& name) const;
+    void set(const std::string& name, Tensor value);      // bumps the stamp
+    void bump(const std::string& name);
+    std::vector<std::string> names() const;
+
+    // Device-authoritative bookkeeping (B200 training).
+    mutable Device* device_owner = nullptr;
+    mutable std::set<std::string> device_newer;
+
+private:
+    mutable std::map<std::string, Tensor> weights_;
+    std::map<std::string, uint64_t> stamps_;
+    uint64_t uid_ = 0;
+};
+
+struct SyncStats {
+    uint64_t h2d_bytes = 0;
+    uint64_t d2h_bytes = 0;
+    uint64_t weight_bytes = 0;
+    std::map<std::string, uint64_t> weight_transfers;
+};
+
+struct ExecOptions {
+    int64_t alignment = 64;
+    std::vector<std::string>* trace = nullptr;
+    const std::set<std::string>* materialize = nullptr;
+    bool use_graphs = true;           // capture each bound program into a CUDA graph
+    int gemm_precision = NNCB_PREC_TF32;
+};
+
+struct L1Result {
+    double loss = 0;
+    Tensor grad;
+};
+
+struct Program;   // a bound plan (internal)
+
+class Device {
+public:
+    explicit Device(int ordinal = 0);
+    ~Device();
+    Device(const Device&) = delete;
+    Device& operator=(const Device&) = delete;
+
+    nncb_ctx* ctx() const { return ctx_; }
+    SyncStats sync_stats(bool reset = false);
+
+    /// Data parallelism: one process per GPU, NCCL over NVLink/NVSwitch.
+    void init_comm(int nranks, int rank, const uint8_t id[128]);
+    int nranks() const { return nranks_; }
+    int rank() const { return rank_; }
+
+    // --- internals used by execute/train_step -------------------------
+    void* weight_buffer(const std::string& name, const Tensor& host, uint64_t stamp);
+    void* weight_ptr(const std::string& name) const;
+    void pull_weight(const std::string& name, Tensor& host);
+    void mark_device_newer(HostModel& m, const std::string& name, uint64_t new_stamp);
+    /// Makes `ptr` (a trainer's flat parameter region) the device home of a weight.
+    void adopt_weight(const std::string& name, void* ptr, size_t bytes, uint64_t stamp);
+    uint64_t cached_stamp(const std::string& name) const;
+    std::map<const void*, std::unique_ptr<Program>>& programs() { return programs_; }
+    SyncStats& stats() { return stats_; }
+
+private:
+    struct CachedWeight {
+        void* ptr = nullptr;
+        size_t bytes = 0;
+        uint64_t stamp = 0;
+        bool external = false;
+    };
+    nncb_ctx* ctx_ = nullptr;
+    std::map<std::string, CachedWeight> cache_;
+    std::map<const void*, std::unique_ptr<Program>> programs_;
+    SyncStats stats_;
+    int nranks_ = 1, rank_ = 0;
+};
+
+/// Process-wide default device (cuda:0 unless NNC_DEVICE is set).
+Device& default_device();
+
+std::map<std::string, Tensor> execute(const plan::ExecutionPlan& p,
+                                      const std::map<std::string, Tensor>& inputs,
+                                      const HostModel& model, Device* device = nullptr,
+                                      const ExecOptions& opts = {});
+
+L1Result l1_loss(const Tensor& pred, const Tensor& target, Device* device = nullptr);
+
+void sgd_step(HostModel& model, const std::map<std::string, Tensor>& grads, double lr,
+              Device* device = nullptr);
+
+double train_step(const plan::VersionPlans& plans, const std::map<std::string, Tensor>& inputs,
+                  const Tensor& target, HostModel& model, double lr, Device* device = nullptr,
+                  const ExecOptions& opts = {});
+
+/// Drops every device program / CUDA graph / trainer cached for these plans.
+void release(const plan::VersionPlans& plans);
+
+/// Forward + loss + backward without the update (for gradient parity tests).
+std::map<std::string, Tensor> gradients(const plan::VersionPlans& plans,
+                                        const std::map<std::string, Tensor>& inputs,
+                                        const Tensor& target, HostModel& model, double* loss,
+                                        Device* device = nullptr, const ExecOptions& opts = {});
+
+/// Device-resident training step for benchmarking: inputs/target already on the
+/// device (pointers), everything stays on the device; returns nothing (the loss
+/// is left in a device double readable with last_loss()).
+struct Trainer {
+    Trainer(const plan::VersionPlans& plans, HostModel& model, Device& device,
+            const ExecOptions& opts = {});
+    ~Trainer();
+    /// H2D of host inputs+target, one graph replay, D2H of the loss.
+    double step(const std::map<std::string, Tensor>& inputs, const Tensor& target, double lr);
+    /// Device-resident variant (no host copies): enqueue one step.
+    void step_device(double lr);
+    double last_loss();
+    void* input_device_ptr(const std::string& name);
+    void* target_device_ptr();
+    size_t arena_bytes() const;
+    uint64_t launches_per_step() const;
+    struct Impl;
+    std::unique_ptr<Impl> impl;
+};
+
+}  // namespace nnc::runtime

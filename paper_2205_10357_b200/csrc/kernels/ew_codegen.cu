@@ -1,0 +1,251 @@
+// ew_codegen.cu -- fused elementwise groups: register program -> sm_100a kernel.
+//
+// Replaces the reference's per-element interpreter run_ew<T> (runtime.cpp:280-306),
+// which walks the EwInstr program (plan.cpp:296-337) once per element on one CPU
+// core (0.081 GB/s on the C2 chain). Here the program is a
+// compile-time specialisation: each register becomes a local variable, the
+// program body is emitted straight-line, and NVRTC compiles it for sm_100a once
+// per distinct program (cached per context). Each thread streams 2 x float4 per
+// element-mode slot per iteration (128-bit coalesced loads/stores, grid-stride,
+// grid = multiple of the SM count), so the kernel is HBM-bound.
+//
+// Arithmetic is bitwise-identical to the reference: Add/Mul use __fadd_rn /
+// __fmul_rn (no FMA contraction), ReLU is x > 0 ? x : 0 (-0 and NaN -> +0,
+// kernels.hpp:47-50), ReluGrad masks on the forward input (kernels.hpp:52-55).
+#include <nvrtc.h>
+
+#include <cstring>
+#include <sstream>
+
+#include "driver_api.cuh"
+#include "nncb_internal.cuh"
+
+struct nncb_ew_kernel {
+    std::string source;
+    CUmodule module = nullptr;
+    CUfunction fn = nullptr;
+    int n_slots = 0;
+    bool uses_channels = false;
+};
+
+void nncb::ew_release(nncb_ew_kernel* k) {
+    if (!k) return;
+    if (k->module) nncb::drv::table().moduleUnload(k->module);
+    delete k;
+}
+
+namespace {
+
+constexpr int kMaxSlots = 48;
+
+const char* kPrelude = R"(
+typedef long long i64;
+struct EwArgs { float* p[48]; i64 n; i64 C; };
+__device__ __forceinline__ float relu_(float x) { return x > 0.f ? x : 0.f; }
+__device__ __forceinline__ float relu_grad_(float x, float g) { return x > 0.f ? g : 0.f; }
+__device__ __forceinline__ float bn_apply_(float x, float m, float s, float ga, float be) {
+  return __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(x, m), s), ga), be);
+}
+__device__ __forceinline__ float bn_infer_(float x, float m, float v, float ga, float be, double eps) {
+  float s = (float)(1.0 / sqrt((double)v + eps));
+  return bn_apply_(x, m, s, ga, be);
+}
+__device__ __forceinline__ float gelu_(float x) {
+  double xd = (double)x;
+  return (float)(0.5 * xd * (1.0 + erf(xd * 0.70710678118654752440)));
+}
+__device__ __forceinline__ float gelu_grad_(float x, float g) {
+  double xd = (double)x;
+  double cdf = 0.5 * (1.0 + erf(xd * 0.70710678118654752440));
+  double pdf = exp(-0.5 * xd * xd) * 0.39894228040143267794;
+  return (float)((double)g * (cdf + xd * pdf));
+}
+__device__ __forceinline__ float bn_grad_(float x, float g, float m, float s, float ga, float sg, float sgx,
+                                          float cnt) {
+  float xhat = __fmul_rn(__fsub_rn(x, m), s);
+  float t = __fadd_rn(sg, __fmul_rn(xhat, sgx));
+  float u = __fsub_rn(g, __fdiv_rn(t, cnt));
+  return __fmul_rn(__fmul_rn(ga, s), u);
+}
+)";
+
+std::string reg(int r) { return "r" + std::to_string(r); }
+
+// Emits the body for W lanes (W = 4: float4 path, W = 1: scalar tail).
+void emit_body(std::ostringstream& os, const nncb_ew_program& p, int W, bool uses_ch) {
+    os << "  float ";
+    for (int r = 0; r < p.n_regs; ++r) os << (r ? ", " : "") << reg(r) << "[" << W << "]";
+    os << ";\n";
+    if (uses_ch) {
+        os << "  int ch[" << W << "]; { i64 c0 = i % A.C; ch[0] = (int)c0;\n";
+        for (int j = 1; j < W; ++j) os << "    ch[" << j << "] = ch[" << j - 1 << "] + 1 == (int)A.C ? 0 : ch[" << j - 1 << "] + 1;\n";
+        os << "  }\n";
+    }
+    for (int k = 0; k < p.n_instr; ++k) {
+        const nncb_ew_instr& in = p.instr[k];
+        std::string d = reg(in.dst), a = reg(in.a), b = reg(in.b), c = reg(in.c), dd = reg(in.d), e = reg(in.e),
+                    f = reg(in.f), h = reg(in.h);
+        std::string ptr = "A.p[" + std::to_string(in.slot) + "]";
+        switch (in.op) {
+            case NNCB_EW_LOAD:
+                if (W == 4)
+                    os << "  { float4 t = __ldg(reinterpret_cast<const float4*>(" << ptr << " + i)); " << d
+                       << "[0]=t.x; " << d << "[1]=t.y; " << d << "[2]=t.z; " << d << "[3]=t.w; }\n";
+                else
+                    os << "  " << d << "[0] = __ldg(" << ptr << " + i);\n";
+                continue;
+            case NNCB_EW_LOAD_CH:
+                os << "  #pragma unroll\n  for (int j = 0; j < " << W << "; ++j) " << d << "[j] = __ldg(" << ptr
+                   << " + ch[j]);\n";
+                continue;
+            case NNCB_EW_STORE:
+                if (W == 4)
+                    os << "  *reinterpret_cast<float4*>(" << ptr << " + i) = make_float4(" << a << "[0], " << a
+                       << "[1], " << a << "[2], " << a << "[3]);\n";
+                else
+                    os << "  " << ptr << "[i] = " << a << "[0];\n";
+                continue;
+            default: break;
+        }
+        std::string expr;
+        switch (in.op) {
+            case NNCB_EW_RELU: expr = "relu_(" + a + "[j])"; break;
+            case NNCB_EW_RELU_GRAD: expr = "relu_grad_(" + a + "[j], " + b + "[j])"; break;
+            case NNCB_EW_ADD: expr = "__fadd_rn(" + a + "[j], " + b + "[j])"; break;
+            case NNCB_EW_MUL: expr = "__fmul_rn(" + a + "[j], " + b + "[j])"; break;
+            case NNCB_EW_COPY: expr = a + "[j]"; break;
+            case NNCB_EW_GELU: expr = "gelu_(" + a + "[j])"; break;
+            case NNCB_EW_GELU_GRAD: expr = "gelu_grad_(" + a + "[j], " + b + "[j])"; break;
+            case NNCB_EW_BN_APPLY:
+                expr = "bn_apply_(" + a + "[j], " + b + "[j], " + c + "[j], " + dd + "[j], " + e + "[j])";
+                break;
+            case NNCB_EW_BN_INFER: {
+                std::ostringstream eps;
+                eps.precision(17);
+                eps << in.imm;
+                expr = "bn_infer_(" + a + "[j], " + b + "[j], " + c + "[j], " + dd + "[j], " + e + "[j], " +
+                       eps.str() + ")";
+                break;
+            }
+            case NNCB_EW_BN_GRAD: {
+                std::ostringstream cnt;
+                cnt.precision(17);
+                cnt << static_cast<float>(in.imm) << "f";
+                expr = "bn_grad_(" + a + "[j], " + b + "[j], " + c + "[j], " + dd + "[j], " + e + "[j], " + f +
+                       "[j], " + h + "[j], " + cnt.str() + ")";
+                break;
+            }
+            default: expr = "0.f /* unknown op */"; break;
+        }
+        os << "  #pragma unroll\n  for (int j = 0; j < " << W << "; ++j) " << d << "[j] = " << expr << ";\n";
+    }
+}
+
+std::string generate(const nncb_ew_program& p, bool uses_ch) {
+    std::ostringstream os;
+    os << kPrelude;
+    os << "__device__ __forceinline__ void body4(const EwArgs& A, i64 i) {\n";
+    emit_body(os, p, 4, uses_ch);
+    os << "}\n__device__ __forceinline__ void body1(const EwArgs& A, i64 i) {\n";
+    emit_body(os, p, 1, uses_ch);
+    os << "}\n";
+    os << R"(extern "C" __global__ void __launch_bounds__(256) nnc_fused_ew(const EwArgs A) {
+  const i64 nvec = A.n >> 2;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; v + stride < nvec; v += 2 * stride) { body4(A, v << 2); body4(A, (v + stride) << 2); }
+  if (v < nvec) body4(A, v << 2);
+  for (i64 i = (nvec << 2) + (i64)blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += stride) body1(A, i);
+}
+)";
+    return os.str();
+}
+
+int nvrtc_fail(nvrtcProgram prog, nvrtcResult r, const std::string& src) {
+    std::string log;
+    size_t n = 0;
+    if (prog && nvrtcGetProgramLogSize(prog, &n) == NVRTC_SUCCESS && n > 1) {
+        log.resize(n);
+        nvrtcGetProgramLog(prog, log.data());
+    }
+    if (prog) nvrtcDestroyProgram(&prog);
+    return nncb::fail(std::string("NVRTC: ") + nvrtcGetErrorString(r) + "\n" + log + "\n--- source ---\n" + src);
+}
+
+}  // namespace
+
+extern "C" {
+
+int nncb_ew_compile(nncb_ctx* ctx, const nncb_ew_program* p, nncb_ew_kernel** out) {
+    if (p->n_slots > kMaxSlots) return nncb::fail("nncb_ew_compile: too many slots");
+    bool uses_ch = false;
+    for (int k = 0; k < p->n_instr; ++k) uses_ch = uses_ch || p->instr[k].op == NNCB_EW_LOAD_CH;
+    std::string src = generate(*p, uses_ch);
+    auto hit = ctx->ew_cache.find(src);
+    if (hit != ctx->ew_cache.end()) {
+        *out = hit->second;
+        return 0;
+    }
+    NNCB_CUDA(cudaSetDevice(ctx->device));
+    NNCB_CUDA(cudaFree(nullptr));  // make the primary context current for the driver API
+    nvrtcProgram prog = nullptr;
+    nvrtcResult r = nvrtcCreateProgram(&prog, src.c_str(), "nnc_fused_ew.cu", 0, nullptr, nullptr);
+    if (r != NVRTC_SUCCESS) return nvrtc_fail(prog, r, src);
+    const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "--fmad=false"};
+    r = nvrtcCompileProgram(prog, 4, opts);
+    if (r != NVRTC_SUCCESS) return nvrtc_fail(prog, r, src);
+    size_t cubin_size = 0;
+    r = nvrtcGetCUBINSize(prog, &cubin_size);
+    if (r != NVRTC_SUCCESS) return nvrtc_fail(prog, r, src);
+    std::vector<char> cubin(cubin_size);
+    r = nvrtcGetCUBIN(prog, cubin.data());
+    if (r != NVRTC_SUCCESS) return nvrtc_fail(prog, r, src);
+    nvrtcDestroyProgram(&prog);
+    auto* k = new nncb_ew_kernel;
+    k->source = src;
+    k->n_slots = p->n_slots;
+    k->uses_channels = uses_ch;
+    const auto& D = nncb::drv::table();
+    if (!D.ok) {
+        nncb::ew_release(k);
+        return nncb::fail("CUDA driver entry points unavailable");
+    }
+    CUresult cr = D.moduleLoadData(&k->module, cubin.data());
+    if (cr == CUDA_SUCCESS) cr = D.moduleGetFunction(&k->fn, k->module, "nnc_fused_ew");
+    if (cr != CUDA_SUCCESS) {
+        nncb::ew_release(k);
+        return nncb::fail(std::string("cuModuleLoadData: ") + nncb::drv::error_string(cr));
+    }
+    ctx->ew_cache[src] = k;
+    *out = k;
+    return 0;
+}
+
+int nncb_ew_launch(nncb_ctx* ctx, nncb_ew_kernel* k, void* const* slots, int64_t n, int64_t channels) {
+    if (n <= 0) return 0;
+    struct {
+        float* p[kMaxSlots];
+        long long n;
+        long long C;
+    } args{};
+    for (int s = 0; s < k->n_slots; ++s) {
+        args.p[s] = static_cast<float*>(slots[s]);
+        if (reinterpret_cast<uintptr_t>(slots[s]) == 0) return nncb::fail("nncb_ew_launch: null slot");
+    }
+    args.n = n;
+    args.C = channels > 0 ? channels : 1;
+    if (k->uses_channels && channels <= 0) return nncb::fail("nncb_ew_launch: per-channel program needs C");
+    int64_t nvec = (n + 3) / 4;
+    unsigned grid = nncb::grid_for(ctx, (nvec + 1) / 2, 256, 8);
+    void* params[] = {&args};
+    CUresult r = nncb::drv::table().launchKernel(k->fn, grid, 1, 1, 256, 1, 1, 0,
+                                                 reinterpret_cast<CUstream>(ctx->stream), params, nullptr);
+    if (r != CUDA_SUCCESS)
+        return nncb::fail(std::string("cuLaunchKernel(fused ew): ") + nncb::drv::error_string(r));
+    ctx->launches.fetch_add(1, std::memory_order_relaxed);
+    return 0;
+}
+
+const char* nncb_ew_source(nncb_ew_kernel* k) { return k ? k->source.c_str() : ""; }
+
+}  // extern "C"

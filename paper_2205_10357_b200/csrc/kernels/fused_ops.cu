@@ -1,0 +1,525 @@
+// fused_ops.cu -- the non-GEMM members of fused groups: pooling, reductions,
+// BatchNorm / LayerNorm statistics, L1 loss and the SGD update.
+//
+// Bit-exactness notes (vs the reference CPU kernels):
+//  * maxpool fwd: strict '>' scan in window order, first max wins, index stored
+//    as float (kernels.hpp:258-284) -> bit-exact.
+//  * maxpool bwd / avgpool bwd are written as GATHERS (no atomics): each input
+//    element sums its contributions in increasing (oh, ow) order starting from
+//    +0, exactly the order the reference's scatter-add loop (kernels.hpp:286-344)
+//    applies them -> bit-exact.
+//  * avgpool fwd accumulates the window in (h, w) order then multiplies by
+//    T(1)/T(count) (kernels.hpp:304-322) -> bit-exact.
+//  * cumsum is sequential along the axis per line (kernels.hpp:76-111) -> bit-exact.
+//  * column sums (SumCols/SumNHW), BN/LN statistics accumulate in double with a
+//    fixed (deterministic) two-level order: more accurate than the reference's
+//    float running sum; compared against the oracle with a tolerance.
+//  * L1 gradient and SGD are computed in double per element and cast, exactly
+//    like runtime.cpp:468-496 -> bit-exact; the loss is a double tree sum.
+#include "nncb_internal.cuh"
+
+namespace {
+
+__global__ void maxpool_fwd_k(const float* __restrict__ x, float* __restrict__ y, float* __restrict__ idx,
+                              nncb_pool_geom g) {
+    int64_t total = g.n * g.oh * g.ow * g.c;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t c = t % g.c;
+        int64_t r = t / g.c;
+        int64_t ow = r % g.ow;
+        r /= g.ow;
+        int64_t oh = r % g.oh;
+        int64_t n = r / g.oh;
+        float best = 0.f;
+        int best_i = -1;
+        for (int64_t dh = 0; dh < g.kh; ++dh)
+            for (int64_t dw = 0; dw < g.kw; ++dw) {
+                int64_t h = oh * g.sh + dh, w = ow * g.sw + dw;
+                float v = __ldg(x + ((n * g.ih + h) * g.iw + w) * g.c + c);
+                if (best_i < 0 || v > best) {
+                    best = v;
+                    best_i = static_cast<int>(dh * g.kw + dw);
+                }
+            }
+        y[t] = best;
+        if (idx) idx[t] = static_cast<float>(best_i);
+    }
+}
+
+__global__ void maxpool_bwd_k(const float* __restrict__ idx, const float* __restrict__ gy, float* __restrict__ gx,
+                              nncb_pool_geom g) {
+    int64_t total = g.n * g.ih * g.iw * g.c;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t c = t % g.c;
+        int64_t r = t / g.c;
+        int64_t w = r % g.iw;
+        r /= g.iw;
+        int64_t h = r % g.ih;
+        int64_t n = r / g.ih;
+        int64_t oh0 = h - g.kh + 1 > 0 ? (h - g.kh + 1 + g.sh - 1) / g.sh : 0;
+        int64_t oh1 = h / g.sh < g.oh - 1 ? h / g.sh : g.oh - 1;
+        int64_t ow0 = w - g.kw + 1 > 0 ? (w - g.kw + 1 + g.sw - 1) / g.sw : 0;
+        int64_t ow1 = w / g.sw < g.ow - 1 ? w / g.sw : g.ow - 1;
+        float acc = 0.f;
+        for (int64_t oh = oh0; oh <= oh1; ++oh)
+            for (int64_t ow = ow0; ow <= ow1; ++ow) {
+                int64_t at = ((n * g.oh + oh) * g.ow + ow) * g.c + c;
+                int64_t wi = static_cast<int64_t>(__ldg(idx + at));
+                if (oh * g.sh + wi / g.kw == h && ow * g.sw + wi % g.kw == w) acc = __fadd_rn(acc, __ldg(gy + at));
+            }
+        gx[t] = acc;
+    }
+}
+
+__device__ __forceinline__ int64_t a_start(int64_t o, int64_t in, int64_t out) { return (o * in) / out; }
+__device__ __forceinline__ int64_t a_end(int64_t o, int64_t in, int64_t out) { return ((o + 1) * in + out - 1) / out; }
+
+__global__ void avgpool_fwd_k(const float* __restrict__ x, float* __restrict__ y, int64_t n, int64_t ih, int64_t iw,
+                              int64_t c, int64_t oh, int64_t ow) {
+    int64_t total = n * oh * ow * c;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t ch = t % c;
+        int64_t r = t / c;
+        int64_t p = r % ow;
+        r /= ow;
+        int64_t o = r % oh;
+        int64_t b = r / oh;
+        int64_t h0 = a_start(o, ih, oh), h1 = a_end(o, ih, oh), w0 = a_start(p, iw, ow), w1 = a_end(p, iw, ow);
+        float scale = __fdiv_rn(1.f, static_cast<float>((h1 - h0) * (w1 - w0)));
+        float acc = 0.f;
+        for (int64_t h = h0; h < h1; ++h)
+            for (int64_t w = w0; w < w1; ++w) acc = __fadd_rn(acc, __ldg(x + ((b * ih + h) * iw + w) * c + ch));
+        y[t] = __fmul_rn(acc, scale);
+    }
+}
+
+__global__ void avgpool_bwd_k(const float* __restrict__ gy, float* __restrict__ gx, int64_t n, int64_t ih, int64_t iw,
+                              int64_t c, int64_t oh, int64_t ow) {
+    int64_t total = n * ih * iw * c;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t ch = t % c;
+        int64_t r = t / c;
+        int64_t w = r % iw;
+        r /= iw;
+        int64_t h = r % ih;
+        int64_t b = r / ih;
+        float acc = 0.f;
+        for (int64_t o = 0; o < oh; ++o) {
+            int64_t h0 = a_start(o, ih, oh), h1 = a_end(o, ih, oh);
+            if (h < h0 || h >= h1) continue;
+            for (int64_t p = 0; p < ow; ++p) {
+                int64_t w0 = a_start(p, iw, ow), w1 = a_end(p, iw, ow);
+                if (w < w0 || w >= w1) continue;
+                float scale = __fdiv_rn(1.f, static_cast<float>((h1 - h0) * (w1 - w0)));
+                acc = __fadd_rn(acc, __fmul_rn(__ldg(gy + ((b * oh + o) * ow + p) * c + ch), scale));
+            }
+        }
+        gx[t] = acc;
+    }
+}
+
+// Column reductions over x[rows, C]: block (32 x 8) handles a 32-column tile
+// and a chunk of rows; partial sums (double) go to part[chunk][C] and a second
+// pass folds the chunks in order.
+template <int MODE>
+__global__ void col_partial_k(const float* __restrict__ x, const float* __restrict__ g, const float* __restrict__ stats,
+                              double* __restrict__ part, int64_t rows, int64_t C, int64_t rows_per_chunk) {
+    int64_t col = blockIdx.x * 32 + threadIdx.x;
+    int64_t chunk = blockIdx.y;
+    int64_t r0 = chunk * rows_per_chunk, r1 = min(rows, r0 + rows_per_chunk);
+    double s0 = 0, s1 = 0;
+    if (col < C) {
+        float mean = 0.f, invstd = 0.f;
+        if (MODE == 2) {
+            mean = stats[col];
+            invstd = stats[C + col];
+        }
+        for (int64_t r = r0 + threadIdx.y; r < r1; r += blockDim.y) {
+            float v = __ldg(x + r * C + col);
+            if (MODE == 0) {
+                s0 += v;
+            } else if (MODE == 1) {
+                s0 += v;
+                s1 += (double)v * (double)v;
+            } else {
+                float gv = __ldg(g + r * C + col);
+                double xhat = ((double)v - (double)mean) * (double)invstd;
+                s0 += gv;
+                s1 += (double)gv * xhat;
+            }
+        }
+    }
+    __shared__ double sh0[8][33], sh1[8][33];
+    sh0[threadIdx.y][threadIdx.x] = s0;
+    sh1[threadIdx.y][threadIdx.x] = s1;
+    __syncthreads();
+    if (threadIdx.y == 0 && col < C) {
+        for (int k = 1; k < (int)blockDim.y; ++k) {
+            s0 += sh0[k][threadIdx.x];
+            s1 += sh1[k][threadIdx.x];
+        }
+        part[(chunk * 2 + 0) * C + col] = s0;
+        part[(chunk * 2 + 1) * C + col] = s1;
+    }
+}
+
+template <int MODE>
+__global__ void col_final_k(const double* __restrict__ part, int64_t chunks, int64_t C, int64_t rows, double eps,
+                            float* __restrict__ out0, float* __restrict__ out1) {
+    int64_t col = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (col >= C) return;
+    double s0 = 0, s1 = 0;
+    for (int64_t k = 0; k < chunks; ++k) {
+        s0 += part[(k * 2 + 0) * C + col];
+        s1 += part[(k * 2 + 1) * C + col];
+    }
+    if (MODE == 0) {
+        out0[col] = (float)s0;
+    } else if (MODE == 1) {  // BN statistics: mean, 1/sqrt(var + eps), biased variance
+        double mean = s0 / (double)rows;
+        double var = s1 / (double)rows - mean * mean;
+        if (var < 0) var = 0;
+        out0[col] = (float)mean;
+        out0[C + col] = (float)(1.0 / sqrt(var + eps));
+    } else {
+        out0[col] = (float)s0;
+        out1[col] = (float)s1;
+    }
+}
+
+template <int MODE>
+int col_reduce(nncb_ctx* ctx, const float* x, const float* g, const float* stats, int64_t rows, int64_t C, double eps,
+               float* out0, float* out1) {
+    if (C <= 0) return 0;
+    int64_t col_tiles = (C + 31) / 32;
+    // enough chunks to fill ~4 waves of 148 SMs, at least 256 rows per chunk
+    int64_t target = (int64_t)ctx->sm_count * 8;
+    int64_t chunks = target / col_tiles;
+    if (chunks < 1) chunks = 1;
+    int64_t max_chunks = (rows + 255) / 256;
+    if (chunks > max_chunks) chunks = max_chunks;
+    if (chunks > 65535) chunks = 65535;
+    if (chunks < 1) chunks = 1;
+    int64_t rpc = (rows + chunks - 1) / chunks;
+    double* part = static_cast<double*>(nncb::scratch(ctx, sizeof(double) * 2 * chunks * C));
+    if (!part) return nncb::fail("col_reduce: scratch allocation failed");
+    dim3 grid((unsigned)col_tiles, (unsigned)chunks);
+    col_partial_k<MODE><<<grid, dim3(32, 8), 0, ctx->stream>>>(x, g, stats, part, rows, C, rpc);
+    NNCB_LAUNCHED(ctx);
+    col_final_k<MODE><<<(unsigned)((C + 127) / 128), 128, 0, ctx->stream>>>(part, chunks, C, rows, eps, out0, out1);
+    NNCB_LAUNCHED(ctx);
+    return 0;
+}
+
+__global__ void sum_rows_exact_k(const float* __restrict__ x, float* __restrict__ out, int64_t rows, int64_t C) {
+    int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= C) return;
+    float acc = 0.f;
+    for (int64_t r = 0; r < rows; ++r) acc = __fadd_rn(acc, __ldg(x + r * C + c));
+    out[c] = acc;
+}
+
+__global__ void cumsum_k(const float* __restrict__ x, float* __restrict__ y, int64_t outer, int64_t len, int64_t inner,
+                         int exclusive, int reverse) {
+    int64_t lines = outer * inner;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < lines; t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t o = t / inner, in = t % inner;
+        const float* xs = x + o * len * inner + in;
+        float* ys = y + o * len * inner + in;
+        float acc = 0.f;
+        for (int64_t k = 0; k < len; ++k) {
+            int64_t i = reverse ? len - 1 - k : k;
+            if (exclusive) {
+                ys[i * inner] = acc;
+                acc = __fadd_rn(acc, xs[i * inner]);
+            } else {
+                acc = __fadd_rn(acc, xs[i * inner]);
+                ys[i * inner] = acc;
+            }
+        }
+    }
+}
+
+// LayerNorm: one CTA (256 threads) per row; row statistics in double.
+template <int MODE>  // 0: forward, 1: backward dx, 2: row stats only
+__global__ void __launch_bounds__(256) layernorm_k(const float* __restrict__ x, const float* __restrict__ gamma,
+                                                   const float* __restrict__ beta, const float* __restrict__ gy,
+                                                   float* __restrict__ out, float* __restrict__ row_stats, int64_t C,
+                                                   double eps) {
+    int64_t row = blockIdx.x;
+    const float* xr = x + row * C;
+    __shared__ double red[2][8];
+    double s0 = 0, s1 = 0;
+    for (int64_t c = threadIdx.x; c < C; c += 256) {
+        double v = xr[c];
+        s0 += v;
+        s1 += v * v;
+    }
+    for (int o = 16; o; o >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    }
+    int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (lane == 0) {
+        red[0][warp] = s0;
+        red[1][warp] = s1;
+    }
+    __syncthreads();
+    s0 = 0;
+    s1 = 0;
+    for (int k = 0; k < 8; ++k) {
+        s0 += red[0][k];
+        s1 += red[1][k];
+    }
+    double mean_d = s0 / (double)C;
+    double var = s1 / (double)C - mean_d * mean_d;
+    if (var < 0) var = 0;
+    float mean = (float)mean_d;
+    float rstd = (float)(1.0 / sqrt(var + eps));
+    if (MODE == 2) {
+        if (threadIdx.x == 0) {
+            row_stats[row * 2] = mean;
+            row_stats[row * 2 + 1] = rstd;
+        }
+        return;
+    }
+    if (MODE == 0) {
+        for (int64_t c = threadIdx.x; c < C; c += 256) {
+            float xhat = __fmul_rn(__fsub_rn(xr[c], mean), rstd);
+            out[row * C + c] = __fadd_rn(__fmul_rn(xhat, gamma[c]), beta[c]);
+        }
+        return;
+    }
+    // backward: gg = g*gamma; s1' = sum gg, s2' = sum gg*xhat
+    const float* gr = gy + row * C;
+    __syncthreads();
+    double t0 = 0, t1 = 0;
+    for (int64_t c = threadIdx.x; c < C; c += 256) {
+        float xhat = __fmul_rn(__fsub_rn(xr[c], mean), rstd);
+        float gg = __fmul_rn(gr[c], gamma[c]);
+        t0 += gg;
+        t1 += (double)gg * (double)xhat;
+    }
+    for (int o = 16; o; o >>= 1) {
+        t0 += __shfl_xor_sync(0xffffffffu, t0, o);
+        t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+    }
+    if (lane == 0) {
+        red[0][warp] = t0;
+        red[1][warp] = t1;
+    }
+    __syncthreads();
+    t0 = 0;
+    t1 = 0;
+    for (int k = 0; k < 8; ++k) {
+        t0 += red[0][k];
+        t1 += red[1][k];
+    }
+    float sg = (float)t0, sgx = (float)t1, cnt = (float)C;
+    for (int64_t c = threadIdx.x; c < C; c += 256) {
+        float xhat = __fmul_rn(__fsub_rn(xr[c], mean), rstd);
+        float gg = __fmul_rn(gr[c], gamma[c]);
+        float t = __fadd_rn(sg, __fmul_rn(xhat, sgx));
+        float u = __fsub_rn(gg, __fdiv_rn(t, cnt));
+        out[row * C + c] = __fmul_rn(rstd, u);
+    }
+}
+
+__global__ void ln_dgamma_partial_k(const float* __restrict__ x, const float* __restrict__ g,
+                                    const float* __restrict__ rs, double* __restrict__ part, int64_t rows, int64_t C,
+                                    int64_t rpc) {
+    int64_t col = blockIdx.x * 32 + threadIdx.x;
+    int64_t chunk = blockIdx.y;
+    int64_t r0 = chunk * rpc, r1 = min(rows, r0 + rpc);
+    double s = 0;
+    if (col < C)
+        for (int64_t r = r0 + threadIdx.y; r < r1; r += blockDim.y) {
+            float xhat = __fmul_rn(__fsub_rn(x[r * C + col], rs[r * 2]), rs[r * 2 + 1]);
+            s += (double)g[r * C + col] * (double)xhat;
+        }
+    __shared__ double sh[8][33];
+    sh[threadIdx.y][threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.y == 0 && col < C) {
+        for (int k = 1; k < (int)blockDim.y; ++k) s += sh[k][threadIdx.x];
+        part[(chunk * 2) * C + col] = s;
+        part[(chunk * 2 + 1) * C + col] = 0;
+    }
+}
+
+__global__ void l1_k(const float* __restrict__ p, const float* __restrict__ t, float* __restrict__ grad,
+                     double* __restrict__ partial, int64_t n) {
+    double inv = n > 0 ? 1.0 / (double)n : 0.0;
+    double acc = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double d = __dsub_rn((double)p[i], (double)t[i]);
+        acc = __dadd_rn(acc, fabs(d));
+        grad[i] = (float)(d > 0 ? inv : (d < 0 ? -inv : 0.0));
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    __shared__ double red[32];
+    if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0;
+        for (int k = 0; k < (int)(blockDim.x / 32); ++k) s += red[k];
+        partial[blockIdx.x] = s;
+    }
+}
+
+__global__ void l1_final_k(const double* __restrict__ partial, int blocks, int64_t n, double* __restrict__ loss) {
+    if (threadIdx.x != 0) return;
+    double s = 0;
+    for (int k = 0; k < blocks; ++k) s += partial[k];
+    *loss = s * (n > 0 ? 1.0 / (double)n : 0.0);
+}
+
+// (float)((double)w - lr*(double)g) with separately rounded double ops, exactly
+// runtime.cpp:493 (no FMA contraction).
+__device__ __forceinline__ float sgd1(float w, float g, double lr, double scale) {
+    return (float)__dsub_rn((double)w, __dmul_rn(lr, __dmul_rn((double)g, scale)));
+}
+
+__global__ void sgd_k(float* __restrict__ w, const float* __restrict__ g, int64_t n, double lr, double scale) {
+    int64_t nv = n >> 2;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
+        float4 wv = reinterpret_cast<float4*>(w)[v];
+        float4 gv = __ldg(reinterpret_cast<const float4*>(g) + v);
+        wv.x = sgd1(wv.x, gv.x, lr, scale);
+        wv.y = sgd1(wv.y, gv.y, lr, scale);
+        wv.z = sgd1(wv.z, gv.z, lr, scale);
+        wv.w = sgd1(wv.w, gv.w, lr, scale);
+        reinterpret_cast<float4*>(w)[v] = wv;
+    }
+    for (int64_t i = (nv << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        w[i] = sgd1(w[i], g[i], lr, scale);
+}
+
+}  // namespace
+
+extern "C" {
+
+int nncb_maxpool_fwd(nncb_ctx* ctx, const nncb_pool_geom* g, const float* x, float* y, float* idx) {
+    int64_t total = g->n * g->oh * g->ow * g->c;
+    if (total == 0) return 0;
+    maxpool_fwd_k<<<nncb::grid_for(ctx, total, 256), 256, 0, ctx->stream>>>(x, y, idx, *g);
+    NNCB_LAUNCHED(ctx);
+    return 0;
+}
+
+int nncb_maxpool_bwd(nncb_ctx* ctx, const nncb_pool_geom* g, const float* idx, const float* gy, float* gx) {
+    int64_t total = g->n * g->ih * g->iw * g->c;
+    if (total == 0) return 0;
+    maxpool_bwd_k<<<nncb::grid_for(ctx, total, 256), 256, 0, ctx->stream>>>(idx, gy, gx, *g);
+    NNCB_LAUNCHED(ctx);
+    return 0;
+}
+
+int nncb_avgpool_fwd(nncb_ctx* ctx, int64_t n, int64_t ih, int64_t iw, int64_t c, int64_t oh, int64_t ow,
+                     const float* x, float* y) {
+    int64_t total = n * oh * ow * c;
+    if (total == 0) return 0;
+    avgpool_fwd_k<<<nncb::grid_for(ctx, total, 256), 256, 0, ctx->stream>>>(x, y, n, ih, iw, c, oh, ow);
+    NNCB_LAUNCHED(ctx);
+    return 0;
+}
+
+int nncb_avgpool_bwd(nncb_ctx* ctx, int64_t n, int64_t ih, int64_t iw, int64_t c, int64_t oh, int64_t ow,
+                     const float* gy, float* gx) {
+    int64_t total = n * ih * iw * c;
+    if (total == 0) return 0;
+    avgpool_bwd_k<<<nncb::grid_for(ctx, total, 256), 256, 0, ctx->stream>>>(gy, gx, n, ih, iw, c, oh, ow);
+    NNCB_LAUNCHED(ctx);
+    return 0;
+}
+
+int nncb_sum_rows(nncb_ctx* ctx, const float* x, float* out, int64_t rows, int64_t cols, int exact) {
+    if (!exact) return col_reduce<0>(ctx, x, nullptr, nullptr, rows, cols, 0.0, out, nullptr);
+    if (cols == 0) return 0;
+    sum_rows_exact_k<<<(unsigned)((cols + 127) / 128), 128, 0, ctx->stream>>>(x, out, rows, cols);
+    NNCB_LAUNCHED(ctx);
+    return 0;
+}
+
+int nncb_cumsum(nncb_ctx* ctx, const float* x, float* y, int64_t outer, int64_t len, int64_t inner, int exclusive,
+                int reverse) {
+    int64_t lines = outer * inner;
+    if (lines == 0 || len == 0) return 0;
+    cumsum_k<<<nncb::grid_for(ctx, lines, 128), 128, 0, ctx->stream>>>(x, y, outer, len, inner, exclusive, reverse);
+    NNCB_LAUNCHED(ctx);
+    return 0;
+}
+
+int nncb_bn_stats(nncb_ctx* ctx, const float* x, float* stats, int64_t rows, int64_t C, double eps) {
+    return col_reduce<1>(ctx, x, nullptr, nullptr, rows, C, eps, stats, nullptr);
+}
+
+int nncb_bn_grad_reduce(nncb_ctx* ctx, const float* x, const float* stats, const float* g, float* sum_g,
+                        float* sum_gx, int64_t rows, int64_t C) {
+    return col_reduce<2>(ctx, x, g, stats, rows, C, 0.0, sum_g, sum_gx);
+}
+
+int nncb_layernorm_fwd(nncb_ctx* ctx, const float* x, const float* gamma, const float* beta, float* y, int64_t rows,
+                       int64_t C, double eps) {
+    if (rows == 0) return 0;
+    layernorm_k<0><<<(unsigned)rows, 256, 0, ctx->stream>>>(x, gamma, beta, nullptr, y, nullptr, C, eps);
+    NNCB_LAUNCHED(ctx);
+    return 0;
+}
+
+int nncb_layernorm_bwd(nncb_ctx* ctx, const float* x, const float* gamma, const float* g, float* gx, int64_t rows,
+                       int64_t C, double eps) {
+    if (rows == 0) return 0;
+    layernorm_k<1><<<(unsigned)rows, 256, 0, ctx->stream>>>(x, gamma, nullptr, g, gx, nullptr, C, eps);
+    NNCB_LAUNCHED(ctx);
+    return 0;
+}
+
+int nncb_layernorm_dgamma(nncb_ctx* ctx, const float* x, const float* g, float* dgamma, int64_t rows, int64_t C,
+                          double eps) {
+    if (rows == 0) return 0;
+    int64_t col_tiles = (C + 31) / 32;
+    int64_t chunks = ((int64_t)ctx->sm_count * 8) / col_tiles;
+    if (chunks < 1) chunks = 1;
+    if (chunks > (rows + 63) / 64) chunks = (rows + 63) / 64;
+    if (chunks < 1) chunks = 1;
+    int64_t rpc = (rows + chunks - 1) / chunks;
+    size_t stats_bytes = sizeof(float) * 2 * rows;
+    size_t part_off = (stats_bytes + 255) / 256 * 256;
+    char* base = static_cast<char*>(nncb::scratch(ctx, part_off + sizeof(double) * 2 * chunks * C));
+    if (!base) return nncb::fail("layernorm_dgamma: scratch allocation failed");
+    float* rs = reinterpret_cast<float*>(base);
+    double* part = reinterpret_cast<double*>(base + part_off);
+    layernorm_k<2><<<(unsigned)rows, 256, 0, ctx->stream>>>(x, nullptr, nullptr, nullptr, nullptr, rs, C, eps);
+    NNCB_LAUNCHED(ctx);
+    ln_dgamma_partial_k<<<dim3((unsigned)col_tiles, (unsigned)chunks), dim3(32, 8), 0, ctx->stream>>>(x, g, rs, part,
+                                                                                                      rows, C, rpc);
+    NNCB_LAUNCHED(ctx);
+    col_final_k<0><<<(unsigned)((C + 127) / 128), 128, 0, ctx->stream>>>(part, chunks, C, rows, 0.0, dgamma, nullptr);
+    NNCB_LAUNCHED(ctx);
+    return 0;
+}
+
+int nncb_l1_loss(nncb_ctx* ctx, const float* pred, const float* target, float* grad, double* loss_dev, int64_t n) {
+    const int threads = 256;
+    unsigned blocks = nncb::grid_for(ctx, n, threads, 2);
+    double* partial = static_cast<double*>(nncb::scratch(ctx, sizeof(double) * blocks));
+    if (!partial) return nncb::fail("l1_loss: scratch allocation failed");
+    l1_k<<<blocks, threads, 0, ctx->stream>>>(pred, target, grad, partial, n);
+    NNCB_LAUNCHED(ctx);
+    l1_final_k<<<1, 32, 0, ctx->stream>>>(partial, (int)blocks, n, loss_dev);
+    NNCB_LAUNCHED(ctx);
+    return 0;
+}
+
+int nncb_sgd(nncb_ctx* ctx, float* w, const float* g, int64_t n, double lr, double grad_scale) {
+    if (n <= 0) return 0;
+    if ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(g)) & 15)
+        return nncb::fail("nncb_sgd: buffers must be 16-byte aligned");
+    sgd_k<<<nncb::grid_for(ctx, (n + 3) / 4, 256), 256, 0, ctx->stream>>>(w, g, n, lr, grad_scale);
+    NNCB_LAUNCHED(ctx);
+    return 0;
+}
+
+}  // extern "C"

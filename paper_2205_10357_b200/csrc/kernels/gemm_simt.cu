@@ -1,0 +1,237 @@
+// gemm_simt.cu -- exact-order fp32 implicit GEMM (NNCB_PREC_FP32, parity mode).
+//
+// All six contractions of the reference (kernels.hpp:118-243) as one tiled
+// implicit GEMM C[M,N] = sum_k A[m,k] B[k,n] whose per-output accumulation
+// visits k in exactly the reference loop order with separately rounded
+// products (__fmul_rn/__fadd_rn, no FMA), so results are bit-identical to the
+// reference REF / GEMM_TILED CPU kernels:
+//   dense fwd    acc = bias; k = i ascending                 (kernels.hpp:118-127)
+//   dense dgrad  acc = 0;    k = o ascending                 (kernels.hpp:130-139)
+//   dense wgrad  acc = 0;    k = b ascending                 (kernels.hpp:142-151)
+//   conv fwd     acc = bias; k = (dh, dw, ci) ascending      (kernels.hpp:166-190)
+//   conv wgrad   acc = 0;    k = (n, oh, ow) ascending       (kernels.hpp:220-243)
+//   conv dgrad   acc = 0;    per tap (oh, ow) ascending == (dh, dw) descending, an
+//                inner sum over co is rounded before it is added (kernels.hpp:192-218)
+// Out-of-range taps contribute exact zeros. The tensor-core path (gemm_tc.cu)
+// is the production path; this kernel pins it and serves the fp32 mode.
+#include "nncb_internal.cuh"
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16;
+
+struct Geo {
+    int64_t M, N, K;
+    nncb_gemm_desc d;
+};
+
+template <int KIND>
+__device__ __forceinline__ float a_val(const float* __restrict__ a, const Geo& G, int64_t m, int64_t k) {
+    const nncb_gemm_desc& d = G.d;
+    if (m >= G.M || k >= G.K) return 0.f;
+    if (KIND == NNCB_DENSE_FWD) return a[m * d.in_f + k];
+    if (KIND == NNCB_DENSE_DGRAD) return a[m * d.out_f + k];
+    if (KIND == NNCB_DENSE_WGRAD) return a[k * d.in_f + m];
+    if (KIND == NNCB_CONV_FWD) {
+        int64_t ci = k % d.ci, t = k / d.ci, dw = t % d.kw, dh = t / d.kw;
+        int64_t ow = m % d.ow, r = m / d.ow, oh = r % d.oh, n = r / d.oh;
+        int64_t h = oh * d.sh + dh - d.pad_top, w = ow * d.sw + dw - d.pad_left;
+        if (h < 0 || h >= d.ih || w < 0 || w >= d.iw) return 0.f;
+        return a[((n * d.ih + h) * d.iw + w) * d.ci + ci];
+    }
+    if (KIND == NNCB_CONV_WGRAD) {  // m = (dh, dw, ci), k = (n, oh, ow)
+        int64_t ci = m % d.ci, t = m / d.ci, dw = t % d.kw, dh = t / d.kw;
+        int64_t ow = k % d.ow, r = k / d.ow, oh = r % d.oh, n = r / d.oh;
+        int64_t h = oh * d.sh + dh - d.pad_top, w = ow * d.sw + dw - d.pad_left;
+        if (h < 0 || h >= d.ih || w < 0 || w >= d.iw) return 0.f;
+        return a[((n * d.ih + h) * d.iw + w) * d.ci + ci];
+    }
+    return 0.f;
+}
+
+template <int KIND>
+__device__ __forceinline__ float b_val(const float* __restrict__ b, const Geo& G, int64_t k, int64_t n) {
+    const nncb_gemm_desc& d = G.d;
+    if (k >= G.K || n >= G.N) return 0.f;
+    if (KIND == NNCB_DENSE_FWD) return b[k * d.out_f + n];
+    if (KIND == NNCB_DENSE_DGRAD) return b[n * d.out_f + k];
+    if (KIND == NNCB_DENSE_WGRAD) return b[k * d.out_f + n];
+    if (KIND == NNCB_CONV_FWD) return b[k * d.co + n];
+    if (KIND == NNCB_CONV_WGRAD) return b[k * d.co + n];
+    return 0.f;
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(256) gemm_exact_k(const float* __restrict__ a, const float* __restrict__ b,
+                                                   const float* __restrict__ bias, float* __restrict__ out, Geo G) {
+    __shared__ float As[BK][BM + 4];
+    __shared__ float Bs[BK][BN + 4];
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+    float acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            int64_t n = n0 + tx * 4 + j;
+            acc[i][j] = (bias && n < G.N) ? bias[n] : 0.f;
+        }
+    for (int64_t k0 = 0; k0 < G.K; k0 += BK) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            int idx = threadIdx.x + e * 256;
+            int kk = idx % BK, mm = idx / BK;
+            As[kk][mm] = a_val<KIND>(a, G, m0 + mm, k0 + kk);
+            int nn = idx % BN, kb = idx / BN;
+            Bs[kb][nn] = b_val<KIND>(b, G, k0 + kb, n0 + nn);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < BK; ++kk) {
+            if (k0 + kk >= G.K) break;
+            float av[4], bv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) av[i] = As[kk][ty * 4 + i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(av[i], bv[j]));
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        int64_t m = m0 + ty * 4 + i;
+        if (m >= G.M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            int64_t n = n0 + tx * 4 + j;
+            if (n < G.N) out[m * G.N + n] = acc[i][j];
+        }
+    }
+}
+
+// Conv dgrad with the reference's two-level rounding: for output pixel m=(n,h,w)
+// and channel ci, taps are visited in (dh, dw) DESCENDING order (== (oh, ow)
+// ascending); each valid tap contributes its own rounded sum over co.
+__global__ void __launch_bounds__(256) conv_dgrad_exact_k(const float* __restrict__ g, const float* __restrict__ k,
+                                                         float* __restrict__ gx, Geo G) {
+    const nncb_gemm_desc& d = G.d;
+    __shared__ float As[BK][BM + 4];
+    __shared__ float Bs[BK][BN + 4];
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+    float acc[4][4] = {};
+    for (int64_t tap = d.kh * d.kw - 1; tap >= 0; --tap) {
+        const int64_t dh = tap / d.kw, dw = tap % d.kw;
+        float part[4][4] = {};
+        for (int64_t c0 = 0; c0 < d.co; c0 += BK) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                int idx = threadIdx.x + e * 256;
+                int kk = idx % BK, mm = idx / BK;
+                int64_t m = m0 + mm, co = c0 + kk;
+                float v = 0.f;
+                if (m < G.M && co < d.co) {
+                    int64_t w = m % d.iw, r = m / d.iw, h = r % d.ih, n = r / d.ih;
+                    int64_t th = h + d.pad_top - dh, tw = w + d.pad_left - dw;
+                    if (th >= 0 && tw >= 0 && th % d.sh == 0 && tw % d.sw == 0) {
+                        int64_t oh = th / d.sh, ow = tw / d.sw;
+                        if (oh < d.oh && ow < d.ow) v = g[((n * d.oh + oh) * d.ow + ow) * d.co + co];
+                    }
+                }
+                As[kk][mm] = v;
+                int nn = idx % BN, kb = idx / BN;
+                int64_t ci = n0 + nn, cob = c0 + kb;
+                Bs[kb][nn] = (ci < d.ci && cob < d.co) ? k[((dh * d.kw + dw) * d.ci + ci) * d.co + cob] : 0.f;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int kk = 0; kk < BK; ++kk) {
+                if (c0 + kk >= d.co) break;
+                float av[4], bv[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) av[i] = As[kk][ty * 4 + i];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) part[i][j] = __fadd_rn(part[i][j], __fmul_rn(av[i], bv[j]));
+            }
+            __syncthreads();
+        }
+        // add this tap's rounded partial only where the tap is valid for the row
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            int64_t m = m0 + ty * 4 + i;
+            bool valid = false;
+            if (m < G.M) {
+                int64_t w = m % d.iw, r = m / d.iw, h = r % d.ih;
+                int64_t th = h + d.pad_top - dh, tw = w + d.pad_left - dw;
+                valid = th >= 0 && tw >= 0 && th % d.sh == 0 && tw % d.sw == 0 && th / d.sh < d.oh && tw / d.sw < d.ow;
+            }
+            if (valid)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = __fadd_rn(acc[i][j], part[i][j]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        int64_t m = m0 + ty * 4 + i;
+        if (m >= G.M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            int64_t n = n0 + tx * 4 + j;
+            if (n < G.N) gx[m * G.N + n] = acc[i][j];
+        }
+    }
+}
+
+}  // namespace
+
+namespace nncb {
+
+int gemm_simt(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const float* bias, float* out) {
+    Geo G{};
+    G.d = *d;
+    switch (d->kind) {
+        case NNCB_DENSE_FWD: G.M = d->batch; G.N = d->out_f; G.K = d->in_f; break;
+        case NNCB_DENSE_DGRAD: G.M = d->batch; G.N = d->in_f; G.K = d->out_f; break;
+        case NNCB_DENSE_WGRAD: G.M = d->in_f; G.N = d->out_f; G.K = d->batch; break;
+        case NNCB_CONV_FWD: G.M = d->n * d->oh * d->ow; G.N = d->co; G.K = d->kh * d->kw * d->ci; break;
+        case NNCB_CONV_WGRAD: G.M = d->kh * d->kw * d->ci; G.N = d->co; G.K = d->n * d->oh * d->ow; break;
+        case NNCB_CONV_DGRAD: G.M = d->n * d->ih * d->iw; G.N = d->ci; G.K = d->kh * d->kw * d->co; break;
+        default: return fail("gemm: unknown kind");
+    }
+    if (G.M == 0 || G.N == 0) return 0;
+    if ((G.N + BN - 1) / BN > 0x7fffffff || (G.M + BM - 1) / BM > 65535 * 1024)
+        return fail("gemm: problem too large for the exact path");
+    dim3 grid((unsigned)((G.N + BN - 1) / BN), (unsigned)((G.M + BM - 1) / BM));
+    if (grid.y > 65535) return fail("gemm exact: M too large (grid.y > 65535); use the tensor-core path");
+    const float* bi = (d->epilogue & NNCB_EPI_BIAS) ? bias : nullptr;
+    switch (d->kind) {
+        case NNCB_DENSE_FWD: gemm_exact_k<NNCB_DENSE_FWD><<<grid, 256, 0, ctx->stream>>>(a, b, bi, out, G); break;
+        case NNCB_DENSE_DGRAD: gemm_exact_k<NNCB_DENSE_DGRAD><<<grid, 256, 0, ctx->stream>>>(a, b, nullptr, out, G); break;
+        case NNCB_DENSE_WGRAD: gemm_exact_k<NNCB_DENSE_WGRAD><<<grid, 256, 0, ctx->stream>>>(a, b, nullptr, out, G); break;
+        case NNCB_CONV_FWD: gemm_exact_k<NNCB_CONV_FWD><<<grid, 256, 0, ctx->stream>>>(a, b, bi, out, G); break;
+        case NNCB_CONV_WGRAD: gemm_exact_k<NNCB_CONV_WGRAD><<<grid, 256, 0, ctx->stream>>>(a, b, nullptr, out, G); break;
+        case NNCB_CONV_DGRAD: conv_dgrad_exact_k<<<grid, 256, 0, ctx->stream>>>(a, b, out, G); break;
+    }
+    NNCB_LAUNCHED(ctx);
+    return 0;
+}
+
+}  // namespace nncb
+
+extern "C" int nncb_gemm(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const float* bias,
+                         float* out) {
+    if (d->precision == NNCB_PREC_TF32) {
+        bool handled = false;
+        int rc = nncb::gemm_tc(ctx, d, a, b, bias, out, &handled);
+        if (rc || handled) return rc;
+    }
+    return nncb::gemm_simt(ctx, d, a, b, bias, out);
+}

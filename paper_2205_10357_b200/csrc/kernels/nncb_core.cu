@@ -1,0 +1,190 @@
+// nncb_core.cu -- context, device memory, streams, CUDA graphs, events.
+// Replaces the reference's host-side ExecutionContext byte store
+// (runtime.cpp:108-152) and OffloadDevice transfers (runtime.cpp:71-102).
+#include <cstdio>
+#include <cstring>
+
+#include "nncb_internal.cuh"
+
+namespace nncb {
+
+static thread_local std::string g_error;
+
+void set_error(const std::string& msg) { g_error = msg; }
+int fail(const std::string& msg) {
+    g_error = msg;
+    return 1;
+}
+
+void* scratch(nncb_ctx* ctx, size_t bytes) {
+    if (bytes <= ctx->scratch_bytes) return ctx->scratch;
+    if (ctx->scratch) ctx->retired.push_back(ctx->scratch);
+    size_t want = bytes < (1u << 20) ? (1u << 20) : bytes;
+    if (cudaMalloc(&ctx->scratch, want) != cudaSuccess) {
+        ctx->scratch = nullptr;
+        ctx->scratch_bytes = 0;
+        return nullptr;
+    }
+    ctx->scratch_bytes = want;
+    return ctx->scratch;
+}
+
+}  // namespace nncb
+
+using nncb::fail;
+
+extern "C" {
+
+const char* nncb_last_error(void) { return nncb::g_error.c_str(); }
+
+int nncb_create(int device, nncb_ctx** out) {
+    int count = 0;
+    NNCB_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) return fail("nncb_create: no CUDA device " + std::to_string(device));
+    NNCB_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    NNCB_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return fail("nncb_create: this build targets sm_100a (B200); device " + std::string(prop.name) +
+                    " is sm_" + std::to_string(prop.major) + std::to_string(prop.minor));
+    auto* c = new nncb_ctx;
+    c->device = device;
+    c->sm_count = prop.multiProcessorCount;
+    NNCB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    NNCB_CUDA(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    *out = c;
+    return 0;
+}
+
+int nncb_destroy(nncb_ctx* c) {
+    if (!c) return 0;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    nncb_comm_destroy(c);
+    for (auto& [k, v] : c->ew_cache) {
+        (void)k;
+        nncb::ew_release(v);
+    }
+    if (c->scratch) cudaFree(c->scratch);
+    for (void* p : c->retired) cudaFree(p);
+    cudaStreamDestroy(c->stream);
+    cudaStreamDestroy(c->comm_stream);
+    delete c;
+    return 0;
+}
+
+int nncb_device_info(nncb_ctx* c, int* sms, int* major, int* minor, size_t* total) {
+    cudaDeviceProp prop;
+    NNCB_CUDA(cudaGetDeviceProperties(&prop, c->device));
+    if (sms) *sms = prop.multiProcessorCount;
+    if (major) *major = prop.major;
+    if (minor) *minor = prop.minor;
+    if (total) *total = prop.totalGlobalMem;
+    return 0;
+}
+
+int nncb_malloc(nncb_ctx* c, size_t bytes, void** out) {
+    NNCB_CUDA(cudaSetDevice(c->device));
+    *out = nullptr;
+    if (bytes == 0) return 0;
+    NNCB_CUDA(cudaMalloc(out, bytes));
+    return 0;
+}
+
+int nncb_free(nncb_ctx* c, void* p) {
+    if (!p) return 0;
+    NNCB_CUDA(cudaSetDevice(c->device));
+    NNCB_CUDA(cudaFree(p));
+    return 0;
+}
+
+int nncb_host_alloc(size_t bytes, void** out) {
+    NNCB_CUDA(cudaMallocHost(out, bytes ? bytes : 1));
+    return 0;
+}
+
+int nncb_host_free(void* p) {
+    if (p) NNCB_CUDA(cudaFreeHost(p));
+    return 0;
+}
+
+int nncb_memset(nncb_ctx* c, void* dst, int v, size_t bytes) {
+    if (bytes) NNCB_CUDA(cudaMemsetAsync(dst, v, bytes, c->stream));
+    return 0;
+}
+
+int nncb_h2d(nncb_ctx* c, void* dst, const void* src, size_t bytes) {
+    if (bytes) NNCB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
+    return 0;
+}
+
+int nncb_d2h(nncb_ctx* c, void* dst, const void* src, size_t bytes) {
+    if (bytes) NNCB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+    return 0;
+}
+
+int nncb_d2d(nncb_ctx* c, void* dst, const void* src, size_t bytes) {
+    if (bytes) NNCB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c->stream));
+    return 0;
+}
+
+int nncb_sync(nncb_ctx* c) {
+    NNCB_CUDA(cudaStreamSynchronize(c->stream));
+    NNCB_CUDA(cudaGetLastError());
+    return 0;
+}
+
+void* nncb_stream(nncb_ctx* c) { return c->stream; }
+
+int nncb_capture_begin(nncb_ctx* c) {
+    NNCB_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    return 0;
+}
+
+int nncb_capture_end(nncb_ctx* c, void** exec) {
+    cudaGraph_t graph = nullptr;
+    NNCB_CUDA(cudaStreamEndCapture(c->stream, &graph));
+    cudaGraphExec_t ge = nullptr;
+    cudaError_t e = cudaGraphInstantiate(&ge, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return fail(std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+    *exec = ge;
+    return 0;
+}
+
+int nncb_graph_launch(nncb_ctx* c, void* exec) {
+    NNCB_CUDA(cudaGraphLaunch(static_cast<cudaGraphExec_t>(exec), c->stream));
+    return 0;
+}
+
+int nncb_graph_destroy(void* exec) {
+    if (exec) NNCB_CUDA(cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(exec)));
+    return 0;
+}
+
+int nncb_event_create(void** ev) {
+    cudaEvent_t e;
+    NNCB_CUDA(cudaEventCreate(&e));
+    *ev = e;
+    return 0;
+}
+
+int nncb_event_record(nncb_ctx* c, void* ev) {
+    NNCB_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev), c->stream));
+    return 0;
+}
+
+int nncb_event_elapsed_ms(void* a, void* b, float* ms) {
+    NNCB_CUDA(cudaEventSynchronize(static_cast<cudaEvent_t>(b)));
+    NNCB_CUDA(cudaEventElapsedTime(ms, static_cast<cudaEvent_t>(a), static_cast<cudaEvent_t>(b)));
+    return 0;
+}
+
+int nncb_event_destroy(void* ev) {
+    if (ev) NNCB_CUDA(cudaEventDestroy(static_cast<cudaEvent_t>(ev)));
+    return 0;
+}
+
+uint64_t nncb_launch_count(nncb_ctx* c) { return c->launches.load(); }
+
+}  // extern "C"

@@ -1,0 +1,72 @@
+// nncb_internal.cuh -- shared internals of libnncb.so (not part of the ABI).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "nncb.h"
+
+struct nncb_ctx {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t stream = nullptr;       // compute stream
+    cudaStream_t comm_stream = nullptr;  // collectives
+    std::atomic<uint64_t> launches{0};
+    void* nccl_comm = nullptr;
+    int nranks = 1, rank = 0;
+    // fused-kernel cache: program hash -> kernel
+    std::map<std::string, nncb_ew_kernel*> ew_cache;
+    // scratch for reductions (grid partials), grown on demand
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
+    std::vector<void*> retired;          // outgrown scratch kept alive (captured graphs may use it)
+};
+
+namespace nncb {
+
+void set_error(const std::string& msg);
+int fail(const std::string& msg);
+
+#define NNCB_CUDA(expr)                                                                       \
+    do {                                                                                      \
+        cudaError_t _e = (expr);                                                              \
+        if (_e != cudaSuccess)                                                                \
+            return ::nncb::fail(std::string(#expr) + ": " + cudaGetErrorString(_e) + " (" +   \
+                                __FILE__ + ":" + std::to_string(__LINE__) + ")");            \
+    } while (0)
+
+#define NNCB_LAUNCHED(ctx)                                                                    \
+    do {                                                                                      \
+        cudaError_t _e = cudaGetLastError();                                                  \
+        if (_e != cudaSuccess)                                                                \
+            return ::nncb::fail(std::string("launch failed: ") + cudaGetErrorString(_e) +     \
+                                " (" + __FILE__ + ":" + std::to_string(__LINE__) + ")");     \
+        (ctx)->launches.fetch_add(1, std::memory_order_relaxed);                              \
+    } while (0)
+
+/// Grid-stride sizing: a multiple of the SM count (resident CTAs per SM x SMs).
+inline unsigned grid_for(const nncb_ctx* ctx, int64_t work_items, int threads, int per_sm = 8) {
+    int64_t want = (work_items + threads - 1) / threads;
+    int64_t cap = static_cast<int64_t>(ctx->sm_count) * per_sm;
+    if (want < 1) want = 1;
+    return static_cast<unsigned>(want < cap ? want : cap);
+}
+
+void* scratch(nncb_ctx* ctx, size_t bytes);
+void ew_release(nncb_ew_kernel* k);
+
+// GEMM back ends (gemm_simt.cu / gemm_tc.cu)
+int gemm_simt(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const float* bias,
+              float* out);
+int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const float* bias,
+            float* out, bool* handled);
+
+}  // namespace nncb

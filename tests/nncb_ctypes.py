@@ -1,0 +1,62 @@
+"""Direct ctypes access to libnncb.so kernels (the thin C-ABI of include/nncb.h)
+for kernel-level GPU tests."""
+import ctypes
+
+import numpy as np
+
+import paper_2205_10357_b200 as P
+
+K = P._kern
+_P, _I, _I64, _D, _S = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_char_p
+
+
+class GemmDesc(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("kind", "precision", "epilogue", "_pad")] + \
+               [(n, ctypes.c_int64) for n in ("n", "ih", "iw", "ci", "co", "kh", "kw", "sh", "sw", "oh", "ow",
+                                              "pad_top", "pad_left", "batch", "in_f", "out_f")]
+
+
+for name, res, args in [
+    ("nncb_malloc", _I, [_P, ctypes.c_size_t, ctypes.POINTER(_P)]),
+    ("nncb_free", _I, [_P, _P]),
+    ("nncb_h2d", _I, [_P, _P, _P, ctypes.c_size_t]),
+    ("nncb_d2h", _I, [_P, _P, _P, ctypes.c_size_t]),
+    ("nncb_memset", _I, [_P, _P, _I, ctypes.c_size_t]),
+    ("nncb_gemm", _I, [_P, ctypes.POINTER(GemmDesc), _P, _P, _P, _P]),
+]:
+    fn = getattr(K, name)
+    fn.restype, fn.argtypes = res, args
+
+
+def ctx():
+    c = P._host.nnc_device_ctx()
+    assert c, P._host.nnc_last_error()
+    return c
+
+
+class Dev:
+    def __init__(self, arr=None, nbytes=None):
+        self.c = ctx()
+        self.nbytes = arr.nbytes if arr is not None else nbytes
+        self.p = _P()
+        assert K.nncb_malloc(self.c, max(self.nbytes, 16), ctypes.byref(self.p)) == 0
+        if arr is not None:
+            a = np.ascontiguousarray(arr, dtype=np.float32)
+            assert K.nncb_h2d(self.c, self.p, a.ctypes.data, a.nbytes) == 0
+        else:
+            K.nncb_memset(self.c, self.p, 0, self.nbytes)
+
+    def get(self, shape):
+        out = np.empty(shape, dtype=np.float32)
+        assert K.nncb_d2h(self.c, out.ctypes.data, self.p, out.nbytes) == 0
+        K.nncb_sync(self.c)
+        return out
+
+    def __del__(self):
+        K.nncb_free(self.c, self.p)
+
+
+def gemm(desc, a, b, bias, out):
+    rc = K.nncb_gemm(ctx(), ctypes.byref(desc), a.p, b.p, bias.p if bias is not None else None, out.p)
+    assert rc == 0, K.nncb_last_error().decode()
+    assert K.nncb_sync(ctx()) == 0, K.nncb_last_error().decode()

@@ -1,0 +1,94 @@
+"""Kernel-level GEMM tests: the tcgen05 tf32 path against the exact fp32 path
+(bit-identical to the reference CPU loops) for all six contraction kinds,
+strided / padded convolutions and ragged tile edges. Bound: 2e-2 of max|ref|
+(reduced-precision GEMM tolerance); typical tf32 error is ~1e-3."""
+import numpy as np
+import pytest
+
+from tests.nncb_ctypes import Dev, GemmDesc, gemm
+
+pytestmark = pytest.mark.gpu
+
+DENSE_FWD, DENSE_DGRAD, DENSE_WGRAD, CONV_FWD, CONV_DGRAD, CONV_WGRAD = range(6)
+
+
+def conv_geom(n, ih, iw, ci, co, k, s, same=True):
+    oh = -(-ih // s) if same else (ih - k) // s + 1
+    ow = -(-iw // s) if same else (iw - k) // s + 1
+    pt = max((oh - 1) * s + k - ih, 0) // 2 if same else 0
+    pl = max((ow - 1) * s + k - iw, 0) // 2 if same else 0
+    return dict(n=n, ih=ih, iw=iw, ci=ci, co=co, kh=k, kw=k, sh=s, sw=s, oh=oh, ow=ow, pad_top=pt, pad_left=pl)
+
+
+def run_both(kind, geo, a, b, bias, out_shape):
+    outs = []
+    for prec in (0, 1):
+        d = GemmDesc(kind=kind, precision=prec, epilogue=1 if bias is not None else 0, **geo)
+        o = Dev(nbytes=int(np.prod(out_shape)) * 4)
+        gemm(d, a, b, bias, o)
+        outs.append(o.get(out_shape))
+    return outs
+
+
+def check(tc, ex):
+    err = np.max(np.abs(tc.astype(np.float64) - ex)) / max(np.max(np.abs(ex)), 1e-30)
+    assert err < 2e-2, err
+    return err
+
+
+CONVS = [
+    (2, 14, 14, 64, 64, 3, 1), (2, 13, 11, 64, 96, 3, 2), (4, 7, 7, 128, 256, 1, 1),
+    (2, 16, 16, 32, 64, 1, 2), (1, 9, 9, 64, 32, 3, 2), (3, 8, 8, 96, 128, 3, 1),
+]
+
+
+@pytest.mark.parametrize("shape", CONVS)
+def test_conv_fwd(shape):
+    n, ih, iw, ci, co, k, s = shape
+    g = conv_geom(n, ih, iw, ci, co, k, s)
+    rng = np.random.default_rng(0)
+    x = rng.uniform(-1, 1, (n, ih, iw, ci)).astype(np.float32)
+    w = rng.uniform(-1, 1, (k, k, ci, co)).astype(np.float32)
+    bias = rng.uniform(-1, 1, co).astype(np.float32)
+    tc, ex = run_both(CONV_FWD, g, Dev(x), Dev(w), Dev(bias), (n, g["oh"], g["ow"], co))
+    check(tc, ex)
+
+
+@pytest.mark.parametrize("shape", CONVS)
+def test_conv_dgrad(shape):
+    n, ih, iw, ci, co, k, s = shape
+    g = conv_geom(n, ih, iw, ci, co, k, s)
+    rng = np.random.default_rng(1)
+    gy = rng.uniform(-1, 1, (n, g["oh"], g["ow"], co)).astype(np.float32)
+    w = rng.uniform(-1, 1, (k, k, ci, co)).astype(np.float32)
+    tc, ex = run_both(CONV_DGRAD, g, Dev(gy), Dev(w), None, (n, ih, iw, ci))
+    check(tc, ex)
+
+
+@pytest.mark.parametrize("shape", CONVS)
+def test_conv_wgrad(shape):
+    n, ih, iw, ci, co, k, s = shape
+    g = conv_geom(n, ih, iw, ci, co, k, s)
+    rng = np.random.default_rng(2)
+    x = rng.uniform(-1, 1, (n, ih, iw, ci)).astype(np.float32)
+    gy = rng.uniform(-1, 1, (n, g["oh"], g["ow"], co)).astype(np.float32)
+    tc, ex = run_both(CONV_WGRAD, g, Dev(x), Dev(gy), None, (k, k, ci, co))
+    check(tc, ex)
+
+
+@pytest.mark.parametrize("b,i,o", [(32, 2048, 64), (256, 2048, 1000), (200, 96, 160), (64, 128, 16)])
+def test_dense(b, i, o):
+    rng = np.random.default_rng(3)
+    x = rng.uniform(-1, 1, (b, i)).astype(np.float32)
+    w = rng.uniform(-1, 1, (i, o)).astype(np.float32)
+    bias = rng.uniform(-1, 1, o).astype(np.float32)
+    gy = rng.uniform(-1, 1, (b, o)).astype(np.float32)
+    geo = dict(batch=b, in_f=i, out_f=o)
+    tc, ex = run_both(DENSE_FWD, geo, Dev(x), Dev(w), Dev(bias), (b, o))
+    check(tc, ex)
+    ref = x.astype(np.float64) @ w + bias
+    assert np.max(np.abs(ex - ref)) / np.max(np.abs(ref)) < 1e-5
+    tc, ex = run_both(DENSE_DGRAD, geo, Dev(gy), Dev(w), None, (b, i))
+    check(tc, ex)
+    tc, ex = run_both(DENSE_WGRAD, geo, Dev(x), Dev(gy), None, (i, o))
+    check(tc, ex)
