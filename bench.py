@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""bench.py -- headline benchmark of the B200 backend (driver contract).
+
+Default workload (BASELINE.json metric "fwd+bwd samples/sec (ResNet-50-shaped
+graph)"): C4 = the ResNet-50-shaped graph with BatchNorm, one full training
+step (forward, L1 loss, backward, SGD) at batch 256 per GPU, fp32 storage with
+tcgen05 tf32 GEMMs, synthetic U(-1,1) inputs (activations are far larger than
+the 126 MB L2, so no flush is needed between steps).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1|c2|c3|c4|c5] [--impl ours|reference]
+
+Under torchrun (N > 1) every rank trains its own batch shard (weak scaling) and
+gradients are all-reduced with NCCL inside the step's CUDA graph; rank 0 prints
+one JSON line with the max-over-ranks device time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+CONFIGS = {
+    "c1": dict(workload="C1 small CNN (conv-BN-ReLU-maxpool x2, dense, L1) train step", batch=32, kind="train"),
+    "c2": dict(workload="C2 depth-16 BN/ReLU/Mul/Add chain on [256,128,128,64] fp32, train-mode BN forward",
+               batch=256, kind="chain"),
+    "c3": dict(workload="C3 ResNet-50-shaped (BN) inference", batch=256, kind="infer"),
+    "c4": dict(workload="C4 ResNet-50-shaped (BN) training step fwd+L1+bwd+SGD", batch=256, kind="train"),
+    "c5": dict(workload="C5 MLP 4096x8 (Dense+GELU+LayerNorm) training step", batch=8192, kind="train"),
+}
+
+
+def peaks():
+    try:
+        with open(PEAKS_FILE) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return FALLBACK_PEAKS, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (clocks + throttle reasons)."""
+
+    def __init__(self, index: int):
+        self.index, self.samples, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        sm = []
+        smax = None
+        for s in self.samples:
+            try:
+                sm.append(float(s[0]))
+                smax = float(s[1])
+            except ValueError:
+                continue
+            for i, n in enumerate(names):
+                if s[3 + i].lower() in ("active", "1", "yes"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_workload(cfg: str, batch: int):
+    from paper_2205_10357_b200 import workloads as W
+    if cfg == "c1":
+        doc = W.c1_small_cnn(batch, bn=True)
+        inputs = {"x": W.uniform((batch, 32, 32, 3), 1, "x")}
+        out_shape = (batch, 10)
+    elif cfg == "c2":
+        shape = (batch, 128, 128, 64)
+        doc = W.c2_chain(shape, mode="bn")
+        inputs = {"x": W.uniform(shape, 5, "x"), "y": W.uniform(shape, 6, "y")}
+        out_shape = shape
+    elif cfg in ("c3", "c4"):
+        doc = W.resnet50(batch, bn=True)
+        inputs = {"x": W.uniform((batch, 224, 224, 3), 1, "x")}
+        out_shape = (batch, 1000)
+    elif cfg == "c5":
+        doc = W.mlp(batch, 4096, 8)
+        inputs = {"x": W.uniform((batch, 4096), 1, "x")}
+        out_shape = (batch, 4096)
+    else:
+        raise SystemExit(f"unknown config {cfg}")
+    target = W.uniform(out_shape, 2, "target", 0.0, 1.0)
+    return doc, inputs, target
+
+
+def reference_doc(cfg: str, batch: int):
+    """The reference's vocabulary has no BatchNorm / GELU / LayerNorm:
+    its CPU arm runs the same graphs with those layers removed (labelled)."""
+    from paper_2205_10357_b200 import workloads as W
+    if cfg == "c1":
+        return W.c1_small_cnn(batch, bn=False), {"x": W.uniform((batch, 32, 32, 3), 1, "x")}, (batch, 10)
+    if cfg in ("c3", "c4"):
+        return W.resnet50(batch, bn=False), {"x": W.uniform((batch, 224, 224, 3), 1, "x")}, (batch, 1000)
+    if cfg == "c2":
+        shape = (1, 128, 128, 64)
+        return (W.c2_chain(shape, mode="ref"), {"x": W.uniform(shape, 5, "x"), "y": W.uniform(shape, 6, "y")},
+                shape)
+    if cfg == "c5":
+        nodes = json.loads(W.mlp(batch, 4096, 8))
+        nodes["nodes"] = [n for n in nodes["nodes"] if n["op"] == "dense"]
+        for i, n in enumerate(nodes["nodes"]):
+            n["inputs"] = ["x"] if i == 0 else [nodes["nodes"][i - 1]["name"]]
+        nodes["outputs"] = [nodes["nodes"][-1]["name"]]
+        return json.dumps(nodes), {"x": W.uniform((batch, 4096), 1, "x")}, (batch, 4096)
+    raise SystemExit(cfg)
+
+
+def _ref_worker(args):
+    cfg, batch, seconds = args
+    from oracle import reference as R
+    from paper_2205_10357_b200 import workloads as W
+    doc, inputs, out_shape = reference_doc(cfg, batch)
+    m = R.RefModel(doc, 0)
+    target = W.uniform(out_shape, 2, "target", 0.0, 1.0)
+    n, t0 = 0, time.time()
+    while True:
+        if cfg == "c2" or cfg == "c3":
+            m.run(inputs)
+        else:
+            m.train_step(inputs, target, 1e-4)
+        n += 1
+        if time.time() - t0 >= seconds:
+            break
+    return n, time.time() - t0
+
+
+def cpu_reference(cfg: str, seconds: float, cores: int):
+    """The reference CPU implementation (oracle/_ref, compiled from /root/reference
+    sources) on the host cores: `cores` single-threaded replicas (the reference is
+    single-threaded, plans are shareable), each stepping a reduced batch."""
+    from multiprocessing import get_context
+    batch = {"c1": 32, "c2": 1, "c3": 1, "c4": 1, "c5": 8}[cfg]
+    with get_context("spawn").Pool(cores) as pool:
+        res = pool.map(_ref_worker, [(cfg, batch, seconds)] * cores)
+    steps = sum(r[0] for r in res)
+    wall = max(r[1] for r in res)
+    if cfg == "c2":
+        elems = 128 * 128 * 64
+        value = steps * elems * 12 / wall / 1e9
+        unit = "GB/s"
+    else:
+        value = steps * batch / wall
+        unit = "samples/s"
+    sample = {"c1": "C1 without BatchNorm (reference vocabulary), batch 32 per replica",
+              "c2": "C2 chain without BatchNorm, one [1,128,128,64] slice per step",
+              "c3": "ResNet-50-shaped without BatchNorm, batch 1 inference per replica",
+              "c4": "ResNet-50-shaped without BatchNorm, batch 1 train_step per replica",
+              "c5": "MLP without GELU/LayerNorm (8 x Dense 4096), batch 8 per replica"}[cfg]
+    return {"value": value, "unit": unit, "cores": cores, "kind": "reference",
+            "sample": f"{sample}; {steps} steps in {wall:.1f} s on {cores} cores"}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-json", default=None)
+    args = ap.parse_args()
+    world, rank, local = dist_setup()
+    cfg = CONFIGS[args.config]
+    batch = args.batch or cfg["batch"]
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cores = min(os.cpu_count() or 1, 32)
+        per_step = max(args.cpu_seconds / max(args.steps + args.warmup, 1), 2.0)
+        cb = cpu_reference(args.config, per_step * max(args.steps, 1), cores)
+        line = {"metric": cb["unit"] if args.config == "c2" else "fwd+bwd samples/sec (ResNet-50-shaped graph)"
+                if args.config == "c4" else cb["unit"],
+                "value": cb["value"], "unit": cb["unit"], "n_gpus": args.gpus, "steps": args.steps,
+                "warmup": args.warmup, "higher_is_better": True, "impl": "reference", "dtype": "f32",
+                "data": "synthetic", "config": {"workload": cfg["workload"] + " (reference vocabulary)",
+                                                "batch_per_replica": cb["sample"]},
+                "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": cb["unit"], "h2d_bytes_per_step": 0,
+                                            "d2h_bytes_per_step": 0}, "vs_baseline": None}
+        print(json.dumps(line), flush=True)
+        return
+
+    os.environ.setdefault("NNC_DEVICE", str(local))
+    import paper_2205_10357_b200 as P
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+        dist = dist_mod
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        uid = [P.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        P.init_comm(world, rank, uid[0])
+
+    doc, inputs, target = make_workload(args.config, batch)
+    model = P.CompiledModel(doc, precision=P.PREC_TF32)
+    timer = P.DeviceTimer()
+    lr = 1e-4
+    clocks = Clocks(local)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if not dist:
+            return v
+        import torch
+        t = torch.tensor([v], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    if cfg["kind"] in ("train",):
+        model.trainer_prepare(inputs, target)
+        step = lambda: model.trainer_step_device(lr)  # noqa: E731
+        units = batch * world
+        metric = "fwd+bwd samples/sec (ResNet-50-shaped graph)" if args.config == "c4" else "train samples/sec"
+        unit = "samples/s"
+    elif cfg["kind"] == "infer":
+        model.run(inputs)
+        step = lambda: model.infer_device()  # noqa: E731
+        units = batch * world
+        metric, unit = "inference samples/sec", "samples/s"
+    else:  # chain: train-mode BN forward
+        model.run(inputs, role="train_fwd")
+        step = lambda: model.infer_device()  # noqa: E731
+        units = batch * world
+        metric, unit = "fused-group samples/sec", "samples/s"
+
+    for _ in range(args.warmup):
+        step()
+    timer.sync()
+    barrier()
+    clocks.start()
+    l0 = timer.launches()
+    timer.start()
+    for _ in range(args.steps):
+        step()
+    ms = timer.stop()
+    clk = clocks.stop()
+    launches = timer.launches() - l0
+    ms = max_over_ranks(ms)
+    ms_per_step = ms / args.steps
+    value = units / (ms_per_step / 1000.0)
+
+    # ---- end to end through the public API (host buffers every step) ----
+    e2e = None
+    if cfg["kind"] == "train":
+        h2d = sum(v.nbytes for v in inputs.values()) + target.nbytes
+        barrier()
+        t0 = time.perf_counter()
+        timer.start()
+        for _ in range(max(2, args.steps // 2)):
+            model.train_step(inputs, target, lr)
+        e_ms = timer.stop()
+        wall = (time.perf_counter() - t0) * 1000
+        n_e2e = max(2, args.steps // 2)
+        e_ms = max_over_ranks(max(e_ms, wall) / n_e2e)
+        e2e = {"value": units / (e_ms / 1000.0), "unit": unit, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8,
+               "ms_per_step": e_ms}
+
+    # ---- roofline of the dominant kernel (per-launch CUDA events) ----
+    roof, top = None, None
+    if cfg["kind"] == "train" and rank == 0:
+        prof = model.profile_step(0.0)
+        if args.profile_json:
+            with open(args.profile_json, "w") as f:
+                json.dump(prof, f, indent=1)
+        agg = {}
+        for p in prof:
+            a = agg.setdefault(p["label"], {"ms": 0.0, "bytes": 0.0, "flops": 0.0, "kind": p["kind"], "n": 0})
+            a["ms"] += p["ms"]
+            a["bytes"] += p["bytes"]
+            a["flops"] += p["flops"]
+            a["n"] += 1
+        total = sum(a["ms"] for a in agg.values())
+        label, a = max(agg.items(), key=lambda kv: kv[1]["ms"])
+        pk, src = peaks()
+        if a["flops"] > 0:
+            ach = a["flops"] / (a["ms"] / 1000) / 1e12
+            peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+            roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                    "traffic": None, "kernel": f"{a['kind']} {label}", "share_of_step": a["ms"] / total,
+                    "peak_source": f"{src} bf16 sustained (tf32 kind runs at half the bf16 rate)"}
+        else:
+            ach = a["bytes"] / (a["ms"] / 1000) / 1e9
+            peak = pk["hbm_gbs"]
+            roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                    "traffic": None, "kernel": f"{a['kind']} {label}", "share_of_step": a["ms"] / total,
+                    "peak_source": f"{src} HBM copy"}
+        by_kind = {}
+        for p in prof:
+            k = p["kind"].split(":")[0]
+            d = by_kind.setdefault(k, {"ms": 0.0, "bytes": 0.0, "flops": 0.0})
+            d["ms"] += p["ms"]
+            d["bytes"] += p["bytes"]
+            d["flops"] += p["flops"]
+        top = {k: {"ms": round(v["ms"], 3),
+                   "GB/s": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1),
+                   "TFLOP/s": round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 1)} for k, v in by_kind.items()}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            cpu = cpu_reference(args.config, args.cpu_seconds, min(os.cpu_count() or 1, 32))
+        except Exception as exc:  # noqa: BLE001
+            cpu = {"value": None, "error": str(exc)[:200]}
+    line = {
+        "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 (tcgen05 kind::tf32 GEMMs, fp32 accumulate)", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "global_batch": batch * world, "batch_per_gpu": batch,
+                   "parallelism": f"dp{world}", "l2": "activations >> 126 MB L2; no flush needed"},
+        "clocks": clk, "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
+        "by_kernel_kind": top,
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -52,8 +52,15 @@ int      nnc_model_trainer_prepare(nnc_model* m, const float* target, int64_t n)
 int      nnc_model_trainer_step_device(nnc_model* m, double lr);
 int      nnc_model_trainer_loss(nnc_model* m, double* loss);
 uint64_t nnc_model_launches_per_step(nnc_model* m);
+/* One eager step with CUDA events around each launch; JSON list of
+ * {label, kind, ms, bytes, flops} (algorithmic bytes / flops per launch). */
+const char* nnc_model_profile_step(nnc_model* m, double lr);
 uint64_t nnc_model_arena_bytes(nnc_model* m);
 int      nnc_model_infer_device(nnc_model* m);         /* replay inference, no host copies */
+
+/* NVRTC-compiles every generated fused-group kernel of the model's three plans
+ * for sm_100a (no device needed). */
+int nnc_model_check_kernels(nnc_model* m);
 
 /* The device context (nncb_ctx*) for stream events / timing via nncb.h. */
 void* nnc_device_ctx(void);

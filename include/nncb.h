@@ -104,6 +104,8 @@ int nncb_ew_compile(nncb_ctx* ctx, const nncb_ew_program* prog, nncb_ew_kernel**
 /* n = element count of the group's iteration space, channels = C for LOAD_CH. */
 int nncb_ew_launch(nncb_ctx* ctx, nncb_ew_kernel* k, void* const* slots, int64_t n,
                    int64_t channels);
+/* Generates and NVRTC-compiles a program without a device (build-time check). */
+int nncb_ew_compile_check(const nncb_ew_program* prog);
 /* Generated CUDA source of a compiled program (for inspection / profiles). */
 const char* nncb_ew_source(nncb_ew_kernel* k);
 

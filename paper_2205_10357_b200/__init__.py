@@ -71,9 +71,11 @@ def _load():
         "nnc_model_trainer_step_device": (I, [P, D]),
         "nnc_model_trainer_loss": (I, [P, DP]),
         "nnc_model_launches_per_step": (U64, [P]),
+        "nnc_model_profile_step": (S, [P, D]),
         "nnc_model_arena_bytes": (U64, [P]),
         "nnc_model_infer_device": (I, [P]),
         "nnc_device_ctx": (P, []),
+        "nnc_model_check_kernels": (I, [P]),
         "nnc_comm_unique_id": (I, [ctypes.c_char_p]),
         "nnc_init_comm": (I, [I, I, ctypes.c_char_p]),
         "nnc_group_document": (S, [S, S]),
@@ -213,11 +215,22 @@ class CompiledModel:
         _check(_host.nnc_model_trainer_loss(self._h, ctypes.byref(loss)))
         return loss.value
 
+    def profile_step(self, lr: float = 0.0):
+        """Per-launch device times of one eager training step (CUDA events)."""
+        res = _host.nnc_model_profile_step(self._h, lr)
+        if res is None:
+            raise NNCError(100, _host.nnc_last_error().decode())
+        return json.loads(res.decode())
+
     def launches_per_step(self) -> int:
         return int(_host.nnc_model_launches_per_step(self._h))
 
     def arena_bytes(self) -> int:
         return int(_host.nnc_model_arena_bytes(self._h))
+
+    def check_kernels(self):
+        """NVRTC-compile every generated fused-group kernel (no GPU needed)."""
+        _check(_host.nnc_model_check_kernels(self._h))
 
     def infer_device(self):
         _check(_host.nnc_model_infer_device(self._h))

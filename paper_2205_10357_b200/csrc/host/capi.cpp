@@ -230,6 +230,18 @@ int nnc_model_trainer_loss(nnc_model* m, double* loss) {
     });
 }
 
+const char* nnc_model_profile_step(nnc_model* m, double lr) {
+    int rc = guarded([&] {
+        if (!m->trainer) throw Error(Error::Code::BadDocument, "trainer not prepared");
+        auto t = m->trainer->profile_step(lr);
+        nlohmann::json j = nlohmann::json::array();
+        for (const auto& x : t)
+            j.push_back({{"label", x.label}, {"kind", x.kind}, {"ms", x.ms}, {"bytes", x.bytes}, {"flops", x.flops}});
+        g_buf = j.dump();
+    });
+    return rc ? nullptr : g_buf.c_str();
+}
+
 uint64_t nnc_model_launches_per_step(nnc_model* m) { return m->trainer ? m->trainer->launches_per_step() : 0; }
 uint64_t nnc_model_arena_bytes(nnc_model* m) { return m->trainer ? m->trainer->arena_bytes() : 0; }
 
@@ -239,6 +251,20 @@ int nnc_model_infer_device(nnc_model* m) {
         runtime::ExecOptions o = m->opts;
         o.materialize = &none;
         runtime::execute(m->plans.inference, m->inputs, *m->host, nullptr, o);
+    });
+}
+
+int nnc_model_check_kernels(nnc_model* m) {
+    return guarded([&] {
+        for (const auto* p : {&m->plans.inference, &m->plans.train_fwd, &m->plans.train_bwd})
+            for (const auto& g : p->groups)
+                for (const auto& L : g.launches) {
+                    if (L.kind != plan::LaunchKind::Ew) continue;
+                    nncb_ew_program prog{static_cast<int32_t>(L.ew.size()), L.ew.data(), L.ew_regs,
+                                         static_cast<int32_t>(L.args.size())};
+                    if (nncb_ew_compile_check(&prog))
+                        throw Error(Error::Code::DeviceError, L.label + ": " + nncb_last_error());
+                }
     });
 }
 

@@ -151,6 +151,39 @@ void enqueue(nncb_ctx* ctx, const BoundLaunch& b) {
     }
 }
 
+// Algorithmic (minimum) HBM bytes and flops of one launch: every operand read
+// once and every result written once; GEMMs count 2*M*N*K flops.
+void launch_cost(const BoundLaunch& b, const Launch& L, const ExecutionPlan& p, double& bytes, double& flops) {
+    bytes = flops = 0;
+    auto elems = [&](size_t arg) { return static_cast<double>(element_count(p.values[L.args[arg].slot].dims)); };
+    switch (b.kind) {
+        case LaunchKind::Ew: {
+            double n = static_cast<double>(b.n);
+            for (const auto& in : L.ew)
+                if (in.op == NNCB_EW_LOAD || in.op == NNCB_EW_STORE) bytes += 4.0 * n;
+            break;
+        }
+        case LaunchKind::Gemm: {
+            const nncb_gemm_desc& d = b.gemm;
+            double M, N, K;
+            switch (d.kind) {
+                case NNCB_DENSE_FWD: M = d.batch; N = d.out_f; K = d.in_f; break;
+                case NNCB_DENSE_DGRAD: M = d.batch; N = d.in_f; K = d.out_f; break;
+                case NNCB_DENSE_WGRAD: M = d.in_f; N = d.out_f; K = d.batch; break;
+                case NNCB_CONV_FWD: M = double(d.n) * d.oh * d.ow; N = d.co; K = double(d.kh) * d.kw * d.ci; break;
+                case NNCB_CONV_DGRAD: M = double(d.n) * d.ih * d.iw; N = d.ci; K = double(d.kh) * d.kw * d.co; break;
+                default: M = double(d.kh) * d.kw * d.ci; N = d.co; K = double(d.n) * d.oh * d.ow; break;
+            }
+            flops = 2.0 * M * N * K;
+            for (size_t a = 0; a < L.args.size(); ++a) bytes += 4.0 * elems(a);
+            break;
+        }
+        default:
+            for (size_t a = 0; a < L.args.size(); ++a) bytes += 4.0 * elems(a);
+            break;
+    }
+}
+
 }  // namespace
 
 /* ------------------------------------------------------------------ */
@@ -164,6 +197,7 @@ struct Program {
     int64_t arena_bytes = 0;
     std::unordered_map<std::string, void*> where;   // value name -> device pointer
     std::vector<std::vector<BoundLaunch>> steps;     // per plan, flattened launches
+    std::vector<std::vector<const Launch*>> sources; // per plan, the plan launch of each bound launch
     std::vector<std::vector<std::pair<size_t, std::string>>> step_labels;  // per plan: (launch idx, label)
     int precision = NNCB_PREC_TF32;
 
@@ -222,9 +256,13 @@ struct Program {
         for (const ExecutionPlan* p : plans) {
             steps.emplace_back();
             step_labels.emplace_back();
+            sources.emplace_back();
             for (const plan::ExecStep& es : p->exec_steps) {
                 step_labels.back().push_back({steps.back().size(), es.label});
-                for (uint32_t li : es.launches) steps.back().push_back(resolve(*p, p->groups[es.group].launches[li]));
+                for (uint32_t li : es.launches) {
+                    steps.back().push_back(resolve(*p, p->groups[es.group].launches[li]));
+                    sources.back().push_back(&p->groups[es.group].launches[li]);
+                }
             }
         }
     }
@@ -774,6 +812,58 @@ Trainer::Trainer(const plan::VersionPlans& plans, HostModel& model, Device& dev,
 }
 
 Trainer::~Trainer() = default;
+
+std::vector<Trainer::LaunchTiming> Trainer::profile_step(double lr) {
+    Impl& I = *impl;
+    nncb_ctx* ctx = I.dev->ctx();
+    I.sync_params();
+    std::vector<LaunchTiming> out;
+    std::vector<void*> evs;
+    auto ev = [&]() {
+        void* e = nullptr;
+        NNC_CHECK(nncb_event_create(&e));
+        NNC_CHECK(nncb_event_record(ctx, e));
+        evs.push_back(e);
+    };
+    ev();
+    for (size_t pi = 0; pi < 2; ++pi) {
+        const ExecutionPlan& p = *I.prog->plans[pi];
+        for (size_t k = 0; k < I.prog->steps[pi].size(); ++k) {
+            const BoundLaunch& b = I.prog->steps[pi][k];
+            const Launch& L = *I.prog->sources[pi][k];
+            enqueue(ctx, b);
+            ev();
+            LaunchTiming t;
+            t.label = L.label;
+            t.kind = L.kind == LaunchKind::Gemm ? std::string("gemm:") + hlir::op_name(L.op) : plan::launch_kind_name(L.kind);
+            launch_cost(b, L, p, t.bytes, t.flops);
+            out.push_back(t);
+        }
+        if (pi == 0) {
+            int64_t n = element_count(I.plans->train_fwd.values[I.plans->train_fwd.find_value(I.pred)].dims);
+            NNC_CHECK(nncb_l1_loss(ctx, static_cast<float*>(I.prog->ptr(I.pred)), static_cast<float*>(I.target),
+                                   static_cast<float*>(I.prog->ptr(I.dpred)), static_cast<double*>(I.loss), n));
+            ev();
+            out.push_back({"l1_loss", "l1_loss", 0, 12.0 * n, 0});
+        }
+    }
+    NNC_CHECK(nncb_sgd(ctx, static_cast<float*>(I.params), static_cast<float*>(I.grads), I.region_elems, lr,
+                       1.0 / static_cast<double>(I.dev->nranks())));
+    ev();
+    out.push_back({"sgd", "sgd", 0, 12.0 * static_cast<double>(I.region_elems), 0});
+    NNC_CHECK(nncb_sync(ctx));
+    for (size_t i = 0; i < out.size(); ++i) {
+        float ms = 0;
+        NNC_CHECK(nncb_event_elapsed_ms(evs[i], evs[i + 1], &ms));
+        out[i].ms = ms;
+    }
+    for (void* e : evs) nncb_event_destroy(e);
+    for (const std::string& w : I.weights) {
+        I.model->bump(w);
+        I.dev->mark_device_newer(*I.model, w, I.model->stamp(w));
+    }
+    return out;
+}
 
 void* Trainer::input_device_ptr(const std::string& name) { return impl->prog->ptr(name); }
 void* Trainer::target_device_ptr() { return impl->target; }

@@ -149,6 +149,13 @@ struct Trainer {
     /// Device-resident variant (no host copies): enqueue one step.
     void step_device(double lr);
     double last_loss();
+    /// One eager step with CUDA events around every launch on the compute
+    /// stream: (label, kind, ms, algorithmic bytes, algorithmic flops) per launch.
+    struct LaunchTiming {
+        std::string label, kind;
+        double ms = 0, bytes = 0, flops = 0;
+    };
+    std::vector<LaunchTiming> profile_step(double lr);
     void* input_device_ptr(const std::string& name);
     void* target_device_ptr();
     size_t arena_bytes() const;

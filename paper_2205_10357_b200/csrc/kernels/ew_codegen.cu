@@ -14,6 +14,7 @@
 // kernels.hpp:47-50), ReluGrad masks on the forward input (kernels.hpp:52-55).
 #include <nvrtc.h>
 
+#include <cstdio>
 #include <cstring>
 #include <sstream>
 
@@ -120,19 +121,17 @@ void emit_body(std::ostringstream& os, const nncb_ew_program& p, int W, bool use
                 expr = "bn_apply_(" + a + "[j], " + b + "[j], " + c + "[j], " + dd + "[j], " + e + "[j])";
                 break;
             case NNCB_EW_BN_INFER: {
-                std::ostringstream eps;
-                eps.precision(17);
-                eps << in.imm;
+                char eps[64];
+                snprintf(eps, sizeof(eps), "%.17e", in.imm);
                 expr = "bn_infer_(" + a + "[j], " + b + "[j], " + c + "[j], " + dd + "[j], " + e + "[j], " +
-                       eps.str() + ")";
+                       std::string(eps) + ")";
                 break;
             }
             case NNCB_EW_BN_GRAD: {
-                std::ostringstream cnt;
-                cnt.precision(17);
-                cnt << static_cast<float>(in.imm) << "f";
+                char cnt[64];
+                snprintf(cnt, sizeof(cnt), "%.9e", static_cast<double>(static_cast<float>(in.imm)));
                 expr = "bn_grad_(" + a + "[j], " + b + "[j], " + c + "[j], " + dd + "[j], " + e + "[j], " + f +
-                       "[j], " + h + "[j], " + cnt.str() + ")";
+                       "[j], " + h + "[j], (float)" + cnt + ")";
                 break;
             }
             default: expr = "0.f /* unknown op */"; break;
@@ -175,6 +174,21 @@ int nvrtc_fail(nvrtcProgram prog, nvrtcResult r, const std::string& src) {
 }  // namespace
 
 extern "C" {
+
+int nncb_ew_compile_check(const nncb_ew_program* p) {
+    if (p->n_slots > kMaxSlots) return nncb::fail("nncb_ew_compile_check: too many slots");
+    bool uses_ch = false;
+    for (int k = 0; k < p->n_instr; ++k) uses_ch = uses_ch || p->instr[k].op == NNCB_EW_LOAD_CH;
+    std::string src = generate(*p, uses_ch);
+    nvrtcProgram prog = nullptr;
+    nvrtcResult r = nvrtcCreateProgram(&prog, src.c_str(), "nnc_fused_ew.cu", 0, nullptr, nullptr);
+    if (r != NVRTC_SUCCESS) return nvrtc_fail(prog, r, src);
+    const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "--fmad=false"};
+    r = nvrtcCompileProgram(prog, 4, opts);
+    if (r != NVRTC_SUCCESS) return nvrtc_fail(prog, r, src);
+    nvrtcDestroyProgram(&prog);
+    return 0;
+}
 
 int nncb_ew_compile(nncb_ctx* ctx, const nncb_ew_program* p, nncb_ew_kernel** out) {
     if (p->n_slots > kMaxSlots) return nncb::fail("nncb_ew_compile: too many slots");
