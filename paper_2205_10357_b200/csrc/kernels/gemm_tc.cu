@@ -352,9 +352,10 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ partial, float* _
 // ---------------------------------------------------------------------------
 
 bool encode_4d(CUtensorMap* map, const float* base, int64_t c, int64_t w, int64_t h, int64_t n, int bc, int bw,
-               int bh, int bnn, int ew, int eh, bool mn_major) {
+               int bh, int bnn, int ew, int eh, bool mn_major, int64_t pitch = 0) {
+    if (pitch == 0) pitch = c;   // elements between consecutive pixels
     cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
-    cuuint64_t strides[3] = {(cuuint64_t)(c * 4), (cuuint64_t)(c * w * 4), (cuuint64_t)(c * w * h * 4)};
+    cuuint64_t strides[3] = {(cuuint64_t)(pitch * 4), (cuuint64_t)(pitch * w * 4), (cuuint64_t)(pitch * w * h * 4)};
     cuuint32_t box[4] = {(cuuint32_t)bc, (cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)bnn};
     cuuint32_t es[4] = {1, (cuuint32_t)ew, (cuuint32_t)eh, 1};
     CUresult r = nncb::drv::table().tensorMapEncodeTiled(
@@ -418,8 +419,56 @@ int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const Tc
 
 namespace nncb {
 
+int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t lda, const float* b,
+                 const float* bias, float* out, bool* handled);
+
+__global__ void im2col_k(const float* __restrict__ x, float* __restrict__ cols, nncb_gemm_desc g, int64_t K,
+                         int64_t ldk) {
+    // cols[p, k], p = (n, oh, ow), k = (dh, dw, c); zero where the tap is padding
+    int64_t total = g.n * g.oh * g.ow * ldk;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t k = t % ldk, p = t / ldk;
+        float v = 0.f;
+        if (k < K) {
+            int64_t c = k % g.ci, tap = k / g.ci, dw = tap % g.kw, dh = tap / g.kw;
+            int64_t ow = p % g.ow, r = p / g.ow, oh = r % g.oh, n = r / g.oh;
+            int64_t h = oh * g.sh + dh - g.pad_top, w = ow * g.sw + dw - g.pad_left;
+            if (h >= 0 && h < g.ih && w >= 0 && w < g.iw) v = __ldg(x + ((n * g.ih + h) * g.iw + w) * g.ci + c);
+        }
+        cols[t] = v;
+    }
+}
+
 int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const float* bias, float* out,
             bool* handled) {
+    *handled = false;
+    const bool conv = d->kind >= NNCB_CONV_FWD;
+    if (conv && d->ci % 32 != 0 && (d->kind == NNCB_CONV_FWD || d->kind == NNCB_CONV_WGRAD) && drv::table().ok) {
+        // Channels that do not fill a 32-wide K block (the 3-channel stem): lower
+        // to a dense tensor-core GEMM over an im2col workspace [pixels, kh*kw*ci].
+        const int64_t K = d->kh * d->kw * d->ci, ldk = (K + 3) / 4 * 4;
+        const int64_t P = d->n * d->oh * d->ow;
+        if (d->co % 4 != 0 || d->co < 16) return 0;
+        float* cols = static_cast<float*>(workspace(ctx, sizeof(float) * P * ldk));
+        if (!cols) return fail("im2col: workspace allocation failed");
+        im2col_k<<<grid_for(ctx, P * ldk, 256), 256, 0, ctx->stream>>>(a, cols, *d, K, ldk);
+        NNCB_LAUNCHED(ctx);
+        nncb_gemm_desc dd{};
+        dd.kind = d->kind == NNCB_CONV_FWD ? NNCB_DENSE_FWD : NNCB_DENSE_WGRAD;
+        dd.precision = d->precision;
+        dd.epilogue = d->epilogue;
+        dd.batch = P;
+        dd.in_f = K;
+        dd.out_f = d->co;
+        int rc = gemm_tc_impl(ctx, &dd, cols, ldk, b, bias, out, handled);
+        if (!rc && !*handled) return fail("im2col route: dense GEMM rejected");
+        return rc;
+    }
+    return gemm_tc_impl(ctx, d, a, 0, b, bias, out, handled);
+}
+
+int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t lda, const float* b,
+                 const float* bias, float* out, bool* handled) {
     *handled = false;
     if (!drv::table().ok) return 0;
     static const int dbg = getenv("NNCB_TC_DEBUG") ? 1 : 0;
@@ -432,10 +481,15 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
     int64_t oh = dense ? 1 : d->oh, ow = dense ? 1 : d->ow, pt = dense ? 0 : d->pad_top, pl = dense ? 0 : d->pad_left;
     const int kind = dense ? (d->kind == NNCB_DENSE_FWD ? 0 : d->kind == NNCB_DENSE_DGRAD ? 1 : 2)
                            : (d->kind == NNCB_CONV_FWD ? 0 : d->kind == NNCB_CONV_DGRAD ? 1 : 2);
-    // Requirements of the TMA path: 32-channel K blocks, 16-byte row pitches,
-    // taps fit the parameter block, int32 coordinates.
-    if (ci % 32 != 0 || co % 4 != 0 || co < 16 || kh * kw > MAX_TAPS) return 0;
-    if (kind == 1 && (co % 32 != 0 || sh > 2 || sw > 2)) return 0;
+    // Requirements of the TMA path: 32-channel K blocks for multi-tap convs
+    // (single-tap contractions take a ragged last block, zero-filled by TMA),
+    // 16-byte row pitches, taps fit the parameter block, int32 coordinates.
+    const bool single_tap = kh * kw == 1;
+    if (lda == 0) lda = ci;
+    if (co % 4 != 0 || co < 16 || kh * kw > MAX_TAPS || lda % 4 != 0) return 0;
+    if (!single_tap && ci % 32 != 0) return 0;
+    if (single_tap && ci % 4 != 0 && lda == ci) return 0;
+    if (kind == 1 && ((!single_tap && co % 32 != 0) || sh > 2 || sw > 2)) return 0;
     if (n * std::max(ih, oh) * std::max(iw, ow) * std::max(ci, co) >= (int64_t(1) << 31) * 4) return 0;
 
     TcParams P;
@@ -450,7 +504,7 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
         P.bn = pick_bn(Nc);
         P.N = Nc;
         P.ldc = Nc;
-        P.cblocks = static_cast<int>(Ck / 32);
+        P.cblocks = static_cast<int>((Ck + 31) / 32);
         if (fwd) {
             P.gn = (int)n; P.gh = (int)oh; P.gw = (int)ow;
             P.out_h = (int)oh; P.out_w = (int)ow; P.out_s = 1;
@@ -498,7 +552,7 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
         // A: the activation (x for fwd, g for dgrad) as {C, W, H, N}
         const float* act = a;
         if (fwd) {
-            if (!encode_4d(&ma, act, ci, iw, ih, n, 32, P.TW * (int)sw, P.TH * (int)sh, P.TN, (int)sw, (int)sh, false))
+            if (!encode_4d(&ma, act, ci, iw, ih, n, 32, P.TW * (int)sw, P.TH * (int)sh, P.TN, (int)sw, (int)sh, false, lda))
                 return 1;
         } else {
             if (!encode_4d(&ma, act, co, ow, oh, n, 32, P.TW, P.TH, P.TN, 1, 1, false)) return 1;
@@ -540,7 +594,8 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
     splits = std::max<int64_t>(1, std::min<int64_t>(splits, std::max<int64_t>(kboxes / 8, 1)));
     splits = std::min<int64_t>(splits, 128);
     P.splits = static_cast<int>(splits);
-    if (!encode_4d(&ma, a, ci, iw, ih, n, 32, P.TW * (int)sw, P.TH * (int)sh, P.TN, (int)sw, (int)sh, true)) return 1;
+    if (!encode_4d(&ma, a, ci, iw, ih, n, 32, P.TW * (int)sw, P.TH * (int)sh, P.TN, (int)sw, (int)sh, true, lda))
+        return 1;
     if (!encode_4d(&mb, b, co, ow, oh, n, 32, P.TW, P.TH, P.TN, 1, 1, true)) return 1;
     P.out = out;
     if (P.splits > 1) {

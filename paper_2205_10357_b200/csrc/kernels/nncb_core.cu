@@ -29,6 +29,18 @@ void* scratch(nncb_ctx* ctx, size_t bytes) {
     return ctx->scratch;
 }
 
+void* workspace(nncb_ctx* ctx, size_t bytes) {
+    if (bytes <= ctx->workspace_bytes) return ctx->workspace;
+    if (ctx->workspace) ctx->retired.push_back(ctx->workspace);
+    if (cudaMalloc(&ctx->workspace, bytes) != cudaSuccess) {
+        ctx->workspace = nullptr;
+        ctx->workspace_bytes = 0;
+        return nullptr;
+    }
+    ctx->workspace_bytes = bytes;
+    return ctx->workspace;
+}
+
 }  // namespace nncb
 
 using nncb::fail;
@@ -67,6 +79,7 @@ int nncb_destroy(nncb_ctx* c) {
     }
     if (c->scratch) cudaFree(c->scratch);
     for (void* p : c->retired) cudaFree(p);
+    if (c->workspace) cudaFree(c->workspace);
     cudaStreamDestroy(c->stream);
     cudaStreamDestroy(c->comm_stream);
     delete c;

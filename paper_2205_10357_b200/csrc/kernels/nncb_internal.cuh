@@ -28,6 +28,8 @@ struct nncb_ctx {
     void* scratch = nullptr;
     size_t scratch_bytes = 0;
     std::vector<void*> retired;          // outgrown scratch kept alive (captured graphs may use it)
+    void* workspace = nullptr;           // im2col columns (separate from reduction scratch)
+    size_t workspace_bytes = 0;
 };
 
 namespace nncb {
@@ -61,6 +63,7 @@ inline unsigned grid_for(const nncb_ctx* ctx, int64_t work_items, int threads, i
 }
 
 void* scratch(nncb_ctx* ctx, size_t bytes);
+void* workspace(nncb_ctx* ctx, size_t bytes);
 void ew_release(nncb_ew_kernel* k);
 
 // GEMM back ends (gemm_simt.cu / gemm_tc.cu)

@@ -37,6 +37,7 @@ def check(tc, ex):
 
 
 CONVS = [
+    (2, 32, 32, 3, 64, 7, 2), (2, 16, 16, 16, 32, 3, 1),
     (2, 14, 14, 64, 64, 3, 1), (2, 13, 11, 64, 96, 3, 2), (4, 7, 7, 128, 256, 1, 1),
     (2, 16, 16, 32, 64, 1, 2), (1, 9, 9, 64, 32, 3, 2), (3, 8, 8, 96, 128, 3, 1),
 ]
@@ -76,7 +77,7 @@ def test_conv_wgrad(shape):
     check(tc, ex)
 
 
-@pytest.mark.parametrize("b,i,o", [(32, 2048, 64), (256, 2048, 1000), (200, 96, 160), (64, 128, 16)])
+@pytest.mark.parametrize("b,i,o", [(32, 2048, 64), (256, 2048, 1000), (200, 96, 160), (64, 128, 16), (300, 148, 64)])
 def test_dense(b, i, o):
     rng = np.random.default_rng(3)
     x = rng.uniform(-1, 1, (b, i)).astype(np.float32)
