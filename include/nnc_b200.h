@@ -28,6 +28,7 @@ extern "C" {
 typedef struct nnc_model nnc_model;
 
 const char* nnc_last_error(void);
+int         nnc_last_status(void);   /* status of the last failed call (for NULL-returning calls) */
 
 /* Parse + optimize + derive versions + compile plans. gemm_precision:
  * 0 = tcgen05 tf32 (default), 1 = exact fp32 (bit-exact with the reference). */

@@ -56,6 +56,7 @@ def _load():
                        ctypes.POINTER(ctypes.c_double), ctypes.c_char_p)
     sig = {
         "nnc_last_error": (S, []),
+        "nnc_last_status": (I, []),
         "nnc_model_compile": (P, [S, I]),
         "nnc_model_free": (None, [P]),
         "nnc_model_describe": (S, [P]),
@@ -115,7 +116,7 @@ def group_document(document: str, assignment: Optional[Dict[str, int]] = None):
     res = _host.nnc_group_document(document.encode(),
                                    json.dumps(assignment).encode() if assignment is not None else None)
     if res is None:
-        raise NNCError(100, _host.nnc_last_error().decode())
+        raise NNCError(_host.nnc_last_status(), _host.nnc_last_error().decode())
     return json.loads(res.decode())
 
 
@@ -126,7 +127,7 @@ class CompiledModel:
     def __init__(self, document: str, precision: int = PREC_TF32):
         h = _host.nnc_model_compile(document.encode(), precision)
         if not h:
-            raise NNCError(100, _host.nnc_last_error().decode())
+            raise NNCError(_host.nnc_last_status(), _host.nnc_last_error().decode())
         self._h = h
         self.describe = json.loads(_host.nnc_model_describe(h).decode())
         self.weight_shapes = {k: tuple(v) for k, v in self.describe["weights"].items()}

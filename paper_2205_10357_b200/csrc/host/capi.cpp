@@ -34,18 +34,19 @@ namespace {
 
 thread_local std::string g_err;
 thread_local std::string g_buf;
+thread_local int g_status = 0;
 
 template <class F>
 int guarded(F&& f) {
     try {
         f();
-        return 0;
+        return g_status = 0;
     } catch (const Error& e) {
         g_err = e.what();
-        return 1 + static_cast<int>(e.code());
+        return g_status = 1 + static_cast<int>(e.code());
     } catch (const std::exception& e) {
         g_err = e.what();
-        return 100;
+        return g_status = 100;
     }
 }
 
@@ -108,6 +109,7 @@ Tensor target_tensor(nnc_model* m, const float* target, int64_t n) {
 extern "C" {
 
 const char* nnc_last_error(void) { return g_err.c_str(); }
+int nnc_last_status(void) { return g_status; }
 
 nnc_model* nnc_model_compile(const char* doc, int precision) {
     auto m = std::make_unique<nnc_model>();

@@ -16,6 +16,8 @@
 
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <set>
 #include <sstream>
 
 #include "driver_api.cuh"
@@ -180,6 +182,12 @@ int nncb_ew_compile_check(const nncb_ew_program* p) {
     bool uses_ch = false;
     for (int k = 0; k < p->n_instr; ++k) uses_ch = uses_ch || p->instr[k].op == NNCB_EW_LOAD_CH;
     std::string src = generate(*p, uses_ch);
+    static std::mutex mu;
+    static std::set<std::string> checked;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        if (checked.count(src)) return 0;
+    }
     nvrtcProgram prog = nullptr;
     nvrtcResult r = nvrtcCreateProgram(&prog, src.c_str(), "nnc_fused_ew.cu", 0, nullptr, nullptr);
     if (r != NVRTC_SUCCESS) return nvrtc_fail(prog, r, src);
@@ -187,6 +195,8 @@ int nncb_ew_compile_check(const nncb_ew_program* p) {
     r = nvrtcCompileProgram(prog, 4, opts);
     if (r != NVRTC_SUCCESS) return nvrtc_fail(prog, r, src);
     nvrtcDestroyProgram(&prog);
+    std::lock_guard<std::mutex> lock(mu);
+    checked.insert(src);
     return 0;
 }
 

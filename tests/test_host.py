@@ -1,0 +1,121 @@
+"""CPU tests of the host side and the C-ABI boundary (no GPU needed):
+libraries load and export every symbol the headers declare; the partitioner
+reproduces the reference's group_layers; plans lower fused chains to single
+kernels with register-resident interiors; generated kernels compile for
+sm_100a; data errors map to the reference's Error codes."""
+import json
+import os
+import re
+import subprocess
+
+import pytest
+
+import paper_2205_10357_b200 as P
+from paper_2205_10357_b200 import workloads as W
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared(header):
+    src = open(os.path.join(ROOT, "include", header)).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(nncb?_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.mark.parametrize("header,lib", [("nncb.h", P.KERNEL_LIB), ("nnc_b200.h", P.HOST_LIB)])
+def test_abi_exports_every_declared_symbol(header, lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", lib], capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r" T (\w+)", out))
+    missing = [s for s in declared(header) if s not in exported]
+    assert not missing, missing
+
+
+DOCS = {
+    "c1": lambda: W.c1_small_cnn(4, bn=False),
+    "resnet50": lambda: W.resnet50(1, bn=False, image=64),
+    "chain": lambda: W.c2_chain((2, 4, 4, 8), "ref"),
+}
+
+
+@pytest.mark.parametrize("name", sorted(DOCS))
+@pytest.mark.parametrize("policy", [0, 1])
+def test_partition_matches_reference(ref, name, policy):
+    """policy 1: the B200 assignment encoded in reference backends (Conv2D/Dense
+    -> GEMM_TILED, rest -> REF); policy 0: the reference default_assignment
+    (three backends) fed to our group_layers as raw backend ints."""
+    doc = DOCS[name]()
+    rg = [g["members"] for g in ref.group_document(doc, policy)]
+    if policy == 1:
+        mine = P.group_document(doc)
+    else:
+        r = ref.RefModel(doc, 0)
+        assign = {}
+        for g in r.describe["inference"]["groups"]:
+            b = {"ref": 0, "fused_ew": 1, "gemm_tiled": 2}[g["backend"]]
+            for mm in g["members"]:
+                assign[mm] = b
+        mine = P.group_document(doc, assign)
+    assert mine == rg
+
+
+@pytest.mark.parametrize("name", sorted(DOCS))
+def test_versions_match_reference(ref, name):
+    doc = DOCS[name]()
+    mine = P.CompiledModel(doc).describe
+    r = ref.RefModel(doc, 1).describe
+    assert mine["save_set"] == r["save_set"]
+    assert mine["output_grads"] == r["output_grads"]
+    assert mine["weight_grads"] == r["weight_grads"]
+    # forward plans: same value table names/categories in the same order
+    for role in ("inference", "train_fwd"):
+        a = [(v["name"], v["category"], v["resident"]) for v in mine[role]["values"]]
+        b = [(v["name"], v["category"], v["resident"]) for v in r[role]["values"] if not v["name"].endswith(".im2col")]
+        assert a == b, role
+
+
+def test_fused_chain_register_interiors(known_answers=None):
+    """reference test_backends.cpp:246-276: a fused ReLU/Mul/Add chain
+    materializes 0 intermediate buffers and keeps 2 values in registers."""
+    doc = json.dumps({"dialect": "dlb", "name": "chain", "inputs": [{"name": "x", "shape": [6]},
+                                                                      {"name": "y", "shape": [6]}],
+                      "outputs": ["a"], "nodes": [{"name": "r", "op": "relu", "inputs": ["x"]},
+                                                  {"name": "m", "op": "mul", "inputs": ["r", "y"]},
+                                                  {"name": "a", "op": "add", "inputs": ["m", "x"]}]})
+    p = P.CompiledModel(doc).describe["inference"]
+    assert len(p["groups"]) == 1 and len(p["groups"][0]["launches"]) == 1
+    inter = [v for v in p["values"] if v["category"] == "intermediate" and v["storage"] == "buffer"]
+    regs = [v for v in p["values"] if v["storage"] == "register"]
+    assert not inter and len(regs) == 2
+
+
+def test_c2_chain_is_one_kernel_per_bn_barrier():
+    d = P.CompiledModel(W.c2_chain((2, 4, 4, 8), "ref")).describe
+    assert d["inference"]["launch_count"] == 1
+    d = P.CompiledModel(W.c2_chain((2, 4, 4, 8), "bn")).describe
+    kinds = [l["kind"] for g in d["train_fwd"]["groups"] for l in g["launches"]]
+    # 4 BatchNorm statistics barriers, each followed by one fused pass
+    assert kinds.count("bn_stats") == 4 and kinds.count("ew") == 4
+
+
+@pytest.mark.parametrize("doc", [W.c1_small_cnn(2, bn=True), W.mlp(4, 64, 2), W.resnet50(1, bn=True, image=32),
+                                 W.c2_chain((2, 4, 4, 8), "bn")], ids=["c1_bn", "mlp", "resnet50_bn", "c2_bn"])
+def test_generated_kernels_compile_for_sm100a(doc):
+    P.CompiledModel(doc).check_kernels()
+
+
+def test_error_codes_follow_reference():
+    with pytest.raises(P.NNCError) as e:
+        P.CompiledModel(json.dumps({"dialect": "dlb", "inputs": [{"name": "x", "shape": [2, 3]}],
+                                    "outputs": ["s"], "nodes": [{"name": "s", "op": "softplus", "inputs": ["x"]}]}))
+    assert "UnknownOp" in str(e.value)
+    with pytest.raises(P.NNCError) as e:
+        P.CompiledModel(json.dumps({"dialect": "dlb", "inputs": [{"name": "x", "shape": [2, 3]}],
+                                    "outputs": ["c"], "nodes": [{"name": "c", "op": "conv2d", "inputs": ["x"],
+                                                                 "attrs": {"filters": 2, "kernel_size": 1}}]}))
+    assert "BadDocument" in str(e.value) or "RankError" in str(e.value)
+
+
+def test_peak_estimate_counts_registers_as_zero():
+    d = P.CompiledModel(W.c2_chain((2, 4, 4, 8), "ref")).describe
+    # inputs x,y + output only; the 15 chain interiors live in registers
+    assert d["peak"]["inference"] == 3 * 2 * 4 * 4 * 8 * 4
