@@ -129,6 +129,7 @@ void nnc_model_free(nnc_model* m) {
     try {
         m->trainer.reset();
         runtime::release(m->plans);
+        runtime::default_device().evict_model(*m->host);
     } catch (...) {
     }
     delete m;

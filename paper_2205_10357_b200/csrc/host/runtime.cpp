@@ -402,7 +402,7 @@ const Tensor& HostModel::tensor(const std::string& name) const {
     auto it = weights_.find(name);
     if (it == weights_.end()) throw Error(Error::Code::ShapeMismatch, "model has no weight " + name);
     if (device_owner && device_newer.count(name)) {
-        device_owner->pull_weight(name, it->second);
+        device_owner->pull_weight(*this, name, it->second);
         device_newer.erase(name);
     }
     return it->second;
@@ -452,15 +452,16 @@ void Device::init_comm(int nranks, int rank, const uint8_t id[128]) {
     rank_ = rank;
 }
 
-void* Device::weight_buffer(const std::string& name, const Tensor& host, uint64_t stamp) {
-    auto it = cache_.find(name);
+void* Device::weight_buffer(const HostModel& m, const std::string& name, const Tensor& host, uint64_t stamp) {
+    auto key = std::make_pair(m.uid(), name);
+    auto it = cache_.find(key);
     size_t bytes = host.byte_size();
     if (it == cache_.end()) {
         CachedWeight cw;
         cw.bytes = bytes;
         NNC_CHECK(nncb_malloc(ctx_, std::max<size_t>(bytes, 4), &cw.ptr));
         cw.stamp = stamp + 1;  // force upload below
-        it = cache_.emplace(name, cw).first;
+        it = cache_.emplace(key, cw).first;
     }
     CachedWeight& cw = it->second;
     if (cw.bytes != bytes) throw Error(Error::Code::ShapeMismatch, name + ": stored weight does not match plan");
@@ -474,32 +475,46 @@ void* Device::weight_buffer(const std::string& name, const Tensor& host, uint64_
     return cw.ptr;
 }
 
-void* Device::weight_ptr(const std::string& name) const {
-    auto it = cache_.find(name);
+void* Device::weight_ptr(const HostModel& m, const std::string& name) const {
+    auto it = cache_.find({m.uid(), name});
     return it == cache_.end() ? nullptr : it->second.ptr;
 }
 
-void Device::pull_weight(const std::string& name, Tensor& host) {
-    void* p = weight_ptr(name);
+void Device::pull_weight(const HostModel& m, const std::string& name, Tensor& host) {
+    void* p = weight_ptr(m, name);
     if (!p) return;
     NNC_CHECK(nncb_d2h(ctx_, host.data(), p, host.byte_size()));
     NNC_CHECK(nncb_sync(ctx_));
     stats_.d2h_bytes += host.byte_size();
 }
 
-void Device::adopt_weight(const std::string& name, void* ptr, size_t bytes, uint64_t stamp) {
-    auto it = cache_.find(name);
+void Device::adopt_weight(const HostModel& m, const std::string& name, void* ptr, size_t bytes, uint64_t stamp) {
+    auto key = std::make_pair(m.uid(), name);
+    auto it = cache_.find(key);
     if (it != cache_.end() && !it->second.external && it->second.ptr) nncb_free(ctx_, it->second.ptr);
-    cache_[name] = CachedWeight{ptr, bytes, stamp, true};
+    cache_[key] = CachedWeight{ptr, bytes, stamp, true};
 }
 
-uint64_t Device::cached_stamp(const std::string& name) const {
-    auto it = cache_.find(name);
+void Device::evict_model(HostModel& m) {
+    for (const std::string& name : std::vector<std::string>(m.device_newer.begin(), m.device_newer.end()))
+        (void)m.tensor(name);   // pulls and clears device_newer
+    for (auto it = cache_.begin(); it != cache_.end();) {
+        if (it->first.first != m.uid()) {
+            ++it;
+            continue;
+        }
+        if (!it->second.external && it->second.ptr) nncb_free(ctx_, it->second.ptr);
+        it = cache_.erase(it);
+    }
+}
+
+uint64_t Device::cached_stamp(const HostModel& m, const std::string& name) const {
+    auto it = cache_.find({m.uid(), name});
     return it == cache_.end() ? ~0ull : it->second.stamp;
 }
 
 void Device::mark_device_newer(HostModel& m, const std::string& name, uint64_t new_stamp) {
-    auto it = cache_.find(name);
+    auto it = cache_.find({m.uid(), name});
     if (it != cache_.end()) it->second.stamp = new_stamp;
     m.device_owner = this;
     m.device_newer.insert(name);
@@ -561,7 +576,7 @@ std::map<std::string, Tensor> execute(const ExecutionPlan& p, const std::map<std
     auto& slot = exec_caches()[{&dev, p.uid}];
     // weights: stamp-checked device cache (uploads only stale tensors)
     std::map<std::string, void*> wptrs;
-    for (const std::string& w : p.weight_names) wptrs[w] = dev.weight_buffer(w, model.tensor(w), model.stamp(w));
+    for (const std::string& w : p.weight_names) wptrs[w] = dev.weight_buffer(model, w, model.tensor(w), model.stamp(w));
     if (!slot || slot->weight_ptrs != wptrs || slot->prog->precision != opts.gemm_precision) {
         slot = std::make_unique<ExecCache>();
         slot->prog = std::make_unique<Program>();
@@ -679,6 +694,10 @@ struct Trainer::Impl {
     bool warmed = false;
 
     ~Impl() {
+        try {
+            dev->evict_model(*model);   // device-newer weights back to the host before the region goes
+        } catch (...) {
+        }
         if (graph) nncb_graph_destroy(graph);
         if (graph_nosgd) nncb_graph_destroy(graph_nosgd);
         nncb_ctx* ctx = dev->ctx();
@@ -703,8 +722,8 @@ struct Trainer::Impl {
     void sync_params() {
         // host-side edits (HostModel::set) since the last step: re-upload in place
         for (const std::string& w : weights)
-            if (!model->device_newer.count(w) && dev->cached_stamp(w) != model->stamp(w))
-                dev->weight_buffer(w, model->tensor(w), model->stamp(w));
+            if (!model->device_newer.count(w) && dev->cached_stamp(*model, w) != model->stamp(w))
+                dev->weight_buffer(*model, w, model->tensor(w), model->stamp(w));
     }
 
     void run(double lr, bool do_sgd) {
@@ -787,7 +806,7 @@ Trainer::Trainer(const plan::VersionPlans& plans, HostModel& model, Device& dev,
         NNC_CHECK(nncb_h2d(ctx, home, t.data(), t.byte_size()));
         dev.stats().h2d_bytes += t.byte_size();
         dev.stats().weight_bytes += t.byte_size();
-        dev.adopt_weight(w, home, t.byte_size(), model.stamp(w));
+        dev.adopt_weight(model, w, home, t.byte_size(), model.stamp(w));
     }
     // buckets of ~32 MB over the trainable prefix of the region
     int64_t trainable_end = 0;

@@ -87,13 +87,16 @@ public:
     int rank() const { return rank_; }
 
     // --- internals used by execute/train_step -------------------------
-    void* weight_buffer(const std::string& name, const Tensor& host, uint64_t stamp);
-    void* weight_ptr(const std::string& name) const;
-    void pull_weight(const std::string& name, Tensor& host);
+    // The cache is keyed by (HostModel uid, weight name): two models never share entries.
+    void* weight_buffer(const HostModel& m, const std::string& name, const Tensor& host, uint64_t stamp);
+    void* weight_ptr(const HostModel& m, const std::string& name) const;
+    void pull_weight(const HostModel& m, const std::string& name, Tensor& host);
     void mark_device_newer(HostModel& m, const std::string& name, uint64_t new_stamp);
     /// Makes `ptr` (a trainer's flat parameter region) the device home of a weight.
-    void adopt_weight(const std::string& name, void* ptr, size_t bytes, uint64_t stamp);
-    uint64_t cached_stamp(const std::string& name) const;
+    void adopt_weight(const HostModel& m, const std::string& name, void* ptr, size_t bytes, uint64_t stamp);
+    /// Pulls device-newer weights of `m` back to the host and drops its cache entries.
+    void evict_model(HostModel& m);
+    uint64_t cached_stamp(const HostModel& m, const std::string& name) const;
     std::map<const void*, std::unique_ptr<Program>>& programs() { return programs_; }
     SyncStats& stats() { return stats_; }
 
@@ -105,7 +108,7 @@ private:
         bool external = false;
     };
     nncb_ctx* ctx_ = nullptr;
-    std::map<std::string, CachedWeight> cache_;
+    std::map<std::pair<uint64_t, std::string>, CachedWeight> cache_;
     std::map<const void*, std::unique_ptr<Program>> programs_;
     SyncStats stats_;
     int nranks_ = 1, rank_ = 0;

@@ -40,9 +40,11 @@ int fail(const std::string& msg);
 #define NNCB_CUDA(expr)                                                                       \
     do {                                                                                      \
         cudaError_t _e = (expr);                                                              \
-        if (_e != cudaSuccess)                                                                \
+        if (_e != cudaSuccess) {                                                              \
+            cudaGetLastError(); /* clear non-sticky errors so later calls report their own */ \
             return ::nncb::fail(std::string(#expr) + ": " + cudaGetErrorString(_e) + " (" +   \
                                 __FILE__ + ":" + std::to_string(__LINE__) + ")");            \
+        }                                                                                     \
     } while (0)
 
 #define NNCB_LAUNCHED(ctx)                                                                    \

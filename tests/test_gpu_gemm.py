@@ -25,7 +25,7 @@ def run_both(kind, geo, a, b, bias, out_shape):
     for prec in (0, 1):
         d = GemmDesc(kind=kind, precision=prec, epilogue=1 if bias is not None else 0, **geo)
         o = Dev(nbytes=int(np.prod(out_shape)) * 4)
-        gemm(d, a, b, bias, o)
+        gemm(d, a, b, bias, o)   # a, b, bias are held by the caller
         outs.append(o.get(out_shape))
     return outs
 

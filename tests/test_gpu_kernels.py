@@ -1,0 +1,138 @@
+"""Kernel-level known answers and bit-exactness through the thin C-ABI (nncb.h):
+the reference's hand-computed answers (tests/golden/known_answers.json) and the
+restated oracle on random data, including max-pool ties."""
+import ctypes
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import restated as O
+from tests.nncb_ctypes import K, Dev, ctx
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+class PoolGeom(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in ("n", "ih", "iw", "c", "kh", "kw", "sh", "sw", "oh", "ow")]
+
+
+for name, args in [("nncb_maxpool_fwd", [ctypes.c_void_p, ctypes.POINTER(PoolGeom)] + [ctypes.c_void_p] * 3),
+                   ("nncb_maxpool_bwd", [ctypes.c_void_p, ctypes.POINTER(PoolGeom)] + [ctypes.c_void_p] * 3),
+                   ("nncb_l1_loss", [ctypes.c_void_p] * 5 + [ctypes.c_int64]),
+                   ("nncb_sgd", [ctypes.c_void_p] * 3 + [ctypes.c_int64, ctypes.c_double, ctypes.c_double]),
+                   ("nncb_bn_stats", [ctypes.c_void_p] * 3 + [ctypes.c_int64, ctypes.c_int64, ctypes.c_double]),
+                   ("nncb_layernorm_fwd", [ctypes.c_void_p] * 5 + [ctypes.c_int64, ctypes.c_int64, ctypes.c_double]),
+                   ("nncb_avgpool_fwd", [ctypes.c_void_p] + [ctypes.c_int64] * 6 + [ctypes.c_void_p] * 2)]:
+    fn = getattr(K, name)
+    fn.restype, fn.argtypes = ctypes.c_int, args
+
+
+def ok(rc):
+    assert rc == 0, K.nncb_last_error().decode()
+    assert K.nncb_sync(ctx()) == 0
+
+
+@pytest.fixture(scope="module")
+def known():
+    with open(os.path.join(GOLD, "known_answers.json")) as f:
+        return json.load(f)
+
+
+def pool(x, k, s, ties=False):
+    n, ih, iw, c = x.shape
+    oh, ow = (ih - k) // s + 1, (iw - k) // s + 1
+    return PoolGeom(n, ih, iw, c, k, k, s, s, oh, ow), (n, oh, ow, c)
+
+
+def test_maxpool_tie_and_grad_known_answer(known):
+    k = known["maxpool_tie"]
+    x = np.array(k["x"], np.float32).reshape(1, 1, 2, 1)
+    g = PoolGeom(1, 1, 2, 1, 1, 2, 1, 1, 1, 1)
+    y, idx, xd = Dev(nbytes=4), Dev(nbytes=4), Dev(x)
+    ok(K.nncb_maxpool_fwd(ctx(), ctypes.byref(g), xd.p, y.p, idx.p))
+    assert idx.get((1,))[0] == k["argmax"]
+    gx, gy = Dev(nbytes=8), Dev(np.array([k["upstream"]], np.float32))
+    ok(K.nncb_maxpool_bwd(ctx(), ctypes.byref(g), idx.p, gy.p, gx.p))
+    assert gx.get((2,)).tolist() == k["gx"]
+
+
+@pytest.mark.parametrize("k,s", [(2, 2), (3, 2), (3, 1)])
+def test_maxpool_bitexact_with_ties(k, s):
+    rng = np.random.default_rng(k * 10 + s)
+    x = rng.integers(-3, 4, (2, 9, 11, 8)).astype(np.float32)   # many exact ties
+    g, oshape = pool(x, k, s)
+    y, idx, xd = Dev(nbytes=4 * int(np.prod(oshape))), Dev(nbytes=4 * int(np.prod(oshape))), Dev(x)
+    ok(K.nncb_maxpool_fwd(ctx(), ctypes.byref(g), xd.p, y.p, idx.p))
+    pp, _ = O.pool_params(x.shape, (k, k), (s, s))
+    oy, oidx = np.zeros(oshape, np.float32), np.zeros(oshape, np.float32)
+    O.lib().o_maxpool2d(O._f(x), O._f(oy), O._f(oidx), pp)
+    assert np.array_equal(y.get(oshape), oy) and np.array_equal(idx.get(oshape), oidx)
+    gy = rng.uniform(-1, 1, oshape).astype(np.float32)
+    gx, gyd = Dev(nbytes=x.nbytes), Dev(gy)
+    ok(K.nncb_maxpool_bwd(ctx(), ctypes.byref(g), idx.p, gyd.p, gx.p))
+    ogx = np.zeros(x.shape, np.float32)
+    O.lib().o_maxpool2d_grad(O._f(oidx), O._f(gy), O._f(ogx), pp)
+    assert np.array_equal(gx.get(x.shape), ogx)
+
+
+def test_global_avgpool_bitexact():
+    x = np.random.default_rng(3).uniform(-1, 1, (3, 7, 7, 64)).astype(np.float32)
+    y, xd = Dev(nbytes=3 * 64 * 4), Dev(x)
+    ok(K.nncb_avgpool_fwd(ctx(), 3, 7, 7, 64, 1, 1, xd.p, y.p))
+    oy = np.zeros((3, 1, 1, 64), np.float32)
+    O.lib().o_avgpool(O._f(x), O._f(oy), *[O.I64(v) for v in (3, 7, 7, 64, 1, 1)])
+    assert np.array_equal(y.get((3, 1, 1, 64)), oy)
+
+
+def test_l1_and_sgd_known_answers(known):
+    k = known["l1"]
+    grad, loss = Dev(nbytes=4), Dev(nbytes=8)
+    pd, td = Dev(np.array([k["p"]], np.float32)), Dev(np.array([k["t"]], np.float32))
+    ok(K.nncb_l1_loss(ctx(), pd.p, td.p, grad.p, loss.p, 1))
+    assert grad.get((1,))[0] == k["grad"]
+    assert np.frombuffer(loss.get((2,)).tobytes(), np.float64)[0] == k["loss"]
+    k = known["sgd"]
+    w, gd = Dev(np.array([k["w"]], np.float32)), Dev(np.array([k["g"]], np.float32))
+    ok(K.nncb_sgd(ctx(), w.p, gd.p, 1, k["lr"], 1.0))
+    assert w.get((1,))[0] == k["w_after"]
+
+
+def test_l1_and_sgd_bitexact_random():
+    rng = np.random.default_rng(5)
+    p, t = rng.uniform(-2, 2, 4099).astype(np.float32), rng.uniform(-2, 2, 4099).astype(np.float32)
+    t[::7] = p[::7]     # zero differences -> sign(0) = 0
+    grad, loss, pd, td = Dev(nbytes=p.nbytes), Dev(nbytes=8), Dev(p), Dev(t)
+    ok(K.nncb_l1_loss(ctx(), pd.p, td.p, grad.p, loss.p, p.size))
+    og = np.zeros_like(p)
+    ol = O.lib().o_l1_loss(O._f(p), O._f(t), O._f(og), O.I64(p.size))
+    assert np.array_equal(grad.get(p.shape), og)
+    assert abs(np.frombuffer(loss.get((2,)).tobytes(), np.float64)[0] - ol) <= 1e-12 * ol
+    w, g = rng.uniform(-1, 1, 4099).astype(np.float32), rng.uniform(-1, 1, 4099).astype(np.float32)
+    wd, gd = Dev(w), Dev(g)
+    ok(K.nncb_sgd(ctx(), wd.p, gd.p, w.size, 0.0123, 1.0))
+    ow = w.copy()
+    O.lib().o_sgd(O._f(ow), O._f(g), O.I64(w.size), ctypes.c_double(0.0123))
+    assert np.array_equal(wd.get(w.shape), ow)
+
+
+def test_batchnorm_statistics_vs_oracle():
+    x = np.random.default_rng(6).normal(0.3, 2.0, (4096, 96)).astype(np.float32)
+    st, xd = Dev(nbytes=2 * 96 * 4), Dev(x)
+    ok(K.nncb_bn_stats(ctx(), xd.p, st.p, 4096, 96, 1e-3))
+    ost = np.zeros((2, 96), np.float32)
+    O.lib().o_bn_stats(O._f(x), O._f(ost), O.I64(4096), O.I64(96), ctypes.c_double(1e-3))
+    assert np.max(np.abs(st.get((2, 96)) - ost) / np.abs(ost)) < 1e-6
+
+
+def test_layernorm_forward_vs_oracle():
+    rng = np.random.default_rng(7)
+    x = rng.normal(0, 1.5, (64, 4096)).astype(np.float32)
+    ga, be = rng.uniform(0.5, 1.5, 4096).astype(np.float32), rng.uniform(-0.5, 0.5, 4096).astype(np.float32)
+    y, xd, gd, bd = Dev(nbytes=x.nbytes), Dev(x), Dev(ga), Dev(be)
+    ok(K.nncb_layernorm_fwd(ctx(), xd.p, gd.p, bd.p, y.p, 64, 4096, 1e-5))
+    oy = np.zeros_like(x)
+    O.lib().o_layernorm(O._f(x), O._f(ga), O._f(be), O._f(oy), O.I64(64), O.I64(4096), ctypes.c_double(1e-5))
+    assert np.max(np.abs(y.get(x.shape) - oy)) / np.max(np.abs(oy)) < 1e-6
