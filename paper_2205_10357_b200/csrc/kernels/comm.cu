@@ -4,15 +4,72 @@
 // buckets on a dedicated comm stream, ordered after the backward kernels that
 // produced each bucket (event fork/join with the compute stream, so the whole
 // pattern is capturable into the step's CUDA graph).
+// NCCL is loaded lazily (dlopen) when the first communicator is created, so
+// single-GPU processes never map it and a process that imports torch gets
+// torch's bundled NCCL (already loaded, or found next to torch) instead of a
+// second, older copy that would shadow torch's symbols.
+#include <dlfcn.h>
 #include <nccl.h>
+
+#include <cstdlib>
+#include <cstring>
 
 #include "nncb_internal.cuh"
 
+namespace {
+
+struct Nccl {
+    decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+    decltype(&ncclCommInitRank) commInitRank = nullptr;
+    decltype(&ncclCommDestroy) commDestroy = nullptr;
+    decltype(&ncclAllReduce) allReduce = nullptr;
+    decltype(&ncclGetErrorString) getErrorString = nullptr;
+    bool ok = false;
+    std::string where;
+};
+
+const Nccl& nccl() {
+    static Nccl n = [] {
+        Nccl r;
+        std::vector<std::string> candidates;
+        if (const char* env = std::getenv("NNCB_NCCL_LIB")) candidates.push_back(env);
+        candidates.push_back("libnccl.so.2");   // returns an already-loaded copy first
+        void* h = nullptr;
+        for (const auto& c : candidates) {
+            h = dlopen(c.c_str(), RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+            if (h) {
+                r.where = c + " (already loaded)";
+                break;
+            }
+        }
+        if (!h)
+            for (const auto& c : candidates) {
+                h = dlopen(c.c_str(), RTLD_NOW | RTLD_LOCAL);
+                if (h) {
+                    r.where = c;
+                    break;
+                }
+            }
+        if (!h) return r;
+        r.getUniqueId = reinterpret_cast<decltype(r.getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+        r.commInitRank = reinterpret_cast<decltype(r.commInitRank)>(dlsym(h, "ncclCommInitRank"));
+        r.commDestroy = reinterpret_cast<decltype(r.commDestroy)>(dlsym(h, "ncclCommDestroy"));
+        r.allReduce = reinterpret_cast<decltype(r.allReduce)>(dlsym(h, "ncclAllReduce"));
+        r.getErrorString = reinterpret_cast<decltype(r.getErrorString)>(dlsym(h, "ncclGetErrorString"));
+        r.ok = r.getUniqueId && r.commInitRank && r.commDestroy && r.allReduce && r.getErrorString;
+        return r;
+    }();
+    return n;
+}
+
+}  // namespace
+
 #define NNCB_NCCL(expr)                                                                     \
     do {                                                                                    \
+        if (!nccl().ok) return ::nncb::fail("NCCL library could not be loaded");           \
         ncclResult_t _r = (expr);                                                           \
         if (_r != ncclSuccess)                                                              \
-            return ::nncb::fail(std::string(#expr) + ": " + ncclGetErrorString(_r));       \
+            return ::nncb::fail(std::string(#expr) + ": " + nccl().getErrorString(_r));    \
     } while (0)
 
 extern "C" {
@@ -20,7 +77,7 @@ extern "C" {
 int nncb_comm_unique_id(uint8_t id[128]) {
     static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
     ncclUniqueId u;
-    NNCB_NCCL(ncclGetUniqueId(&u));
+    NNCB_NCCL(nccl().getUniqueId(&u));
     memcpy(id, &u, 128);
     return 0;
 }
@@ -31,7 +88,7 @@ int nncb_comm_init(nncb_ctx* ctx, int nranks, int rank, const uint8_t id[128]) {
     ncclUniqueId u;
     memcpy(&u, id, 128);
     ncclComm_t comm;
-    NNCB_NCCL(ncclCommInitRank(&comm, nranks, u, rank));
+    NNCB_NCCL(nccl().commInitRank(&comm, nranks, u, rank));
     ctx->nccl_comm = comm;
     ctx->nranks = nranks;
     ctx->rank = rank;
@@ -40,7 +97,7 @@ int nncb_comm_init(nncb_ctx* ctx, int nranks, int rank, const uint8_t id[128]) {
 
 int nncb_comm_destroy(nncb_ctx* ctx) {
     if (!ctx->nccl_comm) return 0;
-    ncclCommDestroy(static_cast<ncclComm_t>(ctx->nccl_comm));
+    if (nccl().ok) nccl().commDestroy(static_cast<ncclComm_t>(ctx->nccl_comm));
     ctx->nccl_comm = nullptr;
     return 0;
 }
@@ -53,8 +110,8 @@ int nncb_allreduce_sum(nncb_ctx* ctx, float* buf, int64_t count) {
     NNCB_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
     NNCB_CUDA(cudaEventRecord(ready, ctx->stream));
     NNCB_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ready, 0));
-    NNCB_NCCL(ncclAllReduce(buf, buf, static_cast<size_t>(count), ncclFloat32, ncclSum,
-                            static_cast<ncclComm_t>(ctx->nccl_comm), ctx->comm_stream));
+    NNCB_NCCL(nccl().allReduce(buf, buf, static_cast<size_t>(count), ncclFloat32, ncclSum,
+                               static_cast<ncclComm_t>(ctx->nccl_comm), ctx->comm_stream));
     NNCB_CUDA(cudaEventRecord(done, ctx->comm_stream));
     NNCB_CUDA(cudaStreamWaitEvent(ctx->stream, done, 0));
     cudaEventDestroy(ready);
