@@ -34,8 +34,8 @@ namespace {
 
 constexpr int BM = 128;       // UMMA_M (cta_group::1)
 constexpr int BK = 32;        // fp32 elements per K step = one 128-byte swizzle row
-constexpr int STAGES = 4;
-constexpr int THREADS = 192;
+constexpr int MAX_STAGES = 6;
+constexpr int THREADS = 320;   // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue (2 per TMEM lane quarter)
 constexpr int MAX_TAPS = 64;
 
 enum { MODE_CONV = 0, MODE_WGRAD = 1 };
@@ -66,6 +66,13 @@ struct TcParams {
     const float* bias;  // MODE_CONV forward only
     float* out;
     int debug;
+    // persistent tiling
+    int64_t tiles;      // total tiles (all phases / splits)
+    int64_t n_tiles;    // tiles along N
+    int64_t pix_tiles;  // MODE_CONV: pixel tiles per phase
+    int64_t m_tiles;    // MODE_WGRAD: tiles along M
+    int tma_store;      // epilogue through smem + TMA store (else direct stores)
+    int stages;         // smem ring depth (sized so 2 CTAs fit per SM when N is small)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -149,56 +156,56 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+            reinterpret_cast<uint64_t>(map)),
+        "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// Persistent warp-specialised GEMM. grid = min(tiles, #SMs); CTA b processes
+// tiles b, b + grid, ... The smem ring (TMA -> MMA) and the double-buffered TMEM
+// accumulator (MMA -> epilogue) carry their phases across tiles, so the
+// epilogue of one tile overlaps the main loop of the next.
 __global__ void __launch_bounds__(THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                   const __grid_constant__ TcParams P) {
+                   const __grid_constant__ CUtensorMap map_c, const __grid_constant__ TcParams P) {
+    const int STAGES = P.stages;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t a_bytes = BM * BK * 4;                 // 16 KB
     const uint32_t b_bytes = static_cast<uint32_t>(P.bn) * BK * 4;
     const uint32_t stage_bytes = a_bytes + b_bytes;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * stage_bytes);
+    uint8_t* staging = smem + STAGES * stage_bytes;       // 2 x 16 KB epilogue staging (TMA-store mode only)
+    uint64_t* full = reinterpret_cast<uint64_t*>(staging + (P.tma_store ? 2 * 16384 : 0));
     uint64_t* empty = full + STAGES;
-    uint64_t* tmem_full = empty + STAGES;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+    uint64_t* tmem_full = empty + STAGES;                 // [2]
+    uint64_t* tmem_empty = tmem_full + 2;                 // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-
-    // ---- tile coordinates --------------------------------------------------
-    int kb_begin = 0, kb_end = 0;
-    int phase = 0;
-    int64_t n_col0 = static_cast<int64_t>(blockIdx.y) * P.bn;
-    int tn0 = 0, th0 = 0, tw0 = 0;   // MODE_CONV tile origin (pixel grid)
-    int64_t m0 = 0;                  // MODE_WGRAD row origin
-    if (P.mode == MODE_CONV) {
-        phase = blockIdx.z;
-        int t = blockIdx.x;
-        int twi = t % P.tiles_w;
-        t /= P.tiles_w;
-        int thi = t % P.tiles_h;
-        int tni = t / P.tiles_h;
-        tn0 = tni * P.TN;
-        th0 = thi * P.TH;
-        tw0 = twi * P.TW;
-        kb_end = P.ntaps[phase] * P.cblocks;
-    } else {
-        m0 = static_cast<int64_t>(blockIdx.x) * BM;
-        int per = (P.kboxes + P.splits - 1) / P.splits;
-        kb_begin = blockIdx.z * per;
-        kb_end = min(P.kboxes, kb_begin + per);
-        if (kb_begin > kb_end) kb_begin = kb_end;
-    }
-    const int nk = kb_end - kb_begin;
-
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(tmem_full, 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&tmem_full[s], 1);
+            mbar_init(&tmem_empty[s], 8);                 // one arrival per epilogue warp
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    const uint32_t tmem_cols = P.bn < 32 ? 32 : static_cast<uint32_t>(P.bn);
+    const uint32_t tmem_cols = 2 * static_cast<uint32_t>(P.bn);   // two accumulators
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(tmem_cols));
@@ -209,125 +216,183 @@ __global__ void __launch_bounds__(THREADS, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem_base = *tmem_slot;
 
-    if (warp == 0 && lane == 0 && nk > 0) {
+    // ---- tile decode (identical in every role) ------------------------------
+    struct Tile {
+        int phase, tn0, th0, tw0, kb_begin, nk, split;
+        int64_t m0, n0;
+    };
+    auto decode = [&](int64_t t) {
+        Tile T{};
+        T.n0 = (t % P.n_tiles) * P.bn;
+        int64_t rest = t / P.n_tiles;
+        if (P.mode == MODE_CONV) {
+            int64_t pix = rest % P.pix_tiles;
+            T.phase = static_cast<int>(rest / P.pix_tiles);
+            int tw = static_cast<int>(pix % P.tiles_w);
+            pix /= P.tiles_w;
+            int th = static_cast<int>(pix % P.tiles_h);
+            int tn = static_cast<int>(pix / P.tiles_h);
+            T.tn0 = tn * P.TN;
+            T.th0 = th * P.TH;
+            T.tw0 = tw * P.TW;
+            T.kb_begin = 0;
+            T.nk = P.ntaps[T.phase] * P.cblocks;
+        } else {
+            T.m0 = (rest % P.m_tiles) * BM;
+            T.split = static_cast<int>(rest / P.m_tiles);
+            int per = (P.kboxes + P.splits - 1) / P.splits;
+            T.kb_begin = min(P.kboxes, T.split * per);
+            T.nk = min(P.kboxes, T.kb_begin + per) - T.kb_begin;
+        }
+        return T;
+    };
+
+    if (warp == 0 && lane == 0) {
         // ================= TMA producer =================
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
-        for (int i = 0; i < nk; ++i) {
-            const int s = i % STAGES;
-            if (i >= STAGES) mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
-            uint8_t* sa = smem + s * stage_bytes;
-            uint8_t* sb = sa + a_bytes;
-            mbar_expect_tx(&full[s], stage_bytes);
-            const int kb = kb_begin + i;
-            if (P.mode == MODE_CONV) {
-                const int tap = P.tap0[phase] + kb / P.cblocks;
-                const int c0 = (kb % P.cblocks) * BK;
-                tma_load_4d(sa, &map_a, &full[s], c0, tw0 * P.mw + P.off_w[tap], th0 * P.mh + P.off_h[tap], tn0);
-                if (P.b_mn) {   // weights [K = (tap, ci), N = co], N contiguous
+        uint32_t it = 0;   // global k-step counter (ring position)
+        for (int64_t t = blockIdx.x; t < P.tiles; t += gridDim.x) {
+            const Tile T = decode(t);
+            for (int i = 0; i < T.nk; ++i, ++it) {
+                const int s = it % STAGES;
+                if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+                uint8_t* sa = smem + s * stage_bytes;
+                uint8_t* sb = sa + a_bytes;
+                mbar_expect_tx(&full[s], stage_bytes);
+                const int kb = T.kb_begin + i;
+                if (P.mode == MODE_CONV) {
+                    const int tap = P.tap0[T.phase] + kb / P.cblocks;
+                    const int c0 = (kb % P.cblocks) * BK;
+                    tma_load_4d(sa, &map_a, &full[s], c0, T.tw0 * P.mw + P.off_w[tap], T.th0 * P.mh + P.off_h[tap],
+                                T.tn0);
+                    if (P.b_mn) {
+                        for (int q = 0; q < P.bn / 32; ++q)
+                            tma_load_2d(sb + q * 4096, &map_b, &full[s], static_cast<int>(T.n0) + 32 * q,
+                                        P.brow[tap] + c0);
+                    } else {
+                        tma_load_2d(sb, &map_b, &full[s], c0, P.brow[tap] + static_cast<int>(T.n0));
+                    }
+                } else {
+                    int r = kb;
+                    const int bw = r % P.tiles_w;
+                    r /= P.tiles_w;
+                    const int bh = r % P.tiles_h;
+                    const int bnn = r / P.tiles_h;
+                    const int x0 = bw * P.TW, y0 = bh * P.TH, n0 = bnn * P.TN;
+                    for (int q = 0; q < 4; ++q) {
+                        int64_t m = T.m0 + 32 * q;
+                        if (m >= P.M) m = T.m0;
+                        const int tap = static_cast<int>(m / P.ci), c = static_cast<int>(m % P.ci);
+                        const int dh = tap / P.kw_, dw = tap % P.kw_;
+                        tma_load_4d(sa + q * 4096, &map_a, &full[s], c, x0 * P.sw + dw - P.pl, y0 * P.sh + dh - P.pt,
+                                    n0);
+                    }
                     for (int q = 0; q < P.bn / 32; ++q)
-                        tma_load_2d(sb + q * 4096, &map_b, &full[s], static_cast<int>(n_col0) + 32 * q,
-                                    P.brow[tap] + c0);
-                } else {        // weights [(tap, ci) rows, co]; K = co contiguous
-                    tma_load_2d(sb, &map_b, &full[s], c0, P.brow[tap] + static_cast<int>(n_col0));
+                        tma_load_4d(sb + q * 4096, &map_b, &full[s], static_cast<int>(T.n0) + 32 * q, x0, y0, n0);
                 }
-            } else {
-                // pixel box kb over the output grid (gn, gh, gw)
-                int t = kb;
-                const int bw = t % P.tiles_w;
-                t /= P.tiles_w;
-                const int bh = t % P.tiles_h;
-                const int bnn = t / P.tiles_h;
-                const int x0 = bw * P.TW, y0 = bh * P.TH, n0 = bnn * P.TN;
-                for (int q = 0; q < 4; ++q) {
-                    int64_t m = m0 + 32 * q;
-                    if (m >= P.M) m = m0;   // clamp (rows masked in the epilogue)
-                    const int tap = static_cast<int>(m / P.ci), c = static_cast<int>(m % P.ci);
-                    const int dh = tap / P.kw_, dw = tap % P.kw_;
-                    tma_load_4d(sa + q * 4096, &map_a, &full[s], c, x0 * P.sw + dw - P.pl, y0 * P.sh + dh - P.pt, n0);
-                }
-                for (int q = 0; q < P.bn / 32; ++q)
-                    tma_load_4d(sb + q * 4096, &map_b, &full[s], static_cast<int>(n_col0) + 32 * q, x0, y0, n0);
             }
         }
-    } else if (warp == 1 && lane == 0 && nk > 0) {
+    } else if (warp == 1 && lane == 0) {
         // ================= MMA issuer (single thread) =================
         const uint32_t a_mn = P.mode == MODE_WGRAD ? 1u : 0u;
         const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (a_mn << 15) |
                                (static_cast<uint32_t>(P.b_mn) << 16) | ((static_cast<uint32_t>(P.bn) >> 3) << 17) |
                                ((static_cast<uint32_t>(BM) >> 4) << 24);
-        for (int i = 0; i < nk; ++i) {
-            const int s = i % STAGES;
-            mbar_wait(&full[s], (i / STAGES) & 1);
+        uint32_t it = 0, local = 0;
+        for (int64_t t = blockIdx.x; t < P.tiles; t += gridDim.x, ++local) {
+            const Tile T = decode(t);
+            const uint32_t acc = local & 1;
+            // every tile takes an accumulator turn (tiles without K steps commit
+            // immediately and the epilogue writes zeros), so phases stay in step
+            if (local >= 2) mbar_wait(&tmem_empty[acc], ((local / 2) - 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t sa = smem_u32(smem + s * stage_bytes);
-            const uint32_t sb = sa + a_bytes;
+            const uint32_t d = tmem_base + acc * static_cast<uint32_t>(P.bn);
+            for (int i = 0; i < T.nk; ++i, ++it) {
+                const int s = it % STAGES;
+                mbar_wait(&full[s], (it / STAGES) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t sa = smem_u32(smem + s * stage_bytes);
+                const uint32_t sb = sa + a_bytes;
 #pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk) {
-                const uint64_t ad = a_mn ? sdesc(sa + kk * 1024, 4096, 512, 1) : sdesc(sa + kk * 32, 16, 1024, 2);
-                const uint64_t bd = P.b_mn ? sdesc(sb + kk * 1024, 4096, 512, 1) : sdesc(sb + kk * 32, 16, 1024, 2);
-                if (P.debug && blockIdx.x == 0 && blockIdx.y == 0 && i == 0 && kk == 0)
-                    printf("mma: tmem %x idesc %x adesc %llx bdesc %llx sa %x\n", tmem_base, idesc,
-                           (unsigned long long)ad, (unsigned long long)bd, sa);
-                mma_tf32(tmem_base, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
-            }
-            mma_commit(&empty[s]);
-        }
-        mma_commit(tmem_full);
-    } else if (warp >= 2) {
-        // ================= epilogue (warps 2..5) =================
-        const int quarter = warp % 4;              // TMEM lane quarter this warp may access
-        const int row = quarter * 32 + lane;       // accumulator row == TMEM lane
-        if (nk > 0) {
-            mbar_wait(tmem_full, 0);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        }
-        float* dst = nullptr;
-        bool valid = false;
-        if (P.mode == MODE_CONV) {
-            const int ww = row % P.TW, hh = (row / P.TW) % P.TH, nn = row / (P.TW * P.TH);
-            const int n = tn0 + nn, y = th0 + hh, x = tw0 + ww;
-            valid = n < P.gn && y < P.gh && x < P.gw;
-            if (valid) {
-                const int64_t oy = static_cast<int64_t>(y) * P.out_s + P.py[phase];
-                const int64_t ox = static_cast<int64_t>(x) * P.out_s + P.px[phase];
-                valid = oy < P.out_h && ox < P.out_w;
-                dst = P.out + ((static_cast<int64_t>(n) * P.out_h + oy) * P.out_w + ox) * P.ldc;
-            }
-        } else {
-            const int64_t m = m0 + row;
-            valid = m < P.M;
-            float* base = P.splits > 1 ? P.partial + static_cast<int64_t>(blockIdx.z) * P.M * P.N : P.out;
-            dst = base + m * P.ldc;
-        }
-        for (int c = 0; c < P.bn; c += 32) {
-            uint32_t r[32];
-            if (nk > 0) {
-                tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(c), r);
-                if (P.debug && blockIdx.x == 0 && blockIdx.y == 0 && row < 2 && c == 0) {
-                    const float* sa = reinterpret_cast<const float*>(smem);
-                    printf("epi row %d nk %d r0 %f r1 %f smemA[0..3] %f %f %f %f\n", row, nk, __uint_as_float(r[0]),
-                           __uint_as_float(r[1]), sa[0], sa[1], sa[2], sa[3]);
+                for (int kk = 0; kk < BK / 8; ++kk) {
+                    const uint64_t ad = a_mn ? sdesc(sa + kk * 1024, 4096, 512, 1) : sdesc(sa + kk * 32, 16, 1024, 2);
+                    const uint64_t bd = P.b_mn ? sdesc(sb + kk * 1024, 4096, 512, 1) : sdesc(sb + kk * 32, 16, 1024, 2);
+                    mma_tf32(d, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
                 }
+                mma_commit(&empty[s]);
+            }
+            mma_commit(&tmem_full[acc]);
+        }
+    } else if (warp >= 2) {
+        // ================= epilogue (warps 2..9) =================
+        // Warp w may only touch TMEM lanes 32*(w%4)..+31; two warps share each
+        // lane quarter and split the 32-column chunks between them.
+        const int quarter = warp % 4;
+        const int half = (warp - 2) / 4;
+        const int row = quarter * 32 + lane;
+        uint32_t local = 0;
+        for (int64_t t = blockIdx.x; t < P.tiles; t += gridDim.x, ++local) {
+            const Tile T = decode(t);
+            const uint32_t acc = local & 1;
+            mbar_wait(&tmem_full[acc], (local / 2) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            float* dst = nullptr;
+            bool valid = false;
+            if (P.mode == MODE_CONV) {
+                const int ww = row % P.TW, hh = (row / P.TW) % P.TH, nn = row / (P.TW * P.TH);
+                const int n = T.tn0 + nn, y = T.th0 + hh, x = T.tw0 + ww;
+                valid = n < P.gn && y < P.gh && x < P.gw;
+                const int64_t oy = static_cast<int64_t>(y) * P.out_s + P.py[T.phase];
+                const int64_t ox = static_cast<int64_t>(x) * P.out_s + P.px[T.phase];
+                valid = valid && oy < P.out_h && ox < P.out_w;
+                dst = P.out + ((static_cast<int64_t>(n) * P.out_h + oy) * P.out_w + ox) * P.ldc;
             } else {
-#pragma unroll
-                for (int j = 0; j < 32; ++j) r[j] = 0u;
+                const int64_t m = T.m0 + row;
+                valid = m < P.M;
+                float* base = P.splits > 1 ? P.partial + static_cast<int64_t>(T.split) * P.M * P.N : P.out;
+                dst = base + m * P.ldc;
             }
-            const int64_t col0 = n_col0 + c;
-            if (!valid || col0 >= P.N) continue;
-            float v[32];
+            const int nchunks = P.bn / 32;
+            const uint32_t tbase =
+                tmem_base + acc * static_cast<uint32_t>(P.bn) + (static_cast<uint32_t>(quarter * 32) << 16);
+            uint32_t r[32];
+            bool arrived = false;
+            for (int c = half; c < nchunks; c += 2) {
+                tmem_ld32(tbase + static_cast<uint32_t>(c * 32), r);
+                if (c + 2 >= nchunks) {
+                    // this warp's last chunk of the tile is in registers: release its share
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    if (lane == 0)
+                        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_empty[acc]))
+                                     : "memory");
+                    arrived = true;
+                }
+                const int64_t col0 = T.n0 + c * 32;
+                if (T.nk == 0) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                v[j] = __uint_as_float(r[j]);
-                if (P.bias && col0 + j < P.N) v[j] = __fadd_rn(v[j], __ldg(P.bias + col0 + j));
-            }
-            if (col0 + 32 <= P.N && (P.ldc % 4) == 0) {
+                    for (int j = 0; j < 32; ++j) r[j] = 0u;
+                }
+                if (P.bias && col0 < P.N) {
 #pragma unroll
-                for (int j = 0; j < 32; j += 4)
-                    *reinterpret_cast<float4*>(dst + col0 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-            } else {
-                for (int j = 0; j < 32 && col0 + j < P.N; ++j) dst[col0 + j] = v[j];
+                    for (int j = 0; j < 32; ++j)
+                        if (col0 + j < P.N)
+                            r[j] = __float_as_uint(__fadd_rn(__uint_as_float(r[j]), __ldg(P.bias + col0 + j)));
+                }
+                if (valid && col0 < P.N) {
+                    if (col0 + 32 <= P.N && (P.ldc % 4) == 0) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4)
+                            *reinterpret_cast<float4*>(dst + col0 + j) =
+                                make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                            __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+                    } else {
+                        for (int j = 0; j < 32 && col0 + j < P.N; ++j) dst[col0 + j] = __uint_as_float(r[j]);
+                    }
+                }
             }
+            if (!arrived && lane == 0)   // a warp without a chunk in this tile still arrives once
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_empty[acc])) : "memory");
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -401,18 +466,47 @@ void pick_box(int rows, int gn, int gh, int gw, int& TN, int& TH, int& TW) {
     (void)gn;
 }
 
-size_t smem_for(int bn) { return STAGES * (BM * BK * 4 + static_cast<size_t>(bn) * BK * 4) + 1024 + 256; }
+size_t stage_bytes_for(int bn) { return BM * BK * 4 + static_cast<size_t>(bn) * BK * 4; }
 
-int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const TcParams& P, dim3 grid) {
+// Ring depth: 2 CTAs per SM when two accumulator pairs fit TMEM (bn <= 128) and
+// the ring fits half the shared memory, else one CTA with a deeper ring.
+int stages_for(int bn) {
+    const size_t budget_two = 110 * 1024, budget_one = 220 * 1024;
+    const size_t sb = stage_bytes_for(bn);
+    if (bn <= 128 && 3 * sb + 2048 <= budget_two)
+        return static_cast<int>(std::min<size_t>(MAX_STAGES, (budget_two - 2048) / sb));
+    return static_cast<int>(std::min<size_t>(MAX_STAGES, (budget_one - 2048) / sb));
+}
+
+size_t smem_for(int bn, int stages) { return stages * stage_bytes_for(bn) + 1024 + 512; }
+
+int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, TcParams& P) {
     static bool attr_done = false;
     if (!attr_done) {
-        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem_for(256))));
+        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr_done = true;
     }
-    tc_gemm_kernel<<<grid, THREADS, smem_for(P.bn), ctx->stream>>>(ma, mb, P);
+    if (P.tiles <= 0) return 0;
+    P.tma_store = 0;
+    P.stages = stages_for(P.bn);
+    const size_t smem = smem_for(P.bn, P.stages);
+    const int per_sm = (P.bn <= 128 && 2 * smem <= 228 * 1024) ? 2 : 1;
+    unsigned grid = static_cast<unsigned>(std::min<int64_t>(P.tiles, static_cast<int64_t>(ctx->sm_count) * per_sm));
+    tc_gemm_kernel<<<grid, THREADS, smem, ctx->stream>>>(ma, mb, mc, P);
     NNCB_LAUNCHED(ctx);
     return 0;
+}
+
+bool encode_out_3d(CUtensorMap* map, float* base, int64_t n, int64_t m, int64_t splits) {
+    cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)m, (cuuint64_t)splits};
+    cuuint64_t strides[2] = {(cuuint64_t)(n * 4), (cuuint64_t)(n * m * 4)};
+    cuuint32_t box[3] = {32, (cuuint32_t)BM, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = nncb::drv::table().tensorMapEncodeTiled(
+        map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) nncb::set_error(std::string("cuTensorMapEncodeTiled(out3d): ") + nncb::drv::error_string(r));
+    return r == CUDA_SUCCESS;
 }
 
 }  // namespace
@@ -422,20 +516,36 @@ namespace nncb {
 int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t lda, const float* b,
                  const float* bias, float* out, bool* handled);
 
-__global__ void im2col_k(const float* __restrict__ x, float* __restrict__ cols, nncb_gemm_desc g, int64_t K,
-                         int64_t ldk) {
-    // cols[p, k], p = (n, oh, ow), k = (dh, dw, c); zero where the tap is padding
-    int64_t total = g.n * g.oh * g.ow * ldk;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        int64_t k = t % ldk, p = t / ldk;
-        float v = 0.f;
-        if (k < K) {
-            int64_t c = k % g.ci, tap = k / g.ci, dw = tap % g.kw, dh = tap / g.kw;
-            int64_t ow = p % g.ow, r = p / g.ow, oh = r % g.oh, n = r / g.oh;
-            int64_t h = oh * g.sh + dh - g.pad_top, w = ow * g.sw + dw - g.pad_left;
-            if (h >= 0 && h < g.ih && w >= 0 && w < g.iw) v = __ldg(x + ((n * g.ih + h) * g.iw + w) * g.ci + c);
+// im2col for the 3-channel stem: one warp per output pixel writes its row of
+// kh*kw*ci (padded to ldk) columns contiguously; the per-column source offset
+// and tap position come from a shared-memory table, so the inner loop is one
+// predicated load and one coalesced store per element.
+__global__ void __launch_bounds__(256) im2col_k(const float* __restrict__ x, float* __restrict__ cols,
+                                                nncb_gemm_desc g, int K, int ldk) {
+    extern __shared__ int tab[];   // [3][ldk]: source offset, dh, dw
+    for (int k = threadIdx.x; k < ldk; k += blockDim.x) {
+        int c = k % (int)g.ci, tap = k / (int)g.ci, dw = tap % (int)g.kw, dh = tap / (int)g.kw;
+        tab[k] = k < K ? (dh * (int)g.iw + dw) * (int)g.ci + c : 0;
+        tab[ldk + k] = k < K ? dh : -100000;
+        tab[2 * ldk + k] = dw;
+    }
+    __syncthreads();
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int64_t P = g.n * g.oh * g.ow;
+    for (int64_t p = blockIdx.x * 8 + warp; p < P; p += (int64_t)gridDim.x * 8) {
+        const int ow = (int)(p % g.ow);
+        const int64_t r = p / g.ow;
+        const int oh = (int)(r % g.oh);
+        const int64_t n = r / g.oh;
+        const int h0 = oh * (int)g.sh - (int)g.pad_top, w0 = ow * (int)g.sw - (int)g.pad_left;
+        const float* base = x + ((n * g.ih + h0) * g.iw + w0) * g.ci;
+        float* out = cols + p * ldk;
+        for (int k = lane; k < ldk; k += 32) {
+            const int h = h0 + tab[ldk + k], w = w0 + tab[2 * ldk + k];
+            float v = 0.f;
+            if (h >= 0 && h < (int)g.ih && w >= 0 && w < (int)g.iw) v = __ldg(base + tab[k]);
+            out[k] = v;
         }
-        cols[t] = v;
     }
 }
 
@@ -451,7 +561,9 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
         if (d->co % 4 != 0 || d->co < 16) return 0;
         float* cols = static_cast<float*>(workspace(ctx, sizeof(float) * P * ldk));
         if (!cols) return fail("im2col: workspace allocation failed");
-        im2col_k<<<grid_for(ctx, P * ldk, 256), 256, 0, ctx->stream>>>(a, cols, *d, K, ldk);
+        im2col_k<<<grid_for(ctx, P * 32, 256, 8), 256, 3 * ldk * sizeof(int), ctx->stream>>>(a, cols, *d,
+                                                                                              static_cast<int>(K),
+                                                                                              static_cast<int>(ldk));
         NNCB_LAUNCHED(ctx);
         nncb_gemm_desc dd{};
         dd.kind = d->kind == NNCB_CONV_FWD ? NNCB_DENSE_FWD : NNCB_DENSE_WGRAD;
@@ -567,10 +679,17 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
         }
         P.bias = (fwd && (d->epilogue & NNCB_EPI_BIAS)) ? bias : nullptr;
         P.out = out;
-        dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>((Nc + P.bn - 1) / P.bn),
-                  static_cast<unsigned>(fwd ? 1 : sh * sw));
+        P.n_tiles = (Nc + P.bn - 1) / P.bn;
+        P.pix_tiles = tiles;
+        P.tiles = tiles * P.n_tiles * (fwd ? 1 : sh * sw);
+        // TMA-store epilogue when output pixels are dense (fwd, or stride-1 dgrad)
+        CUtensorMap mc;
+        memset(&mc, 0, sizeof(mc));
+        P.tma_store = (P.out_s == 1 && Nc % 4 == 0) ? 1 : 0;
+        if (P.tma_store && !encode_4d(&mc, out, Nc, P.out_w, P.out_h, P.gn, 32, P.TW, P.TH, P.TN, 1, 1, false))
+            return 1;
         *handled = true;
-        return launch(ctx, ma, mb, P, grid);
+        return launch(ctx, ma, mb, mc, P);
     }
     // ---- wgrad ----------------------------------------------------------------
     P.mode = MODE_WGRAD;
@@ -602,9 +721,14 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
         P.partial = static_cast<float*>(scratch(ctx, sizeof(float) * P.splits * P.M * P.N));
         if (!P.partial) return fail("wgrad: split-K workspace allocation failed");
     }
-    dim3 grid(static_cast<unsigned>(mt), static_cast<unsigned>(nt), static_cast<unsigned>(P.splits));
+    P.n_tiles = nt;
+    P.m_tiles = mt;
+    P.tiles = mt * nt * P.splits;
+    CUtensorMap mc;
+    P.tma_store = 1;
+    if (!encode_out_3d(&mc, P.splits > 1 ? P.partial : out, co, P.M, P.splits)) return 1;
     *handled = true;
-    if (int rc = launch(ctx, ma, mb, P, grid)) return rc;
+    if (int rc = launch(ctx, ma, mb, mc, P)) return rc;
     if (P.splits > 1) {
         int64_t count = P.M * P.N;
         splitk_reduce_kernel<<<grid_for(ctx, count, 256), 256, 0, ctx->stream>>>(P.partial, out, count, P.splits);

@@ -84,6 +84,11 @@ def test_c1_batchnorm_vs_oracle(precision, tol_f, tol_b):
     assert abs(loss - oloss) <= tol_f * abs(oloss)
     metric = rel if precision == P.PREC_FP32 else rel_norm
     for w, g in ograds.items():
+        if w in ("c1.bias", "c2.bias"):
+            # a conv bias feeding BatchNorm has an analytically zero gradient (BN
+            # removes the per-channel mean); both sides are rounding noise ~1e-9
+            assert np.max(np.abs(grads[w])) < 1e-6 and np.max(np.abs(g)) < 1e-6, w
+            continue
         assert metric(grads[w], g) < tol_b, w
 
 
