@@ -170,9 +170,9 @@ void launch_cost(const BoundLaunch& b, const Launch& L, const ExecutionPlan& p, 
                 case NNCB_DENSE_FWD: M = d.batch; N = d.out_f; K = d.in_f; break;
                 case NNCB_DENSE_DGRAD: M = d.batch; N = d.in_f; K = d.out_f; break;
                 case NNCB_DENSE_WGRAD: M = d.in_f; N = d.out_f; K = d.batch; break;
-                case NNCB_CONV_FWD: M = double(d.n) * d.oh * d.ow; N = d.co; K = double(d.kh) * d.kw * d.ci; break;
-                case NNCB_CONV_DGRAD: M = double(d.n) * d.ih * d.iw; N = d.ci; K = double(d.kh) * d.kw * d.co; break;
-                default: M = double(d.kh) * d.kw * d.ci; N = d.co; K = double(d.n) * d.oh * d.ow; break;
+                // all three contractions of a convolution perform the forward's
+                // 2*N*OH*OW*CO*KH*KW*CI useful flops (strided dgrad skips zeros)
+                default: M = double(d.n) * d.oh * d.ow; N = d.co; K = double(d.kh) * d.kw * d.ci; break;
             }
             flops = 2.0 * M * N * K;
             for (size_t a = 0; a < L.args.size(); ++a) bytes += 4.0 * elems(a);

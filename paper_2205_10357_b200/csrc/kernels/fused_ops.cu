@@ -20,54 +20,99 @@
 
 namespace {
 
+// Max pooling, 4 channels per thread (C % 4 == 0: float4 loads/stores) or 1.
+// Pixel decomposition in 32-bit (host guarantees n*oh*ow < 2^31).
+template <int V>
 __global__ void maxpool_fwd_k(const float* __restrict__ x, float* __restrict__ y, float* __restrict__ idx,
                               nncb_pool_geom g) {
-    int64_t total = g.n * g.oh * g.ow * g.c;
+    const int C = (int)g.c, CV = C / V;
+    const int OW = (int)g.ow, OH = (int)g.oh, IW = (int)g.iw, IH = (int)g.ih;
+    const int64_t total = g.n * g.oh * g.ow * CV;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        int64_t c = t % g.c;
-        int64_t r = t / g.c;
-        int64_t ow = r % g.ow;
-        r /= g.ow;
-        int64_t oh = r % g.oh;
-        int64_t n = r / g.oh;
-        float best = 0.f;
-        int best_i = -1;
-        for (int64_t dh = 0; dh < g.kh; ++dh)
-            for (int64_t dw = 0; dw < g.kw; ++dw) {
-                int64_t h = oh * g.sh + dh, w = ow * g.sw + dw;
-                float v = __ldg(x + ((n * g.ih + h) * g.iw + w) * g.c + c);
-                if (best_i < 0 || v > best) {
-                    best = v;
-                    best_i = static_cast<int>(dh * g.kw + dw);
+        const int cv = (int)(t % CV);
+        const int64_t pix = t / CV;
+        const int ow = (int)(pix % OW);
+        const int64_t r = pix / OW;
+        const int oh = (int)(r % OH);
+        const int64_t n = r / OH;
+        float best[V];
+        int bi[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) bi[j] = -1;
+        const float* base = x + (n * IH * (int64_t)IW) * C + cv * V;
+        for (int dh = 0; dh < (int)g.kh; ++dh)
+            for (int dw = 0; dw < (int)g.kw; ++dw) {
+                const int h = oh * (int)g.sh + dh, w = ow * (int)g.sw + dw;
+                const float* p = base + ((int64_t)h * IW + w) * C;
+                float v[V];
+                if (V == 4) {
+                    float4 q = __ldg(reinterpret_cast<const float4*>(p));
+                    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+                } else {
+                    v[0] = __ldg(p);
                 }
+                const int k = dh * (int)g.kw + dw;
+#pragma unroll
+                for (int j = 0; j < V; ++j)
+                    if (bi[j] < 0 || v[j] > best[j]) {
+                        best[j] = v[j];
+                        bi[j] = k;
+                    }
             }
-        y[t] = best;
-        if (idx) idx[t] = static_cast<float>(best_i);
+        const int64_t at = pix * C + cv * V;
+        if (V == 4) {
+            *reinterpret_cast<float4*>(y + at) = make_float4(best[0], best[1], best[2], best[3]);
+            if (idx) *reinterpret_cast<float4*>(idx + at) = make_float4((float)bi[0], (float)bi[1], (float)bi[2], (float)bi[3]);
+        } else {
+            y[at] = best[0];
+            if (idx) idx[at] = (float)bi[0];
+        }
     }
 }
 
+// Max-pool backward as a gather over the windows covering each input pixel,
+// in (oh, ow) ascending order = the reference scatter order (bit-exact).
+template <int V>
 __global__ void maxpool_bwd_k(const float* __restrict__ idx, const float* __restrict__ gy, float* __restrict__ gx,
                               nncb_pool_geom g) {
-    int64_t total = g.n * g.ih * g.iw * g.c;
+    const int C = (int)g.c, CV = C / V;
+    const int OW = (int)g.ow, OH = (int)g.oh, IW = (int)g.iw, IH = (int)g.ih;
+    const int KH = (int)g.kh, KW = (int)g.kw, SH = (int)g.sh, SW = (int)g.sw;
+    const int64_t total = g.n * g.ih * g.iw * CV;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        int64_t c = t % g.c;
-        int64_t r = t / g.c;
-        int64_t w = r % g.iw;
-        r /= g.iw;
-        int64_t h = r % g.ih;
-        int64_t n = r / g.ih;
-        int64_t oh0 = h - g.kh + 1 > 0 ? (h - g.kh + 1 + g.sh - 1) / g.sh : 0;
-        int64_t oh1 = h / g.sh < g.oh - 1 ? h / g.sh : g.oh - 1;
-        int64_t ow0 = w - g.kw + 1 > 0 ? (w - g.kw + 1 + g.sw - 1) / g.sw : 0;
-        int64_t ow1 = w / g.sw < g.ow - 1 ? w / g.sw : g.ow - 1;
-        float acc = 0.f;
-        for (int64_t oh = oh0; oh <= oh1; ++oh)
-            for (int64_t ow = ow0; ow <= ow1; ++ow) {
-                int64_t at = ((n * g.oh + oh) * g.ow + ow) * g.c + c;
-                int64_t wi = static_cast<int64_t>(__ldg(idx + at));
-                if (oh * g.sh + wi / g.kw == h && ow * g.sw + wi % g.kw == w) acc = __fadd_rn(acc, __ldg(gy + at));
+        const int cv = (int)(t % CV);
+        const int64_t pix = t / CV;
+        const int w = (int)(pix % IW);
+        const int64_t r = pix / IW;
+        const int h = (int)(r % IH);
+        const int64_t n = r / IH;
+        const int oh0 = h - KH + 1 > 0 ? (h - KH + SH) / SH : 0;
+        const int oh1 = min(h / SH, OH - 1);
+        const int ow0 = w - KW + 1 > 0 ? (w - KW + SW) / SW : 0;
+        const int ow1 = min(w / SW, OW - 1);
+        float acc[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[j] = 0.f;
+        for (int oh = oh0; oh <= oh1; ++oh)
+            for (int ow = ow0; ow <= ow1; ++ow) {
+                const int want = (h - oh * SH) * KW + (w - ow * SW);
+                const int64_t at = ((n * OH + oh) * OW + ow) * C + cv * V;
+                if (V == 4) {
+                    float4 ix = __ldg(reinterpret_cast<const float4*>(idx + at));
+                    float4 gv = __ldg(reinterpret_cast<const float4*>(gy + at));
+                    if ((int)ix.x == want) acc[0] = __fadd_rn(acc[0], gv.x);
+                    if ((int)ix.y == want) acc[1] = __fadd_rn(acc[1], gv.y);
+                    if ((int)ix.z == want) acc[2] = __fadd_rn(acc[2], gv.z);
+                    if ((int)ix.w == want) acc[3] = __fadd_rn(acc[3], gv.w);
+                } else {
+                    if ((int)__ldg(idx + at) == want) acc[0] = __fadd_rn(acc[0], __ldg(gy + at));
+                }
             }
-        gx[t] = acc;
+        const int64_t o = pix * C + cv * V;
+        if (V == 4)
+            *reinterpret_cast<float4*>(gx + o) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        else
+            gx[o] = acc[0];
     }
 }
 
@@ -403,7 +448,10 @@ extern "C" {
 int nncb_maxpool_fwd(nncb_ctx* ctx, const nncb_pool_geom* g, const float* x, float* y, float* idx) {
     int64_t total = g->n * g->oh * g->ow * g->c;
     if (total == 0) return 0;
-    maxpool_fwd_k<<<nncb::grid_for(ctx, total, 256), 256, 0, ctx->stream>>>(x, y, idx, *g);
+    if (g->c % 4 == 0)
+        maxpool_fwd_k<4><<<nncb::grid_for(ctx, total / 4, 256), 256, 0, ctx->stream>>>(x, y, idx, *g);
+    else
+        maxpool_fwd_k<1><<<nncb::grid_for(ctx, total, 256), 256, 0, ctx->stream>>>(x, y, idx, *g);
     NNCB_LAUNCHED(ctx);
     return 0;
 }
@@ -411,7 +459,10 @@ int nncb_maxpool_fwd(nncb_ctx* ctx, const nncb_pool_geom* g, const float* x, flo
 int nncb_maxpool_bwd(nncb_ctx* ctx, const nncb_pool_geom* g, const float* idx, const float* gy, float* gx) {
     int64_t total = g->n * g->ih * g->iw * g->c;
     if (total == 0) return 0;
-    maxpool_bwd_k<<<nncb::grid_for(ctx, total, 256), 256, 0, ctx->stream>>>(idx, gy, gx, *g);
+    if (g->c % 4 == 0)
+        maxpool_bwd_k<4><<<nncb::grid_for(ctx, total / 4, 256), 256, 0, ctx->stream>>>(idx, gy, gx, *g);
+    else
+        maxpool_bwd_k<1><<<nncb::grid_for(ctx, total, 256), 256, 0, ctx->stream>>>(idx, gy, gx, *g);
     NNCB_LAUNCHED(ctx);
     return 0;
 }

