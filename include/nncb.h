@@ -125,7 +125,14 @@ enum nncb_precision {
     NNCB_PREC_TF32 = 0,    /* tcgen05.mma kind::tf32, fp32 accumulate in TMEM (default)    */
     NNCB_PREC_FP32 = 1,    /* exact-order fp32 FFMA path (parity mode)                      */
 };
-enum nncb_epilogue { NNCB_EPI_BIAS = 1, NNCB_EPI_RELU = 2 };
+enum nncb_epilogue {
+    NNCB_EPI_BIAS = 1,
+    NNCB_EPI_RELU = 2,
+    /* per-output-column sum and sum of squares accumulated (double) into
+     * colstats[0:N] / colstats[N:2N] -- BatchNorm statistics fused into the
+     * producing GEMM. The GEMM zeroes the accumulator itself.               */
+    NNCB_EPI_COLSTATS = 4,
+};
 
 typedef struct {
     int32_t kind, precision, epilogue, _pad;
@@ -133,6 +140,8 @@ typedef struct {
     int64_t n, ih, iw, ci, co, kh, kw, sh, sw, oh, ow, pad_top, pad_left;
     /* dense geometry */
     int64_t batch, in_f, out_f;
+    /* NNCB_EPI_COLSTATS accumulator: 2*N doubles */
+    double* colstats;
 } nncb_gemm_desc;
 
 /* FWD:   a = x, b = weight, out = y (bias optional)
@@ -172,6 +181,8 @@ int nncb_cumsum(nncb_ctx* ctx, const float* x, float* y, int64_t outer, int64_t 
  * = 1/sqrt(var + eps) (biased variance); accumulation in double.           */
 int nncb_bn_stats(nncb_ctx* ctx, const float* x, float* stats, int64_t rows, int64_t C,
                   double eps);
+/* stats = (mean, 1/sqrt(var + eps)) from fused column sums (NNCB_EPI_COLSTATS). */
+int nncb_bn_finalize(nncb_ctx* ctx, const double* colstats, float* stats, int64_t rows, int64_t C, double eps);
 /* BatchNorm backward reductions: sum_g[c] = sum g, sum_gx[c] = sum g*xhat.  */
 int nncb_bn_grad_reduce(nncb_ctx* ctx, const float* x, const float* stats, const float* g,
                         float* sum_g, float* sum_gx, int64_t rows, int64_t C);

@@ -114,6 +114,8 @@ private:
 
 struct BoundLaunch {
     LaunchKind kind;
+    bool bn_finalize = false;      // BnStats rewritten to read GEMM-epilogue column sums
+    double* colstats = nullptr;
     std::vector<void*> ptrs;
     nncb_ew_kernel* ew = nullptr;
     int64_t n = 0, c = 0;
@@ -141,7 +143,12 @@ void enqueue(nncb_ctx* ctx, const BoundLaunch& b) {
             break;
         case LaunchKind::SumRows: NNC_CHECK(nncb_sum_rows(ctx, P(0), P(1), b.d0, b.d1, b.flag0)); break;
         case LaunchKind::CumSum: NNC_CHECK(nncb_cumsum(ctx, P(0), P(1), b.d0, b.d1, b.d2, b.flag0, b.flag1)); break;
-        case LaunchKind::BnStats: NNC_CHECK(nncb_bn_stats(ctx, P(0), P(1), b.d0, b.d1, b.eps)); break;
+        case LaunchKind::BnStats:
+            if (b.bn_finalize)
+                NNC_CHECK(nncb_bn_finalize(ctx, b.colstats, P(1), b.d0, b.d1, b.eps));
+            else
+                NNC_CHECK(nncb_bn_stats(ctx, P(0), P(1), b.d0, b.d1, b.eps));
+            break;
         case LaunchKind::BnGradReduce:
             NNC_CHECK(nncb_bn_grad_reduce(ctx, P(0), P(1), P(2), P(3), P(4), b.d0, b.d1));
             break;
@@ -195,6 +202,7 @@ struct Program {
     std::vector<const ExecutionPlan*> plans;
     void* arena = nullptr;
     int64_t arena_bytes = 0;
+    void* side = nullptr;          // fused BatchNorm column-sum accumulators
     std::unordered_map<std::string, void*> where;   // value name -> device pointer
     std::vector<std::vector<BoundLaunch>> steps;     // per plan, flattened launches
     std::vector<std::vector<const Launch*>> sources; // per plan, the plan launch of each bound launch
@@ -203,6 +211,7 @@ struct Program {
 
     ~Program() {
         if (arena) nncb_free(dev->ctx(), arena);
+        if (side) nncb_free(dev->ctx(), side);
     }
 
     void* ptr(const std::string& name) const {
@@ -264,6 +273,48 @@ struct Program {
                     sources.back().push_back(&p->groups[es.group].launches[li]);
                 }
             }
+        }
+        if (precision == NNCB_PREC_TF32) fuse_bn_statistics();
+    }
+
+    /// BatchNorm statistics of a tensor-core GEMM's output are accumulated in
+    /// that GEMM's epilogue (column sum / sum of squares), so the separate
+    /// statistics pass over the activation disappears; the BN launch only
+    /// finalizes mean / invstd from 2*C doubles.
+    void fuse_bn_statistics() {
+        std::vector<BoundLaunch*> fused;
+        int64_t doubles = 0;
+        for (auto& plan_steps : steps)
+            for (size_t j = 0; j < plan_steps.size(); ++j) {
+                BoundLaunch& bn = plan_steps[j];
+                if (bn.kind != LaunchKind::BnStats) continue;
+                for (size_t i = j; i-- > 0;) {
+                    BoundLaunch& g = plan_steps[i];
+                    if (g.kind != LaunchKind::Gemm || g.ptrs.back() != bn.ptrs[0]) continue;
+                    if (g.gemm.kind != NNCB_CONV_FWD && g.gemm.kind != NNCB_DENSE_FWD) break;
+                    // the epilogue reduction only hides behind long main loops:
+                    // fuse when K >= 1024 (else the separate pass is cheaper)
+                    const int64_t K = g.gemm.kind == NNCB_DENSE_FWD ? g.gemm.in_f
+                                                                    : g.gemm.kh * g.gemm.kw * g.gemm.ci;
+                    if (K < 1024 && !std::getenv("NNC_FUSE_ALL_BN_STATS")) break;
+                    g.gemm.epilogue |= NNCB_EPI_COLSTATS;
+                    g.gemm.colstats = reinterpret_cast<double*>(static_cast<uintptr_t>(doubles));  // offset for now
+                    bn.bn_finalize = true;
+                    bn.colstats = g.gemm.colstats;
+                    doubles += 2 * bn.d1;
+                    fused.push_back(&g);
+                    fused.push_back(&bn);
+                    break;
+                }
+            }
+        if (!doubles) return;
+        NNC_CHECK(nncb_malloc(dev->ctx(), static_cast<size_t>(doubles) * sizeof(double), &side));
+        auto rebase = [&](double* off) { return static_cast<double*>(side) + reinterpret_cast<uintptr_t>(off); };
+        for (BoundLaunch* b : fused) {
+            if (b->kind == LaunchKind::Gemm)
+                b->gemm.colstats = rebase(b->gemm.colstats);
+            else
+                b->colstats = rebase(b->colstats);
         }
     }
 

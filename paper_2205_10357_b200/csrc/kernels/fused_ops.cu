@@ -397,6 +397,32 @@ __global__ void sum_rows_exact_k(const float* __restrict__ x, float* __restrict_
     out[c] = acc;
 }
 
+__global__ void bn_finalize_k(const double* __restrict__ cs, float* __restrict__ stats, int64_t rows, int64_t C,
+                              double eps) {
+    int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= C) return;
+    double mean = cs[c] / (double)rows;
+    double var = cs[C + c] / (double)rows - mean * mean;
+    if (var < 0) var = 0;
+    stats[c] = (float)mean;
+    stats[C + c] = (float)(1.0 / sqrt(var + eps));
+}
+
+// colstats accumulation from a materialized output (used when the GEMM ran on
+// the exact path): cs[c] += sum_r y, cs[C+c] += sum_r y^2.
+__global__ void colstats_k(const float* __restrict__ y, double* __restrict__ cs, int64_t rows, int64_t C) {
+    int64_t c = blockIdx.x * 32 + threadIdx.x;
+    if (c >= C) return;
+    double s0 = 0, s1 = 0;
+    for (int64_t r = blockIdx.y * (int64_t)blockDim.y + threadIdx.y; r < rows; r += (int64_t)gridDim.y * blockDim.y) {
+        double v = y[r * C + c];
+        s0 += v;
+        s1 += v * v;
+    }
+    atomicAdd(cs + c, s0);
+    atomicAdd(cs + C + c, s1);
+}
+
 __global__ void cumsum_k(const float* __restrict__ x, float* __restrict__ y, int64_t outer, int64_t len, int64_t inner,
                          int exclusive, int reverse) {
     int64_t lines = outer * inner;
@@ -576,6 +602,16 @@ __global__ void sgd_k(float* __restrict__ w, const float* __restrict__ g, int64_
 
 }  // namespace
 
+namespace nncb {
+int colstats_from_output(nncb_ctx* ctx, const float* y, double* cs, int64_t rows, int64_t C) {
+    NNCB_CUDA(cudaMemsetAsync(cs, 0, sizeof(double) * 2 * C, ctx->stream));
+    dim3 grid((unsigned)((C + 31) / 32), (unsigned)std::min<int64_t>(1024, (rows + 255) / 256));
+    colstats_k<<<grid, dim3(32, 8), 0, ctx->stream>>>(y, cs, rows, C);
+    NNCB_LAUNCHED(ctx);
+    return 0;
+}
+}  // namespace nncb
+
 extern "C" {
 
 int nncb_maxpool_fwd(nncb_ctx* ctx, const nncb_pool_geom* g, const float* x, float* y, float* idx) {
@@ -637,6 +673,13 @@ int nncb_cumsum(nncb_ctx* ctx, const float* x, float* y, int64_t outer, int64_t 
 
 int nncb_bn_stats(nncb_ctx* ctx, const float* x, float* stats, int64_t rows, int64_t C, double eps) {
     return col_reduce<1>(ctx, x, nullptr, nullptr, rows, C, eps, stats, nullptr);
+}
+
+int nncb_bn_finalize(nncb_ctx* ctx, const double* colstats, float* stats, int64_t rows, int64_t C, double eps) {
+    if (C <= 0) return 0;
+    bn_finalize_k<<<(unsigned)((C + 127) / 128), 128, 0, ctx->stream>>>(colstats, stats, rows, C, eps);
+    NNCB_LAUNCHED(ctx);
+    return 0;
 }
 
 int nncb_bn_grad_reduce(nncb_ctx* ctx, const float* x, const float* stats, const float* g, float* sum_g,

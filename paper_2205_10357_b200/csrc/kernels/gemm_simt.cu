@@ -228,10 +228,19 @@ int gemm_simt(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const floa
 
 extern "C" int nncb_gemm(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const float* bias,
                          float* out) {
+    const bool colstats = (d->epilogue & NNCB_EPI_COLSTATS) && d->colstats;
+    if (colstats && d->kind != NNCB_CONV_FWD && d->kind != NNCB_DENSE_FWD)
+        return nncb::fail("nncb_gemm: column statistics are a forward-GEMM epilogue");
     if (d->precision == NNCB_PREC_TF32) {
         bool handled = false;
         int rc = nncb::gemm_tc(ctx, d, a, b, bias, out, &handled);
         if (rc || handled) return rc;
     }
-    return nncb::gemm_simt(ctx, d, a, b, bias, out);
+    if (int rc = nncb::gemm_simt(ctx, d, a, b, bias, out)) return rc;
+    if (colstats) {
+        const bool dense = d->kind == NNCB_DENSE_FWD;
+        const int64_t rows = dense ? d->batch : d->n * d->oh * d->ow, C = dense ? d->out_f : d->co;
+        return nncb::colstats_from_output(ctx, out, d->colstats, rows, C);
+    }
+    return 0;
 }

@@ -73,6 +73,7 @@ struct TcParams {
     int64_t m_tiles;    // MODE_WGRAD: tiles along M
     int tma_store;      // epilogue through smem + TMA store (else direct stores)
     int stages;         // smem ring depth (sized so 2 CTAs fit per SM when N is small)
+    double* colstats;   // fused BatchNorm statistics: [0,N) sum, [N,2N) sum of squares
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -177,6 +178,7 @@ __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: 
 // tiles b, b + grid, ... The smem ring (TMA -> MMA) and the double-buffered TMEM
 // accumulator (MMA -> epilogue) carry their phases across tiles, so the
 // epilogue of one tile overlaps the main loop of the next.
+template <bool CS>
 __global__ void __launch_bounds__(THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_c, const __grid_constant__ TcParams P) {
@@ -192,8 +194,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* tmem_full = empty + STAGES;                 // [2]
     uint64_t* tmem_empty = tmem_full + 2;                 // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+    // CS: per-CTA column sum / sum of squares of the current column range
+    double* cs_acc = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(tmem_slot) + 16);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (CS)
+        for (int i = threadIdx.x; i < 2 * P.bn; i += blockDim.x) cs_acc[i] = 0.0;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
@@ -379,6 +385,41 @@ __global__ void __launch_bounds__(THREADS, 1)
                         if (col0 + j < P.N)
                             r[j] = __float_as_uint(__fadd_rn(__uint_as_float(r[j]), __ldg(P.bias + col0 + j)));
                 }
+                if (CS) {
+                    // column sums of this warp's 32 rows, 8 columns at a time: the
+                    // 8-vector halves across lane bits 4,3,2 (7 shuffles per sum),
+                    // bits 1,0 are a plain xor-sum; lane l then holds column l>>2
+#pragma unroll
+                    for (int g8 = 0; g8 < 4; ++g8) {
+                        float a[8], q[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const float vj = valid ? __uint_as_float(r[g8 * 8 + j]) : 0.f;
+                            a[j] = vj;
+                            q[j] = vj * vj;
+                        }
+#pragma unroll
+                        for (int w = 4, bit = 16; w >= 1; w >>= 1, bit >>= 1) {
+                            const bool upper = (lane & bit) != 0;
+#pragma unroll
+                            for (int j = 0; j < w; ++j) {
+                                const float ra = __shfl_xor_sync(0xffffffffu, upper ? a[j] : a[j + w], bit);
+                                const float rq = __shfl_xor_sync(0xffffffffu, upper ? q[j] : q[j + w], bit);
+                                a[j] = (upper ? a[j + w] : a[j]) + ra;
+                                q[j] = (upper ? q[j + w] : q[j]) + rq;
+                            }
+                        }
+                        a[0] += __shfl_xor_sync(0xffffffffu, a[0], 2);
+                        q[0] += __shfl_xor_sync(0xffffffffu, q[0], 2);
+                        a[0] += __shfl_xor_sync(0xffffffffu, a[0], 1);
+                        q[0] += __shfl_xor_sync(0xffffffffu, q[0], 1);
+                        if ((lane & 3) == 0) {
+                            const int cl = c * 32 + g8 * 8 + (lane >> 2);
+                            atomicAdd(cs_acc + cl, (double)a[0]);
+                            atomicAdd(cs_acc + P.bn + cl, (double)q[0]);
+                        }
+                    }
+                }
                 if (valid && col0 < P.N) {
                     if (col0 + 32 <= P.N && (P.ldc % 4) == 0) {
 #pragma unroll
@@ -393,6 +434,20 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             if (!arrived && lane == 0)   // a warp without a chunk in this tile still arrives once
                 asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_empty[acc])) : "memory");
+            if (CS) {
+                const int64_t tn = t + gridDim.x;
+                const bool flush = tn >= P.tiles || (tn % P.n_tiles) * P.bn != T.n0;
+                if (flush) {
+                    asm volatile("bar.sync 1, 256;" ::: "memory");
+                    const int et = threadIdx.x - 64;
+                    for (int i = et; i < 2 * P.bn; i += 256) {
+                        const int cl = i % P.bn;
+                        if (T.n0 + cl < P.N) atomicAdd(P.colstats + (i / P.bn) * P.N + T.n0 + cl, cs_acc[i]);
+                        cs_acc[i] = 0.0;
+                    }
+                    asm volatile("bar.sync 1, 256;" ::: "memory");
+                }
+            }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -471,19 +526,20 @@ size_t stage_bytes_for(int bn) { return BM * BK * 4 + static_cast<size_t>(bn) * 
 // Ring depth: 2 CTAs per SM when two accumulator pairs fit TMEM (bn <= 128) and
 // the ring fits half the shared memory, else one CTA with a deeper ring.
 int stages_for(int bn) {
-    const size_t budget_two = 110 * 1024, budget_one = 220 * 1024;
+    const size_t budget_two = 108 * 1024, budget_one = 216 * 1024;
     const size_t sb = stage_bytes_for(bn);
     if (bn <= 128 && 3 * sb + 2048 <= budget_two)
         return static_cast<int>(std::min<size_t>(MAX_STAGES, (budget_two - 2048) / sb));
     return static_cast<int>(std::min<size_t>(MAX_STAGES, (budget_one - 2048) / sb));
 }
 
-size_t smem_for(int bn, int stages) { return stages * stage_bytes_for(bn) + 1024 + 512; }
+size_t smem_for(int bn, int stages) { return stages * stage_bytes_for(bn) + 1024 + 512 + 16 * bn; }
 
 int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, TcParams& P) {
     static bool attr_done = false;
     if (!attr_done) {
-        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr_done = true;
     }
     if (P.tiles <= 0) return 0;
@@ -492,7 +548,10 @@ int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CU
     const size_t smem = smem_for(P.bn, P.stages);
     const int per_sm = (P.bn <= 128 && 2 * smem <= 228 * 1024) ? 2 : 1;
     unsigned grid = static_cast<unsigned>(std::min<int64_t>(P.tiles, static_cast<int64_t>(ctx->sm_count) * per_sm));
-    tc_gemm_kernel<<<grid, THREADS, smem, ctx->stream>>>(ma, mb, mc, P);
+    if (P.colstats)
+        tc_gemm_kernel<true><<<grid, THREADS, smem, ctx->stream>>>(ma, mb, mc, P);
+    else
+        tc_gemm_kernel<false><<<grid, THREADS, smem, ctx->stream>>>(ma, mb, mc, P);
     NNCB_LAUNCHED(ctx);
     return 0;
 }
@@ -572,6 +631,7 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
         dd.batch = P;
         dd.in_f = K;
         dd.out_f = d->co;
+        dd.colstats = d->colstats;
         int rc = gemm_tc_impl(ctx, &dd, cols, ldk, b, bias, out, handled);
         if (!rc && !*handled) return fail("im2col route: dense GEMM rejected");
         return rc;
@@ -679,6 +739,8 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
         }
         P.bias = (fwd && (d->epilogue & NNCB_EPI_BIAS)) ? bias : nullptr;
         P.out = out;
+        P.colstats = (fwd && (d->epilogue & NNCB_EPI_COLSTATS)) ? d->colstats : nullptr;
+        if (P.colstats) NNCB_CUDA(cudaMemsetAsync(P.colstats, 0, sizeof(double) * 2 * Nc, ctx->stream));
         P.n_tiles = (Nc + P.bn - 1) / P.bn;
         P.pix_tiles = tiles;
         P.tiles = tiles * P.n_tiles * (fwd ? 1 : sh * sw);

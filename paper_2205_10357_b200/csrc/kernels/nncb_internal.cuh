@@ -68,6 +68,8 @@ void* scratch(nncb_ctx* ctx, size_t bytes);
 void* workspace(nncb_ctx* ctx, size_t bytes);
 void ew_release(nncb_ew_kernel* k);
 
+int colstats_from_output(nncb_ctx* ctx, const float* y, double* cs, int64_t rows, int64_t C);
+
 // GEMM back ends (gemm_simt.cu / gemm_tc.cu)
 int gemm_simt(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const float* bias,
               float* out);
