@@ -73,6 +73,8 @@ struct TcParams {
     int64_t m_tiles;    // MODE_WGRAD: tiles along M
     int tma_store;      // epilogue through smem + TMA store (else direct stores)
     int stages;         // smem ring depth (sized so 2 CTAs fit per SM when N is small)
+    int nostore;        // tuning knob: skip the output stores (epilogue cost probe)
+    int stg_cols;       // epilogue transpose width per pass: 32, 16 or 8 columns (4/2/1 KB per warp)
     double* colstats;   // fused BatchNorm statistics: [0,N) sum, [N,2N) sum of squares
 };
 
@@ -174,12 +176,50 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void*
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
+// Store one warp's 32x32 fp32 accumulator chunk (row `lane` in r[0..31]) to
+// global memory through a per-warp shared-memory transpose of width
+// CH*4 columns (CH 16-byte chunks per row, XOR-swizzled by row), so that each
+// store instruction writes 32/CH whole row segments of CH*16 contiguous
+// bytes instead of 32 scattered 16-byte pieces.
+template <int CH>
+__device__ __forceinline__ void store_chunk_t(const uint32_t (&r)[32], uint8_t* tile, float* dst, bool valid,
+                                              int col0, int N, bool full_cols, int lane) {
+    constexpr int COLS = CH * 4, RPI = 32 / CH;   // columns per pass, rows per store instruction
+#pragma unroll
+    for (int p = 0; p < 32 / COLS; ++p) {
+        uint8_t* rowp = tile + lane * (CH * 16);
+#pragma unroll
+        for (int j = 0; j < CH; ++j)
+            *reinterpret_cast<uint4*>(rowp + ((j ^ (lane % CH)) << 4)) =
+                make_uint4(r[p * COLS + 4 * j], r[p * COLS + 4 * j + 1], r[p * COLS + 4 * j + 2], r[p * COLS + 4 * j + 3]);
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {
+            const int rr = i * RPI + lane / CH, ch = lane % CH;
+            float* rdst = reinterpret_cast<float*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(dst), rr));
+            const int rvalid = __shfl_sync(0xffffffffu, valid ? 1 : 0, rr);
+            const uint4 v4 = *reinterpret_cast<const uint4*>(tile + rr * (CH * 16) + ((ch ^ (rr % CH)) << 4));
+            if (!rvalid) continue;
+            const int c = col0 + p * COLS + ch * 4;
+            if (full_cols) {
+                *reinterpret_cast<uint4*>(rdst + c) = v4;
+            } else {
+                const uint32_t e[4] = {v4.x, v4.y, v4.z, v4.w};
+                for (int q = 0; q < 4; ++q)
+                    if (c + q < N) rdst[c + q] = __uint_as_float(e[q]);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+
 // Persistent warp-specialised GEMM. grid = min(tiles, #SMs); CTA b processes
 // tiles b, b + grid, ... The smem ring (TMA -> MMA) and the double-buffered TMEM
 // accumulator (MMA -> epilogue) carry their phases across tiles, so the
 // epilogue of one tile overlaps the main loop of the next.
 template <bool CS>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(THREADS, 2)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_c, const __grid_constant__ TcParams P) {
     const int STAGES = P.stages;
@@ -188,8 +228,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t a_bytes = BM * BK * 4;                 // 16 KB
     const uint32_t b_bytes = static_cast<uint32_t>(P.bn) * BK * 4;
     const uint32_t stage_bytes = a_bytes + b_bytes;
-    uint8_t* staging = smem + STAGES * stage_bytes;       // 2 x 16 KB epilogue staging (TMA-store mode only)
-    uint64_t* full = reinterpret_cast<uint64_t*>(staging + (P.tma_store ? 2 * 16384 : 0));
+    uint8_t* staging = smem + STAGES * stage_bytes;       // 8 x stg_cols*128 B: one transpose tile per epilogue warp
+    uint64_t* full = reinterpret_cast<uint64_t*>(staging + 8 * P.stg_cols * 128);
     uint64_t* empty = full + STAGES;
     uint64_t* tmem_full = empty + STAGES;                 // [2]
     uint64_t* tmem_empty = tmem_full + 2;                 // [2]
@@ -420,16 +460,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                         }
                     }
                 }
-                if (valid && col0 < P.N) {
-                    if (col0 + 32 <= P.N && (P.ldc % 4) == 0) {
-#pragma unroll
-                        for (int j = 0; j < 32; j += 4)
-                            *reinterpret_cast<float4*>(dst + col0 + j) =
-                                make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                                            __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
-                    } else {
-                        for (int j = 0; j < 32 && col0 + j < P.N; ++j) dst[col0 + j] = __uint_as_float(r[j]);
-                    }
+                if (!P.nostore && col0 < P.N) {
+                    uint8_t* tile = staging + (warp - 2) * (P.stg_cols * 128);
+                    const bool full_cols = col0 + 32 <= P.N && (P.ldc % 4) == 0;
+                    if (P.stg_cols == 32)      store_chunk_t<8>(r, tile, dst, valid, col0, P.N, full_cols, lane);
+                    else if (P.stg_cols == 16) store_chunk_t<4>(r, tile, dst, valid, col0, P.N, full_cols, lane);
+                    else                       store_chunk_t<2>(r, tile, dst, valid, col0, P.N, full_cols, lane);
                 }
             }
             if (!arrived && lane == 0)   // a warp without a chunk in this tile still arrives once
@@ -525,15 +561,30 @@ size_t stage_bytes_for(int bn) { return BM * BK * 4 + static_cast<size_t>(bn) * 
 
 // Ring depth: 2 CTAs per SM when two accumulator pairs fit TMEM (bn <= 128) and
 // the ring fits half the shared memory, else one CTA with a deeper ring.
-int stages_for(int bn) {
-    const size_t budget_two = 108 * 1024, budget_one = 216 * 1024;
-    const size_t sb = stage_bytes_for(bn);
-    if (bn <= 128 && 3 * sb + 2048 <= budget_two)
-        return static_cast<int>(std::min<size_t>(MAX_STAGES, (budget_two - 2048) / sb));
-    return static_cast<int>(std::min<size_t>(MAX_STAGES, (budget_one - 2048) / sb));
+size_t smem_for(int bn, int stages, int stg_cols) {
+    return stages * stage_bytes_for(bn) + 8 * static_cast<size_t>(stg_cols) * 128 + 1024 + 512 + 16 * bn;
 }
 
-size_t smem_for(int bn, int stages) { return stages * stage_bytes_for(bn) + 1024 + 512 + 16 * bn; }
+// Pipeline depth, epilogue staging width and CTAs per SM for an N-tile width.
+// bn <= 128 keeps two CTAs per SM (113 KB each) with >= 3 stages, taking the
+// widest epilogue transpose that still fits; wider tiles run one CTA per SM
+// and take the deepest ring, then the widest transpose.
+struct TcShape { int stages, stg_cols, per_sm; };
+TcShape pick_shape(int bn) {
+    const size_t sb = stage_bytes_for(bn), per_cta_two = 113 * 1024, per_cta_one = 227 * 1024;
+    if (bn <= 128)
+        for (int stg : {32, 16, 8}) {
+            const size_t fixed = smem_for(bn, 0, stg);
+            if (fixed + 3 * sb <= per_cta_two)
+                return {static_cast<int>(std::min<size_t>(MAX_STAGES, (per_cta_two - fixed) / sb)), stg, 2};
+        }
+    TcShape best{0, 32, 1};
+    for (int stg : {32, 16, 8}) {
+        const int st = static_cast<int>(std::min<size_t>(MAX_STAGES, (per_cta_one - smem_for(bn, 0, stg)) / sb));
+        if (st > best.stages) best = {st, stg, 1};
+    }
+    return best;
+}
 
 int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, TcParams& P) {
     static bool attr_done = false;
@@ -544,9 +595,19 @@ int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CU
     }
     if (P.tiles <= 0) return 0;
     P.tma_store = 0;
-    P.stages = stages_for(P.bn);
-    const size_t smem = smem_for(P.bn, P.stages);
-    const int per_sm = (P.bn <= 128 && 2 * smem <= 228 * 1024) ? 2 : 1;
+    const TcShape shp = pick_shape(P.bn);
+    P.stages = shp.stages;
+    P.stg_cols = shp.stg_cols;
+    static const int env_stages = getenv("NNCB_TC_STAGES") ? atoi(getenv("NNCB_TC_STAGES")) : 0;
+    static const int env_persm = getenv("NNCB_TC_PERSM") ? atoi(getenv("NNCB_TC_PERSM")) : 0;
+    static const int env_nostore = getenv("NNCB_TC_NOSTORE") ? 1 : 0;
+    static const int env_stg = getenv("NNCB_TC_STG") ? atoi(getenv("NNCB_TC_STG")) : 0;
+    if (env_stg == 8 || env_stg == 16 || env_stg == 32) P.stg_cols = env_stg;
+    if (env_stages > 0) P.stages = std::min(env_stages, MAX_STAGES);
+    P.nostore = env_nostore;
+    const size_t smem = smem_for(P.bn, P.stages, P.stg_cols);
+    int per_sm = (env_stages > 0) ? ((P.bn <= 128 && smem <= 113 * 1024) ? 2 : 1) : shp.per_sm;
+    if (env_persm > 0 && (env_persm == 1 || 2 * smem <= 228 * 1024)) per_sm = env_persm;
     unsigned grid = static_cast<unsigned>(std::min<int64_t>(P.tiles, static_cast<int64_t>(ctx->sm_count) * per_sm));
     if (P.colstats)
         tc_gemm_kernel<true><<<grid, THREADS, smem, ctx->stream>>>(ma, mb, mc, P);

@@ -1,0 +1,67 @@
+"""Micro-benchmark of the tcgen05 GEMM (nncb_gemm, kind::tf32) on the ResNet-50
+layer shapes at batch 256: per (layer, kind) device time from CUDA events over
+repeated launches, useful TFLOP/s = 2*N*OH*OW*CO*KH*KW*CI / time.
+
+    python tools/gemm_bench.py [--kinds fwd,dgrad,wgrad] [--reps 5] [--layers s0b,s2b]
+
+Kernel tuning knobs are read from the environment by gemm_tc.cu (NNCB_TC_*)."""
+import argparse
+import ctypes
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2205_10357_b200 as P  # noqa: E402
+from tests.nncb_ctypes import Dev, GemmDesc, K, ctx  # noqa: E402
+
+LAYERS = [  # name, h(=w) in, ci, co, k, s   (ResNet-50, batch 256)
+    ("s0b_a", 56, 256, 64, 1, 1), ("s0b_b", 56, 64, 64, 3, 1), ("s0b_c", 56, 64, 256, 1, 1),
+    ("s1b0_b", 56, 128, 128, 3, 2), ("s1b_b", 28, 128, 128, 3, 1), ("s1b_c", 28, 128, 512, 1, 1),
+    ("s1b_a", 28, 512, 128, 1, 1), ("s2b_b", 14, 256, 256, 3, 1), ("s2b_c", 14, 256, 1024, 1, 1),
+    ("s3b_b", 7, 512, 512, 3, 1), ("s3b_c", 7, 512, 2048, 1, 1), ("s3b_a", 7, 2048, 512, 1, 1),
+]
+
+
+def geom(n, h, ci, co, k, s):
+    oh = -(-h // s)
+    pt = max((oh - 1) * s + k - h, 0) // 2
+    return dict(n=n, ih=h, iw=h, ci=ci, co=co, kh=k, kw=k, sh=s, sw=s, oh=oh, ow=oh, pad_top=pt, pad_left=pt)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--kinds", default="fwd,dgrad,wgrad")
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--layers", default="")
+    a = ap.parse_args()
+    timer = P.DeviceTimer()
+    total = {}
+    for name, h, ci, co, k, s in LAYERS:
+        if a.layers and not any(name.startswith(x) for x in a.layers.split(",")):
+            continue
+        g = geom(a.batch, h, ci, co, k, s)
+        flops = 2.0 * a.batch * g["oh"] * g["ow"] * co * k * k * ci
+        x = Dev(nbytes=a.batch * h * h * ci * 4)
+        y = Dev(nbytes=a.batch * g["oh"] * g["ow"] * co * 4)
+        w = Dev(nbytes=k * k * ci * co * 4)
+        for kind in a.kinds.split(","):
+            code, A, B, O = {"fwd": (3, x, w, y), "dgrad": (4, y, w, x), "wgrad": (5, x, y, w)}[kind]
+            d = GemmDesc(kind=code, precision=0, epilogue=0, **g)
+            rc = K.nncb_gemm(ctx(), ctypes.byref(d), A.p, B.p, None, O.p)   # warm-up
+            assert rc == 0, K.nncb_last_error()
+            timer.start()
+            for _ in range(a.reps):
+                K.nncb_gemm(ctx(), ctypes.byref(d), A.p, B.p, None, O.p)
+            ms = timer.stop() / a.reps
+            total[kind] = total.get(kind, 0) + ms
+            print(f"{name:7s} {kind:5s} {ms*1000:8.1f} us {flops/ms/1e9:7.1f} TF/s", flush=True)
+    print("totals (ms, one instance per layer shape):", {k: round(v, 3) for k, v in total.items()})
+
+
+if __name__ == "__main__":
+    main()
