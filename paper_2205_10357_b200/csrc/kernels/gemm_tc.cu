@@ -297,45 +297,77 @@ __global__ void __launch_bounds__(THREADS, 2)
         // ================= TMA producer =================
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
-        uint32_t it = 0;   // global k-step counter (ring position)
+        // Ring position (slot, phase) advances incrementally and box coordinates
+        // are hoisted per tile / stepped like an odometer: this one thread
+        // issues every load, so no divisions may sit on the per-k-step path.
+        int slot = 0;
+        uint32_t phase = 0, filled = 0;
+        auto acquire = [&](uint8_t*& sa, uint64_t*& bar) {
+            if (filled >= static_cast<uint32_t>(STAGES)) mbar_wait(&empty[slot], phase ^ 1u);
+            sa = smem + slot * stage_bytes;
+            bar = &full[slot];
+            mbar_expect_tx(bar, stage_bytes);
+        };
+        auto advance = [&]() {
+            ++filled;
+            if (++slot == STAGES) { slot = 0; phase ^= 1u; }
+        };
         for (int64_t t = blockIdx.x; t < P.tiles; t += gridDim.x) {
             const Tile T = decode(t);
-            for (int i = 0; i < T.nk; ++i, ++it) {
-                const int s = it % STAGES;
-                if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
-                uint8_t* sa = smem + s * stage_bytes;
-                uint8_t* sb = sa + a_bytes;
-                mbar_expect_tx(&full[s], stage_bytes);
-                const int kb = T.kb_begin + i;
-                if (P.mode == MODE_CONV) {
-                    const int tap = P.tap0[T.phase] + kb / P.cblocks;
-                    const int c0 = (kb % P.cblocks) * BK;
-                    tma_load_4d(sa, &map_a, &full[s], c0, T.tw0 * P.mw + P.off_w[tap], T.th0 * P.mh + P.off_h[tap],
-                                T.tn0);
+            if (P.mode == MODE_CONV) {
+                int tap = P.tap0[T.phase], cb = 0;
+                const int aw = T.tw0 * P.mw, ah = T.th0 * P.mh, n0 = static_cast<int>(T.n0);
+                int xw = aw + P.off_w[tap], yh = ah + P.off_h[tap], br = P.brow[tap];
+                for (int i = 0; i < T.nk; ++i) {
+                    uint8_t* sa; uint64_t* bar;
+                    acquire(sa, bar);
+                    uint8_t* sb = sa + a_bytes;
+                    const int c0 = cb * BK;
+                    tma_load_4d(sa, &map_a, bar, c0, xw, yh, T.tn0);
                     if (P.b_mn) {
-                        for (int q = 0; q < P.bn / 32; ++q)
-                            tma_load_2d(sb + q * 4096, &map_b, &full[s], static_cast<int>(T.n0) + 32 * q,
-                                        P.brow[tap] + c0);
+                        for (int q = 0; q < P.bn / 32; ++q) tma_load_2d(sb + q * 4096, &map_b, bar, n0 + 32 * q, br + c0);
                     } else {
-                        tma_load_2d(sb, &map_b, &full[s], c0, P.brow[tap] + static_cast<int>(T.n0));
+                        tma_load_2d(sb, &map_b, bar, c0, br + n0);
                     }
-                } else {
-                    int r = kb;
-                    const int bw = r % P.tiles_w;
-                    r /= P.tiles_w;
-                    const int bh = r % P.tiles_h;
-                    const int bnn = r / P.tiles_h;
-                    const int x0 = bw * P.TW, y0 = bh * P.TH, n0 = bnn * P.TN;
-                    for (int q = 0; q < 4; ++q) {
-                        int64_t m = T.m0 + 32 * q;
-                        if (m >= P.M) m = T.m0;
-                        const int tap = static_cast<int>(m / P.ci), c = static_cast<int>(m % P.ci);
-                        const int dh = tap / P.kw_, dw = tap % P.kw_;
-                        tma_load_4d(sa + q * 4096, &map_a, &full[s], c, x0 * P.sw + dw - P.pl, y0 * P.sh + dh - P.pt,
-                                    n0);
+                    advance();
+                    if (++cb == P.cblocks && i + 1 < T.nk) {
+                        cb = 0;
+                        ++tap;
+                        xw = aw + P.off_w[tap]; yh = ah + P.off_h[tap]; br = P.brow[tap];
                     }
-                    for (int q = 0; q < P.bn / 32; ++q)
-                        tma_load_4d(sb + q * 4096, &map_b, &full[s], static_cast<int>(T.n0) + 32 * q, x0, y0, n0);
+                }
+            } else {
+                int ac[4], ax[4], ay[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    int64_t m = T.m0 + 32 * q;
+                    if (m >= P.M) m = T.m0;
+                    const int tap = static_cast<int>(m / P.ci);
+                    ac[q] = static_cast<int>(m % P.ci);
+                    ax[q] = tap % P.kw_ - P.pl;
+                    ay[q] = tap / P.kw_ - P.pt;
+                }
+                int r = T.kb_begin;
+                const int bw = r % P.tiles_w;
+                r /= P.tiles_w;
+                int x0 = bw * P.TW, y0 = (r % P.tiles_h) * P.TH, n0 = (r / P.tiles_h) * P.TN;
+                const int xend = P.tiles_w * P.TW, yend = P.tiles_h * P.TH;
+                const int nb = P.bn / 32, cn0 = static_cast<int>(T.n0);
+                for (int i = 0; i < T.nk; ++i) {
+                    uint8_t* sa; uint64_t* bar;
+                    acquire(sa, bar);
+                    uint8_t* sb = sa + a_bytes;
+                    const int xs = x0 * P.sw, ys = y0 * P.sh;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) tma_load_4d(sa + q * 4096, &map_a, bar, ac[q], xs + ax[q], ys + ay[q], n0);
+                    for (int q = 0; q < nb; ++q) tma_load_4d(sb + q * 4096, &map_b, bar, cn0 + 32 * q, x0, y0, n0);
+                    advance();
+                    x0 += P.TW;
+                    if (x0 >= xend) {
+                        x0 = 0;
+                        y0 += P.TH;
+                        if (y0 >= yend) { y0 = 0; n0 += P.TN; }
+                    }
                 }
             }
         }
@@ -345,7 +377,8 @@ __global__ void __launch_bounds__(THREADS, 2)
         const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (a_mn << 15) |
                                (static_cast<uint32_t>(P.b_mn) << 16) | ((static_cast<uint32_t>(P.bn) >> 3) << 17) |
                                ((static_cast<uint32_t>(BM) >> 4) << 24);
-        uint32_t it = 0, local = 0;
+        int slot = 0;
+        uint32_t phase = 0, local = 0;
         for (int64_t t = blockIdx.x; t < P.tiles; t += gridDim.x, ++local) {
             const Tile T = decode(t);
             const uint32_t acc = local & 1;
@@ -354,9 +387,10 @@ __global__ void __launch_bounds__(THREADS, 2)
             if (local >= 2) mbar_wait(&tmem_empty[acc], ((local / 2) - 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t d = tmem_base + acc * static_cast<uint32_t>(P.bn);
-            for (int i = 0; i < T.nk; ++i, ++it) {
-                const int s = it % STAGES;
-                mbar_wait(&full[s], (it / STAGES) & 1);
+            for (int i = 0; i < T.nk; ++i) {
+                const int s = slot;
+                mbar_wait(&full[s], phase);
+                if (++slot == STAGES) { slot = 0; phase ^= 1u; }
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t sa = smem_u32(smem + s * stage_bytes);
                 const uint32_t sb = sa + a_bytes;
@@ -568,7 +602,7 @@ size_t smem_for(int bn, int stages, int stg_cols) {
 // Pipeline depth, epilogue staging width and CTAs per SM for an N-tile width.
 // bn <= 128 keeps two CTAs per SM (113 KB each) with >= 3 stages, taking the
 // widest epilogue transpose that still fits; wider tiles run one CTA per SM
-// and take the deepest ring, then the widest transpose.
+// and take the widest transpose that still leaves a 3-deep ring.
 struct TcShape { int stages, stg_cols, per_sm; };
 TcShape pick_shape(int bn) {
     const size_t sb = stage_bytes_for(bn), per_cta_two = 113 * 1024, per_cta_one = 227 * 1024;
@@ -581,6 +615,7 @@ TcShape pick_shape(int bn) {
     TcShape best{0, 32, 1};
     for (int stg : {32, 16, 8}) {
         const int st = static_cast<int>(std::min<size_t>(MAX_STAGES, (per_cta_one - smem_for(bn, 0, stg)) / sb));
+        if (st >= 3) return {st, stg, 1};   // the wide transpose is worth more than a 4th stage
         if (st > best.stages) best = {st, stg, 1};
     }
     return best;
