@@ -38,6 +38,8 @@ int         nncb_host_alloc(size_t bytes, void** out);        /* pinned host mem
 int         nncb_host_free(void* ptr);
 int         nncb_memset(nncb_ctx* ctx, void* dst, int value, size_t bytes);
 int         nncb_h2d(nncb_ctx* ctx, void* dst, const void* src, size_t bytes);
+/* Parallel host memcpy on the library's copy threads (host staging helper). */
+int         nncb_host_copy(void* dst, const void* src, size_t bytes);
 int         nncb_d2h(nncb_ctx* ctx, void* dst, const void* src, size_t bytes);
 int         nncb_d2d(nncb_ctx* ctx, void* dst, const void* src, size_t bytes);
 int         nncb_sync(nncb_ctx* ctx);

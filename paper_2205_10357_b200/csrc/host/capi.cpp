@@ -1,5 +1,6 @@
 // capi.cpp -- extern "C" surface of libnnc_b200.so (include/nnc_b200.h).
 #include "nnc_b200.h"
+#include "nncb.h"
 
 #include <cstring>
 #include <memory>
@@ -26,7 +27,7 @@ struct nnc_model {
     std::map<std::string, Tensor> inputs;
     std::map<std::string, Tensor> outputs;
     std::map<std::string, Tensor> grads;
-    std::unique_ptr<runtime::Trainer> trainer;
+    runtime::Trainer* trainer = nullptr;   // runtime::shared_trainer's, owned by the runtime cache
     std::string desc;
 };
 
@@ -127,7 +128,7 @@ nnc_model* nnc_model_compile(const char* doc, int precision) {
 void nnc_model_free(nnc_model* m) {
     if (!m) return;
     try {
-        m->trainer.reset();
+        m->trainer = nullptr;
         runtime::release(m->plans);
         runtime::default_device().evict_model(*m->host);
     } catch (...) {
@@ -173,7 +174,17 @@ int nnc_model_get_weight(nnc_model* m, const char* name, float* out, int64_t n) 
 }
 
 int nnc_model_set_input(nnc_model* m, const char* name, const float* data, const int64_t* dims, int rank) {
-    return guarded([&] { m->inputs[name] = make(data, dims, rank); });
+    return guarded([&] {
+        // steady-state steps feed the same shapes: copy into the existing
+        // storage on the copy threads instead of allocating (and zero-filling)
+        // a fresh tensor every call
+        std::vector<int64_t> d(dims, dims + rank);
+        auto it = m->inputs.find(name);
+        if (it == m->inputs.end() || it->second.dims() != d) {
+            it = m->inputs.insert_or_assign(name, Tensor(DType::F32, d)).first;
+        }
+        nncb_host_copy(it->second.data(), data, it->second.byte_size());
+    });
 }
 
 int nnc_model_run(nnc_model* m, int role) {
@@ -212,7 +223,7 @@ int nnc_model_grad(nnc_model* m, const char* weight, float* out, int64_t n) {
 int nnc_model_trainer_prepare(nnc_model* m, const float* target, int64_t n) {
     return guarded([&] {
         auto& dev = runtime::default_device();
-        m->trainer = std::make_unique<runtime::Trainer>(m->plans, *m->host, dev, m->opts);
+        m->trainer = &runtime::shared_trainer(m->plans, *m->host, dev, m->opts);
         Tensor t = target_tensor(m, target, n);
         // one full host step uploads inputs + target and warms every kernel
         m->trainer->step(m->inputs, t, 0.0);

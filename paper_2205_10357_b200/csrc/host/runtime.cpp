@@ -971,12 +971,13 @@ std::map<std::pair<uint64_t, uint64_t>, std::unique_ptr<Trainer>>& trainers() {
     static std::map<std::pair<uint64_t, uint64_t>, std::unique_ptr<Trainer>> m;
     return m;
 }
-Trainer& trainer_for(const plan::VersionPlans& plans, HostModel& model, Device& dev, const ExecOptions& opts) {
+}  // namespace
+
+Trainer& shared_trainer(const plan::VersionPlans& plans, HostModel& model, Device& dev, const ExecOptions& opts) {
     auto& t = trainers()[{plans.train_fwd.uid, model.uid()}];
     if (!t || t->impl->dev != &dev) t = std::make_unique<Trainer>(plans, model, dev, opts);
     return *t;
 }
-}  // namespace
 
 void release(const plan::VersionPlans& plans) {
     for (auto it = exec_caches().begin(); it != exec_caches().end();) {
@@ -993,14 +994,14 @@ double train_step(const plan::VersionPlans& plans, const std::map<std::string, T
     Device& dev = device ? *device : default_device();
     if (opts.trace)
         for (const char* ph : {"forward", "loss", "backward", "update"}) opts.trace->push_back(ph);
-    return trainer_for(plans, model, dev, opts).step(inputs, target, lr);
+    return shared_trainer(plans, model, dev, opts).step(inputs, target, lr);
 }
 
 std::map<std::string, Tensor> gradients(const plan::VersionPlans& plans, const std::map<std::string, Tensor>& inputs,
                                         const Tensor& target, HostModel& model, double* loss, Device* device,
                                         const ExecOptions& opts) {
     Device& dev = device ? *device : default_device();
-    Trainer& tr = trainer_for(plans, model, dev, opts);
+    Trainer& tr = shared_trainer(plans, model, dev, opts);
     Trainer::Impl& I = *tr.impl;
     check_inputs(plans.train_fwd, inputs);
     nncb_ctx* ctx = dev.ctx();

@@ -132,7 +132,13 @@ double train_step(const plan::VersionPlans& plans, const std::map<std::string, T
                   const ExecOptions& opts = {});
 
 /// Drops every device program / CUDA graph / trainer cached for these plans.
+class Trainer;
 void release(const plan::VersionPlans& plans);
+
+// The Trainer that train_step / gradients use for (plans, model) on `device`,
+// created on first use and kept until release(plans). Device-resident
+// stepping (Trainer::step_device) through it shares the same arena and graph.
+Trainer& shared_trainer(const plan::VersionPlans& plans, HostModel& model, Device& device, const ExecOptions& opts = {});
 
 /// Forward + loss + backward without the update (for gradient parity tests).
 std::map<std::string, Tensor> gradients(const plan::VersionPlans& plans,

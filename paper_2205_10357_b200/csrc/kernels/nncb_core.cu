@@ -77,6 +77,7 @@ int nncb_destroy(nncb_ctx* c) {
         (void)k;
         nncb::ew_release(v);
     }
+    nncb::staging_release(c);
     if (c->scratch) cudaFree(c->scratch);
     for (void* p : c->retired) cudaFree(p);
     if (c->workspace) cudaFree(c->workspace);
@@ -123,11 +124,6 @@ int nncb_host_free(void* p) {
 
 int nncb_memset(nncb_ctx* c, void* dst, int v, size_t bytes) {
     if (bytes) NNCB_CUDA(cudaMemsetAsync(dst, v, bytes, c->stream));
-    return 0;
-}
-
-int nncb_h2d(nncb_ctx* c, void* dst, const void* src, size_t bytes) {
-    if (bytes) NNCB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
     return 0;
 }
 

@@ -30,11 +30,13 @@ struct nncb_ctx {
     std::vector<void*> retired;          // outgrown scratch kept alive (captured graphs may use it)
     void* workspace = nullptr;           // im2col columns (separate from reduction scratch)
     size_t workspace_bytes = 0;
+    void* staging = nullptr;             // pinned upload ring (host_io.cu), created on first large h2d
 };
 
 namespace nncb {
 
 void set_error(const std::string& msg);
+void staging_release(nncb_ctx* c);
 int fail(const std::string& msg);
 
 #define NNCB_CUDA(expr)                                                                       \
