@@ -149,6 +149,10 @@ typedef struct {
 /* FWD:   a = x, b = weight, out = y (bias optional)
  * DGRAD: a = g, b = weight, out = gx
  * WGRAD: a = x, b = g,      out = gw                                    */
+/* 1 if the calling thread's last nncb_gemm ran on the tcgen05 tensor-core path, 0 if on the exact fp32 path. */
+int nncb_gemm_last_path(void);
+/* Route for convolutions with channels % 32 != 0: 1 = builder-warp gather, 0 = im2col (default). */
+int nncb_gemm_set_manual_a(int on);
 int nncb_gemm(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b,
               const float* bias, float* out);
 

@@ -226,6 +226,14 @@ int gemm_simt(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const floa
 
 }  // namespace nncb
 
+namespace {
+thread_local int g_last_path = -1;
+}
+
+// Which kernel family ran the calling thread's last nncb_gemm: 1 = tcgen05
+// (tf32 tensor cores), 0 = exact fp32 path. Lets tests prove the path taken.
+extern "C" int nncb_gemm_last_path(void) { return g_last_path; }
+
 extern "C" int nncb_gemm(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const float* bias,
                          float* out) {
     const bool colstats = (d->epilogue & NNCB_EPI_COLSTATS) && d->colstats;
@@ -234,8 +242,10 @@ extern "C" int nncb_gemm(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a,
     if (d->precision == NNCB_PREC_TF32) {
         bool handled = false;
         int rc = nncb::gemm_tc(ctx, d, a, b, bias, out, &handled);
+        g_last_path = 1;
         if (rc || handled) return rc;
     }
+    g_last_path = 0;
     if (int rc = nncb::gemm_simt(ctx, d, a, b, bias, out)) return rc;
     if (colstats) {
         const bool dense = d->kind == NNCB_DENSE_FWD;

@@ -23,6 +23,7 @@
 // -> registers -> bias -> 128-bit global stores). A 4-stage smem ring with
 // full/empty mbarriers couples TMA and MMA; tcgen05.commit releases stages.
 // Operand tiles use the 128-byte swizzle (TMA and UMMA descriptors agree).
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -76,6 +77,12 @@ struct TcParams {
     int nostore;        // tuning knob: skip the output stores (epilogue cost probe)
     int stg_cols;       // epilogue transpose width per pass: 32, 16 or 8 columns (4/2/1 KB per warp)
     double* colstats;   // fused BatchNorm statistics: [0,N) sum, [N,2N) sum of squares
+    // --- manual A (channel counts that do not fill a 32-wide TMA block) -----
+    // Builder warps gather A straight from the NHWC activation into the
+    // K-major 128B-swizzled stage layout: no im2col matrix in HBM.
+    const float* xa;    // activation [gn?, ih, iw, ci]
+    int ih_, iw_;       // activation image dims
+    int K_;             // kh*kw*ci
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -89,6 +96,21 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
+}
+
+// 4-byte global->shared async copy; src_bytes 0 zero-fills the destination
+__device__ __forceinline__ void cp_async4(void* dst, const float* src, int src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+                 : "memory");
+}
+
+// arrive on `bar` once all of this thread's prior cp.async copies have landed
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -218,8 +240,8 @@ __device__ __forceinline__ void store_chunk_t(const uint32_t (&r)[32], uint8_t* 
 // tiles b, b + grid, ... The smem ring (TMA -> MMA) and the double-buffered TMEM
 // accumulator (MMA -> epilogue) carry their phases across tiles, so the
 // epilogue of one tile overlaps the main loop of the next.
-template <bool CS>
-__global__ void __launch_bounds__(THREADS, 2)
+template <bool CS, bool MA>
+__global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MA ? 1 : 2)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_c, const __grid_constant__ TcParams P) {
     const int STAGES = P.stages;
@@ -236,13 +258,15 @@ __global__ void __launch_bounds__(THREADS, 2)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
     // CS: per-CTA column sum / sum of squares of the current column range
     double* cs_acc = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(tmem_slot) + 16);
+    // MA: gather tables after cs_acc (fwd: per K index; wgrad: per box pixel)
+    int* ma_tab = reinterpret_cast<int*>(cs_acc + 2 * P.bn);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     if (CS)
         for (int i = threadIdx.x; i < 2 * P.bn; i += blockDim.x) cs_acc[i] = 0.0;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], MA ? 1 + 128 : 1);   // MA: + one arrival per builder thread
             mbar_init(&empty[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
@@ -250,6 +274,25 @@ __global__ void __launch_bounds__(THREADS, 2)
             mbar_init(&tmem_empty[s], 8);                 // one arrival per epilogue warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (MA) {
+        if (P.mode == MODE_CONV) {
+            // K index -> (source offset within the patch, dh, dw); padding K rows read nothing
+            const int kpad = P.cblocks * BK;
+            for (int k = threadIdx.x; k < kpad; k += blockDim.x) {
+                const int c = k % P.ci, tap = k / P.ci, dw = tap % P.kw_, dh = tap / P.kw_;
+                ma_tab[k] = (dh * P.iw_ + dw) * P.ci + c;
+                ma_tab[kpad + k] = k < P.K_ ? dh : -(1 << 20);
+                ma_tab[2 * kpad + k] = dw;
+            }
+        } else {
+            // pixel k of a 32-pixel box -> (dn, dy, dx)
+            for (int k = threadIdx.x; k < BK; k += blockDim.x) {
+                ma_tab[k] = k / (P.TW * P.TH);
+                ma_tab[BK + k] = (k / P.TW) % P.TH;
+                ma_tab[2 * BK + k] = k % P.TW;
+            }
+        }
     }
     const uint32_t tmem_cols = 2 * static_cast<uint32_t>(P.bn);   // two accumulators
     if (warp == 1) {
@@ -295,7 +338,7 @@ __global__ void __launch_bounds__(THREADS, 2)
 
     if (warp == 0 && lane == 0) {
         // ================= TMA producer =================
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+        if (!MA) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
         // Ring position (slot, phase) advances incrementally and box coordinates
         // are hoisted per tile / stepped like an odometer: this one thread
@@ -306,7 +349,7 @@ __global__ void __launch_bounds__(THREADS, 2)
             if (filled >= static_cast<uint32_t>(STAGES)) mbar_wait(&empty[slot], phase ^ 1u);
             sa = smem + slot * stage_bytes;
             bar = &full[slot];
-            mbar_expect_tx(bar, stage_bytes);
+            mbar_expect_tx(bar, MA ? b_bytes : stage_bytes);
         };
         auto advance = [&]() {
             ++filled;
@@ -323,7 +366,7 @@ __global__ void __launch_bounds__(THREADS, 2)
                     acquire(sa, bar);
                     uint8_t* sb = sa + a_bytes;
                     const int c0 = cb * BK;
-                    tma_load_4d(sa, &map_a, bar, c0, xw, yh, T.tn0);
+                    if (!MA) tma_load_4d(sa, &map_a, bar, c0, xw, yh, T.tn0);
                     if (P.b_mn) {
                         for (int q = 0; q < P.bn / 32; ++q) tma_load_2d(sb + q * 4096, &map_b, bar, n0 + 32 * q, br + c0);
                     } else {
@@ -358,8 +401,11 @@ __global__ void __launch_bounds__(THREADS, 2)
                     acquire(sa, bar);
                     uint8_t* sb = sa + a_bytes;
                     const int xs = x0 * P.sw, ys = y0 * P.sh;
+                    if (!MA) {
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) tma_load_4d(sa + q * 4096, &map_a, bar, ac[q], xs + ax[q], ys + ay[q], n0);
+                        for (int q = 0; q < 4; ++q)
+                            tma_load_4d(sa + q * 4096, &map_a, bar, ac[q], xs + ax[q], ys + ay[q], n0);
+                    }
                     for (int q = 0; q < nb; ++q) tma_load_4d(sb + q * 4096, &map_b, bar, cn0 + 32 * q, x0, y0, n0);
                     advance();
                     x0 += P.TW;
@@ -373,7 +419,7 @@ __global__ void __launch_bounds__(THREADS, 2)
         }
     } else if (warp == 1 && lane == 0) {
         // ================= MMA issuer (single thread) =================
-        const uint32_t a_mn = P.mode == MODE_WGRAD ? 1u : 0u;
+        const uint32_t a_mn = (P.mode == MODE_WGRAD && !MA) ? 1u : 0u;
         const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (a_mn << 15) |
                                (static_cast<uint32_t>(P.b_mn) << 16) | ((static_cast<uint32_t>(P.bn) >> 3) << 17) |
                                ((static_cast<uint32_t>(BM) >> 4) << 24);
@@ -390,6 +436,7 @@ __global__ void __launch_bounds__(THREADS, 2)
             for (int i = 0; i < T.nk; ++i) {
                 const int s = slot;
                 mbar_wait(&full[s], phase);
+                if (MA) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // cp.async data -> async proxy
                 if (++slot == STAGES) { slot = 0; phase ^= 1u; }
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t sa = smem_u32(smem + s * stage_bytes);
@@ -403,6 +450,74 @@ __global__ void __launch_bounds__(THREADS, 2)
                 mma_commit(&empty[s]);
             }
             mma_commit(&tmem_full[acc]);
+        }
+    } else if (MA && warp >= 10) {
+        // ================= A builders (warps 10..13, MA only) =================
+        // Thread t owns row t of the 128 x 32 A tile: it gathers 32 values,
+        // writes them as eight 16-byte chunks at the 128B-swizzled positions
+        // (chunk j of row t lands at j ^ (t % 8), as TMA would place them),
+        // makes the writes visible to the tensor core's async proxy, and
+        // arrives on the stage's full barrier.
+        const int t = threadIdx.x - THREADS;
+        int slot = 0;
+        uint32_t phase = 0, filled = 0;
+        const int kpad = P.cblocks * BK;
+        for (int64_t tt = blockIdx.x; tt < P.tiles; tt += gridDim.x) {
+            const Tile T = decode(tt);
+            if (P.mode == MODE_CONV) {
+                const int pw = T.tw0 + t % P.TW, ph = T.th0 + (t / P.TW) % P.TH, pn = T.tn0 + t / (P.TW * P.TH);
+                const bool pv = pw < P.gw && ph < P.gh && pn < P.gn;
+                const int iy0 = ph * P.sh - P.pt, ix0 = pw * P.sw - P.pl;
+                const float* xb = P.xa + ((static_cast<int64_t>(pv ? pn : 0) * P.ih_ + iy0) * P.iw_ + ix0) * P.ci;
+                for (int i = 0; i < T.nk; ++i) {
+                    if (filled >= static_cast<uint32_t>(STAGES)) mbar_wait(&empty[slot], phase ^ 1u);
+                    uint8_t* row = smem + slot * stage_bytes + t * 128;
+                    // asynchronous gathers (masked elements zero-fill), so the
+                    // builders run up to STAGES k-steps ahead of the MMA
+#pragma unroll
+                    for (int k = 0; k < BK; ++k) {
+                        const int kk = i * BK + k;
+                        const int iy = iy0 + ma_tab[kpad + kk], ix = ix0 + ma_tab[2 * kpad + kk];
+                        const bool ok = pv && iy >= 0 && iy < P.ih_ && ix >= 0 && ix < P.iw_;
+                        cp_async4(row + (((k >> 2) ^ (t & 7)) << 4) + (k & 3) * 4, ok ? xb + ma_tab[kk] : P.xa, ok ? 4 : 0);
+                    }
+                    cp_async_arrive(&full[slot]);
+                    ++filled;
+                    if (++slot == STAGES) { slot = 0; phase ^= 1u; }
+                }
+            } else {
+                const int64_t m = T.m0 + t;
+                const bool mv = m < P.M;
+                const int tap = mv ? static_cast<int>(m / P.ci) : 0, c = mv ? static_cast<int>(m % P.ci) : 0;
+                const int dy = tap / P.kw_ - P.pt, dx = tap % P.kw_ - P.pl;
+                int r = T.kb_begin;
+                const int bw = r % P.tiles_w;
+                r /= P.tiles_w;
+                int x0 = bw * P.TW, y0 = (r % P.tiles_h) * P.TH, n0 = (r / P.tiles_h) * P.TN;
+                const int xend = P.tiles_w * P.TW, yend = P.tiles_h * P.TH;
+                for (int i = 0; i < T.nk; ++i) {
+                    if (filled >= static_cast<uint32_t>(STAGES)) mbar_wait(&empty[slot], phase ^ 1u);
+                    uint8_t* row = smem + slot * stage_bytes + t * 128;
+#pragma unroll
+                    for (int k = 0; k < BK; ++k) {
+                        const int on = n0 + ma_tab[k], oy = y0 + ma_tab[BK + k], ox = x0 + ma_tab[2 * BK + k];
+                        const int iy = oy * P.sh + dy, ix = ox * P.sw + dx;
+                        const bool ok = mv && on < P.gn && oy < P.gh && ox < P.gw && iy >= 0 && iy < P.ih_ &&
+                                        ix >= 0 && ix < P.iw_;
+                        const int64_t off = ((static_cast<int64_t>(on) * P.ih_ + iy) * P.iw_ + ix) * P.ci + c;
+                        cp_async4(row + (((k >> 2) ^ (t & 7)) << 4) + (k & 3) * 4, P.xa + (ok ? off : 0), ok ? 4 : 0);
+                    }
+                    cp_async_arrive(&full[slot]);
+                    ++filled;
+                    if (++slot == STAGES) { slot = 0; phase ^= 1u; }
+                    x0 += P.TW;
+                    if (x0 >= xend) {
+                        x0 = 0;
+                        y0 += P.TH;
+                        if (y0 >= yend) { y0 = 0; n0 += P.TN; }
+                    }
+                }
+            }
         }
     } else if (warp >= 2) {
         // ================= epilogue (warps 2..9) =================
@@ -595,8 +710,9 @@ size_t stage_bytes_for(int bn) { return BM * BK * 4 + static_cast<size_t>(bn) * 
 
 // Ring depth: 2 CTAs per SM when two accumulator pairs fit TMEM (bn <= 128) and
 // the ring fits half the shared memory, else one CTA with a deeper ring.
-size_t smem_for(int bn, int stages, int stg_cols) {
-    return stages * stage_bytes_for(bn) + 8 * static_cast<size_t>(stg_cols) * 128 + 1024 + 512 + 16 * bn;
+size_t smem_for(int bn, int stages, int stg_cols, int ma_tab_ints = 0) {
+    return stages * stage_bytes_for(bn) + 8 * static_cast<size_t>(stg_cols) * 128 + 1024 + 512 + 16 * bn +
+           4 * static_cast<size_t>(ma_tab_ints);
 }
 
 // Pipeline depth, epilogue staging width and CTAs per SM for an N-tile width.
@@ -624,8 +740,10 @@ TcShape pick_shape(int bn) {
 int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, TcParams& P) {
     static bool attr_done = false;
     if (!attr_done) {
-        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr_done = true;
     }
     if (P.tiles <= 0) return 0;
@@ -640,14 +758,27 @@ int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CU
     if (env_stg == 8 || env_stg == 16 || env_stg == 32) P.stg_cols = env_stg;
     if (env_stages > 0) P.stages = std::min(env_stages, MAX_STAGES);
     P.nostore = env_nostore;
-    const size_t smem = smem_for(P.bn, P.stages, P.stg_cols);
+    const bool manual = P.xa != nullptr;
+    const int tab_ints = manual ? 3 * std::max(P.cblocks * BK, BK) : 0;
+    if (manual) {   // one CTA per SM (448 threads); take the deepest ring that fits
+        P.stg_cols = 32;
+        const size_t fixed = smem_for(P.bn, 0, P.stg_cols, tab_ints);
+        P.stages = static_cast<int>(std::min<size_t>(MAX_STAGES, (227 * 1024 - fixed) / stage_bytes_for(P.bn)));
+    }
+    const size_t smem = smem_for(P.bn, P.stages, P.stg_cols, tab_ints);
     int per_sm = (env_stages > 0) ? ((P.bn <= 128 && smem <= 113 * 1024) ? 2 : 1) : shp.per_sm;
     if (env_persm > 0 && (env_persm == 1 || 2 * smem <= 228 * 1024)) per_sm = env_persm;
+    if (manual) per_sm = 1;
     unsigned grid = static_cast<unsigned>(std::min<int64_t>(P.tiles, static_cast<int64_t>(ctx->sm_count) * per_sm));
-    if (P.colstats)
-        tc_gemm_kernel<true><<<grid, THREADS, smem, ctx->stream>>>(ma, mb, mc, P);
+    const unsigned threads = manual ? THREADS + 128 : THREADS;
+    if (P.colstats && manual)
+        tc_gemm_kernel<true, true><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
+    else if (manual)
+        tc_gemm_kernel<false, true><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
+    else if (P.colstats)
+        tc_gemm_kernel<true, false><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
     else
-        tc_gemm_kernel<false><<<grid, THREADS, smem, ctx->stream>>>(ma, mb, mc, P);
+        tc_gemm_kernel<false, false><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
     NNCB_LAUNCHED(ctx);
     return 0;
 }
@@ -669,7 +800,7 @@ bool encode_out_3d(CUtensorMap* map, float* base, int64_t n, int64_t m, int64_t 
 namespace nncb {
 
 int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t lda, const float* b,
-                 const float* bias, float* out, bool* handled);
+                 const float* bias, float* out, bool* handled, bool manual = false);
 
 // im2col for the 3-channel stem: one warp per output pixel writes its row of
 // kh*kw*ci (padded to ldk) columns contiguously; the per-column source offset
@@ -704,10 +835,19 @@ __global__ void __launch_bounds__(256) im2col_k(const float* __restrict__ x, flo
     }
 }
 
+std::atomic<int> g_manual_a{getenv("NNCB_TC_MANUAL_A") ? 1 : 0};
+
 int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const float* bias, float* out,
             bool* handled) {
     *handled = false;
     const bool conv = d->kind >= NNCB_CONV_FWD;
+    if (conv && d->ci % 32 != 0 && d->kh * d->kw > 1 && (d->kind == NNCB_CONV_FWD || d->kind == NNCB_CONV_WGRAD)) {
+        // Channels that do not fill a 32-wide K block: builder warps can gather
+        // A from the activation directly (no im2col matrix). Their 4-byte
+        // gathers are slower than im2col for the stem today, so this is opt-in
+        // (NNCB_TC_MANUAL_A=1) until the gather stages through a TMA patch.
+        if (g_manual_a.load(std::memory_order_relaxed)) return gemm_tc_impl(ctx, d, a, 0, b, bias, out, handled, true);
+    }
     if (conv && d->ci % 32 != 0 && (d->kind == NNCB_CONV_FWD || d->kind == NNCB_CONV_WGRAD) && drv::table().ok) {
         // Channels that do not fill a 32-wide K block (the 3-channel stem): lower
         // to a dense tensor-core GEMM over an im2col workspace [pixels, kh*kw*ci].
@@ -736,7 +876,7 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
 }
 
 int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t lda, const float* b,
-                 const float* bias, float* out, bool* handled) {
+                 const float* bias, float* out, bool* handled, bool manual) {
     *handled = false;
     if (!drv::table().ok) return 0;
     static const int dbg = getenv("NNCB_TC_DEBUG") ? 1 : 0;
@@ -754,8 +894,10 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
     // 16-byte row pitches, taps fit the parameter block, int32 coordinates.
     const bool single_tap = kh * kw == 1;
     if (lda == 0) lda = ci;
-    if (co % 4 != 0 || co < 16 || kh * kw > MAX_TAPS || lda % 4 != 0) return 0;
-    if (!single_tap && ci % 32 != 0) return 0;
+    if (co % 4 != 0 || co < 16) return 0;
+    if (!manual && (kh * kw > MAX_TAPS || lda % 4 != 0)) return 0;
+    if (!single_tap && ci % 32 != 0 && !manual) return 0;
+    if (manual && (dense || kind == 1)) return 0;
     if (single_tap && ci % 4 != 0 && lda == ci) return 0;
     if (kind == 1 && ((!single_tap && co % 32 != 0) || sh > 2 || sw > 2)) return 0;
     if (n * std::max(ih, oh) * std::max(iw, ow) * std::max(ci, co) >= (int64_t(1) << 31) * 4) return 0;
@@ -764,6 +906,14 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
     memset(&P, 0, sizeof(P));
     P.debug = dbg;
     CUtensorMap ma, mb;
+    memset(&ma, 0, sizeof(ma));
+    if (manual) {
+        P.xa = a;
+        P.ih_ = (int)ih; P.iw_ = (int)iw;
+        P.K_ = (int)(kh * kw * ci);
+        P.ci = (int)ci; P.kw_ = (int)kw;
+        P.sh = (int)sh; P.sw = (int)sw; P.pt = (int)pt; P.pl = (int)pl;
+    }
     if (kind == 0 || kind == 1) {
         P.mode = MODE_CONV;
         const bool fwd = kind == 0;
@@ -779,10 +929,14 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
             P.mh = (int)sh; P.mw = (int)sw;
             P.ntaps[0] = (int)(kh * kw);
             P.tap0[0] = 0;
-            for (int t = 0; t < kh * kw; ++t) {
-                P.off_h[t] = (int)(t / kw - pt);
-                P.off_w[t] = (int)(t % kw - pl);
-                P.brow[t] = (int)(t * ci);
+            if (manual) {   // one "tap" whose K blocks run over the whole flattened (tap, ci) patch
+                P.ntaps[0] = 1;
+                P.cblocks = (int)((kh * kw * ci + BK - 1) / BK);
+            }
+            for (int t = 0; t < (manual ? 1 : kh * kw); ++t) {
+                P.off_h[t] = manual ? 0 : (int)(t / kw - pt);
+                P.off_w[t] = manual ? 0 : (int)(t % kw - pl);
+                P.brow[t] = manual ? 0 : (int)(t * ci);
             }
         } else {
             // sub-pixel phases: h = a*sh + ph; taps with (ph + pt - dh) % sh == 0
@@ -820,7 +974,8 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
         // A: the activation (x for fwd, g for dgrad) as {C, W, H, N}
         const float* act = a;
         if (fwd) {
-            if (!encode_4d(&ma, act, ci, iw, ih, n, 32, P.TW * (int)sw, P.TH * (int)sh, P.TN, (int)sw, (int)sh, false, lda))
+            if (!manual &&
+                !encode_4d(&ma, act, ci, iw, ih, n, 32, P.TW * (int)sw, P.TH * (int)sh, P.TN, (int)sw, (int)sh, false, lda))
                 return 1;
         } else {
             if (!encode_4d(&ma, act, co, ow, oh, n, 32, P.TW, P.TH, P.TN, 1, 1, false)) return 1;
@@ -871,7 +1026,8 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
     splits = std::max<int64_t>(1, std::min<int64_t>(splits, std::max<int64_t>(kboxes / 8, 1)));
     splits = std::min<int64_t>(splits, 128);
     P.splits = static_cast<int>(splits);
-    if (!encode_4d(&ma, a, ci, iw, ih, n, 32, P.TW * (int)sw, P.TH * (int)sh, P.TN, (int)sw, (int)sh, true, lda))
+    if (!manual &&
+        !encode_4d(&ma, a, ci, iw, ih, n, 32, P.TW * (int)sw, P.TH * (int)sh, P.TN, (int)sw, (int)sh, true, lda))
         return 1;
     if (!encode_4d(&mb, b, co, ow, oh, n, 32, P.TW, P.TH, P.TN, 1, 1, true)) return 1;
     P.out = out;
@@ -896,3 +1052,10 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
 }
 
 }  // namespace nncb
+
+// Route selection for convolutions whose channel count does not fill a 32-wide
+// K block: 1 = builder-warp gather (manual A), 0 = im2col workspace.
+extern "C" int nncb_gemm_set_manual_a(int on) {
+    nncb::g_manual_a.store(on ? 1 : 0);
+    return 0;
+}

@@ -24,6 +24,8 @@ for name, res, args in [
     ("nncb_d2h", _I, [_P, _P, _P, ctypes.c_size_t]),
     ("nncb_memset", _I, [_P, _P, _I, ctypes.c_size_t]),
     ("nncb_gemm", _I, [_P, ctypes.POINTER(GemmDesc), _P, _P, _P, _P]),
+    ("nncb_gemm_last_path", _I, []),
+    ("nncb_gemm_set_manual_a", _I, [_I]),
 ]:
     fn = getattr(K, name)
     fn.restype, fn.argtypes = res, args

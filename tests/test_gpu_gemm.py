@@ -5,7 +5,7 @@ strided / padded convolutions and ragged tile edges. Bound: 2e-2 of max|ref|
 import numpy as np
 import pytest
 
-from tests.nncb_ctypes import Dev, GemmDesc, gemm
+from tests.nncb_ctypes import K, Dev, GemmDesc, gemm
 
 pytestmark = pytest.mark.gpu
 
@@ -20,12 +20,16 @@ def conv_geom(n, ih, iw, ci, co, k, s, same=True):
     return dict(n=n, ih=ih, iw=iw, ci=ci, co=co, kh=k, kw=k, sh=s, sw=s, oh=oh, ow=ow, pad_top=pt, pad_left=pl)
 
 
-def run_both(kind, geo, a, b, bias, out_shape):
+def run_both(kind, geo, a, b, bias, out_shape, expect_tc=None):
+    """tf32 tensor-core result and exact result; expect_tc=True asserts the
+    tf32 request really ran on the tcgen05 kernel (no silent exact fallback)."""
     outs = []
     for prec in (0, 1):
         d = GemmDesc(kind=kind, precision=prec, epilogue=1 if bias is not None else 0, **geo)
         o = Dev(nbytes=int(np.prod(out_shape)) * 4)
         gemm(d, a, b, bias, o)   # a, b, bias are held by the caller
+        if prec == 0 and expect_tc is not None:
+            assert K.nncb_gemm_last_path() == int(expect_tc), "tensor-core path not taken"
         outs.append(o.get(out_shape))
     return outs
 
@@ -40,6 +44,8 @@ CONVS = [
     (2, 32, 32, 3, 64, 7, 2), (2, 16, 16, 16, 32, 3, 1),
     (2, 14, 14, 64, 64, 3, 1), (2, 13, 11, 64, 96, 3, 2), (4, 7, 7, 128, 256, 1, 1),
     (2, 16, 16, 32, 64, 1, 2), (1, 9, 9, 64, 32, 3, 2), (3, 8, 8, 96, 128, 3, 1),
+    # channel counts below a 32-wide block: builder-warp (manual A) path
+    (3, 19, 23, 3, 32, 3, 1), (2, 15, 15, 12, 64, 5, 2), (1, 30, 30, 4, 128, 7, 2),
 ]
 
 
@@ -51,7 +57,7 @@ def test_conv_fwd(shape):
     x = rng.uniform(-1, 1, (n, ih, iw, ci)).astype(np.float32)
     w = rng.uniform(-1, 1, (k, k, ci, co)).astype(np.float32)
     bias = rng.uniform(-1, 1, co).astype(np.float32)
-    tc, ex = run_both(CONV_FWD, g, Dev(x), Dev(w), Dev(bias), (n, g["oh"], g["ow"], co))
+    tc, ex = run_both(CONV_FWD, g, Dev(x), Dev(w), Dev(bias), (n, g["oh"], g["ow"], co), expect_tc=True)
     check(tc, ex)
 
 
@@ -62,7 +68,8 @@ def test_conv_dgrad(shape):
     rng = np.random.default_rng(1)
     gy = rng.uniform(-1, 1, (n, g["oh"], g["ow"], co)).astype(np.float32)
     w = rng.uniform(-1, 1, (k, k, ci, co)).astype(np.float32)
-    tc, ex = run_both(CONV_DGRAD, g, Dev(gy), Dev(w), None, (n, ih, iw, ci))
+    tc_ok = k == 1 or (ci % 32 == 0 and co % 32 == 0)
+    tc, ex = run_both(CONV_DGRAD, g, Dev(gy), Dev(w), None, (n, ih, iw, ci), expect_tc=True if tc_ok else None)
     check(tc, ex)
 
 
@@ -73,7 +80,7 @@ def test_conv_wgrad(shape):
     rng = np.random.default_rng(2)
     x = rng.uniform(-1, 1, (n, ih, iw, ci)).astype(np.float32)
     gy = rng.uniform(-1, 1, (n, g["oh"], g["ow"], co)).astype(np.float32)
-    tc, ex = run_both(CONV_WGRAD, g, Dev(x), Dev(gy), None, (k, k, ci, co))
+    tc, ex = run_both(CONV_WGRAD, g, Dev(x), Dev(gy), None, (k, k, ci, co), expect_tc=True)
     check(tc, ex)
 
 
@@ -114,3 +121,27 @@ def test_conv_fwd_fused_column_statistics(shape):
     got = np.frombuffer(cs.get((4 * co,)).tobytes(), np.float64)
     assert np.allclose(got[:co], y.sum(0), rtol=1e-5, atol=1e-3)
     assert np.allclose(got[co:], (y * y).sum(0), rtol=1e-5, atol=1e-3)
+
+
+SMALL_C = [c for c in CONVS if c[3] % 32 != 0 and c[5] > 1]
+
+
+@pytest.mark.parametrize("shape", SMALL_C)
+@pytest.mark.parametrize("kind", [CONV_FWD, CONV_WGRAD])
+def test_manual_a_route(shape, kind):
+    """Builder-warp gather route (no im2col) for channels % 32 != 0."""
+    n, ih, iw, ci, co, k, s = shape
+    g = conv_geom(n, ih, iw, ci, co, k, s)
+    rng = np.random.default_rng(5)
+    x = rng.uniform(-1, 1, (n, ih, iw, ci)).astype(np.float32)
+    w = rng.uniform(-1, 1, (k, k, ci, co)).astype(np.float32)
+    gy = rng.uniform(-1, 1, (n, g["oh"], g["ow"], co)).astype(np.float32)
+    K.nncb_gemm_set_manual_a(1)
+    try:
+        if kind == CONV_FWD:
+            tc, ex = run_both(kind, g, Dev(x), Dev(w), None, (n, g["oh"], g["ow"], co), expect_tc=True)
+        else:
+            tc, ex = run_both(kind, g, Dev(x), Dev(gy), None, (k, k, ci, co), expect_tc=True)
+    finally:
+        K.nncb_gemm_set_manual_a(0)
+    check(tc, ex)

@@ -19,6 +19,7 @@ import paper_2205_10357_b200 as P  # noqa: E402
 from tests.nncb_ctypes import Dev, GemmDesc, K, ctx  # noqa: E402
 
 LAYERS = [  # name, h(=w) in, ci, co, k, s   (ResNet-50, batch 256)
+    ("stem", 224, 3, 64, 7, 2),
     ("s0b_a", 56, 256, 64, 1, 1), ("s0b_b", 56, 64, 64, 3, 1), ("s0b_c", 56, 64, 256, 1, 1),
     ("s1b0_b", 56, 128, 128, 3, 2), ("s1b_b", 28, 128, 128, 3, 1), ("s1b_c", 28, 128, 512, 1, 1),
     ("s1b_a", 28, 512, 128, 1, 1), ("s2b_b", 14, 256, 256, 3, 1), ("s2b_c", 14, 256, 1024, 1, 1),
