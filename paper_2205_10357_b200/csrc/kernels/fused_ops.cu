@@ -74,20 +74,20 @@ __global__ void maxpool_fwd_k(const float* __restrict__ x, float* __restrict__ y
 
 // Max-pool backward as a gather over the windows covering each input pixel,
 // in (oh, ow) ascending order = the reference scatter order (bit-exact).
-template <int V>
+template <int V, typename I>
 __global__ void maxpool_bwd_k(const float* __restrict__ idx, const float* __restrict__ gy, float* __restrict__ gx,
                               nncb_pool_geom g) {
     const int C = (int)g.c, CV = C / V;
     const int OW = (int)g.ow, OH = (int)g.oh, IW = (int)g.iw, IH = (int)g.ih;
     const int KH = (int)g.kh, KW = (int)g.kw, SH = (int)g.sh, SW = (int)g.sw;
-    const int64_t total = g.n * g.ih * g.iw * CV;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const I total = static_cast<I>(g.n * g.ih * g.iw * CV);
+    for (I t = blockIdx.x * (I)blockDim.x + threadIdx.x; t < total; t += (I)gridDim.x * blockDim.x) {
         const int cv = (int)(t % CV);
-        const int64_t pix = t / CV;
+        const I pix = t / CV;
         const int w = (int)(pix % IW);
-        const int64_t r = pix / IW;
+        const I r = pix / IW;
         const int h = (int)(r % IH);
-        const int64_t n = r / IH;
+        const I n = r / IH;
         const int oh0 = h - KH + 1 > 0 ? (h - KH + SH) / SH : 0;
         const int oh1 = min(h / SH, OH - 1);
         const int ow0 = w - KW + 1 > 0 ? (w - KW + SW) / SW : 0;
@@ -98,7 +98,7 @@ __global__ void maxpool_bwd_k(const float* __restrict__ idx, const float* __rest
         for (int oh = oh0; oh <= oh1; ++oh)
             for (int ow = ow0; ow <= ow1; ++ow) {
                 const int want = (h - oh * SH) * KW + (w - ow * SW);
-                const int64_t at = ((n * OH + oh) * OW + ow) * C + cv * V;
+                const I at = ((n * OH + oh) * OW + ow) * C + cv * V;
                 if (V == 4) {
                     float4 ix = __ldg(reinterpret_cast<const float4*>(idx + at));
                     float4 gv = __ldg(reinterpret_cast<const float4*>(gy + at));
@@ -110,7 +110,7 @@ __global__ void maxpool_bwd_k(const float* __restrict__ idx, const float* __rest
                     if ((int)__ldg(idx + at) == want) acc[0] = __fadd_rn(acc[0], __ldg(gy + at));
                 }
             }
-        const int64_t o = pix * C + cv * V;
+        const I o = pix * C + cv * V;
         if (V == 4)
             *reinterpret_cast<float4*>(gx + o) = make_float4(acc[0], acc[1], acc[2], acc[3]);
         else
@@ -140,28 +140,61 @@ __global__ void avgpool_fwd_k(const float* __restrict__ x, float* __restrict__ y
     }
 }
 
+// Output windows containing input row h: o in [o_lo(h), o_hi(h)] where
+// a_start(o) <= h < a_end(o); found by stepping from the proportional guess
+// (adaptive windows overlap by at most one position, so the loops run <= 2
+// steps). Contributions accumulate in (o, p) ascending order, as the
+// reference's output-major scatter does.
+__device__ __forceinline__ void a_range(int h, int in, int out, int& lo, int& hi) {
+    int o = static_cast<int>((static_cast<int64_t>(h) * out) / in);
+    while (o > 0 && a_end(o - 1, in, out) > h) --o;
+    while (o < out && a_end(o, in, out) <= h) ++o;
+    lo = o;
+    int e = o;
+    while (e + 1 < out && a_start(e + 1, in, out) <= h) ++e;
+    hi = e;
+}
+
+template <int V, typename I>
 __global__ void avgpool_bwd_k(const float* __restrict__ gy, float* __restrict__ gx, int64_t n, int64_t ih, int64_t iw,
                               int64_t c, int64_t oh, int64_t ow) {
-    int64_t total = n * ih * iw * c;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        int64_t ch = t % c;
-        int64_t r = t / c;
-        int64_t w = r % iw;
-        r /= iw;
-        int64_t h = r % ih;
-        int64_t b = r / ih;
-        float acc = 0.f;
-        for (int64_t o = 0; o < oh; ++o) {
-            int64_t h0 = a_start(o, ih, oh), h1 = a_end(o, ih, oh);
-            if (h < h0 || h >= h1) continue;
-            for (int64_t p = 0; p < ow; ++p) {
-                int64_t w0 = a_start(p, iw, ow), w1 = a_end(p, iw, ow);
-                if (w < w0 || w >= w1) continue;
-                float scale = __fdiv_rn(1.f, static_cast<float>((h1 - h0) * (w1 - w0)));
-                acc = __fadd_rn(acc, __fmul_rn(__ldg(gy + ((b * oh + o) * ow + p) * c + ch), scale));
+    const int C = (int)c, CV = C / V, IH = (int)ih, IW = (int)iw, OH = (int)oh, OW = (int)ow;
+    const I total = static_cast<I>(n * ih * iw * CV);
+    for (I t = blockIdx.x * (I)blockDim.x + threadIdx.x; t < total; t += (I)gridDim.x * blockDim.x) {
+        const int cv = (int)(t % CV);
+        I r = t / CV;
+        const int w = (int)(r % IW);
+        r /= IW;
+        const int h = (int)(r % IH);
+        const I b = r / IH;
+        int o0, o1, p0, p1;
+        a_range(h, IH, OH, o0, o1);
+        a_range(w, IW, OW, p0, p1);
+        float acc[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[j] = 0.f;
+        for (int o = o0; o <= o1; ++o) {
+            const int h0 = (int)a_start(o, IH, OH), h1 = (int)a_end(o, IH, OH);
+            for (int p = p0; p <= p1; ++p) {
+                const int w0 = (int)a_start(p, IW, OW), w1 = (int)a_end(p, IW, OW);
+                const float scale = __fdiv_rn(1.f, static_cast<float>((h1 - h0) * (w1 - w0)));
+                const float* src = gy + ((b * OH + o) * OW + p) * C + cv * V;
+                float v[V];
+                if (V == 4) {
+                    const float4 q = __ldg(reinterpret_cast<const float4*>(src));
+                    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+                } else {
+                    v[0] = __ldg(src);
+                }
+#pragma unroll
+                for (int j = 0; j < V; ++j) acc[j] = __fadd_rn(acc[j], __fmul_rn(v[j], scale));
             }
         }
-        gx[t] = acc;
+        float* dst = gx + t * V;
+        if (V == 4)
+            *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        else
+            dst[0] = acc[0];
     }
 }
 
@@ -628,10 +661,16 @@ int nncb_maxpool_fwd(nncb_ctx* ctx, const nncb_pool_geom* g, const float* x, flo
 int nncb_maxpool_bwd(nncb_ctx* ctx, const nncb_pool_geom* g, const float* idx, const float* gy, float* gx) {
     int64_t total = g->n * g->ih * g->iw * g->c;
     if (total == 0) return 0;
-    if (g->c % 4 == 0)
-        maxpool_bwd_k<4><<<nncb::grid_for(ctx, total / 4, 256), 256, 0, ctx->stream>>>(idx, gy, gx, *g);
+    const int64_t out_total = g->n * g->oh * g->ow * g->c;
+    const bool i32 = std::max(total, out_total) < (int64_t(1) << 31);   // 32-bit index decode when it fits
+    if (g->c % 4 == 0 && i32)
+        maxpool_bwd_k<4, int><<<nncb::grid_for(ctx, total / 4, 256), 256, 0, ctx->stream>>>(idx, gy, gx, *g);
+    else if (g->c % 4 == 0)
+        maxpool_bwd_k<4, int64_t><<<nncb::grid_for(ctx, total / 4, 256), 256, 0, ctx->stream>>>(idx, gy, gx, *g);
+    else if (i32)
+        maxpool_bwd_k<1, int><<<nncb::grid_for(ctx, total, 256), 256, 0, ctx->stream>>>(idx, gy, gx, *g);
     else
-        maxpool_bwd_k<1><<<nncb::grid_for(ctx, total, 256), 256, 0, ctx->stream>>>(idx, gy, gx, *g);
+        maxpool_bwd_k<1, int64_t><<<nncb::grid_for(ctx, total, 256), 256, 0, ctx->stream>>>(idx, gy, gx, *g);
     NNCB_LAUNCHED(ctx);
     return 0;
 }
@@ -649,7 +688,15 @@ int nncb_avgpool_bwd(nncb_ctx* ctx, int64_t n, int64_t ih, int64_t iw, int64_t c
                      const float* gy, float* gx) {
     int64_t total = n * ih * iw * c;
     if (total == 0) return 0;
-    avgpool_bwd_k<<<nncb::grid_for(ctx, total, 256), 256, 0, ctx->stream>>>(gy, gx, n, ih, iw, c, oh, ow);
+    const bool i32 = std::max(total, n * oh * ow * c) < (int64_t(1) << 31);
+    if (c % 4 == 0 && i32)
+        avgpool_bwd_k<4, int><<<nncb::grid_for(ctx, total / 4, 256), 256, 0, ctx->stream>>>(gy, gx, n, ih, iw, c, oh, ow);
+    else if (c % 4 == 0)
+        avgpool_bwd_k<4, int64_t><<<nncb::grid_for(ctx, total / 4, 256), 256, 0, ctx->stream>>>(gy, gx, n, ih, iw, c, oh, ow);
+    else if (i32)
+        avgpool_bwd_k<1, int><<<nncb::grid_for(ctx, total, 256), 256, 0, ctx->stream>>>(gy, gx, n, ih, iw, c, oh, ow);
+    else
+        avgpool_bwd_k<1, int64_t><<<nncb::grid_for(ctx, total, 256), 256, 0, ctx->stream>>>(gy, gx, n, ih, iw, c, oh, ow);
     NNCB_LAUNCHED(ctx);
     return 0;
 }

@@ -203,10 +203,18 @@ __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: 
 // CH*4 columns (CH 16-byte chunks per row, XOR-swizzled by row), so that each
 // store instruction writes 32/CH whole row segments of CH*16 contiguous
 // bytes instead of 32 scattered 16-byte pieces.
-template <int CH>
+//
+// CS: also accumulate BatchNorm column statistics of the valid rows from the
+// staged tile: with COLS columns per pass, lane l sums column l % COLS over
+// rows [(l / COLS) * RPL, +RPL), the 32/COLS row groups are folded with xor
+// shuffles, and one lane per column adds (sum, sum of squares) to the CTA's
+// double accumulator cs_acc at column cs_col0 + pass offset.
+template <int CH, bool CS>
 __device__ __forceinline__ void store_chunk_t(const uint32_t (&r)[32], uint8_t* tile, float* dst, bool valid,
-                                              int col0, int N, bool full_cols, int lane) {
+                                              int col0, int N, bool full_cols, int lane, bool store,
+                                              double* cs_acc = nullptr, int cs_col0 = 0, int cs_n = 0) {
     constexpr int COLS = CH * 4, RPI = 32 / CH;   // columns per pass, rows per store instruction
+    const uint32_t vmask = CS ? __ballot_sync(0xffffffffu, valid) : 0u;
 #pragma unroll
     for (int p = 0; p < 32 / COLS; ++p) {
         uint8_t* rowp = tile + lane * (CH * 16);
@@ -215,6 +223,34 @@ __device__ __forceinline__ void store_chunk_t(const uint32_t (&r)[32], uint8_t* 
             *reinterpret_cast<uint4*>(rowp + ((j ^ (lane % CH)) << 4)) =
                 make_uint4(r[p * COLS + 4 * j], r[p * COLS + 4 * j + 1], r[p * COLS + 4 * j + 2], r[p * COLS + 4 * j + 3]);
         __syncwarp();
+        if (CS) {
+            constexpr int RPL = COLS;              // rows per lane: 32 rows over 32/COLS lane groups
+            const int col = lane % COLS, r0 = (lane / COLS) * RPL;
+            float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+            for (int i = 0; i < RPL; ++i) {
+                const int rr = r0 + i;
+                const float v = *reinterpret_cast<const float*>(tile + rr * (CH * 16) + (((col >> 2) ^ (rr % CH)) << 4) +
+                                                                (col & 3) * 4);
+                const float m = ((vmask >> rr) & 1u) ? v : 0.f;
+                s1 += m;
+                s2 = fmaf(m, m, s2);
+            }
+#pragma unroll
+            for (int sh = COLS; sh < 32; sh <<= 1) {
+                s1 += __shfl_xor_sync(0xffffffffu, s1, sh);
+                s2 += __shfl_xor_sync(0xffffffffu, s2, sh);
+            }
+            const int cl = cs_col0 + p * COLS + col;
+            if (lane < COLS && col0 + p * COLS + col < N) {
+                atomicAdd(cs_acc + cl, static_cast<double>(s1));
+                atomicAdd(cs_acc + cs_n + cl, static_cast<double>(s2));
+            }
+        }
+        if (!store) {
+            __syncwarp();
+            continue;
+        }
 #pragma unroll
         for (int i = 0; i < CH; ++i) {
             const int rr = i * RPI + lane / CH, ch = lane % CH;
@@ -574,47 +610,16 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MA ? 1 : 2)
                         if (col0 + j < P.N)
                             r[j] = __float_as_uint(__fadd_rn(__uint_as_float(r[j]), __ldg(P.bias + col0 + j)));
                 }
-                if (CS) {
-                    // column sums of this warp's 32 rows, 8 columns at a time: the
-                    // 8-vector halves across lane bits 4,3,2 (7 shuffles per sum),
-                    // bits 1,0 are a plain xor-sum; lane l then holds column l>>2
-#pragma unroll
-                    for (int g8 = 0; g8 < 4; ++g8) {
-                        float a[8], q[8];
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            const float vj = valid ? __uint_as_float(r[g8 * 8 + j]) : 0.f;
-                            a[j] = vj;
-                            q[j] = vj * vj;
-                        }
-#pragma unroll
-                        for (int w = 4, bit = 16; w >= 1; w >>= 1, bit >>= 1) {
-                            const bool upper = (lane & bit) != 0;
-#pragma unroll
-                            for (int j = 0; j < w; ++j) {
-                                const float ra = __shfl_xor_sync(0xffffffffu, upper ? a[j] : a[j + w], bit);
-                                const float rq = __shfl_xor_sync(0xffffffffu, upper ? q[j] : q[j + w], bit);
-                                a[j] = (upper ? a[j + w] : a[j]) + ra;
-                                q[j] = (upper ? q[j + w] : q[j]) + rq;
-                            }
-                        }
-                        a[0] += __shfl_xor_sync(0xffffffffu, a[0], 2);
-                        q[0] += __shfl_xor_sync(0xffffffffu, q[0], 2);
-                        a[0] += __shfl_xor_sync(0xffffffffu, a[0], 1);
-                        q[0] += __shfl_xor_sync(0xffffffffu, q[0], 1);
-                        if ((lane & 3) == 0) {
-                            const int cl = c * 32 + g8 * 8 + (lane >> 2);
-                            atomicAdd(cs_acc + cl, (double)a[0]);
-                            atomicAdd(cs_acc + P.bn + cl, (double)q[0]);
-                        }
-                    }
-                }
-                if (!P.nostore && col0 < P.N) {
+                if (col0 < P.N && (CS || !P.nostore)) {
                     uint8_t* tile = staging + (warp - 2) * (P.stg_cols * 128);
                     const bool full_cols = col0 + 32 <= P.N && (P.ldc % 4) == 0;
-                    if (P.stg_cols == 32)      store_chunk_t<8>(r, tile, dst, valid, col0, P.N, full_cols, lane);
-                    else if (P.stg_cols == 16) store_chunk_t<4>(r, tile, dst, valid, col0, P.N, full_cols, lane);
-                    else                       store_chunk_t<2>(r, tile, dst, valid, col0, P.N, full_cols, lane);
+                    const bool st = !P.nostore;
+                    if (P.stg_cols == 32)
+                        store_chunk_t<8, CS>(r, tile, dst, valid, col0, P.N, full_cols, lane, st, cs_acc, c * 32, P.bn);
+                    else if (P.stg_cols == 16)
+                        store_chunk_t<4, CS>(r, tile, dst, valid, col0, P.N, full_cols, lane, st, cs_acc, c * 32, P.bn);
+                    else
+                        store_chunk_t<2, CS>(r, tile, dst, valid, col0, P.N, full_cols, lane, st, cs_acc, c * 32, P.bn);
                 }
             }
             if (!arrived && lane == 0)   // a warp without a chunk in this tile still arrives once

@@ -25,7 +25,8 @@ for name, args in [("nncb_maxpool_fwd", [ctypes.c_void_p, ctypes.POINTER(PoolGeo
                    ("nncb_sgd", [ctypes.c_void_p] * 3 + [ctypes.c_int64, ctypes.c_double, ctypes.c_double]),
                    ("nncb_bn_stats", [ctypes.c_void_p] * 3 + [ctypes.c_int64, ctypes.c_int64, ctypes.c_double]),
                    ("nncb_layernorm_fwd", [ctypes.c_void_p] * 5 + [ctypes.c_int64, ctypes.c_int64, ctypes.c_double]),
-                   ("nncb_avgpool_fwd", [ctypes.c_void_p] + [ctypes.c_int64] * 6 + [ctypes.c_void_p] * 2)]:
+                   ("nncb_avgpool_fwd", [ctypes.c_void_p] + [ctypes.c_int64] * 6 + [ctypes.c_void_p] * 2),
+                   ("nncb_avgpool_bwd", [ctypes.c_void_p] + [ctypes.c_int64] * 6 + [ctypes.c_void_p] * 2)]:
     fn = getattr(K, name)
     fn.restype, fn.argtypes = ctypes.c_int, args
 
@@ -85,6 +86,18 @@ def test_global_avgpool_bitexact():
     oy = np.zeros((3, 1, 1, 64), np.float32)
     O.lib().o_avgpool(O._f(x), O._f(oy), *[O.I64(v) for v in (3, 7, 7, 64, 1, 1)])
     assert np.array_equal(y.get((3, 1, 1, 64)), oy)
+
+
+@pytest.mark.parametrize("geo", [(3, 7, 7, 64, 1, 1), (2, 7, 10, 5, 3, 4), (2, 10, 9, 8, 4, 3), (1, 5, 5, 12, 5, 5),
+                                 (2, 6, 6, 16, 4, 4)])
+def test_adaptive_avgpool_grad_bitexact(geo):
+    n, ih, iw, c, oh, ow = geo
+    gy = np.random.default_rng(4).uniform(-1, 1, (n, oh, ow, c)).astype(np.float32)
+    gyd, gx = Dev(gy), Dev(nbytes=n * ih * iw * c * 4)
+    ok(K.nncb_avgpool_bwd(ctx(), n, ih, iw, c, oh, ow, gyd.p, gx.p))
+    ogx = np.zeros((n, ih, iw, c), np.float32)
+    O.lib().o_avgpool_grad(O._f(gy), O._f(ogx), *[O.I64(v) for v in geo])
+    assert np.array_equal(gx.get((n, ih, iw, c)), ogx)
 
 
 def test_l1_and_sgd_known_answers(known):
