@@ -86,6 +86,14 @@ enum nncb_ew_op {
                                invstd = (float)(1/sqrt((double)var + imm));
                                r[dst] = ((x - mean)*invstd)*gamma + beta;
                                a = x, b = mean, c = var, d = gamma, e = beta         */
+    NNCB_EW_REDUCE_BN_GRAD = 13, /* BatchNorm backward reduction fused into the group that
+                               produces g (replaces nncb_bn_grad_reduce for it):
+                               sum_g[c] += g, sum_gx[c] += g*xhat, xhat = (x-mean)*invstd,
+                               accumulated in double per channel. a = g, b = x,
+                               c = mean, d = invstd (LOAD_CH regs); outputs: slot = sum_g,
+                               e = sum_gx slot index. Needs the channel-stationary launch:
+                               C a power of two in [4, 2048], n % 4 == 0, 16 B-aligned
+                               slots; at most one per program.                          */
 };
 
 typedef struct {

@@ -124,9 +124,13 @@ struct BoundLaunch {
     int64_t d0 = 0, d1 = 0, d2 = 0, d3 = 0, d4 = 0, d5 = 0;
     double eps = 0;
     int flag0 = 0, flag1 = 0;
+    bool skip = false;                      // work absorbed by another launch (fused reduction)
+    std::vector<nncb_ew_instr> ew_prog;     // rewritten Ew program (empty: the plan's own)
+    int ew_regs = 0;
 };
 
 void enqueue(nncb_ctx* ctx, const BoundLaunch& b) {
+    if (b.skip) return;
     auto P = [&](size_t i) { return static_cast<float*>(b.ptrs.at(i)); };
     switch (b.kind) {
         case LaunchKind::Ew: NNC_CHECK(nncb_ew_launch(ctx, b.ew, b.ptrs.data(), b.n, b.c)); break;
@@ -166,7 +170,7 @@ void launch_cost(const BoundLaunch& b, const Launch& L, const ExecutionPlan& p, 
     switch (b.kind) {
         case LaunchKind::Ew: {
             double n = static_cast<double>(b.n);
-            for (const auto& in : L.ew)
+            for (const auto& in : b.ew_prog.empty() ? L.ew : b.ew_prog)
                 if (in.op == NNCB_EW_LOAD || in.op == NNCB_EW_STORE) bytes += 4.0 * n;
             break;
         }
@@ -274,7 +278,73 @@ struct Program {
                 }
             }
         }
-        if (precision == NNCB_PREC_TF32) fuse_bn_statistics();
+        if (precision == NNCB_PREC_TF32) {
+            fuse_bn_statistics();
+            fuse_bn_grad_reduce();
+        }
+    }
+
+    /// The BatchNorm backward reduction (sum g, sum g*xhat per channel) of a
+    /// gradient g that the immediately preceding fused elementwise group
+    /// stores is folded into that group (NNCB_EW_REDUCE_BN_GRAD): g is reduced
+    /// from registers as it is written instead of being read back by a
+    /// separate pass. Applies when the group can run channel-stationary.
+    void fuse_bn_grad_reduce() {
+        if (std::getenv("NNC_NO_FUSED_BN_GRAD")) return;
+        for (size_t pi = 0; pi < steps.size(); ++pi)
+            for (size_t j = 1; j < steps[pi].size(); ++j) {
+                BoundLaunch& r = steps[pi][j];
+                BoundLaunch& e = steps[pi][j - 1];
+                if (r.kind != LaunchKind::BnGradReduce || r.skip || e.kind != LaunchKind::Ew || e.skip) continue;
+                const int64_t rows = r.d0, C = r.d1;
+                if (C < 4 || C > 2048 || (C & (C - 1)) || (rows * C) % 4 || e.n != rows * C) continue;
+                if (e.c > 0 && e.c != C) continue;
+                const Launch& L = *sources[pi][j - 1];
+                std::vector<nncb_ew_instr> prog = e.ew_prog.empty() ? L.ew : e.ew_prog;
+                int regs = e.ew_prog.empty() ? L.ew_regs : e.ew_regs;
+                bool has_reduce = false;
+                int at = -1;
+                for (size_t k = 0; k < prog.size(); ++k) {
+                    has_reduce = has_reduce || prog[k].op == NNCB_EW_REDUCE_BN_GRAD;
+                    if (prog[k].op == NNCB_EW_STORE && e.ptrs[prog[k].slot] == r.ptrs[2]) at = static_cast<int>(k);
+                }
+                if (has_reduce || at < 0 || e.ptrs.size() + 5 > 48) continue;
+                const int s0 = static_cast<int>(e.ptrs.size());
+                std::vector<void*> ptrs = e.ptrs;
+                ptrs.push_back(r.ptrs[0]);                                  // x
+                ptrs.push_back(r.ptrs[1]);                                  // mean   = stats[0:C]
+                ptrs.push_back(static_cast<float*>(r.ptrs[1]) + C);         // invstd = stats[C:2C]
+                ptrs.push_back(r.ptrs[3]);                                  // sum_g
+                ptrs.push_back(r.ptrs[4]);                                  // sum_gx
+                const int rx = regs, rm = regs + 1, rs = regs + 2;
+                auto mk = [](int op, int dst, int slot) {
+                    nncb_ew_instr in{};
+                    in.op = op;
+                    in.dst = dst;
+                    in.slot = slot;
+                    return in;
+                };
+                nncb_ew_instr red{};
+                red.op = NNCB_EW_REDUCE_BN_GRAD;
+                red.a = prog[at].a;
+                red.b = rx;
+                red.c = rm;
+                red.d = rs;
+                red.slot = s0 + 3;
+                red.e = s0 + 4;
+                prog.insert(prog.begin() + at + 1, {mk(NNCB_EW_LOAD, rx, s0), mk(NNCB_EW_LOAD_CH, rm, s0 + 1),
+                                                    mk(NNCB_EW_LOAD_CH, rs, s0 + 2), red});
+                nncb_ew_program ep{static_cast<int32_t>(prog.size()), prog.data(), regs + 3,
+                                   static_cast<int32_t>(ptrs.size())};
+                nncb_ew_kernel* k = nullptr;
+                NNC_CHECK(nncb_ew_compile(dev->ctx(), &ep, &k));
+                e.ew = k;
+                e.ptrs = std::move(ptrs);
+                e.ew_prog = std::move(prog);
+                e.ew_regs = regs + 3;
+                e.c = C;
+                r.skip = true;
+            }
     }
 
     /// BatchNorm statistics of a tensor-core GEMM's output are accumulated in
@@ -901,10 +971,11 @@ std::vector<Trainer::LaunchTiming> Trainer::profile_step(double lr) {
         for (size_t k = 0; k < I.prog->steps[pi].size(); ++k) {
             const BoundLaunch& b = I.prog->steps[pi][k];
             const Launch& L = *I.prog->sources[pi][k];
+            if (b.skip) continue;
             enqueue(ctx, b);
             ev();
             LaunchTiming t;
-            t.label = L.label;
+            t.label = b.ew_prog.empty() ? L.label : L.label + "+bn_grad_reduce";
             t.kind = L.kind == LaunchKind::Gemm ? std::string("gemm:") + hlir::op_name(L.op) : plan::launch_kind_name(L.kind);
             launch_cost(b, L, p, t.bytes, t.flops);
             out.push_back(t);

@@ -30,6 +30,7 @@ struct nncb_ew_kernel {
     CUfunction fn = nullptr;
     int n_slots = 0;
     bool uses_channels = false;
+    int reduce_sg = -1, reduce_sgx = -1;   // REDUCE_BN_GRAD output slots (-1: no reduction)
 };
 
 void nncb::ew_release(nncb_ew_kernel* k) {
@@ -44,7 +45,7 @@ constexpr int kMaxSlots = 48;
 
 const char* kPrelude = R"(
 typedef long long i64;
-struct EwArgs { float* p[48]; i64 n; i64 C; int cs; };
+struct EwArgs { float* p[48]; i64 n; i64 C; int cs; double* part; };
 __device__ __forceinline__ float relu_(float x) { return x > 0.f ? x : 0.f; }
 __device__ __forceinline__ float relu_grad_(float x, float g) { return x > 0.f ? g : 0.f; }
 __device__ __forceinline__ float bn_apply_(float x, float m, float s, float ga, float be) {
@@ -106,6 +107,12 @@ void emit_body(std::ostringstream& os, const nncb_ew_program& p, int W, bool use
                     os << "  #pragma unroll\n  for (int j = 0; j < " << W << "; ++j) " << d << "[j] = __ldg(" << ptr
                        << " + ch[j]);\n";
                 continue;
+            case NNCB_EW_REDUCE_BN_GRAD:
+                if (!stationary) continue;   // launch guarantees the channel-stationary path
+                os << "  #pragma unroll\n  for (int j = 0; j < " << W << "; ++j) { const double xh = ((double)" << b
+                   << "[j] - (double)" << c << "[j]) * (double)" << dd << "[j]; red0[j] += (double)" << a
+                   << "[j]; red1[j] += (double)" << a << "[j] * xh; }\n";
+                continue;
             case NNCB_EW_STORE:
                 if (W == 4)
                     os << "  *reinterpret_cast<float4*>(" << ptr << " + i) = make_float4(" << a << "[0], " << a
@@ -147,8 +154,15 @@ void emit_body(std::ostringstream& os, const nncb_ew_program& p, int W, bool use
     }
 }
 
+int find_reduce(const nncb_ew_program& p) {
+    for (int k = 0; k < p.n_instr; ++k)
+        if (p.instr[k].op == NNCB_EW_REDUCE_BN_GRAD) return k;
+    return -1;
+}
+
 std::string generate(const nncb_ew_program& p, bool uses_ch) {
     std::ostringstream os;
+    const bool red = find_reduce(p) >= 0;
     os << kPrelude;
     os << "__device__ __forceinline__ void body4(const EwArgs& A, i64 i) {\n";
     emit_body(os, p, 4, uses_ch);
@@ -164,11 +178,16 @@ std::string generate(const nncb_ew_program& p, bool uses_ch) {
         // operands are loaded once (float4) into registers before the loop.
         os << "__device__ __forceinline__ void body4s(const EwArgs& A, i64 i";
         for (int k : chregs) os << ", const float (&pc" << p.instr[k].dst << ")[4]";
+        if (red) os << ", double (&red0)[4], double (&red1)[4]";
         os << ") {\n";
         emit_body(os, p, 4, uses_ch, true);
         os << "}\n";
     }
-    os << R"(extern "C" __global__ void __launch_bounds__(256) nnc_fused_ew(const EwArgs A) {
+    // reduction groups carry 16 registers of double accumulators: cap at 64
+    // registers so four blocks stay resident (one wave, see nncb_ew_launch)
+    os << (red ? "extern \"C\" __global__ void __launch_bounds__(256, 4) nnc_fused_ew(const EwArgs A) {"
+               : "extern \"C\" __global__ void __launch_bounds__(256) nnc_fused_ew(const EwArgs A) {");
+    os << R"(
   const i64 nvec = A.n >> 2;
   const i64 stride = (i64)gridDim.x * blockDim.x;
   i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
@@ -183,9 +202,42 @@ std::string generate(const nncb_ew_program& p, bool uses_ch) {
         }
         std::string args;
         for (int k : chregs) args += ", pc" + std::to_string(p.instr[k].dst);
+        if (red) {
+            args += ", red0, red1";
+            os << "    double red0[4] = {0, 0, 0, 0}, red1[4] = {0, 0, 0, 0};\n";
+        }
         os << "    for (; v + stride < nvec; v += 2 * stride) { body4s(A, v << 2" << args << "); body4s(A, (v + stride) << 2"
            << args << "); }\n";
-        os << "    if (v < nvec) body4s(A, v << 2" << args << ");\n    return;\n  }\n";
+        os << "    if (v < nvec) body4s(A, v << 2" << args << ");\n";
+        if (red) {
+            // Per-block partials, deterministic: for C <= 1024 (a power of two)
+            // threads t and t + C/4 share channels and thread q < C/4 folds its
+            // group in t order; for C > 1024 each thread owns its 4 channels.
+            os << R"(    __shared__ double rs[256][8];
+    const int t = threadIdx.x;
+    #pragma unroll
+    for (int j = 0; j < 4; ++j) { rs[t][j] = red0[j]; rs[t][4 + j] = red1[j]; }
+    __syncthreads();
+    const int C = (int)A.C;
+    double* part = A.part + (i64)blockIdx.x * 2 * C;
+    if (C <= 1024) {
+      const int G = C >> 2;
+      if (t < G) {
+        double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int k = t; k < 256; k += G) {
+          #pragma unroll
+          for (int j = 0; j < 8; ++j) a[j] += rs[k][j];
+        }
+        #pragma unroll
+        for (int j = 0; j < 4; ++j) { part[4 * t + j] = a[j]; part[C + 4 * t + j] = a[4 + j]; }
+      }
+    } else {
+      #pragma unroll
+      for (int j = 0; j < 4; ++j) { part[c0 + j] = red0[j]; part[C + c0 + j] = red1[j]; }
+    }
+)";
+        }
+        os << "    return;\n  }\n";
     }
     os << R"(  for (; v + stride < nvec; v += 2 * stride) { body4(A, v << 2); body4(A, (v + stride) << 2); }
   if (v < nvec) body4(A, v << 2);
@@ -204,6 +256,40 @@ int nvrtc_fail(nvrtcProgram prog, nvrtcResult r, const std::string& src) {
     }
     if (prog) nvrtcDestroyProgram(&prog);
     return nncb::fail(std::string("NVRTC: ") + nvrtcGetErrorString(r) + "\n" + log + "\n--- source ---\n" + src);
+}
+
+// Folds the per-block partials of a REDUCE_BN_GRAD group: block (32 x 8)
+// owns 32 channels, lane row y sums blocks k = y, y+8, ... and the 8 rows are
+// folded in order (deterministic). For C > 1024 block k only covers the
+// channels [(1024 k) % C, +1024).
+__global__ void __launch_bounds__(256) ew_red_final_k(const double* __restrict__ part, int grid, int C,
+                                                      float* __restrict__ sg, float* __restrict__ sgx) {
+    __shared__ double fold[2][8][33];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int c = blockIdx.x * 32 + tx;
+    double a = 0.0, b = 0.0;
+    if (c < C) {
+#pragma unroll 4
+        for (int k = ty; k < grid; k += 8) {
+            if (C > 1024) {
+                const int start = static_cast<int>((static_cast<long long>(k) * 1024) % C);
+                if ((c - start + C) % C >= 1024) continue;
+            }
+            a += part[(static_cast<long long>(k) * 2) * C + c];
+            b += part[(static_cast<long long>(k) * 2 + 1) * C + c];
+        }
+    }
+    fold[0][ty][tx] = a;
+    fold[1][ty][tx] = b;
+    __syncthreads();
+    if (ty == 0 && c < C) {
+        for (int y = 1; y < 8; ++y) {
+            a += fold[0][y][tx];
+            b += fold[1][y][tx];
+        }
+        sg[c] = static_cast<float>(a);
+        sgx[c] = static_cast<float>(b);
+    }
 }
 
 }  // namespace
@@ -262,6 +348,10 @@ int nncb_ew_compile(nncb_ctx* ctx, const nncb_ew_program* p, nncb_ew_kernel** ou
     k->source = src;
     k->n_slots = p->n_slots;
     k->uses_channels = uses_ch;
+    if (int r = find_reduce(*p); r >= 0) {
+        k->reduce_sg = p->instr[r].slot;
+        k->reduce_sgx = p->instr[r].e;
+    }
     const auto& D = nncb::drv::table();
     if (!D.ok) {
         nncb::ew_release(k);
@@ -285,6 +375,7 @@ int nncb_ew_launch(nncb_ctx* ctx, nncb_ew_kernel* k, void* const* slots, int64_t
         long long n;
         long long C;
         int cs;
+        double* part;
     } args{};
     for (int s = 0; s < k->n_slots; ++s) {
         args.p[s] = static_cast<float*>(slots[s]);
@@ -306,12 +397,32 @@ int nncb_ew_launch(nncb_ctx* ctx, nncb_ew_kernel* k, void* const* slots, int64_t
                 if (reinterpret_cast<uintptr_t>(slots[s2]) & 15) args.cs = 0;
         }
     }
+    const bool reduce = k->reduce_sg >= 0;
+    if (reduce) {
+        // the reduction runs only on the channel-stationary path: C a power of
+        // two in [4, 2048]; a bounded grid keeps the per-block partials small
+        const int64_t C = channels;
+        if (!args.cs || C < 4 || C > 2048 || (C & (C - 1)))
+            return nncb::fail("nncb_ew_launch: REDUCE_BN_GRAD needs the channel-stationary launch (C power of 2 <= 2048)");
+        const int64_t g = C / std::gcd<int64_t>(C, 1024);
+        const int64_t cap = std::max<int64_t>(g, (4 * static_cast<int64_t>(ctx->sm_count) / g) * g);
+        if (grid > cap) grid = static_cast<unsigned>(cap);
+        args.part = static_cast<double*>(nncb::scratch(ctx, sizeof(double) * 2 * C * grid));
+        if (!args.part) return nncb::fail("nncb_ew_launch: reduction scratch allocation failed");
+    }
     void* params[] = {&args};
     CUresult r = nncb::drv::table().launchKernel(k->fn, grid, 1, 1, 256, 1, 1, 0,
                                                  reinterpret_cast<CUstream>(ctx->stream), params, nullptr);
     if (r != CUDA_SUCCESS)
         return nncb::fail(std::string("cuLaunchKernel(fused ew): ") + nncb::drv::error_string(r));
     ctx->launches.fetch_add(1, std::memory_order_relaxed);
+    if (reduce) {
+        const int C = static_cast<int>(channels);
+        ew_red_final_k<<<(C + 31) / 32, dim3(32, 8), 0, ctx->stream>>>(args.part, static_cast<int>(grid), C,
+                                                                       args.p[k->reduce_sg], args.p[k->reduce_sgx]);
+        NNCB_CUDA(cudaGetLastError());
+        ctx->launches.fetch_add(1, std::memory_order_relaxed);
+    }
     return 0;
 }
 

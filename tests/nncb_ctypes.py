@@ -31,6 +31,43 @@ for name, res, args in [
     fn.restype, fn.argtypes = res, args
 
 
+class EwInstr(ctypes.Structure):
+    _fields_ = [("op", ctypes.c_int32), ("dst", ctypes.c_int32), ("a", ctypes.c_int32), ("b", ctypes.c_int32),
+                ("c", ctypes.c_int32), ("d", ctypes.c_int32), ("e", ctypes.c_int32), ("f", ctypes.c_int32),
+                ("h", ctypes.c_int32), ("slot", ctypes.c_int32), ("imm", ctypes.c_double)]
+
+
+class EwProgram(ctypes.Structure):
+    _fields_ = [("n_instr", ctypes.c_int32), ("instr", ctypes.POINTER(EwInstr)), ("n_regs", ctypes.c_int32),
+                ("n_slots", ctypes.c_int32)]
+
+
+for name, res, args in [
+    ("nncb_ew_compile", _I, [_P, ctypes.POINTER(EwProgram), ctypes.POINTER(_P)]),
+    ("nncb_ew_launch", _I, [_P, _P, ctypes.POINTER(_P), ctypes.c_int64, ctypes.c_int64]),
+    ("nncb_bn_grad_reduce", _I, [_P, _P, _P, _P, _P, _P, ctypes.c_int64, ctypes.c_int64]),
+    ("nncb_sync", _I, [_P]),
+    ("nncb_event_create", _I, [ctypes.POINTER(_P)]),
+    ("nncb_event_record", _I, [_P, _P]),
+    ("nncb_event_elapsed_ms", _I, [_P, _P, ctypes.POINTER(ctypes.c_float)]),
+]:
+    fn = getattr(K, name)
+    fn.restype, fn.argtypes = res, args
+
+
+def ew_run(instrs, n_regs, slots, n, channels):
+    """Compile and launch a fused elementwise program; slots are Dev objects."""
+    arr = (EwInstr * len(instrs))(*[EwInstr(**i) for i in instrs])
+    prog = EwProgram(len(instrs), arr, n_regs, len(slots))
+    kern = _P()
+    rc = K.nncb_ew_compile(ctx(), ctypes.byref(prog), ctypes.byref(kern))
+    assert rc == 0, K.nncb_last_error()
+    ptrs = (_P * len(slots))(*[s.p for s in slots])
+    rc = K.nncb_ew_launch(ctx(), kern, ptrs, n, channels)
+    assert rc == 0, K.nncb_last_error()
+    K.nncb_sync(ctx())
+
+
 def ctx():
     c = P._host.nnc_device_ctx()
     assert c, P._host.nnc_last_error()

@@ -149,3 +149,37 @@ def test_layernorm_forward_vs_oracle():
     oy = np.zeros_like(x)
     O.lib().o_layernorm(O._f(x), O._f(ga), O._f(be), O._f(oy), O.I64(64), O.I64(4096), ctypes.c_double(1e-5))
     assert np.max(np.abs(y.get(x.shape) - oy)) / np.max(np.abs(oy)) < 1e-6
+
+
+@pytest.mark.parametrize("rows,C", [(4096, 64), (1000, 256), (512, 2048), (333, 128), (50, 1024)])
+def test_ew_fused_bn_grad_reduce(rows, C):
+    """REDUCE_BN_GRAD fused into an elementwise group: per-channel sum(g) and
+    sum(g * xhat) of the value the group produces, against float64 numpy and
+    the standalone nncb_bn_grad_reduce (both accumulate in double)."""
+    from tests.nncb_ctypes import ew_run
+    rng = np.random.default_rng(11)
+    g = rng.uniform(-1, 1, (rows, C)).astype(np.float32)
+    x = rng.uniform(-2, 2, (rows, C)).astype(np.float32)
+    mean = x.mean(0).astype(np.float32)
+    invstd = (1.0 / np.sqrt(x.var(0) + 1e-5)).astype(np.float32)
+    gd, xd, md, sd = Dev(g), Dev(x), Dev(mean), Dev(invstd)
+    out, sg, sgx = Dev(nbytes=g.nbytes), Dev(nbytes=C * 4), Dev(nbytes=C * 4)
+    LOAD, LOAD_CH, STORE, RELU, RED = 0, 1, 2, 3, 13
+    prog = [dict(op=LOAD, dst=0, slot=0), dict(op=LOAD, dst=1, slot=1), dict(op=LOAD_CH, dst=2, slot=2),
+            dict(op=LOAD_CH, dst=3, slot=3), dict(op=RELU, dst=4, a=0), dict(op=STORE, a=4, slot=4),
+            dict(op=RED, a=4, b=1, c=2, d=3, slot=5, e=6)]
+    ew_run(prog, 5, [gd, xd, md, sd, out, sg, sgx], rows * C, C)
+    gr = np.maximum(g, 0).astype(np.float64)
+    xhat = (x.astype(np.float64) - mean.astype(np.float64)) * invstd.astype(np.float64)
+    want_g, want_gx = gr.sum(0), (gr * xhat).sum(0)
+    assert np.array_equal(out.get((rows, C)), np.maximum(g, 0))
+    got_g, got_gx = sg.get((C,)), sgx.get((C,))
+    scale = np.abs(gr).sum(0) + 1e-30
+    assert np.max(np.abs(got_g - want_g) / scale) < 1e-6
+    assert np.max(np.abs(got_gx - want_gx) / (np.abs(gr * xhat).sum(0) + 1e-30)) < 1e-6
+    # same answer as the standalone reduction over the stored value
+    stats = Dev(np.concatenate([mean, invstd]))
+    ref_g, ref_gx = Dev(nbytes=C * 4), Dev(nbytes=C * 4)
+    ok(K.nncb_bn_grad_reduce(ctx(), xd.p, stats.p, out.p, ref_g.p, ref_gx.p, rows, C))
+    np.testing.assert_allclose(got_g, ref_g.get((C,)), rtol=1e-5, atol=1e-5)
+    np.testing.assert_allclose(got_gx, ref_gx.get((C,)), rtol=1e-5, atol=1e-5)
