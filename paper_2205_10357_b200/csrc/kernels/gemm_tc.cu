@@ -24,6 +24,10 @@
 // full/empty mbarriers couples TMA and MMA; tcgen05.commit releases stages.
 // Operand tiles use the 128-byte swizzle (TMA and UMMA descriptors agree).
 #include <atomic>
+#include <vector>
+#include <string>
+#include <mutex>
+#include <map>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -692,7 +696,16 @@ bool encode_2d(CUtensorMap* map, const float* base, int64_t inner, int64_t rows,
     return r == CUDA_SUCCESS;
 }
 
+thread_local int g_force_bn = 0;   // set by the autotuner (gemm_tc) for one call
+
 int pick_bn(int64_t n) {
+    static const int env_bn = getenv("NNCB_TC_BN") ? atoi(getenv("NNCB_TC_BN")) : 0;   // tuning knob
+    const int force = g_force_bn ? g_force_bn : env_bn;
+    if (force == 64 || force == 128 || force == 256) {   // widths stay in {64, 128, 256} (TMEM: power-of-two columns)
+        int w = force;
+        while (w > 64 && w / 2 >= n) w /= 2;
+        return w;
+    }
     if (n <= 64) return 64;
     if (n <= 128) return 128;
     return n % 256 == 0 || n > 1024 ? 256 : 128;
@@ -842,8 +855,82 @@ __global__ void __launch_bounds__(256) im2col_k(const float* __restrict__ x, flo
 
 std::atomic<int> g_manual_a{getenv("NNCB_TC_MANUAL_A") ? 1 : 0};
 
+int gemm_tc_route(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const float* bias,
+                  float* out, bool* handled);
+
+// Measured tile selection: the first time a GEMM shape is seen outside stream
+// capture, each candidate N-tile width is run and timed with CUDA events on
+// the context's stream (the output is simply rewritten), and the fastest is
+// remembered for the shape. 128-wide tiles (two CTAs per SM) win for some
+// layers and 256-wide (one CTA, half the A re-reads) for others; no static
+// rule separates them. NNCB_TC_AUTOTUNE=0 keeps the static choice.
 int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const float* bias, float* out,
             bool* handled) {
+    static const bool enabled = !(getenv("NNCB_TC_AUTOTUNE") && atoi(getenv("NNCB_TC_AUTOTUNE")) == 0);
+    static std::mutex mu;
+    static std::map<std::string, int> tuned;
+    const bool dense = d->kind <= NNCB_DENSE_WGRAD;
+    const int64_t N = d->kind == NNCB_DENSE_DGRAD ? d->in_f : d->kind == NNCB_CONV_DGRAD ? d->ci
+                      : dense ? d->out_f : d->co;
+    char key[256];
+    snprintf(key, sizeof(key), "%d|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%lld|%d|%d",
+             d->kind, (long long)d->n, (long long)d->ih, (long long)d->iw, (long long)d->ci, (long long)d->co,
+             (long long)d->kh, (long long)d->kw, (long long)d->sh, (long long)d->sw, (long long)d->oh,
+             (long long)d->ow, (long long)d->pad_top, (long long)d->pad_left, (long long)d->batch,
+             (long long)(d->in_f * 1000003 + d->out_f), d->epilogue, g_manual_a.load() ? 1 : 0);
+    int choice = 0;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = tuned.find(key);
+        if (it != tuned.end()) choice = it->second;
+    }
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(ctx->stream, &cap);
+    if (!choice && enabled && N > 64 && cap == cudaStreamCaptureStatusNone) {
+        std::vector<int> cands = N <= 128 ? std::vector<int>{64, 128} : std::vector<int>{128, 256};
+        cudaEvent_t e0, e1;
+        NNCB_CUDA(cudaEventCreate(&e0));
+        NNCB_CUDA(cudaEventCreate(&e1));
+        float best = 0.f;
+        for (int c : cands) {
+            g_force_bn = c;
+            int rc = gemm_tc_route(ctx, d, a, b, bias, out, handled);   // warm-up (and validity)
+            if (rc || !*handled) {
+                g_force_bn = 0;
+                cudaEventDestroy(e0);
+                cudaEventDestroy(e1);
+                return rc;
+            }
+            cudaEventRecord(e0, ctx->stream);
+            for (int r = 0; r < 3 && !rc; ++r) rc = gemm_tc_route(ctx, d, a, b, bias, out, handled);
+            cudaEventRecord(e1, ctx->stream);
+            g_force_bn = 0;
+            if (rc) {
+                cudaEventDestroy(e0);
+                cudaEventDestroy(e1);
+                return rc;
+            }
+            NNCB_CUDA(cudaEventSynchronize(e1));
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (!choice || ms < best) {
+                best = ms;
+                choice = c;
+            }
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        std::lock_guard<std::mutex> lk(mu);
+        tuned[key] = choice;
+    }
+    g_force_bn = choice;
+    const int rc = gemm_tc_route(ctx, d, a, b, bias, out, handled);
+    g_force_bn = 0;
+    return rc;
+}
+
+int gemm_tc_route(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const float* bias,
+                  float* out, bool* handled) {
     *handled = false;
     const bool conv = d->kind >= NNCB_CONV_FWD;
     if (conv && d->ci % 32 != 0 && d->kh * d->kw > 1 && (d->kind == NNCB_CONV_FWD || d->kind == NNCB_CONV_WGRAD)) {

@@ -51,6 +51,8 @@ def main():
         y = Dev(nbytes=a.batch * g["oh"] * g["ow"] * co * 4)
         w = Dev(nbytes=k * k * ci * co * 4)
         for kind in a.kinds.split(","):
+            if kind == "dgrad" and ci % 32 and k > 1:
+                continue   # the stem's input gradient is never needed (and has no tensor-core lowering)
             code, A, B, O = {"fwd": (3, x, w, y), "dgrad": (4, y, w, x), "wgrad": (5, x, y, w)}[kind]
             d = GemmDesc(kind=code, precision=0, epilogue=0, **g)
             rc = K.nncb_gemm(ctx(), ctypes.byref(d), A.p, B.p, None, O.p)   # warm-up
