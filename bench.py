@@ -42,6 +42,17 @@ CONFIGS = {
 }
 
 
+def ncu_summary():
+    """Newest profiles/r*/ncu_summary.json (written from this repo's ncu captures)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r*",
+                                          "ncu_summary.json")))
+    if not files:
+        return {}
+    with open(files[-1]) as f:
+        return json.load(f)
+
+
 def peaks():
     try:
         with open(PEAKS_FILE) as f:
@@ -52,10 +63,16 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (clocks + throttle reasons)."""
+    """nvidia-smi sampling (clocks + throttle reasons) kept for the timed region.
+
+    The sampler starts before the warm-up (nvidia-smi needs a few hundred ms to
+    emit its first line); `mark_start` / `stop` bracket the timed region and
+    only samples taken inside it are kept (or the nearest ones if the region is
+    shorter than the sampling period)."""
 
     def __init__(self, index: int):
         self.index, self.samples, self.proc = index, [], None
+        self.t0 = self.t1 = None
 
     def start(self):
         try:
@@ -63,31 +80,40 @@ class Clocks:
                 ["nvidia-smi", "-i", str(self.index),
                  "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except FileNotFoundError:
             self.proc = None
 
+    def mark_start(self):
+        self.t0 = time.time()
+
     def _read(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) >= 7:
-                self.samples.append(parts)
+                self.samples.append((time.time(), parts))
 
     def stop(self):
+        self.t1 = time.time()
+        time.sleep(0.25)   # let the sample covering the region's end arrive
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+        t0 = self.t0 if self.t0 is not None else self.t1
+        inside = [p for t, p in self.samples if t0 <= t <= self.t1 + 0.1]
+        if not inside and self.samples:   # region shorter than the period: nearest samples
+            inside = [min(self.samples, key=lambda tp: abs(tp[0] - (t0 + self.t1) / 2))[1]]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
         sm = []
         smax = None
-        for s in self.samples:
+        for s in inside:
             try:
                 sm.append(float(s[0]))
                 smax = float(s[1])
@@ -279,11 +305,12 @@ def main():
         units = batch * world
         metric, unit = "fused-group samples/sec", "samples/s"
 
+    clocks.start()   # sampler warms up during the warm-up steps
     for _ in range(args.warmup):
         step()
     timer.sync()
     barrier()
-    clocks.start()
+    clocks.mark_start()
     l0 = timer.launches()
     timer.start()
     for _ in range(args.steps):
@@ -353,6 +380,14 @@ def main():
         roof = roofline(top_k, fam[top_k])
         if "ew" in fam:
             fused_roof = roofline("ew (generated fused groups)", fam["ew"])
+        # DRAM traffic per launch from the committed `ncu --set full` capture of
+        # a representative launch of each family, beside its algorithmic bytes
+        for r, fk in ((roof, "gemm" if top_k == "gemm" else top_k), (fused_roof, "ew")):
+            summ = ncu_summary().get(fk) if r else None
+            if summ:
+                r["traffic"] = summ["dram_read_bytes"] + summ["dram_write_bytes"]
+                r["traffic_launch"] = {"launch": summ["launch"], "algorithmic_bytes": summ["algorithmic_bytes"],
+                                       "source": summ["report"]}
         by_kind = {}
         for p in prof:
             k = p["kind"].split(":")[0]

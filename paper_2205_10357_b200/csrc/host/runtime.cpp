@@ -863,10 +863,16 @@ struct Trainer::Impl {
                 g = nullptr;
             }
             if (!g) {
+                // the captured kernels are exactly what every replay launches
+                // (the first eager step also ran the GEMM tile autotuner)
+                const uint64_t before = nncb_launch_count(ctx);
                 NNC_CHECK(nncb_capture_begin(ctx));
                 enqueue_step(lr, do_sgd);
                 NNC_CHECK(nncb_capture_end(ctx, &g));
-                if (do_sgd) graph_lr = lr;
+                if (do_sgd) {
+                    graph_lr = lr;
+                    launches_per_step = nncb_launch_count(ctx) - before;
+                }
             }
             NNC_CHECK(nncb_graph_launch(ctx, g));
         }
