@@ -853,6 +853,95 @@ __global__ void __launch_bounds__(256) im2col_k(const float* __restrict__ x, flo
     }
 }
 
+
+// ---- space-to-depth lowering for stride-2 convolutions with few channels ----
+// y = conv_{k x k, stride 2}(x) equals a stride-1 VALID conv of the 2x2-blocked
+// input x'[n, Y, X, (by*2+bx)*ci + c] = x[n, 2Y+by-pt, 2X+bx-pl, c] (zero outside)
+// with weights W'[a, b, (by,bx,c), co] = W[2a+by, 2b+bx, c, co] (zero past k).
+// Channels are zero-padded to 32 so the TMA implicit-GEMM path applies.
+__global__ void s2d_input_k(const float* __restrict__ x, float* __restrict__ xs, int n, int ih, int iw, int ci,
+                            int H2, int W2, int pt, int pl) {
+    const int64_t total = static_cast<int64_t>(n) * H2 * W2 * 8;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int q = static_cast<int>(t & 7);
+        const int64_t pix = t >> 3;
+        const int X = static_cast<int>(pix % W2);
+        const int Y = static_cast<int>((pix / W2) % H2);
+        const int64_t nn = pix / (static_cast<int64_t>(W2) * H2);
+        float v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int cc = q * 4 + j;
+            v[j] = 0.f;
+            if (cc < 4 * ci) {
+                const int blk = cc / ci, c = cc % ci;
+                const int iy = 2 * Y + (blk >> 1) - pt, ix = 2 * X + (blk & 1) - pl;
+                if (iy >= 0 && iy < ih && ix >= 0 && ix < iw) v[j] = __ldg(x + ((nn * ih + iy) * iw + ix) * ci + c);
+            }
+        }
+        reinterpret_cast<float4*>(xs)[t] = make_float4(v[0], v[1], v[2], v[3]);
+    }
+}
+
+__global__ void s2d_weight_k(const float* __restrict__ w, float* __restrict__ ws, int kh, int kw, int ci, int co,
+                             int kh2, int kw2) {
+    const int total = kh2 * kw2 * 32 * co;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const int o = t % co, cc = (t / co) % 32, b = (t / (co * 32)) % kw2, a = t / (co * 32 * kw2);
+        float v = 0.f;
+        if (cc < 4 * ci) {
+            const int blk = cc / ci, c = cc % ci;
+            const int dh = 2 * a + (blk >> 1), dw = 2 * b + (blk & 1);
+            if (dh < kh && dw < kw) v = w[((dh * kw + dw) * ci + c) * co + o];
+        }
+        ws[t] = v;
+    }
+}
+
+__global__ void s2d_wgrad_back_k(const float* __restrict__ dws, float* __restrict__ dw, int kh, int kw, int ci, int co,
+                                 int kw2) {
+    const int total = kh * kw * ci * co;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const int o = t % co, c = (t / co) % ci, x = (t / (co * ci)) % kw, y = t / (co * ci * kw);
+        const int cc = ((y & 1) * 2 + (x & 1)) * ci + c;
+        dw[t] = dws[(((y >> 1) * kw2 + (x >> 1)) * 32 + cc) * co + o];
+    }
+}
+
+int gemm_tc_s2d(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const float* bias, float* out,
+                bool* handled) {
+    const int kh2 = static_cast<int>((d->kh + 1) / 2), kw2 = static_cast<int>((d->kw + 1) / 2);
+    const int H2 = static_cast<int>(d->oh) + kh2 - 1, W2 = static_cast<int>(d->ow) + kw2 - 1;
+    const size_t xs_bytes = sizeof(float) * static_cast<size_t>(d->n) * H2 * W2 * 32;
+    const size_t w_bytes = sizeof(float) * static_cast<size_t>(kh2) * kw2 * 32 * d->co;
+    const size_t w_off = (xs_bytes + 255) / 256 * 256;
+    char* ws = static_cast<char*>(workspace(ctx, w_off + w_bytes));
+    if (!ws) return fail("space-to-depth: workspace allocation failed");
+    float* xs = reinterpret_cast<float*>(ws);
+    float* wsp = reinterpret_cast<float*>(ws + w_off);
+    s2d_input_k<<<grid_for(ctx, static_cast<int64_t>(d->n) * H2 * W2 * 8, 256), 256, 0, ctx->stream>>>(
+        a, xs, (int)d->n, (int)d->ih, (int)d->iw, (int)d->ci, H2, W2, (int)d->pad_top, (int)d->pad_left);
+    NNCB_LAUNCHED(ctx);
+    nncb_gemm_desc dd = *d;
+    dd.ih = H2; dd.iw = W2; dd.ci = 32; dd.kh = kh2; dd.kw = kw2; dd.sh = 1; dd.sw = 1;
+    dd.pad_top = 0; dd.pad_left = 0;
+    if (d->kind == NNCB_CONV_FWD) {
+        s2d_weight_k<<<grid_for(ctx, kh2 * kw2 * 32 * d->co, 256), 256, 0, ctx->stream>>>(
+            b, wsp, (int)d->kh, (int)d->kw, (int)d->ci, (int)d->co, kh2, kw2);
+        NNCB_LAUNCHED(ctx);
+        int rc = gemm_tc_impl(ctx, &dd, xs, 0, wsp, bias, out, handled);
+        if (!rc && !*handled) return fail("space-to-depth route: conv rejected");
+        return rc;
+    }
+    int rc = gemm_tc_impl(ctx, &dd, xs, 0, b, nullptr, wsp, handled);   // dW' = wgrad over x'
+    if (rc) return rc;
+    if (!*handled) return fail("space-to-depth route: wgrad rejected");
+    s2d_wgrad_back_k<<<grid_for(ctx, d->kh * d->kw * d->ci * d->co, 256), 256, 0, ctx->stream>>>(
+        wsp, out, (int)d->kh, (int)d->kw, (int)d->ci, (int)d->co, kw2);
+    NNCB_LAUNCHED(ctx);
+    return 0;
+}
+
 std::atomic<int> g_manual_a{getenv("NNCB_TC_MANUAL_A") ? 1 : 0};
 
 int gemm_tc_route(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const float* bias,
@@ -939,6 +1028,9 @@ int gemm_tc_route(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const 
         // gathers are slower than im2col for the stem today, so this is opt-in
         // (NNCB_TC_MANUAL_A=1) until the gather stages through a TMA patch.
         if (g_manual_a.load(std::memory_order_relaxed)) return gemm_tc_impl(ctx, d, a, 0, b, bias, out, handled, true);
+        static const bool im2col_stem = getenv("NNCB_TC_STEM") && std::string(getenv("NNCB_TC_STEM")) == "im2col";
+        if (d->sh == 2 && d->sw == 2 && 4 * d->ci <= 32 && !im2col_stem && drv::table().ok)
+            return gemm_tc_s2d(ctx, d, a, b, bias, out, handled);
     }
     if (conv && d->ci % 32 != 0 && (d->kind == NNCB_CONV_FWD || d->kind == NNCB_CONV_WGRAD) && drv::table().ok) {
         // Channels that do not fill a 32-wide K block (the 3-channel stem): lower

@@ -46,6 +46,8 @@ CONVS = [
     (2, 16, 16, 32, 64, 1, 2), (1, 9, 9, 64, 32, 3, 2), (3, 8, 8, 96, 128, 3, 1),
     # channel counts below a 32-wide block: builder-warp (manual A) path
     (3, 19, 23, 3, 32, 3, 1), (2, 15, 15, 12, 64, 5, 2), (1, 30, 30, 4, 128, 7, 2),
+    # stride-2 few-channel convs: space-to-depth route (odd sizes, SAME padding)
+    (2, 17, 23, 3, 32, 7, 2), (1, 9, 9, 8, 16, 3, 2),
 ]
 
 
