@@ -86,6 +86,10 @@ enum nncb_ew_op {
                                invstd = (float)(1/sqrt((double)var + imm));
                                r[dst] = ((x - mean)*invstd)*gamma + beta;
                                a = x, b = mean, c = var, d = gamma, e = beta         */
+    NNCB_EW_BN_GRAD_FAST = 14, /* BN_GRAD operands, per-channel quotients instead of a per-element
+                               division: dx = (gamma*invstd) * ((g - sum_g/M) - xhat*(sum_gx/M)).
+                               Not bit-identical to BN_GRAD; the runtime uses it only in the
+                               tf32 precision mode.                                       */
     NNCB_EW_REDUCE_BN_GRAD = 13, /* BatchNorm backward reduction fused into the group that
                                produces g (replaces nncb_bn_grad_reduce for it):
                                sum_g[c] += g, sum_gx[c] += g*xhat, xhat = (x-mean)*invstd,

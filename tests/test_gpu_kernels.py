@@ -183,3 +183,30 @@ def test_ew_fused_bn_grad_reduce(rows, C):
     ok(K.nncb_bn_grad_reduce(ctx(), xd.p, stats.p, out.p, ref_g.p, ref_gx.p, rows, C))
     np.testing.assert_allclose(got_g, ref_g.get((C,)), rtol=1e-5, atol=1e-5)
     np.testing.assert_allclose(got_gx, ref_gx.get((C,)), rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("rows,C", [(4096, 64), (1000, 256)])
+def test_bn_grad_fast_matches_exact(rows, C):
+    """tf32-mode BatchNorm input gradient (per-channel quotients) against the
+    bit-exact form (per-element IEEE division): same operands, <= 1e-5 of max."""
+    from tests.nncb_ctypes import ew_run
+    rng = np.random.default_rng(12)
+    x = rng.uniform(-2, 2, (rows, C)).astype(np.float32)
+    g = rng.uniform(-1, 1, (rows, C)).astype(np.float32)
+    mean = x.mean(0).astype(np.float32)
+    inv = (1.0 / np.sqrt(x.var(0) + 1e-5)).astype(np.float32)
+    gamma = rng.uniform(0.5, 1.5, C).astype(np.float32)
+    xhat = (x - mean) * inv
+    sg, sgx = g.sum(0).astype(np.float32), (g * xhat).sum(0).astype(np.float32)
+    outs = []
+    for op in (11, 14):
+        slots = [Dev(x), Dev(g), Dev(mean), Dev(inv), Dev(gamma), Dev(sg), Dev(sgx), Dev(nbytes=x.nbytes)]
+        prog = [dict(op=0, dst=0, slot=0), dict(op=0, dst=1, slot=1)] + \
+               [dict(op=1, dst=2 + i, slot=2 + i) for i in range(5)] + \
+               [dict(op=op, dst=7, a=0, b=1, c=2, d=3, e=4, f=5, h=6, imm=float(rows)), dict(op=2, a=7, slot=7)]
+        ew_run(prog, 8, slots, rows * C, C)
+        outs.append(slots[7].get((rows, C)))
+    exact, fast = outs
+    ref = gamma * inv * (g - (sg + xhat * sgx) / rows)
+    assert np.max(np.abs(exact - ref)) <= 1e-5 * np.max(np.abs(ref))
+    assert np.max(np.abs(fast - exact)) <= 1e-5 * np.max(np.abs(exact))
