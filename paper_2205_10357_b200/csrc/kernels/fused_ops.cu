@@ -384,6 +384,7 @@ __global__ void col_final_k(const double* __restrict__ part, int64_t chunks, int
     }
 }
 
+
 template <int MODE>
 int col_reduce(nncb_ctx* ctx, const float* x, const float* g, const float* stats, int64_t rows, int64_t C, double eps,
                float* out0, float* out1) {
@@ -398,7 +399,10 @@ int col_reduce(nncb_ctx* ctx, const float* x, const float* g, const float* stats
     if (chunks > 65535) chunks = 65535;
     if (chunks < 1) chunks = 1;
     int64_t rpc = (rows + chunks - 1) / chunks;
-    if (false && C % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+    // col_partial4_k (float4 rows) measured slower than the scalar 32x8 tiles on
+    // every ResNet-50 shape; kept behind NNCB_COL_VEC=1 for experiments
+    static const int vec = getenv("NNCB_COL_VEC") ? atoi(getenv("NNCB_COL_VEC")) : 0;
+    if (vec == 1 && C % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
         (!g || (reinterpret_cast<uintptr_t>(g) & 15) == 0) && (!stats || (reinterpret_cast<uintptr_t>(stats) & 15) == 0)) {
         int64_t ch4 = std::min<int64_t>((int64_t)ctx->sm_count * 8, std::max<int64_t>(1, rows / 64));
         int64_t rpc4 = (rows + ch4 - 1) / ch4;
