@@ -362,11 +362,15 @@ struct Program {
                     BoundLaunch& g = plan_steps[i];
                     if (g.kind != LaunchKind::Gemm || g.ptrs.back() != bn.ptrs[0]) continue;
                     if (g.gemm.kind != NNCB_CONV_FWD && g.gemm.kind != NNCB_DENSE_FWD) break;
-                    // the epilogue reduction only hides behind long main loops:
-                    // fuse when K >= 1024 (else the separate pass is cheaper)
+                    // measured per ResNet-50 shape (tools/gemm_bench.py --colstats vs
+                    // tools/stats_bench.py): the epilogue statistics cost less than a
+                    // separate pass over the output on every shape
+                    if (std::getenv("NNC_NO_FUSED_BN_STATS")) break;
+                    static const int64_t min_k = std::getenv("NNC_BN_STATS_FUSE_MIN_K")
+                                                     ? std::atoll(std::getenv("NNC_BN_STATS_FUSE_MIN_K")) : 0;
                     const int64_t K = g.gemm.kind == NNCB_DENSE_FWD ? g.gemm.in_f
                                                                     : g.gemm.kh * g.gemm.kw * g.gemm.ci;
-                    if (K < 1024 && !std::getenv("NNC_FUSE_ALL_BN_STATS")) break;
+                    if (K < min_k) break;
                     g.gemm.epilogue |= NNCB_EPI_COLSTATS;
                     g.gemm.colstats = reinterpret_cast<double*>(static_cast<uintptr_t>(doubles));  // offset for now
                     bn.bn_finalize = true;

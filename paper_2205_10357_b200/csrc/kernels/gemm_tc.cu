@@ -208,15 +208,15 @@ __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: 
 // store instruction writes 32/CH whole row segments of CH*16 contiguous
 // bytes instead of 32 scattered 16-byte pieces.
 //
-// CS: also accumulate BatchNorm column statistics of the valid rows from the
+// CS: also return BatchNorm column statistics of the valid rows, read from the
 // staged tile: with COLS columns per pass, lane l sums column l % COLS over
 // rows [(l / COLS) * RPL, +RPL), the 32/COLS row groups are folded with xor
-// shuffles, and one lane per column adds (sum, sum of squares) to the CTA's
-// double accumulator cs_acc at column cs_col0 + pass offset.
+// shuffles, and the pass's sums move to lane (pass * COLS + column), so on
+// return lane l holds (sum, sum of squares) of chunk column l in cs1 / cs2.
 template <int CH, bool CS>
 __device__ __forceinline__ void store_chunk_t(const uint32_t (&r)[32], uint8_t* tile, float* dst, bool valid,
-                                              int col0, int N, bool full_cols, int lane, bool store,
-                                              double* cs_acc = nullptr, int cs_col0 = 0, int cs_n = 0) {
+                                              int col0, int N, bool full_cols, int lane, bool store, float& cs1,
+                                              float& cs2) {
     constexpr int COLS = CH * 4, RPI = 32 / CH;   // columns per pass, rows per store instruction
     const uint32_t vmask = CS ? __ballot_sync(0xffffffffu, valid) : 0u;
 #pragma unroll
@@ -245,10 +245,12 @@ __device__ __forceinline__ void store_chunk_t(const uint32_t (&r)[32], uint8_t* 
                 s1 += __shfl_xor_sync(0xffffffffu, s1, sh);
                 s2 += __shfl_xor_sync(0xffffffffu, s2, sh);
             }
-            const int cl = cs_col0 + p * COLS + col;
-            if (lane < COLS && col0 + p * COLS + col < N) {
-                atomicAdd(cs_acc + cl, static_cast<double>(s1));
-                atomicAdd(cs_acc + cs_n + cl, static_cast<double>(s2));
+            // lanes [p*COLS, (p+1)*COLS) take columns p*COLS.. from lanes 0..COLS-1
+            const float t1 = __shfl_sync(0xffffffffu, s1, lane % COLS);
+            const float t2 = __shfl_sync(0xffffffffu, s2, lane % COLS);
+            if (lane / COLS == p) {
+                cs1 = t1;
+                cs2 = t2;
             }
         }
         if (!store) {
@@ -280,8 +282,10 @@ __device__ __forceinline__ void store_chunk_t(const uint32_t (&r)[32], uint8_t* 
 // tiles b, b + grid, ... The smem ring (TMA -> MMA) and the double-buffered TMEM
 // accumulator (MMA -> epilogue) carry their phases across tiles, so the
 // epilogue of one tile overlaps the main loop of the next.
-template <bool CS, bool MA>
-__global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MA ? 1 : 2)
+// MINB: CTAs per SM the build is register-budgeted for (2: <= 96 registers;
+// 1: no cap, used by the 448-thread MA build and by CS with 256-wide tiles).
+template <bool CS, bool MA, int MINB>
+__global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_c, const __grid_constant__ TcParams P) {
     const int STAGES = P.stages;
@@ -302,8 +306,6 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MA ? 1 : 2)
     int* ma_tab = reinterpret_cast<int*>(cs_acc + 2 * P.bn);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    if (CS)
-        for (int i = threadIdx.x; i < 2 * P.bn; i += blockDim.x) cs_acc[i] = 0.0;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], MA ? 1 + 128 : 1);   // MA: + one arrival per builder thread
@@ -566,6 +568,7 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MA ? 1 : 2)
         const int quarter = warp % 4;
         const int half = (warp - 2) / 4;
         const int row = quarter * 32 + lane;
+        double cs_sum[4] = {0, 0, 0, 0}, cs_sq[4] = {0, 0, 0, 0};   // CS: per-lane column accumulators
         uint32_t local = 0;
         for (int64_t t = blockIdx.x; t < P.tiles; t += gridDim.x, ++local) {
             const Tile T = decode(t);
@@ -593,7 +596,10 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MA ? 1 : 2)
                 tmem_base + acc * static_cast<uint32_t>(P.bn) + (static_cast<uint32_t>(quarter * 32) << 16);
             uint32_t r[32];
             bool arrived = false;
-            for (int c = half; c < nchunks; c += 2) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {   // this warp's chunks: c = half, half + 2, ... (<= 8 chunks)
+                const int c = half + 2 * k;
+                if (c >= nchunks) break;
                 tmem_ld32(tbase + static_cast<uint32_t>(c * 32), r);
                 if (c + 2 >= nchunks) {
                     // this warp's last chunk of the tile is in registers: release its share
@@ -618,28 +624,37 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MA ? 1 : 2)
                     uint8_t* tile = staging + (warp - 2) * (P.stg_cols * 128);
                     const bool full_cols = col0 + 32 <= P.N && (P.ldc % 4) == 0;
                     const bool st = !P.nostore;
+                    float c1 = 0.f, c2 = 0.f;
                     if (P.stg_cols == 32)
-                        store_chunk_t<8, CS>(r, tile, dst, valid, col0, P.N, full_cols, lane, st, cs_acc, c * 32, P.bn);
+                        store_chunk_t<8, CS>(r, tile, dst, valid, col0, P.N, full_cols, lane, st, c1, c2);
                     else if (P.stg_cols == 16)
-                        store_chunk_t<4, CS>(r, tile, dst, valid, col0, P.N, full_cols, lane, st, cs_acc, c * 32, P.bn);
+                        store_chunk_t<4, CS>(r, tile, dst, valid, col0, P.N, full_cols, lane, st, c1, c2);
                     else
-                        store_chunk_t<2, CS>(r, tile, dst, valid, col0, P.N, full_cols, lane, st, cs_acc, c * 32, P.bn);
+                        store_chunk_t<2, CS>(r, tile, dst, valid, col0, P.N, full_cols, lane, st, c1, c2);
+                    if (CS) {
+                        cs_sum[k] += static_cast<double>(c1);
+                        cs_sq[k] += static_cast<double>(c2);
+                    }
                 }
             }
             if (!arrived && lane == 0)   // a warp without a chunk in this tile still arrives once
                 asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_empty[acc])) : "memory");
             if (CS) {
+                // flush this warp's column accumulators when the CTA's next tile
+                // covers other columns (normally once, after the last tile)
                 const int64_t tn = t + gridDim.x;
                 const bool flush = tn >= P.tiles || (tn % P.n_tiles) * P.bn != T.n0;
                 if (flush) {
-                    asm volatile("bar.sync 1, 256;" ::: "memory");
-                    const int et = threadIdx.x - 64;
-                    for (int i = et; i < 2 * P.bn; i += 256) {
-                        const int cl = i % P.bn;
-                        if (T.n0 + cl < P.N) atomicAdd(P.colstats + (i / P.bn) * P.N + T.n0 + cl, cs_acc[i]);
-                        cs_acc[i] = 0.0;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int64_t col = T.n0 + (half + 2 * k) * 32 + lane;
+                        if (half + 2 * k < nchunks && col < P.N && cs_sum[k] != 0.0) {
+                            atomicAdd(P.colstats + col, cs_sum[k]);
+                            atomicAdd(P.colstats + P.N + col, cs_sq[k]);
+                        }
+                        cs_sum[k] = 0.0;
+                        cs_sq[k] = 0.0;
                     }
-                    asm volatile("bar.sync 1, 256;" ::: "memory");
                 }
             }
         }
@@ -758,10 +773,11 @@ TcShape pick_shape(int bn) {
 int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, TcParams& P) {
     static bool attr_done = false;
     if (!attr_done) {
-        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<false, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<true, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<true, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<false, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<true, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr_done = true;
     }
     if (P.tiles <= 0) return 0;
@@ -786,17 +802,19 @@ int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CU
     const size_t smem = smem_for(P.bn, P.stages, P.stg_cols, tab_ints);
     int per_sm = (env_stages > 0) ? ((P.bn <= 128 && smem <= 113 * 1024) ? 2 : 1) : shp.per_sm;
     if (env_persm > 0 && (env_persm == 1 || 2 * smem <= 228 * 1024)) per_sm = env_persm;
-    if (manual) per_sm = 1;
+    if (manual) per_sm = 1;   // the 448-thread build is compiled for one CTA per SM
     unsigned grid = static_cast<unsigned>(std::min<int64_t>(P.tiles, static_cast<int64_t>(ctx->sm_count) * per_sm));
     const unsigned threads = manual ? THREADS + 128 : THREADS;
     if (P.colstats && manual)
-        tc_gemm_kernel<true, true><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
+        tc_gemm_kernel<true, true, 1><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
     else if (manual)
-        tc_gemm_kernel<false, true><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
+        tc_gemm_kernel<false, true, 1><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
+    else if (P.colstats && per_sm == 1)
+        tc_gemm_kernel<true, false, 1><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
     else if (P.colstats)
-        tc_gemm_kernel<true, false><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
+        tc_gemm_kernel<true, false, 2><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
     else
-        tc_gemm_kernel<false, false><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
+        tc_gemm_kernel<false, false, 2><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
     NNCB_LAUNCHED(ctx);
     return 0;
 }

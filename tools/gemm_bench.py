@@ -39,6 +39,7 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--layers", default="")
+    ap.add_argument("--colstats", action="store_true", help="forward GEMMs also accumulate BN column statistics")
     a = ap.parse_args()
     timer = P.DeviceTimer()
     total = {}
@@ -54,7 +55,10 @@ def main():
             if kind == "dgrad" and ci % 32 and k > 1:
                 continue   # the stem's input gradient is never needed (and has no tensor-core lowering)
             code, A, B, O = {"fwd": (3, x, w, y), "dgrad": (4, y, w, x), "wgrad": (5, x, y, w)}[kind]
-            d = GemmDesc(kind=code, precision=0, epilogue=0, **g)
+            cs = Dev(nbytes=2 * co * 8) if (a.colstats and kind == "fwd") else None
+            d = GemmDesc(kind=code, precision=0, epilogue=4 if cs else 0, **g)
+            if cs:
+                d.colstats = cs.p
             rc = K.nncb_gemm(ctx(), ctypes.byref(d), A.p, B.p, None, O.p)   # warm-up
             assert rc == 0, K.nncb_last_error()
             timer.start()
