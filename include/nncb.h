@@ -97,7 +97,8 @@ enum nncb_ew_op {
                                c = mean, d = invstd (LOAD_CH regs); outputs: slot = sum_g,
                                e = sum_gx slot index. Needs the channel-stationary launch:
                                C a power of two in [4, 2048], n % 4 == 0, 16 B-aligned
-                               slots; at most one per program.                          */
+                               slots; at most two per program (e.g. the two BatchNorms
+                               of a residual join fed the same gradient).                */
 };
 
 typedef struct {

@@ -336,9 +336,11 @@ struct Lowering {
                     absorbed.insert(b->name);
                 }
             }
+            // each bundle takes its own dbeta sum: BatchNorms fed the same gradient
+            // (a residual join) have one SumNHW each, all equal to that bundle's sum_g
             for (const Node* n : mem)
                 if ((n->op == OpKind::SumNHW || n->op == OpKind::SumCols) && n->inputs[0] == head->inputs[2] &&
-                    sg.empty()) {
+                    sg.empty() && !absorbed.count(n->name)) {
                     sg = n->outputs[0];
                     bundle_of[n->name] = key;
                     absorbed.insert(n->name);

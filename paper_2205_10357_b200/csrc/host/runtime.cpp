@@ -294,21 +294,33 @@ struct Program {
         for (size_t pi = 0; pi < steps.size(); ++pi)
             for (size_t j = 1; j < steps[pi].size(); ++j) {
                 BoundLaunch& r = steps[pi][j];
-                BoundLaunch& e = steps[pi][j - 1];
-                if (r.kind != LaunchKind::BnGradReduce || r.skip || e.kind != LaunchKind::Ew || e.skip) continue;
+                if (r.kind != LaunchKind::BnGradReduce || r.skip) continue;
+                // the group that stores g: g, x and the statistics are all live
+                // until this reduction, so nothing in between overwrites them
+                size_t pj = j;
+                for (size_t i = j; i-- > 0 && pj == j;) {
+                    const BoundLaunch& c = steps[pi][i];
+                    if (c.kind != LaunchKind::Ew || c.skip) continue;
+                    for (const auto& in : c.ew_prog.empty() ? sources[pi][i]->ew : c.ew_prog)
+                        if (in.op == NNCB_EW_STORE && c.ptrs[in.slot] == r.ptrs[2]) pj = i;
+                }
+                if (pj == j) continue;
+                BoundLaunch& e = steps[pi][pj];
                 const int64_t rows = r.d0, C = r.d1;
                 if (C < 4 || C > 2048 || (C & (C - 1)) || (rows * C) % 4 || e.n != rows * C) continue;
                 if (e.c > 0 && e.c != C) continue;
-                const Launch& L = *sources[pi][j - 1];
+                const Launch& L = *sources[pi][pj];
                 std::vector<nncb_ew_instr> prog = e.ew_prog.empty() ? L.ew : e.ew_prog;
                 int regs = e.ew_prog.empty() ? L.ew_regs : e.ew_regs;
-                bool has_reduce = false;
+                int n_reduce = 0;
                 int at = -1;
                 for (size_t k = 0; k < prog.size(); ++k) {
-                    has_reduce = has_reduce || prog[k].op == NNCB_EW_REDUCE_BN_GRAD;
+                    n_reduce += prog[k].op == NNCB_EW_REDUCE_BN_GRAD;
                     if (prog[k].op == NNCB_EW_STORE && e.ptrs[prog[k].slot] == r.ptrs[2]) at = static_cast<int>(k);
                 }
-                if (has_reduce || at < 0 || e.ptrs.size() + 5 > 48) continue;
+                // one reduction per group: a second one (residual joins) needs a
+                // 2-block register budget and measured slower than the standalone pass
+                if (n_reduce >= 1 || at < 0 || e.ptrs.size() + 5 > 48) continue;
                 const int s0 = static_cast<int>(e.ptrs.size());
                 std::vector<void*> ptrs = e.ptrs;
                 ptrs.push_back(r.ptrs[0]);                                  // x

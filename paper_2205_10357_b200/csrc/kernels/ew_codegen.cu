@@ -30,7 +30,8 @@ struct nncb_ew_kernel {
     CUfunction fn = nullptr;
     int n_slots = 0;
     bool uses_channels = false;
-    int reduce_sg = -1, reduce_sgx = -1;   // REDUCE_BN_GRAD output slots (-1: no reduction)
+    int n_reduce = 0;                      // REDUCE_BN_GRAD instructions (<= 2)
+    int reduce_sg[2] = {-1, -1}, reduce_sgx[2] = {-1, -1};   // their output slots
 };
 
 void nncb::ew_release(nncb_ew_kernel* k) {
@@ -84,6 +85,7 @@ std::string reg(int r) { return "r" + std::to_string(r); }
 
 // Emits the body for W lanes (W = 4: float4 path, W = 1: scalar tail).
 void emit_body(std::ostringstream& os, const nncb_ew_program& p, int W, bool uses_ch, bool stationary = false) {
+    int reduce_index = 0;
     os << "  float ";
     for (int r = 0; r < p.n_regs; ++r) os << (r ? ", " : "") << reg(r) << "[" << W << "]";
     os << ";\n";
@@ -113,12 +115,16 @@ void emit_body(std::ostringstream& os, const nncb_ew_program& p, int W, bool use
                     os << "  #pragma unroll\n  for (int j = 0; j < " << W << "; ++j) " << d << "[j] = __ldg(" << ptr
                        << " + ch[j]);\n";
                 continue;
-            case NNCB_EW_REDUCE_BN_GRAD:
+            case NNCB_EW_REDUCE_BN_GRAD: {
                 if (!stationary) continue;   // launch guarantees the channel-stationary path
+                const std::string r0 = "red" + std::to_string(reduce_index) + "_0",
+                                  r1 = "red" + std::to_string(reduce_index) + "_1";
+                ++reduce_index;
                 os << "  #pragma unroll\n  for (int j = 0; j < " << W << "; ++j) { const double xh = ((double)" << b
-                   << "[j] - (double)" << c << "[j]) * (double)" << dd << "[j]; red0[j] += (double)" << a
-                   << "[j]; red1[j] += (double)" << a << "[j] * xh; }\n";
+                   << "[j] - (double)" << c << "[j]) * (double)" << dd << "[j]; " << r0 << "[j] += (double)" << a
+                   << "[j]; " << r1 << "[j] += (double)" << a << "[j] * xh; }\n";
                 continue;
+            }
             case NNCB_EW_STORE:
                 if (W == 4)
                     os << "  *reinterpret_cast<float4*>(" << ptr << " + i) = make_float4(" << a << "[0], " << a
@@ -161,15 +167,17 @@ void emit_body(std::ostringstream& os, const nncb_ew_program& p, int W, bool use
     }
 }
 
-int find_reduce(const nncb_ew_program& p) {
+std::vector<int> find_reduces(const nncb_ew_program& p) {
+    std::vector<int> r;
     for (int k = 0; k < p.n_instr; ++k)
-        if (p.instr[k].op == NNCB_EW_REDUCE_BN_GRAD) return k;
-    return -1;
+        if (p.instr[k].op == NNCB_EW_REDUCE_BN_GRAD) r.push_back(k);
+    return r;
 }
 
 std::string generate(const nncb_ew_program& p, bool uses_ch) {
     std::ostringstream os;
-    const bool red = find_reduce(p) >= 0;
+    const int nred = static_cast<int>(find_reduces(p).size());
+    const bool red = nred > 0;
     os << kPrelude;
     os << "__device__ __forceinline__ void body4(const EwArgs& A, i64 i) {\n";
     emit_body(os, p, 4, uses_ch);
@@ -185,7 +193,7 @@ std::string generate(const nncb_ew_program& p, bool uses_ch) {
         // operands are loaded once (float4) into registers before the loop.
         os << "__device__ __forceinline__ void body4s(const EwArgs& A, i64 i";
         for (int k : chregs) os << ", const float (&pc" << p.instr[k].dst << ")[4]";
-        if (red) os << ", double (&red0)[4], double (&red1)[4]";
+        for (int q = 0; q < nred; ++q) os << ", double (&red" << q << "_0)[4], double (&red" << q << "_1)[4]";
         os << ") {\n";
         emit_body(os, p, 4, uses_ch, true);
         os << "}\n";
@@ -200,8 +208,9 @@ std::string generate(const nncb_ew_program& p, bool uses_ch) {
     static const int env_min_blocks = getenv("NNCB_EW_MINBLOCKS") ? atoi(getenv("NNCB_EW_MINBLOCKS")) : -1;
     int min_blocks = chregs.size() >= 3 ? 4 : 0;
     if (env_min_blocks >= 0) min_blocks = env_min_blocks;
-    if (red)
-        os << "extern \"C\" __global__ void __launch_bounds__(256, 4) nnc_fused_ew(const EwArgs A) {";
+    if (red)   // 16 double accumulator registers per reduction
+        os << "extern \"C\" __global__ void __launch_bounds__(256, " << (nred > 1 ? 2 : 4)
+           << ") nnc_fused_ew(const EwArgs A) {";
     else if (min_blocks > 0)
         os << "extern \"C\" __global__ void __launch_bounds__(256, " << min_blocks << ") nnc_fused_ew(const EwArgs A) {";
     else
@@ -221,9 +230,9 @@ std::string generate(const nncb_ew_program& p, bool uses_ch) {
         }
         std::string args;
         for (int k : chregs) args += ", pc" + std::to_string(p.instr[k].dst);
-        if (red) {
-            args += ", red0, red1";
-            os << "    double red0[4] = {0, 0, 0, 0}, red1[4] = {0, 0, 0, 0};\n";
+        for (int q = 0; q < nred; ++q) {
+            args += ", red" + std::to_string(q) + "_0, red" + std::to_string(q) + "_1";
+            os << "    double red" << q << "_0[4] = {0, 0, 0, 0}, red" << q << "_1[4] = {0, 0, 0, 0};\n";
         }
         os << "    for (; v + stride < nvec; v += 2 * stride) { body4s(A, v << 2" << args << "); body4s(A, (v + stride) << 2"
            << args << "); }\n";
@@ -232,14 +241,15 @@ std::string generate(const nncb_ew_program& p, bool uses_ch) {
             // Per-block partials, deterministic: for C <= 1024 (a power of two)
             // threads t and t + C/4 share channels and thread q < C/4 folds its
             // group in t order; for C > 1024 each thread owns its 4 channels.
-            os << R"(    __shared__ double rs[256][8];
-    const int t = threadIdx.x;
-    #pragma unroll
-    for (int j = 0; j < 4; ++j) { rs[t][j] = red0[j]; rs[t][4 + j] = red1[j]; }
-    __syncthreads();
-    const int C = (int)A.C;
-    double* part = A.part + (i64)blockIdx.x * 2 * C;
-    if (C <= 1024) {
+            // Reduction q writes the slice A.part + q * gridDim.x * 2C.
+            os << "    __shared__ double rs[256][8];\n    const int t = threadIdx.x;\n    const int C = (int)A.C;\n";
+            for (int q = 0; q < nred; ++q) {
+                const std::string r0 = "red" + std::to_string(q) + "_0", r1 = "red" + std::to_string(q) + "_1";
+                os << "    {\n    if (" << q << " > 0) __syncthreads();\n"
+                   << "    #pragma unroll\n    for (int j = 0; j < 4; ++j) { rs[t][j] = " << r0 << "[j]; rs[t][4 + j] = "
+                   << r1 << "[j]; }\n    __syncthreads();\n"
+                   << "    double* part = A.part + ((i64)" << q << " * gridDim.x + blockIdx.x) * 2 * C;\n"
+                   << R"(    if (C <= 1024) {
       const int G = C >> 2;
       if (t < G) {
         double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -252,9 +262,8 @@ std::string generate(const nncb_ew_program& p, bool uses_ch) {
       }
     } else {
       #pragma unroll
-      for (int j = 0; j < 4; ++j) { part[c0 + j] = red0[j]; part[C + c0 + j] = red1[j]; }
-    }
-)";
+)" << "      for (int j = 0; j < 4; ++j) { part[c0 + j] = " << r0 << "[j]; part[C + c0 + j] = " << r1 << "[j]; }\n    }\n    }\n";
+            }
         }
         os << "    return;\n  }\n";
     }
@@ -367,9 +376,15 @@ int nncb_ew_compile(nncb_ctx* ctx, const nncb_ew_program* p, nncb_ew_kernel** ou
     k->source = src;
     k->n_slots = p->n_slots;
     k->uses_channels = uses_ch;
-    if (int r = find_reduce(*p); r >= 0) {
-        k->reduce_sg = p->instr[r].slot;
-        k->reduce_sgx = p->instr[r].e;
+    const std::vector<int> reds = find_reduces(*p);
+    if (reds.size() > 2) {
+        nncb::ew_release(k);
+        return nncb::fail("nncb_ew_compile: at most two REDUCE_BN_GRAD per program");
+    }
+    for (int r : reds) {
+        k->reduce_sg[k->n_reduce] = p->instr[r].slot;
+        k->reduce_sgx[k->n_reduce] = p->instr[r].e;
+        ++k->n_reduce;
     }
     const auto& D = nncb::drv::table();
     if (!D.ok) {
@@ -420,7 +435,7 @@ int nncb_ew_launch(nncb_ctx* ctx, nncb_ew_kernel* k, void* const* slots, int64_t
     if (dbg)
         fprintf(stderr, "[nncb ew] n=%lld C=%lld uses_ch=%d cs=%d grid=%u slots=%d\n", (long long)n,
                 (long long)channels, (int)k->uses_channels, args.cs, grid, k->n_slots);
-    const bool reduce = k->reduce_sg >= 0;
+    const bool reduce = k->n_reduce > 0;
     if (reduce) {
         // the reduction runs only on the channel-stationary path: C a power of
         // two in [4, 2048]; a bounded grid keeps the per-block partials small
@@ -430,7 +445,7 @@ int nncb_ew_launch(nncb_ctx* ctx, nncb_ew_kernel* k, void* const* slots, int64_t
         const int64_t g = C / std::gcd<int64_t>(C, 1024);
         const int64_t cap = std::max<int64_t>(g, (4 * static_cast<int64_t>(ctx->sm_count) / g) * g);
         if (grid > cap) grid = static_cast<unsigned>(cap);
-        args.part = static_cast<double*>(nncb::scratch(ctx, sizeof(double) * 2 * C * grid));
+        args.part = static_cast<double*>(nncb::scratch(ctx, sizeof(double) * 2 * C * grid * k->n_reduce));
         if (!args.part) return nncb::fail("nncb_ew_launch: reduction scratch allocation failed");
     }
     void* params[] = {&args};
@@ -441,10 +456,13 @@ int nncb_ew_launch(nncb_ctx* ctx, nncb_ew_kernel* k, void* const* slots, int64_t
     ctx->launches.fetch_add(1, std::memory_order_relaxed);
     if (reduce) {
         const int C = static_cast<int>(channels);
-        ew_red_final_k<<<(C + 31) / 32, dim3(32, 8), 0, ctx->stream>>>(args.part, static_cast<int>(grid), C,
-                                                                       args.p[k->reduce_sg], args.p[k->reduce_sgx]);
-        NNCB_CUDA(cudaGetLastError());
-        ctx->launches.fetch_add(1, std::memory_order_relaxed);
+        for (int q = 0; q < k->n_reduce; ++q) {
+            ew_red_final_k<<<(C + 31) / 32, dim3(32, 8), 0, ctx->stream>>>(
+                args.part + static_cast<size_t>(q) * grid * 2 * C, static_cast<int>(grid), C, args.p[k->reduce_sg[q]],
+                args.p[k->reduce_sgx[q]]);
+            NNCB_CUDA(cudaGetLastError());
+            ctx->launches.fetch_add(1, std::memory_order_relaxed);
+        }
     }
     return 0;
 }

@@ -210,3 +210,32 @@ def test_bn_grad_fast_matches_exact(rows, C):
     ref = gamma * inv * (g - (sg + xhat * sgx) / rows)
     assert np.max(np.abs(exact - ref)) <= 1e-5 * np.max(np.abs(ref))
     assert np.max(np.abs(fast - exact)) <= 1e-5 * np.max(np.abs(exact))
+
+
+def test_ew_two_fused_bn_grad_reductions():
+    """Two REDUCE_BN_GRAD in one group (the two BatchNorms of a residual join
+    receive the same gradient): each matches the standalone reduction."""
+    from tests.nncb_ctypes import ew_run
+    rows, C = 2048, 256
+    rng = np.random.default_rng(13)
+    g = rng.uniform(-1, 1, (rows, C)).astype(np.float32)
+    xs = [rng.uniform(-2, 2, (rows, C)).astype(np.float32) for _ in range(2)]
+    stats = [(x.mean(0).astype(np.float32), (1.0 / np.sqrt(x.var(0) + 1e-5)).astype(np.float32)) for x in xs]
+    gd, out = Dev(g), Dev(nbytes=g.nbytes)
+    devs = [(Dev(x), Dev(m), Dev(s), Dev(nbytes=C * 4), Dev(nbytes=C * 4)) for x, (m, s) in zip(xs, stats)]
+    slots = [gd, out] + [d for t in devs for d in t]
+    prog = [dict(op=0, dst=0, slot=0), dict(op=3, dst=1, a=0), dict(op=2, a=1, slot=1)]
+    for q in range(2):
+        b = 2 + 5 * q
+        r = 2 + 3 * q
+        prog += [dict(op=0, dst=r, slot=b), dict(op=1, dst=r + 1, slot=b + 1), dict(op=1, dst=r + 2, slot=b + 2),
+                 dict(op=13, a=1, b=r, c=r + 1, d=r + 2, slot=b + 3, e=b + 4)]
+    ew_run(prog, 8, slots, rows * C, C)
+    gr = np.maximum(g, 0)
+    for q, (xd, md, sd, sg, sgx) in enumerate(devs):
+        ref_g, ref_gx = Dev(nbytes=C * 4), Dev(nbytes=C * 4)
+        st = Dev(np.concatenate(stats[q]))
+        ok(K.nncb_bn_grad_reduce(ctx(), xd.p, st.p, out.p, ref_g.p, ref_gx.p, rows, C))
+        np.testing.assert_allclose(sg.get((C,)), ref_g.get((C,)), rtol=1e-5, atol=1e-5)
+        np.testing.assert_allclose(sgx.get((C,)), ref_gx.get((C,)), rtol=1e-5, atol=1e-5)
+    assert np.array_equal(out.get((rows, C)), gr)
