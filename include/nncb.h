@@ -166,6 +166,8 @@ typedef struct {
 int nncb_gemm_last_path(void);
 /* Route for convolutions with channels % 32 != 0: 1 = builder-warp gather, 0 = im2col (default). */
 int nncb_gemm_set_manual_a(int on);
+/* Forces the tcgen05 tile: N width (64/128/256) | (1 << 16) for CTA pairs (cta_group::2); 0 = autotune. */
+int nncb_gemm_force_tile(int code);
 int nncb_gemm(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b,
               const float* bias, float* out);
 

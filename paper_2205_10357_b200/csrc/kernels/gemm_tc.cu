@@ -87,6 +87,10 @@ struct TcParams {
     const float* xa;    // activation [gn?, ih, iw, ci]
     int ih_, iw_;       // activation image dims
     int K_;             // kh*kw*ci
+    // --- CTA pair (cta_group::2): 256-row tiles over two SMs ----------------
+    int pair;           // 1: cluster of 2, leader issues M=256 MMAs, each CTA loads half of B
+    int64_t pix_pairs;  // MODE_CONV: pixel-box pairs per phase
+    int64_t m_pairs;    // MODE_WGRAD: M-tile pairs
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -111,6 +115,51 @@ __device__ __forceinline__ void cp_async4(void* dst, const float* src, int src_b
 // arrive on `bar` once all of this thread's prior cp.async copies have landed
 __device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// CTA-pair variants: the mbarrier operand is a shared::cluster address (the
+// leader CTA's barrier), the destination is this CTA's own shared memory.
+__device__ __forceinline__ void tma_load_4d_pair(void* dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                                 int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+// shared::cluster address of `p`'s counterpart in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_u32(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx_cluster(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -170,6 +219,23 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64
 
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+// CTA pair: M=256 MMA issued by the leader over both CTAs' shared memory
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// completion of the leader's MMAs arrives on the barrier at the same offset in both CTAs
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 ::"r"(smem_u32(bar)), "h"(static_cast<uint16_t>(3))
                  : "memory");
 }
 
@@ -284,7 +350,7 @@ __device__ __forceinline__ void store_chunk_t(const uint32_t (&r)[32], uint8_t* 
 // epilogue of one tile overlaps the main loop of the next.
 // MINB: CTAs per SM the build is register-budgeted for (2: <= 96 registers;
 // 1: no cap, used by the 448-thread MA build and by CS with 256-wide tiles).
-template <bool CS, bool MA, int MINB>
+template <bool CS, bool MA, int MINB, bool PAIR>
 __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_c, const __grid_constant__ TcParams P) {
@@ -292,7 +358,9 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t a_bytes = BM * BK * 4;                 // 16 KB
-    const uint32_t b_bytes = static_cast<uint32_t>(P.bn) * BK * 4;
+    // PAIR: this CTA holds half of the B tile's columns (the MMA spans both CTAs)
+    const uint32_t b_bytes = static_cast<uint32_t>(PAIR ? P.bn / 2 : P.bn) * BK * 4;
+    const uint32_t rank = PAIR ? cluster_rank() : 0u;
     const uint32_t stage_bytes = a_bytes + b_bytes;
     uint8_t* staging = smem + STAGES * stage_bytes;       // 8 x stg_cols*128 B: one transpose tile per epilogue warp
     uint64_t* full = reinterpret_cast<uint64_t*>(staging + 8 * P.stg_cols * 128);
@@ -308,12 +376,13 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], MA ? 1 + 128 : 1);   // MA: + one arrival per builder thread
+            // MA: + one arrival per builder thread; PAIR: both CTAs' producers arrive (leader's copy)
+            mbar_init(&full[s], MA ? 1 + 128 : PAIR ? 2 : 1);
             mbar_init(&empty[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&tmem_full[s], 1);
-            mbar_init(&tmem_empty[s], 8);                 // one arrival per epilogue warp
+            mbar_init(&tmem_empty[s], PAIR ? 16 : 8);     // one arrival per epilogue warp (of both CTAs)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -338,14 +407,25 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
     }
     const uint32_t tmem_cols = 2 * static_cast<uint32_t>(P.bn);   // two accumulators
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(tmem_cols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if (PAIR) {   // the same columns in both CTAs of the pair
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                         "r"(tmem_cols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                         "r"(tmem_cols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
+    if (PAIR)
+        cluster_sync_all();   // peer barriers initialised before any remote arrive
+    else
+        __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem_base = *tmem_slot;
+    // PAIR: both CTAs of a cluster walk the same tiles (one tile = both CTAs' rows)
+    const int64_t t_begin = PAIR ? blockIdx.x / 2 : blockIdx.x, t_step = PAIR ? gridDim.x / 2 : gridDim.x;
 
     // ---- tile decode (identical in every role) ------------------------------
     struct Tile {
@@ -357,8 +437,10 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
         T.n0 = (t % P.n_tiles) * P.bn;
         int64_t rest = t / P.n_tiles;
         if (P.mode == MODE_CONV) {
-            int64_t pix = rest % P.pix_tiles;
-            T.phase = static_cast<int>(rest / P.pix_tiles);
+            // PAIR: tile t covers pixel boxes 2q, 2q+1 (one per CTA); a box past
+            // the grid is fully out of bounds (zero loads, no stores)
+            int64_t pix = PAIR ? 2 * (rest % P.pix_pairs) + rank : rest % P.pix_tiles;
+            T.phase = static_cast<int>(PAIR ? rest / P.pix_pairs : rest / P.pix_tiles);
             int tw = static_cast<int>(pix % P.tiles_w);
             pix /= P.tiles_w;
             int th = static_cast<int>(pix % P.tiles_h);
@@ -369,8 +451,8 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
             T.kb_begin = 0;
             T.nk = P.ntaps[T.phase] * P.cblocks;
         } else {
-            T.m0 = (rest % P.m_tiles) * BM;
-            T.split = static_cast<int>(rest / P.m_tiles);
+            T.m0 = PAIR ? (2 * (rest % P.m_pairs) + rank) * BM : (rest % P.m_tiles) * BM;
+            T.split = static_cast<int>(PAIR ? rest / P.m_pairs : rest / P.m_tiles);
             int per = (P.kboxes + P.splits - 1) / P.splits;
             T.kb_begin = min(P.kboxes, T.split * per);
             T.nk = min(P.kboxes, T.kb_begin + per) - T.kb_begin;
@@ -387,32 +469,58 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
         // issues every load, so no divisions may sit on the per-k-step path.
         int slot = 0;
         uint32_t phase = 0, filled = 0;
+        uint32_t bar_cl = 0;   // PAIR: the leader's full[slot] as a cluster address
         auto acquire = [&](uint8_t*& sa, uint64_t*& bar) {
             if (filled >= static_cast<uint32_t>(STAGES)) mbar_wait(&empty[slot], phase ^ 1u);
             sa = smem + slot * stage_bytes;
             bar = &full[slot];
-            mbar_expect_tx(bar, MA ? b_bytes : stage_bytes);
+            if (PAIR) {
+                // the leader's barrier counts both CTAs' bytes and one arrival per
+                // producer; these arrivals publish no data (the bytes come with
+                // TMA complete_tx), so no cluster-scope release fence is needed
+                bar_cl = mapa_u32(&full[slot], 0);
+                if (rank == 0)
+                    mbar_expect_tx(bar, 2 * stage_bytes);
+                else
+                    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cl) : "memory");
+            } else {
+                mbar_expect_tx(bar, MA ? b_bytes : stage_bytes);
+            }
         };
+        auto ld4 = [&](void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2, int c3) {
+            if (PAIR)
+                tma_load_4d_pair(dst, map, bar_cl, c0, c1, c2, c3);
+            else
+                tma_load_4d(dst, map, bar, c0, c1, c2, c3);
+        };
+        auto ld2 = [&](void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+            if (PAIR)
+                tma_load_2d_pair(dst, map, bar_cl, c0, c1);
+            else
+                tma_load_2d(dst, map, bar, c0, c1);
+        };
+        // B columns this CTA loads: all of the N tile, or its half in a pair
+        const int bcols = PAIR ? P.bn / 2 : P.bn, boff = PAIR ? static_cast<int>(rank) * (P.bn / 2) : 0;
         auto advance = [&]() {
             ++filled;
             if (++slot == STAGES) { slot = 0; phase ^= 1u; }
         };
-        for (int64_t t = blockIdx.x; t < P.tiles; t += gridDim.x) {
+        for (int64_t t = t_begin; t < P.tiles; t += t_step) {
             const Tile T = decode(t);
             if (P.mode == MODE_CONV) {
                 int tap = P.tap0[T.phase], cb = 0;
-                const int aw = T.tw0 * P.mw, ah = T.th0 * P.mh, n0 = static_cast<int>(T.n0);
+                const int aw = T.tw0 * P.mw, ah = T.th0 * P.mh, n0 = static_cast<int>(T.n0) + boff;
                 int xw = aw + P.off_w[tap], yh = ah + P.off_h[tap], br = P.brow[tap];
                 for (int i = 0; i < T.nk; ++i) {
                     uint8_t* sa; uint64_t* bar;
                     acquire(sa, bar);
                     uint8_t* sb = sa + a_bytes;
                     const int c0 = cb * BK;
-                    if (!MA) tma_load_4d(sa, &map_a, bar, c0, xw, yh, T.tn0);
+                    if (!MA) ld4(sa, &map_a, bar, c0, xw, yh, T.tn0);
                     if (P.b_mn) {
-                        for (int q = 0; q < P.bn / 32; ++q) tma_load_2d(sb + q * 4096, &map_b, bar, n0 + 32 * q, br + c0);
+                        for (int q = 0; q < bcols / 32; ++q) ld2(sb + q * 4096, &map_b, bar, n0 + 32 * q, br + c0);
                     } else {
-                        tma_load_2d(sb, &map_b, bar, c0, br + n0);
+                        ld2(sb, &map_b, bar, c0, br + n0);   // box rows = bcols (encoded on the host)
                     }
                     advance();
                     if (++cb == P.cblocks && i + 1 < T.nk) {
@@ -437,7 +545,7 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                 r /= P.tiles_w;
                 int x0 = bw * P.TW, y0 = (r % P.tiles_h) * P.TH, n0 = (r / P.tiles_h) * P.TN;
                 const int xend = P.tiles_w * P.TW, yend = P.tiles_h * P.TH;
-                const int nb = P.bn / 32, cn0 = static_cast<int>(T.n0);
+                const int nb = bcols / 32, cn0 = static_cast<int>(T.n0) + boff;
                 for (int i = 0; i < T.nk; ++i) {
                     uint8_t* sa; uint64_t* bar;
                     acquire(sa, bar);
@@ -445,10 +553,9 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                     const int xs = x0 * P.sw, ys = y0 * P.sh;
                     if (!MA) {
 #pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            tma_load_4d(sa + q * 4096, &map_a, bar, ac[q], xs + ax[q], ys + ay[q], n0);
+                        for (int q = 0; q < 4; ++q) ld4(sa + q * 4096, &map_a, bar, ac[q], xs + ax[q], ys + ay[q], n0);
                     }
-                    for (int q = 0; q < nb; ++q) tma_load_4d(sb + q * 4096, &map_b, bar, cn0 + 32 * q, x0, y0, n0);
+                    for (int q = 0; q < nb; ++q) ld4(sb + q * 4096, &map_b, bar, cn0 + 32 * q, x0, y0, n0);
                     advance();
                     x0 += P.TW;
                     if (x0 >= xend) {
@@ -459,15 +566,15 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                 }
             }
         }
-    } else if (warp == 1 && lane == 0) {
-        // ================= MMA issuer (single thread) =================
+    } else if (warp == 1 && lane == 0 && (!PAIR || rank == 0)) {
+        // ================= MMA issuer (single thread; PAIR: the leader CTA only) =================
         const uint32_t a_mn = (P.mode == MODE_WGRAD && !MA) ? 1u : 0u;
         const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (a_mn << 15) |
                                (static_cast<uint32_t>(P.b_mn) << 16) | ((static_cast<uint32_t>(P.bn) >> 3) << 17) |
-                               ((static_cast<uint32_t>(BM) >> 4) << 24);
+                               ((static_cast<uint32_t>(PAIR ? 2 * BM : BM) >> 4) << 24);
         int slot = 0;
         uint32_t phase = 0, local = 0;
-        for (int64_t t = blockIdx.x; t < P.tiles; t += gridDim.x, ++local) {
+        for (int64_t t = t_begin; t < P.tiles; t += t_step, ++local) {
             const Tile T = decode(t);
             const uint32_t acc = local & 1;
             // every tile takes an accumulator turn (tiles without K steps commit
@@ -487,11 +594,20 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                 for (int kk = 0; kk < BK / 8; ++kk) {
                     const uint64_t ad = a_mn ? sdesc(sa + kk * 1024, 4096, 512, 1) : sdesc(sa + kk * 32, 16, 1024, 2);
                     const uint64_t bd = P.b_mn ? sdesc(sb + kk * 1024, 4096, 512, 1) : sdesc(sb + kk * 32, 16, 1024, 2);
-                    mma_tf32(d, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                    if (PAIR)
+                        mma_tf32_pair(d, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                    else
+                        mma_tf32(d, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
                 }
-                mma_commit(&empty[s]);
+                if (PAIR)
+                    mma_commit_pair(&empty[s]);   // frees the stage in both CTAs
+                else
+                    mma_commit(&empty[s]);
             }
-            mma_commit(&tmem_full[acc]);
+            if (PAIR)
+                mma_commit_pair(&tmem_full[acc]);
+            else
+                mma_commit(&tmem_full[acc]);
         }
     } else if (MA && warp >= 10) {
         // ================= A builders (warps 10..13, MA only) =================
@@ -504,7 +620,7 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
         int slot = 0;
         uint32_t phase = 0, filled = 0;
         const int kpad = P.cblocks * BK;
-        for (int64_t tt = blockIdx.x; tt < P.tiles; tt += gridDim.x) {
+        for (int64_t tt = t_begin; tt < P.tiles; tt += t_step) {
             const Tile T = decode(tt);
             if (P.mode == MODE_CONV) {
                 const int pw = T.tw0 + t % P.TW, ph = T.th0 + (t / P.TW) % P.TH, pn = T.tn0 + t / (P.TW * P.TH);
@@ -570,7 +686,7 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
         const int row = quarter * 32 + lane;
         double cs_sum[4] = {0, 0, 0, 0}, cs_sq[4] = {0, 0, 0, 0};   // CS: per-lane column accumulators
         uint32_t local = 0;
-        for (int64_t t = blockIdx.x; t < P.tiles; t += gridDim.x, ++local) {
+        for (int64_t t = t_begin; t < P.tiles; t += t_step, ++local) {
             const Tile T = decode(t);
             const uint32_t acc = local & 1;
             mbar_wait(&tmem_full[acc], (local / 2) & 1);
@@ -604,9 +720,13 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                 if (c + 2 >= nchunks) {
                     // this warp's last chunk of the tile is in registers: release its share
                     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                    if (lane == 0)
-                        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_empty[acc]))
-                                     : "memory");
+                    if (lane == 0) {
+                        if (PAIR)   // the leader's MMA waits for both CTAs' epilogues
+                            mbar_arrive_cluster(mapa_u32(&tmem_empty[acc], 0));
+                        else
+                            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_empty[acc]))
+                                         : "memory");
+                    }
                     arrived = true;
                 }
                 const int64_t col0 = T.n0 + c * 32;
@@ -637,12 +757,16 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                     }
                 }
             }
-            if (!arrived && lane == 0)   // a warp without a chunk in this tile still arrives once
-                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_empty[acc])) : "memory");
+            if (!arrived && lane == 0) {   // a warp without a chunk in this tile still arrives once
+                if (PAIR)
+                    mbar_arrive_cluster(mapa_u32(&tmem_empty[acc], 0));
+                else
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_empty[acc])) : "memory");
+            }
             if (CS) {
                 // flush this warp's column accumulators when the CTA's next tile
                 // covers other columns (normally once, after the last tile)
-                const int64_t tn = t + gridDim.x;
+                const int64_t tn = t + t_step;
                 const bool flush = tn >= P.tiles || (tn % P.n_tiles) * P.bn != T.n0;
                 if (flush) {
 #pragma unroll
@@ -660,10 +784,16 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
+    if (PAIR)
+        cluster_sync_all();   // no remote arrive or MMA into this CTA remains outstanding
+    else
+        __syncthreads();
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols));
+        if (PAIR)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols));
     }
 }
 
@@ -711,7 +841,8 @@ bool encode_2d(CUtensorMap* map, const float* base, int64_t inner, int64_t rows,
     return r == CUDA_SUCCESS;
 }
 
-thread_local int g_force_bn = 0;   // set by the autotuner (gemm_tc) for one call
+thread_local int g_force_bn = 0;     // set by the autotuner (gemm_tc) for one call
+thread_local int g_force_pair = 0;   // 1: run the call as CTA pairs (cta_group::2)
 
 int pick_bn(int64_t n) {
     static const int env_bn = getenv("NNCB_TC_BN") ? atoi(getenv("NNCB_TC_BN")) : 0;   // tuning knob
@@ -773,11 +904,13 @@ TcShape pick_shape(int bn) {
 int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, TcParams& P) {
     static bool attr_done = false;
     if (!attr_done) {
-        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<false, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<true, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<true, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<false, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<true, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<false, false, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<true, false, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<true, false, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<false, true, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<true, true, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<false, false, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<true, false, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr_done = true;
     }
     if (P.tiles <= 0) return 0;
@@ -792,6 +925,33 @@ int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CU
     if (env_stg == 8 || env_stg == 16 || env_stg == 32) P.stg_cols = env_stg;
     if (env_stages > 0) P.stages = std::min(env_stages, MAX_STAGES);
     P.nostore = env_nostore;
+    if (P.pair) {
+        // CTA pair: each CTA stages A (128 rows) and half of B; one CTA per SM
+        const int half = P.bn / 2;
+        P.stg_cols = 32;
+        const size_t fixed = smem_for(half, 0, P.stg_cols);
+        P.stages = static_cast<int>(std::min<size_t>(MAX_STAGES, (227 * 1024 - fixed) / stage_bytes_for(half)));
+        const size_t smem = smem_for(half, P.stages, P.stg_cols);
+        const int64_t pairs = std::min<int64_t>(P.tiles, ctx->sm_count / 2);
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));
+        cfg.blockDim = dim3(THREADS);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (P.colstats)
+            NNCB_CUDA(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<true, false, 1, true>, ma, mb, mc, P));
+        else
+            NNCB_CUDA(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<false, false, 1, true>, ma, mb, mc, P));
+        NNCB_LAUNCHED(ctx);
+        return 0;
+    }
     const bool manual = P.xa != nullptr;
     const int tab_ints = manual ? 3 * std::max(P.cblocks * BK, BK) : 0;
     if (manual) {   // one CTA per SM (448 threads); take the deepest ring that fits
@@ -806,15 +966,15 @@ int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CU
     unsigned grid = static_cast<unsigned>(std::min<int64_t>(P.tiles, static_cast<int64_t>(ctx->sm_count) * per_sm));
     const unsigned threads = manual ? THREADS + 128 : THREADS;
     if (P.colstats && manual)
-        tc_gemm_kernel<true, true, 1><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
+        tc_gemm_kernel<true, true, 1, false><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
     else if (manual)
-        tc_gemm_kernel<false, true, 1><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
+        tc_gemm_kernel<false, true, 1, false><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
     else if (P.colstats && per_sm == 1)
-        tc_gemm_kernel<true, false, 1><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
+        tc_gemm_kernel<true, false, 1, false><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
     else if (P.colstats)
-        tc_gemm_kernel<true, false, 2><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
+        tc_gemm_kernel<true, false, 2, false><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
     else
-        tc_gemm_kernel<false, false, 2><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
+        tc_gemm_kernel<false, false, 2, false><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
     NNCB_LAUNCHED(ctx);
     return 0;
 }
@@ -961,6 +1121,7 @@ int gemm_tc_s2d(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const fl
 }
 
 std::atomic<int> g_manual_a{getenv("NNCB_TC_MANUAL_A") ? 1 : 0};
+std::atomic<int> g_forced_tile{0};   // nncb_gemm_force_tile: width | pair << 16 (0: autotune)
 
 int gemm_tc_route(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const float* bias,
                   float* out, bool* handled);
@@ -985,8 +1146,8 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
              (long long)d->kh, (long long)d->kw, (long long)d->sh, (long long)d->sw, (long long)d->oh,
              (long long)d->ow, (long long)d->pad_top, (long long)d->pad_left, (long long)d->batch,
              (long long)(d->in_f * 1000003 + d->out_f), d->epilogue, g_manual_a.load() ? 1 : 0);
-    int choice = 0;
-    {
+    int choice = g_forced_tile.load(std::memory_order_relaxed);
+    if (!choice) {
         std::lock_guard<std::mutex> lk(mu);
         auto it = tuned.find(key);
         if (it != tuned.end()) choice = it->second;
@@ -994,16 +1155,24 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(ctx->stream, &cap);
     if (!choice && enabled && N > 64 && cap == cudaStreamCaptureStatusNone) {
+        // bit 16: CTA pair (cta_group::2, 256-row tiles over two SMs)
+        static const bool pairs = !(getenv("NNCB_TC_PAIR") && atoi(getenv("NNCB_TC_PAIR")) == 0);
         std::vector<int> cands = N <= 128 ? std::vector<int>{64, 128} : std::vector<int>{128, 256};
+        if (pairs && !dense) {
+            cands.push_back(0x10000 | 128);
+            if (N > 128) cands.push_back(0x10000 | 256);
+        }
         cudaEvent_t e0, e1;
         NNCB_CUDA(cudaEventCreate(&e0));
         NNCB_CUDA(cudaEventCreate(&e1));
         float best = 0.f;
         for (int c : cands) {
-            g_force_bn = c;
+            g_force_bn = c & 0xffff;
+            g_force_pair = c >> 16;
             int rc = gemm_tc_route(ctx, d, a, b, bias, out, handled);   // warm-up (and validity)
             if (rc || !*handled) {
                 g_force_bn = 0;
+                g_force_pair = 0;
                 cudaEventDestroy(e0);
                 cudaEventDestroy(e1);
                 return rc;
@@ -1012,6 +1181,7 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
             for (int r = 0; r < 3 && !rc; ++r) rc = gemm_tc_route(ctx, d, a, b, bias, out, handled);
             cudaEventRecord(e1, ctx->stream);
             g_force_bn = 0;
+            g_force_pair = 0;
             if (rc) {
                 cudaEventDestroy(e0);
                 cudaEventDestroy(e1);
@@ -1030,9 +1200,11 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
         std::lock_guard<std::mutex> lk(mu);
         tuned[key] = choice;
     }
-    g_force_bn = choice;
+    g_force_bn = choice & 0xffff;
+    g_force_pair = choice >> 16;
     const int rc = gemm_tc_route(ctx, d, a, b, bias, out, handled);
     g_force_bn = 0;
+    g_force_pair = 0;
     return rc;
 }
 
@@ -1122,6 +1294,7 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
         const int64_t Nc = fwd ? co : ci;             // GEMM N
         const int64_t Ck = fwd ? ci : co;             // channels per tap (K block source)
         P.bn = pick_bn(Nc);
+        P.pair = (g_force_pair && !manual && P.bn >= 64) ? 1 : 0;
         P.N = Nc;
         P.ldc = Nc;
         P.cblocks = static_cast<int>((Ck + 31) / 32);
@@ -1188,7 +1361,7 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
             if (!encode_2d(&mb, b, co, kh * kw * ci, 32, BK, true)) return 1;
         } else {
             P.b_mn = 0;
-            if (!encode_2d(&mb, b, co, kh * kw * ci, BK, P.bn, false)) return 1;
+            if (!encode_2d(&mb, b, co, kh * kw * ci, BK, P.pair ? P.bn / 2 : P.bn, false)) return 1;
         }
         P.bias = (fwd && (d->epilogue & NNCB_EPI_BIAS)) ? bias : nullptr;
         P.out = out;
@@ -1196,7 +1369,8 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
         if (P.colstats) NNCB_CUDA(cudaMemsetAsync(P.colstats, 0, sizeof(double) * 2 * Nc, ctx->stream));
         P.n_tiles = (Nc + P.bn - 1) / P.bn;
         P.pix_tiles = tiles;
-        P.tiles = tiles * P.n_tiles * (fwd ? 1 : sh * sw);
+        P.pix_pairs = (tiles + 1) / 2;
+        P.tiles = (P.pair ? P.pix_pairs : tiles) * P.n_tiles * (fwd ? 1 : sh * sw);
         // TMA-store epilogue when output pixels are dense (fwd, or stride-1 dgrad)
         CUtensorMap mc;
         memset(&mc, 0, sizeof(mc));
@@ -1213,6 +1387,7 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
     P.N = co;
     P.ldc = co;
     P.bn = pick_bn(co);
+    P.pair = (g_force_pair && !manual && P.bn >= 64) ? 1 : 0;
     P.ci = (int)ci;
     P.kw_ = (int)kw;
     P.sh = (int)sh; P.sw = (int)sw; P.pt = (int)pt; P.pl = (int)pl;
@@ -1239,7 +1414,8 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
     }
     P.n_tiles = nt;
     P.m_tiles = mt;
-    P.tiles = mt * nt * P.splits;
+    P.m_pairs = (mt + 1) / 2;
+    P.tiles = (P.pair ? P.m_pairs : mt) * nt * P.splits;
     CUtensorMap mc;
     P.tma_store = 1;
     if (!encode_out_3d(&mc, P.splits > 1 ? P.partial : out, co, P.M, P.splits)) return 1;
@@ -1259,5 +1435,12 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
 // K block: 1 = builder-warp gather (manual A), 0 = im2col workspace.
 extern "C" int nncb_gemm_set_manual_a(int on) {
     nncb::g_manual_a.store(on ? 1 : 0);
+    return 0;
+}
+
+// Forces the tensor-core tile choice for subsequent GEMMs (tests / tuning):
+// code = N-tile width (64/128/256) | 1 << 16 for CTA pairs; 0 restores autotuning.
+extern "C" int nncb_gemm_force_tile(int code) {
+    nncb::g_forced_tile.store(code);
     return 0;
 }

@@ -26,6 +26,7 @@ for name, res, args in [
     ("nncb_gemm", _I, [_P, ctypes.POINTER(GemmDesc), _P, _P, _P, _P]),
     ("nncb_gemm_last_path", _I, []),
     ("nncb_gemm_set_manual_a", _I, [_I]),
+    ("nncb_gemm_force_tile", _I, [_I]),
 ]:
     fn = getattr(K, name)
     fn.restype, fn.argtypes = res, args

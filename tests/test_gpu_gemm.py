@@ -147,3 +147,30 @@ def test_manual_a_route(shape, kind):
     finally:
         K.nncb_gemm_set_manual_a(0)
     check(tc, ex)
+
+
+PAIR_CONVS = [c for c in CONVS if c[3] % 32 == 0 or c[5] == 1] + [(2, 30, 30, 64, 256, 3, 1), (3, 20, 20, 128, 64, 3, 2)]
+
+
+@pytest.mark.parametrize("shape", PAIR_CONVS)
+@pytest.mark.parametrize("tile", [0x10000 | 128, 0x10000 | 256])
+def test_cta_pair(shape, tile):
+    """CTA pairs (tcgen05 cta_group::2, 256-row tiles over two SMs, each CTA
+    staging half of B) for the three convolution contractions."""
+    n, ih, iw, ci, co, k, s = shape
+    g = conv_geom(n, ih, iw, ci, co, k, s)
+    rng = np.random.default_rng(7)
+    x = rng.uniform(-1, 1, (n, ih, iw, ci)).astype(np.float32)
+    w = rng.uniform(-1, 1, (k, k, ci, co)).astype(np.float32)
+    gy = rng.uniform(-1, 1, (n, g["oh"], g["ow"], co)).astype(np.float32)
+    K.nncb_gemm_force_tile(tile)
+    try:
+        tc, ex = run_both(CONV_FWD, g, Dev(x), Dev(w), None, (n, g["oh"], g["ow"], co), expect_tc=True)
+        check(tc, ex)
+        if (k == 1 or (ci % 32 == 0 and co % 32 == 0)) and s <= 2:
+            tc, ex = run_both(CONV_DGRAD, g, Dev(gy), Dev(w), None, (n, ih, iw, ci), expect_tc=True)
+            check(tc, ex)
+        tc, ex = run_both(CONV_WGRAD, g, Dev(x), Dev(gy), None, (k, k, ci, co), expect_tc=True)
+        check(tc, ex)
+    finally:
+        K.nncb_gemm_force_tile(0)

@@ -40,8 +40,12 @@ def main():
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--layers", default="")
     ap.add_argument("--colstats", action="store_true", help="forward GEMMs also accumulate BN column statistics")
+    ap.add_argument("--tile", default="auto", help="auto | 128 | 256 | p128 | p256 (p = CTA pair)")
     a = ap.parse_args()
     timer = P.DeviceTimer()
+    if a.tile != "auto":
+        code = int(a.tile.lstrip("p")) | (0x10000 if a.tile.startswith("p") else 0)
+        K.nncb_gemm_force_tile(code)
     total = {}
     for name, h, ci, co, k, s in LAYERS:
         if a.layers and not any(name.startswith(x) for x in a.layers.split(",")):
