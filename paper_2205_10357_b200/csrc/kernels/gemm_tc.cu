@@ -332,7 +332,11 @@ __device__ __forceinline__ void store_chunk_t(const uint32_t (&r)[32], uint8_t* 
             if (!rvalid) continue;
             const int c = col0 + p * COLS + ch * 4;
             if (full_cols) {
-                *reinterpret_cast<uint4*>(rdst + c) = v4;
+                // explicit global store: the row pointer arrives through a shuffle,
+                // so the compiler cannot prove its state space (generic ST.E otherwise)
+                asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(rdst + c), "r"(v4.x), "r"(v4.y),
+                             "r"(v4.z), "r"(v4.w)
+                             : "memory");
             } else {
                 const uint32_t e[4] = {v4.x, v4.y, v4.z, v4.w};
                 for (int q = 0; q < 4; ++q)
@@ -843,6 +847,7 @@ bool encode_2d(CUtensorMap* map, const float* base, int64_t inner, int64_t rows,
 
 thread_local int g_force_bn = 0;     // set by the autotuner (gemm_tc) for one call
 thread_local int g_force_pair = 0;   // 1: run the call as CTA pairs (cta_group::2)
+thread_local int g_force_wide = 0;   // 1: full-width (32-column) epilogue staging even at 2 CTAs/SM
 
 int pick_bn(int64_t n) {
     static const int env_bn = getenv("NNCB_TC_BN") ? atoi(getenv("NNCB_TC_BN")) : 0;   // tuning knob
@@ -954,6 +959,13 @@ int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CU
     }
     const bool manual = P.xa != nullptr;
     const int tab_ints = manual ? 3 * std::max(P.cblocks * BK, BK) : 0;
+    if (g_force_wide && shp.per_sm == 2 && !manual) {
+        // output-bound shapes: whole 128-byte row segments per store beat a deeper ring
+        P.stg_cols = 32;
+        const size_t fixed = smem_for(P.bn, 0, 32);
+        P.stages = static_cast<int>(std::min<size_t>(MAX_STAGES, (113 * 1024 - fixed) / stage_bytes_for(P.bn)));
+        if (P.stages < 2) { P.stages = shp.stages; P.stg_cols = shp.stg_cols; }
+    }
     if (manual) {   // one CTA per SM (448 threads); take the deepest ring that fits
         P.stg_cols = 32;
         const size_t fixed = smem_for(P.bn, 0, P.stg_cols, tab_ints);
@@ -1162,17 +1174,20 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
             cands.push_back(0x10000 | 128);
             if (N > 128) cands.push_back(0x10000 | 256);
         }
+        cands.push_back(0x20000 | 128);   // bit 17: 128-wide tiles with full-width staging
         cudaEvent_t e0, e1;
         NNCB_CUDA(cudaEventCreate(&e0));
         NNCB_CUDA(cudaEventCreate(&e1));
         float best = 0.f;
         for (int c : cands) {
             g_force_bn = c & 0xffff;
-            g_force_pair = c >> 16;
+            g_force_pair = (c >> 16) & 1;
+            g_force_wide = (c >> 17) & 1;
             int rc = gemm_tc_route(ctx, d, a, b, bias, out, handled);   // warm-up (and validity)
             if (rc || !*handled) {
                 g_force_bn = 0;
                 g_force_pair = 0;
+                g_force_wide = 0;
                 cudaEventDestroy(e0);
                 cudaEventDestroy(e1);
                 return rc;
@@ -1182,6 +1197,7 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
             cudaEventRecord(e1, ctx->stream);
             g_force_bn = 0;
             g_force_pair = 0;
+            g_force_wide = 0;
             if (rc) {
                 cudaEventDestroy(e0);
                 cudaEventDestroy(e1);
@@ -1201,10 +1217,12 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
         tuned[key] = choice;
     }
     g_force_bn = choice & 0xffff;
-    g_force_pair = choice >> 16;
+    g_force_pair = (choice >> 16) & 1;
+    g_force_wide = (choice >> 17) & 1;
     const int rc = gemm_tc_route(ctx, d, a, b, bias, out, handled);
     g_force_bn = 0;
     g_force_pair = 0;
+    g_force_wide = 0;
     return rc;
 }
 
