@@ -296,14 +296,15 @@ def main():
         unit = "samples/s"
     elif cfg["kind"] == "infer":
         model.run(inputs)
-        step = lambda: model.infer_device()  # noqa: E731
+        step = lambda: model.run_device("inference")  # noqa: E731
         units = batch * world
         metric, unit = "inference samples/sec", "samples/s"
-    else:  # chain: train-mode BN forward
+    else:  # chain: train-mode BN forward, reported as algorithmic HBM GB/s (SURVEY.md §8(d) C2 mode B)
         model.run(inputs, role="train_fwd")
-        step = lambda: model.infer_device()  # noqa: E731
-        units = batch * world
-        metric, unit = "fused-group samples/sec", "samples/s"
+        step = lambda: model.run_device("train_fwd")  # noqa: E731
+        elems = int(np.prod(inputs["x"].shape))
+        units = 40.0 * elems * world / 1e9   # GB per pass: 4 stats barriers with recompute (40 B/element)
+        metric, unit = "fused-group HBM GB/s (C2 chain, train-mode BN)", "GB/s"
 
     clocks.start()   # sampler warms up during the warm-up steps
     for _ in range(args.warmup):
@@ -326,6 +327,21 @@ def main():
 
     # ---- end to end through the public API (host buffers every step) ----
     e2e = None
+    if cfg["kind"] in ("infer", "chain"):
+        role = "inference" if cfg["kind"] == "infer" else "train_fwd"
+        h2d = sum(v.nbytes for v in inputs.values())
+        final = [v["name"] for v in model.describe[role]["values"] if v["category"] == "output"]
+        out = model.run(inputs, role=role, outputs=final)   # untimed warm-up; only the graph outputs come back
+        d2h = sum(v.nbytes for v in out.values())
+        timer.sync()
+        barrier()
+        t0 = time.perf_counter()
+        n_e2e = max(2, args.steps // 2)
+        for _ in range(n_e2e):
+            model.run(inputs, role=role, outputs=final)
+        e_ms = max_over_ranks((time.perf_counter() - t0) * 1000 / n_e2e)
+        e2e = {"value": units / (e_ms / 1000.0), "unit": unit, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": e_ms}
     if cfg["kind"] == "train":
         h2d = sum(v.nbytes for v in inputs.values()) + target.nbytes
         model.train_step(inputs, target, lr)   # untimed warm-up of the public path

@@ -42,6 +42,8 @@ int nnc_model_set_input(nnc_model* m, const char* name, const float* data, const
 
 /* role: 0 = inference plan, 1 = train_fwd plan (outputs include the SaveSet). */
 int nnc_model_run(nnc_model* m, int role);
+/* nnc_model_run copying back only the comma-separated outputs `names` (ExecOptions::materialize). */
+int nnc_model_run_outputs(nnc_model* m, int role, const char* names);
 int nnc_model_output(nnc_model* m, const char* name, float* out, int64_t n);
 
 int nnc_model_train_step(nnc_model* m, const float* target, int64_t n, double lr, double* loss);
@@ -58,6 +60,9 @@ uint64_t nnc_model_launches_per_step(nnc_model* m);
 const char* nnc_model_profile_step(nnc_model* m, double lr);
 uint64_t nnc_model_arena_bytes(nnc_model* m);
 int      nnc_model_infer_device(nnc_model* m);         /* replay inference, no host copies */
+/* Replays plan `role` (0 inference, 1 train_fwd) with the inputs already on the device
+   (from the last nnc_model_run of that role): no host<->device copies. */
+int      nnc_model_run_device(nnc_model* m, int role);
 
 /* NVRTC-compiles every generated fused-group kernel of the model's three plans
  * for sm_100a (no device needed). */

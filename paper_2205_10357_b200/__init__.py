@@ -19,7 +19,7 @@ from __future__ import annotations
 import ctypes
 import json
 import os
-from typing import Dict, Optional
+from typing import Dict, Optional, Sequence
 
 import numpy as np
 
@@ -75,6 +75,8 @@ def _load():
         "nnc_model_profile_step": (S, [P, D]),
         "nnc_model_arena_bytes": (U64, [P]),
         "nnc_model_infer_device": (I, [P]),
+        "nnc_model_run_device": (I, [P, I]),
+        "nnc_model_run_outputs": (I, [P, I, ctypes.c_char_p]),
         "nnc_device_ctx": (P, []),
         "nnc_model_check_kernels": (I, [P]),
         "nnc_comm_unique_id": (I, [ctypes.c_char_p]),
@@ -162,15 +164,23 @@ class CompiledModel:
                 return v
         raise KeyError(name)
 
-    def run(self, inputs: Dict[str, np.ndarray], role: str = "inference") -> Dict[str, np.ndarray]:
-        """runtime::execute on the inference (or train_fwd) plan; returns every output."""
+    def run(self, inputs: Dict[str, np.ndarray], role: str = "inference",
+            outputs: Optional[Sequence[str]] = None) -> Dict[str, np.ndarray]:
+        """runtime::execute on the inference (or train_fwd) plan; returns every output,
+        or only `outputs` (the others stay on the device)."""
         for k, v in inputs.items():
             self.feed(k, v)
-        _check(_host.nnc_model_run(self._h, 1 if role == "train_fwd" else 0))
+        r = 1 if role == "train_fwd" else 0
+        if outputs is None:
+            _check(_host.nnc_model_run(self._h, r))
+        else:
+            _check(_host.nnc_model_run_outputs(self._h, r, ",".join(outputs).encode()))
         out = {}
         plan = self.describe[role]
         out_names = [plan["values"][i]["name"] for i in range(len(plan["values"]))
                      if plan["values"][i]["category"] in ("output", "saved") and plan["values"][i]["resident"]]
+        if outputs is not None:
+            out_names = [n for n in out_names if n in set(outputs)]
         for name in out_names:
             v = self._plan_value(role, name)
             if v["storage"] != "buffer":
@@ -235,6 +245,10 @@ class CompiledModel:
 
     def infer_device(self):
         _check(_host.nnc_model_infer_device(self._h))
+
+    def run_device(self, role: str = "inference"):
+        """Replay `role` with inputs already resident (from the last run() of that role)."""
+        _check(_host.nnc_model_run_device(self._h, 1 if role == "train_fwd" else 0))
 
 
 class DeviceTimer:

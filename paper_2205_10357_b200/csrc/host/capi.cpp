@@ -194,6 +194,27 @@ int nnc_model_run(nnc_model* m, int role) {
     });
 }
 
+int nnc_model_run_outputs(nnc_model* m, int role, const char* names) {
+    return guarded([&] {
+        // ExecOptions::materialize: only the named outputs are copied back
+        std::set<std::string> want;
+        std::string cur;
+        for (const char* c = names; c && *c; ++c) {
+            if (*c == ',') {
+                if (!cur.empty()) want.insert(cur);
+                cur.clear();
+            } else {
+                cur += *c;
+            }
+        }
+        if (!cur.empty()) want.insert(cur);
+        runtime::ExecOptions o = m->opts;
+        o.materialize = &want;
+        const plan::ExecutionPlan& p = role == 1 ? m->plans.train_fwd : m->plans.inference;
+        m->outputs = runtime::execute(p, m->inputs, *m->host, nullptr, o);
+    });
+}
+
 int nnc_model_output(nnc_model* m, const char* name, float* out, int64_t n) {
     return guarded([&] {
         auto it = m->outputs.find(name);
@@ -259,14 +280,17 @@ const char* nnc_model_profile_step(nnc_model* m, double lr) {
 uint64_t nnc_model_launches_per_step(nnc_model* m) { return m->trainer ? m->trainer->launches_per_step() : 0; }
 uint64_t nnc_model_arena_bytes(nnc_model* m) { return m->trainer ? m->trainer->arena_bytes() : 0; }
 
-int nnc_model_infer_device(nnc_model* m) {
+int nnc_model_run_device(nnc_model* m, int role) {
     return guarded([&] {
         std::set<std::string> none;
         runtime::ExecOptions o = m->opts;
         o.materialize = &none;
-        runtime::execute(m->plans.inference, m->inputs, *m->host, nullptr, o);
+        o.inputs_resident = true;
+        runtime::execute(role == 1 ? m->plans.train_fwd : m->plans.inference, m->inputs, *m->host, nullptr, o);
     });
 }
+
+int nnc_model_infer_device(nnc_model* m) { return nnc_model_run_device(m, 0); }
 
 int nnc_model_check_kernels(nnc_model* m) {
     return guarded([&] {

@@ -62,6 +62,9 @@ struct ExecOptions {
     const std::set<std::string>* materialize = nullptr;
     bool use_graphs = true;           // capture each bound program into a CUDA graph
     int gemm_precision = NNCB_PREC_TF32;
+    // inputs already on the device from a previous execute of this plan:
+    // skip the host->device input copies (device-resident replay)
+    bool inputs_resident = false;
 };
 
 struct L1Result {
