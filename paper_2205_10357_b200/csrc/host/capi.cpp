@@ -181,7 +181,7 @@ int nnc_model_set_input(nnc_model* m, const char* name, const float* data, const
         std::vector<int64_t> d(dims, dims + rank);
         auto it = m->inputs.find(name);
         if (it == m->inputs.end() || it->second.dims() != d) {
-            it = m->inputs.insert_or_assign(name, Tensor(DType::F32, d)).first;
+            it = m->inputs.insert_or_assign(name, Tensor::uninitialized(DType::F32, d)).first;
         }
         nncb_host_copy(it->second.data(), data, it->second.byte_size());
     });
@@ -220,7 +220,7 @@ int nnc_model_output(nnc_model* m, const char* name, float* out, int64_t n) {
         auto it = m->outputs.find(name);
         if (it == m->outputs.end()) throw Error(Error::Code::ShapeMismatch, std::string("no output ") + name);
         if (it->second.elements() != n) throw Error(Error::Code::ShapeMismatch, "output size mismatch");
-        std::memcpy(out, it->second.data(), it->second.byte_size());
+        nncb_host_copy(out, it->second.data(), it->second.byte_size());
     });
 }
 

@@ -28,6 +28,14 @@ Tensor::Tensor(DType dt, std::vector<int64_t> dims) : dtype_(dt), dims_(std::mov
     data_.assign(static_cast<size_t>(element_count(dims_)) * dtype_size(dt), 0);
 }
 
+Tensor Tensor::uninitialized(DType dt, std::vector<int64_t> dims) {
+    Tensor t;
+    t.dtype_ = dt;
+    t.dims_ = std::move(dims);
+    t.data_.resize(static_cast<size_t>(element_count(t.dims_)) * dtype_size(dt));
+    return t;
+}
+
 Tensor Tensor::from_f32(std::vector<int64_t> dims, std::vector<float> values) {
     Tensor t(DType::F32, std::move(dims));
     std::memcpy(t.data(), values.data(), t.byte_size());

@@ -761,7 +761,7 @@ std::map<std::string, Tensor> execute(const ExecutionPlan& p, const std::map<std
     for (uint32_t s : p.output_slots) {
         const auto& v = p.values[s];
         if (opts.materialize && !opts.materialize->count(v.name)) continue;
-        Tensor t(p.dtype, v.dims);
+        Tensor t = Tensor::uninitialized(p.dtype, v.dims);   // the download overwrites every byte
         NNC_CHECK(nncb_d2h(ctx, t.data(), prog.ptr(v.name), t.byte_size()));
         dev.stats().d2h_bytes += t.byte_size();
         out.emplace(v.name, std::move(t));

@@ -4,10 +4,28 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <memory>
+#include <utility>
 #include <string>
 #include <vector>
 
 namespace nnc {
+
+// Byte storage whose resize() leaves new bytes uninitialised (value-init is
+// skipped), so buffers that are about to be overwritten by a copy are not
+// zero-filled first; assign(n, 0) still zero-fills explicitly.
+template <typename T>
+struct DefaultInitAllocator : std::allocator<T> {
+    template <typename U>
+    struct rebind { using other = DefaultInitAllocator<U>; };
+    DefaultInitAllocator() = default;
+    template <typename U>
+    DefaultInitAllocator(const DefaultInitAllocator<U>&) noexcept {}
+    template <typename U>
+    void construct(U* p) noexcept { ::new (static_cast<void*>(p)) U; }
+    template <typename U, typename... Args>
+    void construct(U* p, Args&&... args) { ::new (static_cast<void*>(p)) U(std::forward<Args>(args)...); }
+};
 
 enum class DType : uint8_t { F32 = 0, F64 = 1 };
 inline size_t dtype_size(DType dt) { return dt == DType::F32 ? 4 : 8; }
@@ -18,8 +36,10 @@ std::string dims_to_string(const std::vector<int64_t>& dims);
 class Tensor {
 public:
     Tensor() = default;
-    Tensor(DType dt, std::vector<int64_t> dims);
+    Tensor(DType dt, std::vector<int64_t> dims);   // zero-filled (as the reference's)
     static Tensor from_f32(std::vector<int64_t> dims, std::vector<float> values);
+    // storage left uninitialised: only for tensors fully overwritten right away
+    static Tensor uninitialized(DType dt, std::vector<int64_t> dims);
 
     DType dtype() const { return dtype_; }
     const std::vector<int64_t>& dims() const { return dims_; }
@@ -36,7 +56,7 @@ public:
 private:
     DType dtype_ = DType::F32;
     std::vector<int64_t> dims_;
-    std::vector<uint8_t> data_;
+    std::vector<uint8_t, DefaultInitAllocator<uint8_t>> data_;
 };
 
 }  // namespace nnc

@@ -193,6 +193,43 @@ int nncb_h2d(nncb_ctx* c, void* dst, const void* src, size_t bytes) {
     return 0;
 }
 
+// Large downloads into pageable memory: DMA chunk i+1 (and i+2) into the pinned
+// ring while the copy threads move chunk i out; returns once dst is filled.
+int nncb_d2h(nncb_ctx* c, void* dst, const void* src, size_t bytes) {
+    if (!bytes) return 0;
+    cudaPointerAttributes attr{};
+    const bool pinned = cudaPointerGetAttributes(&attr, dst) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(c->stream, &cap);
+    Staging* s = (bytes >= kStagedMin && !pinned && cap == cudaStreamCaptureStatusNone) ? nncb::staging_for(c) : nullptr;
+    if (!s || !s->ok) {
+        NNCB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+        return 0;
+    }
+    const size_t nchunks = (bytes + kChunk - 1) / kChunk;
+    auto issue = [&](size_t i) -> int {
+        const size_t off = i * kChunk, n = std::min(kChunk, bytes - off);
+        const int slot = static_cast<int>(i % kRing);
+        NNCB_CUDA(cudaEventSynchronize(s->ev[slot]));   // the slot's previous user is done
+        NNCB_CUDA(cudaMemcpyAsync(s->pin[slot], static_cast<const char*>(src) + off, n, cudaMemcpyDeviceToHost,
+                                  c->stream));
+        NNCB_CUDA(cudaEventRecord(s->ev[slot], c->stream));
+        return 0;
+    };
+    for (size_t i = 0; i < std::min<size_t>(kRing, nchunks); ++i)
+        if (int rc = issue(i)) return rc;
+    for (size_t i = 0; i < nchunks; ++i) {
+        const size_t off = i * kChunk, n = std::min(kChunk, bytes - off);
+        const int slot = static_cast<int>(i % kRing);
+        NNCB_CUDA(cudaEventSynchronize(s->ev[slot]));
+        parallel_copy(static_cast<char*>(dst) + off, s->pin[slot], n);
+        if (i + kRing < nchunks)
+            if (int rc = issue(i + kRing)) return rc;
+    }
+    return 0;
+}
+
 int nncb_host_copy(void* dst, const void* src, size_t bytes) {
     if (bytes) parallel_copy(dst, src, bytes);
     return 0;

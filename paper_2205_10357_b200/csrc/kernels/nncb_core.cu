@@ -127,11 +127,6 @@ int nncb_memset(nncb_ctx* c, void* dst, int v, size_t bytes) {
     return 0;
 }
 
-int nncb_d2h(nncb_ctx* c, void* dst, const void* src, size_t bytes) {
-    if (bytes) NNCB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
-    return 0;
-}
-
 int nncb_d2d(nncb_ctx* c, void* dst, const void* src, size_t bytes) {
     if (bytes) NNCB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c->stream));
     return 0;
