@@ -89,6 +89,8 @@ struct TcParams {
     int K_;             // kh*kw*ci
     // --- CTA pair (cta_group::2): 256-row tiles over two SMs ----------------
     int pair;           // 1: cluster of 2, leader issues M=256 MMAs, each CTA loads half of B
+    int tma_out;        // epilogue stores through TMA: 1 = 4-D pixel grid (stride-1 outputs), 2 = 3-D [splits][M][N]
+    int ob_w, ob_h, ob_n;   // tma_out 1: a warp's 32-row sub-box of the pixel tile
     int64_t pix_pairs;  // MODE_CONV: pixel-box pairs per phase
     int64_t m_pairs;    // MODE_WGRAD: M-tile pairs
 };
@@ -279,18 +281,38 @@ __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: 
 // rows [(l / COLS) * RPL, +RPL), the 32/COLS row groups are folded with xor
 // shuffles, and the pass's sums move to lane (pass * COLS + column), so on
 // return lane l holds (sum, sum of squares) of chunk column l in cs1 / cs2.
+// 16-byte chunk position of chunk j in staged row rr: TMA's SWIZZLE_128B / 64B /
+// 32B patterns for 128 / 64 / 32-byte rows (address bits [4:6] ^= [7:9] on a
+// 1 KB-aligned tile), so a staged chunk can leave through a TMA store as is.
+template <int CH>
+__device__ __forceinline__ int swz(int j, int rr) {
+    return CH == 8 ? (j ^ (rr & 7)) : CH == 4 ? (j ^ ((rr >> 1) & 3)) : (j ^ ((rr >> 2) & 1));
+}
+
+// TMA epilogue: the staged COLS-wide pass leaves as one tensor store of the
+// warp's 32-row sub-box (mode 1: 4-D pixel grid, mode 2: 3-D [split][row][col]).
+struct TmaOut {
+    const CUtensorMap* map;
+    int mode;           // 0: direct stores
+    int c1, c2, c3;     // non-column box coordinates
+};
+
 template <int CH, bool CS>
 __device__ __forceinline__ void store_chunk_t(const uint32_t (&r)[32], uint8_t* tile, float* dst, bool valid,
                                               int col0, int N, bool full_cols, int lane, bool store, float& cs1,
-                                              float& cs2) {
+                                              float& cs2, const TmaOut& to) {
     constexpr int COLS = CH * 4, RPI = 32 / CH;   // columns per pass, rows per store instruction
     const uint32_t vmask = CS ? __ballot_sync(0xffffffffu, valid) : 0u;
 #pragma unroll
     for (int p = 0; p < 32 / COLS; ++p) {
+        if (to.mode) {   // the previous TMA store out of this tile has finished reading it
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
+        }
         uint8_t* rowp = tile + lane * (CH * 16);
 #pragma unroll
         for (int j = 0; j < CH; ++j)
-            *reinterpret_cast<uint4*>(rowp + ((j ^ (lane % CH)) << 4)) =
+            *reinterpret_cast<uint4*>(rowp + (swz<CH>(j, lane) << 4)) =
                 make_uint4(r[p * COLS + 4 * j], r[p * COLS + 4 * j + 1], r[p * COLS + 4 * j + 2], r[p * COLS + 4 * j + 3]);
         __syncwarp();
         if (CS) {
@@ -300,7 +322,7 @@ __device__ __forceinline__ void store_chunk_t(const uint32_t (&r)[32], uint8_t* 
 #pragma unroll
             for (int i = 0; i < RPL; ++i) {
                 const int rr = r0 + i;
-                const float v = *reinterpret_cast<const float*>(tile + rr * (CH * 16) + (((col >> 2) ^ (rr % CH)) << 4) +
+                const float v = *reinterpret_cast<const float*>(tile + rr * (CH * 16) + (swz<CH>(col >> 2, rr) << 4) +
                                                                 (col & 3) * 4);
                 const float m = ((vmask >> rr) & 1u) ? v : 0.f;
                 s1 += m;
@@ -323,12 +345,24 @@ __device__ __forceinline__ void store_chunk_t(const uint32_t (&r)[32], uint8_t* 
             __syncwarp();
             continue;
         }
+        if (to.mode) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // staged writes -> TMA (async proxy)
+            __syncwarp();
+            if (lane == 0) {
+                if (to.mode == 1)
+                    tma_store_4d(to.map, tile, col0 + p * COLS, to.c1, to.c2, to.c3);
+                else
+                    tma_store_3d(to.map, tile, col0 + p * COLS, to.c1, to.c2);
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            continue;
+        }
 #pragma unroll
         for (int i = 0; i < CH; ++i) {
             const int rr = i * RPI + lane / CH, ch = lane % CH;
             float* rdst = reinterpret_cast<float*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(dst), rr));
             const int rvalid = __shfl_sync(0xffffffffu, valid ? 1 : 0, rr);
-            const uint4 v4 = *reinterpret_cast<const uint4*>(tile + rr * (CH * 16) + ((ch ^ (rr % CH)) << 4));
+            const uint4 v4 = *reinterpret_cast<const uint4*>(tile + rr * (CH * 16) + (swz<CH>(ch, rr) << 4));
             if (!rvalid) continue;
             const int c = col0 + p * COLS + ch * 4;
             if (full_cols) {
@@ -712,6 +746,16 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                 dst = base + m * P.ldc;
             }
             const int nchunks = P.bn / 32;
+            TmaOut to{&map_c, P.tma_out, 0, 0, 0};
+            if (P.tma_out == 1) {   // the warp's quarter of the pixel tile as a sub-box origin
+                const int q0 = quarter * 32;
+                to.c1 = T.tw0 + q0 % P.TW;
+                to.c2 = T.th0 + (q0 / P.TW) % P.TH;
+                to.c3 = T.tn0 + q0 / (P.TW * P.TH);
+            } else if (P.tma_out == 2) {
+                to.c1 = static_cast<int>(T.m0) + quarter * 32;
+                to.c2 = P.splits > 1 ? T.split : 0;
+            }
             const uint32_t tbase =
                 tmem_base + acc * static_cast<uint32_t>(P.bn) + (static_cast<uint32_t>(quarter * 32) << 16);
             uint32_t r[32];
@@ -750,11 +794,11 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                     const bool st = !P.nostore;
                     float c1 = 0.f, c2 = 0.f;
                     if (P.stg_cols == 32)
-                        store_chunk_t<8, CS>(r, tile, dst, valid, col0, P.N, full_cols, lane, st, c1, c2);
+                        store_chunk_t<8, CS>(r, tile, dst, valid, col0, P.N, full_cols, lane, st, c1, c2, to);
                     else if (P.stg_cols == 16)
-                        store_chunk_t<4, CS>(r, tile, dst, valid, col0, P.N, full_cols, lane, st, c1, c2);
+                        store_chunk_t<4, CS>(r, tile, dst, valid, col0, P.N, full_cols, lane, st, c1, c2, to);
                     else
-                        store_chunk_t<2, CS>(r, tile, dst, valid, col0, P.N, full_cols, lane, st, c1, c2);
+                        store_chunk_t<2, CS>(r, tile, dst, valid, col0, P.N, full_cols, lane, st, c1, c2, to);
                     if (CS) {
                         cs_sum[k] += static_cast<double>(c1);
                         cs_sq[k] += static_cast<double>(c2);
@@ -786,6 +830,8 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                 }
             }
         }
+        if (P.tma_out && lane == 0)   // every TMA store issued by this warp has completed
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     if (PAIR)
@@ -906,7 +952,50 @@ TcShape pick_shape(int bn) {
     return best;
 }
 
-int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, TcParams& P) {
+// Output tensor map for the TMA epilogue, encoded once the staging width
+// (COLS = stg_cols) is known. Returns false (direct stores) when not applicable.
+bool encode_tma_out(CUtensorMap* mc, TcParams& P) {
+    static const bool enabled = !(getenv("NNCB_TC_TMA_OUT") && atoi(getenv("NNCB_TC_TMA_OUT")) == 0);
+    P.tma_out = 0;
+    if (!enabled || P.N % 4 != 0 || P.ldc != P.N) return false;
+    const int cols = P.stg_cols;
+    const CUtensorMapSwizzle sw = cols == 32 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : cols == 16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+    CUresult r;
+    if (P.mode == MODE_CONV) {
+        if (P.out_s != 1) return false;   // strided-dgrad phases interleave pixels: direct stores
+        P.ob_w = P.TW >= 32 ? 32 : P.TW;
+        P.ob_h = P.TW >= 32 ? 1 : std::min(P.TH, 32 / P.TW);
+        P.ob_n = 32 / (P.ob_w * P.ob_h);
+        if (P.ob_n > P.TN && P.ob_n > 1) return false;
+        cuuint64_t dims[4] = {(cuuint64_t)P.N, (cuuint64_t)P.out_w, (cuuint64_t)P.out_h, (cuuint64_t)P.gn};
+        cuuint64_t strides[3] = {(cuuint64_t)(P.N * 4), (cuuint64_t)(P.N * P.out_w * 4),
+                                 (cuuint64_t)(P.N * P.out_w * P.out_h * 4)};
+        cuuint32_t box[4] = {(cuuint32_t)cols, (cuuint32_t)P.ob_w, (cuuint32_t)P.ob_h, (cuuint32_t)P.ob_n};
+        cuuint32_t es[4] = {1, 1, 1, 1};
+        r = nncb::drv::table().tensorMapEncodeTiled(mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, P.out, dims, strides, box, es,
+                                              CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return false;
+        P.tma_out = 1;
+        return true;
+    }
+    float* base = P.splits > 1 ? P.partial : P.out;
+    cuuint64_t dims[3] = {(cuuint64_t)P.N, (cuuint64_t)P.M, (cuuint64_t)std::max(P.splits, 1)};
+    cuuint64_t strides[2] = {(cuuint64_t)(P.N * 4), (cuuint64_t)(P.N * P.M * 4)};
+    cuuint32_t box[3] = {(cuuint32_t)cols, 32, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    r = nncb::drv::table().tensorMapEncodeTiled(mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, es,
+                                          CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+    P.tma_out = 2;
+    return true;
+}
+
+int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc_unused, TcParams& P) {
+    CUtensorMap mc;
+    memset(&mc, 0, sizeof(mc));
     static bool attr_done = false;
     if (!attr_done) {
         NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<false, false, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -937,6 +1026,7 @@ int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CU
         const size_t fixed = smem_for(half, 0, P.stg_cols);
         P.stages = static_cast<int>(std::min<size_t>(MAX_STAGES, (227 * 1024 - fixed) / stage_bytes_for(half)));
         const size_t smem = smem_for(half, P.stages, P.stg_cols);
+        encode_tma_out(&mc, P);
         const int64_t pairs = std::min<int64_t>(P.tiles, ctx->sm_count / 2);
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));
@@ -972,6 +1062,7 @@ int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CU
         P.stages = static_cast<int>(std::min<size_t>(MAX_STAGES, (227 * 1024 - fixed) / stage_bytes_for(P.bn)));
     }
     const size_t smem = smem_for(P.bn, P.stages, P.stg_cols, tab_ints);
+    encode_tma_out(&mc, P);
     int per_sm = (env_stages > 0) ? ((P.bn <= 128 && smem <= 113 * 1024) ? 2 : 1) : shp.per_sm;
     if (env_persm > 0 && (env_persm == 1 || 2 * smem <= 228 * 1024)) per_sm = env_persm;
     if (manual) per_sm = 1;   // the 448-thread build is compiled for one CTA per SM
