@@ -64,6 +64,7 @@ struct TcParams {
     // --- MODE_WGRAD ---------------------------------------------------------
     int64_t M;          // rows of C = taps * ci
     int ci, kw_;        // for (tap, c) = divmod(m, ci); tap -> (dh, dw)
+    int dil_w;          // horizontal tap dilation (space-to-depth packing); 1 otherwise
     int sh, sw, pt, pl;
     int kboxes;         // pixel boxes (TN*TH*TW == 32 pixels each)
     int splits;
@@ -575,7 +576,7 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                     if (m >= P.M) m = T.m0;
                     const int tap = static_cast<int>(m / P.ci);
                     ac[q] = static_cast<int>(m % P.ci);
-                    ax[q] = tap % P.kw_ - P.pl;
+                    ax[q] = (tap % P.kw_) * P.dil_w - P.pl;
                     ay[q] = tap / P.kw_ - P.pt;
                 }
                 int r = T.kb_begin;
@@ -894,6 +895,7 @@ bool encode_2d(CUtensorMap* map, const float* base, int64_t inner, int64_t rows,
 thread_local int g_force_bn = 0;     // set by the autotuner (gemm_tc) for one call
 thread_local int g_force_pair = 0;   // 1: run the call as CTA pairs (cta_group::2)
 thread_local int g_force_wide = 0;   // 1: full-width (32-column) epilogue staging even at 2 CTAs/SM
+thread_local int g_dil_w = 1;        // horizontal tap dilation for the next implicit GEMM (internal)
 
 int pick_bn(int64_t n) {
     static const int env_bn = getenv("NNCB_TC_BN") ? atoi(getenv("NNCB_TC_BN")) : 0;   // tuning knob
@@ -1139,9 +1141,20 @@ __global__ void __launch_bounds__(256) im2col_k(const float* __restrict__ x, flo
 // y = conv_{k x k, stride 2}(x) equals a stride-1 VALID conv of the 2x2-blocked
 // input x'[n, Y, X, (by*2+bx)*ci + c] = x[n, 2Y+by-pt, 2X+bx-pl, c] (zero outside)
 // with weights W'[a, b, (by,bx,c), co] = W[2a+by, 2b+bx, c, co] (zero past k).
-// Channels are zero-padded to 32 so the TMA implicit-GEMM path applies.
+// When 4*ci <= 16 two horizontally adjacent blocks share one 32-channel group
+// ("pack"): x''[Y, X] = [x'[Y, X] | x'[Y, X+1]] (16 channels each), and the
+// kw' = ceil(k/2) horizontal taps pair up into ceil(kw'/2) taps two apart
+// (dilation 2), halving K. Channels are zero-padded to 32 for the TMA path.
+__device__ __forceinline__ void s2d_chan(int cc, int ci, bool pack, int& half, int& blk, int& c, bool& real) {
+    half = pack ? cc / 16 : 0;
+    const int cl = pack ? cc % 16 : cc;
+    real = cl < 4 * ci;
+    blk = real ? cl / ci : 0;
+    c = real ? cl % ci : 0;
+}
+
 __global__ void s2d_input_k(const float* __restrict__ x, float* __restrict__ xs, int n, int ih, int iw, int ci,
-                            int H2, int W2, int pt, int pl) {
+                            int H2, int W2, int pt, int pl, int pack) {
     const int64_t total = static_cast<int64_t>(n) * H2 * W2 * 8;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         const int q = static_cast<int>(t & 7);
@@ -1152,11 +1165,12 @@ __global__ void s2d_input_k(const float* __restrict__ x, float* __restrict__ xs,
         float v[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const int cc = q * 4 + j;
+            int half, blk, c;
+            bool real;
+            s2d_chan(q * 4 + j, ci, pack != 0, half, blk, c, real);
             v[j] = 0.f;
-            if (cc < 4 * ci) {
-                const int blk = cc / ci, c = cc % ci;
-                const int iy = 2 * Y + (blk >> 1) - pt, ix = 2 * X + (blk & 1) - pl;
+            if (real) {
+                const int iy = 2 * Y + (blk >> 1) - pt, ix = 2 * (X + half) + (blk & 1) - pl;
                 if (iy >= 0 && iy < ih && ix >= 0 && ix < iw) v[j] = __ldg(x + ((nn * ih + iy) * iw + ix) * ci + c);
             }
         }
@@ -1164,61 +1178,70 @@ __global__ void s2d_input_k(const float* __restrict__ x, float* __restrict__ xs,
     }
 }
 
+// W''[a, b2, cc, co]: tap (a, b2) of the lowered conv, cc its 32-channel index
 __global__ void s2d_weight_k(const float* __restrict__ w, float* __restrict__ ws, int kh, int kw, int ci, int co,
-                             int kh2, int kw2) {
-    const int total = kh2 * kw2 * 32 * co;
+                             int kh2, int kwt, int pack) {
+    const int total = kh2 * kwt * 32 * co;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-        const int o = t % co, cc = (t / co) % 32, b = (t / (co * 32)) % kw2, a = t / (co * 32 * kw2);
-        float v = 0.f;
-        if (cc < 4 * ci) {
-            const int blk = cc / ci, c = cc % ci;
-            const int dh = 2 * a + (blk >> 1), dw = 2 * b + (blk & 1);
-            if (dh < kh && dw < kw) v = w[((dh * kw + dw) * ci + c) * co + o];
-        }
-        ws[t] = v;
+        const int o = t % co, cc = (t / co) % 32, b2 = (t / (co * 32)) % kwt, a = t / (co * 32 * kwt);
+        int half, blk, c;
+        bool real;
+        s2d_chan(cc, ci, pack != 0, half, blk, c, real);
+        const int b = pack ? 2 * b2 + half : b2;
+        const int dh = 2 * a + (blk >> 1), dw = 2 * b + (blk & 1);
+        ws[t] = (real && dh < kh && dw < kw) ? w[((dh * kw + dw) * ci + c) * co + o] : 0.f;
     }
 }
 
 __global__ void s2d_wgrad_back_k(const float* __restrict__ dws, float* __restrict__ dw, int kh, int kw, int ci, int co,
-                                 int kw2) {
+                                 int kwt, int pack) {
     const int total = kh * kw * ci * co;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
         const int o = t % co, c = (t / co) % ci, x = (t / (co * ci)) % kw, y = t / (co * ci * kw);
-        const int cc = ((y & 1) * 2 + (x & 1)) * ci + c;
-        dw[t] = dws[(((y >> 1) * kw2 + (x >> 1)) * 32 + cc) * co + o];
+        const int blk = (y & 1) * 2 + (x & 1), b = x >> 1;
+        const int b2 = pack ? b >> 1 : b, half = pack ? b & 1 : 0;
+        const int cc = half * 16 + blk * ci + c;
+        dw[t] = dws[(((y >> 1) * kwt + b2) * 32 + cc) * co + o];
     }
 }
 
 int gemm_tc_s2d(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const float* bias, float* out,
                 bool* handled) {
+    static const bool allow_pack = !(getenv("NNCB_TC_S2D_PACK") && atoi(getenv("NNCB_TC_S2D_PACK")) == 0);
+    const int pack = (allow_pack && 4 * d->ci <= 16) ? 1 : 0;
     const int kh2 = static_cast<int>((d->kh + 1) / 2), kw2 = static_cast<int>((d->kw + 1) / 2);
+    const int kwt = pack ? (kw2 + 1) / 2 : kw2;   // horizontal taps of the lowered conv
     const int H2 = static_cast<int>(d->oh) + kh2 - 1, W2 = static_cast<int>(d->ow) + kw2 - 1;
     const size_t xs_bytes = sizeof(float) * static_cast<size_t>(d->n) * H2 * W2 * 32;
-    const size_t w_bytes = sizeof(float) * static_cast<size_t>(kh2) * kw2 * 32 * d->co;
+    const size_t w_bytes = sizeof(float) * static_cast<size_t>(kh2) * kwt * 32 * d->co;
     const size_t w_off = (xs_bytes + 255) / 256 * 256;
     char* ws = static_cast<char*>(workspace(ctx, w_off + w_bytes));
     if (!ws) return fail("space-to-depth: workspace allocation failed");
     float* xs = reinterpret_cast<float*>(ws);
     float* wsp = reinterpret_cast<float*>(ws + w_off);
     s2d_input_k<<<grid_for(ctx, static_cast<int64_t>(d->n) * H2 * W2 * 8, 256), 256, 0, ctx->stream>>>(
-        a, xs, (int)d->n, (int)d->ih, (int)d->iw, (int)d->ci, H2, W2, (int)d->pad_top, (int)d->pad_left);
+        a, xs, (int)d->n, (int)d->ih, (int)d->iw, (int)d->ci, H2, W2, (int)d->pad_top, (int)d->pad_left, pack);
     NNCB_LAUNCHED(ctx);
     nncb_gemm_desc dd = *d;
-    dd.ih = H2; dd.iw = W2; dd.ci = 32; dd.kh = kh2; dd.kw = kw2; dd.sh = 1; dd.sw = 1;
+    dd.ih = H2; dd.iw = W2; dd.ci = 32; dd.kh = kh2; dd.kw = kwt; dd.sh = 1; dd.sw = 1;
     dd.pad_top = 0; dd.pad_left = 0;
+    g_dil_w = pack ? 2 : 1;
+    int rc = 0;
     if (d->kind == NNCB_CONV_FWD) {
-        s2d_weight_k<<<grid_for(ctx, kh2 * kw2 * 32 * d->co, 256), 256, 0, ctx->stream>>>(
-            b, wsp, (int)d->kh, (int)d->kw, (int)d->ci, (int)d->co, kh2, kw2);
+        s2d_weight_k<<<grid_for(ctx, kh2 * kwt * 32 * d->co, 256), 256, 0, ctx->stream>>>(
+            b, wsp, (int)d->kh, (int)d->kw, (int)d->ci, (int)d->co, kh2, kwt, pack);
         NNCB_LAUNCHED(ctx);
-        int rc = gemm_tc_impl(ctx, &dd, xs, 0, wsp, bias, out, handled);
+        rc = gemm_tc_impl(ctx, &dd, xs, 0, wsp, bias, out, handled);
+        g_dil_w = 1;
         if (!rc && !*handled) return fail("space-to-depth route: conv rejected");
         return rc;
     }
-    int rc = gemm_tc_impl(ctx, &dd, xs, 0, b, nullptr, wsp, handled);   // dW' = wgrad over x'
+    rc = gemm_tc_impl(ctx, &dd, xs, 0, b, nullptr, wsp, handled);   // dW'' = wgrad over x''
+    g_dil_w = 1;
     if (rc) return rc;
     if (!*handled) return fail("space-to-depth route: wgrad rejected");
     s2d_wgrad_back_k<<<grid_for(ctx, d->kh * d->kw * d->ci * d->co, 256), 256, 0, ctx->stream>>>(
-        wsp, out, (int)d->kh, (int)d->kw, (int)d->ci, (int)d->co, kw2);
+        wsp, out, (int)d->kh, (int)d->kw, (int)d->ci, (int)d->co, kwt, pack);
     NNCB_LAUNCHED(ctx);
     return 0;
 }
@@ -1388,6 +1411,7 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
     TcParams P;
     memset(&P, 0, sizeof(P));
     P.debug = dbg;
+    P.dil_w = g_dil_w;
     CUtensorMap ma, mb;
     memset(&ma, 0, sizeof(ma));
     if (manual) {
@@ -1419,7 +1443,7 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
             }
             for (int t = 0; t < (manual ? 1 : kh * kw); ++t) {
                 P.off_h[t] = manual ? 0 : (int)(t / kw - pt);
-                P.off_w[t] = manual ? 0 : (int)(t % kw - pl);
+                P.off_w[t] = manual ? 0 : (int)((t % kw) * g_dil_w - pl);
                 P.brow[t] = manual ? 0 : (int)(t * ci);
             }
         } else {
