@@ -39,6 +39,9 @@ const char* nnc_model_describe(nnc_model* m);          /* JSON: plans, groups, l
 int nnc_model_set_weight(nnc_model* m, const char* name, const float* data, int64_t n);
 int nnc_model_get_weight(nnc_model* m, const char* name, float* out, int64_t n);
 int nnc_model_set_input(nnc_model* m, const char* name, const float* data, const int64_t* dims, int rank);
+/* Like nnc_model_set_input but without a copy: `data` is borrowed and must stay
+   valid and unchanged until the next run / gradients / train_step call returns. */
+int nnc_model_set_input_borrowed(nnc_model* m, const char* name, const float* data, const int64_t* dims, int rank);
 
 /* role: 0 = inference plan, 1 = train_fwd plan (outputs include the SaveSet). */
 int nnc_model_run(nnc_model* m, int role);

@@ -77,6 +77,8 @@ def _load():
         "nnc_model_infer_device": (I, [P]),
         "nnc_model_run_device": (I, [P, I]),
         "nnc_model_run_outputs": (I, [P, I, ctypes.c_char_p]),
+        "nnc_model_set_input_borrowed": (I, [P, ctypes.c_char_p, ctypes.POINTER(ctypes.c_float),
+                                             ctypes.POINTER(ctypes.c_int64), I]),
         "nnc_device_ctx": (P, []),
         "nnc_model_check_kernels": (I, [P]),
         "nnc_comm_unique_id": (I, [ctypes.c_char_p]),
@@ -158,6 +160,17 @@ class CompiledModel:
         dims = (ctypes.c_int64 * v.ndim)(*v.shape)
         _check(_host.nnc_model_set_input(self._h, name.encode(), _fptr(v), dims, v.ndim))
 
+    def _borrow(self, inputs: Dict[str, np.ndarray]):
+        """Feed inputs without a host copy; returns the arrays that must stay
+        alive until the consuming call returns."""
+        keep = []
+        for k, v in inputs.items():
+            a = np.ascontiguousarray(v, dtype=np.float32)
+            keep.append(a)
+            dims = (ctypes.c_int64 * a.ndim)(*a.shape)
+            _check(_host.nnc_model_set_input_borrowed(self._h, k.encode(), _fptr(a), dims, a.ndim))
+        return keep
+
     def _plan_value(self, role: str, name: str):
         for v in self.describe[role]["values"]:
             if v["name"] == name:
@@ -168,8 +181,7 @@ class CompiledModel:
             outputs: Optional[Sequence[str]] = None) -> Dict[str, np.ndarray]:
         """runtime::execute on the inference (or train_fwd) plan; returns every output,
         or only `outputs` (the others stay on the device)."""
-        for k, v in inputs.items():
-            self.feed(k, v)
+        keep = self._borrow(inputs)   # noqa: F841  (alive until the run returns)
         r = 1 if role == "train_fwd" else 0
         if outputs is None:
             _check(_host.nnc_model_run(self._h, r))
@@ -191,16 +203,14 @@ class CompiledModel:
         return out
 
     def train_step(self, inputs: Dict[str, np.ndarray], target: np.ndarray, lr: float) -> float:
-        for k, v in inputs.items():
-            self.feed(k, v)
+        keep = self._borrow(inputs)   # noqa: F841
         t = np.ascontiguousarray(target, dtype=np.float32)
         loss = ctypes.c_double()
         _check(_host.nnc_model_train_step(self._h, _fptr(t), t.size, lr, ctypes.byref(loss)))
         return loss.value
 
     def gradients(self, inputs: Dict[str, np.ndarray], target: np.ndarray):
-        for k, v in inputs.items():
-            self.feed(k, v)
+        keep = self._borrow(inputs)   # noqa: F841
         t = np.ascontiguousarray(target, dtype=np.float32)
         loss = ctypes.c_double()
         _check(_host.nnc_model_gradients(self._h, _fptr(t), t.size, ctypes.byref(loss)))
@@ -213,8 +223,7 @@ class CompiledModel:
 
     # -- device-resident stepping (benchmarks) ------------------------------
     def trainer_prepare(self, inputs: Dict[str, np.ndarray], target: np.ndarray):
-        for k, v in inputs.items():
-            self.feed(k, v)
+        keep = self._borrow(inputs)   # noqa: F841
         t = np.ascontiguousarray(target, dtype=np.float32)
         _check(_host.nnc_model_trainer_prepare(self._h, _fptr(t), t.size))
 

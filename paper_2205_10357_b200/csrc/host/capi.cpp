@@ -180,22 +180,35 @@ int nnc_model_set_input(nnc_model* m, const char* name, const float* data, const
         // a fresh tensor every call
         std::vector<int64_t> d(dims, dims + rank);
         auto it = m->inputs.find(name);
-        if (it == m->inputs.end() || it->second.dims() != d) {
+        if (it == m->inputs.end() || it->second.dims() != d || it->second.is_view()) {
             it = m->inputs.insert_or_assign(name, Tensor::uninitialized(DType::F32, d)).first;
         }
         nncb_host_copy(it->second.data(), data, it->second.byte_size());
     });
 }
 
+// borrowed inputs are valid only for the call that consumes them
+void drop_views(nnc_model* m) {
+    for (auto it = m->inputs.begin(); it != m->inputs.end();)
+        it = it->second.is_view() ? m->inputs.erase(it) : std::next(it);
+}
+
+int nnc_model_set_input_borrowed(nnc_model* m, const char* name, const float* data, const int64_t* dims, int rank) {
+    // no copy: the next run / train_step streams straight from `data`
+    return guarded([&] { m->inputs.insert_or_assign(name, Tensor::view(DType::F32, std::vector<int64_t>(dims, dims + rank), data)); });
+}
+
 int nnc_model_run(nnc_model* m, int role) {
-    return guarded([&] {
+    const int rc = guarded([&] {
         const plan::ExecutionPlan& p = role == 1 ? m->plans.train_fwd : m->plans.inference;
         m->outputs = runtime::execute(p, m->inputs, *m->host, nullptr, m->opts);
     });
+    drop_views(m);
+    return rc;
 }
 
 int nnc_model_run_outputs(nnc_model* m, int role, const char* names) {
-    return guarded([&] {
+    const int rc = guarded([&] {
         // ExecOptions::materialize: only the named outputs are copied back
         std::set<std::string> want;
         std::string cur;
@@ -213,6 +226,8 @@ int nnc_model_run_outputs(nnc_model* m, int role, const char* names) {
         const plan::ExecutionPlan& p = role == 1 ? m->plans.train_fwd : m->plans.inference;
         m->outputs = runtime::execute(p, m->inputs, *m->host, nullptr, o);
     });
+    drop_views(m);
+    return rc;
 }
 
 int nnc_model_output(nnc_model* m, const char* name, float* out, int64_t n) {
@@ -225,11 +240,15 @@ int nnc_model_output(nnc_model* m, const char* name, float* out, int64_t n) {
 }
 
 int nnc_model_train_step(nnc_model* m, const float* target, int64_t n, double lr, double* loss) {
-    return guarded([&] { *loss = runtime::train_step(m->plans, m->inputs, target_tensor(m, target, n), *m->host, lr, nullptr, m->opts); });
+    const int rc = guarded([&] { *loss = runtime::train_step(m->plans, m->inputs, target_tensor(m, target, n), *m->host, lr, nullptr, m->opts); });
+    drop_views(m);
+    return rc;
 }
 
 int nnc_model_gradients(nnc_model* m, const float* target, int64_t n, double* loss) {
-    return guarded([&] { m->grads = runtime::gradients(m->plans, m->inputs, target_tensor(m, target, n), *m->host, loss, nullptr, m->opts); });
+    const int rc = guarded([&] { m->grads = runtime::gradients(m->plans, m->inputs, target_tensor(m, target, n), *m->host, loss, nullptr, m->opts); });
+    drop_views(m);
+    return rc;
 }
 
 int nnc_model_grad(nnc_model* m, const char* weight, float* out, int64_t n) {
@@ -242,13 +261,15 @@ int nnc_model_grad(nnc_model* m, const char* weight, float* out, int64_t n) {
 }
 
 int nnc_model_trainer_prepare(nnc_model* m, const float* target, int64_t n) {
-    return guarded([&] {
+    const int rc = guarded([&] {
         auto& dev = runtime::default_device();
         m->trainer = &runtime::shared_trainer(m->plans, *m->host, dev, m->opts);
         Tensor t = target_tensor(m, target, n);
         // one full host step uploads inputs + target and warms every kernel
         m->trainer->step(m->inputs, t, 0.0);
     });
+    drop_views(m);
+    return rc;
 }
 
 int nnc_model_trainer_step_device(nnc_model* m, double lr) {

@@ -36,6 +36,22 @@ Tensor Tensor::uninitialized(DType dt, std::vector<int64_t> dims) {
     return t;
 }
 
+Tensor Tensor::view(DType dt, std::vector<int64_t> dims, const void* data) {
+    Tensor t;
+    t.dtype_ = dt;
+    t.dims_ = std::move(dims);
+    t.view_ = static_cast<const uint8_t*>(data);
+    t.view_bytes_ = static_cast<size_t>(element_count(t.dims_)) * dtype_size(dt);
+    return t;
+}
+
+void Tensor::own() {
+    data_.resize(view_bytes_);
+    std::memcpy(data_.data(), view_, view_bytes_);
+    view_ = nullptr;
+    view_bytes_ = 0;
+}
+
 Tensor Tensor::from_f32(std::vector<int64_t> dims, std::vector<float> values) {
     Tensor t(DType::F32, std::move(dims));
     std::memcpy(t.data(), values.data(), t.byte_size());
@@ -43,15 +59,15 @@ Tensor Tensor::from_f32(std::vector<int64_t> dims, std::vector<float> values) {
 }
 
 double Tensor::get(int64_t i) const {
-    if (dtype_ == DType::F32) return reinterpret_cast<const float*>(data_.data())[i];
-    return reinterpret_cast<const double*>(data_.data())[i];
+    if (dtype_ == DType::F32) return reinterpret_cast<const float*>(data())[i];
+    return reinterpret_cast<const double*>(data())[i];
 }
 
 void Tensor::set(int64_t i, double v) {
     if (dtype_ == DType::F32)
-        reinterpret_cast<float*>(data_.data())[i] = static_cast<float>(v);
+        reinterpret_cast<float*>(data())[i] = static_cast<float>(v);
     else
-        reinterpret_cast<double*>(data_.data())[i] = v;
+        reinterpret_cast<double*>(data())[i] = v;
 }
 
 }  // namespace nnc

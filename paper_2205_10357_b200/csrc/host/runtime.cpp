@@ -720,8 +720,9 @@ void check_inputs(const ExecutionPlan& p, const std::map<std::string, Tensor>& i
 std::map<std::string, Tensor> execute(const ExecutionPlan& p, const std::map<std::string, Tensor>& inputs,
                                       const HostModel& model, Device* device, const ExecOptions& opts) {
     Device& dev = device ? *device : default_device();
-    check_inputs(p, inputs);
     auto& slot = exec_caches()[{&dev, p.uid}];
+    const bool reuse_inputs = opts.inputs_resident && slot && slot->runs > 0;
+    if (!reuse_inputs) check_inputs(p, inputs);
     // weights: stamp-checked device cache (uploads only stale tensors)
     std::map<std::string, void*> wptrs;
     for (const std::string& w : p.weight_names) wptrs[w] = dev.weight_buffer(model, w, model.tensor(w), model.stamp(w));
@@ -737,7 +738,7 @@ std::map<std::string, Tensor> execute(const ExecutionPlan& p, const std::map<std
     }
     Program& prog = *slot->prog;
     nncb_ctx* ctx = dev.ctx();
-    if (!opts.inputs_resident || slot->runs == 0)
+    if (!reuse_inputs || slot->runs == 0)   // (a rebound program starts with runs == 0)
         for (uint32_t s : p.input_slots) {
             const Tensor& t = inputs.at(p.values[s].name);
             NNC_CHECK(nncb_h2d(ctx, prog.ptr(p.values[s].name), t.data(), t.byte_size()));

@@ -45,18 +45,29 @@ public:
     const std::vector<int64_t>& dims() const { return dims_; }
     size_t rank() const { return dims_.size(); }
     int64_t elements() const { return element_count(dims_); }
-    size_t byte_size() const { return data_.size(); }
-    const uint8_t* data() const { return data_.data(); }
-    uint8_t* data() { return data_.data(); }
-    const float* f32() const { return reinterpret_cast<const float*>(data_.data()); }
-    float* f32() { return reinterpret_cast<float*>(data_.data()); }
+    // read-only view of caller memory (not owned; must outlive every use).
+    // Writing through a view first copies it into owned storage.
+    static Tensor view(DType dt, std::vector<int64_t> dims, const void* data);
+    bool is_view() const { return view_ != nullptr; }
+
+    size_t byte_size() const { return view_ ? view_bytes_ : data_.size(); }
+    const uint8_t* data() const { return view_ ? view_ : data_.data(); }
+    uint8_t* data() {
+        if (view_) own();
+        return data_.data();
+    }
+    const float* f32() const { return reinterpret_cast<const float*>(data()); }
+    float* f32() { return reinterpret_cast<float*>(data()); }
     double get(int64_t i) const;
     void set(int64_t i, double v);
 
 private:
+    void own();
     DType dtype_ = DType::F32;
     std::vector<int64_t> dims_;
     std::vector<uint8_t, DefaultInitAllocator<uint8_t>> data_;
+    const uint8_t* view_ = nullptr;
+    size_t view_bytes_ = 0;
 };
 
 }  // namespace nnc
