@@ -90,6 +90,8 @@ enum nncb_ew_op {
                                division: dx = (gamma*invstd) * ((g - sum_g/M) - xhat*(sum_gx/M)).
                                Not bit-identical to BN_GRAD; the runtime uses it only in the
                                tf32 precision mode.                                       */
+    NNCB_EW_GELU_FAST = 15,      /* GELU in fp32 (erff): tf32 precision mode only            */
+    NNCB_EW_GELU_GRAD_FAST = 16, /* GELU gradient in fp32 (erff/expf): tf32 precision mode only */
     NNCB_EW_REDUCE_BN_GRAD = 13, /* BatchNorm backward reduction fused into the group that
                                produces g (replaces nncb_bn_grad_reduce for it):
                                sum_g[c] += g, sum_gx[c] += g*xhat, xhat = (x-mean)*invstd,

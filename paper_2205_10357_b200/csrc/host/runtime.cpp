@@ -416,13 +416,18 @@ struct Program {
                 nncb_ew_program prog{static_cast<int32_t>(L.ew.size()), L.ew.data(), L.ew_regs,
                                      static_cast<int32_t>(L.args.size())};
                 // tf32 mode: the BatchNorm input gradient takes per-channel
-                // quotients instead of a per-element IEEE division
+                // quotients instead of a per-element IEEE division, and GELU
+                // is evaluated in fp32 instead of double
                 bool fast = false;
-                for (const auto& in : L.ew) fast = fast || in.op == NNCB_EW_BN_GRAD;
+                for (const auto& in : L.ew)
+                    fast = fast || in.op == NNCB_EW_BN_GRAD || in.op == NNCB_EW_GELU || in.op == NNCB_EW_GELU_GRAD;
                 if (fast && precision == NNCB_PREC_TF32 && !std::getenv("NNC_EXACT_BN_GRAD")) {
                     b.ew_prog = L.ew;
-                    for (auto& in : b.ew_prog)
+                    for (auto& in : b.ew_prog) {
                         if (in.op == NNCB_EW_BN_GRAD) in.op = NNCB_EW_BN_GRAD_FAST;
+                        if (in.op == NNCB_EW_GELU) in.op = NNCB_EW_GELU_FAST;
+                        if (in.op == NNCB_EW_GELU_GRAD) in.op = NNCB_EW_GELU_GRAD_FAST;
+                    }
                     b.ew_regs = L.ew_regs;
                     prog.instr = b.ew_prog.data();
                 }

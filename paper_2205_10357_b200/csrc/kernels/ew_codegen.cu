@@ -66,6 +66,14 @@ __device__ __forceinline__ float gelu_grad_(float x, float g) {
   double pdf = exp(-0.5 * xd * xd) * 0.39894228040143267794;
   return (float)((double)g * (cdf + xd * pdf));
 }
+__device__ __forceinline__ float gelu_fast_(float x) {
+  return __fmul_rn(__fmul_rn(0.5f, x), __fadd_rn(1.f, erff(__fmul_rn(x, 0.70710678118654752440f))));
+}
+__device__ __forceinline__ float gelu_grad_fast_(float x, float g) {
+  const float cdf = __fmul_rn(0.5f, __fadd_rn(1.f, erff(__fmul_rn(x, 0.70710678118654752440f))));
+  const float pdf = __fmul_rn(__expf(__fmul_rn(__fmul_rn(-0.5f, x), x)), 0.39894228040143267794f);
+  return __fmul_rn(g, __fadd_rn(cdf, __fmul_rn(x, pdf)));
+}
 __device__ __forceinline__ float bn_grad_(float x, float g, float m, float s, float ga, float sg, float sgx,
                                           float cnt) {
   float xhat = __fmul_rn(__fsub_rn(x, m), s);
@@ -143,6 +151,8 @@ void emit_body(std::ostringstream& os, const nncb_ew_program& p, int W, bool use
             case NNCB_EW_COPY: expr = a + "[j]"; break;
             case NNCB_EW_GELU: expr = "gelu_(" + a + "[j])"; break;
             case NNCB_EW_GELU_GRAD: expr = "gelu_grad_(" + a + "[j], " + b + "[j])"; break;
+            case NNCB_EW_GELU_FAST: expr = "gelu_fast_(" + a + "[j])"; break;
+            case NNCB_EW_GELU_GRAD_FAST: expr = "gelu_grad_fast_(" + a + "[j], " + b + "[j])"; break;
             case NNCB_EW_BN_APPLY:
                 expr = "bn_apply_(" + a + "[j], " + b + "[j], " + c + "[j], " + dd + "[j], " + e + "[j])";
                 break;

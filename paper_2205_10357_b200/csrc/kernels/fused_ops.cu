@@ -566,6 +566,136 @@ __global__ void __launch_bounds__(256) layernorm_k(const float* __restrict__ x, 
     }
 }
 
+// LayerNorm with the row held in registers: VPT float4 per thread (C = 1024*VPT
+// or less, C % 4 == 0), one global read of x (and g), float partial sums per
+// thread folded in double. Same per-element arithmetic as layernorm_k.
+template <int MODE, int VPT>
+__global__ void __launch_bounds__(256) layernorm_reg_k(const float* __restrict__ x, const float* __restrict__ gamma,
+                                                       const float* __restrict__ beta, const float* __restrict__ gy,
+                                                       float* __restrict__ out, float* __restrict__ row_stats, int C,
+                                                       double eps) {
+    const int64_t row = blockIdx.x;
+    const float4* xr = reinterpret_cast<const float4*>(x + row * C);
+    const int C4 = C >> 2;
+    __shared__ double red[2][8];
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    auto block_sum2 = [&](double a, double b, double& ra, double& rb) {
+        for (int o = 16; o; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            b += __shfl_xor_sync(0xffffffffu, b, o);
+        }
+        __syncthreads();
+        if (lane == 0) {
+            red[0][warp] = a;
+            red[1][warp] = b;
+        }
+        __syncthreads();
+        ra = 0;
+        rb = 0;
+        for (int k = 0; k < 8; ++k) {
+            ra += red[0][k];
+            rb += red[1][k];
+        }
+    };
+    float4 v[VPT];
+    float f0 = 0.f, f1 = 0.f;
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+        const int c4 = threadIdx.x + 256 * k;
+        v[k] = c4 < C4 ? __ldg(xr + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        f0 += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+        f1 += (v[k].x * v[k].x + v[k].y * v[k].y) + (v[k].z * v[k].z + v[k].w * v[k].w);
+    }
+    double s0, s1;
+    block_sum2(f0, f1, s0, s1);
+    const double mean_d = s0 / (double)C;
+    double var = s1 / (double)C - mean_d * mean_d;
+    if (var < 0) var = 0;
+    const float mean = (float)mean_d;
+    const float rstd = (float)(1.0 / sqrt(var + eps));
+    if (MODE == 2) {
+        if (threadIdx.x == 0) {
+            row_stats[row * 2] = mean;
+            row_stats[row * 2 + 1] = rstd;
+        }
+        return;
+    }
+    const float4* g4 = reinterpret_cast<const float4*>(gamma);
+    float4* o4 = reinterpret_cast<float4*>(out + row * C);
+    if (MODE == 0) {
+        const float4* b4 = reinterpret_cast<const float4*>(beta);
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+            const int c4 = threadIdx.x + 256 * k;
+            if (c4 >= C4) continue;
+            const float4 ga = __ldg(g4 + c4), be = __ldg(b4 + c4);
+            float4 y;
+            y.x = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(v[k].x, mean), rstd), ga.x), be.x);
+            y.y = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(v[k].y, mean), rstd), ga.y), be.y);
+            y.z = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(v[k].z, mean), rstd), ga.z), be.z);
+            y.w = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(v[k].w, mean), rstd), ga.w), be.w);
+            o4[c4] = y;
+        }
+        return;
+    }
+    // backward: gg = g*gamma; sums of gg and gg*xhat, then dx
+    const float4* gr = reinterpret_cast<const float4*>(gy + row * C);
+    float4 gg[VPT];
+    float t0f = 0.f, t1f = 0.f;
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+        const int c4 = threadIdx.x + 256 * k;
+        if (c4 >= C4) {
+            gg[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            continue;
+        }
+        const float4 gv = __ldg(gr + c4), ga = __ldg(g4 + c4);
+        gg[k] = make_float4(__fmul_rn(gv.x, ga.x), __fmul_rn(gv.y, ga.y), __fmul_rn(gv.z, ga.z), __fmul_rn(gv.w, ga.w));
+        const float xh[4] = {__fmul_rn(__fsub_rn(v[k].x, mean), rstd), __fmul_rn(__fsub_rn(v[k].y, mean), rstd),
+                             __fmul_rn(__fsub_rn(v[k].z, mean), rstd), __fmul_rn(__fsub_rn(v[k].w, mean), rstd)};
+        t0f += (gg[k].x + gg[k].y) + (gg[k].z + gg[k].w);
+        t1f += (gg[k].x * xh[0] + gg[k].y * xh[1]) + (gg[k].z * xh[2] + gg[k].w * xh[3]);
+    }
+    double t0, t1;
+    block_sum2(t0f, t1f, t0, t1);
+    const float sg = (float)t0, sgx = (float)t1, cnt = (float)C;
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+        const int c4 = threadIdx.x + 256 * k;
+        if (c4 >= C4) continue;
+        const float vv[4] = {v[k].x, v[k].y, v[k].z, v[k].w}, gq[4] = {gg[k].x, gg[k].y, gg[k].z, gg[k].w};
+        float r[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float xhat = __fmul_rn(__fsub_rn(vv[j], mean), rstd);
+            const float t = __fadd_rn(sg, __fmul_rn(xhat, sgx));
+            r[j] = __fmul_rn(rstd, __fsub_rn(gq[j], __fdiv_rn(t, cnt)));
+        }
+        o4[c4] = make_float4(r[0], r[1], r[2], r[3]);
+    }
+}
+
+template <int MODE>
+bool layernorm_reg(nncb_ctx* ctx, const float* x, const float* gamma, const float* beta, const float* g, float* out,
+                   float* rs, int64_t rows, int64_t C, double eps) {
+    static const bool off = getenv("NNCB_LN_REG") && atoi(getenv("NNCB_LN_REG")) == 0;
+    if (off || C % 4 != 0 || C > 8192) return false;
+    for (const void* p : {(const void*)x, (const void*)gamma, (const void*)beta, (const void*)g, (const void*)out})
+        if (p && (reinterpret_cast<uintptr_t>(p) & 15)) return false;
+    const int vpt = static_cast<int>((C / 4 + 255) / 256);
+    const unsigned grid = static_cast<unsigned>(rows);
+    const int Ci = static_cast<int>(C);
+    if (vpt <= 1)
+        layernorm_reg_k<MODE, 1><<<grid, 256, 0, ctx->stream>>>(x, gamma, beta, g, out, rs, Ci, eps);
+    else if (vpt <= 2)
+        layernorm_reg_k<MODE, 2><<<grid, 256, 0, ctx->stream>>>(x, gamma, beta, g, out, rs, Ci, eps);
+    else if (vpt <= 4)
+        layernorm_reg_k<MODE, 4><<<grid, 256, 0, ctx->stream>>>(x, gamma, beta, g, out, rs, Ci, eps);
+    else
+        layernorm_reg_k<MODE, 8><<<grid, 256, 0, ctx->stream>>>(x, gamma, beta, g, out, rs, Ci, eps);
+    return true;
+}
+
 __global__ void ln_dgamma_partial_k(const float* __restrict__ x, const float* __restrict__ g,
                                     const float* __restrict__ rs, double* __restrict__ part, int64_t rows, int64_t C,
                                     int64_t rpc) {
@@ -741,7 +871,8 @@ int nncb_bn_grad_reduce(nncb_ctx* ctx, const float* x, const float* stats, const
 int nncb_layernorm_fwd(nncb_ctx* ctx, const float* x, const float* gamma, const float* beta, float* y, int64_t rows,
                        int64_t C, double eps) {
     if (rows == 0) return 0;
-    layernorm_k<0><<<(unsigned)rows, 256, 0, ctx->stream>>>(x, gamma, beta, nullptr, y, nullptr, C, eps);
+    if (!layernorm_reg<0>(ctx, x, gamma, beta, nullptr, y, nullptr, rows, C, eps))
+        layernorm_k<0><<<(unsigned)rows, 256, 0, ctx->stream>>>(x, gamma, beta, nullptr, y, nullptr, C, eps);
     NNCB_LAUNCHED(ctx);
     return 0;
 }
@@ -749,7 +880,8 @@ int nncb_layernorm_fwd(nncb_ctx* ctx, const float* x, const float* gamma, const 
 int nncb_layernorm_bwd(nncb_ctx* ctx, const float* x, const float* gamma, const float* g, float* gx, int64_t rows,
                        int64_t C, double eps) {
     if (rows == 0) return 0;
-    layernorm_k<1><<<(unsigned)rows, 256, 0, ctx->stream>>>(x, gamma, nullptr, g, gx, nullptr, C, eps);
+    if (!layernorm_reg<1>(ctx, x, gamma, nullptr, g, gx, nullptr, rows, C, eps))
+        layernorm_k<1><<<(unsigned)rows, 256, 0, ctx->stream>>>(x, gamma, nullptr, g, gx, nullptr, C, eps);
     NNCB_LAUNCHED(ctx);
     return 0;
 }
@@ -769,7 +901,8 @@ int nncb_layernorm_dgamma(nncb_ctx* ctx, const float* x, const float* g, float* 
     if (!base) return nncb::fail("layernorm_dgamma: scratch allocation failed");
     float* rs = reinterpret_cast<float*>(base);
     double* part = reinterpret_cast<double*>(base + part_off);
-    layernorm_k<2><<<(unsigned)rows, 256, 0, ctx->stream>>>(x, nullptr, nullptr, nullptr, nullptr, rs, C, eps);
+    if (!layernorm_reg<2>(ctx, x, nullptr, nullptr, nullptr, nullptr, rs, rows, C, eps))
+        layernorm_k<2><<<(unsigned)rows, 256, 0, ctx->stream>>>(x, nullptr, nullptr, nullptr, nullptr, rs, C, eps);
     NNCB_LAUNCHED(ctx);
     ln_dgamma_partial_k<<<dim3((unsigned)col_tiles, (unsigned)chunks), dim3(32, 8), 0, ctx->stream>>>(x, g, rs, part,
                                                                                                       rows, C, rpc);
