@@ -722,11 +722,30 @@ __global__ void l1_k(const float* __restrict__ p, const float* __restrict__ t, f
                      double* __restrict__ partial, int64_t n) {
     double inv = n > 0 ? 1.0 / (double)n : 0.0;
     double acc = 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        double d = __dsub_rn((double)p[i], (double)t[i]);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x, t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    auto one = [&](float pv, float tv) -> float {
+        const double d = __dsub_rn((double)pv, (double)tv);
         acc = __dadd_rn(acc, fabs(d));
-        grad[i] = (float)(d > 0 ? inv : (d < 0 ? -inv : 0.0));
+        return (float)(d > 0 ? inv : (d < 0 ? -inv : 0.0));
+    };
+    const bool vec = ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(t) |
+                       reinterpret_cast<uintptr_t>(grad)) & 15) == 0;
+    int64_t tail = 0;
+    if (vec) {   // float4 body; the gradient element values are unchanged
+        const int64_t n4 = n / 4;
+        for (int64_t i = t0; i < n4; i += stride) {
+            const float4 pv = __ldg(reinterpret_cast<const float4*>(p) + i);
+            const float4 tv = __ldg(reinterpret_cast<const float4*>(t) + i);
+            float4 gv;
+            gv.x = one(pv.x, tv.x);
+            gv.y = one(pv.y, tv.y);
+            gv.z = one(pv.z, tv.z);
+            gv.w = one(pv.w, tv.w);
+            reinterpret_cast<float4*>(grad)[i] = gv;
+        }
+        tail = n4 * 4;
     }
+    for (int64_t i = tail + t0; i < n; i += stride) grad[i] = one(p[i], t[i]);
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     __shared__ double red[32];
     if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = acc;
