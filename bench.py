@@ -425,6 +425,24 @@ def main():
             cpu = cpu_reference(args.config, args.cpu_seconds, min(os.cpu_count() or 1, 32))
         except Exception as exc:  # noqa: BLE001
             cpu = {"value": None, "error": str(exc)[:200]}
+    mode_a = None
+    if cfg["kind"] == "chain" and rank == 0:
+        # SURVEY.md §8(d) C2 mode A: inference BatchNorm (per-channel affine),
+        # the whole chain one fused group: read x, y, write out = 12 B/element
+        model.run(inputs, role="inference", outputs=[])
+        for _ in range(3):
+            model.run_device("inference")
+        timer.sync()
+        timer.start()
+        for _ in range(args.steps):
+            model.run_device("inference")
+        a_ms = timer.stop() / args.steps
+        elems = int(np.prod(inputs["x"].shape))
+        pk, src = peaks()
+        gbs = 12.0 * elems / (a_ms / 1000.0) / 1e9
+        mode_a = {"metric": "fused-group HBM GB/s (C2 chain, inference BN)", "value": gbs, "unit": "GB/s",
+                  "ms_per_pass": a_ms, "bytes_per_element": 12, "frac_of_hbm_peak": gbs / pk["hbm_gbs"],
+                  "peak_source": f"{src} HBM copy"}
     line = {
         "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
@@ -435,6 +453,10 @@ def main():
         "cpu_baseline": cpu,
         "by_kernel_kind": top,
     }
+    if mode_a:
+        line["mode_a"] = mode_a
+        line["config"]["note"] = ("value = mode B (train-mode BN forward: 40 B/element algorithmic; the train_fwd "
+                                  "plan also writes the values backward needs); mode_a = inference-BN chain")
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

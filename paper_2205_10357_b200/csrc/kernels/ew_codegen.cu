@@ -216,7 +216,9 @@ std::string generate(const nncb_ew_program& p, bool uses_ch) {
     // (measured: 5.1 -> 6.1 TB/s for the BN input gradient). Light programs keep
     // the default. NNCB_EW_MINBLOCKS overrides.
     static const int env_min_blocks = getenv("NNCB_EW_MINBLOCKS") ? atoi(getenv("NNCB_EW_MINBLOCKS")) : -1;
-    int min_blocks = chregs.size() >= 3 ? 4 : 0;
+    // (more than 8 per-channel float4 operands would not fit 64 registers:
+    // those programs, e.g. a chain of inference BatchNorms, get a 2-block budget)
+    int min_blocks = chregs.size() > 8 ? 2 : chregs.size() >= 3 ? 4 : 0;
     if (env_min_blocks >= 0) min_blocks = env_min_blocks;
     if (red)   // 16 double accumulator registers per reduction
         os << "extern \"C\" __global__ void __launch_bounds__(256, " << (nred > 1 ? 2 : 4)
