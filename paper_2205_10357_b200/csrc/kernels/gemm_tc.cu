@@ -1284,7 +1284,7 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
         // bit 16: CTA pair (cta_group::2, 256-row tiles over two SMs)
         static const bool pairs = !(getenv("NNCB_TC_PAIR") && atoi(getenv("NNCB_TC_PAIR")) == 0);
         std::vector<int> cands = N <= 128 ? std::vector<int>{64, 128} : std::vector<int>{128, 256};
-        if (pairs && !dense) {
+        if (pairs) {
             cands.push_back(0x10000 | 128);
             if (N > 128) cands.push_back(0x10000 | 256);
         }

@@ -174,3 +174,24 @@ def test_cta_pair(shape, tile):
         check(tc, ex)
     finally:
         K.nncb_gemm_force_tile(0)
+
+
+@pytest.mark.parametrize("tile", [0x10000 | 128, 0x10000 | 256])
+@pytest.mark.parametrize("b,i,o", [(300, 256, 320), (1024, 512, 512), (64, 96, 160)])
+def test_cta_pair_dense(b, i, o, tile):
+    """CTA pairs on the dense contractions (1x1 convolutions over [batch, 1, 1, features])."""
+    rng = np.random.default_rng(8)
+    x = rng.uniform(-1, 1, (b, i)).astype(np.float32)
+    w = rng.uniform(-1, 1, (i, o)).astype(np.float32)
+    bias = rng.uniform(-1, 1, o).astype(np.float32)
+    gy = rng.uniform(-1, 1, (b, o)).astype(np.float32)
+    geo = dict(batch=b, in_f=i, out_f=o)
+    K.nncb_gemm_force_tile(tile)
+    try:
+        for kind, args, shape in [(DENSE_FWD, (Dev(x), Dev(w), Dev(bias)), (b, o)),
+                                  (DENSE_DGRAD, (Dev(gy), Dev(w), None), (b, i)),
+                                  (DENSE_WGRAD, (Dev(x), Dev(gy), None), (i, o))]:
+            tc, ex = run_both(kind, geo, *args, shape, expect_tc=True)
+            check(tc, ex)
+    finally:
+        K.nncb_gemm_force_tile(0)
