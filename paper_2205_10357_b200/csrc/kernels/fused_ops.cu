@@ -74,12 +74,14 @@ __global__ void maxpool_fwd_k(const float* __restrict__ x, float* __restrict__ y
 
 // Max-pool backward as a gather over the windows covering each input pixel,
 // in (oh, ow) ascending order = the reference scatter order (bit-exact).
-template <int V, typename I>
+// K3S2 = 1: the 3x3 stride-2 window (ResNet stem) with compile-time window
+// arithmetic; 0: window and stride from the descriptor.
+template <int V, typename I, int K3S2 = 0>
 __global__ void maxpool_bwd_k(const float* __restrict__ idx, const float* __restrict__ gy, float* __restrict__ gx,
                               nncb_pool_geom g) {
     const int C = (int)g.c, CV = C / V;
     const int OW = (int)g.ow, OH = (int)g.oh, IW = (int)g.iw, IH = (int)g.ih;
-    const int KH = (int)g.kh, KW = (int)g.kw, SH = (int)g.sh, SW = (int)g.sw;
+    const int KH = K3S2 ? 3 : (int)g.kh, KW = K3S2 ? 3 : (int)g.kw, SH = K3S2 ? 2 : (int)g.sh, SW = K3S2 ? 2 : (int)g.sw;
     const I total = static_cast<I>(g.n * g.ih * g.iw * CV);
     for (I t = blockIdx.x * (I)blockDim.x + threadIdx.x; t < total; t += (I)gridDim.x * blockDim.x) {
         const int cv = (int)(t % CV);
@@ -817,7 +819,10 @@ int nncb_maxpool_bwd(nncb_ctx* ctx, const nncb_pool_geom* g, const float* idx, c
     const int64_t out_total = g->n * g->oh * g->ow * g->c;
     const bool i32 = std::max(total, out_total) < (int64_t(1) << 31);   // 32-bit index decode when it fits
     if (g->c % 4 == 0 && i32)
-        maxpool_bwd_k<4, int><<<nncb::grid_for(ctx, total / 4, 256), 256, 0, ctx->stream>>>(idx, gy, gx, *g);
+        if (g->kh == 3 && g->kw == 3 && g->sh == 2 && g->sw == 2)
+            maxpool_bwd_k<4, int, 1><<<nncb::grid_for(ctx, total / 4, 256), 256, 0, ctx->stream>>>(idx, gy, gx, *g);
+        else
+            maxpool_bwd_k<4, int><<<nncb::grid_for(ctx, total / 4, 256), 256, 0, ctx->stream>>>(idx, gy, gx, *g);
     else if (g->c % 4 == 0)
         maxpool_bwd_k<4, int64_t><<<nncb::grid_for(ctx, total / 4, 256), 256, 0, ctx->stream>>>(idx, gy, gx, *g);
     else if (i32)
