@@ -72,6 +72,9 @@ int      nnc_model_run_device(nnc_model* m, int role);
 int nnc_model_check_kernels(nnc_model* m);
 
 /* The device context (nncb_ctx*) for stream events / timing via nncb.h. */
+/* Device transfer counters (runtime::OffloadDevice::sync_stats, ref runtime.hpp:50-75): weight_bytes
+   counts each stamp-triggered weight upload at 64-byte alignment; reset zeroes them after reading. */
+int nnc_device_sync_stats(int reset, uint64_t* h2d_bytes, uint64_t* d2h_bytes, uint64_t* weight_bytes);
 void* nnc_device_ctx(void);
 
 /* Data parallelism (one process per GPU). */

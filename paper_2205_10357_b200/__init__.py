@@ -76,6 +76,8 @@ def _load():
         "nnc_model_arena_bytes": (U64, [P]),
         "nnc_model_infer_device": (I, [P]),
         "nnc_model_run_device": (I, [P, I]),
+        "nnc_device_sync_stats": (I, [I, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64),
+                                      ctypes.POINTER(ctypes.c_uint64)]),
         "nnc_model_run_outputs": (I, [P, I, ctypes.c_char_p]),
         "nnc_model_set_input_borrowed": (I, [P, ctypes.c_char_p, ctypes.POINTER(ctypes.c_float),
                                              ctypes.POINTER(ctypes.c_int64), I]),
@@ -293,6 +295,13 @@ def comm_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(_host.nnc_comm_unique_id(buf))
     return buf.raw
+
+
+def sync_stats(reset: bool = False) -> Dict[str, int]:
+    """Device transfer counters (the reference's OffloadDevice::sync_stats)."""
+    h, d, w = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    _check(_host.nnc_device_sync_stats(1 if reset else 0, ctypes.byref(h), ctypes.byref(d), ctypes.byref(w)))
+    return {"h2d_bytes": h.value, "d2h_bytes": d.value, "weight_bytes": w.value}
 
 
 def init_comm(nranks: int, rank: int, uid: bytes):

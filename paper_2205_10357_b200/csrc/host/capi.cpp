@@ -327,6 +327,15 @@ int nnc_model_check_kernels(nnc_model* m) {
     });
 }
 
+int nnc_device_sync_stats(int reset, uint64_t* h2d_bytes, uint64_t* d2h_bytes, uint64_t* weight_bytes) {
+    return guarded([&] {
+        runtime::SyncStats st = runtime::default_device().sync_stats(reset != 0);
+        if (h2d_bytes) *h2d_bytes = st.h2d_bytes;
+        if (d2h_bytes) *d2h_bytes = st.d2h_bytes;
+        if (weight_bytes) *weight_bytes = st.weight_bytes;
+    });
+}
+
 void* nnc_device_ctx(void) {
     try {
         return runtime::default_device().ctx();

@@ -622,7 +622,7 @@ void* Device::weight_buffer(const HostModel& m, const std::string& name, const T
         NNC_CHECK(nncb_h2d(ctx_, cw.ptr, host.data(), bytes));
         cw.stamp = stamp;
         stats_.h2d_bytes += bytes;
-        stats_.weight_bytes += bytes;
+        stats_.weight_bytes += plan::align_bytes(static_cast<int64_t>(bytes), 64);   // aligned, as the reference counts
         ++stats_.weight_transfers[name];
     }
     return cw.ptr;

@@ -101,3 +101,29 @@ def test_c1_gradients_tf32(ref):
     assert abs(loss - rloss) <= 2e-2 * abs(rloss)
     for w, g in rgrads.items():
         assert rel_err(grads[w], g) < 2e-2, w
+
+
+def test_offload_protocol_ac8():
+    """The reference's offload protocol (AC-8; test_runtime.cpp:129-193,
+    acceptance.cpp:511-561) on the device weight cache: the first run uploads
+    every weight, a second run moves 0 weight bytes with bit-identical outputs,
+    and one mutation moves exactly that weight's (64-byte aligned) bytes."""
+    doc = W.c1_small_cnn(4, bn=False)
+    x = W.uniform((4, 32, 32, 3), 1, "x")
+    m = P.CompiledModel(doc, precision=P.PREC_FP32)
+    P.sync_stats(reset=True)
+    out1 = m.run({"x": x})
+    s1 = P.sync_stats(reset=True)
+    expect = sum(-(-int(np.prod(shape)) * 4 // 64) * 64 for shape in m.weight_shapes.values())
+    assert s1["weight_bytes"] == expect
+    out2 = m.run({"x": x})
+    s2 = P.sync_stats(reset=True)
+    assert s2["weight_bytes"] == 0
+    for k in out1:
+        assert np.array_equal(out1[k], out2[k]), k
+    name = sorted(m.weight_shapes)[0]
+    w = np.random.default_rng(3).uniform(-0.1, 0.1, m.weight_shapes[name]).astype(np.float32)
+    m.set_weight(name, w)
+    m.run({"x": x})
+    s3 = P.sync_stats(reset=True)
+    assert s3["weight_bytes"] == -(-w.size * 4 // 64) * 64
