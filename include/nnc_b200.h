@@ -62,6 +62,9 @@ uint64_t nnc_model_launches_per_step(nnc_model* m);
  * {label, kind, ms, bytes, flops} (algorithmic bytes / flops per launch). */
 const char* nnc_model_profile_step(nnc_model* m, double lr);
 uint64_t nnc_model_arena_bytes(nnc_model* m);
+/* Device memory of a bound program (role 0 inference / 1 train_fwd after a run, 2 the trainer):
+   arena address span, live-bytes high water and plan::estimate_peak at the same 256-byte alignment. */
+int      nnc_model_memory(nnc_model* m, int role, uint64_t* arena, uint64_t* live_high, uint64_t* estimate);
 int      nnc_model_infer_device(nnc_model* m);         /* replay inference, no host copies */
 /* Replays plan `role` (0 inference, 1 train_fwd) with the inputs already on the device
    (from the last nnc_model_run of that role): no host<->device copies. */

@@ -76,6 +76,8 @@ def _load():
         "nnc_model_arena_bytes": (U64, [P]),
         "nnc_model_infer_device": (I, [P]),
         "nnc_model_run_device": (I, [P, I]),
+        "nnc_model_memory": (I, [P, I, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64),
+                                 ctypes.POINTER(ctypes.c_uint64)]),
         "nnc_device_sync_stats": (I, [I, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64),
                                       ctypes.POINTER(ctypes.c_uint64)]),
         "nnc_model_run_outputs": (I, [P, I, ctypes.c_char_p]),
@@ -246,6 +248,13 @@ class CompiledModel:
 
     def launches_per_step(self) -> int:
         return int(_host.nnc_model_launches_per_step(self._h))
+
+    def memory(self, role: str = "training") -> Dict[str, int]:
+        """Bound program memory vs the static planner (arena span, live high water, estimate)."""
+        a, lh, e = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        r = {"inference": 0, "train_fwd": 1, "training": 2}[role]
+        _check(_host.nnc_model_memory(self._h, r, ctypes.byref(a), ctypes.byref(lh), ctypes.byref(e)))
+        return {"arena_bytes": a.value, "live_high_water": lh.value, "estimate": e.value}
 
     def arena_bytes(self) -> int:
         return int(_host.nnc_model_arena_bytes(self._h))

@@ -298,6 +298,21 @@ const char* nnc_model_profile_step(nnc_model* m, double lr) {
     return rc ? nullptr : g_buf.c_str();
 }
 
+int nnc_model_memory(nnc_model* m, int role, uint64_t* arena, uint64_t* live_high, uint64_t* estimate) {
+    return guarded([&] {
+        runtime::MemoryReport r;
+        if (role == 2) {
+            if (!m->trainer) throw Error(Error::Code::BadDocument, "trainer not prepared");
+            r = m->trainer->memory_report();
+        } else {
+            r = runtime::memory_report(role == 1 ? m->plans.train_fwd : m->plans.inference);
+        }
+        *arena = static_cast<uint64_t>(r.arena_bytes);
+        *live_high = static_cast<uint64_t>(r.live_high_water);
+        *estimate = static_cast<uint64_t>(r.estimate);
+    });
+}
+
 uint64_t nnc_model_launches_per_step(nnc_model* m) { return m->trainer ? m->trainer->launches_per_step() : 0; }
 uint64_t nnc_model_arena_bytes(nnc_model* m) { return m->trainer ? m->trainer->arena_bytes() : 0; }
 

@@ -206,6 +206,10 @@ struct Program {
     std::vector<const ExecutionPlan*> plans;
     void* arena = nullptr;
     int64_t arena_bytes = 0;
+    // live bytes (every Buffer value, wherever it is stored: arena, weight
+    // cache, gradient region) replayed over the plan events at kAlign: the
+    // high water equals plan::estimate_peak at the same alignment
+    int64_t live_high = 0;
     void* side = nullptr;          // fused BatchNorm column-sum accumulators
     std::unordered_map<std::string, void*> where;   // value name -> device pointer
     std::vector<std::vector<BoundLaunch>> steps;     // per plan, flattened launches
@@ -231,10 +235,24 @@ struct Program {
         OffsetPlanner pl;
         std::unordered_map<std::string, int64_t> offset;
         std::unordered_map<std::string, bool> live;
+        std::unordered_map<std::string, int64_t> live_bytes;
+        int64_t live_cur = 0;
         for (const ExecutionPlan* p : plans)
             for (const plan::PlanEvent& ev : p->events) {
                 const plan::ValueEntry& v = p->values[ev.slot];
                 if (v.storage != StorageClass::Buffer) continue;
+                if (ev.alloc && !live_bytes.count(v.name)) {
+                    const int64_t b = plan::align_bytes(value_bytes(*p, ev.slot), kAlign);
+                    live_bytes[v.name] = b;
+                    live_cur += b;
+                    live_high = std::max(live_high, live_cur);
+                } else if (!ev.alloc) {
+                    auto lb = live_bytes.find(v.name);
+                    if (lb != live_bytes.end()) {
+                        live_cur -= lb->second;
+                        live_bytes.erase(lb);
+                    }
+                }
                 if (v.category == MemCategory::Parameter) {
                     if (!where.count(v.name)) where[v.name] = param_ptr(v.source_weight);
                     continue;
@@ -1050,6 +1068,26 @@ void* Trainer::input_device_ptr(const std::string& name) { return impl->prog->pt
 void* Trainer::target_device_ptr() { return impl->target; }
 size_t Trainer::arena_bytes() const { return static_cast<size_t>(impl->prog->arena_bytes); }
 uint64_t Trainer::launches_per_step() const { return impl->launches_per_step; }
+
+MemoryReport Trainer::memory_report() const {
+    MemoryReport r;
+    r.arena_bytes = impl->prog->arena_bytes;
+    r.live_high_water = impl->prog->live_high;
+    r.estimate = plan::estimate_peak(*impl->plans, kAlign).training_bytes;
+    return r;
+}
+
+MemoryReport memory_report(const ExecutionPlan& p, Device* device) {
+    Device& dev = device ? *device : default_device();
+    auto it = exec_caches().find({&dev, p.uid});
+    if (it == exec_caches().end() || !it->second)
+        throw Error(Error::Code::BadDocument, "memory_report: the plan has not been executed on this device");
+    MemoryReport r;
+    r.arena_bytes = it->second->prog->arena_bytes;
+    r.live_high_water = it->second->prog->live_high;
+    r.estimate = plan::plan_peak(p, kAlign);
+    return r;
+}
 
 double Trainer::step(const std::map<std::string, Tensor>& inputs, const Tensor& target, double lr) {
     Impl& I = *impl;

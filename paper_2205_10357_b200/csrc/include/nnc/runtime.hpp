@@ -135,6 +135,16 @@ double train_step(const plan::VersionPlans& plans, const std::map<std::string, T
                   const ExecOptions& opts = {});
 
 /// Drops every device program / CUDA graph / trainer cached for these plans.
+// Device memory of a bound program against the static planner: arena_bytes is
+// the arena's address span (best-fit offsets), live_high_water the live-bytes
+// high water of every buffer value replayed over the plan events, estimate
+// plan::estimate_peak at the arena alignment (256 B). live == estimate is the
+// reference's runtime high_water == estimate invariant (test_runtime.cpp:195-240).
+struct MemoryReport {
+    int64_t arena_bytes = 0, live_high_water = 0, estimate = 0;
+};
+MemoryReport memory_report(const plan::ExecutionPlan& inference_plan, Device* device = nullptr);
+
 class Trainer;
 void release(const plan::VersionPlans& plans);
 
@@ -172,6 +182,7 @@ struct Trainer {
     void* target_device_ptr();
     size_t arena_bytes() const;
     uint64_t launches_per_step() const;
+    MemoryReport memory_report() const;
     struct Impl;
     std::unique_ptr<Impl> impl;
 };

@@ -127,3 +127,24 @@ def test_offload_protocol_ac8():
     m.run({"x": x})
     s3 = P.sync_stats(reset=True)
     assert s3["weight_bytes"] == -(-w.size * 4 // 64) * 64
+
+
+@pytest.mark.parametrize("bn", [False, True])
+def test_device_memory_matches_static_estimate(bn):
+    """The reference's invariant runtime high_water == estimate_peak
+    (test_runtime.cpp:195-240) for the B200 bound programs: the live bytes of
+    every buffer value replayed over the events equal plan::estimate_peak at the
+    arena alignment, for inference and for the fused train_fwd + train_bwd
+    program; the arena's address span (best-fit offsets) is reported beside it."""
+    doc = W.c1_small_cnn(8, bn=bn)
+    x = W.uniform((8, 32, 32, 3), 1, "x")
+    t = W.uniform((8, 10), 2, "t")
+    m = P.CompiledModel(doc, precision=P.PREC_FP32)
+    m.run({"x": x})
+    inf = m.memory("inference")
+    assert inf["live_high_water"] == inf["estimate"] > 0
+    assert inf["arena_bytes"] >= inf["live_high_water"] - sum(-(-int(np.prod(s)) * 4 // 256) * 256
+                                                               for s in m.weight_shapes.values())
+    m.trainer_prepare({"x": x}, t)
+    tr = m.memory("training")
+    assert tr["live_high_water"] == tr["estimate"] > 0
