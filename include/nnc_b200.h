@@ -44,6 +44,10 @@ int nnc_model_set_input(nnc_model* m, const char* name, const float* data, const
 int nnc_model_set_input_borrowed(nnc_model* m, const char* name, const float* data, const int64_t* dims, int rank);
 
 /* role: 0 = inference plan, 1 = train_fwd plan (outputs include the SaveSet). */
+/* SOLP serialization of the compiled plans (ref plan.hpp:154-160: serialize_plan / load_plan), carrying
+   the B200 launch descriptors. save: out == NULL queries *size. load replaces the model's plans. */
+int nnc_model_save_plans(nnc_model* m, uint8_t* out, uint64_t capacity, uint64_t* size);
+int nnc_model_load_plans(nnc_model* m, const uint8_t* bytes, uint64_t n);
 int nnc_model_run(nnc_model* m, int role);
 /* nnc_model_run copying back only the comma-separated outputs `names` (ExecOptions::materialize). */
 int nnc_model_run_outputs(nnc_model* m, int role, const char* names);

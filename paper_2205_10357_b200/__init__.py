@@ -76,6 +76,8 @@ def _load():
         "nnc_model_arena_bytes": (U64, [P]),
         "nnc_model_infer_device": (I, [P]),
         "nnc_model_run_device": (I, [P, I]),
+        "nnc_model_save_plans": (I, [P, ctypes.c_char_p, U64, ctypes.POINTER(ctypes.c_uint64)]),
+        "nnc_model_load_plans": (I, [P, ctypes.c_char_p, U64]),
         "nnc_model_memory": (I, [P, I, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64),
                                  ctypes.POINTER(ctypes.c_uint64)]),
         "nnc_device_sync_stats": (I, [I, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64),
@@ -248,6 +250,19 @@ class CompiledModel:
 
     def launches_per_step(self) -> int:
         return int(_host.nnc_model_launches_per_step(self._h))
+
+    def save_plans(self) -> bytes:
+        """SOLP bytes of the compiled plans (deterministic)."""
+        n = ctypes.c_uint64()
+        _check(_host.nnc_model_save_plans(self._h, None, 0, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value)
+        _check(_host.nnc_model_save_plans(self._h, buf, n.value, ctypes.byref(n)))
+        return buf.raw[: n.value]
+
+    def load_plans(self, data: bytes):
+        """Replace the compiled plans with a SOLP stream (deploy path)."""
+        _check(_host.nnc_model_load_plans(self._h, data, len(data)))
+        self.describe = json.loads(_host.nnc_model_describe(self._h).decode())
 
     def memory(self, role: str = "training") -> Dict[str, int]:
         """Bound program memory vs the static planner (arena span, live high water, estimate)."""

@@ -198,6 +198,30 @@ int nnc_model_set_input_borrowed(nnc_model* m, const char* name, const float* da
     return guarded([&] { m->inputs.insert_or_assign(name, Tensor::view(DType::F32, std::vector<int64_t>(dims, dims + rank), data)); });
 }
 
+int nnc_model_save_plans(nnc_model* m, uint8_t* out, uint64_t capacity, uint64_t* size) {
+    return guarded([&] {
+        // SOLP stream of the three role plans (ref plan.cpp:633-848 plus B200 launch descriptors);
+        // call with out == nullptr to query the size
+        std::vector<uint8_t> b = plan::serialize_version_plans(m->plans);
+        *size = b.size();
+        if (out) {
+            if (capacity < b.size()) throw Error(Error::Code::ShapeMismatch, "save_plans: buffer too small");
+            std::memcpy(out, b.data(), b.size());
+        }
+    });
+}
+
+int nnc_model_load_plans(nnc_model* m, const uint8_t* bytes, uint64_t n) {
+    return guarded([&] {
+        plan::VersionPlans v = plan::load_version_plans(std::vector<uint8_t>(bytes, bytes + n));
+        for (const std::string& w : v.inference.weight_names)
+            if (!m->host->has(w)) throw Error(Error::Code::BadDocument, "load_plans: plan weight " + w + " is not in the model");
+        m->trainer = nullptr;
+        runtime::release(m->plans);
+        m->plans = std::move(v);
+    });
+}
+
 int nnc_model_run(nnc_model* m, int role) {
     const int rc = guarded([&] {
         const plan::ExecutionPlan& p = role == 1 ? m->plans.train_fwd : m->plans.inference;

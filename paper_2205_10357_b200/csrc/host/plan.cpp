@@ -435,14 +435,18 @@ struct Lowering {
 
 }  // namespace
 
+uint64_t next_plan_uid() {
+    static std::atomic<uint64_t> next_uid{1};
+    return next_uid.fetch_add(1);
+}
+
 ExecutionPlan compile_plan(const Graph& input_graph, const std::vector<FusionGroup>& groups, PlanRole role,
                            const autodiff::VersionSet* versions) {
     Graph g = passes::infer_shapes(input_graph).graph;
     if ((role == PlanRole::TrainFwd || role == PlanRole::TrainBwd) && !versions)
         throw Error(Error::Code::BadDocument, "training plans need the version set");
-    static std::atomic<uint64_t> next_uid{1};
     ExecutionPlan plan;
-    plan.uid = next_uid.fetch_add(1);
+    plan.uid = next_plan_uid();
     plan.dtype = g.dtype;
     plan.role = role;
     std::unordered_map<std::string, uint32_t> slot_of;

@@ -124,6 +124,20 @@ VersionPlans compile_version_set(
     const autodiff::VersionSet& versions,
     const std::function<backends::BackendAssignment(const hlir::Graph&)>& assign);
 
+// Process-unique plan id (runtime caches key on it).
+uint64_t next_plan_uid();
+
+/* ------------------------------------------------------------------ */
+/*  Serialization (SOLP; ref plan.hpp:154-160) with B200 descriptors    */
+/* ------------------------------------------------------------------ */
+std::vector<uint8_t> serialize_plan(const ExecutionPlan& p);
+ExecutionPlan load_plan(const std::vector<uint8_t>& bytes);
+ExecutionPlan load_plan_file(const std::string& path);
+void save_plan_file(const ExecutionPlan& p, const std::string& path);
+// The three role plans plus the version-set maps, one stream.
+std::vector<uint8_t> serialize_version_plans(const VersionPlans& v);
+VersionPlans load_version_plans(const std::vector<uint8_t>& bytes);
+
 struct PeakEstimate {
     int64_t inference_bytes = 0;
     int64_t training_bytes = 0;

@@ -148,3 +148,19 @@ def test_device_memory_matches_static_estimate(bn):
     m.trainer_prepare({"x": x}, t)
     tr = m.memory("training")
     assert tr["live_high_water"] == tr["estimate"] > 0
+
+
+def test_solp_loaded_plans_execute_bitwise():
+    """Deploy path: plans serialized to SOLP and loaded into a fresh model run
+    bitwise-identically to the compiled ones (ref test_backends.cpp:308-333)."""
+    doc = W.c1_small_cnn(8, bn=True)
+    x = W.uniform((8, 32, 32, 3), 1, "x")
+    t = W.uniform((8, 10), 2, "t")
+    a = P.CompiledModel(doc, precision=P.PREC_FP32)
+    b = P.CompiledModel(doc, precision=P.PREC_FP32)
+    b.load_plans(a.save_plans())
+    ra, rb = a.run({"x": x}), b.run({"x": x})
+    assert ra.keys() == rb.keys() and all(np.array_equal(ra[k], rb[k]) for k in ra)
+    la, ga = a.gradients({"x": x}, t)
+    lb, gb = b.gradients({"x": x}, t)
+    assert la == lb and all(np.array_equal(ga[k], gb[k]) for k in ga)

@@ -119,3 +119,20 @@ def test_peak_estimate_counts_registers_as_zero():
     d = P.CompiledModel(W.c2_chain((2, 4, 4, 8), "ref")).describe
     # inputs x,y + output only; the 15 chain interiors live in registers
     assert d["peak"]["inference"] == 3 * 2 * 4 * 4 * 8 * 4
+
+
+def test_solp_plan_serialization_round_trip():
+    """SOLP plan format with B200 launch descriptors (ref plan.hpp:154-160,
+    test_backends.cpp:308-333): deterministic bytes, recompiling gives the same
+    bytes, load then save is the identity, and foreign streams are rejected."""
+    doc = W.c1_small_cnn(4, bn=True)
+    a, b = P.CompiledModel(doc, precision=P.PREC_TF32), P.CompiledModel(doc, precision=P.PREC_TF32)
+    bytes1 = a.save_plans()
+    assert bytes1[:4] == b"SOLV" and a.save_plans() == bytes1
+    assert b.save_plans() == bytes1
+    b.load_plans(bytes1)
+    assert b.save_plans() == bytes1
+    assert b.describe["train_bwd"]["launch_count"] == a.describe["train_bwd"]["launch_count"]
+    for junk in (b"SOLX\x01\x00\x00\x00", bytes1[:-3], b"SOLV" + bytes1[4:12]):
+        with pytest.raises(P.NNCError):
+            b.load_plans(junk)
