@@ -65,6 +65,7 @@ struct TcParams {
     int64_t M;          // rows of C = taps * ci
     int ci, kw_;        // for (tap, c) = divmod(m, ci); tap -> (dh, dw)
     int dil_w;          // horizontal tap dilation (space-to-depth packing); 1 otherwise
+    int bt;             // MODE_CONV forward with K-major (transposed) weights: B box at (tap*ci + c0, n0)
     int sh, sw, pt, pl;
     int kboxes;         // pixel boxes (TN*TH*TW == 32 pixels each)
     int splits;
@@ -201,6 +202,13 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
 // operands must use SWIZZLE_128B_BASE32B (layout type 1: 32-byte granules, 4-row
 // atoms, SBO = 512 B between K-row groups, LBO = stride between 32-element MN
 // chunks) -- the only MN-major layout tcgen05 accepts for 32-bit operands.
+// true in exactly one lane of the (fully active) warp
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+    return pred != 0;
+}
+
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes, uint32_t layout) {
     uint64_t d = 0;
     d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
@@ -558,6 +566,8 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                     if (!MA) ld4(sa, &map_a, bar, c0, xw, yh, T.tn0);
                     if (P.b_mn) {
                         for (int q = 0; q < bcols / 32; ++q) ld2(sb + q * 4096, &map_b, bar, n0 + 32 * q, br + c0);
+                    } else if (P.bt) {
+                        ld2(sb, &map_b, bar, br + c0, n0);   // transposed forward weights [co][kh*kw*ci]
                     } else {
                         ld2(sb, &map_b, bar, c0, br + n0);   // box rows = bcols (encoded on the host)
                     }
@@ -605,12 +615,23 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                 }
             }
         }
-    } else if (warp == 1 && lane == 0 && (!PAIR || rank == 0)) {
-        // ================= MMA issuer (single thread; PAIR: the leader CTA only) =================
+    } else if (warp == 1 && (!PAIR || rank == 0)) {
+        // ================= MMA issuer (PAIR: the leader CTA only) =================
+        // The whole warp walks the loop, so every value is provably warp-uniform
+        // (uniform registers, no per-MMA waterfall loop), and one elected lane
+        // issues. Descriptors are a hoisted base plus additive stage / k offsets
+        // (the 14-bit start-address field, in 16-byte units, cannot carry: smem
+        // offsets stay below 256 KB).
         const uint32_t a_mn = (P.mode == MODE_WGRAD && !MA) ? 1u : 0u;
         const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (a_mn << 15) |
                                (static_cast<uint32_t>(P.b_mn) << 16) | ((static_cast<uint32_t>(P.bn) >> 3) << 17) |
                                ((static_cast<uint32_t>(PAIR ? 2 * BM : BM) >> 4) << 24);
+        const uint32_t s0 = smem_u32(smem);
+        const uint64_t adesc0 = a_mn ? sdesc(s0, 4096, 512, 1) : sdesc(s0, 16, 1024, 2);
+        const uint64_t bdesc0 = P.b_mn ? sdesc(s0 + a_bytes, 4096, 512, 1) : sdesc(s0 + a_bytes, 16, 1024, 2);
+        const uint64_t a_kstep = a_mn ? (1024 >> 4) : (32 >> 4), b_kstep = P.b_mn ? (1024 >> 4) : (32 >> 4);
+        const uint64_t stage16 = stage_bytes >> 4;
+        const bool leader = elect_one();
         int slot = 0;
         uint32_t phase = 0, local = 0;
         for (int64_t t = t_begin; t < P.tiles; t += t_step, ++local) {
@@ -627,26 +648,30 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                 if (MA) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // cp.async data -> async proxy
                 if (++slot == STAGES) { slot = 0; phase ^= 1u; }
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t sa = smem_u32(smem + s * stage_bytes);
-                const uint32_t sb = sa + a_bytes;
+                if (leader) {
+                    const uint64_t so = static_cast<uint64_t>(s) * stage16;
 #pragma unroll
-                for (int kk = 0; kk < BK / 8; ++kk) {
-                    const uint64_t ad = a_mn ? sdesc(sa + kk * 1024, 4096, 512, 1) : sdesc(sa + kk * 32, 16, 1024, 2);
-                    const uint64_t bd = P.b_mn ? sdesc(sb + kk * 1024, 4096, 512, 1) : sdesc(sb + kk * 32, 16, 1024, 2);
+                    for (int kk = 0; kk < BK / 8; ++kk) {
+                        const uint64_t ad = adesc0 + so + kk * a_kstep, bd = bdesc0 + so + kk * b_kstep;
+                        if (PAIR)
+                            mma_tf32_pair(d, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                        else
+                            mma_tf32(d, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                    }
                     if (PAIR)
-                        mma_tf32_pair(d, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                        mma_commit_pair(&empty[s]);   // frees the stage in both CTAs
                     else
-                        mma_tf32(d, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                        mma_commit(&empty[s]);
                 }
-                if (PAIR)
-                    mma_commit_pair(&empty[s]);   // frees the stage in both CTAs
-                else
-                    mma_commit(&empty[s]);
+                __syncwarp();
             }
-            if (PAIR)
-                mma_commit_pair(&tmem_full[acc]);
-            else
-                mma_commit(&tmem_full[acc]);
+            if (leader) {
+                if (PAIR)
+                    mma_commit_pair(&tmem_full[acc]);
+                else
+                    mma_commit(&tmem_full[acc]);
+            }
+            __syncwarp();
         }
     } else if (MA && warp >= 10) {
         // ================= A builders (warps 10..13, MA only) =================
@@ -896,6 +921,7 @@ thread_local int g_force_bn = 0;     // set by the autotuner (gemm_tc) for one c
 thread_local int g_force_pair = 0;   // 1: run the call as CTA pairs (cta_group::2)
 thread_local int g_force_wide = 0;   // 1: full-width (32-column) epilogue staging even at 2 CTAs/SM
 thread_local int g_dil_w = 1;        // horizontal tap dilation for the next implicit GEMM (internal)
+thread_local int g_force_tb = 0;     // 1: forward convolution with transposed (K-major) weights
 
 int pick_bn(int64_t n) {
     static const int env_bn = getenv("NNCB_TC_BN") ? atoi(getenv("NNCB_TC_BN")) : 0;   // tuning knob
@@ -1289,6 +1315,10 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
             if (N > 128) cands.push_back(0x10000 | 256);
         }
         cands.push_back(0x20000 | 128);   // bit 17: 128-wide tiles with full-width staging
+        if (d->kind == NNCB_CONV_FWD || d->kind == NNCB_DENSE_FWD) {   // bit 18: K-major (transposed) weights
+            const size_t nb = cands.size();
+            for (size_t ci_ = 0; ci_ < nb; ++ci_) cands.push_back(cands[ci_] | 0x40000);
+        }
         cudaEvent_t e0, e1;
         NNCB_CUDA(cudaEventCreate(&e0));
         NNCB_CUDA(cudaEventCreate(&e1));
@@ -1297,11 +1327,13 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
             g_force_bn = c & 0xffff;
             g_force_pair = (c >> 16) & 1;
             g_force_wide = (c >> 17) & 1;
+            g_force_tb = (c >> 18) & 1;
             int rc = gemm_tc_route(ctx, d, a, b, bias, out, handled);   // warm-up (and validity)
             if (rc || !*handled) {
                 g_force_bn = 0;
                 g_force_pair = 0;
                 g_force_wide = 0;
+                g_force_tb = 0;
                 cudaEventDestroy(e0);
                 cudaEventDestroy(e1);
                 return rc;
@@ -1312,6 +1344,7 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
             g_force_bn = 0;
             g_force_pair = 0;
             g_force_wide = 0;
+            g_force_tb = 0;
             if (rc) {
                 cudaEventDestroy(e0);
                 cudaEventDestroy(e1);
@@ -1333,10 +1366,12 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
     g_force_bn = choice & 0xffff;
     g_force_pair = (choice >> 16) & 1;
     g_force_wide = (choice >> 17) & 1;
+    g_force_tb = (choice >> 18) & 1;
     const int rc = gemm_tc_route(ctx, d, a, b, bias, out, handled);
     g_force_bn = 0;
     g_force_pair = 0;
     g_force_wide = 0;
+    g_force_tb = 0;
     return rc;
 }
 
@@ -1379,6 +1414,21 @@ int gemm_tc_route(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const 
         return rc;
     }
     return gemm_tc_impl(ctx, d, a, 0, b, bias, out, handled);
+}
+
+// W[rows][cols] -> Wt[cols][rows], 32x32 shared-memory tiles (coalesced both ways)
+__global__ void transpose_k(const float* __restrict__ w, float* __restrict__ wt, int rows, int cols) {
+    __shared__ float tile[32][33];
+    const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+    for (int j = threadIdx.y; j < 32; j += 8) {
+        const int r = by + j, c = bx + threadIdx.x;
+        if (r < rows && c < cols) tile[j][threadIdx.x] = w[static_cast<int64_t>(r) * cols + c];
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += 8) {
+        const int c = bx + j, r = by + threadIdx.x;
+        if (r < rows && c < cols) wt[static_cast<int64_t>(c) * rows + r] = tile[threadIdx.x][j];
+    }
 }
 
 int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t lda, const float* b,
@@ -1489,7 +1539,19 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
             if (!encode_4d(&ma, act, co, ow, oh, n, 32, P.TW, P.TH, P.TN, 1, 1, false)) return 1;
         }
         // B: weights [kh*kw*ci, co]
-        if (fwd) {
+        const int64_t kfull = kh * kw * ci;
+        if (fwd && g_force_tb && !manual && kfull % 4 == 0) {
+            // K-major copy [co][kh*kw*ci]: the tensor core reads K-major tf32
+            // operands faster than MN-major ones (measured fwd vs dgrad)
+            float* wt = static_cast<float*>(wt_buffer(ctx, sizeof(float) * kfull * co));
+            if (!wt) return fail("conv fwd: transposed-weight buffer allocation failed");
+            transpose_k<<<dim3((unsigned)((co + 31) / 32), (unsigned)((kfull + 31) / 32)), dim3(32, 8), 0, ctx->stream>>>(
+                b, wt, (int)kfull, (int)co);
+            NNCB_LAUNCHED(ctx);
+            P.b_mn = 0;
+            P.bt = 1;
+            if (!encode_2d(&mb, wt, kfull, co, BK, P.pair ? P.bn / 2 : P.bn, false)) return 1;
+        } else if (fwd) {
             P.b_mn = 1;
             if (!encode_2d(&mb, b, co, kh * kw * ci, 32, BK, true)) return 1;
         } else {

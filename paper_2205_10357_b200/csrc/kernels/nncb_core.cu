@@ -29,6 +29,18 @@ void* scratch(nncb_ctx* ctx, size_t bytes) {
     return ctx->scratch;
 }
 
+void* wt_buffer(nncb_ctx* ctx, size_t bytes) {
+    if (bytes <= ctx->wt_bytes) return ctx->wt;
+    if (ctx->wt) ctx->retired.push_back(ctx->wt);   // captured graphs may still reference it
+    if (cudaMalloc(&ctx->wt, bytes) != cudaSuccess) {
+        ctx->wt = nullptr;
+        ctx->wt_bytes = 0;
+        return nullptr;
+    }
+    ctx->wt_bytes = bytes;
+    return ctx->wt;
+}
+
 void* workspace(nncb_ctx* ctx, size_t bytes) {
     if (bytes <= ctx->workspace_bytes) return ctx->workspace;
     if (ctx->workspace) ctx->retired.push_back(ctx->workspace);
@@ -81,6 +93,7 @@ int nncb_destroy(nncb_ctx* c) {
     if (c->scratch) cudaFree(c->scratch);
     for (void* p : c->retired) cudaFree(p);
     if (c->workspace) cudaFree(c->workspace);
+    if (c->wt) cudaFree(c->wt);
     cudaStreamDestroy(c->stream);
     cudaStreamDestroy(c->comm_stream);
     delete c;

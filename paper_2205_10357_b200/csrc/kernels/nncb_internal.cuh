@@ -31,12 +31,15 @@ struct nncb_ctx {
     void* workspace = nullptr;           // im2col columns (separate from reduction scratch)
     size_t workspace_bytes = 0;
     void* staging = nullptr;             // pinned upload ring (host_io.cu), created on first large h2d
+    void* wt = nullptr;                  // transposed (K-major) forward weights, grown on demand
+    size_t wt_bytes = 0;
 };
 
 namespace nncb {
 
 void set_error(const std::string& msg);
 void staging_release(nncb_ctx* c);
+void* wt_buffer(nncb_ctx* ctx, size_t bytes);
 int fail(const std::string& msg);
 
 #define NNCB_CUDA(expr)                                                                       \

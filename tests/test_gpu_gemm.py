@@ -195,3 +195,28 @@ def test_cta_pair_dense(b, i, o, tile):
             check(tc, ex)
     finally:
         K.nncb_gemm_force_tile(0)
+
+
+@pytest.mark.parametrize("tile", [0x40000 | 128, 0x40000 | 256, 0x50000 | 256, 0x60000 | 128])
+@pytest.mark.parametrize("shape", [(2, 14, 14, 64, 64, 3, 1), (2, 13, 11, 64, 96, 3, 2), (4, 7, 7, 128, 256, 1, 1),
+                                   (3, 8, 8, 96, 128, 3, 1)])
+def test_conv_fwd_transposed_weights(shape, tile):
+    """Forward convolution with the weights transposed to K-major on the fly
+    (autotune bit 18), alone and with CTA pairs / wide staging."""
+    n, ih, iw, ci, co, k, s = shape
+    g = conv_geom(n, ih, iw, ci, co, k, s)
+    rng = np.random.default_rng(9)
+    x = rng.uniform(-1, 1, (n, ih, iw, ci)).astype(np.float32)
+    w = rng.uniform(-1, 1, (k, k, ci, co)).astype(np.float32)
+    bias = rng.uniform(-1, 1, co).astype(np.float32)
+    K.nncb_gemm_force_tile(tile)
+    try:
+        tc, ex = run_both(CONV_FWD, g, Dev(x), Dev(w), Dev(bias), (n, g["oh"], g["ow"], co), expect_tc=True)
+        check(tc, ex)
+        geo = dict(batch=37, in_f=ci, out_f=co)
+        xd = rng.uniform(-1, 1, (37, ci)).astype(np.float32)
+        wd = rng.uniform(-1, 1, (ci, co)).astype(np.float32)
+        tc, ex = run_both(DENSE_FWD, geo, Dev(xd), Dev(wd), Dev(bias), (37, co), expect_tc=True)
+        check(tc, ex)
+    finally:
+        K.nncb_gemm_force_tile(0)

@@ -40,11 +40,12 @@ def main():
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--layers", default="")
     ap.add_argument("--colstats", action="store_true", help="forward GEMMs also accumulate BN column statistics")
-    ap.add_argument("--tile", default="auto", help="auto | 128 | 256 | p128 | p256 | w128 (p = CTA pair, w = wide staging)")
+    ap.add_argument("--tile", default="auto", help="auto | 128 | 256 | p128 | p256 | w128 | t128 | tp256 ... (p = CTA pair, w = wide staging, t = K-major weights)")
     a = ap.parse_args()
     timer = P.DeviceTimer()
     if a.tile != "auto":
-        code = int(a.tile.lstrip("pw")) | (0x10000 if a.tile.startswith("p") else 0) | (0x20000 if a.tile.startswith("w") else 0)
+        t = a.tile
+        code = int(t.lstrip("pwt")) | (0x10000 if "p" in t else 0) | (0x20000 if "w" in t else 0) | (0x40000 if "t" in t else 0)
         K.nncb_gemm_force_tile(code)
     total = {}
     for name, h, ci, co, k, s in LAYERS:
