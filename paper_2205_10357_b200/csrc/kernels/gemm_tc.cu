@@ -1306,15 +1306,16 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
     }
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(ctx->stream, &cap);
-    if (!choice && enabled && N > 64 && cap == cudaStreamCaptureStatusNone) {
+    if (!choice && enabled && cap == cudaStreamCaptureStatusNone) {
         // bit 16: CTA pair (cta_group::2, 256-row tiles over two SMs)
         static const bool pairs = !(getenv("NNCB_TC_PAIR") && atoi(getenv("NNCB_TC_PAIR")) == 0);
-        std::vector<int> cands = N <= 128 ? std::vector<int>{64, 128} : std::vector<int>{128, 256};
+        std::vector<int> cands = N <= 64 ? std::vector<int>{64} : N <= 128 ? std::vector<int>{64, 128}
+                                                                            : std::vector<int>{128, 256};
         if (pairs) {
-            cands.push_back(0x10000 | 128);
+            cands.push_back(0x10000 | (N <= 64 ? 64 : 128));
             if (N > 128) cands.push_back(0x10000 | 256);
         }
-        cands.push_back(0x20000 | 128);   // bit 17: 128-wide tiles with full-width staging
+        cands.push_back(0x20000 | (N <= 64 ? 64 : 128));   // bit 17: full-width staging at 2 CTAs/SM
         if (d->kind == NNCB_CONV_FWD || d->kind == NNCB_DENSE_FWD) {   // bit 18: K-major (transposed) weights
             const size_t nb = cands.size();
             for (size_t ci_ = 0; ci_ < nb; ++ci_) cands.push_back(cands[ci_] | 0x40000);
