@@ -149,6 +149,14 @@ enum nncb_epilogue {
      * colstats[0:N] / colstats[N:2N] -- BatchNorm statistics fused into the
      * producing GEMM. The GEMM zeroes the accumulator itself.               */
     NNCB_EPI_COLSTATS = 4,
+    /* The stored value is the gradient at the input of the ReLU that follows
+     * this GEMM's consumer (dgrad epilogue fusion): dy = eg_mask[i] > 0 ?
+     * acc (+ eg_res[i]) : 0, eg_mask / eg_res laid out like the output. The
+     * BatchNorm backward sums of dy are accumulated alongside (double):
+     * eg_sums[0:N] += dy, eg_sums[N:2N] += dy * (eg_x[i] - mean) * invstd with
+     * eg_stats = [mean; invstd] (2N floats); the GEMM zeroes eg_sums.
+     * Tensor-core path only (returns unhandled otherwise).                   */
+    NNCB_EPI_RELU_GRAD = 8,
 };
 
 typedef struct {
@@ -159,7 +167,16 @@ typedef struct {
     int64_t batch, in_f, out_f;
     /* NNCB_EPI_COLSTATS accumulator: 2*N doubles */
     double* colstats;
+    /* NNCB_EPI_RELU_GRAD operands (see above); eg_res may be NULL */
+    const float* eg_mask;
+    const float* eg_res;
+    const float* eg_x;
+    const float* eg_stats;
+    double* eg_sums;
 } nncb_gemm_desc;
+
+/* float32 sums[0:C] -> out0, sums[C:2C] -> out1 (finalize of NNCB_EPI_RELU_GRAD sums). */
+int nncb_colsums_to_float(nncb_ctx* ctx, const double* sums, float* out0, float* out1, int64_t C);
 
 /* FWD:   a = x, b = weight, out = y (bias optional)
  * DGRAD: a = g, b = weight, out = gx

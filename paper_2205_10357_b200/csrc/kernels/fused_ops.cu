@@ -880,6 +880,24 @@ int nncb_bn_stats(nncb_ctx* ctx, const float* x, float* stats, int64_t rows, int
     return col_reduce<1>(ctx, x, nullptr, nullptr, rows, C, eps, stats, nullptr);
 }
 
+namespace {
+__global__ void colsums_to_float_k(const double* __restrict__ s, float* __restrict__ o0, float* __restrict__ o1,
+                                   int64_t C) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c < C) {
+        o0[c] = static_cast<float>(s[c]);
+        o1[c] = static_cast<float>(s[C + c]);
+    }
+}
+}  // namespace
+
+int nncb_colsums_to_float(nncb_ctx* ctx, const double* sums, float* out0, float* out1, int64_t C) {
+    if (C <= 0) return 0;
+    colsums_to_float_k<<<(unsigned)((C + 255) / 256), 256, 0, ctx->stream>>>(sums, out0, out1, C);
+    NNCB_LAUNCHED(ctx);
+    return 0;
+}
+
 int nncb_bn_finalize(nncb_ctx* ctx, const double* colstats, float* stats, int64_t rows, int64_t C, double eps) {
     if (C <= 0) return 0;
     bn_finalize_k<<<(unsigned)((C + 127) / 128), 128, 0, ctx->stream>>>(colstats, stats, rows, C, eps);

@@ -245,6 +245,8 @@ extern "C" int nncb_gemm(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a,
         g_last_path = 1;
         if (rc || handled) return rc;
     }
+    if (d->epilogue & NNCB_EPI_RELU_GRAD)
+        return nncb::fail("nncb_gemm: NNCB_EPI_RELU_GRAD is a tensor-core epilogue (tf32 precision, TMA-eligible shape)");
     g_last_path = 0;
     if (int rc = nncb::gemm_simt(ctx, d, a, b, bias, out)) return rc;
     if (colstats) {

@@ -66,6 +66,12 @@ struct TcParams {
     int ci, kw_;        // for (tap, c) = divmod(m, ci); tap -> (dh, dw)
     int dil_w;          // horizontal tap dilation (space-to-depth packing); 1 otherwise
     int bt;             // MODE_CONV forward with K-major (transposed) weights: B box at (tap*ci + c0, n0)
+    // --- gradient epilogue (NNCB_EPI_RELU_GRAD; requires the CS build, colstats = eg sums) ---
+    int eg;
+    const float* eg_mask;
+    const float* eg_res;
+    const float* eg_x;
+    const float* eg_stats;
     int sh, sw, pt, pl;
     int kboxes;         // pixel boxes (TN*TH*TW == 32 pixels each)
     int splits;
@@ -309,7 +315,7 @@ struct TmaOut {
 template <int CH, bool CS>
 __device__ __forceinline__ void store_chunk_t(const uint32_t (&r)[32], uint8_t* tile, float* dst, bool valid,
                                               int col0, int N, bool full_cols, int lane, bool store, float& cs1,
-                                              float& cs2, const TmaOut& to) {
+                                              float& cs2, const TmaOut& to, const TcParams& P) {
     constexpr int COLS = CH * 4, RPI = 32 / CH;   // columns per pass, rows per store instruction
     const uint32_t vmask = CS ? __ballot_sync(0xffffffffu, valid) : 0u;
 #pragma unroll
@@ -328,15 +334,43 @@ __device__ __forceinline__ void store_chunk_t(const uint32_t (&r)[32], uint8_t* 
             constexpr int RPL = COLS;              // rows per lane: 32 rows over 32/COLS lane groups
             const int col = lane % COLS, r0 = (lane / COLS) * RPL;
             float s1 = 0.f, s2 = 0.f;
+            // gradient epilogue: lane (col, row group) turns the staged GEMM
+            // result into dy = mask > 0 ? acc (+ res) : 0 in place, reading the
+            // rows' mask / residual / x values coalesced (a row's 32 columns are
+            // one 128-byte segment), and sums dy and dy * xhat for BatchNorm
+            const int cg = col0 + p * COLS + col;
+            const int64_t doff = P.eg ? static_cast<int64_t>(dst - P.out) : 0;   // this lane's row, output layout
+            float em = 0.f, es = 0.f;
+            if (P.eg && cg < N) {
+                em = __ldg(P.eg_stats + cg);
+                es = __ldg(P.eg_stats + N + cg);
+            }
 #pragma unroll
             for (int i = 0; i < RPL; ++i) {
                 const int rr = r0 + i;
-                const float v = *reinterpret_cast<const float*>(tile + rr * (CH * 16) + (swz<CH>(col >> 2, rr) << 4) +
-                                                                (col & 3) * 4);
-                const float m = ((vmask >> rr) & 1u) ? v : 0.f;
-                s1 += m;
-                s2 = fmaf(m, m, s2);
+                float* tp = reinterpret_cast<float*>(tile + rr * (CH * 16) + (swz<CH>(col >> 2, rr) << 4) + (col & 3) * 4);
+                const float v = *tp;
+                const bool rv = (vmask >> rr) & 1u;
+                if (P.eg) {
+                    const int64_t off = __shfl_sync(0xffffffffu, static_cast<long long>(doff), rr);
+                    float dy = 0.f, xh = 0.f;
+                    if (rv && cg < N) {
+                        const int64_t e = off + cg;
+                        float gsum = v;
+                        if (P.eg_res) gsum = __fadd_rn(gsum, __ldg(P.eg_res + e));
+                        dy = __ldg(P.eg_mask + e) > 0.f ? gsum : 0.f;
+                        xh = (__ldg(P.eg_x + e) - em) * es;
+                    }
+                    *tp = dy;
+                    s1 += dy;
+                    s2 = fmaf(dy, xh, s2);
+                } else {
+                    const float m = rv ? v : 0.f;
+                    s1 += m;
+                    s2 = fmaf(m, m, s2);
+                }
             }
+            if (P.eg) __syncwarp();   // dy written back before the stores read the tile
 #pragma unroll
             for (int sh = COLS; sh < 32; sh <<= 1) {
                 s1 += __shfl_xor_sync(0xffffffffu, s1, sh);
@@ -820,11 +854,11 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                     const bool st = !P.nostore;
                     float c1 = 0.f, c2 = 0.f;
                     if (P.stg_cols == 32)
-                        store_chunk_t<8, CS>(r, tile, dst, valid, col0, P.N, full_cols, lane, st, c1, c2, to);
+                        store_chunk_t<8, CS>(r, tile, dst, valid, col0, P.N, full_cols, lane, st, c1, c2, to, P);
                     else if (P.stg_cols == 16)
-                        store_chunk_t<4, CS>(r, tile, dst, valid, col0, P.N, full_cols, lane, st, c1, c2, to);
+                        store_chunk_t<4, CS>(r, tile, dst, valid, col0, P.N, full_cols, lane, st, c1, c2, to, P);
                     else
-                        store_chunk_t<2, CS>(r, tile, dst, valid, col0, P.N, full_cols, lane, st, c1, c2, to);
+                        store_chunk_t<2, CS>(r, tile, dst, valid, col0, P.N, full_cols, lane, st, c1, c2, to, P);
                     if (CS) {
                         cs_sum[k] += static_cast<double>(c1);
                         cs_sq[k] += static_cast<double>(c2);
@@ -1562,6 +1596,16 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
         P.bias = (fwd && (d->epilogue & NNCB_EPI_BIAS)) ? bias : nullptr;
         P.out = out;
         P.colstats = (fwd && (d->epilogue & NNCB_EPI_COLSTATS)) ? d->colstats : nullptr;
+        if (d->epilogue & NNCB_EPI_RELU_GRAD) {
+            if (!d->eg_mask || !d->eg_x || !d->eg_stats || !d->eg_sums || P.colstats)
+                return fail("gemm: NNCB_EPI_RELU_GRAD needs eg_mask, eg_x, eg_stats, eg_sums (and no COLSTATS)");
+            P.eg = 1;
+            P.eg_mask = d->eg_mask;
+            P.eg_res = d->eg_res;
+            P.eg_x = d->eg_x;
+            P.eg_stats = d->eg_stats;
+            P.colstats = d->eg_sums;   // the CS build accumulates the dy sums
+        }
         if (P.colstats) NNCB_CUDA(cudaMemsetAsync(P.colstats, 0, sizeof(double) * 2 * Nc, ctx->stream));
         P.n_tiles = (Nc + P.bn - 1) / P.bn;
         P.pix_tiles = tiles;

@@ -14,7 +14,8 @@ class GemmDesc(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in ("kind", "precision", "epilogue", "_pad")] + \
                [(n, ctypes.c_int64) for n in ("n", "ih", "iw", "ci", "co", "kh", "kw", "sh", "sw", "oh", "ow",
                                               "pad_top", "pad_left", "batch", "in_f", "out_f")] + \
-               [("colstats", ctypes.c_void_p)]
+               [("colstats", ctypes.c_void_p), ("eg_mask", ctypes.c_void_p), ("eg_res", ctypes.c_void_p),
+                ("eg_x", ctypes.c_void_p), ("eg_stats", ctypes.c_void_p), ("eg_sums", ctypes.c_void_p)]
 
 
 for name, res, args in [

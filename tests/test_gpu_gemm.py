@@ -5,7 +5,7 @@ strided / padded convolutions and ragged tile edges. Bound: 2e-2 of max|ref|
 import numpy as np
 import pytest
 
-from tests.nncb_ctypes import K, Dev, GemmDesc, gemm
+from tests.nncb_ctypes import K, Dev, GemmDesc, ctx, gemm
 
 pytestmark = pytest.mark.gpu
 
@@ -220,3 +220,49 @@ def test_conv_fwd_transposed_weights(shape, tile):
         check(tc, ex)
     finally:
         K.nncb_gemm_force_tile(0)
+
+
+@pytest.mark.parametrize("res", [False, True])
+@pytest.mark.parametrize("shape,tile", [((2, 14, 14, 64, 64, 3, 1), 0), ((4, 7, 7, 128, 256, 1, 1), 0),
+                                        ((2, 13, 11, 64, 96, 3, 2), 0), ((3, 8, 8, 96, 128, 3, 1), 0x10000 | 256),
+                                        ((2, 16, 16, 64, 32, 1, 1), 0)])
+def test_dgrad_relu_grad_epilogue(shape, tile, res):
+    """Dgrad epilogue that emits the gradient at the input of the following
+    ReLU (dy = mask > 0 ? acc (+ residual) : 0) with the BatchNorm backward sums
+    of dy (NNCB_EPI_RELU_GRAD), against the exact dgrad + numpy."""
+    n, ih, iw, ci, co, k, s = shape
+    g = conv_geom(n, ih, iw, ci, co, k, s)
+    rng = np.random.default_rng(21)
+    gy = rng.uniform(-1, 1, (n, g["oh"], g["ow"], co)).astype(np.float32)
+    w = rng.uniform(-1, 1, (k, k, ci, co)).astype(np.float32)
+    mask = np.maximum(rng.uniform(-1, 1, (n, ih, iw, ci)), 0).astype(np.float32)
+    resid = rng.uniform(-1, 1, (n, ih, iw, ci)).astype(np.float32) if res else None
+    x = rng.uniform(-2, 2, (n, ih, iw, ci)).astype(np.float32)
+    stats = np.concatenate([rng.uniform(-0.5, 0.5, ci), rng.uniform(0.5, 2, ci)]).astype(np.float32)
+    gyd, wd = Dev(gy), Dev(w)
+    ex = Dev(nbytes=mask.nbytes)
+    gemm(GemmDesc(kind=CONV_DGRAD, precision=1, epilogue=0, **g), gyd, wd, None, ex)
+    exact = ex.get(mask.shape).astype(np.float64)
+    md, xd, sd = Dev(mask), Dev(x), Dev(stats)
+    rd = Dev(resid) if res else None
+    sums, out = Dev(nbytes=2 * ci * 8), Dev(nbytes=mask.nbytes)
+    d = GemmDesc(kind=CONV_DGRAD, precision=0, epilogue=8, **g)
+    d.eg_mask, d.eg_x, d.eg_stats, d.eg_sums = md.p, xd.p, sd.p, sums.p
+    d.eg_res = rd.p if res else None
+    K.nncb_gemm_force_tile(tile)
+    try:
+        gemm(d, gyd, wd, None, out)
+        assert K.nncb_gemm_last_path() == 1
+    finally:
+        K.nncb_gemm_force_tile(0)
+    want = np.where(mask > 0, exact + (resid if res else 0), 0.0)
+    got = out.get(mask.shape)
+    assert np.max(np.abs(got - want)) <= 2e-2 * np.max(np.abs(want))
+    raw = np.empty(2 * ci, np.float64)
+    assert K.nncb_d2h(ctx(), raw.ctypes.data, sums.p, raw.nbytes) == 0
+    K.nncb_sync(ctx())
+    xhat = (x.astype(np.float64) - stats[:ci]) * stats[ci:]
+    s1 = want.reshape(-1, ci).sum(0)
+    s2 = (want * xhat).reshape(-1, ci).sum(0)
+    assert np.linalg.norm(raw[:ci] - s1) <= 2e-2 * np.linalg.norm(s1)
+    assert np.linalg.norm(raw[ci:] - s2) <= 2e-2 * np.linalg.norm(s2)
