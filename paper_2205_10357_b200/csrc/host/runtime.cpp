@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -125,6 +126,9 @@ struct BoundLaunch {
     double eps = 0;
     int flag0 = 0, flag1 = 0;
     bool skip = false;                      // work absorbed by another launch (fused reduction)
+    // Gemm with NNCB_EPI_RELU_GRAD: the dy sums (2C doubles) -> the group's sum_g / sum_gx
+    float* eg_sg = nullptr;
+    float* eg_sgx = nullptr;
     std::vector<nncb_ew_instr> ew_prog;     // rewritten Ew program (empty: the plan's own)
     int ew_regs = 0;
 };
@@ -136,6 +140,9 @@ void enqueue(nncb_ctx* ctx, const BoundLaunch& b) {
         case LaunchKind::Ew: NNC_CHECK(nncb_ew_launch(ctx, b.ew, b.ptrs.data(), b.n, b.c)); break;
         case LaunchKind::Gemm:
             NNC_CHECK(nncb_gemm(ctx, &b.gemm, P(0), P(1), b.flag0 ? P(2) : nullptr, P(b.ptrs.size() - 1)));
+            if (b.eg_sg)
+                NNC_CHECK(nncb_colsums_to_float(ctx, b.gemm.eg_sums, b.eg_sg, b.eg_sgx,
+                                                b.gemm.kind == NNCB_DENSE_DGRAD ? b.gemm.in_f : b.gemm.ci));
             break;
         case LaunchKind::MaxPool:
             NNC_CHECK(nncb_maxpool_fwd(ctx, &b.pool, P(0), P(1), b.ptrs.size() > 2 ? P(2) : nullptr));
@@ -211,6 +218,7 @@ struct Program {
     // high water equals plan::estimate_peak at the same alignment
     int64_t live_high = 0;
     void* side = nullptr;          // fused BatchNorm column-sum accumulators
+    void* side_eg = nullptr;       // dgrad-epilogue BatchNorm backward sums
     std::unordered_map<std::string, void*> where;   // value name -> device pointer
     std::vector<std::vector<BoundLaunch>> steps;     // per plan, flattened launches
     std::vector<std::vector<const Launch*>> sources; // per plan, the plan launch of each bound launch
@@ -220,6 +228,7 @@ struct Program {
     ~Program() {
         if (arena) nncb_free(dev->ctx(), arena);
         if (side) nncb_free(dev->ctx(), side);
+        if (side_eg) nncb_free(dev->ctx(), side_eg);
     }
 
     void* ptr(const std::string& name) const {
@@ -299,6 +308,7 @@ struct Program {
         if (precision == NNCB_PREC_TF32) {
             fuse_bn_statistics();
             fuse_bn_grad_reduce();
+            fuse_relu_grad_epilogue();
         }
     }
 
@@ -307,6 +317,185 @@ struct Program {
     /// stores is folded into that group (NNCB_EW_REDUCE_BN_GRAD): g is reduced
     /// from registers as it is written instead of being read back by a
     /// separate pass. Applies when the group can run channel-stationary.
+    /// A fused group that only turns a dgrad's output g into the gradient at
+    /// the input of the following ReLU, dy = relu_grad(mask, g [+ residual]),
+    /// and reduces dy for BatchNorm (REDUCE_BN_GRAD), moves into that dgrad's
+    /// epilogue (NNCB_EPI_RELU_GRAD): g is never written or read back. The
+    /// group's program is checked symbolically, and g must have no other reader.
+    void fuse_relu_grad_epilogue() {
+        // opt-in: the fused epilogue is correct but measured slower than the
+        // separate pass (relu-grad epilogue)
+        if (!std::getenv("NNC_RELU_GRAD_EPILOGUE")) return;
+        const bool debug = std::getenv("NNC_EG_DEBUG") != nullptr;
+        struct Fused { BoundLaunch* g; int64_t C; };
+        std::vector<Fused> fused;
+        for (size_t pi = 0; pi < steps.size(); ++pi)
+            for (size_t j = 1; j < steps[pi].size(); ++j) {
+                BoundLaunch& e = steps[pi][j];
+                if (e.kind != LaunchKind::Ew || e.skip) continue;
+                // the dgrad producing a value this group loads (the layer's wgrad
+                // usually sits in between)
+                size_t gi = j;
+                for (size_t i = j; i-- > 0 && j - i <= 6;) {
+                    const BoundLaunch& c = steps[pi][i];
+                    if (c.kind != LaunchKind::Gemm || c.skip || c.eg_sg) continue;
+                    if (c.gemm.kind != NNCB_CONV_DGRAD) continue;   // the epilogue exists in the conv path
+                    if (std::find(e.ptrs.begin(), e.ptrs.end(), c.ptrs.back()) != e.ptrs.end()) {
+                        gi = i;
+                        break;
+                    }
+                }
+                if (gi == j) {
+                    if (debug && sources[pi][j]->label.find("relu") != std::string::npos)
+                        std::fprintf(stderr, "relu_grad_epilogue: %s: no dgrad producer\n", sources[pi][j]->label.c_str());
+                    continue;
+                }
+                BoundLaunch& g = steps[pi][gi];
+                void* gout = g.ptrs.back();
+                const std::vector<nncb_ew_instr>& prog = e.ew_prog.empty() ? sources[pi][j]->ew : e.ew_prog;
+                // symbolic registers: kind 0 unknown, 1 LOAD(ptr), 2 LOAD_CH(ptr), 3 g (+res) sum, 4 dy
+                struct Sym { int kind = 0; void* ptr = nullptr; void* res = nullptr; void* mask = nullptr; };
+                std::map<int, Sym> r;
+                void *dy = nullptr, *x = nullptr, *mean = nullptr, *inv = nullptr, *sg = nullptr, *sgx = nullptr,
+                     *res = nullptr, *mask = nullptr;
+                int stores = 0, reduces = 0;
+                bool ok = true;
+                for (const nncb_ew_instr& in : prog) {
+                    switch (in.op) {
+                        case NNCB_EW_LOAD: r[in.dst] = {1, e.ptrs[in.slot]}; break;
+                        case NNCB_EW_LOAD_CH: r[in.dst] = {2, e.ptrs[in.slot]}; break;
+                        case NNCB_EW_ADD: {
+                            const Sym &a = r[in.a], &b = r[in.b];
+                            if (a.kind == 1 && b.kind == 1 && (a.ptr == gout) != (b.ptr == gout))
+                                r[in.dst] = {3, gout, a.ptr == gout ? b.ptr : a.ptr};
+                            else
+                                ok = false;
+                            break;
+                        }
+                        case NNCB_EW_RELU_GRAD: {   // relu_grad(x = mask, g)
+                            const Sym &m = r[in.a], &gg = r[in.b];
+                            const bool plain = gg.kind == 1 && gg.ptr == gout;
+                            if (m.kind == 1 && m.ptr != gout && (plain || gg.kind == 3)) {
+                                Sym d;
+                                d.kind = 4;
+                                d.res = plain ? nullptr : gg.res;
+                                d.mask = m.ptr;
+                                r[in.dst] = d;
+                            } else {
+                                ok = false;
+                            }
+                            break;
+                        }
+                        case NNCB_EW_STORE:
+                            ++stores;
+                            if (r[in.a].kind != 4) ok = false;
+                            dy = e.ptrs[in.slot];
+                            res = r[in.a].res;
+                            mask = r[in.a].mask;
+                            break;
+                        case NNCB_EW_REDUCE_BN_GRAD: {
+                            ++reduces;
+                            const Sym &a = r[in.a], &b = r[in.b], &c = r[in.c], &dd = r[in.d];
+                            if (a.kind != 4 || b.kind != 1 || c.kind != 2 || dd.kind != 2) ok = false;
+                            x = b.ptr;
+                            mean = c.ptr;
+                            inv = dd.ptr;
+                            sg = e.ptrs[in.slot];
+                            sgx = e.ptrs[in.e];
+                            break;
+                        }
+                        default: ok = false; break;
+                    }
+                    if (!ok) break;
+                }
+                const int64_t C = g.gemm.ci;
+                if (!ok || stores != 1 || reduces != 1 || !dy || dy == gout ||
+                    static_cast<float*>(inv) != static_cast<float*>(mean) + C) {
+                    if (debug)
+                        std::fprintf(stderr, "relu_grad_epilogue: %s: program (ok %d stores %d reduces %d)\n",
+                                     sources[pi][j]->label.c_str(), ok, stores, reduces);
+                    continue;
+                }
+                // g (a value of this plan; arena addresses are shared between
+                // values with disjoint lifetimes) must have no other reader
+                const Launch& gl = *sources[pi][gi];
+                bool other = gl.args.empty() || !gl.is_out.back();
+                const uint32_t gslot = other ? 0 : gl.args.back().slot;
+                for (uint32_t o : plans[pi]->output_slots) other = other || o == gslot;
+                for (size_t k = 0; k < sources[pi].size() && !other; ++k) {
+                    if (k == j || k == gi) continue;
+                    const Launch& L = *sources[pi][k];
+                    for (size_t a = 0; a < L.args.size(); ++a)
+                        other = other || (L.args[a].slot == gslot && !(a < L.is_out.size() && L.is_out[a]));
+                }
+                // values are shared between the bound plans by name
+                const std::string& gname = plans[pi]->values[gslot].name;
+                for (size_t pk = 0; pk < plans.size() && !other; ++pk)
+                    if (pk != pi && plans[pk]->find_value(gname) >= 0) other = true;
+                if (other) {
+                    if (debug) std::fprintf(stderr, "relu_grad_epilogue: %s: g has another reader\n", sources[pi][j]->label.c_str());
+                    continue;
+                }
+                // dy is now written at the dgrad, before the launches in between
+                // (the layer's wgrad): none of them may touch dy's arena bytes
+                // (the planner may share them with a value that dies there), and
+                // none may write a side input the epilogue reads
+                {
+                    auto overlaps = [](const char* a0, int64_t an, const char* b0, int64_t bn) {
+                        return a0 < b0 + bn && b0 < a0 + an;
+                    };
+                    const int64_t B = e.n * static_cast<int64_t>(sizeof(float));
+                    const char* dyc = static_cast<const char*>(dy);
+                    const char* side_in[4] = {static_cast<const char*>(mask), static_cast<const char*>(x),
+                                              static_cast<const char*>(res), static_cast<const char*>(mean)};
+                    const int64_t side_n[4] = {B, B, B, 2 * C * static_cast<int64_t>(sizeof(float))};
+                    bool clash = false;
+                    for (size_t k = gi; k < j && !clash; ++k) {   // k == gi: the dgrad's own inputs
+                        const Launch& L = *sources[pi][k];
+                        for (size_t a = 0; a < L.args.size() && !clash; ++a) {
+                            if (k == gi && a < L.is_out.size() && L.is_out[a]) continue;
+                            const plan::ValueEntry& v = plans[pi]->values[L.args[a].slot];
+                            const char* b0 = static_cast<const char*>(ptr(v.name));
+                            const int64_t bn = element_count(v.dims) * static_cast<int64_t>(sizeof(float));
+                            clash = overlaps(b0, bn, dyc, B);
+                            if (a < L.is_out.size() && L.is_out[a])
+                                for (int q = 0; q < 4 && !clash; ++q)
+                                    clash = side_in[q] && overlaps(b0, bn, side_in[q], side_n[q]);
+                        }
+                        // pointers bound beyond the plan arguments (a folded reduction's sums)
+                        for (size_t a = L.args.size(); a < steps[pi][k].ptrs.size() && !clash; ++a)
+                            clash = overlaps(static_cast<const char*>(steps[pi][k].ptrs[a]), 1, dyc, B);
+                    }
+                    if (clash) {
+                        if (debug)
+                            std::fprintf(stderr, "relu_grad_epilogue: %s: dy / side inputs alias a value live in between\n",
+                                         sources[pi][j]->label.c_str());
+                        continue;
+                    }
+                }
+                if (debug) std::fprintf(stderr, "relu_grad_epilogue: %s: fused\n", sources[pi][j]->label.c_str());
+                g.gemm.epilogue |= NNCB_EPI_RELU_GRAD;
+                g.gemm.eg_mask = static_cast<const float*>(mask);
+                g.gemm.eg_res = static_cast<const float*>(res);
+                g.gemm.eg_x = static_cast<const float*>(x);
+                g.gemm.eg_stats = static_cast<const float*>(mean);
+                g.ptrs.back() = dy;
+                g.eg_sg = static_cast<float*>(sg);
+                g.eg_sgx = static_cast<float*>(sgx);
+                e.skip = true;
+                fused.push_back({&g, C});
+            }
+        if (fused.empty()) return;
+        int64_t doubles = 0;
+        for (const Fused& f : fused) doubles += 2 * f.C;
+        NNC_CHECK(nncb_malloc(dev->ctx(), static_cast<size_t>(doubles) * sizeof(double), &side_eg));
+        int64_t off = 0;
+        for (const Fused& f : fused) {
+            f.g->gemm.eg_sums = static_cast<double*>(side_eg) + off;
+            off += 2 * f.C;
+        }
+    }
+
     void fuse_bn_grad_reduce() {
         if (std::getenv("NNC_NO_FUSED_BN_GRAD")) return;
         for (size_t pi = 0; pi < steps.size(); ++pi)

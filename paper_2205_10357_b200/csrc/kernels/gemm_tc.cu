@@ -72,6 +72,7 @@ struct TcParams {
     const float* eg_res;
     const float* eg_x;
     const float* eg_stats;
+    int eg_side;        // TMA-staged side tiles per pass (2: mask, x; 3: + residual); 0: per-row loads
     int sh, sw, pt, pl;
     int kboxes;         // pixel boxes (TN*TH*TW == 32 pixels each)
     int splits;
@@ -195,6 +196,14 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
@@ -306,16 +315,49 @@ __device__ __forceinline__ int swz(int j, int rr) {
 
 // TMA epilogue: the staged COLS-wide pass leaves as one tensor store of the
 // warp's 32-row sub-box (mode 1: 4-D pixel grid, mode 2: 3-D [split][row][col]).
+// Side inputs of the gradient epilogue (mask, x, residual), encoded with the
+// output map's geometry and swizzle so a side tile has the staging tile's layout.
+struct alignas(64) EgMaps {
+    CUtensorMap m[3];
+};
+
 struct TmaOut {
     const CUtensorMap* map;
     int mode;           // 0: direct stores
     int c1, c2, c3;     // non-column box coordinates
 };
 
-template <int CH, bool CS>
+// Gradient-epilogue side tiles: one warp's 32 rows x COLS columns of each side
+// input at output column `col`, into its side buffer (lane 0 only).
+// Double-buffered: item i (a pass of one chunk of one tile, in the warp's
+// processing order) lands in buffer i & 1; item i + 1 is issued before item i
+// is consumed, so one load is always in flight behind the computation.
+struct EgSide {
+    const EgMaps* maps;
+    uint8_t* buf;        // 2 buffers of eg_side tiles of COLS * 128 bytes
+    uint64_t* bar;       // [2]
+    uint32_t issued, consumed;
+    TmaOut next_to;      // the item after this chunk's last pass: next chunk or next tile
+    int next_col;        // (-1: none known yet)
+};
+
+template <int COLS>
+__device__ __forceinline__ void eg_side_load(EgSide& es, int n, const TmaOut& to, int col) {
+    const uint32_t b = es.issued & 1u;
+    uint8_t* dst = es.buf + b * n * COLS * 128;
+    mbar_expect_tx(&es.bar[b], static_cast<uint32_t>(n * COLS * 128));
+    for (int a = 0; a < n; ++a) {
+        if (to.mode == 1)
+            tma_load_4d(dst + a * COLS * 128, &es.maps->m[a], &es.bar[b], col, to.c1, to.c2, to.c3);
+        else
+            tma_load_3d(dst + a * COLS * 128, &es.maps->m[a], &es.bar[b], col, to.c1, to.c2);
+    }
+}
+
+template <int CH, bool CS, bool EG = false>
 __device__ __forceinline__ void store_chunk_t(const uint32_t (&r)[32], uint8_t* tile, float* dst, bool valid,
                                               int col0, int N, bool full_cols, int lane, bool store, float& cs1,
-                                              float& cs2, const TmaOut& to, const TcParams& P) {
+                                              float& cs2, const TmaOut& to, const TcParams& P, EgSide& es) {
     constexpr int COLS = CH * 4, RPI = 32 / CH;   // columns per pass, rows per store instruction
     const uint32_t vmask = CS ? __ballot_sync(0xffffffffu, valid) : 0u;
 #pragma unroll
@@ -330,53 +372,146 @@ __device__ __forceinline__ void store_chunk_t(const uint32_t (&r)[32], uint8_t* 
             *reinterpret_cast<uint4*>(rowp + (swz<CH>(j, lane) << 4)) =
                 make_uint4(r[p * COLS + 4 * j], r[p * COLS + 4 * j + 1], r[p * COLS + 4 * j + 2], r[p * COLS + 4 * j + 3]);
         __syncwarp();
-        if (CS) {
-            constexpr int RPL = COLS;              // rows per lane: 32 rows over 32/COLS lane groups
-            const int col = lane % COLS, r0 = (lane / COLS) * RPL;
-            float s1 = 0.f, s2 = 0.f;
-            // gradient epilogue: lane (col, row group) turns the staged GEMM
-            // result into dy = mask > 0 ? acc (+ res) : 0 in place, reading the
-            // rows' mask / residual / x values coalesced (a row's 32 columns are
-            // one 128-byte segment), and sums dy and dy * xhat for BatchNorm
-            const int cg = col0 + p * COLS + col;
-            const int64_t doff = P.eg ? static_cast<int64_t>(dst - P.out) : 0;   // this lane's row, output layout
-            float em = 0.f, es = 0.f;
-            if (P.eg && cg < N) {
-                em = __ldg(P.eg_stats + cg);
-                es = __ldg(P.eg_stats + N + cg);
+        if (CS && !(EG && !P.eg_side)) {
+            // Vectorised column statistics: lane (chunk j, row group g) owns the
+            // pass's columns 4j..4j+3 over rows g, g + RG, ... (16-byte shared
+            // loads / stores, conflict-free under the swizzle), then the row
+            // groups fold with xor shuffles. CS alone: sum v, sum v^2 of the
+            // GEMM result (BatchNorm forward). EG: the staged result becomes
+            // dy = mask > 0 ? acc (+ res) : 0 in place, from side tiles in the
+            // same layout, with sum dy, sum dy * xhat (BatchNorm backward).
+            constexpr int RG = 32 / CH;
+            const int j = lane % CH, g = lane / CH;
+            const int cg0 = col0 + p * COLS + 4 * j;
+            float a1[4] = {0.f, 0.f, 0.f, 0.f}, a2[4] = {0.f, 0.f, 0.f, 0.f};
+            float em[4] = {0.f, 0.f, 0.f, 0.f}, ev[4] = {0.f, 0.f, 0.f, 0.f};
+            const uint8_t* sm = nullptr;
+            if (EG) {
+                if (cg0 < N) {   // N % 4 == 0 on the side-tile path (TMA output)
+                    const float4 m4 = __ldg(reinterpret_cast<const float4*>(P.eg_stats + cg0));
+                    const float4 s4 = __ldg(reinterpret_cast<const float4*>(P.eg_stats + N + cg0));
+                    em[0] = m4.x; em[1] = m4.y; em[2] = m4.z; em[3] = m4.w;
+                    ev[0] = s4.x; ev[1] = s4.y; ev[2] = s4.z; ev[3] = s4.w;
+                }
+                if (es.issued == es.consumed + 1) {   // keep the following item in flight
+                    const bool more = p + 1 < 32 / COLS;
+                    const int nc = more ? col0 + (p + 1) * COLS : es.next_col;
+                    if (nc >= 0) {
+                        if (lane == 0) eg_side_load<COLS>(es, P.eg_side, more ? to : es.next_to, nc);
+                        ++es.issued;
+                    }
+                }
+                const uint32_t b = es.consumed & 1u;
+                mbar_wait(&es.bar[b], (es.consumed >> 1) & 1u);
+                sm = es.buf + b * P.eg_side * COLS * 128;
             }
 #pragma unroll
-            for (int i = 0; i < RPL; ++i) {
-                const int rr = r0 + i;
-                float* tp = reinterpret_cast<float*>(tile + rr * (CH * 16) + (swz<CH>(col >> 2, rr) << 4) + (col & 3) * 4);
-                const float v = *tp;
+            for (int i = 0; i < CH; ++i) {
+                const int rr = g + i * RG;
+                const int o = rr * (CH * 16) + (swz<CH>(j, rr) << 4);
                 const bool rv = (vmask >> rr) & 1u;
-                if (P.eg) {
-                    const int64_t off = __shfl_sync(0xffffffffu, static_cast<long long>(doff), rr);
-                    float dy = 0.f, xh = 0.f;
-                    if (rv && cg < N) {
-                        const int64_t e = off + cg;
-                        float gsum = v;
-                        if (P.eg_res) gsum = __fadd_rn(gsum, __ldg(P.eg_res + e));
-                        dy = __ldg(P.eg_mask + e) > 0.f ? gsum : 0.f;
-                        xh = (__ldg(P.eg_x + e) - em) * es;
+                float4 v = *reinterpret_cast<const float4*>(tile + o);
+                float e[4] = {v.x, v.y, v.z, v.w};
+                if (EG) {
+                    const float4 m4 = *reinterpret_cast<const float4*>(sm + o);
+                    const float4 x4 = *reinterpret_cast<const float4*>(sm + COLS * 128 + o);
+                    const float mk[4] = {m4.x, m4.y, m4.z, m4.w}, xv[4] = {x4.x, x4.y, x4.z, x4.w};
+                    if (P.eg_side == 3) {
+                        const float4 r4 = *reinterpret_cast<const float4*>(sm + 2 * COLS * 128 + o);
+                        e[0] = __fadd_rn(e[0], r4.x);
+                        e[1] = __fadd_rn(e[1], r4.y);
+                        e[2] = __fadd_rn(e[2], r4.z);
+                        e[3] = __fadd_rn(e[3], r4.w);
                     }
-                    *tp = dy;
-                    s1 += dy;
-                    s2 = fmaf(dy, xh, s2);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        e[q] = (rv && mk[q] > 0.f) ? e[q] : 0.f;   // out-of-range columns: side tiles are 0
+                        a1[q] += e[q];
+                        a2[q] = fmaf(e[q], (xv[q] - em[q]) * ev[q], a2[q]);
+                    }
+                    *reinterpret_cast<float4*>(tile + o) = make_float4(e[0], e[1], e[2], e[3]);
                 } else {
-                    const float m = rv ? v : 0.f;
-                    s1 += m;
-                    s2 = fmaf(m, m, s2);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const float m = rv ? e[q] : 0.f;
+                        a1[q] += m;
+                        a2[q] = fmaf(m, m, a2[q]);
+                    }
                 }
             }
-            if (P.eg) __syncwarp();   // dy written back before the stores read the tile
+            if (EG) {
+                __syncwarp();   // side buffer consumed (free for item consumed + 2); dy staged for the store
+                ++es.consumed;
+            }
+#pragma unroll
+            for (int sh = CH; sh < 32; sh <<= 1)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    a1[q] += __shfl_xor_sync(0xffffffffu, a1[q], sh);
+                    a2[q] += __shfl_xor_sync(0xffffffffu, a2[q], sh);
+                }
+            // lanes [p*COLS, (p+1)*COLS) take column lane % COLS of this pass
+            // from the lane holding its 4-column chunk (row group 0: lane cc / 4)
+            const int cc = lane % COLS;
+            float t1 = 0.f, t2 = 0.f;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float u1 = __shfl_sync(0xffffffffu, a1[q], cc >> 2);
+                const float u2 = __shfl_sync(0xffffffffu, a2[q], cc >> 2);
+                if ((cc & 3) == q) {
+                    t1 = u1;
+                    t2 = u2;
+                }
+            }
+            if (lane / COLS == p) {
+                cs1 = t1;
+                cs2 = t2;
+            }
+        } else if (CS) {
+            // gradient epilogue without side tiles (direct-store outputs): lane
+            // (col, row group) reads its rows' mask / residual / x from global
+            // memory, 8 rows of loads in flight at a time
+            constexpr int RPL = COLS;
+            const int col = lane % COLS, r0 = (lane / COLS) * RPL;
+            float s1 = 0.f, s2 = 0.f;
+            const int cg = col0 + p * COLS + col;
+            const int64_t doff = static_cast<int64_t>(dst - P.out);   // this lane's row, output layout
+            float em = 0.f, es_ = 0.f;
+            if (cg < N) {
+                em = __ldg(P.eg_stats + cg);
+                es_ = __ldg(P.eg_stats + N + cg);
+            }
+            constexpr int BR = 8;
+#pragma unroll
+            for (int i0 = 0; i0 < RPL; i0 += BR) {
+                float mv[BR], xv[BR], rs[BR];
+#pragma unroll
+                for (int i = 0; i < BR; ++i) {
+                    const int rr = r0 + i0 + i;
+                    const int64_t off = __shfl_sync(0xffffffffu, static_cast<long long>(doff), rr);
+                    const bool ok = ((vmask >> rr) & 1u) && cg < N;
+                    const int64_t e = ok ? off + cg : 0;
+                    mv[i] = ok ? __ldg(P.eg_mask + e) : 0.f;
+                    xv[i] = ok ? __ldg(P.eg_x + e) : 0.f;
+                    rs[i] = (ok && P.eg_res) ? __ldg(P.eg_res + e) : 0.f;
+                }
+#pragma unroll
+                for (int i = 0; i < BR; ++i) {
+                    const int rr = r0 + i0 + i;
+                    float* tp = reinterpret_cast<float*>(tile + rr * (CH * 16) + (swz<CH>(col >> 2, rr) << 4) + (col & 3) * 4);
+                    const float gsum = P.eg_res ? __fadd_rn(*tp, rs[i]) : *tp;
+                    const float dy = mv[i] > 0.f ? gsum : 0.f;   // invalid rows/cols: mask 0
+                    *tp = dy;
+                    s1 += dy;
+                    s2 = fmaf(dy, (xv[i] - em) * es_, s2);
+                }
+            }
+            __syncwarp();   // dy written back before the stores read the tile
 #pragma unroll
             for (int sh = COLS; sh < 32; sh <<= 1) {
                 s1 += __shfl_xor_sync(0xffffffffu, s1, sh);
                 s2 += __shfl_xor_sync(0xffffffffu, s2, sh);
             }
-            // lanes [p*COLS, (p+1)*COLS) take columns p*COLS.. from lanes 0..COLS-1
             const float t1 = __shfl_sync(0xffffffffu, s1, lane % COLS);
             const float t2 = __shfl_sync(0xffffffffu, s2, lane % COLS);
             if (lane / COLS == p) {
@@ -431,10 +566,11 @@ __device__ __forceinline__ void store_chunk_t(const uint32_t (&r)[32], uint8_t* 
 // epilogue of one tile overlaps the main loop of the next.
 // MINB: CTAs per SM the build is register-budgeted for (2: <= 96 registers;
 // 1: no cap, used by the 448-thread MA build and by CS with 256-wide tiles).
-template <bool CS, bool MA, int MINB, bool PAIR>
+template <bool CS, bool MA, int MINB, bool PAIR, bool EG = false>
 __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                   const __grid_constant__ CUtensorMap map_c, const __grid_constant__ TcParams P) {
+                   const __grid_constant__ CUtensorMap map_c, const __grid_constant__ TcParams P,
+                   const __grid_constant__ EgMaps eg_maps) {
     const int STAGES = P.stages;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -444,13 +580,15 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
     const uint32_t rank = PAIR ? cluster_rank() : 0u;
     const uint32_t stage_bytes = a_bytes + b_bytes;
     uint8_t* staging = smem + STAGES * stage_bytes;       // 8 x stg_cols*128 B: one transpose tile per epilogue warp
-    uint64_t* full = reinterpret_cast<uint64_t*>(staging + 8 * P.stg_cols * 128);
+    uint8_t* side = staging + 8 * P.stg_cols * 128;       // EG: 8 x eg_side x stg_cols*128 B side tiles
+    uint64_t* full = reinterpret_cast<uint64_t*>(side + (EG ? 16 * P.eg_side * P.stg_cols * 128 : 0));
     uint64_t* empty = full + STAGES;
     uint64_t* tmem_full = empty + STAGES;                 // [2]
     uint64_t* tmem_empty = tmem_full + 2;                 // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+    uint64_t* side_bar = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(tmem_slot) + 16);   // [8][2]
     // CS: per-CTA column sum / sum of squares of the current column range
-    double* cs_acc = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(tmem_slot) + 16);
+    double* cs_acc = reinterpret_cast<double*>(side_bar + 16);
     // MA: gather tables after cs_acc (fwd: per K index; wgrad: per box pixel)
     int* ma_tab = reinterpret_cast<int*>(cs_acc + 2 * P.bn);
 
@@ -465,6 +603,8 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
             mbar_init(&tmem_full[s], 1);
             mbar_init(&tmem_empty[s], PAIR ? 16 : 8);     // one arrival per epilogue warp (of both CTAs)
         }
+        if (EG)
+            for (int w = 0; w < 16; ++w) mbar_init(&side_bar[w], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (MA) {
@@ -513,27 +653,32 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
         int phase, tn0, th0, tw0, kb_begin, nk, split;
         int64_t m0, n0;
     };
-    auto decode = [&](int64_t t) {
+    // 32-bit index arithmetic (the host caps tile counts below 2^31): every
+    // role decodes each of its tiles, and 64-bit divisions cost ~4x more
+    auto decode = [&](int64_t t64) {
         Tile T{};
-        T.n0 = (t % P.n_tiles) * P.bn;
-        int64_t rest = t / P.n_tiles;
+        const uint32_t t = static_cast<uint32_t>(t64), nt = static_cast<uint32_t>(P.n_tiles);
+        const uint32_t rest = t / nt;
+        T.n0 = static_cast<int64_t>(t - rest * nt) * P.bn;
         if (P.mode == MODE_CONV) {
             // PAIR: tile t covers pixel boxes 2q, 2q+1 (one per CTA); a box past
             // the grid is fully out of bounds (zero loads, no stores)
-            int64_t pix = PAIR ? 2 * (rest % P.pix_pairs) + rank : rest % P.pix_tiles;
-            T.phase = static_cast<int>(PAIR ? rest / P.pix_pairs : rest / P.pix_tiles);
-            int tw = static_cast<int>(pix % P.tiles_w);
-            pix /= P.tiles_w;
-            int th = static_cast<int>(pix % P.tiles_h);
-            int tn = static_cast<int>(pix / P.tiles_h);
-            T.tn0 = tn * P.TN;
-            T.th0 = th * P.TH;
-            T.tw0 = tw * P.TW;
+            const uint32_t per = static_cast<uint32_t>(PAIR ? P.pix_pairs : P.pix_tiles);
+            const uint32_t ph = rest / per, q = rest - ph * per;
+            uint32_t pix = PAIR ? 2 * q + rank : q;
+            T.phase = static_cast<int>(ph);
+            const uint32_t tw_ = static_cast<uint32_t>(P.tiles_w), th_ = static_cast<uint32_t>(P.tiles_h);
+            const uint32_t p1 = pix / tw_, p2 = p1 / th_;
+            T.tn0 = static_cast<int>(p2) * P.TN;
+            T.th0 = static_cast<int>(p1 - p2 * th_) * P.TH;
+            T.tw0 = static_cast<int>(pix - p1 * tw_) * P.TW;
             T.kb_begin = 0;
             T.nk = P.ntaps[T.phase] * P.cblocks;
         } else {
-            T.m0 = PAIR ? (2 * (rest % P.m_pairs) + rank) * BM : (rest % P.m_tiles) * BM;
-            T.split = static_cast<int>(PAIR ? rest / P.m_pairs : rest / P.m_tiles);
+            const uint32_t mper = static_cast<uint32_t>(PAIR ? P.m_pairs : P.m_tiles);
+            const uint32_t sp = rest / mper, q = rest - sp * mper;
+            T.m0 = static_cast<int64_t>(PAIR ? 2 * q + rank : q) * BM;
+            T.split = static_cast<int>(sp);
             int per = (P.kboxes + P.splits - 1) / P.splits;
             T.kb_begin = min(P.kboxes, T.split * per);
             T.nk = min(P.kboxes, T.kb_begin + per) - T.kb_begin;
@@ -783,17 +928,57 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
         const int half = (warp - 2) / 4;
         const int row = quarter * 32 + lane;
         double cs_sum[4] = {0, 0, 0, 0}, cs_sq[4] = {0, 0, 0, 0};   // CS: per-lane column accumulators
+        const int nchunks = P.bn / 32;
+        auto out_box = [&](const Tile& T) {
+            TmaOut to{&map_c, P.tma_out, 0, 0, 0};
+            if (P.tma_out == 1) {   // the warp's quarter of the pixel tile as a sub-box origin
+                const int q0 = quarter * 32;
+                to.c1 = T.tw0 + q0 % P.TW;
+                to.c2 = T.th0 + (q0 / P.TW) % P.TH;
+                to.c3 = T.tn0 + q0 / (P.TW * P.TH);
+            } else if (P.tma_out == 2) {
+                to.c1 = static_cast<int>(T.m0) + quarter * 32;
+                to.c2 = P.splits > 1 ? T.split : 0;
+            }
+            return to;
+        };
+        // EG side tiles: this warp's chunks are c = half, half + 2, ... with col0 < N
+        auto chunk_col = [&](const Tile& T, int c) -> int {
+            return (c < nchunks && T.n0 + c * 32 < P.N) ? static_cast<int>(T.n0 + c * 32) : -1;
+        };
+        EgSide es{&eg_maps, side + (warp - 2) * 2 * P.eg_side * P.stg_cols * 128, &side_bar[2 * (warp - 2)], 0u, 0u,
+                  TmaOut{&map_c, 0, 0, 0, 0}, -1};
+        auto side_issue = [&](const TmaOut& to, int col) {
+            if (P.stg_cols == 32)
+                eg_side_load<32>(es, P.eg_side, to, col);
+            else if (P.stg_cols == 16)
+                eg_side_load<16>(es, P.eg_side, to, col);
+            else
+                eg_side_load<8>(es, P.eg_side, to, col);
+        };
+        const bool side_on = EG && P.eg_side > 0;
+        // this lane's row within a pixel tile (tile-independent)
+        const int r_ww = row % P.TW, r_hh = (row / P.TW) % P.TH, r_nn = row / (P.TW * P.TH);
         uint32_t local = 0;
+        Tile Tnext = t_begin < P.tiles ? decode(t_begin) : Tile{};   // each tile decoded once
         for (int64_t t = t_begin; t < P.tiles; t += t_step, ++local) {
-            const Tile T = decode(t);
+            const Tile T = Tnext;
+            const bool has_next = t + t_step < P.tiles;
+            if (has_next) Tnext = decode(t + t_step);
             const uint32_t acc = local & 1;
+            if (side_on && es.issued == es.consumed) {   // nothing in flight: this tile's first side tiles
+                const int c0 = chunk_col(T, half);
+                if (c0 >= 0) {
+                    if (lane == 0) side_issue(out_box(T), c0);
+                    ++es.issued;
+                }
+            }
             mbar_wait(&tmem_full[acc], (local / 2) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             float* dst = nullptr;
             bool valid = false;
             if (P.mode == MODE_CONV) {
-                const int ww = row % P.TW, hh = (row / P.TW) % P.TH, nn = row / (P.TW * P.TH);
-                const int n = T.tn0 + nn, y = T.th0 + hh, x = T.tw0 + ww;
+                const int n = T.tn0 + r_nn, y = T.th0 + r_hh, x = T.tw0 + r_ww;
                 valid = n < P.gn && y < P.gh && x < P.gw;
                 const int64_t oy = static_cast<int64_t>(y) * P.out_s + P.py[T.phase];
                 const int64_t ox = static_cast<int64_t>(x) * P.out_s + P.px[T.phase];
@@ -805,17 +990,7 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                 float* base = P.splits > 1 ? P.partial + static_cast<int64_t>(T.split) * P.M * P.N : P.out;
                 dst = base + m * P.ldc;
             }
-            const int nchunks = P.bn / 32;
-            TmaOut to{&map_c, P.tma_out, 0, 0, 0};
-            if (P.tma_out == 1) {   // the warp's quarter of the pixel tile as a sub-box origin
-                const int q0 = quarter * 32;
-                to.c1 = T.tw0 + q0 % P.TW;
-                to.c2 = T.th0 + (q0 / P.TW) % P.TH;
-                to.c3 = T.tn0 + q0 / (P.TW * P.TH);
-            } else if (P.tma_out == 2) {
-                to.c1 = static_cast<int>(T.m0) + quarter * 32;
-                to.c2 = P.splits > 1 ? T.split : 0;
-            }
+            const TmaOut to = out_box(T);
             const uint32_t tbase =
                 tmem_base + acc * static_cast<uint32_t>(P.bn) + (static_cast<uint32_t>(quarter * 32) << 16);
             uint32_t r[32];
@@ -853,12 +1028,20 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                     const bool full_cols = col0 + 32 <= P.N && (P.ldc % 4) == 0;
                     const bool st = !P.nostore;
                     float c1 = 0.f, c2 = 0.f;
+                    if (side_on) {   // the item after this chunk: the next chunk, else the next tile's first
+                        es.next_to = to;
+                        es.next_col = chunk_col(T, c + 2);
+                        if (es.next_col < 0 && has_next) {
+                            es.next_to = out_box(Tnext);
+                            es.next_col = chunk_col(Tnext, half);
+                        }
+                    }
                     if (P.stg_cols == 32)
-                        store_chunk_t<8, CS>(r, tile, dst, valid, col0, P.N, full_cols, lane, st, c1, c2, to, P);
+                        store_chunk_t<8, CS, EG>(r, tile, dst, valid, col0, P.N, full_cols, lane, st, c1, c2, to, P, es);
                     else if (P.stg_cols == 16)
-                        store_chunk_t<4, CS>(r, tile, dst, valid, col0, P.N, full_cols, lane, st, c1, c2, to, P);
+                        store_chunk_t<4, CS, EG>(r, tile, dst, valid, col0, P.N, full_cols, lane, st, c1, c2, to, P, es);
                     else
-                        store_chunk_t<2, CS>(r, tile, dst, valid, col0, P.N, full_cols, lane, st, c1, c2, to, P);
+                        store_chunk_t<2, CS, EG>(r, tile, dst, valid, col0, P.N, full_cols, lane, st, c1, c2, to, P, es);
                     if (CS) {
                         cs_sum[k] += static_cast<double>(c1);
                         cs_sq[k] += static_cast<double>(c2);
@@ -874,8 +1057,7 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
             if (CS) {
                 // flush this warp's column accumulators when the CTA's next tile
                 // covers other columns (normally once, after the last tile)
-                const int64_t tn = t + t_step;
-                const bool flush = tn >= P.tiles || (tn % P.n_tiles) * P.bn != T.n0;
+                const bool flush = !has_next || Tnext.n0 != T.n0;
                 if (flush) {
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
@@ -1014,46 +1196,89 @@ TcShape pick_shape(int bn) {
     return best;
 }
 
+// Tensor map with the TMA epilogue's output geometry (P.tma_out 1: 4-D pixel
+// grid, 2: 3-D [split][row][col]) over `base`: the output itself, or a side
+// input of the gradient epilogue laid out like it.
+bool encode_out_like(CUtensorMap* m, const TcParams& P, const void* base) {
+    const int cols = P.stg_cols;
+    const CUtensorMapSwizzle sw = cols == 32 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : cols == 16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+    CUresult r;
+    if (P.tma_out == 1) {
+        cuuint64_t dims[4] = {(cuuint64_t)P.N, (cuuint64_t)P.out_w, (cuuint64_t)P.out_h, (cuuint64_t)P.gn};
+        cuuint64_t strides[3] = {(cuuint64_t)(P.N * 4), (cuuint64_t)(P.N * P.out_w * 4),
+                                 (cuuint64_t)(P.N * P.out_w * P.out_h * 4)};
+        cuuint32_t box[4] = {(cuuint32_t)cols, (cuuint32_t)P.ob_w, (cuuint32_t)P.ob_h, (cuuint32_t)P.ob_n};
+        cuuint32_t es[4] = {1, 1, 1, 1};
+        r = nncb::drv::table().tensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(base), dims,
+                                                    strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                                                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+        cuuint64_t dims[3] = {(cuuint64_t)P.N, (cuuint64_t)P.M, (cuuint64_t)std::max(P.splits, 1)};
+        cuuint64_t strides[2] = {(cuuint64_t)(P.N * 4), (cuuint64_t)(P.N * P.M * 4)};
+        cuuint32_t box[3] = {(cuuint32_t)cols, 32, 1};
+        cuuint32_t es[3] = {1, 1, 1};
+        r = nncb::drv::table().tensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims,
+                                                    strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                                                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
+    return r == CUDA_SUCCESS;
+}
+
 // Output tensor map for the TMA epilogue, encoded once the staging width
 // (COLS = stg_cols) is known. Returns false (direct stores) when not applicable.
 bool encode_tma_out(CUtensorMap* mc, TcParams& P) {
     static const bool enabled = !(getenv("NNCB_TC_TMA_OUT") && atoi(getenv("NNCB_TC_TMA_OUT")) == 0);
     P.tma_out = 0;
     if (!enabled || P.N % 4 != 0 || P.ldc != P.N) return false;
-    const int cols = P.stg_cols;
-    const CUtensorMapSwizzle sw = cols == 32 ? CU_TENSOR_MAP_SWIZZLE_128B
-                                  : cols == 16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
-    CUresult r;
     if (P.mode == MODE_CONV) {
         if (P.out_s != 1) return false;   // strided-dgrad phases interleave pixels: direct stores
         P.ob_w = P.TW >= 32 ? 32 : P.TW;
         P.ob_h = P.TW >= 32 ? 1 : std::min(P.TH, 32 / P.TW);
         P.ob_n = 32 / (P.ob_w * P.ob_h);
         if (P.ob_n > P.TN && P.ob_n > 1) return false;
-        cuuint64_t dims[4] = {(cuuint64_t)P.N, (cuuint64_t)P.out_w, (cuuint64_t)P.out_h, (cuuint64_t)P.gn};
-        cuuint64_t strides[3] = {(cuuint64_t)(P.N * 4), (cuuint64_t)(P.N * P.out_w * 4),
-                                 (cuuint64_t)(P.N * P.out_w * P.out_h * 4)};
-        cuuint32_t box[4] = {(cuuint32_t)cols, (cuuint32_t)P.ob_w, (cuuint32_t)P.ob_h, (cuuint32_t)P.ob_n};
-        cuuint32_t es[4] = {1, 1, 1, 1};
-        r = nncb::drv::table().tensorMapEncodeTiled(mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, P.out, dims, strides, box, es,
-                                              CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) return false;
         P.tma_out = 1;
-        return true;
+        if (encode_out_like(mc, P, P.out)) return true;
+    } else {
+        P.tma_out = 2;
+        if (encode_out_like(mc, P, P.splits > 1 ? P.partial : P.out)) return true;
     }
-    float* base = P.splits > 1 ? P.partial : P.out;
-    cuuint64_t dims[3] = {(cuuint64_t)P.N, (cuuint64_t)P.M, (cuuint64_t)std::max(P.splits, 1)};
-    cuuint64_t strides[2] = {(cuuint64_t)(P.N * 4), (cuuint64_t)(P.N * P.M * 4)};
-    cuuint32_t box[3] = {(cuuint32_t)cols, 32, 1};
-    cuuint32_t es[3] = {1, 1, 1};
-    r = nncb::drv::table().tensorMapEncodeTiled(mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, es,
-                                          CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return false;
-    P.tma_out = 2;
-    return true;
+    P.tma_out = 0;
+    return false;
 }
+
+// Gradient epilogue: side tiles through TMA when the output leaves through
+// TMA (same geometry); otherwise the epilogue loads the side inputs per row.
+void encode_eg_side(EgMaps* em, TcParams& P) {
+    P.eg_side = 0;
+    if (!P.eg || !P.tma_out) return;
+    const int n = P.eg_res ? 3 : 2;
+    const float* src[3] = {P.eg_mask, P.eg_x, P.eg_res};
+    for (int a = 0; a < n; ++a)
+        if (!encode_out_like(&em->m[a], P, src[a])) return;
+    P.eg_side = n;
+}
+
+// Shared-memory shape of a gradient-epilogue launch (one CTA per SM): the
+// widest staging whose double-buffered side tiles still leave a 2-deep ring
+// (the fused dgrads are output-bound: side bandwidth beats ring depth).
+void eg_shape(TcParams& P, int bn_smem) {
+    const size_t sb = stage_bytes_for(bn_smem);
+    const int nside = P.eg_res ? 3 : 2;
+    for (int need : {2})
+        for (int stg : {32, 16, 8}) {
+            const size_t fixed = smem_for(bn_smem, 0, stg) + 16 * static_cast<size_t>(nside) * stg * 128;
+            if (fixed >= 227 * 1024) continue;
+            const int st = static_cast<int>(std::min<size_t>(MAX_STAGES, (227 * 1024 - fixed) / sb));
+            if (st >= need) {
+                P.stg_cols = stg;
+                P.stages = st;
+                return;
+            }
+        }
+}
+
+size_t eg_side_bytes(const TcParams& P) { return P.eg ? 16 * static_cast<size_t>(P.eg_res ? 3 : 2) * P.stg_cols * 128 : 0; }
 
 int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc_unused, TcParams& P) {
     CUtensorMap mc;
@@ -1067,9 +1292,12 @@ int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CU
         NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<true, true, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<false, false, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<true, false, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<true, false, 1, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<true, false, 1, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr_done = true;
     }
     if (P.tiles <= 0) return 0;
+    if (P.tiles >= (int64_t(1) << 31)) return nncb::fail("gemm: tile count exceeds the kernel's 32-bit tile index");
     P.tma_store = 0;
     const TcShape shp = pick_shape(P.bn);
     P.stages = shp.stages;
@@ -1081,14 +1309,19 @@ int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CU
     if (env_stg == 8 || env_stg == 16 || env_stg == 32) P.stg_cols = env_stg;
     if (env_stages > 0) P.stages = std::min(env_stages, MAX_STAGES);
     P.nostore = env_nostore;
+    EgMaps em;
+    memset(&em, 0, sizeof(em));
+    if (P.eg && (P.xa != nullptr || P.nostore)) return nncb::fail("gemm: the gradient epilogue has no manual-A / no-store build");
     if (P.pair) {
         // CTA pair: each CTA stages A (128 rows) and half of B; one CTA per SM
         const int half = P.bn / 2;
         P.stg_cols = 32;
         const size_t fixed = smem_for(half, 0, P.stg_cols);
         P.stages = static_cast<int>(std::min<size_t>(MAX_STAGES, (227 * 1024 - fixed) / stage_bytes_for(half)));
-        const size_t smem = smem_for(half, P.stages, P.stg_cols);
+        if (P.eg) eg_shape(P, half);
+        const size_t smem = smem_for(half, P.stages, P.stg_cols) + eg_side_bytes(P);
         encode_tma_out(&mc, P);
+        encode_eg_side(&em, P);
         const int64_t pairs = std::min<int64_t>(P.tiles, ctx->sm_count / 2);
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));
@@ -1102,10 +1335,12 @@ int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CU
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        if (P.colstats)
-            NNCB_CUDA(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<true, false, 1, true>, ma, mb, mc, P));
+        if (P.eg)
+            NNCB_CUDA(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<true, false, 1, true, true>, ma, mb, mc, P, em));
+        else if (P.colstats)
+            NNCB_CUDA(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<true, false, 1, true>, ma, mb, mc, P, em));
         else
-            NNCB_CUDA(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<false, false, 1, true>, ma, mb, mc, P));
+            NNCB_CUDA(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<false, false, 1, true>, ma, mb, mc, P, em));
         NNCB_LAUNCHED(ctx);
         return 0;
     }
@@ -1123,23 +1358,28 @@ int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CU
         const size_t fixed = smem_for(P.bn, 0, P.stg_cols, tab_ints);
         P.stages = static_cast<int>(std::min<size_t>(MAX_STAGES, (227 * 1024 - fixed) / stage_bytes_for(P.bn)));
     }
-    const size_t smem = smem_for(P.bn, P.stages, P.stg_cols, tab_ints);
+    if (P.eg) eg_shape(P, P.bn);
+    const size_t smem = smem_for(P.bn, P.stages, P.stg_cols, tab_ints) + eg_side_bytes(P);
     encode_tma_out(&mc, P);
+    encode_eg_side(&em, P);
     int per_sm = (env_stages > 0) ? ((P.bn <= 128 && smem <= 113 * 1024) ? 2 : 1) : shp.per_sm;
     if (env_persm > 0 && (env_persm == 1 || 2 * smem <= 228 * 1024)) per_sm = env_persm;
     if (manual) per_sm = 1;   // the 448-thread build is compiled for one CTA per SM
+    if (P.eg) per_sm = 1;      // the gradient epilogue needs the 168-register build
     unsigned grid = static_cast<unsigned>(std::min<int64_t>(P.tiles, static_cast<int64_t>(ctx->sm_count) * per_sm));
     const unsigned threads = manual ? THREADS + 128 : THREADS;
     if (P.colstats && manual)
-        tc_gemm_kernel<true, true, 1, false><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
+        tc_gemm_kernel<true, true, 1, false><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P, em);
     else if (manual)
-        tc_gemm_kernel<false, true, 1, false><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
+        tc_gemm_kernel<false, true, 1, false><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P, em);
+    else if (P.eg)
+        tc_gemm_kernel<true, false, 1, false, true><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P, em);
     else if (P.colstats && per_sm == 1)
-        tc_gemm_kernel<true, false, 1, false><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
+        tc_gemm_kernel<true, false, 1, false><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P, em);
     else if (P.colstats)
-        tc_gemm_kernel<true, false, 2, false><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
+        tc_gemm_kernel<true, false, 2, false><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P, em);
     else
-        tc_gemm_kernel<false, false, 2, false><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P);
+        tc_gemm_kernel<false, false, 2, false><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P, em);
     NNCB_LAUNCHED(ctx);
     return 0;
 }

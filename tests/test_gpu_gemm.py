@@ -225,7 +225,8 @@ def test_conv_fwd_transposed_weights(shape, tile):
 @pytest.mark.parametrize("res", [False, True])
 @pytest.mark.parametrize("shape,tile", [((2, 14, 14, 64, 64, 3, 1), 0), ((4, 7, 7, 128, 256, 1, 1), 0),
                                         ((2, 13, 11, 64, 96, 3, 2), 0), ((3, 8, 8, 96, 128, 3, 1), 0x10000 | 256),
-                                        ((2, 16, 16, 64, 32, 1, 1), 0)])
+                                        ((2, 16, 16, 64, 32, 1, 1), 0), ((16, 56, 56, 64, 64, 1, 1), 0),
+                                        ((4, 28, 28, 256, 64, 1, 1), 256), ((8, 14, 14, 256, 128, 3, 1), 0x10000 | 256)])
 def test_dgrad_relu_grad_epilogue(shape, tile, res):
     """Dgrad epilogue that emits the gradient at the input of the following
     ReLU (dy = mask > 0 ? acc (+ residual) : 0) with the BatchNorm backward sums

@@ -164,3 +164,27 @@ def test_solp_loaded_plans_execute_bitwise():
     la, ga = a.gradients({"x": x}, t)
     lb, gb = b.gradients({"x": x}, t)
     assert la == lb and all(np.array_equal(ga[k], gb[k]) for k in ga)
+
+
+def test_relu_grad_epilogue_fusion_matches_separate_pass(monkeypatch):
+    """Opt-in runtime pass (NNC_RELU_GRAD_EPILOGUE): the relu-grad + BatchNorm
+    reduction groups move into the dgrad GEMM epilogues of a residual network
+    (fewer launches per step), with the same loss and gradients as the separate
+    elementwise pass to within the tf32 bound."""
+    doc = W.resnet50(2, image=64)
+    x = W.uniform((2, 64, 64, 3), 1, "x")
+    t = W.uniform((2, 1000), 2, "t", 0.0, 1.0)
+    monkeypatch.delenv("NNC_RELU_GRAD_EPILOGUE", raising=False)
+    a = P.CompiledModel(doc, precision=P.PREC_TF32)
+    loss_a, grads_a = a.gradients({"x": x}, t)
+    a.trainer_prepare({"x": x}, t)
+    n_a = len(a.profile_step(0.0))
+    monkeypatch.setenv("NNC_RELU_GRAD_EPILOGUE", "1")
+    b = P.CompiledModel(doc, precision=P.PREC_TF32)
+    loss_b, grads_b = b.gradients({"x": x}, t)
+    b.trainer_prepare({"x": x}, t)
+    n_b = len(b.profile_step(0.0))
+    assert n_b < n_a - 30, (n_a, n_b)
+    assert abs(loss_b - loss_a) <= 1e-3 * abs(loss_a)
+    for w, g in grads_a.items():
+        assert rel_err(grads_b[w], g) < 2e-2, w

@@ -40,6 +40,8 @@ def main():
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--layers", default="")
     ap.add_argument("--colstats", action="store_true", help="forward GEMMs also accumulate BN column statistics")
+    ap.add_argument("--eg", action="store_true", help="dgrad GEMMs run the ReLU-gradient + BN-sums epilogue")
+    ap.add_argument("--res", action="store_true", help="with --eg: add a residual gradient")
     ap.add_argument("--tile", default="auto", help="auto | 128 | 256 | p128 | p256 | w128 | t128 | tp256 ... (p = CTA pair, w = wide staging, t = K-major weights)")
     a = ap.parse_args()
     timer = P.DeviceTimer()
@@ -64,6 +66,11 @@ def main():
             d = GemmDesc(kind=code, precision=0, epilogue=4 if cs else 0, **g)
             if cs:
                 d.colstats = cs.p
+            if a.eg and kind == "dgrad":
+                eg = [Dev(nbytes=a.batch * h * h * ci * 4) for _ in range(3)] + [Dev(nbytes=2 * ci * 4), Dev(nbytes=2 * ci * 8)]
+                d.epilogue = 8
+                d.eg_mask, d.eg_x, d.eg_stats, d.eg_sums = eg[0].p, eg[1].p, eg[3].p, eg[4].p
+                d.eg_res = eg[2].p if a.res else None
             rc = K.nncb_gemm(ctx(), ctypes.byref(d), A.p, B.p, None, O.p)   # warm-up
             assert rc == 0, K.nncb_last_error()
             timer.start()

@@ -17,7 +17,7 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t 
     return d;
 }
 
-__global__ void __launch_bounds__(128, 1) probe(int N, int iters, float* sink, int stress) {
+__global__ void __launch_bounds__(128, 1) probe(int N, int iters, float* sink, int stress, int M) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     __shared__ uint64_t bar, bar2;
@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(128, 1) probe(int N, int iters, float* sink, i
             for (int j = 0; j < 8; ++j) w[((threadIdx.x - 32) * 8 + j) & 1023] = v;
     }
     if (threadIdx.x == 0) {
-        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((128u >> 4) << 24);
+        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
         const uint32_t a0 = smem_u32(sa), b0 = smem_u32(sb);
         uint32_t phase = 0;
         for (int it = 0; it < iters; ++it) {
@@ -80,22 +80,23 @@ int main() {
     int sms;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
-    for (int stress : {0, -1})
-    for (int N : {128, 256}) {
+    const int stress = 0;
+    for (int M : {64, 128})
+    for (int N : {64, 128, 256}) {
         const int iters = 4096;
-        probe<<<sms, 128, 80 * 1024>>>(N, 64, sink, stress);
+        probe<<<sms, 128, 80 * 1024>>>(N, 64, sink, stress, M);
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
         cudaEventRecord(e0);
-        probe<<<sms, 128, 80 * 1024>>>(N, iters, sink, stress);
+        probe<<<sms, 128, 80 * 1024>>>(N, iters, sink, stress, M);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms;
         cudaEventElapsedTime(&ms, e0, e1);
-        double flops = 2.0 * 128 * N * 32 * (double)iters * sms;
+        double flops = 2.0 * M * N * 32 * (double)iters * sms;
         // stress s: per k-step 96 threads x 8 x 16 B x s = 12 KB x s of smem stores
-        printf("stress %d (%2d KB/k-step)  M=128 N=%3d: %.1f TFLOP/s (%s)\n", stress, 12 * stress, N, flops / ms / 1e9,
+        printf("M=%3d N=%3d: %.1f TFLOP/s (%s)\n", M, N, flops / ms / 1e9,
                cudaGetErrorString(cudaGetLastError()));
     }
     return 0;
