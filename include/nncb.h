@@ -157,6 +157,14 @@ enum nncb_epilogue {
      * eg_stats = [mean; invstd] (2N floats); the GEMM zeroes eg_sums.
      * Tensor-core path only (returns unhandled otherwise).                   */
     NNCB_EPI_RELU_GRAD = 8,
+    /* Hint for NNCB_CONV_WGRAD: the activation `a` holds the same bytes that
+     * the most recent NNCB_CONV_FWD on this context read from the same
+     * address with the same geometry, and nothing has written it since (in
+     * stream order). Lowered copies made by that forward call (the
+     * space-to-depth input of a strided small-channel conv) are reused
+     * instead of rebuilt. The library re-derives the copy whenever it cannot
+     * match the forward call; the caller vouches only for the bytes.       */
+    NNCB_EPI_A_UNCHANGED = 16,
 };
 
 typedef struct {

@@ -29,6 +29,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <set>
 #include <list>
 #include <mutex>
 #include <unordered_map>
@@ -310,6 +311,26 @@ struct Program {
             fuse_bn_grad_reduce();
             fuse_relu_grad_epilogue();
         }
+        hint_unchanged_activations();
+    }
+
+    /// A weight gradient whose activation is a value an earlier forward conv
+    /// of the same step already read (values are written once per step, so
+    /// its bytes are unchanged) may reuse that call's lowered copy of it
+    /// (NNCB_EPI_A_UNCHANGED; the space-to-depth input of the stem).
+    void hint_unchanged_activations() {
+        std::set<std::string> fwd_inputs;
+        for (size_t pi = 0; pi < steps.size(); ++pi)
+            for (size_t k = 0; k < steps[pi].size(); ++k) {
+                BoundLaunch& b = steps[pi][k];
+                const Launch& L = *sources[pi][k];
+                if (b.kind != LaunchKind::Gemm || b.skip || L.args.empty()) continue;
+                const std::string& an = plans[pi]->values[L.args[0].slot].name;
+                if (b.gemm.kind == NNCB_CONV_FWD)
+                    fwd_inputs.insert(an);
+                else if (b.gemm.kind == NNCB_CONV_WGRAD && fwd_inputs.count(an))
+                    b.gemm.epilogue |= NNCB_EPI_A_UNCHANGED;
+            }
     }
 
     /// The BatchNorm backward reduction (sum g, sum g*xhat per channel) of a

@@ -1453,26 +1453,38 @@ __device__ __forceinline__ void s2d_chan(int cc, int ci, bool pack, int& half, i
     c = real ? cl % ci : 0;
 }
 
+// Thread t writes 16 bytes (channels 4q..4q+3, q = t & 7) of lowered pixel
+// t >> 3. The grid stride is a multiple of 8, so q and its channel -> (row,
+// column, source channel) mapping are fixed per thread; 32-bit pixel index
+// arithmetic (the host caps n*H2*W2*8 below 2^31).
 __global__ void s2d_input_k(const float* __restrict__ x, float* __restrict__ xs, int n, int ih, int iw, int ci,
                             int H2, int W2, int pt, int pl, int pack) {
-    const int64_t total = static_cast<int64_t>(n) * H2 * W2 * 8;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        const int q = static_cast<int>(t & 7);
-        const int64_t pix = t >> 3;
-        const int X = static_cast<int>(pix % W2);
-        const int Y = static_cast<int>((pix / W2) % H2);
-        const int64_t nn = pix / (static_cast<int64_t>(W2) * H2);
+    const uint32_t total = static_cast<uint32_t>(n) * H2 * W2 * 8;
+    uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int q = static_cast<int>(t & 7);
+    int dy[4], dx[4], ch[4];
+    bool real[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        int half, blk, c;
+        s2d_chan(q * 4 + j, ci, pack != 0, half, blk, c, real[j]);
+        dy[j] = (blk >> 1) - pt;
+        dx[j] = 2 * half + (blk & 1) - pl;
+        ch[j] = c;
+    }
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (; t < total; t += stride) {
+        const uint32_t pix = t >> 3;
+        const uint32_t r = pix / static_cast<uint32_t>(W2);
+        const int X = static_cast<int>(pix - r * W2);
+        const uint32_t nn = r / static_cast<uint32_t>(H2);
+        const int Y = static_cast<int>(r - nn * H2);
+        const float* xn = x + static_cast<int64_t>(nn) * ih * iw * ci;
         float v[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            int half, blk, c;
-            bool real;
-            s2d_chan(q * 4 + j, ci, pack != 0, half, blk, c, real);
-            v[j] = 0.f;
-            if (real) {
-                const int iy = 2 * Y + (blk >> 1) - pt, ix = 2 * (X + half) + (blk & 1) - pl;
-                if (iy >= 0 && iy < ih && ix >= 0 && ix < iw) v[j] = __ldg(x + ((nn * ih + iy) * iw + ix) * ci + c);
-            }
+            const int iy = 2 * Y + dy[j], ix = 2 * X + dx[j];
+            v[j] = (real[j] && iy >= 0 && iy < ih && ix >= 0 && ix < iw) ? __ldg(xn + (iy * iw + ix) * ci + ch[j]) : 0.f;
         }
         reinterpret_cast<float4*>(xs)[t] = make_float4(v[0], v[1], v[2], v[3]);
     }
@@ -1519,9 +1531,19 @@ int gemm_tc_s2d(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const fl
     if (!ws) return fail("space-to-depth: workspace allocation failed");
     float* xs = reinterpret_cast<float*>(ws);
     float* wsp = reinterpret_cast<float*>(ws + w_off);
-    s2d_input_k<<<grid_for(ctx, static_cast<int64_t>(d->n) * H2 * W2 * 8, 256), 256, 0, ctx->stream>>>(
-        a, xs, (int)d->n, (int)d->ih, (int)d->iw, (int)d->ci, H2, W2, (int)d->pad_top, (int)d->pad_left, pack);
-    NNCB_LAUNCHED(ctx);
+    if (static_cast<int64_t>(d->n) * H2 * W2 * 8 >= (int64_t(1) << 31))
+        return fail("space-to-depth: input exceeds the 32-bit lowering index");
+    const int64_t key[8] = {d->n, d->ih, d->iw, d->ci, d->pad_top, d->pad_left, H2 * int64_t(1 << 20) + W2, pack};
+    const bool reuse = d->kind == NNCB_CONV_WGRAD && (d->epilogue & NNCB_EPI_A_UNCHANGED) && ctx->s2d_src == a &&
+                       ctx->s2d_ws == ctx->workspace && std::equal(key, key + 8, ctx->s2d_key);
+    if (!reuse) {
+        s2d_input_k<<<grid_for(ctx, static_cast<int64_t>(d->n) * H2 * W2 * 8, 256), 256, 0, ctx->stream>>>(
+            a, xs, (int)d->n, (int)d->ih, (int)d->iw, (int)d->ci, H2, W2, (int)d->pad_top, (int)d->pad_left, pack);
+        NNCB_LAUNCHED(ctx);
+        ctx->s2d_src = a;
+        ctx->s2d_ws = ctx->workspace;
+        std::copy(key, key + 8, ctx->s2d_key);
+    }
     nncb_gemm_desc dd = *d;
     dd.ih = H2; dd.iw = W2; dd.ci = 32; dd.kh = kh2; dd.kw = kwt; dd.sh = 1; dd.sw = 1;
     dd.pad_top = 0; dd.pad_left = 0;
@@ -1672,6 +1694,7 @@ int gemm_tc_route(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const 
         if (d->co % 4 != 0 || d->co < 16) return 0;
         float* cols = static_cast<float*>(workspace(ctx, sizeof(float) * P * ldk));
         if (!cols) return fail("im2col: workspace allocation failed");
+        ctx->s2d_src = nullptr;   // the columns overwrite any lowered space-to-depth input
         im2col_k<<<grid_for(ctx, P * 32, 256, 8), 256, 3 * ldk * sizeof(int), ctx->stream>>>(a, cols, *d,
                                                                                               static_cast<int>(K),
                                                                                               static_cast<int>(ldk));

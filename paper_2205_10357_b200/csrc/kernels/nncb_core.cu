@@ -44,6 +44,7 @@ void* wt_buffer(nncb_ctx* ctx, size_t bytes) {
 void* workspace(nncb_ctx* ctx, size_t bytes) {
     if (bytes <= ctx->workspace_bytes) return ctx->workspace;
     if (ctx->workspace) ctx->retired.push_back(ctx->workspace);
+    ctx->s2d_src = nullptr;   // a lowered input in the old workspace is not carried over
     if (cudaMalloc(&ctx->workspace, bytes) != cudaSuccess) {
         ctx->workspace = nullptr;
         ctx->workspace_bytes = 0;

@@ -30,6 +30,11 @@ struct nncb_ctx {
     std::vector<void*> retired;          // outgrown scratch kept alive (captured graphs may use it)
     void* workspace = nullptr;           // im2col columns (separate from reduction scratch)
     size_t workspace_bytes = 0;
+    // the space-to-depth input most recently lowered into `workspace` (stream
+    // order): source, geometry and the workspace it lives in (NNCB_EPI_A_UNCHANGED)
+    const void* s2d_src = nullptr;
+    int64_t s2d_key[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    void* s2d_ws = nullptr;
     void* staging = nullptr;             // pinned upload ring (host_io.cu), created on first large h2d
     void* wt = nullptr;                  // transposed (K-major) forward weights, grown on demand
     size_t wt_bytes = 0;

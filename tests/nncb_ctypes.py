@@ -28,6 +28,7 @@ for name, res, args in [
     ("nncb_gemm_last_path", _I, []),
     ("nncb_gemm_set_manual_a", _I, [_I]),
     ("nncb_gemm_force_tile", _I, [_I]),
+    ("nncb_launch_count", ctypes.c_uint64, [_P]),
 ]:
     fn = getattr(K, name)
     fn.restype, fn.argtypes = res, args

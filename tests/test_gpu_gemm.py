@@ -267,3 +267,35 @@ def test_dgrad_relu_grad_epilogue(shape, tile, res):
     s2 = (want * xhat).reshape(-1, ci).sum(0)
     assert np.linalg.norm(raw[:ci] - s1) <= 2e-2 * np.linalg.norm(s1)
     assert np.linalg.norm(raw[ci:] - s2) <= 2e-2 * np.linalg.norm(s2)
+
+
+@pytest.mark.parametrize("shape", [(2, 32, 32, 3, 64, 7, 2), (2, 17, 23, 3, 32, 7, 2)])
+def test_s2d_wgrad_reuses_forward_lowering(shape):
+    """NNCB_EPI_A_UNCHANGED: a weight gradient after the forward conv on the
+    same activation reuses the forward's space-to-depth input (one lowering
+    launch fewer) and matches the exact wgrad; the hint on a different tensor
+    re-lowers (still correct)."""
+    n, ih, iw, ci, co, k, s = shape
+    g = conv_geom(n, ih, iw, ci, co, k, s)
+    rng = np.random.default_rng(5)
+    x = rng.uniform(-1, 1, (n, ih, iw, ci)).astype(np.float32)
+    x2 = rng.uniform(-1, 1, (n, ih, iw, ci)).astype(np.float32)
+    w = rng.uniform(-1, 1, (k, k, ci, co)).astype(np.float32)
+    gy = rng.uniform(-1, 1, (n, g["oh"], g["ow"], co)).astype(np.float32)
+    xd, x2d, wd, gyd = Dev(x), Dev(x2), Dev(w), Dev(gy)
+    y = Dev(nbytes=gy.nbytes)
+    dw = Dev(nbytes=w.nbytes)
+    gemm(GemmDesc(kind=CONV_WGRAD, precision=0, epilogue=16, **g), xd, gyd, None, dw)   # autotune outside the count
+    for xs, other in ((xd, None), (x2d, xd)):
+        ex = Dev(nbytes=w.nbytes)
+        gemm(GemmDesc(kind=CONV_WGRAD, precision=1, epilogue=0, **g), xs, gyd, None, ex)
+        gemm(GemmDesc(kind=CONV_FWD, precision=0, epilogue=0, **g), other or xs, wd, None, y)
+        before = K.nncb_launch_count(ctx())
+        dw = Dev(nbytes=w.nbytes)
+        gemm(GemmDesc(kind=CONV_WGRAD, precision=0, epilogue=16, **g), xs, gyd, None, dw)
+        launched = K.nncb_launch_count(ctx()) - before
+        assert K.nncb_gemm_last_path() == 1
+        check(dw.get(w.shape), ex.get(w.shape).astype(np.float64))
+        if other is None:
+            # reuse: no space-to-depth input launch (GEMM + weight fold-back [+ split-K reduce])
+            assert launched <= 3, launched
