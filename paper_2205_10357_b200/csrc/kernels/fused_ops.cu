@@ -120,6 +120,86 @@ __global__ void maxpool_bwd_k(const float* __restrict__ idx, const float* __rest
     }
 }
 
+// 3x3 stride-2 max pooling (the ResNet stem), 4 channels per thread, 32-bit
+// index decode (host: element counts < 2^31). All nine window rows are loaded
+// before the compare chain, which keeps the reference's scan order.
+__global__ void maxpool_fwd_k33(const float* __restrict__ x, float* __restrict__ y, float* __restrict__ idx,
+                                nncb_pool_geom g) {
+    const uint32_t C = (uint32_t)g.c, CV = C / 4, OW = (uint32_t)g.ow, OH = (uint32_t)g.oh;
+    const uint32_t IW = (uint32_t)g.iw, IH = (uint32_t)g.ih;
+    const uint32_t total = (uint32_t)(g.n * g.oh * g.ow) * CV;
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const uint32_t pix = t / CV, cv = t - pix * CV;
+        const uint32_t r = pix / OW, ow = pix - r * OW;
+        const uint32_t n = r / OH, oh = r - n * OH;
+        const float* p0 = x + ((size_t)(n * IH + 2 * oh) * IW + 2 * ow) * C + cv * 4;
+        float4 v[9];
+#pragma unroll
+        for (int dh = 0; dh < 3; ++dh)
+#pragma unroll
+            for (int dw = 0; dw < 3; ++dw) v[dh * 3 + dw] = __ldg(reinterpret_cast<const float4*>(p0 + ((size_t)dh * IW + dw) * C));
+        float4 best = v[0];
+        float4 bi = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int k = 1; k < 9; ++k) {   // strict '>': the first maximum in window order wins
+            if (v[k].x > best.x) { best.x = v[k].x; bi.x = (float)k; }
+            if (v[k].y > best.y) { best.y = v[k].y; bi.y = (float)k; }
+            if (v[k].z > best.z) { best.z = v[k].z; bi.z = (float)k; }
+            if (v[k].w > best.w) { best.w = v[k].w; bi.w = (float)k; }
+        }
+        const size_t at = (size_t)pix * C + cv * 4;
+        *reinterpret_cast<float4*>(y + at) = best;
+        if (idx) *reinterpret_cast<float4*>(idx + at) = bi;
+    }
+}
+
+// 3x3 stride-2 max-pool backward: input row h is covered by windows
+// oh in {h/2 - 1 (h even), h/2}, likewise for columns; the (up to) four
+// candidate windows are loaded together and added in ascending (oh, ow)
+// order, the reference's scatter order (bit-exact).
+__global__ void maxpool_bwd_k33(const float* __restrict__ idx, const float* __restrict__ gy, float* __restrict__ gx,
+                                nncb_pool_geom g) {
+    const uint32_t C = (uint32_t)g.c, CV = C / 4, OW = (uint32_t)g.ow, OH = (uint32_t)g.oh;
+    const uint32_t IW = (uint32_t)g.iw, IH = (uint32_t)g.ih;
+    const uint32_t total = (uint32_t)(g.n * g.ih * g.iw) * CV;
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const uint32_t pix = t / CV, cv = t - pix * CV;
+        const uint32_t r = pix / IW, w = pix - r * IW;
+        const uint32_t n = r / IH, h = r - n * IH;
+        const int hc1 = (int)(h >> 1), wc1 = (int)(w >> 1);
+        const int oh_c[2] = {hc1 - 1, hc1}, ow_c[2] = {wc1 - 1, wc1};
+        const bool oh_ok[2] = {(h & 1) == 0 && hc1 >= 1, hc1 < (int)OH};
+        const bool ow_ok[2] = {(w & 1) == 0 && wc1 >= 1, wc1 < (int)OW};
+        float4 ix[4], gv[4];
+        bool on[4];
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+                const int q = a * 2 + b;
+                on[q] = oh_ok[a] && ow_ok[b];
+                const size_t at = on[q] ? ((size_t)(n * OH + oh_c[a]) * OW + ow_c[b]) * C + cv * 4 : 0;
+                ix[q] = on[q] ? __ldg(reinterpret_cast<const float4*>(idx + at)) : make_float4(-1.f, -1.f, -1.f, -1.f);
+                gv[q] = on[q] ? __ldg(reinterpret_cast<const float4*>(gy + at)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+                const int q = a * 2 + b;
+                const float want = (float)(((int)h - 2 * oh_c[a]) * 3 + ((int)w - 2 * ow_c[b]));
+                if (on[q]) {
+                    if (ix[q].x == want) acc[0] = __fadd_rn(acc[0], gv[q].x);
+                    if (ix[q].y == want) acc[1] = __fadd_rn(acc[1], gv[q].y);
+                    if (ix[q].z == want) acc[2] = __fadd_rn(acc[2], gv[q].z);
+                    if (ix[q].w == want) acc[3] = __fadd_rn(acc[3], gv[q].w);
+                }
+            }
+        *reinterpret_cast<float4*>(gx + (size_t)pix * C + cv * 4) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    }
+}
+
 __device__ __forceinline__ int64_t a_start(int64_t o, int64_t in, int64_t out) { return (o * in) / out; }
 __device__ __forceinline__ int64_t a_end(int64_t o, int64_t in, int64_t out) { return ((o + 1) * in + out - 1) / out; }
 
@@ -805,7 +885,11 @@ extern "C" {
 int nncb_maxpool_fwd(nncb_ctx* ctx, const nncb_pool_geom* g, const float* x, float* y, float* idx) {
     int64_t total = g->n * g->oh * g->ow * g->c;
     if (total == 0) return 0;
-    if (g->c % 4 == 0)
+    const bool k33 = g->kh == 3 && g->kw == 3 && g->sh == 2 && g->sw == 2 && g->c % 4 == 0 &&
+                     std::max(total, g->n * g->ih * g->iw * g->c) < (int64_t(1) << 31);
+    if (k33)
+        maxpool_fwd_k33<<<nncb::grid_for(ctx, total / 4, 256), 256, 0, ctx->stream>>>(x, y, idx, *g);
+    else if (g->c % 4 == 0)
         maxpool_fwd_k<4><<<nncb::grid_for(ctx, total / 4, 256), 256, 0, ctx->stream>>>(x, y, idx, *g);
     else
         maxpool_fwd_k<1><<<nncb::grid_for(ctx, total, 256), 256, 0, ctx->stream>>>(x, y, idx, *g);
@@ -820,7 +904,7 @@ int nncb_maxpool_bwd(nncb_ctx* ctx, const nncb_pool_geom* g, const float* idx, c
     const bool i32 = std::max(total, out_total) < (int64_t(1) << 31);   // 32-bit index decode when it fits
     if (g->c % 4 == 0 && i32)
         if (g->kh == 3 && g->kw == 3 && g->sh == 2 && g->sw == 2)
-            maxpool_bwd_k<4, int, 1><<<nncb::grid_for(ctx, total / 4, 256), 256, 0, ctx->stream>>>(idx, gy, gx, *g);
+            maxpool_bwd_k33<<<nncb::grid_for(ctx, total / 4, 256), 256, 0, ctx->stream>>>(idx, gy, gx, *g);
         else
             maxpool_bwd_k<4, int><<<nncb::grid_for(ctx, total / 4, 256), 256, 0, ctx->stream>>>(idx, gy, gx, *g);
     else if (g->c % 4 == 0)

@@ -60,10 +60,11 @@ def test_maxpool_tie_and_grad_known_answer(known):
     assert gx.get((2,)).tolist() == k["gx"]
 
 
-@pytest.mark.parametrize("k,s", [(2, 2), (3, 2), (3, 1)])
-def test_maxpool_bitexact_with_ties(k, s):
+@pytest.mark.parametrize("k,s,shape", [(2, 2, (2, 9, 11, 8)), (3, 2, (2, 9, 11, 8)), (3, 1, (2, 9, 11, 8)),
+                                       (3, 2, (3, 10, 12, 64)), (3, 2, (1, 16, 15, 12))])
+def test_maxpool_bitexact_with_ties(k, s, shape):
     rng = np.random.default_rng(k * 10 + s)
-    x = rng.integers(-3, 4, (2, 9, 11, 8)).astype(np.float32)   # many exact ties
+    x = rng.integers(-3, 4, shape).astype(np.float32)   # many exact ties
     g, oshape = pool(x, k, s)
     y, idx, xd = Dev(nbytes=4 * int(np.prod(oshape))), Dev(nbytes=4 * int(np.prod(oshape))), Dev(x)
     ok(K.nncb_maxpool_fwd(ctx(), ctypes.byref(g), xd.p, y.p, idx.p))
