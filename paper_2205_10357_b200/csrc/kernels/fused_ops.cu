@@ -237,6 +237,22 @@ __device__ __forceinline__ void a_range(int h, int in, int out, int& lo, int& hi
     hi = e;
 }
 
+// Global average pooling backward (1x1 output): every input element of
+// image b, channel c receives 0 + gy[b, c] * (1 / (IH*IW)) -- the general
+// kernel's arithmetic for its single window (the +0 keeps a -0 product +0).
+__global__ void avgpool_bwd_global_k(const float* __restrict__ gy, float* __restrict__ gx, uint32_t hw, uint32_t CV,
+                                     uint32_t total) {
+    const float scale = __fdiv_rn(1.f, static_cast<float>(hw));
+    const uint32_t per_image = hw * CV;
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const uint32_t b = t / per_image, cv = (t - b * per_image) % CV;
+        const float4 q = __ldg(reinterpret_cast<const float4*>(gy) + (size_t)b * CV + cv);
+        reinterpret_cast<float4*>(gx)[t] =
+            make_float4(__fadd_rn(0.f, __fmul_rn(q.x, scale)), __fadd_rn(0.f, __fmul_rn(q.y, scale)),
+                        __fadd_rn(0.f, __fmul_rn(q.z, scale)), __fadd_rn(0.f, __fmul_rn(q.w, scale)));
+    }
+}
+
 template <int V, typename I>
 __global__ void avgpool_bwd_k(const float* __restrict__ gy, float* __restrict__ gx, int64_t n, int64_t ih, int64_t iw,
                               int64_t c, int64_t oh, int64_t ow) {
@@ -931,7 +947,10 @@ int nncb_avgpool_bwd(nncb_ctx* ctx, int64_t n, int64_t ih, int64_t iw, int64_t c
     int64_t total = n * ih * iw * c;
     if (total == 0) return 0;
     const bool i32 = std::max(total, n * oh * ow * c) < (int64_t(1) << 31);
-    if (c % 4 == 0 && i32)
+    if (oh == 1 && ow == 1 && c % 4 == 0 && i32)
+        avgpool_bwd_global_k<<<nncb::grid_for(ctx, total / 4, 256), 256, 0, ctx->stream>>>(
+            gy, gx, static_cast<uint32_t>(ih * iw), static_cast<uint32_t>(c / 4), static_cast<uint32_t>(total / 4));
+    else if (c % 4 == 0 && i32)
         avgpool_bwd_k<4, int><<<nncb::grid_for(ctx, total / 4, 256), 256, 0, ctx->stream>>>(gy, gx, n, ih, iw, c, oh, ow);
     else if (c % 4 == 0)
         avgpool_bwd_k<4, int64_t><<<nncb::grid_for(ctx, total / 4, 256), 256, 0, ctx->stream>>>(gy, gx, n, ih, iw, c, oh, ow);

@@ -240,3 +240,17 @@ def test_ew_two_fused_bn_grad_reductions():
         np.testing.assert_allclose(sg.get((C,)), ref_g.get((C,)), rtol=1e-5, atol=1e-5)
         np.testing.assert_allclose(sgx.get((C,)), ref_gx.get((C,)), rtol=1e-5, atol=1e-5)
     assert np.array_equal(out.get((rows, C)), gr)
+
+
+def test_global_avgpool_grad_signed_zero_bitwise():
+    """Global pooling backward bit for bit (uint32 view), including gy = -0.0
+    (0 + (-0) * scale = +0 in the reference's accumulation)."""
+    n, ih, iw, c = 2, 7, 7, 2048
+    gy = np.random.default_rng(9).uniform(-1, 1, (n, 1, 1, c)).astype(np.float32)
+    gy.reshape(-1)[::7] = -0.0
+    gy.reshape(-1)[1::7] = 0.0
+    gyd, gx = Dev(gy), Dev(nbytes=n * ih * iw * c * 4)
+    ok(K.nncb_avgpool_bwd(ctx(), n, ih, iw, c, 1, 1, gyd.p, gx.p))
+    ogx = np.zeros((n, ih, iw, c), np.float32)
+    O.lib().o_avgpool_grad(O._f(gy), O._f(ogx), *[O.I64(v) for v in (n, ih, iw, c, 1, 1)])
+    assert np.array_equal(gx.get((n, ih, iw, c)).view(np.uint32), ogx.view(np.uint32))
