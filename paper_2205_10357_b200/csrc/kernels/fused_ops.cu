@@ -153,50 +153,53 @@ __global__ void maxpool_fwd_k33(const float* __restrict__ x, float* __restrict__
     }
 }
 
-// 3x3 stride-2 max-pool backward: input row h is covered by windows
-// oh in {h/2 - 1 (h even), h/2}, likewise for columns; the (up to) four
-// candidate windows are loaded together and added in ascending (oh, ow)
-// order, the reference's scatter order (bit-exact).
+// 3x3 stride-2 max-pool backward over 2x2 input blocks: rows 2a, 2a+1 and
+// columns 2b, 2b+1 are covered only by windows oh in {a-1, a}, ow in {b-1, b}
+// (odd rows / columns by a / b alone). Each thread loads those four windows
+// once (index and gradient) and writes its block, every pixel adding its
+// windows in ascending (oh, ow) order -- the reference's scatter order.
 __global__ void maxpool_bwd_k33(const float* __restrict__ idx, const float* __restrict__ gy, float* __restrict__ gx,
                                 nncb_pool_geom g) {
     const uint32_t C = (uint32_t)g.c, CV = C / 4, OW = (uint32_t)g.ow, OH = (uint32_t)g.oh;
-    const uint32_t IW = (uint32_t)g.iw, IH = (uint32_t)g.ih;
-    const uint32_t total = (uint32_t)(g.n * g.ih * g.iw) * CV;
+    const uint32_t IW = (uint32_t)g.iw, IH = (uint32_t)g.ih, BW = (IW + 1) / 2, BH = (IH + 1) / 2;
+    const uint32_t total = (uint32_t)g.n * BH * BW * CV;
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-        const uint32_t pix = t / CV, cv = t - pix * CV;
-        const uint32_t r = pix / IW, w = pix - r * IW;
-        const uint32_t n = r / IH, h = r - n * IH;
-        const int hc1 = (int)(h >> 1), wc1 = (int)(w >> 1);
-        const int oh_c[2] = {hc1 - 1, hc1}, ow_c[2] = {wc1 - 1, wc1};
-        const bool oh_ok[2] = {(h & 1) == 0 && hc1 >= 1, hc1 < (int)OH};
-        const bool ow_ok[2] = {(w & 1) == 0 && wc1 >= 1, wc1 < (int)OW};
+        const uint32_t blk = t / CV, cv = t - blk * CV;
+        const uint32_t r = blk / BW, b = blk - r * BW;
+        const uint32_t n = r / BH, a = r - n * BH;
+        // windows q = (a-1, b-1), (a-1, b), (a, b-1), (a, b)
         float4 ix[4], gv[4];
         bool on[4];
 #pragma unroll
-        for (int a = 0; a < 2; ++a)
+        for (int q = 0; q < 4; ++q) {
+            const int oh = (int)a - 1 + (q >> 1), ow = (int)b - 1 + (q & 1);
+            on[q] = oh >= 0 && oh < (int)OH && ow >= 0 && ow < (int)OW;
+            const size_t at = on[q] ? ((size_t)(n * OH + oh) * OW + ow) * C + cv * 4 : 0;
+            ix[q] = on[q] ? __ldg(reinterpret_cast<const float4*>(idx + at)) : make_float4(-1.f, -1.f, -1.f, -1.f);
+            gv[q] = on[q] ? __ldg(reinterpret_cast<const float4*>(gy + at)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
 #pragma unroll
-            for (int b = 0; b < 2; ++b) {
-                const int q = a * 2 + b;
-                on[q] = oh_ok[a] && ow_ok[b];
-                const size_t at = on[q] ? ((size_t)(n * OH + oh_c[a]) * OW + ow_c[b]) * C + cv * 4 : 0;
-                ix[q] = on[q] ? __ldg(reinterpret_cast<const float4*>(idx + at)) : make_float4(-1.f, -1.f, -1.f, -1.f);
-                gv[q] = on[q] ? __ldg(reinterpret_cast<const float4*>(gy + at)) : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int dy = 0; dy < 2; ++dy)
 #pragma unroll
-        for (int a = 0; a < 2; ++a)
+            for (int dx = 0; dx < 2; ++dx) {
+                const uint32_t h = 2 * a + dy, w = 2 * b + dx;
+                if (h >= IH || w >= IW) continue;
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int b = 0; b < 2; ++b) {
-                const int q = a * 2 + b;
-                const float want = (float)(((int)h - 2 * oh_c[a]) * 3 + ((int)w - 2 * ow_c[b]));
-                if (on[q]) {
+                for (int q = 0; q < 4; ++q) {
+                    const int wy = q >> 1, wx = q & 1;   // window row a-1+wy, column b-1+wx
+                    if ((dy == 1 && wy == 0) || (dx == 1 && wx == 0)) continue;   // odd rows/cols: one window
+                    // offset of pixel (h, w) inside window (a-1+wy, b-1+wx)
+                    const float want = (float)((dy + 2 * (1 - wy)) * 3 + (dx + 2 * (1 - wx)));
+                    if (!on[q]) continue;
                     if (ix[q].x == want) acc[0] = __fadd_rn(acc[0], gv[q].x);
                     if (ix[q].y == want) acc[1] = __fadd_rn(acc[1], gv[q].y);
                     if (ix[q].z == want) acc[2] = __fadd_rn(acc[2], gv[q].z);
                     if (ix[q].w == want) acc[3] = __fadd_rn(acc[3], gv[q].w);
                 }
+                *reinterpret_cast<float4*>(gx + ((size_t)(n * IH + h) * IW + w) * C + cv * 4) =
+                    make_float4(acc[0], acc[1], acc[2], acc[3]);
             }
-        *reinterpret_cast<float4*>(gx + (size_t)pix * C + cv * 4) = make_float4(acc[0], acc[1], acc[2], acc[3]);
     }
 }
 
@@ -920,7 +923,7 @@ int nncb_maxpool_bwd(nncb_ctx* ctx, const nncb_pool_geom* g, const float* idx, c
     const bool i32 = std::max(total, out_total) < (int64_t(1) << 31);   // 32-bit index decode when it fits
     if (g->c % 4 == 0 && i32)
         if (g->kh == 3 && g->kw == 3 && g->sh == 2 && g->sw == 2)
-            maxpool_bwd_k33<<<nncb::grid_for(ctx, total / 4, 256), 256, 0, ctx->stream>>>(idx, gy, gx, *g);
+            maxpool_bwd_k33<<<nncb::grid_for(ctx, total / 16, 256), 256, 0, ctx->stream>>>(idx, gy, gx, *g);
         else
             maxpool_bwd_k<4, int><<<nncb::grid_for(ctx, total / 4, 256), 256, 0, ctx->stream>>>(idx, gy, gx, *g);
     else if (g->c % 4 == 0)
