@@ -54,6 +54,14 @@ int nnc_model_run_outputs(nnc_model* m, int role, const char* names);
 int nnc_model_output(nnc_model* m, const char* name, float* out, int64_t n);
 
 int nnc_model_train_step(nnc_model* m, const float* target, int64_t n, double lr, double* loss);
+/* Pipelined training from host buffers: stage the current inputs + target of
+ * step i + 1 (host bytes are consumed on return; the upload runs on the copy
+ * stream) while step i computes. Order per step: train_step_staged (launch the
+ * oldest staged step), stage_step (the next one), staged_loss (wait for the
+ * launched step's loss). Same result as nnc_model_train_step per step.     */
+int nnc_model_stage_step(nnc_model* m, const float* target, int64_t n);
+int nnc_model_train_step_staged(nnc_model* m, double lr);
+int nnc_model_staged_loss(nnc_model* m, double* loss);
 int nnc_model_gradients(nnc_model* m, const float* target, int64_t n, double* loss);
 int nnc_model_grad(nnc_model* m, const char* weight, float* out, int64_t n);
 

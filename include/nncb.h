@@ -57,6 +57,18 @@ int nncb_event_record(nncb_ctx* ctx, void* ev);
 int nncb_event_elapsed_ms(void* start, void* stop, float* ms);
 int nncb_event_destroy(void* ev);
 
+/* Input pipelining: uploads on the context's copy stream overlap the compute
+ * stream. nncb_h2d_async returns once the host bytes are handed to DMA (a
+ * pageable source is first copied into the pinned ring by the copy threads),
+ * so `src` may be reused on return; the device bytes are valid after the
+ * copy stream reaches that point (nncb_event_record_on / nncb_stream_wait). */
+enum nncb_stream_id { NNCB_STREAM_COMPUTE = 0, NNCB_STREAM_COPY = 1 };
+int nncb_h2d_async(nncb_ctx* ctx, void* dst, const void* src, size_t bytes);
+int nncb_d2h_async(nncb_ctx* ctx, void* dst_pinned, const void* src, size_t bytes);   /* compute stream */
+int nncb_event_record_on(nncb_ctx* ctx, int stream, void* ev);
+int nncb_stream_wait(nncb_ctx* ctx, int stream, void* ev);
+int nncb_event_sync(void* ev);
+
 /* Number of nncb kernel launches issued on this context (all families). */
 uint64_t nncb_launch_count(nncb_ctx* ctx);
 

@@ -19,7 +19,7 @@ from __future__ import annotations
 import ctypes
 import json
 import os
-from typing import Dict, Optional, Sequence
+from typing import Dict, List, Optional, Sequence
 
 import numpy as np
 
@@ -66,6 +66,9 @@ def _load():
         "nnc_model_run": (I, [P, I]),
         "nnc_model_output": (I, [P, S, FP, I64]),
         "nnc_model_train_step": (I, [P, FP, I64, D, DP]),
+        "nnc_model_stage_step": (I, [P, FP, I64]),
+        "nnc_model_train_step_staged": (I, [P, D]),
+        "nnc_model_staged_loss": (I, [P, DP]),
         "nnc_model_gradients": (I, [P, FP, I64, DP]),
         "nnc_model_grad": (I, [P, S, FP, I64]),
         "nnc_model_trainer_prepare": (I, [P, FP, I64]),
@@ -214,6 +217,35 @@ class CompiledModel:
         loss = ctypes.c_double()
         _check(_host.nnc_model_train_step(self._h, _fptr(t), t.size, lr, ctypes.byref(loss)))
         return loss.value
+
+    def train_steps(self, batches, lr: float) -> List[float]:
+        """One training step per (inputs, target) pair of `batches` (any
+        iterable), from host buffers, returning each step's loss. The upload of
+        step i + 1 runs on the copy stream while step i computes; each step's
+        result equals train_step's."""
+        it = iter(batches)
+        losses: List[float] = []
+        first = next(it, None)
+        if first is None:
+            return losses
+        self._stage(*first)
+        pending = next(it, None)   # the step after the one being launched
+        loss = ctypes.c_double()
+        while True:
+            _check(_host.nnc_model_train_step_staged(self._h, lr))
+            staged_next = pending is not None
+            if staged_next:
+                self._stage(*pending)   # uploads while the launched step computes
+                pending = next(it, None)
+            _check(_host.nnc_model_staged_loss(self._h, ctypes.byref(loss)))
+            losses.append(loss.value)
+            if not staged_next:
+                return losses
+
+    def _stage(self, inputs: Dict[str, np.ndarray], target: np.ndarray):
+        keep = self._borrow(inputs)   # noqa: F841  (host bytes are consumed before the call returns)
+        t = np.ascontiguousarray(target, dtype=np.float32)
+        _check(_host.nnc_model_stage_step(self._h, _fptr(t), t.size))
 
     def gradients(self, inputs: Dict[str, np.ndarray], target: np.ndarray):
         keep = self._borrow(inputs)   # noqa: F841

@@ -269,6 +269,25 @@ int nnc_model_train_step(nnc_model* m, const float* target, int64_t n, double lr
     return rc;
 }
 
+// Pipelined training from host buffers (runtime::Trainer::stage / launch_staged /
+// staged_loss): stage step i + 1 while step i computes.
+int nnc_model_stage_step(nnc_model* m, const float* target, int64_t n) {
+    const int rc = guarded([&] {
+        runtime::Trainer& t = runtime::shared_trainer(m->plans, *m->host, runtime::default_device(), m->opts);
+        t.stage(m->inputs, target_tensor(m, target, n));
+    });
+    drop_views(m);
+    return rc;
+}
+
+int nnc_model_train_step_staged(nnc_model* m, double lr) {
+    return guarded([&] { runtime::shared_trainer(m->plans, *m->host, runtime::default_device(), m->opts).launch_staged(lr); });
+}
+
+int nnc_model_staged_loss(nnc_model* m, double* loss) {
+    return guarded([&] { *loss = runtime::shared_trainer(m->plans, *m->host, runtime::default_device(), m->opts).staged_loss(); });
+}
+
 int nnc_model_gradients(nnc_model* m, const float* target, int64_t n, double* loss) {
     const int rc = guarded([&] { m->grads = runtime::gradients(m->plans, m->inputs, target_tensor(m, target, n), *m->host, loss, nullptr, m->opts); });
     drop_views(m);

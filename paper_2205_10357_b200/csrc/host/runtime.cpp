@@ -1075,6 +1075,18 @@ struct Trainer::Impl {
     std::vector<std::pair<int64_t, int64_t>> buckets;   // (offset, count) in reverse backward order
     uint64_t launches_per_step = 0;
     bool warmed = false;
+    // pipelined stepping (stage / launch_staged / staged_loss): two staging slots
+    struct Slot {
+        std::vector<void*> in;            // per train_fwd input slot, in input_slots order
+        void* tgt = nullptr;
+        void* ready = nullptr;            // copy stream: slot filled
+        void* consumed = nullptr;         // compute stream: slot copied into the step's inputs
+        bool used = false;
+    };
+    Slot slots[2];
+    uint64_t n_staged = 0, n_launched = 0;
+    double* loss_host = nullptr;          // pinned
+    void* loss_ev = nullptr;
 
     ~Impl() {
         try {
@@ -1084,6 +1096,15 @@ struct Trainer::Impl {
         if (graph) nncb_graph_destroy(graph);
         if (graph_nosgd) nncb_graph_destroy(graph_nosgd);
         nncb_ctx* ctx = dev->ctx();
+        nncb_sync(ctx);
+        for (Slot& s : slots) {
+            for (void* p : s.in) nncb_free(ctx, p);
+            if (s.tgt) nncb_free(ctx, s.tgt);
+            for (void* e : {s.ready, s.consumed})
+                if (e) nncb_event_destroy(e);
+        }
+        if (loss_ev) nncb_event_destroy(loss_ev);
+        if (loss_host) nncb_host_free(loss_host);
         for (void* p : {params, grads, target, loss})
             if (p) nncb_free(ctx, p);
     }
@@ -1317,6 +1338,68 @@ double Trainer::step(const std::map<std::string, Tensor>& inputs, const Tensor& 
 }
 
 void Trainer::step_device(double lr) { impl->run(lr, true); }
+
+void Trainer::stage(const std::map<std::string, Tensor>& inputs, const Tensor& target) {
+    Impl& I = *impl;
+    const ExecutionPlan& p = I.plans->train_fwd;
+    check_inputs(p, inputs);
+    nncb_ctx* ctx = I.dev->ctx();
+    Impl::Slot& S = I.slots[I.n_staged % 2];
+    if (!S.ready) {
+        for (uint32_t s : p.input_slots) {
+            void* b = nullptr;
+            NNC_CHECK(nncb_malloc(ctx, static_cast<size_t>(element_count(p.values[s].dims)) * 4, &b));
+            S.in.push_back(b);
+        }
+        NNC_CHECK(nncb_malloc(ctx, std::max<size_t>(target.byte_size(), 16), &S.tgt));
+        NNC_CHECK(nncb_event_create(&S.ready));
+        NNC_CHECK(nncb_event_create(&S.consumed));
+    }
+    if (target.elements() != element_count(p.values[p.find_value(I.pred)].dims))
+        throw Error(Error::Code::ShapeMismatch, "stage: target size differs from the prediction");
+    if (S.used) NNC_CHECK(nncb_stream_wait(ctx, NNCB_STREAM_COPY, S.consumed));   // the step reading it has copied it out
+    for (size_t k = 0; k < p.input_slots.size(); ++k) {
+        const Tensor& t = inputs.at(p.values[p.input_slots[k]].name);
+        NNC_CHECK(nncb_h2d_async(ctx, S.in[k], t.data(), t.byte_size()));
+    }
+    NNC_CHECK(nncb_h2d_async(ctx, S.tgt, target.data(), target.byte_size()));
+    NNC_CHECK(nncb_event_record_on(ctx, NNCB_STREAM_COPY, S.ready));
+    ++I.n_staged;
+}
+
+void Trainer::launch_staged(double lr) {
+    Impl& I = *impl;
+    if (I.n_launched >= I.n_staged) throw Error(Error::Code::BadDocument, "launch_staged: no staged step");
+    const ExecutionPlan& p = I.plans->train_fwd;
+    nncb_ctx* ctx = I.dev->ctx();
+    Impl::Slot& S = I.slots[I.n_launched % 2];
+    NNC_CHECK(nncb_stream_wait(ctx, NNCB_STREAM_COMPUTE, S.ready));
+    for (size_t k = 0; k < p.input_slots.size(); ++k) {
+        const std::string& name = p.values[p.input_slots[k]].name;
+        NNC_CHECK(nncb_d2d(ctx, I.prog->ptr(name), S.in[k], static_cast<size_t>(element_count(p.values[p.input_slots[k]].dims)) * 4));
+    }
+    const int64_t n = element_count(p.values[p.find_value(I.pred)].dims);
+    NNC_CHECK(nncb_d2d(ctx, I.target, S.tgt, static_cast<size_t>(n) * 4));
+    NNC_CHECK(nncb_event_record_on(ctx, NNCB_STREAM_COMPUTE, S.consumed));
+    S.used = true;
+    I.run(lr, true);
+    if (!I.loss_host) {
+        void* h = nullptr;
+        NNC_CHECK(nncb_host_alloc(sizeof(double), &h));
+        I.loss_host = static_cast<double*>(h);
+        NNC_CHECK(nncb_event_create(&I.loss_ev));
+    }
+    NNC_CHECK(nncb_d2h_async(ctx, I.loss_host, I.loss, sizeof(double)));
+    NNC_CHECK(nncb_event_record_on(ctx, NNCB_STREAM_COMPUTE, I.loss_ev));
+    ++I.n_launched;
+}
+
+double Trainer::staged_loss() {
+    Impl& I = *impl;
+    if (!I.loss_ev) throw Error(Error::Code::BadDocument, "staged_loss: no step launched");
+    NNC_CHECK(nncb_event_sync(I.loss_ev));
+    return *I.loss_host;
+}
 
 double Trainer::last_loss() {
     double loss = 0;

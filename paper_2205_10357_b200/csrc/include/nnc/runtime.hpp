@@ -171,6 +171,17 @@ struct Trainer {
     /// Device-resident variant (no host copies): enqueue one step.
     void step_device(double lr);
     double last_loss();
+    /// Pipelined stepping from host buffers. stage() uploads the next step's
+    /// inputs + target into one of two device staging slots on the copy
+    /// stream (the host bytes are consumed on return); launch_staged() makes
+    /// the compute stream wait for the oldest staged slot, copies it into the
+    /// step's input values (device to device), replays the step and reads the
+    /// loss back asynchronously; staged_loss() waits for that loss. Calling
+    /// stage(i + 1) between launch_staged() and staged_loss() of step i
+    /// overlaps the upload of step i + 1 with the compute of step i.
+    void stage(const std::map<std::string, Tensor>& inputs, const Tensor& target);
+    void launch_staged(double lr);
+    double staged_loss();
     /// One eager step with CUDA events around every launch on the compute
     /// stream: (label, kind, ms, algorithmic bytes, algorithmic flops) per launch.
     struct LaunchTiming {

@@ -166,9 +166,43 @@ void staging_release(nncb_ctx* c) {
     c->staging = nullptr;
 }
 
+// Pageable upload through the pinned ring on `stream`: the copy threads fill
+// chunk i while the DMA of chunk i-1 (and i-2) runs.
+int h2d_staged(nncb_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t stream, bool allow_ring) {
+    cudaPointerAttributes attr{};
+    const bool pinned = cudaPointerGetAttributes(&attr, src) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    Staging* s = (allow_ring && bytes >= kStagedMin && !pinned) ? staging_for(c) : nullptr;
+    if (!s || !s->ok) {
+        NNCB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream));
+        if (!pinned) NNCB_CUDA(cudaStreamSynchronize(stream));   // pageable: src is reusable on return
+        return 0;
+    }
+    int slot = 0;
+    for (size_t off = 0; off < bytes; off += kChunk, slot = (slot + 1) % kRing) {
+        const size_t n = std::min(kChunk, bytes - off);
+        NNCB_CUDA(cudaEventSynchronize(s->ev[slot]));   // previous DMA out of this chunk has drained
+        parallel_copy(s->pin[slot], static_cast<const char*>(src) + off, n);
+        NNCB_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, s->pin[slot], n, cudaMemcpyHostToDevice, stream));
+        NNCB_CUDA(cudaEventRecord(s->ev[slot], stream));
+    }
+    return 0;
+}
+
 }  // namespace nncb
 
 extern "C" {
+
+int nncb_h2d_async(nncb_ctx* c, void* dst, const void* src, size_t bytes) {
+    if (!bytes) return 0;
+    return nncb::h2d_staged(c, dst, src, bytes, c->copy_stream, true);
+}
+
+int nncb_d2h_async(nncb_ctx* c, void* dst, const void* src, size_t bytes) {
+    if (!bytes) return 0;
+    NNCB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+    return 0;
+}
 
 int nncb_h2d(nncb_ctx* c, void* dst, const void* src, size_t bytes) {
     if (!bytes) return 0;

@@ -77,6 +77,7 @@ int nncb_create(int device, nncb_ctx** out) {
     c->sm_count = prop.multiProcessorCount;
     NNCB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     NNCB_CUDA(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    NNCB_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     *out = c;
     return 0;
 }
@@ -85,6 +86,7 @@ int nncb_destroy(nncb_ctx* c) {
     if (!c) return 0;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
+    cudaStreamSynchronize(c->copy_stream);
     nncb_comm_destroy(c);
     for (auto& [k, v] : c->ew_cache) {
         (void)k;
@@ -97,6 +99,7 @@ int nncb_destroy(nncb_ctx* c) {
     if (c->wt) cudaFree(c->wt);
     cudaStreamDestroy(c->stream);
     cudaStreamDestroy(c->comm_stream);
+    cudaStreamDestroy(c->copy_stream);
     delete c;
     return 0;
 }
@@ -189,6 +192,21 @@ int nncb_event_create(void** ev) {
 
 int nncb_event_record(nncb_ctx* c, void* ev) {
     NNCB_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev), c->stream));
+    return 0;
+}
+
+int nncb_event_record_on(nncb_ctx* c, int stream, void* ev) {
+    NNCB_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev), stream == NNCB_STREAM_COPY ? c->copy_stream : c->stream));
+    return 0;
+}
+
+int nncb_stream_wait(nncb_ctx* c, int stream, void* ev) {
+    NNCB_CUDA(cudaStreamWaitEvent(stream == NNCB_STREAM_COPY ? c->copy_stream : c->stream, static_cast<cudaEvent_t>(ev), 0));
+    return 0;
+}
+
+int nncb_event_sync(void* ev) {
+    NNCB_CUDA(cudaEventSynchronize(static_cast<cudaEvent_t>(ev)));
     return 0;
 }
 

@@ -19,6 +19,7 @@ struct nncb_ctx {
     int sm_count = 148;
     cudaStream_t stream = nullptr;       // compute stream
     cudaStream_t comm_stream = nullptr;  // collectives
+    cudaStream_t copy_stream = nullptr;  // pipelined input uploads (nncb_h2d_async)
     std::atomic<uint64_t> launches{0};
     void* nccl_comm = nullptr;
     int nranks = 1, rank = 0;

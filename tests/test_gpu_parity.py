@@ -188,3 +188,19 @@ def test_relu_grad_epilogue_fusion_matches_separate_pass(monkeypatch):
     assert abs(loss_b - loss_a) <= 1e-3 * abs(loss_a)
     for w, g in grads_a.items():
         assert rel_err(grads_b[w], g) < 2e-2, w
+
+
+def test_pipelined_train_steps_match_sequential():
+    """train_steps (upload of step i+1 on the copy stream while step i runs)
+    gives bitwise the same losses and weights as one train_step per batch."""
+    doc = W.c1_small_cnn(8, bn=True)
+    batches = [({"x": W.uniform((8, 32, 32, 3), 10 + i, "x")}, W.uniform((8, 10), 20 + i, "t")) for i in range(4)]
+    a = P.CompiledModel(doc, precision=P.PREC_TF32)
+    b = P.CompiledModel(doc, precision=P.PREC_TF32)
+    seq = [a.train_step(x, t, 0.05) for x, t in batches]
+    pipe = b.train_steps(batches, 0.05)
+    assert seq == pipe
+    for w in a.weight_shapes:
+        assert np.array_equal(a.weight(w), b.weight(w)), w
+    assert b.train_steps([], 0.05) == []
+    assert len(b.train_steps(batches[:1], 0.05)) == 1
