@@ -298,19 +298,20 @@ int nvrtc_fail(nvrtcProgram prog, nvrtcResult r, const std::string& src) {
     return nncb::fail(std::string("NVRTC: ") + nvrtcGetErrorString(r) + "\n" + log + "\n--- source ---\n" + src);
 }
 
-// Folds the per-block partials of a REDUCE_BN_GRAD group: block (32 x 32)
-// owns 32 channels, lane row y sums blocks k = y, y+32, ... and the 32 rows are
-// folded in order (deterministic). For C > 1024 block k only covers the
-// channels [(1024 k) % C, +1024).
+// Folds the per-block partials of a REDUCE_BN_GRAD group: a block of 1024
+// threads owns 8 channels; lane row y (0..127) sums the main kernel's blocks
+// k = y, y+128, ... and the 128 rows are folded by a fixed tree
+// (deterministic). For C > 1024 main-kernel block k only covers the channels
+// [(1024 k) % C, +1024).
 __global__ void __launch_bounds__(1024) ew_red_final_k(const double* __restrict__ part, int grid, int C,
                                                        float* __restrict__ sg, float* __restrict__ sgx) {
-    __shared__ double fold[2][32][33];
-    const int tx = threadIdx.x, ty = threadIdx.y;
-    const int c = blockIdx.x * 32 + tx;
+    __shared__ double fold[2][128][8];
+    const int tx = threadIdx.x % 8, ty = threadIdx.x / 8;
+    const int c = blockIdx.x * 8 + tx;
     double a = 0.0, b = 0.0;
     if (c < C) {
-#pragma unroll 4
-        for (int k = ty; k < grid; k += 32) {
+#pragma unroll 2
+        for (int k = ty; k < grid; k += 128) {
             if (C > 1024) {
                 const int start = static_cast<int>((static_cast<long long>(k) * 1024) % C);
                 if ((c - start + C) % C >= 1024) continue;
@@ -322,13 +323,16 @@ __global__ void __launch_bounds__(1024) ew_red_final_k(const double* __restrict_
     fold[0][ty][tx] = a;
     fold[1][ty][tx] = b;
     __syncthreads();
-    if (ty == 0 && c < C) {
-        for (int y = 1; y < 32; ++y) {
-            a += fold[0][y][tx];
-            b += fold[1][y][tx];
+    for (int h = 64; h >= 1; h >>= 1) {
+        if (ty < h) {
+            fold[0][ty][tx] += fold[0][ty + h][tx];
+            fold[1][ty][tx] += fold[1][ty + h][tx];
         }
-        sg[c] = static_cast<float>(a);
-        sgx[c] = static_cast<float>(b);
+        __syncthreads();
+    }
+    if (ty == 0 && c < C) {
+        sg[c] = static_cast<float>(fold[0][0][tx]);
+        sgx[c] = static_cast<float>(fold[1][0][tx]);
     }
 }
 
@@ -469,7 +473,7 @@ int nncb_ew_launch(nncb_ctx* ctx, nncb_ew_kernel* k, void* const* slots, int64_t
     if (reduce) {
         const int C = static_cast<int>(channels);
         for (int q = 0; q < k->n_reduce; ++q) {
-            ew_red_final_k<<<(C + 31) / 32, dim3(32, 32), 0, ctx->stream>>>(
+            ew_red_final_k<<<(C + 7) / 8, 1024, 0, ctx->stream>>>(
                 args.part + static_cast<size_t>(q) * grid * 2 * C, static_cast<int>(grid), C, args.p[k->reduce_sg[q]],
                 args.p[k->reduce_sgx[q]]);
             NNCB_CUDA(cudaGetLastError());
