@@ -227,6 +227,10 @@ std::string generate(const nncb_ew_program& p, bool uses_ch) {
         os << "extern \"C\" __global__ void __launch_bounds__(256, " << min_blocks << ") nnc_fused_ew(const EwArgs A) {";
     else
         os << "extern \"C\" __global__ void __launch_bounds__(256) nnc_fused_ew(const EwArgs A) {";
+    // reduction groups: the finalize kernel is a programmatic dependent
+    // launch; let it be scheduled while this grid drains (it waits on
+    // griddepcontrol.wait for this grid's completion and memory)
+    if (red) os << "\n  asm volatile(\"griddepcontrol.launch_dependents;\");";
     os << R"(
   const i64 nvec = A.n >> 2;
   const i64 stride = (i64)gridDim.x * blockDim.x;
@@ -306,6 +310,9 @@ int nvrtc_fail(nvrtcProgram prog, nvrtcResult r, const std::string& src) {
 __global__ void __launch_bounds__(1024) ew_red_final_k(const double* __restrict__ part, int grid, int C,
                                                        float* __restrict__ sg, float* __restrict__ sgx) {
     __shared__ double fold[2][128][8];
+    // programmatic dependent launch: the reducing grid's partials are
+    // complete and visible past this point
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int tx = threadIdx.x % 8, ty = threadIdx.x / 8;
     const int c = blockIdx.x * 8 + tx;
     double a = 0.0, b = 0.0;
@@ -459,7 +466,8 @@ int nncb_ew_launch(nncb_ctx* ctx, nncb_ew_kernel* k, void* const* slots, int64_t
         if (!args.cs || C < 4 || C > 2048 || (C & (C - 1)))
             return nncb::fail("nncb_ew_launch: REDUCE_BN_GRAD needs the channel-stationary launch (C power of 2 <= 2048)");
         const int64_t g = C / std::gcd<int64_t>(C, 1024);
-        const int64_t cap = std::max<int64_t>(g, (4 * static_cast<int64_t>(ctx->sm_count) / g) * g);
+        static const int64_t per_sm = getenv("NNCB_EW_RED_BLOCKS") ? std::max(1, atoi(getenv("NNCB_EW_RED_BLOCKS"))) : 4;
+        const int64_t cap = std::max<int64_t>(g, (per_sm * static_cast<int64_t>(ctx->sm_count) / g) * g);
         if (grid > cap) grid = static_cast<unsigned>(cap);
         args.part = static_cast<double*>(nncb::scratch(ctx, sizeof(double) * 2 * C * grid * k->n_reduce));
         if (!args.part) return nncb::fail("nncb_ew_launch: reduction scratch allocation failed");
@@ -473,10 +481,17 @@ int nncb_ew_launch(nncb_ctx* ctx, nncb_ew_kernel* k, void* const* slots, int64_t
     if (reduce) {
         const int C = static_cast<int>(channels);
         for (int q = 0; q < k->n_reduce; ++q) {
-            ew_red_final_k<<<(C + 7) / 8, 1024, 0, ctx->stream>>>(
-                args.part + static_cast<size_t>(q) * grid * 2 * C, static_cast<int>(grid), C, args.p[k->reduce_sg[q]],
-                args.p[k->reduce_sgx[q]]);
-            NNCB_CUDA(cudaGetLastError());
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(static_cast<unsigned>((C + 7) / 8));
+            cfg.blockDim = dim3(1024);
+            cfg.stream = ctx->stream;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = q == 0 ? 1 : 0;   // the first follows the reducing grid
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            NNCB_CUDA(cudaLaunchKernelEx(&cfg, ew_red_final_k, static_cast<const double*>(args.part + static_cast<size_t>(q) * grid * 2 * C),
+                                         static_cast<int>(grid), C, args.p[k->reduce_sg[q]], args.p[k->reduce_sgx[q]]));
             ctx->launches.fetch_add(1, std::memory_order_relaxed);
         }
     }
