@@ -537,6 +537,7 @@ __global__ void sum_rows_exact_k(const float* __restrict__ x, float* __restrict_
 
 __global__ void bn_finalize_k(const double* __restrict__ cs, float* __restrict__ stats, int64_t rows, int64_t C,
                               double eps) {
+    nncb::pdl_wait();   // launched as a programmatic dependent of the producing GEMM / reduction
     int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= C) return;
     double mean = cs[c] / (double)rows;
@@ -989,6 +990,7 @@ int nncb_bn_stats(nncb_ctx* ctx, const float* x, float* stats, int64_t rows, int
 namespace {
 __global__ void colsums_to_float_k(const double* __restrict__ s, float* __restrict__ o0, float* __restrict__ o1,
                                    int64_t C) {
+    nncb::pdl_wait();
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c < C) {
         o0[c] = static_cast<float>(s[c]);
@@ -999,14 +1001,16 @@ __global__ void colsums_to_float_k(const double* __restrict__ s, float* __restri
 
 int nncb_colsums_to_float(nncb_ctx* ctx, const double* sums, float* out0, float* out1, int64_t C) {
     if (C <= 0) return 0;
-    colsums_to_float_k<<<(unsigned)((C + 255) / 256), 256, 0, ctx->stream>>>(sums, out0, out1, C);
+    NNCB_CUDA(nncb::launch_pdl(colsums_to_float_k, dim3((unsigned)((C + 255) / 256)), dim3(256), ctx->stream, sums, out0,
+                               out1, C));
     NNCB_LAUNCHED(ctx);
     return 0;
 }
 
 int nncb_bn_finalize(nncb_ctx* ctx, const double* colstats, float* stats, int64_t rows, int64_t C, double eps) {
     if (C <= 0) return 0;
-    bn_finalize_k<<<(unsigned)((C + 127) / 128), 128, 0, ctx->stream>>>(colstats, stats, rows, C, eps);
+    NNCB_CUDA(nncb::launch_pdl(bn_finalize_k, dim3((unsigned)((C + 127) / 128)), dim3(128), ctx->stream, colstats, stats,
+                               rows, C, eps));
     NNCB_LAUNCHED(ctx);
     return 0;
 }

@@ -610,6 +610,7 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                    const __grid_constant__ CUtensorMap map_c, const __grid_constant__ TcParams P,
                    const __grid_constant__ EgMaps eg_maps) {
     const int STAGES = P.stages;
+    nncb::pdl_trigger();   // follow-up folds / finalizes may be scheduled while this grid drains
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t a_bytes = BM * BK * 4;                 // 16 KB
@@ -1129,6 +1130,7 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
 
 __global__ void splitk_reduce_kernel(const float* __restrict__ partial, float* __restrict__ out, int64_t count,
                                      int splits) {
+    nncb::pdl_wait();   // programmatic dependent of the split-K GEMM
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
         float s = partial[i];
         for (int k = 1; k < splits; ++k) s = __fadd_rn(s, partial[k * count + i]);
@@ -1141,6 +1143,7 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ partial, float* _
 // deterministic order with a quarter of the dependent-add latency.
 __global__ void splitk_reduce4_kernel(const float4* __restrict__ partial, float4* __restrict__ out, int64_t count4,
                                       int splits) {
+    nncb::pdl_wait();   // programmatic dependent of the split-K GEMM
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count4; i += (int64_t)gridDim.x * blockDim.x) {
         float4 c[4];
 #pragma unroll
@@ -2015,10 +2018,12 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
     if (P.splits > 1) {
         int64_t count = P.M * P.N;
         if (count % 4 == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0)
-            splitk_reduce4_kernel<<<grid_for(ctx, count / 4, 256), 256, 0, ctx->stream>>>(
-                reinterpret_cast<const float4*>(P.partial), reinterpret_cast<float4*>(out), count / 4, P.splits);
+            NNCB_CUDA(launch_pdl(splitk_reduce4_kernel, dim3(grid_for(ctx, count / 4, 256)), dim3(256), ctx->stream,
+                                 reinterpret_cast<const float4*>(P.partial), reinterpret_cast<float4*>(out), count / 4,
+                                 P.splits));
         else
-            splitk_reduce_kernel<<<grid_for(ctx, count, 256), 256, 0, ctx->stream>>>(P.partial, out, count, P.splits);
+            NNCB_CUDA(launch_pdl(splitk_reduce_kernel, dim3(grid_for(ctx, count, 256)), dim3(256), ctx->stream,
+                                 static_cast<const float*>(P.partial), out, count, P.splits));
         NNCB_LAUNCHED(ctx);
     }
     return 0;

@@ -43,6 +43,27 @@ struct nncb_ctx {
 
 namespace nncb {
 
+// Programmatic dependent launch of a small follow-up kernel (finalize, fold):
+// it may be scheduled while the preceding grid drains and must begin with
+// pdl_wait() (griddepcontrol.wait: the preceding grid is complete and its
+// memory visible past that point).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t stream, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+
+
 void set_error(const std::string& msg);
 void staging_release(nncb_ctx* c);
 void* wt_buffer(nncb_ctx* ctx, size_t bytes);
