@@ -548,7 +548,10 @@ struct Program {
                 }
                 // one reduction per group: a second one (residual joins) needs a
                 // 2-block register budget and measured slower than the standalone pass
-                if (n_reduce >= 1 || at < 0 || e.ptrs.size() + 5 > 48) continue;
+                // NNC_BN_GRAD_REDUCE_MAX=2 folds the second reduction of a residual
+                // join too: measured neutral on C4 at 2 or 3 resident blocks
+                static const int max_reduce = std::getenv("NNC_BN_GRAD_REDUCE_MAX") ? std::atoi(std::getenv("NNC_BN_GRAD_REDUCE_MAX")) : 1;
+                if (n_reduce >= max_reduce || at < 0 || e.ptrs.size() + 5 > 48) continue;
                 const int s0 = static_cast<int>(e.ptrs.size());
                 std::vector<void*> ptrs = e.ptrs;
                 ptrs.push_back(r.ptrs[0]);                                  // x

@@ -184,6 +184,13 @@ std::vector<int> find_reduces(const nncb_ew_program& p) {
     return r;
 }
 
+// resident blocks per SM the two-reduction build is register-budgeted for
+// (NNCB_EW_RED2_BLOCKS; default 2)
+int red2_blocks() {
+    static const int b = getenv("NNCB_EW_RED2_BLOCKS") ? std::max(1, atoi(getenv("NNCB_EW_RED2_BLOCKS"))) : 2;
+    return b;
+}
+
 std::string generate(const nncb_ew_program& p, bool uses_ch) {
     std::ostringstream os;
     const int nred = static_cast<int>(find_reduces(p).size());
@@ -221,7 +228,7 @@ std::string generate(const nncb_ew_program& p, bool uses_ch) {
     int min_blocks = chregs.size() > 8 ? 2 : chregs.size() >= 3 ? 4 : 0;
     if (env_min_blocks >= 0) min_blocks = env_min_blocks;
     if (red)   // 16 double accumulator registers per reduction
-        os << "extern \"C\" __global__ void __launch_bounds__(256, " << (nred > 1 ? 2 : 4)
+        os << "extern \"C\" __global__ void __launch_bounds__(256, " << (nred > 1 ? red2_blocks() : 4)
            << ") nnc_fused_ew(const EwArgs A) {";
     else if (min_blocks > 0)
         os << "extern \"C\" __global__ void __launch_bounds__(256, " << min_blocks << ") nnc_fused_ew(const EwArgs A) {";
@@ -467,7 +474,9 @@ int nncb_ew_launch(nncb_ctx* ctx, nncb_ew_kernel* k, void* const* slots, int64_t
             return nncb::fail("nncb_ew_launch: REDUCE_BN_GRAD needs the channel-stationary launch (C power of 2 <= 2048)");
         const int64_t g = C / std::gcd<int64_t>(C, 1024);
         static const int64_t per_sm = getenv("NNCB_EW_RED_BLOCKS") ? std::max(1, atoi(getenv("NNCB_EW_RED_BLOCKS"))) : 4;
-        const int64_t cap = std::max<int64_t>(g, (per_sm * static_cast<int64_t>(ctx->sm_count) / g) * g);
+        // one wave: the two-reduction build is budgeted for red2_blocks() per SM
+        const int64_t resident = k->n_reduce > 1 ? std::min<int64_t>(per_sm, red2_blocks()) : per_sm;
+        const int64_t cap = std::max<int64_t>(g, (resident * static_cast<int64_t>(ctx->sm_count) / g) * g);
         if (grid > cap) grid = static_cast<unsigned>(cap);
         args.part = static_cast<double*>(nncb::scratch(ctx, sizeof(double) * 2 * C * grid * k->n_reduce));
         if (!args.part) return nncb::fail("nncb_ew_launch: reduction scratch allocation failed");
