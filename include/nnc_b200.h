@@ -65,6 +65,11 @@ int nnc_model_staged_loss(nnc_model* m, double* loss);
 int nnc_model_gradients(nnc_model* m, const float* target, int64_t n, double* loss);
 int nnc_model_grad(nnc_model* m, const char* weight, float* out, int64_t n);
 
+/* Data-parallel layout (runtime::dp_layout) as JSON: region order, ~bucket_bytes
+ * all-reduce buckets and the backward launch after which each can start.
+ * Host-only. Returns NULL on error. The string is valid until the next call. */
+const char* nnc_model_dp_schedule(nnc_model* m, int64_t bucket_bytes);
+
 /* Device-resident stepping for benchmarks: inputs/target stay on the device. */
 int      nnc_model_trainer_prepare(nnc_model* m, const float* target, int64_t n);
 int      nnc_model_trainer_step_device(nnc_model* m, double lr);

@@ -275,6 +275,12 @@ int nncb_comm_destroy(nncb_ctx* ctx);
 /* in-place sum all-reduce of fp32 on the comm stream, ordered after all work
  * enqueued so far on the compute stream; the compute stream waits for it.  */
 int nncb_allreduce_sum(nncb_ctx* ctx, float* buf, int64_t count);
+/* Overlapped variant: the comm stream waits for the compute stream's current
+ * position and all-reduces there; the compute stream continues without
+ * waiting. nncb_comm_join makes the compute stream wait for every collective
+ * issued so far (before the buffers are read, e.g. by SGD).                 */
+int nncb_allreduce_sum_async(nncb_ctx* ctx, float* buf, int64_t count);
+int nncb_comm_join(nncb_ctx* ctx);
 
 #ifdef __cplusplus
 }

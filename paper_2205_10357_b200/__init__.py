@@ -76,6 +76,7 @@ def _load():
         "nnc_model_trainer_loss": (I, [P, DP]),
         "nnc_model_launches_per_step": (U64, [P]),
         "nnc_model_profile_step": (S, [P, D]),
+        "nnc_model_dp_schedule": (S, [P, I64]),
         "nnc_model_arena_bytes": (U64, [P]),
         "nnc_model_infer_device": (I, [P]),
         "nnc_model_run_device": (I, [P, I]),
@@ -276,6 +277,13 @@ class CompiledModel:
     def profile_step(self, lr: float = 0.0):
         """Per-launch device times of one eager training step (CUDA events)."""
         res = _host.nnc_model_profile_step(self._h, lr)
+        if res is None:
+            raise NNCError(100, _host.nnc_last_error().decode())
+        return json.loads(res.decode())
+
+    def dp_schedule(self, bucket_bytes: int = 32 << 20) -> dict:
+        """Data-parallel region layout and all-reduce bucket schedule (host-only)."""
+        res = _host.nnc_model_dp_schedule(self._h, bucket_bytes)
         if res is None:
             raise NNCError(100, _host.nnc_last_error().decode())
         return json.loads(res.decode())

@@ -329,6 +329,21 @@ int nnc_model_trainer_loss(nnc_model* m, double* loss) {
     });
 }
 
+// Data-parallel region layout and bucket schedule (runtime::dp_layout) as
+// JSON; host-only (no device needed).
+const char* nnc_model_dp_schedule(nnc_model* m, int64_t bucket_bytes) {
+    int rc = guarded([&] {
+        runtime::DpLayout L = runtime::dp_layout(m->plans, *m->host, std::max<int64_t>(bucket_bytes / 4, 64));
+        nlohmann::json w = nlohmann::json::array(), b = nlohmann::json::array();
+        for (const std::string& n : L.weights)
+            w.push_back({{"name", n}, {"offset", L.offset[n]}, {"elements", L.elements[n]}, {"grad_launch", L.grad_launch[n]}});
+        for (const auto& x : L.buckets) b.push_back({{"offset", x.offset}, {"count", x.count}, {"close_launch", x.close_launch}});
+        g_buf = nlohmann::json{{"region_elems", L.region_elems}, {"bwd_launches", L.bwd_launches}, {"weights", w},
+                               {"buckets", b}}.dump();
+    });
+    return rc ? nullptr : g_buf.c_str();
+}
+
 const char* nnc_model_profile_step(nnc_model* m, double lr) {
     int rc = guarded([&] {
         if (!m->trainer) throw Error(Error::Code::BadDocument, "trainer not prepared");

@@ -753,12 +753,14 @@ struct Program {
         return b;
     }
 
-    void enqueue_plan(size_t pi, std::vector<std::string>* trace) const {
+    void enqueue_plan(size_t pi, std::vector<std::string>* trace,
+                      const std::function<void(size_t)>& after = nullptr) const {
         const auto& labels = step_labels[pi];
         size_t li = 0;
         for (size_t k = 0; k < steps[pi].size(); ++k) {
             while (trace && li < labels.size() && labels[li].first == k) trace->push_back("exec:" + labels[li++].second);
             enqueue(dev->ctx(), steps[pi][k]);
+            if (after) after(k);
         }
         while (trace && li < labels.size()) trace->push_back("exec:" + labels[li++].second);
     }
@@ -1075,7 +1077,7 @@ struct Trainer::Impl {
     void* graph = nullptr;
     void* graph_nosgd = nullptr;
     double graph_lr = std::nan("");
-    std::vector<std::pair<int64_t, int64_t>> buckets;   // (offset, count) in reverse backward order
+    DpLayout layout;                                      // region order and all-reduce buckets
     uint64_t launches_per_step = 0;
     bool warmed = false;
     // pipelined stepping (stage / launch_staged / staged_loss): two staging slots
@@ -1118,9 +1120,28 @@ struct Trainer::Impl {
         int64_t n = element_count(plans->train_fwd.values[plans->train_fwd.find_value(pred)].dims);
         NNC_CHECK(nncb_l1_loss(ctx, static_cast<float*>(prog->ptr(pred)), static_cast<float*>(target),
                                static_cast<float*>(prog->ptr(dpred)), static_cast<double*>(loss), n));
-        prog->enqueue_plan(1, nullptr);
-        if (dev->nranks() > 1)
-            for (auto [off, cnt] : buckets) NNC_CHECK(nncb_allreduce_sum(ctx, static_cast<float*>(grads) + off, cnt));
+        if (dev->nranks() > 1) {
+            // each bucket's all-reduce starts on the comm stream right after the
+            // launch that writes its last gradient, overlapping the rest of the
+            // backward pass; SGD waits for all of them
+            std::map<int64_t, std::vector<size_t>> closing;
+            for (size_t b = 0; b < layout.buckets.size(); ++b) closing[layout.buckets[b].close_launch].push_back(b);
+            auto start = [&](size_t b) {
+                const DpBucket& bk = layout.buckets[b];
+                NNC_CHECK(nncb_allreduce_sum_async(ctx, static_cast<float*>(grads) + bk.offset, bk.count));
+            };
+            prog->enqueue_plan(1, nullptr, [&](size_t k) {
+                auto it = closing.find(static_cast<int64_t>(k));
+                if (it != closing.end())
+                    for (size_t b : it->second) start(b);
+            });
+            for (auto& [k, bs] : closing)   // buckets without a producing launch (none in a well-formed plan)
+                if (k < 0 || k >= static_cast<int64_t>(prog->steps[1].size()))
+                    for (size_t b : bs) start(b);
+            NNC_CHECK(nncb_comm_join(ctx));
+        } else {
+            prog->enqueue_plan(1, nullptr);
+        }
         if (do_sgd)
             NNC_CHECK(nncb_sgd(ctx, static_cast<float*>(params), static_cast<float*>(grads), region_elems, lr,
                                1.0 / static_cast<double>(dev->nranks())));
@@ -1170,6 +1191,51 @@ struct Trainer::Impl {
     }
 };
 
+DpLayout dp_layout(const plan::VersionPlans& plans, HostModel& model, int64_t bucket_elems) {
+    DpLayout L;
+    std::map<std::string, std::string> grad_to_weight;
+    for (const auto& [w, gv] : plans.weight_grads) grad_to_weight[gv] = w;
+    const ExecutionPlan& bwd = plans.train_bwd;
+    int64_t k = 0;
+    for (const auto& es : bwd.exec_steps)
+        for (uint32_t li : es.launches) {
+            const auto& Lc = bwd.groups[es.group].launches[li];
+            for (size_t a = 0; a < Lc.args.size(); ++a) {
+                if (!Lc.is_out[a]) continue;
+                auto it = grad_to_weight.find(bwd.values[Lc.args[a].slot].name);
+                if (it == grad_to_weight.end()) continue;
+                if (!L.grad_launch.count(it->second)) L.weights.push_back(it->second);   // first production order
+                L.grad_launch[it->second] = k;                                          // last write
+            }
+            ++k;
+        }
+    L.bwd_launches = k;
+    for (const auto* p : {&plans.train_fwd, &plans.train_bwd})
+        for (const std::string& w : p->weight_names)
+            if (std::find(L.weights.begin(), L.weights.end(), w) == L.weights.end()) {
+                L.weights.push_back(w);
+                L.grad_launch[w] = -1;
+            }
+    int64_t trainable_end = 0;
+    for (const std::string& w : L.weights) {
+        const int64_t n = model.tensor(w).elements();
+        L.offset[w] = L.region_elems;
+        L.elements[w] = n;
+        if (L.grad_launch[w] >= 0) trainable_end = L.region_elems + n;
+        L.region_elems += (n + 63) / 64 * 64;   // 256-byte aligned tensors
+    }
+    for (int64_t off = 0; off < trainable_end; off += bucket_elems) {
+        DpBucket b;
+        b.offset = off;
+        b.count = std::min(bucket_elems, trainable_end - off);
+        for (const std::string& w : L.weights)
+            if (L.grad_launch[w] >= 0 && L.offset[w] < off + b.count && off < L.offset[w] + L.elements[w])
+                b.close_launch = std::max(b.close_launch, L.grad_launch[w]);
+        L.buckets.push_back(b);
+    }
+    return L;
+}
+
 Trainer::Trainer(const plan::VersionPlans& plans, HostModel& model, Device& dev, const ExecOptions& opts)
     : impl(std::make_unique<Impl>()) {
     Impl& I = *impl;
@@ -1182,32 +1248,12 @@ Trainer::Trainer(const plan::VersionPlans& plans, HostModel& model, Device& dev,
     I.pred = plans.inference.values[plans.inference.output_slots[0]].name;
     I.dpred = "d." + I.pred;
     nncb_ctx* ctx = dev.ctx();
-    // flat parameter / gradient regions: trainable weights in reverse order of
-    // gradient production (so all-reduce buckets close early in backward), then
-    // the remaining parameters.
-    std::vector<std::string> order;
-    std::map<std::string, std::string> grad_to_weight;
-    for (const auto& [w, gv] : plans.weight_grads) grad_to_weight[gv] = w;
-    const ExecutionPlan& bwd = plans.train_bwd;
-    for (const auto& es : bwd.exec_steps)
-        for (uint32_t li : es.launches)
-            for (size_t a = 0; a < bwd.groups[es.group].launches[li].args.size(); ++a) {
-                const auto& L = bwd.groups[es.group].launches[li];
-                if (!L.is_out[a]) continue;
-                auto it = grad_to_weight.find(bwd.values[L.args[a].slot].name);
-                if (it != grad_to_weight.end() && std::find(order.begin(), order.end(), it->second) == order.end())
-                    order.push_back(it->second);
-            }
-    for (const auto* p : {&plans.train_fwd, &plans.train_bwd})
-        for (const std::string& w : p->weight_names)
-            if (std::find(order.begin(), order.end(), w) == order.end()) order.push_back(w);
-    for (const std::string& w : order) {
-        const Tensor& t = model.tensor(w);
-        I.w_off[w] = I.region_elems;
-        I.w_elems[w] = t.elements();
-        I.region_elems += (t.elements() + 63) / 64 * 64;   // 256-byte aligned tensors
-        I.weights.push_back(w);
-    }
+    // flat parameter / gradient regions and all-reduce buckets (dp_layout)
+    I.layout = dp_layout(plans, model);
+    I.weights = I.layout.weights;
+    I.w_off = I.layout.offset;
+    I.w_elems = I.layout.elements;
+    I.region_elems = I.layout.region_elems;
     size_t region_bytes = static_cast<size_t>(std::max<int64_t>(I.region_elems, 64)) * 4;
     NNC_CHECK(nncb_malloc(ctx, region_bytes, &I.params));
     NNC_CHECK(nncb_malloc(ctx, region_bytes, &I.grads));
@@ -1221,12 +1267,6 @@ Trainer::Trainer(const plan::VersionPlans& plans, HostModel& model, Device& dev,
         dev.stats().weight_bytes += t.byte_size();
         dev.adopt_weight(model, w, home, t.byte_size(), model.stamp(w));
     }
-    // buckets of ~32 MB over the trainable prefix of the region
-    int64_t trainable_end = 0;
-    for (const auto& [w, gv] : plans.weight_grads) trainable_end = std::max(trainable_end, I.w_off[w] + I.w_elems[w]);
-    const int64_t bucket = 8 << 20;   // elements (32 MB)
-    for (int64_t off = 0; off < trainable_end; off += bucket)
-        I.buckets.push_back({off, std::min(bucket, trainable_end - off)});
     const int64_t pred_elems = element_count(plans.train_fwd.values[plans.train_fwd.find_value(I.pred)].dims);
     NNC_CHECK(nncb_malloc(ctx, static_cast<size_t>(std::max<int64_t>(pred_elems, 4)) * 4, &I.target));
     NNC_CHECK(nncb_malloc(ctx, 64, &I.loss));
@@ -1234,7 +1274,8 @@ Trainer::Trainer(const plan::VersionPlans& plans, HostModel& model, Device& dev,
     I.prog->dev = &dev;
     I.prog->plans = {&plans.train_fwd, &plans.train_bwd};
     I.prog->precision = opts.gemm_precision;
-    std::map<std::string, std::string> weight_of_grad = grad_to_weight;
+    std::map<std::string, std::string> weight_of_grad;
+    for (const auto& [w, gv] : plans.weight_grads) weight_of_grad[gv] = w;
     I.prog->bind([&](const std::string& w) { return static_cast<void*>(static_cast<float*>(I.params) + I.w_off.at(w)); },
                  [&](const std::string& v) -> void* {
                      auto it = weight_of_grad.find(v);

@@ -159,6 +159,25 @@ std::map<std::string, Tensor> gradients(const plan::VersionPlans& plans,
                                         const Tensor& target, HostModel& model, double* loss,
                                         Device* device = nullptr, const ExecOptions& opts = {});
 
+/// Data-parallel layout of the flat parameter / gradient regions: trainable
+/// weights in the order their gradients are produced by the backward plan
+/// (so all-reduce buckets close early), then the remaining parameters; 256-byte
+/// aligned. Buckets of ~bucket_elems cover the trainable prefix; close_launch
+/// is the index (flattened exec_steps x launches order of train_bwd) of the
+/// launch after which every gradient in the bucket has been written: its
+/// all-reduce can start there, overlapping the rest of the backward pass.
+struct DpBucket {
+    int64_t offset = 0, count = 0, close_launch = -1;
+};
+struct DpLayout {
+    std::vector<std::string> weights;              // region order
+    std::map<std::string, int64_t> offset, elements, grad_launch;   // grad_launch: -1 for non-trainable
+    int64_t region_elems = 0;
+    int64_t bwd_launches = 0;
+    std::vector<DpBucket> buckets;
+};
+DpLayout dp_layout(const plan::VersionPlans& plans, HostModel& model, int64_t bucket_elems = int64_t(8) << 20);
+
 /// Device-resident training step for benchmarking: inputs/target already on the
 /// device (pointers), everything stays on the device; returns nothing (the loss
 /// is left in a device double readable with last_loss()).

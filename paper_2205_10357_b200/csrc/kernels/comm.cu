@@ -119,4 +119,26 @@ int nncb_allreduce_sum(nncb_ctx* ctx, float* buf, int64_t count) {
     return 0;
 }
 
+int nncb_allreduce_sum_async(nncb_ctx* ctx, float* buf, int64_t count) {
+    if (!ctx->nccl_comm) return nncb::fail("nncb_allreduce_sum_async: communicator not initialised");
+    if (count <= 0) return 0;
+    cudaEvent_t ready;
+    NNCB_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    NNCB_CUDA(cudaEventRecord(ready, ctx->stream));
+    NNCB_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ready, 0));
+    NNCB_NCCL(nccl().allReduce(buf, buf, static_cast<size_t>(count), ncclFloat32, ncclSum,
+                               static_cast<ncclComm_t>(ctx->nccl_comm), ctx->comm_stream));
+    cudaEventDestroy(ready);
+    return 0;
+}
+
+int nncb_comm_join(nncb_ctx* ctx) {
+    cudaEvent_t done;
+    NNCB_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    NNCB_CUDA(cudaEventRecord(done, ctx->comm_stream));
+    NNCB_CUDA(cudaStreamWaitEvent(ctx->stream, done, 0));
+    cudaEventDestroy(done);
+    return 0;
+}
+
 }  // extern "C"
