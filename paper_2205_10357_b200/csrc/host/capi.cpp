@@ -90,19 +90,15 @@ void describe_plan(std::ostringstream& os, const plan::ExecutionPlan& p) {
     os << "],\"launch_count\":" << p.launch_count() << "}";
 }
 
-Tensor make(const float* data, const int64_t* dims, int rank) {
-    Tensor t(DType::F32, std::vector<int64_t>(dims, dims + rank));
-    std::memcpy(t.data(), data, t.byte_size());
-    return t;
-}
-
 const plan::ExecutionPlan& pred_plan(nnc_model* m) { return m->plans.inference; }
 
 Tensor target_tensor(nnc_model* m, const float* target, int64_t n) {
     const auto& p = pred_plan(m);
     const auto& v = p.values[p.output_slots.at(0)];
     if (element_count(v.dims) != n) throw Error(Error::Code::ShapeMismatch, "target size mismatch");
-    return make(target, v.dims.data(), static_cast<int>(v.dims.size()));
+    // borrowed: every consumer (train_step, gradients, stage, trainer_prepare)
+    // has uploaded it before the C-ABI call returns
+    return Tensor::view(DType::F32, v.dims, target);
 }
 
 }  // namespace
