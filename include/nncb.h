@@ -193,7 +193,24 @@ typedef struct {
     const float* eg_x;
     const float* eg_stats;
     double* eg_sums;
+    /* NNCB_CONV_FWD: optional K-major copy of the weights, [co][kh*kw*ci],
+     * kept current by the caller (nncb_transpose_batch). Tiles that read
+     * K-major weights use it instead of transposing per call; routes that
+     * lower the weights themselves (space-to-depth, im2col) ignore it.     */
+    const float* b_kmajor;
 } nncb_gemm_desc;
+
+/* One launch transposing many row-major [rows][cols] matrices into [cols][rows]
+ * (e.g. every forward conv's weights into their K-major copies). `jobs` is a
+ * device array; tile0 is the exclusive prefix sum of each job's 32x32 tiles,
+ * total_tiles the sum.                                                       */
+typedef struct {
+    const float* src;
+    float* dst;
+    int32_t rows, cols;
+    int64_t tile0;
+} nncb_transpose_job;
+int nncb_transpose_batch(nncb_ctx* ctx, const nncb_transpose_job* jobs, int n, int64_t total_tiles);
 
 /* float32 sums[0:C] -> out0, sums[C:2C] -> out1 (finalize of NNCB_EPI_RELU_GRAD sums). */
 int nncb_colsums_to_float(nncb_ctx* ctx, const double* sums, float* out0, float* out1, int64_t C);

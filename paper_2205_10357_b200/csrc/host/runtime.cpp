@@ -220,6 +220,15 @@ struct Program {
     int64_t live_high = 0;
     void* side = nullptr;          // fused BatchNorm column-sum accumulators
     void* side_eg = nullptr;       // dgrad-epilogue BatchNorm backward sums
+    // K-major copies of the forward conv weights, refreshed by one batched
+    // transpose at the head of each plan (nncb_transpose_batch)
+    void* wt_region = nullptr;
+    struct KmajorSet {
+        void* jobs = nullptr;      // device nncb_transpose_job[n]
+        int n = 0;
+        int64_t tiles = 0;
+    };
+    std::vector<KmajorSet> kmajor;   // per plan
     std::unordered_map<std::string, void*> where;   // value name -> device pointer
     std::vector<std::vector<BoundLaunch>> steps;     // per plan, flattened launches
     std::vector<std::vector<const Launch*>> sources; // per plan, the plan launch of each bound launch
@@ -230,6 +239,60 @@ struct Program {
         if (arena) nncb_free(dev->ctx(), arena);
         if (side) nncb_free(dev->ctx(), side);
         if (side_eg) nncb_free(dev->ctx(), side_eg);
+        if (wt_region) nncb_free(dev->ctx(), wt_region);
+        for (const KmajorSet& k : kmajor)
+            if (k.jobs) nncb_free(dev->ctx(), k.jobs);
+    }
+
+    /// tf32 forward convolutions on the implicit-GEMM path read K-major
+    /// weights: instead of each GEMM transposing its weights per call, the
+    /// copies live in one region and a single launch at the head of the plan
+    /// refreshes them all (after the previous step's SGD in training).
+    void prepare_kmajor_weights() {
+        kmajor.assign(steps.size(), KmajorSet{});
+        std::vector<std::vector<std::pair<size_t, nncb_transpose_job>>> jobs(steps.size());
+        int64_t elems = 0;
+        for (size_t pi = 0; pi < steps.size(); ++pi)
+            for (size_t k = 0; k < steps[pi].size(); ++k) {
+                const BoundLaunch& b = steps[pi][k];
+                if (b.kind != LaunchKind::Gemm || b.skip || b.gemm.kind != NNCB_CONV_FWD) continue;
+                const int64_t K = b.gemm.kh * b.gemm.kw * b.gemm.ci, co = b.gemm.co;
+                if (b.gemm.ci % 32 != 0 || K % 4 != 0 || K >= (int64_t(1) << 31) || co >= (int64_t(1) << 31)) continue;
+                nncb_transpose_job j{};
+                j.src = static_cast<const float*>(b.ptrs[1]);
+                j.rows = static_cast<int32_t>(K);
+                j.cols = static_cast<int32_t>(co);
+                j.tile0 = elems;   // element offset for now
+                jobs[pi].push_back({k, j});
+                elems += (K * co + 63) / 64 * 64;
+            }
+        if (elems == 0) return;
+        NNC_CHECK(nncb_malloc(dev->ctx(), static_cast<size_t>(elems) * sizeof(float), &wt_region));
+        for (size_t pi = 0; pi < steps.size(); ++pi) {
+            if (jobs[pi].empty()) continue;
+            std::vector<nncb_transpose_job> table;
+            int64_t tiles = 0;
+            for (auto& [k, j] : jobs[pi]) {
+                j.dst = static_cast<float*>(wt_region) + j.tile0;
+                j.tile0 = tiles;
+                tiles += static_cast<int64_t>((j.rows + 31) / 32) * ((j.cols + 31) / 32);
+                steps[pi][k].gemm.b_kmajor = j.dst;
+                table.push_back(j);
+            }
+            KmajorSet& s = kmajor[pi];
+            s.n = static_cast<int>(table.size());
+            s.tiles = tiles;
+            NNC_CHECK(nncb_malloc(dev->ctx(), table.size() * sizeof(nncb_transpose_job), &s.jobs));
+            NNC_CHECK(nncb_h2d(dev->ctx(), s.jobs, table.data(), table.size() * sizeof(nncb_transpose_job)));
+        }
+        NNC_CHECK(nncb_sync(dev->ctx()));
+    }
+
+    /// Work every plan execution starts with: the K-major weight refresh.
+    void plan_prologue(size_t pi) const {
+        if (pi < kmajor.size() && kmajor[pi].n)
+            NNC_CHECK(nncb_transpose_batch(dev->ctx(), static_cast<const nncb_transpose_job*>(kmajor[pi].jobs),
+                                           kmajor[pi].n, kmajor[pi].tiles));
     }
 
     void* ptr(const std::string& name) const {
@@ -310,6 +373,7 @@ struct Program {
             fuse_bn_statistics();
             fuse_bn_grad_reduce();
             fuse_relu_grad_epilogue();
+            if (!std::getenv("NNC_NO_KMAJOR_BATCH")) prepare_kmajor_weights();
         }
         hint_unchanged_activations();
     }
@@ -757,6 +821,7 @@ struct Program {
                       const std::function<void(size_t)>& after = nullptr) const {
         const auto& labels = step_labels[pi];
         size_t li = 0;
+        plan_prologue(pi);
         for (size_t k = 0; k < steps[pi].size(); ++k) {
             while (trace && li < labels.size() && labels[li].first == k) trace->push_back("exec:" + labels[li++].second);
             enqueue(dev->ctx(), steps[pi][k]);
@@ -1301,6 +1366,11 @@ std::vector<Trainer::LaunchTiming> Trainer::profile_step(double lr) {
     ev();
     for (size_t pi = 0; pi < 2; ++pi) {
         const ExecutionPlan& p = *I.prog->plans[pi];
+        if (pi < I.prog->kmajor.size() && I.prog->kmajor[pi].n) {
+            I.prog->plan_prologue(pi);
+            ev();
+            out.push_back({"kmajor_weights", "transpose", 0, 8.0 * 1024 * static_cast<double>(I.prog->kmajor[pi].tiles), 0});
+        }
         for (size_t k = 0; k < I.prog->steps[pi].size(); ++k) {
             const BoundLaunch& b = I.prog->steps[pi][k];
             const Launch& L = *I.prog->sources[pi][k];

@@ -1636,6 +1636,7 @@ int gemm_tc_s2d(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const fl
         std::copy(key, key + 8, ctx->s2d_key);
     }
     nncb_gemm_desc dd = *d;
+    dd.b_kmajor = nullptr;   // the lowered conv has its own weight layout
     dd.ih = H2; dd.iw = W2; dd.ci = 32; dd.kh = kh2; dd.kw = kwt; dd.sh = 1; dd.sw = 1;
     dd.pad_top = 0; dd.pad_left = 0;
     g_dil_w = pack ? 2 : 1;
@@ -1820,6 +1821,33 @@ __global__ void transpose_k(const float* __restrict__ w, float* __restrict__ wt,
     }
 }
 
+// Many transposes in one launch: block -> (job, 32x32 tile) by a binary search
+// over the jobs' tile prefix sums.
+__global__ void transpose_batch_k(const nncb_transpose_job* __restrict__ jobs, int n, int64_t total) {
+    __shared__ float tile[32][33];
+    for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+        int lo = 0, hi = n - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) / 2;
+            if (jobs[mid].tile0 <= t) lo = mid; else hi = mid - 1;
+        }
+        const nncb_transpose_job J = jobs[lo];
+        const int64_t local = t - J.tile0;
+        const int tcols = (J.cols + 31) / 32;
+        const int bx = static_cast<int>(local % tcols) * 32, by = static_cast<int>(local / tcols) * 32;
+        for (int j = threadIdx.y; j < 32; j += 8) {
+            const int r = by + j, c = bx + threadIdx.x;
+            if (r < J.rows && c < J.cols) tile[j][threadIdx.x] = J.src[static_cast<int64_t>(r) * J.cols + c];
+        }
+        __syncthreads();
+        for (int j = threadIdx.y; j < 32; j += 8) {
+            const int c = bx + j, r = by + threadIdx.x;
+            if (r < J.rows && c < J.cols) J.dst[static_cast<int64_t>(c) * J.rows + r] = tile[threadIdx.x][j];
+        }
+        __syncthreads();
+    }
+}
+
 int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t lda, const float* b,
                  const float* bias, float* out, bool* handled, bool manual) {
     *handled = false;
@@ -1931,12 +1959,17 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
         const int64_t kfull = kh * kw * ci;
         if (fwd && g_force_tb && !manual && kfull % 4 == 0) {
             // K-major copy [co][kh*kw*ci]: the tensor core reads K-major tf32
-            // operands faster than MN-major ones (measured fwd vs dgrad)
-            float* wt = static_cast<float*>(wt_buffer(ctx, sizeof(float) * kfull * co));
-            if (!wt) return fail("conv fwd: transposed-weight buffer allocation failed");
-            transpose_k<<<dim3((unsigned)((co + 31) / 32), (unsigned)((kfull + 31) / 32)), dim3(32, 8), 0, ctx->stream>>>(
-                b, wt, (int)kfull, (int)co);
-            NNCB_LAUNCHED(ctx);
+            // operands faster than MN-major ones (measured fwd vs dgrad). The
+            // caller's copy (b_kmajor, refreshed once per plan) or a per-call one.
+            const float* wt = d->b_kmajor;
+            if (!wt) {
+                float* w2 = static_cast<float*>(wt_buffer(ctx, sizeof(float) * kfull * co));
+                if (!w2) return fail("conv fwd: transposed-weight buffer allocation failed");
+                transpose_k<<<dim3((unsigned)((co + 31) / 32), (unsigned)((kfull + 31) / 32)), dim3(32, 8), 0, ctx->stream>>>(
+                    b, w2, (int)kfull, (int)co);
+                NNCB_LAUNCHED(ctx);
+                wt = w2;
+            }
             P.b_mn = 0;
             P.bt = 1;
             if (!encode_2d(&mb, wt, kfull, co, BK, P.pair ? P.bn / 2 : P.bn, false)) return 1;
@@ -2033,6 +2066,14 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
 
 // Route selection for convolutions whose channel count does not fill a 32-wide
 // K block: 1 = builder-warp gather (manual A), 0 = im2col workspace.
+extern "C" int nncb_transpose_batch(nncb_ctx* ctx, const nncb_transpose_job* jobs, int n, int64_t total_tiles) {
+    if (n <= 0 || total_tiles <= 0) return 0;
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(total_tiles, static_cast<int64_t>(ctx->sm_count) * 16));
+    nncb::transpose_batch_k<<<grid, dim3(32, 8), 0, ctx->stream>>>(jobs, n, total_tiles);
+    NNCB_LAUNCHED(ctx);
+    return 0;
+}
+
 extern "C" int nncb_gemm_set_manual_a(int on) {
     nncb::g_manual_a.store(on ? 1 : 0);
     return 0;

@@ -15,7 +15,13 @@ class GemmDesc(ctypes.Structure):
                [(n, ctypes.c_int64) for n in ("n", "ih", "iw", "ci", "co", "kh", "kw", "sh", "sw", "oh", "ow",
                                               "pad_top", "pad_left", "batch", "in_f", "out_f")] + \
                [("colstats", ctypes.c_void_p), ("eg_mask", ctypes.c_void_p), ("eg_res", ctypes.c_void_p),
-                ("eg_x", ctypes.c_void_p), ("eg_stats", ctypes.c_void_p), ("eg_sums", ctypes.c_void_p)]
+                ("eg_x", ctypes.c_void_p), ("eg_stats", ctypes.c_void_p), ("eg_sums", ctypes.c_void_p),
+                ("b_kmajor", ctypes.c_void_p)]
+
+
+class TransposeJob(ctypes.Structure):
+    _fields_ = [("src", ctypes.c_void_p), ("dst", ctypes.c_void_p), ("rows", ctypes.c_int32), ("cols", ctypes.c_int32),
+                ("tile0", ctypes.c_int64)]
 
 
 for name, res, args in [
@@ -29,6 +35,7 @@ for name, res, args in [
     ("nncb_gemm_set_manual_a", _I, [_I]),
     ("nncb_gemm_force_tile", _I, [_I]),
     ("nncb_launch_count", ctypes.c_uint64, [_P]),
+    ("nncb_transpose_batch", _I, [_P, _P, _I, ctypes.c_int64]),
 ]:
     fn = getattr(K, name)
     fn.restype, fn.argtypes = res, args

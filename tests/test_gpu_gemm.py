@@ -2,6 +2,7 @@
 (bit-identical to the reference CPU loops) for all six contraction kinds,
 strided / padded convolutions and ragged tile edges. Bound: 2e-2 of max|ref|
 (reduced-precision GEMM tolerance); typical tf32 error is ~1e-3."""
+import ctypes
 import numpy as np
 import pytest
 
@@ -299,3 +300,50 @@ def test_s2d_wgrad_reuses_forward_lowering(shape):
         if other is None:
             # reuse: no space-to-depth input launch (GEMM + weight fold-back [+ split-K reduce])
             assert launched <= 3, launched
+
+
+def test_transpose_batch_bitwise():
+    """nncb_transpose_batch: several row-major matrices (ragged sizes) into
+    their transposes in one launch, bit for bit."""
+    from tests.nncb_ctypes import TransposeJob
+    rng = np.random.default_rng(12)
+    shapes = [(576, 64), (33, 70), (1, 5), (2304, 256), (147, 64)]
+    mats = [rng.standard_normal(s).astype(np.float32) for s in shapes]
+    src = [Dev(m) for m in mats]
+    dst = [Dev(nbytes=m.nbytes) for m in mats]
+    jobs, t0 = [], 0
+    for m, s, d in zip(mats, src, dst):
+        jobs.append(TransposeJob(s.p, d.p, m.shape[0], m.shape[1], t0))
+        t0 += -(-m.shape[0] // 32) * -(-m.shape[1] // 32)
+    table = (TransposeJob * len(jobs))(*jobs)
+    jd = Dev(nbytes=ctypes.sizeof(table))
+    assert K.nncb_h2d(ctx(), jd.p, ctypes.addressof(table), ctypes.sizeof(table)) == 0
+    assert K.nncb_transpose_batch(ctx(), jd.p, len(jobs), t0) == 0
+    for m, d in zip(mats, dst):
+        assert np.array_equal(d.get((m.shape[1], m.shape[0])), m.T)
+
+
+@pytest.mark.parametrize("shape", [(2, 14, 14, 64, 64, 3, 1), (4, 7, 7, 128, 256, 1, 1), (2, 13, 11, 64, 96, 3, 2)])
+def test_conv_fwd_caller_kmajor_weights(shape):
+    """b_kmajor: a forward conv reading the caller's K-major weight copy (the
+    K-major tile forced) matches the exact path."""
+    n, ih, iw, ci, co, k, s = shape
+    g = conv_geom(n, ih, iw, ci, co, k, s)
+    rng = np.random.default_rng(13)
+    x = rng.uniform(-1, 1, (n, ih, iw, ci)).astype(np.float32)
+    w = rng.uniform(-1, 1, (k, k, ci, co)).astype(np.float32)
+    xd, wd, wk = Dev(x), Dev(w), Dev(np.ascontiguousarray(w.reshape(-1, co).T))
+    ex = Dev(nbytes=n * g["oh"] * g["ow"] * co * 4)
+    gemm(GemmDesc(kind=CONV_FWD, precision=1, epilogue=0, **g), xd, wd, None, ex)
+    out = Dev(nbytes=n * g["oh"] * g["ow"] * co * 4)
+    d = GemmDesc(kind=CONV_FWD, precision=0, epilogue=0, **g)
+    d.b_kmajor = wk.p
+    K.nncb_gemm_force_tile(0x40000 | 128)
+    try:
+        before = K.nncb_launch_count(ctx())
+        gemm(d, xd, wd, None, out)
+        assert K.nncb_gemm_last_path() == 1
+        assert K.nncb_launch_count(ctx()) - before == 1   # no per-call transpose
+    finally:
+        K.nncb_gemm_force_tile(0)
+    check(out.get((n, g["oh"], g["ow"], co)), ex.get((n, g["oh"], g["ow"], co)).astype(np.float64))
