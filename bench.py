@@ -331,15 +331,17 @@ def main():
         role = "inference" if cfg["kind"] == "infer" else "train_fwd"
         h2d = sum(v.nbytes for v in inputs.values())
         final = [v["name"] for v in model.describe[role]["values"] if v["category"] == "output"]
-        out = model.run(inputs, role=role, outputs=final)   # untimed warm-up; only the graph outputs come back
+        # the public pipelined loop: every run uploads its inputs from host memory
+        # (the next run's upload overlaps this run) and downloads its outputs
+        out = model.run_many([inputs] * 2, role=role, outputs=final)[-1]   # untimed warm-up
         d2h = sum(v.nbytes for v in out.values())
         timer.sync()
         barrier()
         t0 = time.perf_counter()
         n_e2e = max(2, args.steps // 2)
-        for _ in range(n_e2e):
-            model.run(inputs, role=role, outputs=final)
+        outs = model.run_many([inputs] * n_e2e, role=role, outputs=final)
         e_ms = max_over_ranks((time.perf_counter() - t0) * 1000 / n_e2e)
+        assert len(outs) == n_e2e
         e2e = {"value": units / (e_ms / 1000.0), "unit": unit, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": e_ms}
     if cfg["kind"] == "train":

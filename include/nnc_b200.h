@@ -52,6 +52,14 @@ int nnc_model_run(nnc_model* m, int role);
 /* nnc_model_run copying back only the comma-separated outputs `names` (ExecOptions::materialize). */
 int nnc_model_run_outputs(nnc_model* m, int role, const char* names);
 int nnc_model_output(nnc_model* m, const char* name, float* out, int64_t n);
+/* Pipelined runs from host buffers: nnc_model_run_staged launches the oldest
+ * staged run (names: comma-separated outputs, NULL or "" = all),
+ * nnc_model_stage_run stages the current inputs of the next one (the upload
+ * overlaps the launched run), nnc_model_staged_outputs waits for the launched
+ * run and makes its outputs readable with nnc_model_output.                */
+int nnc_model_stage_run(nnc_model* m, int role);
+int nnc_model_run_staged(nnc_model* m, int role, const char* names);
+int nnc_model_staged_outputs(nnc_model* m, int role);
 
 int nnc_model_train_step(nnc_model* m, const float* target, int64_t n, double lr, double* loss);
 /* Pipelined training from host buffers: stage the current inputs + target of

@@ -67,6 +67,9 @@ def _load():
         "nnc_model_output": (I, [P, S, FP, I64]),
         "nnc_model_train_step": (I, [P, FP, I64, D, DP]),
         "nnc_model_stage_step": (I, [P, FP, I64]),
+        "nnc_model_stage_run": (I, [P, I]),
+        "nnc_model_run_staged": (I, [P, I, S]),
+        "nnc_model_staged_outputs": (I, [P, I]),
         "nnc_model_train_step_staged": (I, [P, D]),
         "nnc_model_staged_loss": (I, [P, DP]),
         "nnc_model_gradients": (I, [P, FP, I64, DP]),
@@ -211,6 +214,47 @@ class CompiledModel:
             if _host.nnc_model_output(self._h, name.encode(), _fptr(arr), arr.size) == 0:
                 out[name] = arr
         return out
+
+    def _collect(self, role: str, outputs: Optional[Sequence[str]]) -> Dict[str, np.ndarray]:
+        out = {}
+        plan = self.describe[role]
+        out_names = [v["name"] for v in plan["values"] if v["category"] in ("output", "saved") and v["resident"]]
+        if outputs is not None:
+            out_names = [n for n in out_names if n in set(outputs)]
+        for name in out_names:
+            v = self._plan_value(role, name)
+            if v["storage"] != "buffer":
+                continue
+            arr = np.empty(v["dims"], dtype=np.float32)
+            if _host.nnc_model_output(self._h, name.encode(), _fptr(arr), arr.size) == 0:
+                out[name] = arr
+        return out
+
+    def run_many(self, batches, role: str = "inference",
+                 outputs: Optional[Sequence[str]] = None) -> List[Dict[str, np.ndarray]]:
+        """run() over an iterable of input dicts from host buffers, returning
+        each run's outputs; the upload of run i + 1 overlaps run i."""
+        r = 1 if role == "train_fwd" else 0
+        names = ",".join(outputs).encode() if outputs is not None else b""
+        it = iter(batches)
+        results: List[Dict[str, np.ndarray]] = []
+        first = next(it, None)
+        if first is None:
+            return results
+        keep = self._borrow(first)   # noqa: F841
+        _check(_host.nnc_model_stage_run(self._h, r))
+        pending = next(it, None)
+        while True:
+            _check(_host.nnc_model_run_staged(self._h, r, names))
+            staged_next = pending is not None
+            if staged_next:
+                keep = self._borrow(pending)   # noqa: F841  (consumed by the stage call)
+                _check(_host.nnc_model_stage_run(self._h, r))
+                pending = next(it, None)
+            _check(_host.nnc_model_staged_outputs(self._h, r))
+            results.append(self._collect(role, outputs))
+            if not staged_next:
+                return results
 
     def train_step(self, inputs: Dict[str, np.ndarray], target: np.ndarray, lr: float) -> float:
         keep = self._borrow(inputs)   # noqa: F841

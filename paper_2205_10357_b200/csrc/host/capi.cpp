@@ -250,6 +250,44 @@ int nnc_model_run_outputs(nnc_model* m, int role, const char* names) {
     return rc;
 }
 
+// Pipelined runs from host buffers (runtime::execute_stage / execute_launch_staged /
+// execute_staged_outputs). names: comma-separated outputs to bring back (NULL or "" = all).
+int nnc_model_stage_run(nnc_model* m, int role) {
+    const int rc = guarded([&] {
+        const plan::ExecutionPlan& p = role == 1 ? m->plans.train_fwd : m->plans.inference;
+        runtime::execute_stage(p, m->inputs, nullptr);
+    });
+    drop_views(m);
+    return rc;
+}
+
+int nnc_model_run_staged(nnc_model* m, int role, const char* names) {
+    return guarded([&] {
+        std::set<std::string> want;
+        std::string cur;
+        for (const char* c = names; c && *c; ++c) {
+            if (*c == ',') {
+                if (!cur.empty()) want.insert(cur);
+                cur.clear();
+            } else {
+                cur += *c;
+            }
+        }
+        if (!cur.empty()) want.insert(cur);
+        runtime::ExecOptions o = m->opts;
+        if (!want.empty()) o.materialize = &want;
+        const plan::ExecutionPlan& p = role == 1 ? m->plans.train_fwd : m->plans.inference;
+        runtime::execute_launch_staged(p, *m->host, nullptr, o);
+    });
+}
+
+int nnc_model_staged_outputs(nnc_model* m, int role) {
+    return guarded([&] {
+        const plan::ExecutionPlan& p = role == 1 ? m->plans.train_fwd : m->plans.inference;
+        m->outputs = runtime::execute_staged_outputs(p, nullptr);
+    });
+}
+
 int nnc_model_output(nnc_model* m, const char* name, float* out, int64_t n) {
     return guarded([&] {
         auto it = m->outputs.find(name);

@@ -1020,13 +1020,12 @@ void check_inputs(const ExecutionPlan& p, const std::map<std::string, Tensor>& i
 
 }  // namespace
 
-std::map<std::string, Tensor> execute(const ExecutionPlan& p, const std::map<std::string, Tensor>& inputs,
-                                      const HostModel& model, Device* device, const ExecOptions& opts) {
-    Device& dev = device ? *device : default_device();
+namespace {
+
+// The bound program of `p` on `dev` with the current weights (stamp-checked
+// device cache; a changed weight pointer rebinds).
+ExecCache& bound_cache(const ExecutionPlan& p, const HostModel& model, Device& dev, const ExecOptions& opts) {
     auto& slot = exec_caches()[{&dev, p.uid}];
-    const bool reuse_inputs = opts.inputs_resident && slot && slot->runs > 0;
-    if (!reuse_inputs) check_inputs(p, inputs);
-    // weights: stamp-checked device cache (uploads only stale tensors)
     std::map<std::string, void*> wptrs;
     for (const std::string& w : p.weight_names) wptrs[w] = dev.weight_buffer(model, w, model.tensor(w), model.stamp(w));
     if (!slot || slot->weight_ptrs != wptrs || slot->prog->precision != opts.gemm_precision) {
@@ -1039,28 +1038,89 @@ std::map<std::string, Tensor> execute(const ExecutionPlan& p, const std::map<std
                          [](const std::string&) -> void* { return nullptr; });
         slot->weight_ptrs = wptrs;
     }
-    Program& prog = *slot->prog;
+    return *slot;
+}
+
+// first run eagerly (sizes scratch, compiles kernels); later runs replay a graph
+void run_bound(ExecCache& c, const ExecutionPlan& p, const ExecOptions& opts) {
+    nncb_ctx* ctx = c.prog->dev->ctx();
+    if (!opts.use_graphs || c.runs == 0) {
+        c.prog->enqueue_plan(0, opts.trace);
+    } else {
+        if (!c.graph) {
+            NNC_CHECK(nncb_capture_begin(ctx));
+            c.prog->enqueue_plan(0, nullptr);
+            NNC_CHECK(nncb_capture_end(ctx, &c.graph));
+        }
+        if (opts.trace)
+            for (const auto& es : p.exec_steps) opts.trace->push_back("exec:" + es.label);
+        NNC_CHECK(nncb_graph_launch(ctx, c.graph));
+    }
+    ++c.runs;
+}
+
+// Pipelined execute (execute_stage / execute_launch_staged / execute_staged_outputs)
+struct StagedIO {
+    struct Slot {
+        std::vector<void*> in;   // per input slot of the plan
+        void* ready = nullptr;
+        void* consumed = nullptr;
+        bool used = false;
+    };
+    Device* dev = nullptr;
+    Slot slots[2];
+    uint64_t n_staged = 0, n_launched = 0;
+    std::vector<std::string> out_names;
+    std::vector<void*> out_pinned;
+    std::vector<std::vector<int64_t>> out_dims;
+    void* done = nullptr;
+    bool pending = false;
+    ~StagedIO() {
+        try {
+            nncb_ctx* ctx = dev->ctx();
+            nncb_sync(ctx);
+            for (Slot& s : slots) {
+                for (void* q : s.in) nncb_free(ctx, q);
+                for (void* e : {s.ready, s.consumed})
+                    if (e) nncb_event_destroy(e);
+            }
+            for (void* h : out_pinned) nncb_host_free(h);
+            if (done) nncb_event_destroy(done);
+        } catch (...) {
+        }
+    }
+};
+
+std::map<std::pair<const Device*, uint64_t>, std::unique_ptr<StagedIO>>& staged_ios() {
+    static std::map<std::pair<const Device*, uint64_t>, std::unique_ptr<StagedIO>> m;
+    return m;
+}
+
+}  // namespace
+
+std::map<std::string, Tensor> execute(const ExecutionPlan& p, const std::map<std::string, Tensor>& inputs,
+                                      const HostModel& model, Device* device, const ExecOptions& opts) {
+    Device& dev = device ? *device : default_device();
+    {
+        auto it = exec_caches().find({&dev, p.uid});
+        const bool reuse = opts.inputs_resident && it != exec_caches().end() && it->second && it->second->runs > 0;
+        if (!reuse) check_inputs(p, inputs);
+    }
+    const bool had_runs = [&] {
+        auto it = exec_caches().find({&dev, p.uid});
+        return it != exec_caches().end() && it->second && it->second->runs > 0;
+    }();
+    ExecCache& c = bound_cache(p, model, dev, opts);
+    Program& prog = *c.prog;
     nncb_ctx* ctx = dev.ctx();
-    if (!reuse_inputs || slot->runs == 0)   // (a rebound program starts with runs == 0)
+    const bool reuse_inputs = opts.inputs_resident && had_runs && c.runs > 0;
+    if (!reuse_inputs)   // (a rebound program starts with runs == 0)
         for (uint32_t s : p.input_slots) {
             const Tensor& t = inputs.at(p.values[s].name);
             NNC_CHECK(nncb_h2d(ctx, prog.ptr(p.values[s].name), t.data(), t.byte_size()));
             dev.stats().h2d_bytes += t.byte_size();
         }
-    // first run eagerly (sizes scratch, compiles kernels); later runs replay a graph
-    if (!opts.use_graphs || slot->runs == 0) {
-        prog.enqueue_plan(0, opts.trace);
-    } else {
-        if (!slot->graph) {
-            NNC_CHECK(nncb_capture_begin(ctx));
-            prog.enqueue_plan(0, nullptr);
-            NNC_CHECK(nncb_capture_end(ctx, &slot->graph));
-        }
-        if (opts.trace)
-            for (const auto& es : p.exec_steps) opts.trace->push_back("exec:" + es.label);
-        NNC_CHECK(nncb_graph_launch(ctx, slot->graph));
-    }
-    ++slot->runs;
+    run_bound(c, p, opts);
     std::map<std::string, Tensor> out;
     for (uint32_t s : p.output_slots) {
         const auto& v = p.values[s];
@@ -1071,6 +1131,102 @@ std::map<std::string, Tensor> execute(const ExecutionPlan& p, const std::map<std
         out.emplace(v.name, std::move(t));
     }
     NNC_CHECK(nncb_sync(ctx));
+    return out;
+}
+
+void execute_stage(const ExecutionPlan& p, const std::map<std::string, Tensor>& inputs, Device* device) {
+    Device& dev = device ? *device : default_device();
+    check_inputs(p, inputs);
+    auto& io = staged_ios()[{&dev, p.uid}];
+    if (!io) {
+        io = std::make_unique<StagedIO>();
+        io->dev = &dev;
+    }
+    nncb_ctx* ctx = dev.ctx();
+    StagedIO::Slot& S = io->slots[io->n_staged % 2];
+    if (!S.ready) {
+        for (uint32_t s : p.input_slots) {
+            void* b = nullptr;
+            NNC_CHECK(nncb_malloc(ctx, static_cast<size_t>(element_count(p.values[s].dims)) * dtype_size(p.dtype), &b));
+            S.in.push_back(b);
+        }
+        NNC_CHECK(nncb_event_create(&S.ready));
+        NNC_CHECK(nncb_event_create(&S.consumed));
+    }
+    if (S.used) NNC_CHECK(nncb_stream_wait(ctx, NNCB_STREAM_COPY, S.consumed));
+    for (size_t k = 0; k < p.input_slots.size(); ++k) {
+        const Tensor& t = inputs.at(p.values[p.input_slots[k]].name);
+        NNC_CHECK(nncb_h2d_async(ctx, S.in[k], t.data(), t.byte_size()));
+        dev.stats().h2d_bytes += t.byte_size();
+    }
+    NNC_CHECK(nncb_event_record_on(ctx, NNCB_STREAM_COPY, S.ready));
+    ++io->n_staged;
+}
+
+void execute_launch_staged(const ExecutionPlan& p, const HostModel& model, Device* device, const ExecOptions& opts) {
+    Device& dev = device ? *device : default_device();
+    auto it = staged_ios().find({&dev, p.uid});
+    if (it == staged_ios().end() || it->second->n_launched >= it->second->n_staged)
+        throw Error(Error::Code::BadDocument, "execute_launch_staged: no staged inputs");
+    StagedIO& io = *it->second;
+    if (io.pending) throw Error(Error::Code::BadDocument, "execute_launch_staged: collect the previous outputs first");
+    ExecCache& c = bound_cache(p, model, dev, opts);
+    nncb_ctx* ctx = dev.ctx();
+    StagedIO::Slot& S = io.slots[io.n_launched % 2];
+    NNC_CHECK(nncb_stream_wait(ctx, NNCB_STREAM_COMPUTE, S.ready));
+    for (size_t k = 0; k < p.input_slots.size(); ++k) {
+        const auto& v = p.values[p.input_slots[k]];
+        NNC_CHECK(nncb_d2d(ctx, c.prog->ptr(v.name), S.in[k], static_cast<size_t>(element_count(v.dims)) * dtype_size(p.dtype)));
+    }
+    NNC_CHECK(nncb_event_record_on(ctx, NNCB_STREAM_COMPUTE, S.consumed));
+    S.used = true;
+    run_bound(c, p, opts);
+    // the outputs come back into pinned buffers asynchronously
+    std::vector<std::string> names;
+    std::vector<std::vector<int64_t>> dims;
+    for (uint32_t s : p.output_slots) {
+        const auto& v = p.values[s];
+        if (opts.materialize && !opts.materialize->count(v.name)) continue;
+        names.push_back(v.name);
+        dims.push_back(v.dims);
+    }
+    if (names != io.out_names) {
+        NNC_CHECK(nncb_sync(ctx));
+        for (void* h : io.out_pinned) nncb_host_free(h);
+        io.out_pinned.clear();
+        for (const auto& d : dims) {
+            void* h = nullptr;
+            NNC_CHECK(nncb_host_alloc(std::max<size_t>(static_cast<size_t>(element_count(d)) * dtype_size(p.dtype), 16), &h));
+            io.out_pinned.push_back(h);
+        }
+        io.out_names = names;
+        io.out_dims = dims;
+    }
+    for (size_t k = 0; k < names.size(); ++k) {
+        const size_t bytes = static_cast<size_t>(element_count(dims[k])) * dtype_size(p.dtype);
+        NNC_CHECK(nncb_d2h_async(ctx, io.out_pinned[k], c.prog->ptr(names[k]), bytes));
+        dev.stats().d2h_bytes += bytes;
+    }
+    if (!io.done) NNC_CHECK(nncb_event_create(&io.done));
+    NNC_CHECK(nncb_event_record_on(ctx, NNCB_STREAM_COMPUTE, io.done));
+    io.pending = true;
+    ++io.n_launched;
+}
+
+std::map<std::string, Tensor> execute_staged_outputs(const ExecutionPlan& p, Device* device) {
+    Device& dev = device ? *device : default_device();
+    auto it = staged_ios().find({&dev, p.uid});
+    if (it == staged_ios().end() || !it->second->pending)
+        throw Error(Error::Code::BadDocument, "execute_staged_outputs: no launched run");
+    StagedIO& io = *it->second;
+    NNC_CHECK(nncb_event_sync(io.done));
+    std::map<std::string, Tensor> out;
+    for (size_t k = 0; k < io.out_names.size(); ++k) {
+        Tensor t = Tensor::uninitialized(p.dtype, io.out_dims[k]);
+        nncb_host_copy(t.data(), io.out_pinned[k], t.byte_size());
+        out.emplace(io.out_names[k], std::move(t));
+    }
+    io.pending = false;
     return out;
 }
 

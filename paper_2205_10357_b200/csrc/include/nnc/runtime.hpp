@@ -125,6 +125,20 @@ std::map<std::string, Tensor> execute(const plan::ExecutionPlan& p,
                                       const HostModel& model, Device* device = nullptr,
                                       const ExecOptions& opts = {});
 
+/// Pipelined execute from host buffers. execute_stage uploads the next run's
+/// inputs into one of two device staging slots on the copy stream (the host
+/// bytes are consumed on return); execute_launch_staged makes the compute
+/// stream wait for the oldest staged slot, copies it into the plan's inputs
+/// (device to device), runs the plan and starts the output downloads into
+/// pinned buffers; execute_staged_outputs waits for them. Calling
+/// execute_stage for run i + 1 between the launch and the collection of run i
+/// overlaps its upload with run i. Outputs equal execute()'s.
+void execute_stage(const plan::ExecutionPlan& p, const std::map<std::string, Tensor>& inputs,
+                   Device* device = nullptr);
+void execute_launch_staged(const plan::ExecutionPlan& p, const HostModel& model, Device* device = nullptr,
+                           const ExecOptions& opts = {});
+std::map<std::string, Tensor> execute_staged_outputs(const plan::ExecutionPlan& p, Device* device = nullptr);
+
 L1Result l1_loss(const Tensor& pred, const Tensor& target, Device* device = nullptr);
 
 void sgd_step(HostModel& model, const std::map<std::string, Tensor>& grads, double lr,

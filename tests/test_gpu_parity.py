@@ -204,3 +204,23 @@ def test_pipelined_train_steps_match_sequential():
         assert np.array_equal(a.weight(w), b.weight(w)), w
     assert b.train_steps([], 0.05) == []
     assert len(b.train_steps(batches[:1], 0.05)) == 1
+
+
+def test_pipelined_runs_match_sequential():
+    """run_many (upload of run i+1 on the copy stream while run i executes)
+    returns bitwise the outputs of one run() per batch, also for a subset."""
+    doc = W.c1_small_cnn(8, bn=True)
+    m = P.CompiledModel(doc, precision=P.PREC_TF32)
+    batches = [{"x": W.uniform((8, 32, 32, 3), 30 + i, "x")} for i in range(4)]
+    seq = [m.run(b) for b in batches]
+    pipe = m.run_many(batches)
+    assert len(pipe) == 4
+    for a, b in zip(seq, pipe):
+        assert a.keys() == b.keys()
+        for k in a:
+            assert np.array_equal(a[k], b[k]), k
+    name = sorted(seq[0])[0]
+    sub = m.run_many(batches[:2], outputs=[name])
+    assert [list(o) for o in sub] == [[name], [name]]
+    assert np.array_equal(sub[1][name], seq[1][name])
+    assert m.run_many([]) == []
