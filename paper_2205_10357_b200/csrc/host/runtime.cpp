@@ -425,6 +425,9 @@ struct Program {
                     const BoundLaunch& c = steps[pi][i];
                     if (c.kind != LaunchKind::Gemm || c.skip || c.eg_sg) continue;
                     if (c.gemm.kind != NNCB_CONV_DGRAD) continue;   // the epilogue exists in the conv path
+                    // strided dgrads store sub-pixel phases directly: no TMA side
+                    // tiles, and the per-row side loads measured 2-6x slower
+                    if (c.gemm.sh != 1 || c.gemm.sw != 1) continue;
                     if (std::find(e.ptrs.begin(), e.ptrs.end(), c.ptrs.back()) != e.ptrs.end()) {
                         gi = i;
                         break;
