@@ -42,6 +42,8 @@ constexpr int BK = 32;        // fp32 elements per K step = one 128-byte swizzle
 constexpr int MAX_STAGES = 6;
 constexpr int THREADS = 320;   // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue (2 per TMEM lane quarter)
 constexpr int MAX_TAPS = 64;
+constexpr int HALO_TW = 8, HALO_TH = 16;
+constexpr uint32_t HALO_A_BYTES = (HALO_TW + 2) * HALO_TH * 128;   // 20 KB, 1 KB-aligned
 
 enum { MODE_CONV = 0, MODE_WGRAD = 1 };
 
@@ -90,6 +92,11 @@ struct TcParams {
     int nostore;        // tuning knob: skip the output stores (epilogue cost probe)
     int stg_cols;       // epilogue transpose width per pass: 32, 16 or 8 columns (4/2/1 KB per warp)
     int stg_bufs;       // staging tiles per warp: 2 lets a pass's TMA store overlap staging of the next
+    // --- halo (3x3 stride-1 forward): one (TW+2) x TH input patch per (32-channel
+    // block, kernel row) feeds the row's three taps through shifted descriptors
+    // (TW = 8, TH = 16, TN = 1: each 8-row core-matrix group is one image row,
+    // group stride TW + 2 rows); a stage = patch + the three taps' B tiles
+    int halo;
     double* colstats;   // fused BatchNorm statistics: [0,N) sum, [N,2N) sum of squares
     // --- manual A (channel counts that do not fill a 32-wide TMA block) -----
     // Builder warps gather A straight from the NHWC activation into the
@@ -613,9 +620,10 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
     nncb::pdl_trigger();   // follow-up folds / finalizes may be scheduled while this grid drains
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const uint32_t a_bytes = BM * BK * 4;                 // 16 KB
+    const uint32_t a_bytes = P.halo ? HALO_A_BYTES : BM * BK * 4;   // 16 KB (halo: 20 KB patch)
     // PAIR: this CTA holds half of the B tile's columns (the MMA spans both CTAs)
-    const uint32_t b_bytes = static_cast<uint32_t>(PAIR ? P.bn / 2 : P.bn) * BK * 4;
+    const uint32_t bt_bytes = static_cast<uint32_t>(PAIR ? P.bn / 2 : P.bn) * BK * 4;   // one tap's B tile
+    const uint32_t b_bytes = bt_bytes * (P.halo ? 3u : 1u);
     const uint32_t rank = PAIR ? cluster_rank() : 0u;
     const uint32_t stage_bytes = a_bytes + b_bytes;
     uint8_t* staging = smem + STAGES * stage_bytes;       // 8 x stg_cols*128 B: one transpose tile per epilogue warp
@@ -772,7 +780,30 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
         };
         for (int64_t t = t_begin; t < P.tiles; t += t_step) {
             const Tile T = decode(t);
-            if (P.mode == MODE_CONV) {
+            if (P.mode == MODE_CONV && P.halo) {
+                // k-step (kernel row dh, channel block cb): the (TW+2) x TH patch at
+                // (tw0 - 1, th0 - 1 + dh) and the row's three taps' weights
+                const int aw = T.tw0 + P.off_w[0], ah = T.th0 + P.off_h[0], n0 = static_cast<int>(T.n0) + boff;
+                int cb = 0, dh = 0;
+                for (int i = 0; i < T.nk; ++i) {
+                    uint8_t* sa; uint64_t* bar;
+                    acquire(sa, bar);
+                    const int c0 = cb * BK;
+                    ld4(sa, &map_a, bar, c0, aw, ah + dh, T.tn0);
+#pragma unroll
+                    for (int dw = 0; dw < 3; ++dw) {
+                        uint8_t* sb = sa + a_bytes + dw * bt_bytes;
+                        const int br = P.brow[dh * 3 + dw];
+                        if (P.b_mn) {
+                            for (int q = 0; q < bcols / 32; ++q) ld2(sb + q * 4096, &map_b, bar, n0 + 32 * q, br + c0);
+                        } else {
+                            ld2(sb, &map_b, bar, br + c0, n0);   // K-major forward weights [co][kh*kw*ci]
+                        }
+                    }
+                    advance();
+                    if (++cb == P.cblocks) { cb = 0; ++dh; }
+                }
+            } else if (P.mode == MODE_CONV) {
                 int tap = P.tap0[T.phase], cb = 0;
                 const int aw = T.tw0 * P.mw, ah = T.th0 * P.mh, n0 = static_cast<int>(T.n0) + boff;
                 int xw = aw + P.off_w[tap], yh = ah + P.off_h[tap], br = P.brow[tap];
@@ -845,7 +876,9 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                                (static_cast<uint32_t>(P.b_mn) << 16) | ((static_cast<uint32_t>(P.bn) >> 3) << 17) |
                                ((static_cast<uint32_t>(PAIR ? 2 * BM : BM) >> 4) << 24);
         const uint32_t s0 = smem_u32(smem);
-        const uint64_t adesc0 = a_mn ? sdesc(s0, 4096, 512, 1) : sdesc(s0, 16, 1024, 2);
+        // halo: the A window of tap dw starts dw rows into the patch; 8-row groups
+        // are image rows, (TW + 2) rows apart (measured: tools/mma_probe/halo_probe.cu)
+        const uint64_t adesc0 = a_mn ? sdesc(s0, 4096, 512, 1) : sdesc(s0, 16, P.halo ? (HALO_TW + 2) * 128 : 1024, 2);
         const uint64_t bdesc0 = P.b_mn ? sdesc(s0 + a_bytes, 4096, 512, 1) : sdesc(s0 + a_bytes, 16, 1024, 2);
         const uint64_t a_kstep = a_mn ? (1024 >> 4) : (32 >> 4), b_kstep = P.b_mn ? (1024 >> 4) : (32 >> 4);
         const uint64_t stage16 = stage_bytes >> 4;
@@ -866,7 +899,18 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                 if (MA) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // cp.async data -> async proxy
                 if (++slot == STAGES) { slot = 0; phase ^= 1u; }
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                if (leader) {
+                if (leader && P.halo) {
+                    const uint64_t so = static_cast<uint64_t>(s) * stage16;
+#pragma unroll
+                    for (int dw = 0; dw < 3; ++dw)
+#pragma unroll
+                        for (int kk = 0; kk < BK / 8; ++kk) {
+                            const uint64_t ad = adesc0 + so + dw * (128 >> 4) + kk * a_kstep;
+                            const uint64_t bd = bdesc0 + so + dw * (bt_bytes >> 4) + kk * b_kstep;
+                            mma_tf32(d, ad, bd, idesc, (i > 0 || dw > 0 || kk > 0) ? 1u : 0u);
+                        }
+                    mma_commit(&empty[s]);
+                } else if (leader) {
                     const uint64_t so = static_cast<uint64_t>(s) * stage16;
 #pragma unroll
                     for (int kk = 0; kk < BK / 8; ++kk) {
@@ -1208,6 +1252,7 @@ thread_local int g_force_pair = 0;   // 1: run the call as CTA pairs (cta_group:
 thread_local int g_force_wide = 0;   // 1: full-width (32-column) epilogue staging even at 2 CTAs/SM
 thread_local int g_dil_w = 1;        // horizontal tap dilation for the next implicit GEMM (internal)
 thread_local int g_force_tb = 0;     // 1: forward convolution with transposed (K-major) weights
+thread_local int g_force_halo = 0;   // 1: 3x3 stride-1 forward convolution through halo patches
 
 int pick_bn(int64_t n) {
     static const int env_bn = getenv("NNCB_TC_BN") ? atoi(getenv("NNCB_TC_BN")) : 0;   // tuning knob
@@ -1373,6 +1418,7 @@ int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CU
     static bool attr_done = false;
     if (!attr_done) {
         NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<false, false, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<false, false, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<true, false, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<true, false, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         NNCB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<false, true, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -1435,6 +1481,46 @@ int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CU
     }
     const bool manual = P.xa != nullptr;
     const int tab_ints = manual ? 3 * std::max(P.cblocks * BK, BK) : 0;
+    if (P.halo) {
+        // stage = patch + three taps' B tiles: two CTAs per SM when two stages
+        // fit, else one CTA with a deeper ring
+        const size_t sbh = HALO_A_BYTES + 3 * static_cast<size_t>(P.bn) * BK * 4;
+        int per = 0;
+        for (int stg : {32, 16, 8}) {
+            const size_t fixed = smem_for(P.bn, 0, stg);
+            if (fixed + 2 * sbh <= 113 * 1024 && P.bn <= 128) {
+                P.stg_cols = stg;
+                P.stages = static_cast<int>(std::min<size_t>(MAX_STAGES, (113 * 1024 - fixed) / sbh));
+                per = 2;
+                break;
+            }
+        }
+        if (!per)
+            for (int stg : {32, 16, 8}) {
+                const size_t fixed = smem_for(P.bn, 0, stg);
+                if (fixed + 2 * sbh <= 227 * 1024) {
+                    P.stg_cols = stg;
+                    P.stages = static_cast<int>(std::min<size_t>(MAX_STAGES, (227 * 1024 - fixed) / sbh));
+                    per = 1;
+                    if (P.stages >= 3) break;
+                }
+            }
+        if (!per) return nncb::fail("gemm: halo tile does not fit shared memory");
+        P.stg_bufs = 1;
+        const size_t smem = static_cast<size_t>(P.stages) * sbh + smem_for(P.bn, 0, P.stg_cols);
+        encode_tma_out(&mc, P);
+        const unsigned grid = static_cast<unsigned>(std::min<int64_t>(P.tiles, static_cast<int64_t>(ctx->sm_count) * per));
+        if (per == 2 && P.colstats)
+            tc_gemm_kernel<true, false, 2, false><<<grid, THREADS, smem, ctx->stream>>>(ma, mb, mc, P, em);
+        else if (per == 2)
+            tc_gemm_kernel<false, false, 2, false><<<grid, THREADS, smem, ctx->stream>>>(ma, mb, mc, P, em);
+        else if (P.colstats)
+            tc_gemm_kernel<true, false, 1, false><<<grid, THREADS, smem, ctx->stream>>>(ma, mb, mc, P, em);
+        else
+            tc_gemm_kernel<false, false, 1, false><<<grid, THREADS, smem, ctx->stream>>>(ma, mb, mc, P, em);
+        NNCB_LAUNCHED(ctx);
+        return 0;
+    }
     if (g_force_wide && shp.per_sm == 2 && !manual) {
         // output-bound shapes: whole 128-byte row segments per store beat a deeper ring
         P.stg_cols = 32;
@@ -1708,6 +1794,13 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
             const size_t nb = cands.size();
             for (size_t ci_ = 0; ci_ < nb; ++ci_) cands.push_back(cands[ci_] | 0x40000);
         }
+        static const bool halo_on = !(getenv("NNCB_TC_HALO") && atoi(getenv("NNCB_TC_HALO")) == 0);
+        if (halo_on && d->kind == NNCB_CONV_FWD && d->kh == 3 && d->kw == 3 && d->sh == 1 && d->sw == 1 &&
+            d->pad_top == 1 && d->pad_left == 1 && d->ci % 32 == 0 && d->ow >= HALO_TW) {   // bit 19: halo patches
+            const size_t nb = cands.size();
+            for (size_t ci_ = 0; ci_ < nb; ++ci_)
+                if (!(cands[ci_] & 0x30000)) cands.push_back(cands[ci_] | 0x80000);   // 1-CTA tiles, default staging
+        }
         cudaEvent_t e0, e1;
         NNCB_CUDA(cudaEventCreate(&e0));
         NNCB_CUDA(cudaEventCreate(&e1));
@@ -1717,12 +1810,14 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
             g_force_pair = (c >> 16) & 1;
             g_force_wide = (c >> 17) & 1;
             g_force_tb = (c >> 18) & 1;
+            g_force_halo = (c >> 19) & 1;
             int rc = gemm_tc_route(ctx, d, a, b, bias, out, handled);   // warm-up (and validity)
             if (rc || !*handled) {
                 g_force_bn = 0;
                 g_force_pair = 0;
                 g_force_wide = 0;
                 g_force_tb = 0;
+                g_force_halo = 0;
                 cudaEventDestroy(e0);
                 cudaEventDestroy(e1);
                 return rc;
@@ -1734,6 +1829,7 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
             g_force_pair = 0;
             g_force_wide = 0;
             g_force_tb = 0;
+            g_force_halo = 0;
             if (rc) {
                 cudaEventDestroy(e0);
                 cudaEventDestroy(e1);
@@ -1756,11 +1852,13 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
     g_force_pair = (choice >> 16) & 1;
     g_force_wide = (choice >> 17) & 1;
     g_force_tb = (choice >> 18) & 1;
+    g_force_halo = (choice >> 19) & 1;
     const int rc = gemm_tc_route(ctx, d, a, b, bias, out, handled);
     g_force_bn = 0;
     g_force_pair = 0;
     g_force_wide = 0;
     g_force_tb = 0;
+    g_force_halo = 0;
     return rc;
 }
 
@@ -1941,6 +2039,16 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
                 }
         }
         pick_box(BM, P.gn, P.gh, P.gw, P.TN, P.TH, P.TW);
+        if (fwd && g_force_halo && !manual && !P.pair && kh == 3 && kw == 3 && sh == 1 && sw == 1 && pt == 1 &&
+            pl == 1 && ci % 32 == 0 && g_dil_w == 1 && ow >= HALO_TW &&
+            2 * (HALO_A_BYTES + 3 * static_cast<size_t>(P.bn) * BK * 4) + smem_for(P.bn, 0, 8) <= 227 * 1024) {
+            // (a two-stage ring must fit: 256-wide tiles do not)
+            P.halo = 1;
+            P.TN = 1;
+            P.TH = HALO_TH;
+            P.TW = HALO_TW;
+            P.ntaps[0] = 3;   // k-steps per channel block: one per kernel row
+        }
         P.tiles_w = (P.gw + P.TW - 1) / P.TW;
         P.tiles_h = (P.gh + P.TH - 1) / P.TH;
         const int tiles_n = (P.gn + P.TN - 1) / P.TN;
@@ -1948,7 +2056,9 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
         if (tiles >= (int64_t(1) << 31) || P.TW * P.mw > 256 || P.TH * P.mh > 256) return 0;
         // A: the activation (x for fwd, g for dgrad) as {C, W, H, N}
         const float* act = a;
-        if (fwd) {
+        if (fwd && P.halo) {
+            if (!encode_4d(&ma, act, ci, iw, ih, n, 32, P.TW + 2, P.TH, 1, 1, 1, false, lda)) return 1;
+        } else if (fwd) {
             if (!manual &&
                 !encode_4d(&ma, act, ci, iw, ih, n, 32, P.TW * (int)sw, P.TH * (int)sh, P.TN, (int)sw, (int)sh, false, lda))
                 return 1;

@@ -347,3 +347,46 @@ def test_conv_fwd_caller_kmajor_weights(shape):
     finally:
         K.nncb_gemm_force_tile(0)
     check(out.get((n, g["oh"], g["ow"], co)), ex.get((n, g["oh"], g["ow"], co)).astype(np.float64))
+
+
+HALO_CONVS = [(2, 14, 14, 64, 64, 3, 1), (2, 56, 56, 64, 64, 3, 1), (1, 28, 28, 128, 128, 3, 1),
+              (3, 9, 13, 32, 64, 3, 1), (2, 30, 30, 256, 256, 3, 1)]
+
+
+@pytest.mark.parametrize("shape", HALO_CONVS)
+@pytest.mark.parametrize("tile", [0x80000 | 64, 0x80000 | 128, 0x80000 | 0x40000 | 128, 0x80000 | 256])
+def test_conv_fwd_halo(shape, tile):
+    """3x3 stride-1 forward through halo patches (one (TW+2) x TH patch per
+    channel block and kernel row, taps as shifted descriptors), with bias and
+    BatchNorm column statistics, against the exact path."""
+    n, ih, iw, ci, co, k, s = shape
+    if (tile & 0xffff) > 64 and co <= 64 and (tile & 0xffff) == 256:
+        pytest.skip("256-wide tile on a 64-channel output")
+    g = conv_geom(n, ih, iw, ci, co, k, s)
+    rng = np.random.default_rng(17)
+    x = rng.uniform(-1, 1, (n, ih, iw, ci)).astype(np.float32)
+    w = rng.uniform(-1, 1, (k, k, ci, co)).astype(np.float32)
+    bias = rng.uniform(-1, 1, co).astype(np.float32)
+    xd, wd, bd = Dev(x), Dev(w), Dev(bias)
+    oshape = (n, g["oh"], g["ow"], co)
+    ex = Dev(nbytes=int(np.prod(oshape)) * 4)
+    gemm(GemmDesc(kind=CONV_FWD, precision=1, epilogue=1, **g), xd, wd, bd, ex)
+    out = Dev(nbytes=int(np.prod(oshape)) * 4)
+    cs = Dev(nbytes=2 * co * 8)
+    d = GemmDesc(kind=CONV_FWD, precision=0, epilogue=1 | 4, **g)
+    d.colstats = cs.p
+    K.nncb_gemm_force_tile(tile)
+    try:
+        gemm(d, xd, wd, bd, out)
+        assert K.nncb_gemm_last_path() == 1
+    finally:
+        K.nncb_gemm_force_tile(0)
+    want = ex.get(oshape).astype(np.float64)
+    check(out.get(oshape), want)
+    raw = np.empty(2 * co, np.float64)
+    assert K.nncb_d2h(ctx(), raw.ctypes.data, cs.p, raw.nbytes) == 0
+    K.nncb_sync(ctx())
+    s1 = want.reshape(-1, co).sum(0)
+    s2 = (want ** 2).reshape(-1, co).sum(0)
+    assert np.linalg.norm(raw[:co] - s1) <= 2e-2 * np.linalg.norm(s1)
+    assert np.linalg.norm(raw[co:] - s2) <= 2e-2 * np.linalg.norm(s2)

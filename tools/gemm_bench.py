@@ -42,12 +42,13 @@ def main():
     ap.add_argument("--colstats", action="store_true", help="forward GEMMs also accumulate BN column statistics")
     ap.add_argument("--eg", action="store_true", help="dgrad GEMMs run the ReLU-gradient + BN-sums epilogue")
     ap.add_argument("--res", action="store_true", help="with --eg: add a residual gradient")
-    ap.add_argument("--tile", default="auto", help="auto | 128 | 256 | p128 | p256 | w128 | t128 | tp256 ... (p = CTA pair, w = wide staging, t = K-major weights)")
+    ap.add_argument("--tile", default="auto", help="auto | 128 | 256 | p128 | p256 | w128 | t128 | h64 | th128 ... (p = CTA pair, w = wide staging, t = K-major weights, h = halo patches)")
     a = ap.parse_args()
     timer = P.DeviceTimer()
     if a.tile != "auto":
         t = a.tile
-        code = int(t.lstrip("pwt")) | (0x10000 if "p" in t else 0) | (0x20000 if "w" in t else 0) | (0x40000 if "t" in t else 0)
+        code = (int(t.lstrip("pwth")) | (0x10000 if "p" in t else 0) | (0x20000 if "w" in t else 0) |
+                (0x40000 if "t" in t else 0) | (0x80000 if "h" in t else 0))
         K.nncb_gemm_force_tile(code)
     total = {}
     for name, h, ci, co, k, s in LAYERS:
