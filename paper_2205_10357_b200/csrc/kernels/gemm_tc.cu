@@ -796,8 +796,10 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                         const int br = P.brow[dh * 3 + dw];
                         if (P.b_mn) {
                             for (int q = 0; q < bcols / 32; ++q) ld2(sb + q * 4096, &map_b, bar, n0 + 32 * q, br + c0);
-                        } else {
+                        } else if (P.bt) {
                             ld2(sb, &map_b, bar, br + c0, n0);   // K-major forward weights [co][kh*kw*ci]
+                        } else {
+                            ld2(sb, &map_b, bar, c0, br + n0);   // dgrad: weights [tap][ci][co], K = co
                         }
                     }
                     advance();
@@ -1795,8 +1797,11 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
             for (size_t ci_ = 0; ci_ < nb; ++ci_) cands.push_back(cands[ci_] | 0x40000);
         }
         static const bool halo_on = !(getenv("NNCB_TC_HALO") && atoi(getenv("NNCB_TC_HALO")) == 0);
-        if (halo_on && d->kind == NNCB_CONV_FWD && d->kh == 3 && d->kw == 3 && d->sh == 1 && d->sw == 1 &&
-            d->pad_top == 1 && d->pad_left == 1 && d->ci % 32 == 0 && d->ow >= HALO_TW) {   // bit 19: halo patches
+        const bool halo_fwd = d->kind == NNCB_CONV_FWD && d->ci % 32 == 0 && d->ow >= HALO_TW;
+        const bool halo_dgrad = d->kind == NNCB_CONV_DGRAD && d->co % 32 == 0 && d->iw >= HALO_TW;
+        if (halo_on && (halo_fwd || halo_dgrad) && !(d->epilogue & NNCB_EPI_RELU_GRAD) && d->kh == 3 && d->kw == 3 &&
+            d->sh == 1 && d->sw == 1 &&
+            d->pad_top == 1 && d->pad_left == 1) {   // bit 19: halo patches
             const size_t nb = cands.size();
             for (size_t ci_ = 0; ci_ < nb; ++ci_)
                 if (!(cands[ci_] & 0x30000)) cands.push_back(cands[ci_] | 0x80000);   // 1-CTA tiles, default staging
@@ -2039,8 +2044,11 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
                 }
         }
         pick_box(BM, P.gn, P.gh, P.gw, P.TN, P.TH, P.TW);
-        if (fwd && g_force_halo && !manual && !P.pair && kh == 3 && kw == 3 && sh == 1 && sw == 1 && pt == 1 &&
-            pl == 1 && ci % 32 == 0 && g_dil_w == 1 && ow >= HALO_TW &&
+        // halo: forward, or a stride-1 dgrad (its tap table visits kernel rows
+        // with off_w = -1, 0, 1 in order, like the forward)
+        if (g_force_halo && !manual && !P.pair && !(d->epilogue & NNCB_EPI_RELU_GRAD) && kh == 3 && kw == 3 && sh == 1 &&
+            sw == 1 && pt == 1 && pl == 1 &&
+            Ck % 32 == 0 && g_dil_w == 1 && (fwd ? ow : iw) >= HALO_TW &&
             2 * (HALO_A_BYTES + 3 * static_cast<size_t>(P.bn) * BK * 4) + smem_for(P.bn, 0, 8) <= 227 * 1024) {
             // (a two-stage ring must fit: 256-wide tiles do not)
             P.halo = 1;
@@ -2062,6 +2070,8 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
             if (!manual &&
                 !encode_4d(&ma, act, ci, iw, ih, n, 32, P.TW * (int)sw, P.TH * (int)sh, P.TN, (int)sw, (int)sh, false, lda))
                 return 1;
+        } else if (P.halo) {
+            if (!encode_4d(&ma, act, co, ow, oh, n, 32, P.TW + 2, P.TH, 1, 1, 1, false)) return 1;
         } else {
             if (!encode_4d(&ma, act, co, ow, oh, n, 32, P.TW, P.TH, P.TN, 1, 1, false)) return 1;
         }

@@ -390,3 +390,31 @@ def test_conv_fwd_halo(shape, tile):
     s2 = (want ** 2).reshape(-1, co).sum(0)
     assert np.linalg.norm(raw[:co] - s1) <= 2e-2 * np.linalg.norm(s1)
     assert np.linalg.norm(raw[co:] - s2) <= 2e-2 * np.linalg.norm(s2)
+
+
+@pytest.mark.parametrize("shape", HALO_CONVS[:4])
+@pytest.mark.parametrize("tile", [0x80000 | 64, 0x80000 | 128])
+def test_conv_dgrad_halo(shape, tile):
+    """3x3 stride-1 input gradient through halo patches of dY against the
+    exact dgrad."""
+    n, ih, iw, ci, co, k, s = shape
+    g = conv_geom(n, ih, iw, ci, co, k, s)
+    rng = np.random.default_rng(19)
+    gy = rng.uniform(-1, 1, (n, g["oh"], g["ow"], co)).astype(np.float32)
+    w = rng.uniform(-1, 1, (k, k, ci, co)).astype(np.float32)
+    gyd, wd = Dev(gy), Dev(w)
+    ex, out = Dev(nbytes=n * ih * iw * ci * 4), Dev(nbytes=n * ih * iw * ci * 4)
+    gemm(GemmDesc(kind=CONV_DGRAD, precision=1, epilogue=0, **g), gyd, wd, None, ex)
+    K.nncb_gemm_force_tile(tile)
+    try:
+        gemm(GemmDesc(kind=CONV_DGRAD, precision=0, epilogue=0, **g), gyd, wd, None, out)
+        assert K.nncb_gemm_last_path() == 1
+    finally:
+        K.nncb_gemm_force_tile(0)
+    check(out.get((n, ih, iw, ci)), ex.get((n, ih, iw, ci)).astype(np.float64))
+
+
+def test_dgrad_halo_relu_grad_epilogue():
+    """A forced halo tile with the relu-grad epilogue falls back to the regular
+    tile (halo launches have no side-tile build) and stays correct."""
+    test_dgrad_relu_grad_epilogue((2, 14, 14, 64, 64, 3, 1), 0x80000 | 64, True)
