@@ -44,6 +44,7 @@ constexpr int THREADS = 320;   // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue (2
 constexpr int MAX_TAPS = 64;
 constexpr int HALO_TW = 8, HALO_TH = 16;
 constexpr uint32_t HALO_A_BYTES = (HALO_TW + 2) * HALO_TH * 128;   // 20 KB, 1 KB-aligned
+constexpr uint32_t HALO9_A_BYTES = ((HALO_TW + 2) * (HALO_TH + 2) * 128 + 1023) / 1024 * 1024;   // full 3x3 patch, 23 KB
 
 enum { MODE_CONV = 0, MODE_WGRAD = 1 };
 
@@ -620,10 +621,13 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
     nncb::pdl_trigger();   // follow-up folds / finalizes may be scheduled while this grid drains
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const uint32_t a_bytes = P.halo ? HALO_A_BYTES : BM * BK * 4;   // 16 KB (halo: 20 KB patch)
+    // 16 KB (halo 1: 20 KB kernel-row patch; halo 2: 23 KB full 3x3 patch)
+    const uint32_t a_bytes = P.halo == 2 ? HALO9_A_BYTES : P.halo ? HALO_A_BYTES : BM * BK * 4;
     // PAIR: this CTA holds half of the B tile's columns (the MMA spans both CTAs)
     const uint32_t bt_bytes = static_cast<uint32_t>(PAIR ? P.bn / 2 : P.bn) * BK * 4;   // one tap's B tile
-    const uint32_t b_bytes = bt_bytes * (P.halo ? 3u : 1u);
+    const uint32_t b_bytes = bt_bytes * (P.halo == 2 ? 9u : P.halo ? 3u : 1u);
+    // bytes the TMA loads of one stage deliver (the full patch is padded to 1 KB in smem)
+    const uint32_t tx_bytes = (P.halo == 2 ? (HALO_TW + 2) * (HALO_TH + 2) * 128 : a_bytes) + b_bytes;
     const uint32_t rank = PAIR ? cluster_rank() : 0u;
     const uint32_t stage_bytes = a_bytes + b_bytes;
     uint8_t* staging = smem + STAGES * stage_bytes;       // 8 x stg_cols*128 B: one transpose tile per epilogue warp
@@ -757,7 +761,7 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                 else
                     asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cl) : "memory");
             } else {
-                mbar_expect_tx(bar, MA ? b_bytes : stage_bytes);
+                mbar_expect_tx(bar, MA ? b_bytes : tx_bytes);
             }
         };
         auto ld4 = [&](void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2, int c3) {
@@ -783,15 +787,16 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
             if (P.mode == MODE_CONV && P.halo) {
                 // k-step (kernel row dh, channel block cb): the (TW+2) x TH patch at
                 // (tw0 - 1, th0 - 1 + dh) and the row's three taps' weights
+                // (halo 2: the full (TW+2) x (TH+2) patch and all nine taps per channel block)
                 const int aw = T.tw0 + P.off_w[0], ah = T.th0 + P.off_h[0], n0 = static_cast<int>(T.n0) + boff;
+                const int ntap = P.halo == 2 ? 9 : 3;
                 int cb = 0, dh = 0;
                 for (int i = 0; i < T.nk; ++i) {
                     uint8_t* sa; uint64_t* bar;
                     acquire(sa, bar);
                     const int c0 = cb * BK;
                     ld4(sa, &map_a, bar, c0, aw, ah + dh, T.tn0);
-#pragma unroll
-                    for (int dw = 0; dw < 3; ++dw) {
+                    for (int dw = 0; dw < ntap; ++dw) {
                         uint8_t* sb = sa + a_bytes + dw * bt_bytes;
                         const int br = P.brow[dh * 3 + dw];
                         if (P.b_mn) {
@@ -901,7 +906,19 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                 if (MA) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // cp.async data -> async proxy
                 if (++slot == STAGES) { slot = 0; phase ^= 1u; }
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                if (leader && P.halo) {
+                if (leader && P.halo == 2) {
+                    const uint64_t so = static_cast<uint64_t>(s) * stage16;
+                    for (int j = 0; j < 9; ++j) {
+                        const uint64_t a_off = static_cast<uint64_t>((j / 3) * (HALO_TW + 2) + j % 3) * (128 >> 4);
+#pragma unroll
+                        for (int kk = 0; kk < BK / 8; ++kk) {
+                            const uint64_t ad = adesc0 + so + a_off + kk * a_kstep;
+                            const uint64_t bd = bdesc0 + so + j * (bt_bytes >> 4) + kk * b_kstep;
+                            mma_tf32(d, ad, bd, idesc, (i > 0 || j > 0 || kk > 0) ? 1u : 0u);
+                        }
+                    }
+                    mma_commit(&empty[s]);
+                } else if (leader && P.halo) {
                     const uint64_t so = static_cast<uint64_t>(s) * stage16;
 #pragma unroll
                     for (int dw = 0; dw < 3; ++dw)
@@ -1254,7 +1271,7 @@ thread_local int g_force_pair = 0;   // 1: run the call as CTA pairs (cta_group:
 thread_local int g_force_wide = 0;   // 1: full-width (32-column) epilogue staging even at 2 CTAs/SM
 thread_local int g_dil_w = 1;        // horizontal tap dilation for the next implicit GEMM (internal)
 thread_local int g_force_tb = 0;     // 1: forward convolution with transposed (K-major) weights
-thread_local int g_force_halo = 0;   // 1: 3x3 stride-1 forward convolution through halo patches
+thread_local int g_force_halo = 0;   // 1: 3x3 stride-1 conv through kernel-row halo patches; 2: full 3x3 patches
 
 int pick_bn(int64_t n) {
     static const int env_bn = getenv("NNCB_TC_BN") ? atoi(getenv("NNCB_TC_BN")) : 0;   // tuning knob
@@ -1486,7 +1503,8 @@ int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CU
     if (P.halo) {
         // stage = patch + three taps' B tiles: two CTAs per SM when two stages
         // fit, else one CTA with a deeper ring
-        const size_t sbh = HALO_A_BYTES + 3 * static_cast<size_t>(P.bn) * BK * 4;
+        const size_t sbh = P.halo == 2 ? HALO9_A_BYTES + 9 * static_cast<size_t>(P.bn) * BK * 4
+                                       : HALO_A_BYTES + 3 * static_cast<size_t>(P.bn) * BK * 4;
         int per = 0;
         for (int stg : {32, 16, 8}) {
             const size_t fixed = smem_for(P.bn, 0, stg);
@@ -1805,6 +1823,8 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
             const size_t nb = cands.size();
             for (size_t ci_ = 0; ci_ < nb; ++ci_)
                 if (!(cands[ci_] & 0x30000)) cands.push_back(cands[ci_] | 0x80000);   // 1-CTA tiles, default staging
+            // (bit 20, full 3x3 patches: correct but measured no faster than
+            // kernel-row patches at one CTA per SM; force_tile only)
         }
         cudaEvent_t e0, e1;
         NNCB_CUDA(cudaEventCreate(&e0));
@@ -1815,7 +1835,7 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
             g_force_pair = (c >> 16) & 1;
             g_force_wide = (c >> 17) & 1;
             g_force_tb = (c >> 18) & 1;
-            g_force_halo = (c >> 19) & 1;
+            g_force_halo = (c >> 20) & 1 ? 2 : (c >> 19) & 1;
             int rc = gemm_tc_route(ctx, d, a, b, bias, out, handled);   // warm-up (and validity)
             if (rc || !*handled) {
                 g_force_bn = 0;
@@ -1857,7 +1877,7 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
     g_force_pair = (choice >> 16) & 1;
     g_force_wide = (choice >> 17) & 1;
     g_force_tb = (choice >> 18) & 1;
-    g_force_halo = (choice >> 19) & 1;
+    g_force_halo = (choice >> 20) & 1 ? 2 : (choice >> 19) & 1;
     const int rc = gemm_tc_route(ctx, d, a, b, bias, out, handled);
     g_force_bn = 0;
     g_force_pair = 0;
@@ -2051,11 +2071,13 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
             Ck % 32 == 0 && g_dil_w == 1 && (fwd ? ow : iw) >= HALO_TW &&
             2 * (HALO_A_BYTES + 3 * static_cast<size_t>(P.bn) * BK * 4) + smem_for(P.bn, 0, 8) <= 227 * 1024) {
             // (a two-stage ring must fit: 256-wide tiles do not)
-            P.halo = 1;
+            const bool full = g_force_halo == 2 &&
+                              2 * (HALO9_A_BYTES + 9 * static_cast<size_t>(P.bn) * BK * 4) + smem_for(P.bn, 0, 8) <= 227 * 1024;
+            P.halo = full ? 2 : 1;
             P.TN = 1;
             P.TH = HALO_TH;
             P.TW = HALO_TW;
-            P.ntaps[0] = 3;   // k-steps per channel block: one per kernel row
+            P.ntaps[0] = full ? 1 : 3;   // k-steps per channel block: one per kernel row, or one
         }
         P.tiles_w = (P.gw + P.TW - 1) / P.TW;
         P.tiles_h = (P.gh + P.TH - 1) / P.TH;
@@ -2065,13 +2087,13 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
         // A: the activation (x for fwd, g for dgrad) as {C, W, H, N}
         const float* act = a;
         if (fwd && P.halo) {
-            if (!encode_4d(&ma, act, ci, iw, ih, n, 32, P.TW + 2, P.TH, 1, 1, 1, false, lda)) return 1;
+            if (!encode_4d(&ma, act, ci, iw, ih, n, 32, P.TW + 2, P.TH + (P.halo == 2 ? 2 : 0), 1, 1, 1, false, lda)) return 1;
         } else if (fwd) {
             if (!manual &&
                 !encode_4d(&ma, act, ci, iw, ih, n, 32, P.TW * (int)sw, P.TH * (int)sh, P.TN, (int)sw, (int)sh, false, lda))
                 return 1;
         } else if (P.halo) {
-            if (!encode_4d(&ma, act, co, ow, oh, n, 32, P.TW + 2, P.TH, 1, 1, 1, false)) return 1;
+            if (!encode_4d(&ma, act, co, ow, oh, n, 32, P.TW + 2, P.TH + (P.halo == 2 ? 2 : 0), 1, 1, 1, false)) return 1;
         } else {
             if (!encode_4d(&ma, act, co, ow, oh, n, 32, P.TW, P.TH, P.TN, 1, 1, false)) return 1;
         }
