@@ -98,6 +98,11 @@ struct TcParams {
     // (TW = 8, TH = 16, TN = 1: each 8-row core-matrix group is one image row,
     // group stride TW + 2 rows); a stage = patch + the three taps' B tiles
     int halo;
+    // halo with resident B (single N tile): every tap / channel-block B tile is
+    // loaded once per CTA into bres_bytes at the front of shared memory, and
+    // stages carry only patches
+    int bres;
+    uint32_t bres_bytes;
     double* colstats;   // fused BatchNorm statistics: [0,N) sum, [N,2N) sum of squares
     // --- manual A (channel counts that do not fill a 32-wide TMA block) -----
     // Builder warps gather A straight from the NHWC activation into the
@@ -620,12 +625,13 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
     const int STAGES = P.stages;
     nncb::pdl_trigger();   // follow-up folds / finalizes may be scheduled while this grid drains
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* bres_base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem = bres_base + P.bres_bytes;   // the ring and everything after it
     // 16 KB (halo 1: 20 KB kernel-row patch; halo 2: 23 KB full 3x3 patch)
     const uint32_t a_bytes = P.halo == 2 ? HALO9_A_BYTES : P.halo ? HALO_A_BYTES : BM * BK * 4;
     // PAIR: this CTA holds half of the B tile's columns (the MMA spans both CTAs)
     const uint32_t bt_bytes = static_cast<uint32_t>(PAIR ? P.bn / 2 : P.bn) * BK * 4;   // one tap's B tile
-    const uint32_t b_bytes = bt_bytes * (P.halo == 2 ? 9u : P.halo ? 3u : 1u);
+    const uint32_t b_bytes = P.bres ? 0u : bt_bytes * (P.halo == 2 ? 9u : P.halo ? 3u : 1u);
     // bytes the TMA loads of one stage deliver (the full patch is padded to 1 KB in smem)
     const uint32_t tx_bytes = (P.halo == 2 ? (HALO_TW + 2) * (HALO_TH + 2) * 128 : a_bytes) + b_bytes;
     const uint32_t rank = PAIR ? cluster_rank() : 0u;
@@ -638,8 +644,9 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
     uint64_t* tmem_empty = tmem_full + 2;                 // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
     uint64_t* side_bar = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(tmem_slot) + 16);   // [8][2]
+    uint64_t* bres_bar = side_bar + 16;                   // resident B loaded
     // CS: per-CTA column sum / sum of squares of the current column range
-    double* cs_acc = reinterpret_cast<double*>(side_bar + 16);
+    double* cs_acc = reinterpret_cast<double*>(side_bar + 18);
     // MA: gather tables after cs_acc (fwd: per K index; wgrad: per box pixel)
     int* ma_tab = reinterpret_cast<int*>(cs_acc + 2 * P.bn);
 
@@ -656,6 +663,7 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
         }
         if (EG)
             for (int w = 0; w < 16; ++w) mbar_init(&side_bar[w], 1);
+        if (P.bres) mbar_init(bres_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (MA) {
@@ -782,6 +790,22 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
             ++filled;
             if (++slot == STAGES) { slot = 0; phase ^= 1u; }
         };
+        if (P.bres && t_begin < P.tiles) {
+            // every (channel block, tap) B tile once, [cb][tap] order
+            mbar_expect_tx(bres_bar, P.bres_bytes);
+            for (int cb = 0; cb < P.cblocks; ++cb)
+                for (int j = 0; j < 9; ++j) {
+                    uint8_t* sb = bres_base + (cb * 9 + j) * bt_bytes;
+                    const int br = P.brow[j], c0 = cb * BK;
+                    if (P.b_mn) {
+                        for (int q = 0; q < bcols / 32; ++q) tma_load_2d(sb + q * 4096, &map_b, bres_bar, 32 * q, br + c0);
+                    } else if (P.bt) {
+                        tma_load_2d(sb, &map_b, bres_bar, br + c0, 0);
+                    } else {
+                        tma_load_2d(sb, &map_b, bres_bar, c0, br);
+                    }
+                }
+        }
         for (int64_t t = t_begin; t < P.tiles; t += t_step) {
             const Tile T = decode(t);
             if (P.mode == MODE_CONV && P.halo) {
@@ -796,7 +820,7 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                     acquire(sa, bar);
                     const int c0 = cb * BK;
                     ld4(sa, &map_a, bar, c0, aw, ah + dh, T.tn0);
-                    for (int dw = 0; dw < ntap; ++dw) {
+                    for (int dw = 0; dw < (P.bres ? 0 : ntap); ++dw) {
                         uint8_t* sb = sa + a_bytes + dw * bt_bytes;
                         const int br = P.brow[dh * 3 + dw];
                         if (P.b_mn) {
@@ -888,6 +912,9 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
         const uint64_t adesc0 = a_mn ? sdesc(s0, 4096, 512, 1) : sdesc(s0, 16, P.halo ? (HALO_TW + 2) * 128 : 1024, 2);
         const uint64_t bdesc0 = P.b_mn ? sdesc(s0 + a_bytes, 4096, 512, 1) : sdesc(s0 + a_bytes, 16, 1024, 2);
         const uint64_t a_kstep = a_mn ? (1024 >> 4) : (32 >> 4), b_kstep = P.b_mn ? (1024 >> 4) : (32 >> 4);
+        const uint32_t sres = smem_u32(bres_base);
+        const uint64_t bresdesc0 = P.b_mn ? sdesc(sres, 4096, 512, 1) : sdesc(sres, 16, 1024, 2);
+        if (P.bres && t_begin < P.tiles) mbar_wait(bres_bar, 0);   // resident B in place (once per CTA)
         const uint64_t stage16 = stage_bytes >> 4;
         const bool leader = elect_one();
         int slot = 0;
@@ -906,7 +933,21 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                 if (MA) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // cp.async data -> async proxy
                 if (++slot == STAGES) { slot = 0; phase ^= 1u; }
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                if (leader && P.halo == 2) {
+                if (leader && P.bres) {
+                    // B from the resident copy: tile (cb, dh * 3 + dw)
+                    const uint64_t so = static_cast<uint64_t>(s) * stage16;
+                    const int cb = i % P.cblocks, dh = i / P.cblocks;
+#pragma unroll
+                    for (int dw = 0; dw < 3; ++dw)
+#pragma unroll
+                        for (int kk = 0; kk < BK / 8; ++kk) {
+                            const uint64_t ad = adesc0 + so + dw * (128 >> 4) + kk * a_kstep;
+                            const uint64_t bd = bresdesc0 + static_cast<uint64_t>((cb * 9 + dh * 3 + dw) * bt_bytes >> 4) +
+                                                kk * b_kstep;
+                            mma_tf32(d, ad, bd, idesc, (i > 0 || dw > 0 || kk > 0) ? 1u : 0u);
+                        }
+                    mma_commit(&empty[s]);
+                } else if (leader && P.halo == 2) {
                     const uint64_t so = static_cast<uint64_t>(s) * stage16;
                     for (int j = 0; j < 9; ++j) {
                         const uint64_t a_off = static_cast<uint64_t>((j / 3) * (HALO_TW + 2) + j % 3) * (128 >> 4);
@@ -1271,6 +1312,7 @@ thread_local int g_force_pair = 0;   // 1: run the call as CTA pairs (cta_group:
 thread_local int g_force_wide = 0;   // 1: full-width (32-column) epilogue staging even at 2 CTAs/SM
 thread_local int g_dil_w = 1;        // horizontal tap dilation for the next implicit GEMM (internal)
 thread_local int g_force_tb = 0;     // 1: forward convolution with transposed (K-major) weights
+thread_local int g_force_bres = 0;   // 1: halo tiles with resident B (single N tile)
 thread_local int g_force_halo = 0;   // 1: 3x3 stride-1 conv through kernel-row halo patches; 2: full 3x3 patches
 
 int pick_bn(int64_t n) {
@@ -1503,10 +1545,22 @@ int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CU
     if (P.halo) {
         // stage = patch + three taps' B tiles: two CTAs per SM when two stages
         // fit, else one CTA with a deeper ring
-        const size_t sbh = P.halo == 2 ? HALO9_A_BYTES + 9 * static_cast<size_t>(P.bn) * BK * 4
-                                       : HALO_A_BYTES + 3 * static_cast<size_t>(P.bn) * BK * 4;
+        const size_t sbh = P.bres ? HALO_A_BYTES
+                           : P.halo == 2 ? HALO9_A_BYTES + 9 * static_cast<size_t>(P.bn) * BK * 4
+                                         : HALO_A_BYTES + 3 * static_cast<size_t>(P.bn) * BK * 4;
         int per = 0;
+        if (P.bres)   // one CTA per SM: resident B + the deepest patch ring that fits
+            for (int stg : {16, 8}) {
+                const size_t fixed = smem_for(P.bn, 0, stg) + P.bres_bytes;
+                if (fixed + 2 * sbh <= 227 * 1024) {
+                    P.stg_cols = stg;
+                    P.stages = static_cast<int>(std::min<size_t>(MAX_STAGES, (227 * 1024 - fixed) / sbh));
+                    per = 1;
+                    break;
+                }
+            }
         for (int stg : {32, 16, 8}) {
+            if (P.bres) break;
             const size_t fixed = smem_for(P.bn, 0, stg);
             if (fixed + 2 * sbh <= 113 * 1024 && P.bn <= 128) {
                 P.stg_cols = stg;
@@ -1515,7 +1569,7 @@ int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CU
                 break;
             }
         }
-        if (!per)
+        if (!per && !P.bres)
             for (int stg : {32, 16, 8}) {
                 const size_t fixed = smem_for(P.bn, 0, stg);
                 if (fixed + 2 * sbh <= 227 * 1024) {
@@ -1527,7 +1581,7 @@ int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CU
             }
         if (!per) return nncb::fail("gemm: halo tile does not fit shared memory");
         P.stg_bufs = 1;
-        const size_t smem = static_cast<size_t>(P.stages) * sbh + smem_for(P.bn, 0, P.stg_cols);
+        const size_t smem = static_cast<size_t>(P.stages) * sbh + smem_for(P.bn, 0, P.stg_cols) + P.bres_bytes;
         encode_tma_out(&mc, P);
         const unsigned grid = static_cast<unsigned>(std::min<int64_t>(P.tiles, static_cast<int64_t>(ctx->sm_count) * per));
         if (per == 2 && P.colstats)
@@ -1825,6 +1879,9 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
                 if (!(cands[ci_] & 0x30000)) cands.push_back(cands[ci_] | 0x80000);   // 1-CTA tiles, default staging
             // (bit 20, full 3x3 patches: correct but measured no faster than
             // kernel-row patches at one CTA per SM; force_tile only)
+            // (bit 21, resident B for 64-wide single-N-tile halo convs: correct,
+            // but 15-20% slower at one CTA per SM -- the kernel-row halo tile is
+            // no longer L2-bound at ~79% of the N = 64 MMA ceiling; force_tile only)
         }
         cudaEvent_t e0, e1;
         NNCB_CUDA(cudaEventCreate(&e0));
@@ -1836,6 +1893,7 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
             g_force_wide = (c >> 17) & 1;
             g_force_tb = (c >> 18) & 1;
             g_force_halo = (c >> 20) & 1 ? 2 : (c >> 19) & 1;
+            g_force_bres = (c >> 21) & 1;
             int rc = gemm_tc_route(ctx, d, a, b, bias, out, handled);   // warm-up (and validity)
             if (rc || !*handled) {
                 g_force_bn = 0;
@@ -1843,6 +1901,7 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
                 g_force_wide = 0;
                 g_force_tb = 0;
                 g_force_halo = 0;
+                g_force_bres = 0;
                 cudaEventDestroy(e0);
                 cudaEventDestroy(e1);
                 return rc;
@@ -1855,6 +1914,7 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
             g_force_wide = 0;
             g_force_tb = 0;
             g_force_halo = 0;
+            g_force_bres = 0;
             if (rc) {
                 cudaEventDestroy(e0);
                 cudaEventDestroy(e1);
@@ -1878,12 +1938,14 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
     g_force_wide = (choice >> 17) & 1;
     g_force_tb = (choice >> 18) & 1;
     g_force_halo = (choice >> 20) & 1 ? 2 : (choice >> 19) & 1;
+    g_force_bres = (choice >> 21) & 1;
     const int rc = gemm_tc_route(ctx, d, a, b, bias, out, handled);
     g_force_bn = 0;
     g_force_pair = 0;
     g_force_wide = 0;
     g_force_tb = 0;
     g_force_halo = 0;
+    g_force_bres = 0;
     return rc;
 }
 
@@ -2078,6 +2140,12 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
             P.TH = HALO_TH;
             P.TW = HALO_TW;
             P.ntaps[0] = full ? 1 : 3;   // k-steps per channel block: one per kernel row, or one
+            const size_t bres = 9 * static_cast<size_t>(P.cblocks) * P.bn * BK * 4;
+            if (g_force_bres && !full && Nc <= P.bn &&
+                bres + 2 * HALO_A_BYTES + smem_for(P.bn, 0, 8) <= 227 * 1024) {
+                P.bres = 1;
+                P.bres_bytes = static_cast<uint32_t>(bres);
+            }
         }
         P.tiles_w = (P.gw + P.TW - 1) / P.TW;
         P.tiles_h = (P.gh + P.TH - 1) / P.TH;

@@ -355,7 +355,7 @@ HALO_CONVS = [(2, 14, 14, 64, 64, 3, 1), (2, 56, 56, 64, 64, 3, 1), (1, 28, 28, 
 
 @pytest.mark.parametrize("shape", HALO_CONVS)
 @pytest.mark.parametrize("tile", [0x80000 | 64, 0x80000 | 128, 0x80000 | 0x40000 | 128, 0x80000 | 256, 0x180000 | 64,
-                                  0x180000 | 0x40000 | 64])
+                                  0x180000 | 0x40000 | 64, 0x280000 | 64, 0x280000 | 0x40000 | 64])
 def test_conv_fwd_halo(shape, tile):
     """3x3 stride-1 forward through halo patches (one (TW+2) x TH patch per
     channel block and kernel row, taps as shifted descriptors), with bias and
@@ -394,7 +394,7 @@ def test_conv_fwd_halo(shape, tile):
 
 
 @pytest.mark.parametrize("shape", HALO_CONVS[:4])
-@pytest.mark.parametrize("tile", [0x80000 | 64, 0x80000 | 128, 0x180000 | 64])
+@pytest.mark.parametrize("tile", [0x80000 | 64, 0x80000 | 128, 0x180000 | 64, 0x280000 | 64])
 def test_conv_dgrad_halo(shape, tile):
     """3x3 stride-1 input gradient through halo patches of dY against the
     exact dgrad."""

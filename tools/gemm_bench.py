@@ -47,8 +47,9 @@ def main():
     timer = P.DeviceTimer()
     if a.tile != "auto":
         t = a.tile
-        code = (int(t.lstrip("pwthf")) | (0x10000 if "p" in t else 0) | (0x20000 if "w" in t else 0) |
-                (0x40000 if "t" in t else 0) | (0x80000 if "h" in t else 0) | (0x100000 if "f" in t else 0))
+        code = (int(t.lstrip("pwthfr")) | (0x10000 if "p" in t else 0) | (0x20000 if "w" in t else 0) |
+                (0x40000 if "t" in t else 0) | (0x80000 if "h" in t else 0) | (0x100000 if "f" in t else 0) |
+                (0x200000 if "r" in t else 0))
         K.nncb_gemm_force_tile(code)
     total = {}
     for name, h, ci, co, k, s in LAYERS:
