@@ -103,6 +103,7 @@ struct TcParams {
     // stages carry only patches
     int bres;
     uint32_t bres_bytes;
+    int halo_kw;        // halo 1: taps per kernel row (3; 2 for the space-to-depth stem, spaced dil_w rows)
     double* colstats;   // fused BatchNorm statistics: [0,N) sum, [N,2N) sum of squares
     // --- manual A (channel counts that do not fill a 32-wide TMA block) -----
     // Builder warps gather A straight from the NHWC activation into the
@@ -631,7 +632,7 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
     const uint32_t a_bytes = P.halo == 2 ? HALO9_A_BYTES : P.halo ? HALO_A_BYTES : BM * BK * 4;
     // PAIR: this CTA holds half of the B tile's columns (the MMA spans both CTAs)
     const uint32_t bt_bytes = static_cast<uint32_t>(PAIR ? P.bn / 2 : P.bn) * BK * 4;   // one tap's B tile
-    const uint32_t b_bytes = P.bres ? 0u : bt_bytes * (P.halo == 2 ? 9u : P.halo ? 3u : 1u);
+    const uint32_t b_bytes = P.bres ? 0u : bt_bytes * (P.halo == 2 ? 9u : P.halo ? static_cast<uint32_t>(P.halo_kw) : 1u);
     // bytes the TMA loads of one stage deliver (the full patch is padded to 1 KB in smem)
     const uint32_t tx_bytes = (P.halo == 2 ? (HALO_TW + 2) * (HALO_TH + 2) * 128 : a_bytes) + b_bytes;
     const uint32_t rank = PAIR ? cluster_rank() : 0u;
@@ -813,7 +814,7 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                 // (tw0 - 1, th0 - 1 + dh) and the row's three taps' weights
                 // (halo 2: the full (TW+2) x (TH+2) patch and all nine taps per channel block)
                 const int aw = T.tw0 + P.off_w[0], ah = T.th0 + P.off_h[0], n0 = static_cast<int>(T.n0) + boff;
-                const int ntap = P.halo == 2 ? 9 : 3;
+                const int ntap = P.halo == 2 ? 9 : P.halo_kw;
                 int cb = 0, dh = 0;
                 for (int i = 0; i < T.nk; ++i) {
                     uint8_t* sa; uint64_t* bar;
@@ -822,7 +823,7 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                     ld4(sa, &map_a, bar, c0, aw, ah + dh, T.tn0);
                     for (int dw = 0; dw < (P.bres ? 0 : ntap); ++dw) {
                         uint8_t* sb = sa + a_bytes + dw * bt_bytes;
-                        const int br = P.brow[dh * 3 + dw];
+                        const int br = P.brow[P.halo == 2 ? dw : dh * P.halo_kw + dw];
                         if (P.b_mn) {
                             for (int q = 0; q < bcols / 32; ++q) ld2(sb + q * 4096, &map_b, bar, n0 + 32 * q, br + c0);
                         } else if (P.bt) {
@@ -962,13 +963,15 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                 } else if (leader && P.halo) {
                     const uint64_t so = static_cast<uint64_t>(s) * stage16;
 #pragma unroll
-                    for (int dw = 0; dw < 3; ++dw)
+                    for (int dw = 0; dw < 3; ++dw) {
+                        if (dw >= P.halo_kw) break;
 #pragma unroll
                         for (int kk = 0; kk < BK / 8; ++kk) {
-                            const uint64_t ad = adesc0 + so + dw * (128 >> 4) + kk * a_kstep;
+                            const uint64_t ad = adesc0 + so + dw * P.dil_w * (128 >> 4) + kk * a_kstep;
                             const uint64_t bd = bdesc0 + so + dw * (bt_bytes >> 4) + kk * b_kstep;
                             mma_tf32(d, ad, bd, idesc, (i > 0 || dw > 0 || kk > 0) ? 1u : 0u);
                         }
+                    }
                     mma_commit(&empty[s]);
                 } else if (leader) {
                     const uint64_t so = static_cast<uint64_t>(s) * stage16;
@@ -1547,7 +1550,7 @@ int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CU
         // fit, else one CTA with a deeper ring
         const size_t sbh = P.bres ? HALO_A_BYTES
                            : P.halo == 2 ? HALO9_A_BYTES + 9 * static_cast<size_t>(P.bn) * BK * 4
-                                         : HALO_A_BYTES + 3 * static_cast<size_t>(P.bn) * BK * 4;
+                                         : HALO_A_BYTES + P.halo_kw * static_cast<size_t>(P.bn) * BK * 4;
         int per = 0;
         if (P.bres)   // one CTA per SM: resident B + the deepest patch ring that fits
             for (int stg : {16, 8}) {
@@ -1870,10 +1873,13 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
         }
         static const bool halo_on = !(getenv("NNCB_TC_HALO") && atoi(getenv("NNCB_TC_HALO")) == 0);
         const bool halo_fwd = d->kind == NNCB_CONV_FWD && d->ci % 32 == 0 && d->ow >= HALO_TW;
+        // the space-to-depth stem (packed: its lowered conv has 2 taps per row spaced 2)
+        const bool halo_stem = d->kind == NNCB_CONV_FWD && d->ci % 32 != 0 && d->sh == 2 && d->sw == 2 &&
+                               4 * d->ci <= 16 && d->kw == 7 && d->kh == 7 && d->ow >= HALO_TW;
         const bool halo_dgrad = d->kind == NNCB_CONV_DGRAD && d->co % 32 == 0 && d->iw >= HALO_TW;
-        if (halo_on && (halo_fwd || halo_dgrad) && !(d->epilogue & NNCB_EPI_RELU_GRAD) && d->kh == 3 && d->kw == 3 &&
-            d->sh == 1 && d->sw == 1 &&
-            d->pad_top == 1 && d->pad_left == 1) {   // bit 19: halo patches
+        if (halo_on && !(d->epilogue & NNCB_EPI_RELU_GRAD) &&
+            (halo_stem || ((halo_fwd || halo_dgrad) && d->kh == 3 && d->kw == 3 && d->sh == 1 && d->sw == 1 &&
+                           d->pad_top == 1 && d->pad_left == 1))) {   // bit 19: halo patches
             const size_t nb = cands.size();
             for (size_t ci_ = 0; ci_ < nb; ++ci_)
                 if (!(cands[ci_] & 0x30000)) cands.push_back(cands[ci_] | 0x80000);   // 1-CTA tiles, default staging
@@ -2128,20 +2134,23 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
         pick_box(BM, P.gn, P.gh, P.gw, P.TN, P.TH, P.TW);
         // halo: forward, or a stride-1 dgrad (its tap table visits kernel rows
         // with off_w = -1, 0, 1 in order, like the forward)
-        if (g_force_halo && !manual && !P.pair && !(d->epilogue & NNCB_EPI_RELU_GRAD) && kh == 3 && kw == 3 && sh == 1 &&
-            sw == 1 && pt == 1 && pl == 1 &&
-            Ck % 32 == 0 && g_dil_w == 1 && (fwd ? ow : iw) >= HALO_TW &&
-            2 * (HALO_A_BYTES + 3 * static_cast<size_t>(P.bn) * BK * 4) + smem_for(P.bn, 0, 8) <= 227 * 1024) {
+        // (or the space-to-depth stem: 2 taps per row spaced 2, any padding)
+        const bool halo33 = kh == 3 && kw == 3 && pt == 1 && pl == 1 && g_dil_w == 1;
+        const bool halo_s2d = fwd && kw == 2 && g_dil_w == 2 && kh <= 4;
+        if (g_force_halo && !manual && !P.pair && !(d->epilogue & NNCB_EPI_RELU_GRAD) && (halo33 || halo_s2d) &&
+            sh == 1 && sw == 1 && Ck % 32 == 0 && (fwd ? ow : iw) >= HALO_TW &&
+            2 * (HALO_A_BYTES + kw * static_cast<size_t>(P.bn) * BK * 4) + smem_for(P.bn, 0, 8) <= 227 * 1024) {
             // (a two-stage ring must fit: 256-wide tiles do not)
-            const bool full = g_force_halo == 2 &&
+            const bool full = halo33 && g_force_halo == 2 &&
                               2 * (HALO9_A_BYTES + 9 * static_cast<size_t>(P.bn) * BK * 4) + smem_for(P.bn, 0, 8) <= 227 * 1024;
             P.halo = full ? 2 : 1;
             P.TN = 1;
             P.TH = HALO_TH;
             P.TW = HALO_TW;
-            P.ntaps[0] = full ? 1 : 3;   // k-steps per channel block: one per kernel row, or one
+            P.halo_kw = static_cast<int>(kw);
+            P.ntaps[0] = full ? 1 : static_cast<int>(kh);   // k-steps per channel block: one per kernel row, or one
             const size_t bres = 9 * static_cast<size_t>(P.cblocks) * P.bn * BK * 4;
-            if (g_force_bres && !full && Nc <= P.bn &&
+            if (g_force_bres && halo33 && !full && Nc <= P.bn &&
                 bres + 2 * HALO_A_BYTES + smem_for(P.bn, 0, 8) <= 227 * 1024) {
                 P.bres = 1;
                 P.bres_bytes = static_cast<uint32_t>(bres);

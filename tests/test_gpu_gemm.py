@@ -419,3 +419,28 @@ def test_dgrad_halo_relu_grad_epilogue():
     """A forced halo tile with the relu-grad epilogue falls back to the regular
     tile (halo launches have no side-tile build) and stays correct."""
     test_dgrad_relu_grad_epilogue((2, 14, 14, 64, 64, 3, 1), 0x80000 | 64, True)
+
+
+@pytest.mark.parametrize("shape", [(2, 32, 32, 3, 64, 7, 2), (2, 17, 23, 3, 32, 7, 2), (4, 64, 64, 3, 64, 7, 2)])
+@pytest.mark.parametrize("tile", [0x80000 | 64, 0x80000 | 0x40000 | 64])
+def test_stem_space_to_depth_halo(shape, tile):
+    """The space-to-depth stem's lowered conv (4 kernel rows x 2 taps spaced 2)
+    through halo patches, against the exact path."""
+    n, ih, iw, ci, co, k, s = shape
+    g = conv_geom(n, ih, iw, ci, co, k, s)
+    if g["ow"] < 8:
+        pytest.skip("output narrower than a halo tile")
+    rng = np.random.default_rng(23)
+    x = rng.uniform(-1, 1, (n, ih, iw, ci)).astype(np.float32)
+    w = rng.uniform(-1, 1, (k, k, ci, co)).astype(np.float32)
+    xd, wd = Dev(x), Dev(w)
+    oshape = (n, g["oh"], g["ow"], co)
+    ex, out = Dev(nbytes=int(np.prod(oshape)) * 4), Dev(nbytes=int(np.prod(oshape)) * 4)
+    gemm(GemmDesc(kind=CONV_FWD, precision=1, epilogue=0, **g), xd, wd, None, ex)
+    K.nncb_gemm_force_tile(tile)
+    try:
+        gemm(GemmDesc(kind=CONV_FWD, precision=0, epilogue=0, **g), xd, wd, None, out)
+        assert K.nncb_gemm_last_path() == 1
+    finally:
+        K.nncb_gemm_force_tile(0)
+    check(out.get(oshape), ex.get(oshape).astype(np.float64))
