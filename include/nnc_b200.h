@@ -72,6 +72,13 @@ int nnc_model_train_step_staged(nnc_model* m, double lr);
 int nnc_model_staged_loss(nnc_model* m, double* loss);
 int nnc_model_gradients(nnc_model* m, const float* target, int64_t n, double* loss);
 int nnc_model_grad(nnc_model* m, const char* weight, float* out, int64_t n);
+/* Parity debugging: with keep_values on, the training step binds every value
+ * to its own device bytes (no arena reuse), so after gradients() any forward
+ * or backward value can be read back by name (nnc_model_trainer_value; out
+ * NULL returns only dims/rank). Not for production: the arena grows to the
+ * sum of all values. Values living in fused-group registers have no bytes.  */
+int nnc_model_debug_keep_values(nnc_model* m, int on);
+int nnc_model_trainer_value(nnc_model* m, const char* name, float* out, int64_t n, int64_t* dims, int* rank);
 
 /* Data-parallel layout (runtime::dp_layout) as JSON: region order, ~bucket_bytes
  * all-reduce buckets and the backward launch after which each can start.

@@ -62,12 +62,21 @@ int nncb_event_destroy(void* ev);
  * pageable source is first copied into the pinned ring by the copy threads),
  * so `src` may be reused on return; the device bytes are valid after the
  * copy stream reaches that point (nncb_event_record_on / nncb_stream_wait). */
-enum nncb_stream_id { NNCB_STREAM_COMPUTE = 0, NNCB_STREAM_COPY = 1 };
+enum nncb_stream_id { NNCB_STREAM_COMPUTE = 0, NNCB_STREAM_COPY = 1, NNCB_STREAM_COMM = 2 };
 int nncb_h2d_async(nncb_ctx* ctx, void* dst, const void* src, size_t bytes);
 int nncb_d2h_async(nncb_ctx* ctx, void* dst_pinned, const void* src, size_t bytes);   /* compute stream */
 int nncb_event_record_on(nncb_ctx* ctx, int stream, void* ev);
 int nncb_stream_wait(nncb_ctx* ctx, int stream, void* ev);
 int nncb_event_sync(void* ev);
+/* Fork/join between the compute stream and another context stream (pooled
+ * events, safe inside a capture): nncb_fork makes `to_stream` wait for the
+ * compute stream's current position; nncb_join makes the compute stream wait
+ * for everything issued on `from_stream` so far.                            */
+int nncb_fork(nncb_ctx* ctx, int to_stream);
+int nncb_join(nncb_ctx* ctx, int from_stream);
+/* Stream-ordered write of one double (e.g. the learning rate a captured step
+ * graph reads; not for use during a capture).                              */
+int nncb_set_f64(nncb_ctx* ctx, double* dst_dev, double value);
 
 /* Number of nncb kernel launches issued on this context (all families). */
 uint64_t nncb_launch_count(nncb_ctx* ctx);
@@ -282,6 +291,11 @@ int nncb_l1_loss(nncb_ctx* ctx, const float* pred, const float* target, float* g
  * one layout): w = (float)((double)w - lr*((double)g*grad_scale)). With
  * grad_scale = 1 this is bit-identical to runtime::sgd_step (runtime.cpp:493). */
 int nncb_sgd(nncb_ctx* ctx, float* w, const float* g, int64_t n, double lr, double grad_scale);
+/* The same update with the learning rate read from device memory (*lr_dev),
+ * launched on context stream `stream` (a bucket's update on the comm stream
+ * right after its all-reduce, overlapping the rest of the backward pass).  */
+int nncb_sgd_dev(nncb_ctx* ctx, int stream, float* w, const float* g, int64_t n, const double* lr_dev,
+                 double grad_scale);
 
 /* ------------------------------------------------------------------ */
 /*  Data-parallel collectives (NCCL over NVLink/NVSwitch)               */
@@ -298,6 +312,10 @@ int nncb_allreduce_sum(nncb_ctx* ctx, float* buf, int64_t count);
  * issued so far (before the buffers are read, e.g. by SGD).                 */
 int nncb_allreduce_sum_async(nncb_ctx* ctx, float* buf, int64_t count);
 int nncb_comm_join(nncb_ctx* ctx);
+/* The all-reduce alone, on the comm stream (the caller forks/joins).       */
+int nncb_allreduce_sum_on_comm(nncb_ctx* ctx, float* buf, int64_t count);
+/* 1 if a communicator is initialised on this context.                      */
+int nncb_comm_active(nncb_ctx* ctx);
 
 #ifdef __cplusplus
 }

@@ -26,6 +26,9 @@ def available() -> bool:
 def lib():
     global _lib
     if _lib is None:
+        # the C++ runtime must be global before an RTLD_LOCAL C++ library is
+        # mapped into this (C) process, or libnncref's first std:: call faults
+        ctypes.CDLL("libstdc++.so.6", mode=ctypes.RTLD_GLOBAL)
         l = ctypes.CDLL(LIB, mode=ctypes.RTLD_LOCAL)
         P, I, I64, D, S = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_char_p
         DP, I64P = ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)

@@ -4,7 +4,9 @@ Python mirror of the reference's C++ pipeline (nnc::ingest / passes / autodiff /
 plan / runtime), bound through the C-ABI in include/nnc_b200.h. The compute path
 is libnnc_b200.so (C++ host: partitioning, buffer planning, launch scheduling)
 over libnncb.so (hand-written sm_100a kernels, include/nncb.h). There is no CPU
-fallback: if the native libraries are missing, importing this package raises.
+fallback: the native libraries are loaded on first use (so importing the
+package's pure-Python helpers, e.g. `workloads`, maps no native code), and
+that first use raises if they are missing.
 
 Reference call chain being replaced (file:line in /root/reference/proj):
     ingest::parse_model        core/src/ingest.cpp:411-500
@@ -74,6 +76,8 @@ def _load():
         "nnc_model_staged_loss": (I, [P, DP]),
         "nnc_model_gradients": (I, [P, FP, I64, DP]),
         "nnc_model_grad": (I, [P, S, FP, I64]),
+        "nnc_model_debug_keep_values": (I, [P, I]),
+        "nnc_model_trainer_value": (I, [P, S, FP, I64, I64P, ctypes.POINTER(ctypes.c_int)]),
         "nnc_model_trainer_prepare": (I, [P, FP, I64]),
         "nnc_model_trainer_step_device": (I, [P, D]),
         "nnc_model_trainer_loss": (I, [P, DP]),
@@ -116,7 +120,32 @@ def _load():
     return host, kern
 
 
-_host, _kern = _load()
+_libs = None
+
+
+def _lib_pair():
+    global _libs
+    if _libs is None:
+        _libs = _load()
+    return _libs
+
+
+class _LazyLib:
+    """Attribute access loads libnncb.so / libnnc_b200.so on first use."""
+
+    def __init__(self, index: int):
+        self._index = index
+
+    def __getattr__(self, name):
+        return getattr(_lib_pair()[self._index], name)
+
+
+_host, _kern = _LazyLib(0), _LazyLib(1)
+
+
+def load_native():
+    """Load the native libraries now (raises ImportError if they are not built)."""
+    _lib_pair()
 
 
 def _check(status: int):
@@ -304,6 +333,22 @@ class CompiledModel:
             grads[w] = g
         return loss.value, grads
 
+    # -- parity debugging ---------------------------------------------------
+    def debug_keep_values(self, on: bool = True):
+        """Bind the training step without arena reuse so every value survives
+        the step (then read them with step_value)."""
+        _check(_host.nnc_model_debug_keep_values(self._h, 1 if on else 0))
+
+    def step_value(self, name: str) -> np.ndarray:
+        """Device contents of a value of the last training step (forward or
+        backward); raises NNCError for values held in fused-group registers."""
+        dims = (ctypes.c_int64 * 8)()
+        rank = ctypes.c_int()
+        _check(_host.nnc_model_trainer_value(self._h, name.encode(), None, 0, dims, ctypes.byref(rank)))
+        out = np.empty(tuple(dims[: rank.value]), dtype=np.float32)
+        _check(_host.nnc_model_trainer_value(self._h, name.encode(), _fptr(out), out.size, dims, ctypes.byref(rank)))
+        return out
+
     # -- device-resident stepping (benchmarks) ------------------------------
     def trainer_prepare(self, inputs: Dict[str, np.ndarray], target: np.ndarray):
         keep = self._borrow(inputs)   # noqa: F841
@@ -416,5 +461,5 @@ def init_comm(nranks: int, rank: int, uid: bytes):
     _check(_host.nnc_init_comm(nranks, rank, uid))
 
 
-__all__ = ["CompiledModel", "DeviceTimer", "NNCError", "group_document", "comm_unique_id",
+__all__ = ["load_native", "CompiledModel", "DeviceTimer", "NNCError", "group_document", "comm_unique_id",
            "init_comm", "PREC_TF32", "PREC_FP32", "HOST_LIB", "KERNEL_LIB"]

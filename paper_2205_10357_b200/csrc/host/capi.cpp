@@ -328,6 +328,28 @@ int nnc_model_gradients(nnc_model* m, const float* target, int64_t n, double* lo
     return rc;
 }
 
+int nnc_model_debug_keep_values(nnc_model* m, int on) {
+    return guarded([&] {
+        runtime::release(m->plans);   // the next training call binds afresh
+        m->trainer = nullptr;
+        m->opts.keep_values = on != 0;
+    });
+}
+
+int nnc_model_trainer_value(nnc_model* m, const char* name, float* out, int64_t n, int64_t* dims, int* rank) {
+    return guarded([&] {
+        runtime::Trainer& t = runtime::shared_trainer(m->plans, *m->host, runtime::default_device(), m->opts);
+        Tensor v = t.value(name);
+        if (rank) {
+            *rank = static_cast<int>(v.dims().size());
+            for (size_t i = 0; i < v.dims().size() && i < 8; ++i) dims[i] = v.dims()[i];
+        }
+        if (!out) return;
+        if (v.elements() != n) throw Error(Error::Code::ShapeMismatch, std::string("value size mismatch: ") + name);
+        std::memcpy(out, v.data(), v.byte_size());
+    });
+}
+
 int nnc_model_grad(nnc_model* m, const char* weight, float* out, int64_t n) {
     return guarded([&] {
         auto it = m->grads.find(weight);

@@ -177,11 +177,27 @@ void launch_cost(const BoundLaunch& b, const Launch& L, const ExecutionPlan& p, 
     auto elems = [&](size_t arg) { return static_cast<double>(element_count(p.values[L.args[arg].slot].dims)); };
     switch (b.kind) {
         case LaunchKind::Ew: {
-            double n = static_cast<double>(b.n);
-            for (const auto& in : b.ew_prog.empty() ? L.ew : b.ew_prog)
+            // element loads / stores move n floats; per-channel operands C
+            // floats; a folded BatchNorm backward reduction writes 2C floats
+            const double n = static_cast<double>(b.n);
+            const double c = static_cast<double>(std::max<int64_t>(b.c, 1));
+            for (const auto& in : b.ew_prog.empty() ? L.ew : b.ew_prog) {
                 if (in.op == NNCB_EW_LOAD || in.op == NNCB_EW_STORE) bytes += 4.0 * n;
+                if (in.op == NNCB_EW_LOAD_CH) bytes += 4.0 * c;
+                if (in.op == NNCB_EW_REDUCE_BN_GRAD) bytes += 8.0 * c;
+            }
             break;
         }
+        case LaunchKind::BnStats:
+            if (b.bn_finalize) {   // reads the GEMM epilogue's 2C double sums, writes 2C floats
+                bytes = 16.0 * b.d1 + 8.0 * b.d1;
+                break;
+            }
+            bytes = 4.0 * elems(0) + 8.0 * b.d1;
+            break;
+        case LaunchKind::BnGradReduce:   // reads x, g (rows*C) and the 2C stats; writes 2C sums
+            bytes = 8.0 * elems(0) + 16.0 * b.d1;
+            break;
         case LaunchKind::Gemm: {
             const nncb_gemm_desc& d = b.gemm;
             double M, N, K;
@@ -303,6 +319,8 @@ struct Program {
 
     /// `param_ptr(name)` supplies Parameter buffers; `fixed(name)` may pin other
     /// values (flat gradient region) -- return nullptr to arena-allocate.
+    bool keep_values = false;   // no arena reuse (parity debugging)
+
     void bind(const std::function<void*(const std::string&)>& param_ptr,
               const std::function<void*(const std::string&)>& fixed) {
         OffsetPlanner pl;
@@ -341,7 +359,7 @@ struct Program {
                     pl.note();
                 } else {
                     auto it = offset.find(v.name);
-                    if (it != offset.end() && live[v.name]) {
+                    if (it != offset.end() && live[v.name] && !keep_values) {
                         pl.release(it->second);
                         live[v.name] = false;
                     }
@@ -395,6 +413,66 @@ struct Program {
                 else if (b.gemm.kind == NNCB_CONV_WGRAD && fwd_inputs.count(an))
                     b.gemm.epilogue |= NNCB_EPI_A_UNCHANGED;
             }
+    }
+
+    /// Device byte ranges a bound launch reads or writes. Arena offsets are
+    /// shared between values with disjoint lifetimes, so producer/consumer
+    /// matching must go by byte overlap, never by pointer identity alone.
+    struct Range {
+        const char* p;
+        int64_t n;
+        bool overlaps(const char* q, int64_t m) const { return p < q + m && q < p + n; }
+    };
+    std::vector<Range> launch_ranges(size_t pi, size_t k, bool outputs) const {
+        std::vector<Range> r;
+        const BoundLaunch& b = steps[pi][k];
+        if (b.skip) return r;   // its work (if any) runs inside the absorbing launch
+        const Launch& L = *sources[pi][k];
+        const ExecutionPlan& p = *plans[pi];
+        for (size_t a = 0; a < L.args.size() && a < b.ptrs.size(); ++a) {
+            const bool out = a < L.is_out.size() && L.is_out[a];
+            if (out != outputs) continue;
+            const int64_t bytes = (element_count(p.values[L.args[a].slot].dims) - L.args[a].offset) *
+                                  static_cast<int64_t>(dtype_size(p.dtype));
+            r.push_back({static_cast<const char*>(b.ptrs[a]), std::max<int64_t>(bytes, 1)});
+        }
+        // operands bound beyond the plan arguments
+        const int64_t cb = std::max<int64_t>(b.c, 1) * static_cast<int64_t>(sizeof(float));
+        // folded BatchNorm reductions append x, mean, invstd (read), sum_g, sum_gx (written)
+        for (size_t s0 = L.args.size(); b.kind == LaunchKind::Ew && s0 + 5 <= b.ptrs.size(); s0 += 5) {
+            if (outputs) {
+                r.push_back({static_cast<const char*>(b.ptrs[s0 + 3]), cb});
+                r.push_back({static_cast<const char*>(b.ptrs[s0 + 4]), cb});
+            } else {
+                r.push_back({static_cast<const char*>(b.ptrs[s0]), b.n * static_cast<int64_t>(sizeof(float))});
+                r.push_back({static_cast<const char*>(b.ptrs[s0 + 1]), 2 * cb});
+            }
+        }
+        if (b.kind == LaunchKind::Gemm && b.eg_sg) {
+            const int64_t C = (b.gemm.kind == NNCB_DENSE_DGRAD ? b.gemm.in_f : b.gemm.ci) * 4;
+            if (outputs) {
+                r.push_back({reinterpret_cast<const char*>(b.eg_sg), C});
+                r.push_back({reinterpret_cast<const char*>(b.eg_sgx), C});
+            }
+        }
+        return r;
+    }
+    bool launch_touches(size_t pi, size_t k, const char* q, int64_t m, bool outputs) const {
+        for (const Range& r : launch_ranges(pi, k, outputs))
+            if (r.overlaps(q, m)) return true;
+        return false;
+    }
+    int64_t arg_bytes(size_t pi, size_t k, size_t a) const {
+        const Launch& L = *sources[pi][k];
+        const ExecutionPlan& p = *plans[pi];
+        return (element_count(p.values[L.args[a].slot].dims) - L.args[a].offset) *
+               static_cast<int64_t>(dtype_size(p.dtype));
+    }
+    /// The nearest launch before `j` that writes any byte of [q, q+m), or -1.
+    int64_t last_writer(size_t pi, size_t j, const char* q, int64_t m) const {
+        for (size_t i = j; i-- > 0;)
+            if (launch_touches(pi, i, q, m, true)) return static_cast<int64_t>(i);
+        return -1;
     }
 
     /// The BatchNorm backward reduction (sum g, sum g*xhat per channel) of a
@@ -590,16 +668,42 @@ struct Program {
             for (size_t j = 1; j < steps[pi].size(); ++j) {
                 BoundLaunch& r = steps[pi][j];
                 if (r.kind != LaunchKind::BnGradReduce || r.skip) continue;
-                // the group that stores g: g, x and the statistics are all live
-                // until this reduction, so nothing in between overwrites them
-                size_t pj = j;
-                for (size_t i = j; i-- > 0 && pj == j;) {
-                    const BoundLaunch& c = steps[pi][i];
-                    if (c.kind != LaunchKind::Ew || c.skip) continue;
-                    for (const auto& in : c.ew_prog.empty() ? sources[pi][i]->ew : c.ew_prog)
-                        if (in.op == NNCB_EW_STORE && c.ptrs[in.slot] == r.ptrs[2]) pj = i;
+                // the launch that last wrote g's bytes must be a fused group
+                // storing exactly g (arena bytes are shared between values with
+                // disjoint lifetimes: an older launch that stored a dead value
+                // at the same address is not the producer)
+                const char* gp = static_cast<const char*>(r.ptrs[2]);
+                const int64_t gbytes = arg_bytes(pi, j, 2);
+                const int64_t w = last_writer(pi, j, gp, gbytes);
+                if (w < 0) continue;
+                const size_t pj = static_cast<size_t>(w);
+                if (steps[pi][pj].kind != LaunchKind::Ew) continue;
+                {
+                    bool stores_g = false;
+                    const BoundLaunch& c = steps[pi][pj];
+                    for (const auto& in : c.ew_prog.empty() ? sources[pi][pj]->ew : c.ew_prog)
+                        stores_g = stores_g || (in.op == NNCB_EW_STORE && c.ptrs[in.slot] == r.ptrs[2]);
+                    if (!stores_g) continue;
                 }
-                if (pj == j) continue;
+                // the reduction moves from j up to pj: x and the statistics must
+                // hold their final bytes there already (no writer in [pj, j)),
+                // and the sums it writes early must not be read or written by
+                // any launch in between (their bytes may belong to a value that
+                // is live there)
+                {
+                    const int64_t C0 = r.d1;
+                    const Range xr{static_cast<const char*>(r.ptrs[0]), arg_bytes(pi, j, 0)};
+                    const Range sr{static_cast<const char*>(r.ptrs[1]), 2 * C0 * 4};
+                    const Range o0{static_cast<const char*>(r.ptrs[3]), C0 * 4}, o1{static_cast<const char*>(r.ptrs[4]), C0 * 4};
+                    bool clash = false;
+                    for (size_t k = pj; k < j && !clash; ++k) {
+                        clash = launch_touches(pi, k, xr.p, xr.n, true) || launch_touches(pi, k, sr.p, sr.n, true);
+                        if (k > pj)
+                            for (const Range& q : {o0, o1})
+                                clash = clash || launch_touches(pi, k, q.p, q.n, true) || launch_touches(pi, k, q.p, q.n, false);
+                    }
+                    if (clash) continue;
+                }
                 BoundLaunch& e = steps[pi][pj];
                 const int64_t rows = r.d0, C = r.d1;
                 if (C < 4 || C > 2048 || (C & (C - 1)) || (rows * C) % 4 || e.n != rows * C) continue;
@@ -668,9 +772,15 @@ struct Program {
             for (size_t j = 0; j < plan_steps.size(); ++j) {
                 BoundLaunch& bn = plan_steps[j];
                 if (bn.kind != LaunchKind::BnStats) continue;
-                for (size_t i = j; i-- > 0;) {
-                    BoundLaunch& g = plan_steps[i];
-                    if (g.kind != LaunchKind::Gemm || g.ptrs.back() != bn.ptrs[0]) continue;
+                // the launch that last wrote the BatchNorm input's bytes; fuse
+                // only if it is a forward GEMM whose output is exactly that
+                // input (an older GEMM that wrote a dead value at a reused
+                // arena address must never be matched)
+                const size_t pi = static_cast<size_t>(&plan_steps - steps.data());
+                const int64_t w = last_writer(pi, j, static_cast<const char*>(bn.ptrs[0]), arg_bytes(pi, j, 0));
+                for (int64_t once = w; once >= 0; once = -1) {   // `break` = do not fuse
+                    BoundLaunch& g = plan_steps[static_cast<size_t>(once)];
+                    if (g.kind != LaunchKind::Gemm || g.ptrs.back() != bn.ptrs[0]) break;
                     if (g.gemm.kind != NNCB_CONV_FWD && g.gemm.kind != NNCB_DENSE_FWD) break;
                     // measured per ResNet-50 shape (tools/gemm_bench.py --colstats vs
                     // tools/stats_bench.py): the epilogue statistics cost less than a
@@ -1298,9 +1408,10 @@ struct Trainer::Impl {
     std::map<std::string, int64_t> w_off, w_elems;    // element offsets in the flat regions
     int64_t region_elems = 0;
     void *params = nullptr, *grads = nullptr, *target = nullptr, *loss = nullptr;
+    double* lr_dev = nullptr;                 // the learning rate the update kernels read
+    double lr_written = std::nan("");
     void* graph = nullptr;
     void* graph_nosgd = nullptr;
-    double graph_lr = std::nan("");
     DpLayout layout;                                      // region order and all-reduce buckets
     uint64_t launches_per_step = 0;
     bool warmed = false;
@@ -1334,41 +1445,54 @@ struct Trainer::Impl {
         }
         if (loss_ev) nncb_event_destroy(loss_ev);
         if (loss_host) nncb_host_free(loss_host);
-        for (void* p : {params, grads, target, loss})
+        for (void* p : {params, grads, target, loss, static_cast<void*>(lr_dev)})
             if (p) nncb_free(ctx, p);
     }
 
-    void enqueue_step(double lr, bool do_sgd) {
+    /// One training step on the compute stream. The update is issued per
+    /// all-reduce bucket as soon as it is legal -- the bucket's gradients are
+    /// final and no later backward launch reads its weights (DpBucket::
+    /// update_launch) -- on the comm stream, so it overlaps the rest of the
+    /// backward pass: at G > 1 it directly follows the bucket's all-reduce
+    /// (a per-bucket post-all-reduce epilogue), at G = 1 it forks off the
+    /// compute stream. The compute stream joins the comm stream at the end
+    /// (before the next step's forward reads the weights). The learning rate
+    /// is read from device memory, so the captured graph survives lr changes.
+    void enqueue_step(bool do_sgd) {
         nncb_ctx* ctx = dev->ctx();
         prog->enqueue_plan(0, nullptr);
         int64_t n = element_count(plans->train_fwd.values[plans->train_fwd.find_value(pred)].dims);
         NNC_CHECK(nncb_l1_loss(ctx, static_cast<float*>(prog->ptr(pred)), static_cast<float*>(target),
                                static_cast<float*>(prog->ptr(dpred)), static_cast<double*>(loss), n));
-        if (dev->nranks() > 1) {
-            // each bucket's all-reduce starts on the comm stream right after the
-            // launch that writes its last gradient, overlapping the rest of the
-            // backward pass; SGD waits for all of them
-            std::map<int64_t, std::vector<size_t>> closing;
-            for (size_t b = 0; b < layout.buckets.size(); ++b) closing[layout.buckets[b].close_launch].push_back(b);
-            auto start = [&](size_t b) {
-                const DpBucket& bk = layout.buckets[b];
-                NNC_CHECK(nncb_allreduce_sum_async(ctx, static_cast<float*>(grads) + bk.offset, bk.count));
-            };
-            prog->enqueue_plan(1, nullptr, [&](size_t k) {
-                auto it = closing.find(static_cast<int64_t>(k));
-                if (it != closing.end())
-                    for (size_t b : it->second) start(b);
-            });
-            for (auto& [k, bs] : closing)   // buckets without a producing launch (none in a well-formed plan)
-                if (k < 0 || k >= static_cast<int64_t>(prog->steps[1].size()))
-                    for (size_t b : bs) start(b);
-            NNC_CHECK(nncb_comm_join(ctx));
-        } else {
-            prog->enqueue_plan(1, nullptr);
+        const bool comm = nncb_comm_active(ctx) != 0;
+        const double scale = 1.0 / static_cast<double>(dev->nranks());
+        std::map<int64_t, std::vector<size_t>> closing, updating;
+        const int64_t nl = static_cast<int64_t>(prog->steps[1].size());
+        auto at = [&](int64_t k) { return (k < 0 || k >= nl) ? nl - 1 : k; };
+        for (size_t b = 0; b < layout.buckets.size(); ++b) {
+            if (comm) closing[at(layout.buckets[b].close_launch)].push_back(b);
+            if (do_sgd) updating[at(layout.buckets[b].update_launch)].push_back(b);
         }
-        if (do_sgd)
-            NNC_CHECK(nncb_sgd(ctx, static_cast<float*>(params), static_cast<float*>(grads), region_elems, lr,
-                               1.0 / static_cast<double>(dev->nranks())));
+        bool forked = false;
+        prog->enqueue_plan(1, nullptr, [&](size_t k) {
+            auto c = closing.find(static_cast<int64_t>(k));
+            auto u = updating.find(static_cast<int64_t>(k));
+            if (c == closing.end() && u == updating.end()) return;
+            NNC_CHECK(nncb_fork(ctx, NNCB_STREAM_COMM));
+            forked = true;
+            if (c != closing.end())
+                for (size_t b : c->second) {
+                    const DpBucket& bk = layout.buckets[b];
+                    NNC_CHECK(nncb_allreduce_sum_on_comm(ctx, static_cast<float*>(grads) + bk.offset, bk.count));
+                }
+            if (u != updating.end())
+                for (size_t b : u->second) {
+                    const DpBucket& bk = layout.buckets[b];
+                    NNC_CHECK(nncb_sgd_dev(ctx, NNCB_STREAM_COMM, static_cast<float*>(params) + bk.offset,
+                                           static_cast<float*>(grads) + bk.offset, bk.count, lr_dev, scale));
+                }
+        });
+        if (forked) NNC_CHECK(nncb_join(ctx, NNCB_STREAM_COMM));
     }
 
     void sync_params() {
@@ -1381,29 +1505,26 @@ struct Trainer::Impl {
     void run(double lr, bool do_sgd) {
         nncb_ctx* ctx = dev->ctx();
         sync_params();
+        if (do_sgd && !(lr == lr_written)) {   // stream-ordered before the step that reads it
+            NNC_CHECK(nncb_set_f64(ctx, lr_dev, lr));
+            lr_written = lr;
+        }
         if (!opts.use_graphs || !warmed) {
             uint64_t before = nncb_launch_count(ctx);
-            enqueue_step(lr, do_sgd);
+            enqueue_step(do_sgd);
             NNC_CHECK(nncb_sync(ctx));
             if (do_sgd) launches_per_step = nncb_launch_count(ctx) - before;
             warmed = true;
         } else {
             void*& g = do_sgd ? graph : graph_nosgd;
-            if (do_sgd && g && graph_lr != lr) {
-                nncb_graph_destroy(g);
-                g = nullptr;
-            }
             if (!g) {
                 // the captured kernels are exactly what every replay launches
                 // (the first eager step also ran the GEMM tile autotuner)
                 const uint64_t before = nncb_launch_count(ctx);
                 NNC_CHECK(nncb_capture_begin(ctx));
-                enqueue_step(lr, do_sgd);
+                enqueue_step(do_sgd);
                 NNC_CHECK(nncb_capture_end(ctx, &g));
-                if (do_sgd) {
-                    graph_lr = lr;
-                    launches_per_step = nncb_launch_count(ctx) - before;
-                }
+                if (do_sgd) launches_per_step = nncb_launch_count(ctx) - before;
             }
             NNC_CHECK(nncb_graph_launch(ctx, g));
         }
@@ -1425,8 +1546,10 @@ DpLayout dp_layout(const plan::VersionPlans& plans, HostModel& model, int64_t bu
         for (uint32_t li : es.launches) {
             const auto& Lc = bwd.groups[es.group].launches[li];
             for (size_t a = 0; a < Lc.args.size(); ++a) {
+                const plan::ValueEntry& v = bwd.values[Lc.args[a].slot];
+                if (!Lc.is_out[a] && v.category == MemCategory::Parameter) L.read_launch[v.source_weight] = k;
                 if (!Lc.is_out[a]) continue;
-                auto it = grad_to_weight.find(bwd.values[Lc.args[a].slot].name);
+                auto it = grad_to_weight.find(v.name);
                 if (it == grad_to_weight.end()) continue;
                 if (!L.grad_launch.count(it->second)) L.weights.push_back(it->second);   // first production order
                 L.grad_launch[it->second] = k;                                          // last write
@@ -1453,8 +1576,12 @@ DpLayout dp_layout(const plan::VersionPlans& plans, HostModel& model, int64_t bu
         b.offset = off;
         b.count = std::min(bucket_elems, trainable_end - off);
         for (const std::string& w : L.weights)
-            if (L.grad_launch[w] >= 0 && L.offset[w] < off + b.count && off < L.offset[w] + L.elements[w])
+            if (L.grad_launch[w] >= 0 && L.offset[w] < off + b.count && off < L.offset[w] + L.elements[w]) {
                 b.close_launch = std::max(b.close_launch, L.grad_launch[w]);
+                auto rd = L.read_launch.find(w);
+                b.update_launch = std::max(b.update_launch, rd == L.read_launch.end() ? int64_t(-1) : rd->second);
+            }
+        b.update_launch = std::max(b.update_launch, b.close_launch);
         L.buckets.push_back(b);
     }
     return L;
@@ -1494,10 +1621,16 @@ Trainer::Trainer(const plan::VersionPlans& plans, HostModel& model, Device& dev,
     const int64_t pred_elems = element_count(plans.train_fwd.values[plans.train_fwd.find_value(I.pred)].dims);
     NNC_CHECK(nncb_malloc(ctx, static_cast<size_t>(std::max<int64_t>(pred_elems, 4)) * 4, &I.target));
     NNC_CHECK(nncb_malloc(ctx, 64, &I.loss));
+    {
+        void* p = nullptr;
+        NNC_CHECK(nncb_malloc(ctx, 64, &p));
+        I.lr_dev = static_cast<double*>(p);
+    }
     I.prog = std::make_unique<Program>();
     I.prog->dev = &dev;
     I.prog->plans = {&plans.train_fwd, &plans.train_bwd};
     I.prog->precision = opts.gemm_precision;
+    I.prog->keep_values = opts.keep_values;
     std::map<std::string, std::string> weight_of_grad;
     for (const auto& [w, gv] : plans.weight_grads) weight_of_grad[gv] = w;
     I.prog->bind([&](const std::string& w) { return static_cast<void*>(static_cast<float*>(I.params) + I.w_off.at(w)); },
@@ -1569,6 +1702,23 @@ std::vector<Trainer::LaunchTiming> Trainer::profile_step(double lr) {
 }
 
 void* Trainer::input_device_ptr(const std::string& name) { return impl->prog->ptr(name); }
+
+Tensor Trainer::value(const std::string& name) {
+    Impl& I = *impl;
+    for (const ExecutionPlan* p : I.prog->plans) {
+        const int s = p->find_value(name);
+        if (s < 0) continue;
+        const plan::ValueEntry& v = p->values[s];
+        if (v.storage != StorageClass::Buffer)
+            throw Error(Error::Code::ShapeMismatch, name + " lives in registers of a fused group");
+        Tensor t(p->dtype, v.dims);
+        NNC_CHECK(nncb_sync(I.dev->ctx()));
+        NNC_CHECK(nncb_d2h(I.dev->ctx(), t.data(), I.prog->ptr(name), t.byte_size()));
+        NNC_CHECK(nncb_sync(I.dev->ctx()));
+        return t;
+    }
+    throw Error(Error::Code::ShapeMismatch, "no value " + name + " in the training step");
+}
 void* Trainer::target_device_ptr() { return impl->target; }
 size_t Trainer::arena_bytes() const { return static_cast<size_t>(impl->prog->arena_bytes); }
 uint64_t Trainer::launches_per_step() const { return impl->launches_per_step; }

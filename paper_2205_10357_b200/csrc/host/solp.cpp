@@ -9,6 +9,7 @@
 // originating op with its attributes. The process-unique plan uid is not
 // serialized (a loaded plan gets a fresh one). Truncated or foreign streams
 // throw nnc::Error(BadDocument).
+#include <algorithm>
 #include <cstring>
 #include <fstream>
 #include <iterator>
@@ -198,6 +199,96 @@ void write_plan(Writer& w, const ExecutionPlan& p) {
     for (const std::string& n : p.weight_names) w.str(n);
 }
 
+/// Semantic validation of a decoded plan: every enum in range, every slot,
+/// register, element offset and schedule index inside what it indexes. A
+/// well-formed but inconsistent stream must be rejected here -- the runtime
+/// turns these fields into device pointer arithmetic and generated kernels.
+void validate_plan(const ExecutionPlan& p) {
+    auto bad = [](const std::string& what) { throw Error(Error::Code::BadDocument, "SOLP: " + what); };
+    if (p.dtype != DType::F32 && p.dtype != DType::F64) bad("dtype out of range");
+    if (static_cast<unsigned>(p.role) > static_cast<unsigned>(PlanRole::TrainBwd)) bad("role out of range");
+    // names are printable ASCII identifiers (DLB documents); anything else is corruption
+    auto name_ok = [&](const std::string& n) {
+        for (unsigned char c : n)
+            if (c < 0x20 || c > 0x7E) bad("non-printable byte in a name");
+    };
+    for (const ValueEntry& v : p.values) {
+        name_ok(v.name);
+        name_ok(v.source_weight);
+    }
+    for (const GroupKernel& g : p.groups) {
+        name_ok(g.label);
+        for (const std::string& m : g.members) name_ok(m);
+        for (const Launch& L : g.launches) name_ok(L.label);
+    }
+    for (const ExecStep& es : p.exec_steps) name_ok(es.label);
+    for (const std::string& w : p.weight_names) name_ok(w);
+    std::vector<int64_t> elems;
+    for (const ValueEntry& v : p.values) {
+        if (static_cast<unsigned>(v.category) > static_cast<unsigned>(MemCategory::Saved)) bad("value category");
+        if (static_cast<unsigned>(v.storage) > static_cast<unsigned>(StorageClass::FusedRegister)) bad("storage class");
+        if (v.dims.size() > 8) bad("value rank");
+        int64_t n = 1;
+        for (int64_t d : v.dims) {
+            if (d < 0 || d > (int64_t(1) << 40)) bad("dimension out of range in " + v.name);
+            n *= std::max<int64_t>(d, 1);
+            if (n > (int64_t(1) << 40)) bad("value too large: " + v.name);
+        }
+        elems.push_back(n);
+    }
+    constexpr int kMaxSlots = 48, kMaxRegs = 512;
+    for (const GroupKernel& g : p.groups) {
+        if (g.backend != backends::BackendId::B200_FUSED && g.backend != backends::BackendId::B200_GEMM)
+            bad("backend id out of range");
+        for (const Launch& L : g.launches) {
+            if (static_cast<unsigned>(L.kind) > static_cast<unsigned>(LaunchKind::LnDgamma)) bad("launch kind");
+            if (static_cast<unsigned>(L.op) > static_cast<unsigned>(hlir::OpKind::LayerNormGradGamma)) bad("op kind");
+            if (L.is_out.size() != L.args.size()) bad("argument flags");
+            if (L.args.size() > static_cast<size_t>(kMaxSlots)) bad("too many launch arguments");
+            for (const Arg& a : L.args)
+                if (a.offset < 0 || a.offset >= std::max<int64_t>(elems[a.slot], 1)) bad("argument offset out of range");
+            if (L.kind != LaunchKind::Ew) continue;
+            if (L.ew_regs < 0 || L.ew_regs > kMaxRegs) bad("register count");
+            const int nargs = static_cast<int>(L.args.size());
+            for (const nncb_ew_instr& in : L.ew) {
+                // register operands each opcode reads (unused fields are -1)
+                int need = 0;   // bit i: field i of {dst, a, b, c, d, e, f, h} must be a register
+                switch (in.op) {
+                    case NNCB_EW_LOAD: case NNCB_EW_LOAD_CH: need = 0x01; break;
+                    case NNCB_EW_STORE: need = 0x02; break;
+                    case NNCB_EW_RELU: case NNCB_EW_COPY: case NNCB_EW_GELU: case NNCB_EW_GELU_FAST: need = 0x03; break;
+                    case NNCB_EW_RELU_GRAD: case NNCB_EW_ADD: case NNCB_EW_MUL: case NNCB_EW_GELU_GRAD:
+                    case NNCB_EW_GELU_GRAD_FAST: need = 0x07; break;
+                    case NNCB_EW_BN_APPLY: case NNCB_EW_BN_INFER: need = 0x3F; break;
+                    case NNCB_EW_BN_GRAD: case NNCB_EW_BN_GRAD_FAST: need = 0xFF; break;
+                    case NNCB_EW_REDUCE_BN_GRAD: need = 0x1E; break;
+                    default: bad("elementwise opcode");
+                }
+                const int fields[8] = {in.dst, in.a, in.b, in.c, in.d, in.e, in.f, in.h};
+                for (int f = 0; f < 8; ++f) {
+                    if (f == 5 && in.op == NNCB_EW_REDUCE_BN_GRAD) continue;   // e is a slot there
+                    const int r = fields[f];
+                    const bool ok = (need >> f & 1) ? (r >= 0 && r < L.ew_regs) : (r >= -1 && r < std::max(L.ew_regs, 1));
+                    if (!ok)
+                        bad("register field " + std::to_string(f) + " = " + std::to_string(r) + " out of range (" +
+                            std::to_string(L.ew_regs) + " registers) in " + L.label);
+                }
+                const bool slotted = in.op == NNCB_EW_LOAD || in.op == NNCB_EW_LOAD_CH || in.op == NNCB_EW_STORE ||
+                                     in.op == NNCB_EW_REDUCE_BN_GRAD;
+                if (slotted && (in.slot < 0 || in.slot >= nargs)) bad("elementwise slot out of range in " + L.label);
+                if (in.op == NNCB_EW_REDUCE_BN_GRAD && (in.e < 0 || in.e >= nargs))
+                    bad("elementwise slot out of range in " + L.label);
+            }
+        }
+    }
+    for (const ExecStep& es : p.exec_steps)
+        if (es.kernel < -1 || es.kernel >= static_cast<int32_t>(p.groups[es.group].members.size()))
+            bad("exec step kernel index");
+    const int32_t last = static_cast<int32_t>(p.exec_steps.size());
+    for (const PlanEvent& e : p.events)
+        if (e.step < 0 || e.step > last) bad("event step out of range");
+}
+
 ExecutionPlan read_plan(Reader& r) {
     r.need(4);
     if (std::memcmp(r.in.data() + r.pos, kMagic, 4) != 0) throw Error(Error::Code::BadDocument, "SOLP: bad magic");
@@ -298,6 +389,7 @@ ExecutionPlan read_plan(Reader& r) {
     for (uint32_t i = 0; i < n; ++i) p.output_slots.push_back(slot(r.u32()));
     n = r.count(4);
     for (uint32_t i = 0; i < n; ++i) p.weight_names.push_back(r.str());
+    validate_plan(p);
     p.uid = next_plan_uid();
     return p;
 }
@@ -367,14 +459,20 @@ VersionPlans load_version_plans(const std::vector<uint8_t>& bytes) {
         r.pos += n;
         *p = load_plan(b);
     }
+    auto name = [&]() {
+        std::string s = r.str();
+        for (unsigned char c : s)
+            if (c < 0x20 || c > 0x7E) throw Error(Error::Code::BadDocument, "SOLP: non-printable byte in a name");
+        return s;
+    };
     uint32_t n = r.count(4);
-    for (uint32_t i = 0; i < n; ++i) v.save_set.push_back(r.str());
+    for (uint32_t i = 0; i < n; ++i) v.save_set.push_back(name());
     n = r.count(4);
-    for (uint32_t i = 0; i < n; ++i) v.output_grads.push_back(r.str());
+    for (uint32_t i = 0; i < n; ++i) v.output_grads.push_back(name());
     n = r.count(8);
     for (uint32_t i = 0; i < n; ++i) {
-        std::string k = r.str();
-        v.weight_grads[k] = r.str();
+        std::string k = name();
+        v.weight_grads[k] = name();
     }
     if (r.pos != bytes.size()) throw Error(Error::Code::BadDocument, "SOLP: trailing bytes after the plan set");
     return v;

@@ -65,6 +65,10 @@ struct ExecOptions {
     // inputs already on the device from a previous execute of this plan:
     // skip the host->device input copies (device-resident replay)
     bool inputs_resident = false;
+    // parity debugging: every Buffer value of a training step gets its own
+    // arena bytes (no reuse), so after a step every forward and backward
+    // value can be read back (Trainer::value) and checked launch by launch
+    bool keep_values = false;
 };
 
 struct L1Result {
@@ -182,10 +186,14 @@ std::map<std::string, Tensor> gradients(const plan::VersionPlans& plans,
 /// all-reduce can start there, overlapping the rest of the backward pass.
 struct DpBucket {
     int64_t offset = 0, count = 0, close_launch = -1;
+    // the launch after which the bucket's weights may be updated: its
+    // gradients are final AND no later backward launch reads its weights
+    int64_t update_launch = -1;
 };
 struct DpLayout {
     std::vector<std::string> weights;              // region order
     std::map<std::string, int64_t> offset, elements, grad_launch;   // grad_launch: -1 for non-trainable
+    std::map<std::string, int64_t> read_launch;    // last backward launch reading the weight (-1: none)
     int64_t region_elems = 0;
     int64_t bwd_launches = 0;
     std::vector<DpBucket> buckets;
@@ -223,6 +231,9 @@ struct Trainer {
     };
     std::vector<LaunchTiming> profile_step(double lr);
     void* input_device_ptr(const std::string& name);
+    /// Device bytes of any Buffer value of the bound step (meaningful for
+    /// every value only when the trainer was built with keep_values).
+    Tensor value(const std::string& name);
     void* target_device_ptr();
     size_t arena_bytes() const;
     uint64_t launches_per_step() const;

@@ -105,40 +105,27 @@ int nncb_comm_destroy(nncb_ctx* ctx) {
 int nncb_allreduce_sum(nncb_ctx* ctx, float* buf, int64_t count) {
     if (!ctx->nccl_comm) return nncb::fail("nncb_allreduce_sum: communicator not initialised");
     if (count <= 0) return 0;
-    cudaEvent_t ready, done;
-    NNCB_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-    NNCB_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
-    NNCB_CUDA(cudaEventRecord(ready, ctx->stream));
-    NNCB_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ready, 0));
+    if (int rc = nncb_allreduce_sum_async(ctx, buf, count)) return rc;
+    return nncb_comm_join(ctx);
+}
+
+int nncb_allreduce_sum_on_comm(nncb_ctx* ctx, float* buf, int64_t count) {
+    if (!ctx->nccl_comm) return nncb::fail("nncb_allreduce_sum_on_comm: communicator not initialised");
+    if (count <= 0) return 0;
     NNCB_NCCL(nccl().allReduce(buf, buf, static_cast<size_t>(count), ncclFloat32, ncclSum,
                                static_cast<ncclComm_t>(ctx->nccl_comm), ctx->comm_stream));
-    NNCB_CUDA(cudaEventRecord(done, ctx->comm_stream));
-    NNCB_CUDA(cudaStreamWaitEvent(ctx->stream, done, 0));
-    cudaEventDestroy(ready);
-    cudaEventDestroy(done);
     return 0;
 }
 
 int nncb_allreduce_sum_async(nncb_ctx* ctx, float* buf, int64_t count) {
     if (!ctx->nccl_comm) return nncb::fail("nncb_allreduce_sum_async: communicator not initialised");
     if (count <= 0) return 0;
-    cudaEvent_t ready;
-    NNCB_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-    NNCB_CUDA(cudaEventRecord(ready, ctx->stream));
-    NNCB_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ready, 0));
-    NNCB_NCCL(nccl().allReduce(buf, buf, static_cast<size_t>(count), ncclFloat32, ncclSum,
-                               static_cast<ncclComm_t>(ctx->nccl_comm), ctx->comm_stream));
-    cudaEventDestroy(ready);
-    return 0;
+    if (int rc = nncb_fork(ctx, NNCB_STREAM_COMM)) return rc;
+    return nncb_allreduce_sum_on_comm(ctx, buf, count);
 }
 
-int nncb_comm_join(nncb_ctx* ctx) {
-    cudaEvent_t done;
-    NNCB_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
-    NNCB_CUDA(cudaEventRecord(done, ctx->comm_stream));
-    NNCB_CUDA(cudaStreamWaitEvent(ctx->stream, done, 0));
-    cudaEventDestroy(done);
-    return 0;
-}
+int nncb_comm_join(nncb_ctx* ctx) { return nncb_join(ctx, NNCB_STREAM_COMM); }
+
+int nncb_comm_active(nncb_ctx* ctx) { return ctx->nccl_comm ? 1 : 0; }
 
 }  // extern "C"

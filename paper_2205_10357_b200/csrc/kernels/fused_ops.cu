@@ -872,6 +872,25 @@ __device__ __forceinline__ float sgd1(float w, float g, double lr, double scale)
     return (float)__dsub_rn((double)w, __dmul_rn(lr, __dmul_rn((double)g, scale)));
 }
 
+// lr read from device memory (a captured step graph stays valid across learning-rate changes)
+__global__ void sgd_dev_k(float* __restrict__ w, const float* __restrict__ g, int64_t n,
+                          const double* __restrict__ lr_dev, double scale) {
+    const double lr = *lr_dev;
+    int64_t nv = n >> 2;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
+        float4 wv = reinterpret_cast<float4*>(w)[v];
+        float4 gv = __ldg(reinterpret_cast<const float4*>(g) + v);
+        wv.x = sgd1(wv.x, gv.x, lr, scale);
+        wv.y = sgd1(wv.y, gv.y, lr, scale);
+        wv.z = sgd1(wv.z, gv.z, lr, scale);
+        wv.w = sgd1(wv.w, gv.w, lr, scale);
+        reinterpret_cast<float4*>(w)[v] = wv;
+    }
+    for (int64_t i = (nv << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        w[i] = sgd1(w[i], g[i], lr, scale);
+}
+
 __global__ void sgd_k(float* __restrict__ w, const float* __restrict__ g, int64_t n, double lr, double scale) {
     int64_t nv = n >> 2;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
@@ -1081,6 +1100,17 @@ int nncb_sgd(nncb_ctx* ctx, float* w, const float* g, int64_t n, double lr, doub
     if ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(g)) & 15)
         return nncb::fail("nncb_sgd: buffers must be 16-byte aligned");
     sgd_k<<<nncb::grid_for(ctx, (n + 3) / 4, 256), 256, 0, ctx->stream>>>(w, g, n, lr, grad_scale);
+    NNCB_LAUNCHED(ctx);
+    return 0;
+}
+
+int nncb_sgd_dev(nncb_ctx* ctx, int stream, float* w, const float* g, int64_t n, const double* lr_dev,
+                 double grad_scale) {
+    if (n <= 0) return 0;
+    if ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(g)) & 15)
+        return nncb::fail("nncb_sgd_dev: buffers must be 16-byte aligned");
+    sgd_dev_k<<<nncb::grid_for(ctx, (n + 3) / 4, 256), 256, 0, nncb::stream_of(ctx, stream)>>>(w, g, n, lr_dev,
+                                                                                              grad_scale);
     NNCB_LAUNCHED(ctx);
     return 0;
 }

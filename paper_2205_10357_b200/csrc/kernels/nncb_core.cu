@@ -58,6 +58,17 @@ void* workspace(nncb_ctx* ctx, size_t bytes) {
 
 using nncb::fail;
 
+namespace nncb {
+cudaEvent_t fork_event(nncb_ctx* ctx) {
+    cudaEvent_t e = ctx->fork_events[ctx->fork_next];
+    ctx->fork_next = (ctx->fork_next + 1) % ctx->fork_events.size();
+    return e;
+}
+cudaStream_t stream_of(nncb_ctx* ctx, int id) {
+    return id == NNCB_STREAM_COPY ? ctx->copy_stream : id == NNCB_STREAM_COMM ? ctx->comm_stream : ctx->stream;
+}
+}  // namespace nncb
+
 extern "C" {
 
 const char* nncb_last_error(void) { return nncb::g_error.c_str(); }
@@ -78,6 +89,8 @@ int nncb_create(int device, nncb_ctx** out) {
     NNCB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     NNCB_CUDA(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
     NNCB_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    c->fork_events.resize(256);
+    for (auto& e : c->fork_events) NNCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     *out = c;
     return 0;
 }
@@ -97,6 +110,8 @@ int nncb_destroy(nncb_ctx* c) {
     for (void* p : c->retired) cudaFree(p);
     if (c->workspace) cudaFree(c->workspace);
     if (c->wt) cudaFree(c->wt);
+    cudaStreamSynchronize(c->comm_stream);
+    for (cudaEvent_t e : c->fork_events) cudaEventDestroy(e);
     cudaStreamDestroy(c->stream);
     cudaStreamDestroy(c->comm_stream);
     cudaStreamDestroy(c->copy_stream);
@@ -196,12 +211,33 @@ int nncb_event_record(nncb_ctx* c, void* ev) {
 }
 
 int nncb_event_record_on(nncb_ctx* c, int stream, void* ev) {
-    NNCB_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev), stream == NNCB_STREAM_COPY ? c->copy_stream : c->stream));
+    NNCB_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev), nncb::stream_of(c, stream)));
     return 0;
 }
 
 int nncb_stream_wait(nncb_ctx* c, int stream, void* ev) {
-    NNCB_CUDA(cudaStreamWaitEvent(stream == NNCB_STREAM_COPY ? c->copy_stream : c->stream, static_cast<cudaEvent_t>(ev), 0));
+    NNCB_CUDA(cudaStreamWaitEvent(nncb::stream_of(c, stream), static_cast<cudaEvent_t>(ev), 0));
+    return 0;
+}
+
+int nncb_fork(nncb_ctx* c, int to_stream) {
+    cudaEvent_t e = nncb::fork_event(c);
+    NNCB_CUDA(cudaEventRecord(e, c->stream));
+    NNCB_CUDA(cudaStreamWaitEvent(nncb::stream_of(c, to_stream), e, 0));
+    return 0;
+}
+
+int nncb_join(nncb_ctx* c, int from_stream) {
+    cudaEvent_t e = nncb::fork_event(c);
+    NNCB_CUDA(cudaEventRecord(e, nncb::stream_of(c, from_stream)));
+    NNCB_CUDA(cudaStreamWaitEvent(c->stream, e, 0));
+    return 0;
+}
+
+int nncb_set_f64(nncb_ctx* c, double* dst, double value) {
+    // stream-ordered 8-byte write (the pageable source is staged by the driver
+    // before the call returns); never called during a capture
+    NNCB_CUDA(cudaMemcpyAsync(dst, &value, sizeof(double), cudaMemcpyHostToDevice, c->stream));
     return 0;
 }
 

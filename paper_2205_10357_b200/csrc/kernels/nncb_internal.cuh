@@ -39,6 +39,10 @@ struct nncb_ctx {
     void* staging = nullptr;             // pinned upload ring (host_io.cu), created on first large h2d
     void* wt = nullptr;                  // transposed (K-major) forward weights, grown on demand
     size_t wt_bytes = 0;
+    // fork/join events between the compute and comm streams, reused round
+    // robin (created once: nothing is created or destroyed during a capture)
+    std::vector<cudaEvent_t> fork_events;
+    size_t fork_next = 0;
 };
 
 namespace nncb {
@@ -65,6 +69,9 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 
 void set_error(const std::string& msg);
+/// The next event of the context's fork/join pool.
+cudaEvent_t fork_event(nncb_ctx* ctx);
+cudaStream_t stream_of(nncb_ctx* ctx, int id);
 void staging_release(nncb_ctx* c);
 void* wt_buffer(nncb_ctx* ctx, size_t bytes);
 int fail(const std::string& msg);

@@ -136,3 +136,40 @@ def test_solp_plan_serialization_round_trip():
     for junk in (b"SOLX\x01\x00\x00\x00", bytes1[:-3], b"SOLV" + bytes1[4:12]):
         with pytest.raises(P.NNCError):
             b.load_plans(junk)
+
+
+def test_solp_loader_rejects_semantically_corrupt_streams():
+    """a well-formed but inconsistent stream (register / slot /
+    offset / enum fields out of range) must be rejected by the loader, never
+    turned into device pointer arithmetic. Single-byte corruptions of a real
+    plan set either fail to load with an NNCError or load a plan that passes
+    the semantic validation (which then re-serializes); none may crash."""
+    import random
+    doc = W.c1_small_cnn(2, bn=True)
+    good = P.CompiledModel(doc, precision=P.PREC_TF32).save_plans()
+    target = P.CompiledModel(doc, precision=P.PREC_TF32)
+    rng = random.Random(7)
+    rejected = 0
+    for _ in range(400):
+        b = bytearray(good)
+        i = rng.randrange(8, len(b))
+        b[i] = rng.choice([0xFF, 0x7F, 0x80, b[i] ^ 0x40, b[i] + 1 & 0xFF])
+        try:
+            target.load_plans(bytes(b))
+            target.save_plans()
+        except P.NNCError:
+            rejected += 1
+    assert rejected > 100
+
+
+def test_importing_package_helpers_maps_no_native_library():
+    """The reference arm of bench.py imports `workloads` only: it must not map
+    the backend's .so files; the first real use loads them."""
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "import paper_2205_10357_b200 as P\nfrom paper_2205_10357_b200 import workloads\n"
+            "m = open('/proc/self/maps').read()\n"
+            "assert 'libnncb.so' not in m and 'libnnc_b200.so' not in m, 'mapped at import'\n"
+            "P.load_native()\n"
+            "m = open('/proc/self/maps').read()\n"
+            "assert 'libnncb.so' in m and 'libnnc_b200.so' in m\n") % ROOT
+    subprocess.run([os.sys.executable, "-c", code], check=True)
