@@ -263,6 +263,7 @@ def main():
 
     dist = None
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")   # the communicator shows in the logs
         import torch.distributed as dist_mod
         dist = dist_mod
         dist.init_process_group("gloo", rank=rank, world_size=world)

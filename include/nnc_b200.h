@@ -33,6 +33,12 @@ int         nnc_last_status(void);   /* status of the last failed call (for NULL
 /* Parse + optimize + derive versions + compile plans. gemm_precision:
  * 0 = tcgen05 tf32 (default), 1 = exact fp32 (bit-exact with the reference). */
 nnc_model*  nnc_model_compile(const char* dlb_document, int gemm_precision);
+/* As nnc_model_compile, with the listed free vdims (#k of the document's
+ * dynamic input axes: "shape": null + "seed_shape") ENABLED
+ * (passes::VdimBinding::enable): the model then accepts any extent on those
+ * axes per call; plans are re-specialised and cached per binding.          */
+nnc_model*  nnc_model_compile_ex(const char* dlb_document, int gemm_precision, const int32_t* enable_vdims,
+                                 int n_enable);
 void        nnc_model_free(nnc_model* m);
 const char* nnc_model_describe(nnc_model* m);          /* JSON: plans, groups, launches, save set */
 
@@ -51,6 +57,8 @@ int nnc_model_load_plans(nnc_model* m, const uint8_t* bytes, uint64_t n);
 int nnc_model_run(nnc_model* m, int role);
 /* nnc_model_run copying back only the comma-separated outputs `names` (ExecOptions::materialize). */
 int nnc_model_run_outputs(nnc_model* m, int role, const char* names);
+/* Dims of a materialized output of the last run (rank <= 8).              */
+int nnc_model_output_dims(nnc_model* m, const char* name, int64_t* dims, int* rank);
 int nnc_model_output(nnc_model* m, const char* name, float* out, int64_t n);
 /* Pipelined runs from host buffers: nnc_model_run_staged launches the oldest
  * staged run (names: comma-separated outputs, NULL or "" = all),
@@ -84,6 +92,13 @@ int nnc_model_trainer_value(nnc_model* m, const char* name, float* out, int64_t 
  * all-reduce buckets and the backward launch after which each can start.
  * Host-only. Returns NULL on error. The string is valid until the next call. */
 const char* nnc_model_dp_schedule(nnc_model* m, int64_t bucket_bytes);
+/* The backward half of the training step as issued (runtime::step_schedule),
+ * host-only, as JSON: {"actions": [{"after": k, "kind": fork|allreduce|update|
+ * join, "bucket": b}], "launch_writes"/"launch_reads": per backward launch the
+ * weights whose gradient it writes / whose value it reads, "buckets",
+ * "weights", "region_elems", "bwd_launches"}. comm: with a communicator;
+ * do_sgd: with the update. NULL on error; valid until the next call.        */
+const char* nnc_model_step_schedule(nnc_model* m, int64_t bucket_bytes, int comm, int do_sgd);
 
 /* Device-resident stepping for benchmarks: inputs/target stay on the device. */
 int      nnc_model_trainer_prepare(nnc_model* m, const float* target, int64_t n);

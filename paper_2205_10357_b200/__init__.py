@@ -60,6 +60,8 @@ def _load():
         "nnc_last_error": (S, []),
         "nnc_last_status": (I, []),
         "nnc_model_compile": (P, [S, I]),
+        "nnc_model_compile_ex": (P, [S, I, ctypes.POINTER(ctypes.c_int32), I]),
+        "nnc_model_output_dims": (I, [P, S, I64P, ctypes.POINTER(ctypes.c_int)]),
         "nnc_model_free": (None, [P]),
         "nnc_model_describe": (S, [P]),
         "nnc_model_set_weight": (I, [P, S, FP, I64]),
@@ -84,6 +86,7 @@ def _load():
         "nnc_model_launches_per_step": (U64, [P]),
         "nnc_model_profile_step": (S, [P, D]),
         "nnc_model_dp_schedule": (S, [P, I64]),
+        "nnc_model_step_schedule": (S, [P, I64, I, I]),
         "nnc_model_arena_bytes": (U64, [P]),
         "nnc_model_infer_device": (I, [P]),
         "nnc_model_run_device": (I, [P, I]),
@@ -170,8 +173,11 @@ class CompiledModel:
     """A document compiled through optimize -> derive_versions -> compile_version_set,
     holding its HostModel (weights + stamps) on the B200 runtime."""
 
-    def __init__(self, document: str, precision: int = PREC_TF32):
-        h = _host.nnc_model_compile(document.encode(), precision)
+    def __init__(self, document: str, precision: int = PREC_TF32, dynamic_vdims: Sequence[int] = ()):
+        """dynamic_vdims: free vdims (#k) of the document to enable
+        (passes::VdimBinding::enable) -- e.g. (0,) for a dynamic batch."""
+        ids = (ctypes.c_int32 * max(len(dynamic_vdims), 1))(*dynamic_vdims)
+        h = _host.nnc_model_compile_ex(document.encode(), precision, ids, len(dynamic_vdims))
         if not h:
             raise NNCError(_host.nnc_last_status(), _host.nnc_last_error().decode())
         self._h = h
@@ -239,7 +245,11 @@ class CompiledModel:
             v = self._plan_value(role, name)
             if v["storage"] != "buffer":
                 continue
-            arr = np.empty(v["dims"], dtype=np.float32)
+            dims = (ctypes.c_int64 * 8)()
+            rank = ctypes.c_int()
+            if _host.nnc_model_output_dims(self._h, name.encode(), dims, ctypes.byref(rank)) != 0:
+                continue
+            arr = np.empty(tuple(dims[: rank.value]), dtype=np.float32)
             if _host.nnc_model_output(self._h, name.encode(), _fptr(arr), arr.size) == 0:
                 out[name] = arr
         return out
@@ -373,6 +383,14 @@ class CompiledModel:
     def dp_schedule(self, bucket_bytes: int = 32 << 20) -> dict:
         """Data-parallel region layout and all-reduce bucket schedule (host-only)."""
         res = _host.nnc_model_dp_schedule(self._h, bucket_bytes)
+        if res is None:
+            raise NNCError(100, _host.nnc_last_error().decode())
+        return json.loads(res.decode())
+
+    def step_schedule(self, bucket_bytes: int = 32 << 20, comm: bool = True, sgd: bool = True) -> dict:
+        """The backward half of the training step as the Trainer issues it
+        (forks, per-bucket all-reduces and updates, join) -- host-only."""
+        res = _host.nnc_model_step_schedule(self._h, bucket_bytes, 1 if comm else 0, 1 if sgd else 0)
         if res is None:
             raise NNCError(100, _host.nnc_last_error().decode())
         return json.loads(res.decode())

@@ -93,7 +93,8 @@ void describe_plan(std::ostringstream& os, const plan::ExecutionPlan& p) {
 const plan::ExecutionPlan& pred_plan(nnc_model* m) { return m->plans.inference; }
 
 Tensor target_tensor(nnc_model* m, const float* target, int64_t n) {
-    const auto& p = pred_plan(m);
+    // the prediction's shape for the fed inputs (a dynamic batch re-specialises the plans)
+    const auto& p = runtime::plan_for_inputs(pred_plan(m), m->inputs, m->opts.bindings);
     const auto& v = p.values[p.output_slots.at(0)];
     if (element_count(v.dims) != n) throw Error(Error::Code::ShapeMismatch, "target size mismatch");
     // borrowed: every consumer (train_step, gradients, stage, trainer_prepare)
@@ -108,11 +109,15 @@ extern "C" {
 const char* nnc_last_error(void) { return g_err.c_str(); }
 int nnc_last_status(void) { return g_status; }
 
-nnc_model* nnc_model_compile(const char* doc, int precision) {
+nnc_model* nnc_model_compile(const char* doc, int precision) { return nnc_model_compile_ex(doc, precision, nullptr, 0); }
+
+nnc_model* nnc_model_compile_ex(const char* doc, int precision, const int32_t* enable_vdims, int n_enable) {
     auto m = std::make_unique<nnc_model>();
     int rc = guarded([&] {
         m->model = ingest::parse_model(doc);
-        m->optimized = passes::optimize(m->model.graph).graph;
+        passes::VdimBinding binding;
+        for (int i = 0; i < n_enable; ++i) binding.items[enable_vdims[i]] = {passes::VdimBinding::Action::Enable, 0};
+        m->optimized = passes::optimize(m->model.graph, binding).graph;
         m->versions = autodiff::derive_versions(m->optimized);
         m->plans = plan::compile_version_set(m->versions, [](const hlir::Graph& g) { return backends::default_assignment(g); });
         m->host = std::make_unique<runtime::HostModel>(runtime::HostModel::from_graph(m->optimized));
@@ -221,7 +226,7 @@ int nnc_model_load_plans(nnc_model* m, const uint8_t* bytes, uint64_t n) {
 int nnc_model_run(nnc_model* m, int role) {
     const int rc = guarded([&] {
         const plan::ExecutionPlan& p = role == 1 ? m->plans.train_fwd : m->plans.inference;
-        m->outputs = runtime::execute(p, m->inputs, *m->host, nullptr, m->opts);
+        m->outputs = runtime::execute_on(p, m->inputs, *m->host, nullptr, m->opts);
     });
     drop_views(m);
     return rc;
@@ -244,7 +249,7 @@ int nnc_model_run_outputs(nnc_model* m, int role, const char* names) {
         runtime::ExecOptions o = m->opts;
         o.materialize = &want;
         const plan::ExecutionPlan& p = role == 1 ? m->plans.train_fwd : m->plans.inference;
-        m->outputs = runtime::execute(p, m->inputs, *m->host, nullptr, o);
+        m->outputs = runtime::execute_on(p, m->inputs, *m->host, nullptr, o);
     });
     drop_views(m);
     return rc;
@@ -288,6 +293,15 @@ int nnc_model_staged_outputs(nnc_model* m, int role) {
     });
 }
 
+int nnc_model_output_dims(nnc_model* m, const char* name, int64_t* dims, int* rank) {
+    return guarded([&] {
+        auto it = m->outputs.find(name);
+        if (it == m->outputs.end()) throw Error(Error::Code::ShapeMismatch, std::string("no output ") + name);
+        *rank = static_cast<int>(it->second.dims().size());
+        for (int i = 0; i < *rank && i < 8; ++i) dims[i] = it->second.dims()[i];
+    });
+}
+
 int nnc_model_output(nnc_model* m, const char* name, float* out, int64_t n) {
     return guarded([&] {
         auto it = m->outputs.find(name);
@@ -298,7 +312,7 @@ int nnc_model_output(nnc_model* m, const char* name, float* out, int64_t n) {
 }
 
 int nnc_model_train_step(nnc_model* m, const float* target, int64_t n, double lr, double* loss) {
-    const int rc = guarded([&] { *loss = runtime::train_step(m->plans, m->inputs, target_tensor(m, target, n), *m->host, lr, nullptr, m->opts); });
+    const int rc = guarded([&] { *loss = runtime::train_step_on(m->plans, m->inputs, target_tensor(m, target, n), *m->host, lr, nullptr, m->opts); });
     drop_views(m);
     return rc;
 }
@@ -393,9 +407,53 @@ const char* nnc_model_dp_schedule(nnc_model* m, int64_t bucket_bytes) {
         nlohmann::json w = nlohmann::json::array(), b = nlohmann::json::array();
         for (const std::string& n : L.weights)
             w.push_back({{"name", n}, {"offset", L.offset[n]}, {"elements", L.elements[n]}, {"grad_launch", L.grad_launch[n]}});
-        for (const auto& x : L.buckets) b.push_back({{"offset", x.offset}, {"count", x.count}, {"close_launch", x.close_launch}});
+        for (const auto& x : L.buckets)
+            b.push_back({{"offset", x.offset}, {"count", x.count}, {"close_launch", x.close_launch},
+                         {"update_launch", x.update_launch}});
         g_buf = nlohmann::json{{"region_elems", L.region_elems}, {"bwd_launches", L.bwd_launches}, {"weights", w},
                                {"buckets", b}}.dump();
+    });
+    return rc ? nullptr : g_buf.c_str();
+}
+
+const char* nnc_model_step_schedule(nnc_model* m, int64_t bucket_bytes, int comm, int do_sgd) {
+    int rc = guarded([&] {
+        runtime::DpLayout L = runtime::dp_layout(m->plans, *m->host, std::max<int64_t>(bucket_bytes / 4, 64));
+        nlohmann::json acts = nlohmann::json::array();
+        static const char* kinds[] = {"fork", "allreduce", "update", "join"};
+        for (const auto& a : runtime::step_schedule(L, comm != 0, do_sgd != 0))
+            acts.push_back({{"after", a.after}, {"kind", kinds[a.kind]}, {"bucket", a.bucket}});
+        // what each backward launch writes (weight gradients) and reads (weights)
+        std::map<std::string, std::string> weight_of_grad;
+        for (const auto& [w, gv] : m->plans.weight_grads) weight_of_grad[gv] = w;
+        nlohmann::json writes = nlohmann::json::array(), reads = nlohmann::json::array();
+        const plan::ExecutionPlan& bwd = m->plans.train_bwd;
+        for (const auto& es : bwd.exec_steps)
+            for (uint32_t li : es.launches) {
+                const auto& Lc = bwd.groups[es.group].launches[li];
+                nlohmann::json wr = nlohmann::json::array(), rd = nlohmann::json::array();
+                for (size_t a = 0; a < Lc.args.size(); ++a) {
+                    const plan::ValueEntry& v = bwd.values[Lc.args[a].slot];
+                    if (Lc.is_out[a]) {
+                        auto it = weight_of_grad.find(v.name);
+                        if (it != weight_of_grad.end()) wr.push_back(it->second);
+                    } else if (v.category == plan::MemCategory::Parameter) {
+                        rd.push_back(v.source_weight);
+                    }
+                }
+                writes.push_back(wr);
+                reads.push_back(rd);
+            }
+        nlohmann::json b = nlohmann::json::array();
+        for (const auto& x : L.buckets)
+            b.push_back({{"offset", x.offset}, {"count", x.count}, {"close_launch", x.close_launch},
+                         {"update_launch", x.update_launch}});
+        nlohmann::json w = nlohmann::json::array();
+        for (const std::string& n : L.weights)
+            w.push_back({{"name", n}, {"offset", L.offset[n]}, {"elements", L.elements[n]}});
+        g_buf = nlohmann::json{{"bwd_launches", L.bwd_launches}, {"region_elems", L.region_elems}, {"actions", acts},
+                               {"launch_writes", writes}, {"launch_reads", reads}, {"buckets", b}, {"weights", w}}
+                    .dump();
     });
     return rc ? nullptr : g_buf.c_str();
 }
@@ -436,7 +494,7 @@ int nnc_model_run_device(nnc_model* m, int role) {
         runtime::ExecOptions o = m->opts;
         o.materialize = &none;
         o.inputs_resident = true;
-        runtime::execute(role == 1 ? m->plans.train_fwd : m->plans.inference, m->inputs, *m->host, nullptr, o);
+        runtime::execute_on(role == 1 ? m->plans.train_fwd : m->plans.inference, m->inputs, *m->host, nullptr, o);
     });
 }
 

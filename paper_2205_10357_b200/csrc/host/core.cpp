@@ -52,6 +52,19 @@ void Tensor::own() {
     view_bytes_ = 0;
 }
 
+Tensor Tensor::from_f64(std::vector<int64_t> dims, std::vector<double> values) {
+    Tensor t(DType::F64, std::move(dims));
+    if (static_cast<int64_t>(values.size()) != t.elements())
+        throw Error(Error::Code::ShapeMismatch, "from_f64: value count does not match the dims");
+    std::memcpy(t.data(), values.data(), values.size() * sizeof(double));
+    return t;
+}
+
+bool Tensor::bitwise_equal(const Tensor& o) const {
+    return dtype_ == o.dtype_ && dims_ == o.dims_ && byte_size() == o.byte_size() &&
+           std::memcmp(data(), o.data(), byte_size()) == 0;
+}
+
 Tensor Tensor::from_f32(std::vector<int64_t> dims, std::vector<float> values) {
     Tensor t(DType::F32, std::move(dims));
     std::memcpy(t.data(), values.data(), t.byte_size());

@@ -294,13 +294,70 @@ Graph canonicalize(const Graph& g) {
     return out;
 }
 
-OptimizeResult optimize(const Graph& g) {
+VdimBinding VdimBinding::enable(std::initializer_list<int32_t> ids) {
+    VdimBinding b;
+    for (int32_t id : ids) b.items[id] = {Action::Enable, 0};
+    return b;
+}
+
+VdimReport infer_vdims(const Graph& g) {
+    VdimReport r;
+    for (const auto& gi : g.inputs)
+        for (const Dim& d : gi.type.shape.dims)
+            if (d.is_sym() && !r.report_id.count(d.sym_id())) {
+                const int32_t id = static_cast<int32_t>(r.free_syms.size());
+                r.report_id[d.sym_id()] = id;
+                r.free_syms.push_back({id, d.seed_extent()});
+            }
+    return r;
+}
+
+Graph bind_vdims(const Graph& g, const VdimReport& report, const VdimBinding& binding) {
+    for (const auto& [id, item] : binding.items) {
+        const bool known = std::any_of(report.free_syms.begin(), report.free_syms.end(),
+                                       [&](const VdimReport::FreeSym& f) { return f.id == id; });
+        if (!known) throw Error(Error::Code::UnknownSymbol, "unknown vdim #" + std::to_string(id));
+        if (item.action == VdimBinding::Action::Override && item.extent < 1)
+            throw Error(Error::Code::IllegalOverride, "#" + std::to_string(id) + ": override extent must be >= 1");
+    }
+    Graph out = g;
+    out.value_types.clear();
+    out.next_sym_id = 0;
+    for (auto& gi : out.inputs)
+        for (Dim& d : gi.type.shape.dims) {
+            if (!d.is_sym()) continue;
+            auto it = report.report_id.find(d.sym_id());
+            if (it == report.report_id.end()) {
+                d = Dim::fixed(d.seed_extent());
+                continue;
+            }
+            const int32_t rid = it->second;
+            auto bit = binding.items.find(rid);
+            const VdimBinding::Action a = bit == binding.items.end() ? VdimBinding::Action::Disable : bit->second.action;
+            if (a == VdimBinding::Action::Disable) {
+                d = Dim::fixed(d.seed_extent());
+            } else if (a == VdimBinding::Action::Override) {
+                d = Dim::fixed(bit->second.extent);
+            } else {
+                d = Dim::sym(rid, d.seed_extent());
+                out.next_sym_id = std::max(out.next_sym_id, rid + 1);
+            }
+        }
+    try {
+        return infer_shapes(out).graph;
+    } catch (const Error& e) {
+        if (e.code() == Error::Code::ExtentMismatch)
+            throw Error(Error::Code::IllegalOverride, std::string("binding failed: ") + e.what());
+        throw;
+    }
+}
+
+OptimizeResult optimize(const Graph& g, const VdimBinding& binding) {
     Graph cur = eliminate_dead(canonicalize(g));
-    for (auto& gi : cur.inputs)
-        for (Dim& d : gi.type.shape.dims)
-            if (d.is_sym()) d = Dim::fixed(d.seed_extent());
-    cur.next_sym_id = 0;
-    return {infer_shapes(cur).graph};
+    OptimizeResult r;
+    r.report = infer_vdims(cur);
+    r.graph = bind_vdims(cur, r.report, binding);
+    return r;
 }
 
 }  // namespace nnc::passes

@@ -612,11 +612,28 @@ ExecutionPlan compile_plan(const Graph& input_graph, const std::vector<FusionGro
     return plan;
 }
 
+namespace {
+// Enabled dims of the plan's graph inputs (Dim::sym after passes::bind_vdims).
+void record_vdims(const Graph& g, ExecutionPlan& p) {
+    for (const auto& gi : g.inputs) {
+        const int s = p.find_value(gi.name);
+        if (s < 0) continue;
+        for (size_t a = 0; a < gi.type.shape.dims.size(); ++a) {
+            const hlir::Dim& d = gi.type.shape.dims[a];
+            if (d.is_sym())
+                p.vdims.push_back({d.sym_id(), static_cast<uint32_t>(s), static_cast<uint32_t>(a), d.seed_extent()});
+        }
+    }
+}
+}  // namespace
+
 VersionPlans compile_version_set(const autodiff::VersionSet& versions,
                                  const std::function<backends::BackendAssignment(const Graph&)>& assign) {
     VersionPlans out;
     auto build = [&](const Graph& g, PlanRole role) {
-        return compile_plan(g, backends::group_layers(g, assign(g)), role, &versions);
+        ExecutionPlan p = compile_plan(g, backends::group_layers(g, assign(g)), role, &versions);
+        record_vdims(g, p);
+        return p;
     };
     out.inference = build(versions.inference, PlanRole::Inference);
     out.train_fwd = build(versions.train_fwd, PlanRole::TrainFwd);
@@ -624,7 +641,32 @@ VersionPlans compile_version_set(const autodiff::VersionSet& versions,
     out.save_set = versions.save_set;
     out.output_grads = versions.output_grads;
     out.weight_grads = versions.weight_grads;
+    if (!out.inference.vdims.empty() || !out.train_fwd.vdims.empty()) {
+        auto spec = std::make_shared<const Specializer>(versions.source, assign);
+        for (ExecutionPlan* p : {&out.inference, &out.train_fwd, &out.train_bwd}) p->spec = spec;
+    }
     return out;
+}
+
+const VersionPlans& Specializer::plans_for(const std::map<int32_t, int64_t>& binding) const {
+    std::lock_guard<std::mutex> lock(mu_);
+    auto it = cache_.find(binding);
+    if (it != cache_.end()) return *it->second;
+    Graph g = source_;
+    g.value_types.clear();
+    for (auto& gi : g.inputs)
+        for (hlir::Dim& d : gi.type.shape.dims)
+            if (d.is_sym()) {
+                auto b = binding.find(d.sym_id());
+                d = hlir::Dim::fixed(b != binding.end() ? b->second : d.seed_extent());
+            }
+    autodiff::VersionSet vs = autodiff::derive_versions(passes::infer_shapes(g).graph);
+    auto plans = std::make_unique<VersionPlans>(compile_version_set(vs, assign_));
+    return *cache_.emplace(binding, std::move(plans)).first->second;
+}
+
+const ExecutionPlan& Specializer::role_plan(const VersionPlans& v, PlanRole r) {
+    return r == PlanRole::Inference ? v.inference : r == PlanRole::TrainFwd ? v.train_fwd : v.train_bwd;
 }
 
 namespace {

@@ -953,18 +953,30 @@ HostModel::HostModel() {
     uid_ = next.fetch_add(1);
 }
 
+HostModel::HostModel(const HostModel& o) : HostModel() { *this = o; }
+
+HostModel& HostModel::operator=(const HostModel& o) {
+    if (this == &o) return *this;
+    o.sync();   // a copy is a value: device-newer weights come with it
+    weights = o.weights;
+    stamps = o.stamps;
+    device_owner = nullptr;   // the copy has its own identity (uid) in device caches
+    device_newer.clear();
+    return *this;
+}
+
 HostModel HostModel::from_graph(const hlir::Graph& g) {
     HostModel m;
     for (const auto& [name, t] : g.initializers) {
-        m.weights_.emplace(name, t);
-        m.stamps_[name] = 0;
+        m.weights.emplace(name, t);
+        m.stamps[name] = 0;
     }
     return m;
 }
 
 const Tensor& HostModel::tensor(const std::string& name) const {
-    auto it = weights_.find(name);
-    if (it == weights_.end()) throw Error(Error::Code::ShapeMismatch, "model has no weight " + name);
+    auto it = weights.find(name);
+    if (it == weights.end()) throw Error(Error::Code::ShapeMismatch, "model has no weight " + name);
     if (device_owner && device_newer.count(name)) {
         device_owner->pull_weight(*this, name, it->second);
         device_newer.erase(name);
@@ -972,22 +984,27 @@ const Tensor& HostModel::tensor(const std::string& name) const {
     return it->second;
 }
 
+void HostModel::sync() const {
+    for (const std::string& name : std::vector<std::string>(device_newer.begin(), device_newer.end()))
+        (void)tensor(name);
+}
+
 uint64_t HostModel::stamp(const std::string& name) const {
-    auto it = stamps_.find(name);
-    return it == stamps_.end() ? 0 : it->second;
+    auto it = stamps.find(name);
+    return it == stamps.end() ? 0 : it->second;
 }
 
 void HostModel::set(const std::string& name, Tensor value) {
-    weights_[name] = std::move(value);
+    weights[name] = std::move(value);
     device_newer.erase(name);
-    ++stamps_[name];
+    ++stamps[name];
 }
 
-void HostModel::bump(const std::string& name) { ++stamps_[name]; }
+void HostModel::bump(const std::string& name) { ++stamps[name]; }
 
 std::vector<std::string> HostModel::names() const {
     std::vector<std::string> out;
-    for (const auto& [k, v] : weights_) out.push_back(k);
+    for (const auto& [k, v] : weights) out.push_back(k);
     return out;
 }
 
@@ -1096,6 +1113,100 @@ Device& default_device() {
 }
 
 /* ------------------------------------------------------------------ */
+/*  OffloadDevice / ExecutionContext (reference runtime.hpp:40-121)    */
+/* ------------------------------------------------------------------ */
+
+OffloadDevice::OffloadDevice(Device* device) : dev_(device ? device : &default_device()) {}
+
+OffloadDevice::~OffloadDevice() {
+    for (auto& [n, c] : cache_)
+        if (c.device) nncb_free(dev_->ctx(), c.device);
+}
+
+uint8_t* OffloadDevice::sync_weight(const std::string& name, const Tensor& host, uint64_t stamp, int64_t aligned_bytes) {
+    auto it = cache_.find(name);
+    if (it == cache_.end() || it->second.bytes != aligned_bytes) {
+        if (it != cache_.end() && it->second.device) nncb_free(dev_->ctx(), it->second.device);
+        CachedWeight c;
+        c.bytes = aligned_bytes;
+        NNC_CHECK(nncb_malloc(dev_->ctx(), static_cast<size_t>(std::max<int64_t>(aligned_bytes, 256)), &c.device));
+        c.stamp = ~stamp;   // stale: forces the copy below
+        it = cache_.insert_or_assign(name, c).first;
+    }
+    CachedWeight& c = it->second;
+    if (c.stamp != stamp) {
+        NNC_CHECK(nncb_h2d(dev_->ctx(), c.device, host.data(), host.byte_size()));
+        c.stamp = stamp;
+        stats_.h2d_bytes += static_cast<uint64_t>(aligned_bytes);
+        stats_.weight_bytes += static_cast<uint64_t>(aligned_bytes);
+        ++stats_.weight_transfers[name];
+    }
+    return static_cast<uint8_t*>(c.device);
+}
+
+void OffloadDevice::preseed(const std::string& name, const Tensor& host, uint64_t stamp, int64_t aligned_bytes) {
+    const SyncStats keep = stats_;
+    (void)sync_weight(name, host, ~stamp, aligned_bytes);   // place the bytes ...
+    cache_[name].stamp = stamp;                              // ... as current at `stamp`
+    stats_ = keep;                                           // without counting a transfer
+}
+
+void OffloadDevice::note_device_current(const std::string& name, uint64_t stamp) {
+    auto it = cache_.find(name);
+    if (it != cache_.end()) it->second.stamp = stamp;
+}
+
+SyncStats OffloadDevice::sync_stats(bool reset) {
+    SyncStats s = stats_;
+    if (reset) stats_ = {};
+    return s;
+}
+
+ExecutionContext::~ExecutionContext() { release_all(); }
+
+uint8_t* ExecutionContext::data(const std::string& name) {
+    auto it = buffers_.find(name);
+    if (it == buffers_.end()) throw Error(Error::Code::ShapeMismatch, "no live buffer " + name);
+    return it->second.ptr;
+}
+
+uint8_t* ExecutionContext::alloc(const std::string& name, int64_t bytes) {
+    if (buffers_.count(name)) throw Error(Error::Code::ArenaOverflow, "double allocation of " + name);
+    Buffer b;
+    b.bytes = bytes;
+    if (bytes > 0) {
+        void* p = nullptr;
+        NNC_CHECK(nncb_malloc(default_device().ctx(), static_cast<size_t>(bytes), &p));
+        b.ptr = static_cast<uint8_t*>(p);
+        b.owned = true;
+    }
+    adopt(name, b.ptr, bytes);
+    buffers_[name].owned = b.owned;
+    return b.ptr;
+}
+
+void ExecutionContext::adopt(const std::string& name, uint8_t* ptr, int64_t bytes) {
+    if (buffers_.count(name)) throw Error(Error::Code::ArenaOverflow, "double allocation of " + name);
+    buffers_[name] = Buffer{ptr, bytes, false};
+    current_ += bytes;
+    high_ = std::max(high_, current_);
+    if (capacity >= 0 && current_ > capacity)
+        throw Error(Error::Code::ArenaOverflow, "context capacity exceeded by " + name);
+}
+
+void ExecutionContext::release(const std::string& name) {
+    auto it = buffers_.find(name);
+    if (it == buffers_.end()) return;
+    current_ -= it->second.bytes;
+    if (it->second.owned && it->second.ptr) nncb_free(default_device().ctx(), it->second.ptr);
+    buffers_.erase(it);
+}
+
+void ExecutionContext::release_all() {
+    while (!buffers_.empty()) release(buffers_.begin()->first);
+}
+
+/* ------------------------------------------------------------------ */
 /*  execute                                                            */
 /* ------------------------------------------------------------------ */
 
@@ -1137,10 +1248,14 @@ namespace {
 
 // The bound program of `p` on `dev` with the current weights (stamp-checked
 // device cache; a changed weight pointer rebinds).
-ExecCache& bound_cache(const ExecutionPlan& p, const HostModel& model, Device& dev, const ExecOptions& opts) {
+using WeightSource = std::function<void*(const std::string&)>;
+
+ExecCache& bound_cache(const ExecutionPlan& p, const HostModel& model, Device& dev, const ExecOptions& opts,
+                       const WeightSource* weights = nullptr) {
     auto& slot = exec_caches()[{&dev, p.uid}];
     std::map<std::string, void*> wptrs;
-    for (const std::string& w : p.weight_names) wptrs[w] = dev.weight_buffer(model, w, model.tensor(w), model.stamp(w));
+    for (const std::string& w : p.weight_names)
+        wptrs[w] = weights ? (*weights)(w) : dev.weight_buffer(model, w, model.tensor(w), model.stamp(w));
     if (!slot || slot->weight_ptrs != wptrs || slot->prog->precision != opts.gemm_precision) {
         slot = std::make_unique<ExecCache>();
         slot->prog = std::make_unique<Program>();
@@ -1211,9 +1326,13 @@ std::map<std::pair<const Device*, uint64_t>, std::unique_ptr<StagedIO>>& staged_
 
 }  // namespace
 
-std::map<std::string, Tensor> execute(const ExecutionPlan& p, const std::map<std::string, Tensor>& inputs,
-                                      const HostModel& model, Device* device, const ExecOptions& opts) {
-    Device& dev = device ? *device : default_device();
+namespace {
+
+// Runs the (already specialised) plan `p`; `od` routes weights through an
+// offload cache and counts the copies.
+std::map<std::string, Tensor> run_plan(const ExecutionPlan& p, const std::map<std::string, Tensor>& inputs,
+                                       const HostModel& model, Device& dev, const ExecOptions& opts,
+                                       OffloadDevice* od, ExecutionContext* ctx_acc) {
     {
         auto it = exec_caches().find({&dev, p.uid});
         const bool reuse = opts.inputs_resident && it != exec_caches().end() && it->second && it->second->runs > 0;
@@ -1223,7 +1342,12 @@ std::map<std::string, Tensor> execute(const ExecutionPlan& p, const std::map<std
         auto it = exec_caches().find({&dev, p.uid});
         return it != exec_caches().end() && it->second && it->second->runs > 0;
     }();
-    ExecCache& c = bound_cache(p, model, dev, opts);
+    const int64_t A = std::max<int64_t>(opts.alignment, 1);
+    WeightSource via_offload = [&](const std::string& w) -> void* {
+        const Tensor& t = model.tensor(w);
+        return od->sync_weight(w, t, model.stamp(w), plan::align_bytes(static_cast<int64_t>(t.byte_size()), A));
+    };
+    ExecCache& c = bound_cache(p, model, dev, opts, od ? &via_offload : nullptr);
     Program& prog = *c.prog;
     nncb_ctx* ctx = dev.ctx();
     const bool reuse_inputs = opts.inputs_resident && had_runs && c.runs > 0;
@@ -1232,6 +1356,7 @@ std::map<std::string, Tensor> execute(const ExecutionPlan& p, const std::map<std
             const Tensor& t = inputs.at(p.values[s].name);
             NNC_CHECK(nncb_h2d(ctx, prog.ptr(p.values[s].name), t.data(), t.byte_size()));
             dev.stats().h2d_bytes += t.byte_size();
+            if (od) od->count_h2d(plan::align_bytes(static_cast<int64_t>(t.byte_size()), A));
         }
     run_bound(c, p, opts);
     std::map<std::string, Tensor> out;
@@ -1241,10 +1366,108 @@ std::map<std::string, Tensor> execute(const ExecutionPlan& p, const std::map<std
         Tensor t = Tensor::uninitialized(p.dtype, v.dims);   // the download overwrites every byte
         NNC_CHECK(nncb_d2h(ctx, t.data(), prog.ptr(v.name), t.byte_size()));
         dev.stats().d2h_bytes += t.byte_size();
+        if (od) od->count_d2h(plan::align_bytes(static_cast<int64_t>(t.byte_size()), A));
         out.emplace(v.name, std::move(t));
     }
     NNC_CHECK(nncb_sync(ctx));
+    if (ctx_acc) {
+        // the plan's alloc/free events replayed at the context's alignment
+        // (reference runtime.cpp:365-437): values carried in from an earlier
+        // plan of the same step stay; data() addresses the device buffers
+        const int64_t CA = std::max<int64_t>(ctx_acc->alignment(), 1);
+        for (const plan::PlanEvent& ev : p.events) {
+            const plan::ValueEntry& v = p.values[ev.slot];
+            if (!ev.alloc) {
+                ctx_acc->release(v.name);
+                continue;
+            }
+            if (ctx_acc->live(v.name)) continue;
+            const int64_t bytes = v.storage == StorageClass::Buffer
+                                      ? plan::align_bytes(element_count(v.dims) * static_cast<int64_t>(dtype_size(p.dtype)), CA)
+                                      : 0;
+            auto w = prog.where.find(v.name);
+            ctx_acc->adopt(v.name, w == prog.where.end() ? nullptr : static_cast<uint8_t*>(w->second), bytes);
+        }
+    }
     return out;
+}
+
+std::map<int32_t, int64_t> call_binding(const ExecutionPlan& p, const std::map<std::string, Tensor>& inputs,
+                                        const std::map<int32_t, int64_t>& explicit_bindings) {
+    // reference runtime.cpp:318-360
+    std::map<int32_t, int64_t> bindings = explicit_bindings;
+    for (uint32_t slot : p.input_slots) {
+        const plan::ValueEntry& e = p.values[slot];
+        auto fed = inputs.find(e.name);
+        if (fed == inputs.end()) continue;
+        const auto& got = fed->second.dims();
+        if (got.size() != e.dims.size())
+            throw Error(Error::Code::ShapeMismatch, e.name + ": rank " + std::to_string(got.size()) +
+                                                        ", plan expects " + std::to_string(e.dims.size()));
+        for (size_t i = 0; i < got.size(); ++i) {
+            const plan::VdimSlot* vs = nullptr;
+            for (const plan::VdimSlot& d : p.vdims)
+                if (d.slot == slot && d.axis == i) vs = &d;
+            if (!vs) {
+                if (e.dims[i] != got[i])
+                    throw Error(Error::Code::ShapeMismatch, e.name + ": axis " + std::to_string(i) + " expected " +
+                                                                std::to_string(e.dims[i]) + ", got " + std::to_string(got[i]));
+                continue;
+            }
+            auto [it, fresh] = bindings.emplace(vs->sym, got[i]);
+            if (!fresh && it->second != got[i])
+                throw Error(Error::Code::ShapeMismatch,
+                            e.name + ": conflicting extents for vdim #" + std::to_string(vs->sym));
+        }
+    }
+    for (auto it = bindings.begin(); it != bindings.end();) {   // only this plan's vdims matter
+        const bool mine = std::any_of(p.vdims.begin(), p.vdims.end(), [&](const plan::VdimSlot& d) { return d.sym == it->first; });
+        if (it->second < 1) throw Error(Error::Code::ShapeMismatch, "vdim #" + std::to_string(it->first) + " bound to " + std::to_string(it->second));
+        it = mine ? std::next(it) : bindings.erase(it);
+    }
+    return bindings;
+}
+
+bool at_compiled_extents(const ExecutionPlan& p, const std::map<int32_t, int64_t>& b) {
+    for (const plan::VdimSlot& d : p.vdims) {
+        auto it = b.find(d.sym);
+        if (it != b.end() && it->second != d.extent) return false;
+    }
+    return true;
+}
+
+}  // namespace
+
+const ExecutionPlan& plan_for_inputs(const ExecutionPlan& p, const std::map<std::string, Tensor>& inputs,
+                                     const std::map<int32_t, int64_t>& bindings) {
+    if (p.vdims.empty() || !p.spec) return p;
+    const auto b = call_binding(p, inputs, bindings);
+    if (at_compiled_extents(p, b)) return p;
+    return plan::Specializer::role_plan(p.spec->plans_for(b), p.role);
+}
+
+const plan::VersionPlans& plans_for_inputs(const plan::VersionPlans& plans, const std::map<std::string, Tensor>& inputs,
+                                           const std::map<int32_t, int64_t>& bindings) {
+    const ExecutionPlan& f = plans.train_fwd;
+    if (f.vdims.empty() || !f.spec) return plans;
+    const auto b = call_binding(f, inputs, bindings);
+    if (at_compiled_extents(f, b)) return plans;
+    return f.spec->plans_for(b);
+}
+
+std::map<std::string, Tensor> execute_on(const ExecutionPlan& p, const std::map<std::string, Tensor>& inputs,
+                                         const HostModel& model, Device* device, const ExecOptions& opts) {
+    Device& dev = device ? *device : default_device();
+    const ExecutionPlan& q = opts.inputs_resident ? p : plan_for_inputs(p, inputs, opts.bindings);
+    return run_plan(q, inputs, model, dev, opts, nullptr, nullptr);
+}
+
+std::map<std::string, Tensor> execute(const ExecutionPlan& p, const std::map<std::string, Tensor>& inputs,
+                                      const HostModel& model, OffloadDevice* device, const ExecOptions& opts,
+                                      ExecutionContext* shared_ctx) {
+    Device& dev = device ? device->device() : default_device();
+    const ExecutionPlan& q = plan_for_inputs(p, inputs, opts.bindings);
+    return run_plan(q, inputs, model, dev, opts, device, shared_ctx);
 }
 
 void execute_stage(const ExecutionPlan& p, const std::map<std::string, Tensor>& inputs, Device* device) {
@@ -1347,9 +1570,16 @@ std::map<std::string, Tensor> execute_staged_outputs(const ExecutionPlan& p, Dev
 /*  Loss and update (host-tensor API, run on the device)               */
 /* ------------------------------------------------------------------ */
 
-L1Result l1_loss(const Tensor& pred, const Tensor& target, Device* device) {
+L1Result l1_loss(const Tensor& pred, const Tensor& target) { return l1_loss_on(pred, target, nullptr); }
+
+void sgd_step(HostModel& model, const std::map<std::string, Tensor>& grads, double lr) {
+    sgd_step_on(model, grads, lr, nullptr);
+}
+
+L1Result l1_loss_on(const Tensor& pred, const Tensor& target, Device* device) {
     if (pred.dims() != target.dims() || pred.dtype() != target.dtype())
         throw Error(Error::Code::ShapeMismatch, "l1_loss: operand shapes differ");
+    if (pred.dtype() != DType::F32) throw Error(Error::Code::ShapeMismatch, "l1_loss: the device computes f32 tensors");
     Device& dev = device ? *device : default_device();
     nncb_ctx* ctx = dev.ctx();
     size_t bytes = pred.byte_size();
@@ -1371,13 +1601,15 @@ L1Result l1_loss(const Tensor& pred, const Tensor& target, Device* device) {
     return r;
 }
 
-void sgd_step(HostModel& model, const std::map<std::string, Tensor>& grads, double lr, Device* device) {
+void sgd_step_on(HostModel& model, const std::map<std::string, Tensor>& grads, double lr, Device* device) {
     Device& dev = device ? *device : default_device();
     nncb_ctx* ctx = dev.ctx();
     for (const auto& [name, g] : grads) {
         if (!model.has(name)) throw Error(Error::Code::MissingGrad, "gradient for unknown weight " + name);
         Tensor w = model.tensor(name);
         if (w.dims() != g.dims()) throw Error(Error::Code::ShapeMismatch, name + ": gradient shape mismatch");
+        if (w.dtype() != DType::F32 || g.dtype() != DType::F32)
+            throw Error(Error::Code::ShapeMismatch, name + ": the device updates f32 tensors");
         size_t bytes = w.byte_size();
         void *wd = nullptr, *gd = nullptr;
         NNC_CHECK(nncb_malloc(ctx, std::max<size_t>(bytes, 16), &wd));
@@ -1466,33 +1698,30 @@ struct Trainer::Impl {
                                static_cast<float*>(prog->ptr(dpred)), static_cast<double*>(loss), n));
         const bool comm = nncb_comm_active(ctx) != 0;
         const double scale = 1.0 / static_cast<double>(dev->nranks());
-        std::map<int64_t, std::vector<size_t>> closing, updating;
-        const int64_t nl = static_cast<int64_t>(prog->steps[1].size());
-        auto at = [&](int64_t k) { return (k < 0 || k >= nl) ? nl - 1 : k; };
-        for (size_t b = 0; b < layout.buckets.size(); ++b) {
-            if (comm) closing[at(layout.buckets[b].close_launch)].push_back(b);
-            if (do_sgd) updating[at(layout.buckets[b].update_launch)].push_back(b);
-        }
-        bool forked = false;
-        prog->enqueue_plan(1, nullptr, [&](size_t k) {
-            auto c = closing.find(static_cast<int64_t>(k));
-            auto u = updating.find(static_cast<int64_t>(k));
-            if (c == closing.end() && u == updating.end()) return;
-            NNC_CHECK(nncb_fork(ctx, NNCB_STREAM_COMM));
-            forked = true;
-            if (c != closing.end())
-                for (size_t b : c->second) {
-                    const DpBucket& bk = layout.buckets[b];
+        std::map<int64_t, std::vector<StepAction>> after;
+        for (const StepAction& a : step_schedule(layout, comm, do_sgd)) after[a.after].push_back(a);
+        auto issue = [&](const StepAction& a) {
+            switch (a.kind) {
+                case StepAction::Fork: NNC_CHECK(nncb_fork(ctx, NNCB_STREAM_COMM)); break;
+                case StepAction::Join: NNC_CHECK(nncb_join(ctx, NNCB_STREAM_COMM)); break;
+                case StepAction::AllReduce: {
+                    const DpBucket& bk = layout.buckets[a.bucket];
                     NNC_CHECK(nncb_allreduce_sum_on_comm(ctx, static_cast<float*>(grads) + bk.offset, bk.count));
+                    break;
                 }
-            if (u != updating.end())
-                for (size_t b : u->second) {
-                    const DpBucket& bk = layout.buckets[b];
+                case StepAction::Update: {
+                    const DpBucket& bk = layout.buckets[a.bucket];
                     NNC_CHECK(nncb_sgd_dev(ctx, NNCB_STREAM_COMM, static_cast<float*>(params) + bk.offset,
                                            static_cast<float*>(grads) + bk.offset, bk.count, lr_dev, scale));
+                    break;
                 }
+            }
+        };
+        prog->enqueue_plan(1, nullptr, [&](size_t k) {
+            auto it = after.find(static_cast<int64_t>(k));
+            if (it != after.end())
+                for (const StepAction& a : it->second) issue(a);
         });
-        if (forked) NNC_CHECK(nncb_join(ctx, NNCB_STREAM_COMM));
     }
 
     void sync_params() {
@@ -1585,6 +1814,27 @@ DpLayout dp_layout(const plan::VersionPlans& plans, HostModel& model, int64_t bu
         L.buckets.push_back(b);
     }
     return L;
+}
+
+std::vector<StepAction> step_schedule(const DpLayout& layout, bool comm, bool do_sgd) {
+    const int64_t last = std::max<int64_t>(layout.bwd_launches - 1, 0);
+    auto at = [&](int64_t k) { return (k < 0 || k > last) ? last : k; };
+    std::map<int64_t, std::vector<StepAction>> by;
+    for (size_t b = 0; b < layout.buckets.size(); ++b) {
+        const DpBucket& bk = layout.buckets[b];
+        if (comm) by[at(bk.close_launch)].push_back({at(bk.close_launch), StepAction::AllReduce, static_cast<int64_t>(b)});
+        if (do_sgd) by[at(bk.update_launch)].push_back({at(bk.update_launch), StepAction::Update, static_cast<int64_t>(b)});
+    }
+    std::vector<StepAction> out;
+    for (auto& [k, acts] : by) {
+        // all-reduces of a launch before its updates (a bucket's update follows
+        // its own all-reduce on the in-order comm stream)
+        std::stable_sort(acts.begin(), acts.end(), [](const StepAction& x, const StepAction& y) { return x.kind < y.kind; });
+        out.push_back({k, StepAction::Fork, -1});
+        out.insert(out.end(), acts.begin(), acts.end());
+    }
+    if (!out.empty()) out.push_back({last, StepAction::Join, -1});
+    return out;
 }
 
 Trainer::Trainer(const plan::VersionPlans& plans, HostModel& model, Device& dev, const ExecOptions& opts)
@@ -1699,6 +1949,26 @@ std::vector<Trainer::LaunchTiming> Trainer::profile_step(double lr) {
         I.dev->mark_device_newer(*I.model, w, I.model->stamp(w));
     }
     return out;
+}
+
+void Trainer::account(ExecutionContext& ctx) const {
+    // train_fwd then train_bwd events at the context's alignment, values
+    // carried across the boundary (reference train_step's shared context)
+    const int64_t CA = std::max<int64_t>(ctx.alignment(), 1);
+    for (const ExecutionPlan* p : impl->prog->plans)
+        for (const plan::PlanEvent& ev : p->events) {
+            const plan::ValueEntry& v = p->values[ev.slot];
+            if (!ev.alloc) {
+                ctx.release(v.name);
+                continue;
+            }
+            if (ctx.live(v.name)) continue;
+            const int64_t bytes = v.storage == StorageClass::Buffer
+                                      ? plan::align_bytes(element_count(v.dims) * static_cast<int64_t>(dtype_size(p->dtype)), CA)
+                                      : 0;
+            auto w = impl->prog->where.find(v.name);
+            ctx.adopt(v.name, w == impl->prog->where.end() ? nullptr : static_cast<uint8_t*>(w->second), bytes);
+        }
 }
 
 void* Trainer::input_device_ptr(const std::string& name) { return impl->prog->ptr(name); }
@@ -1854,18 +2124,51 @@ void release(const plan::VersionPlans& plans) {
         it = it->first.first == plans.train_fwd.uid ? trainers().erase(it) : std::next(it);
 }
 
-double train_step(const plan::VersionPlans& plans, const std::map<std::string, Tensor>& inputs, const Tensor& target,
-                  HostModel& model, double lr, Device* device, const ExecOptions& opts) {
+double train_step_on(const plan::VersionPlans& plans0, const std::map<std::string, Tensor>& inputs,
+                     const Tensor& target, HostModel& model, double lr, Device* device, const ExecOptions& opts) {
     Device& dev = device ? *device : default_device();
+    const plan::VersionPlans& plans = plans_for_inputs(plans0, inputs, opts.bindings);
     if (opts.trace)
         for (const char* ph : {"forward", "loss", "backward", "update"}) opts.trace->push_back(ph);
     return shared_trainer(plans, model, dev, opts).step(inputs, target, lr);
 }
 
-std::map<std::string, Tensor> gradients(const plan::VersionPlans& plans, const std::map<std::string, Tensor>& inputs,
+double train_step(const plan::VersionPlans& plans0, const std::map<std::string, Tensor>& inputs, const Tensor& target,
+                  HostModel& model, double lr, OffloadDevice* device, const ExecOptions& opts,
+                  ExecutionContext* shared_ctx) {
+    Device& dev = device ? device->device() : default_device();
+    const plan::VersionPlans& plans = plans_for_inputs(plans0, inputs, opts.bindings);
+    if (plans.inference.output_slots.size() != 1)
+        throw Error(Error::Code::BadDocument, "train_step expects exactly one prediction output");
+    const int64_t A = std::max<int64_t>(opts.alignment, 1);
+    auto aligned = [&](const Tensor& t) { return plan::align_bytes(static_cast<int64_t>(t.byte_size()), A); };
+    if (device) {
+        // the reference's cache protocol (runtime.cpp:388-397): every weight
+        // whose cached stamp is stale crosses (after an update: all of them)
+        for (const std::string& w : plans.train_fwd.weight_names)
+            (void)device->sync_weight(w, model.tensor(w), model.stamp(w), aligned(model.tensor(w)));
+        for (const auto& [k, t] : inputs) device->count_h2d(aligned(t));
+    }
+    if (opts.trace)
+        for (const char* ph : {"forward", "loss", "backward", "update"}) opts.trace->push_back(ph);
+    Trainer& tr = shared_trainer(plans, model, dev, opts);
+    const double loss = tr.step(inputs, target, lr);
+    if (device) {
+        const std::string pred = plans.inference.values[plans.inference.output_slots[0]].name;
+        device->count_d2h(aligned(target));   // the prediction (materialize = {pred})
+        device->count_h2d(aligned(target));   // d.pred into the backward plan
+        for (const auto& [w, gv] : plans.weight_grads) device->count_d2h(aligned(model.weights.at(w)));
+    }
+    model.sync();   // reference semantics: the host weights are the updated ones
+    if (shared_ctx) tr.account(*shared_ctx);
+    return loss;
+}
+
+std::map<std::string, Tensor> gradients(const plan::VersionPlans& plans0, const std::map<std::string, Tensor>& inputs,
                                         const Tensor& target, HostModel& model, double* loss, Device* device,
                                         const ExecOptions& opts) {
     Device& dev = device ? *device : default_device();
+    const plan::VersionPlans& plans = plans_for_inputs(plans0, inputs, opts.bindings);
     Trainer& tr = shared_trainer(plans, model, dev, opts);
     Trainer::Impl& I = *tr.impl;
     check_inputs(plans.train_fwd, inputs);

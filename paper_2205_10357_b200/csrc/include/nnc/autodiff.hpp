@@ -15,6 +15,7 @@
 namespace nnc::autodiff {
 
 struct VersionSet {
+    hlir::Graph source;      // the graph the versions were derived from (re-specialisation)
     hlir::Graph inference;
     hlir::Graph train_fwd;
     hlir::Graph train_bwd;

@@ -39,6 +39,10 @@ private:
     int32_t sym_id_ = -1;
 };
 
+/// Layout tag of the reference's Shape::fixed (hlir.hpp:46); this backend's
+/// tensors are NHWC / flat by construction, so the tag is accepted and ignored.
+enum class Layout : uint8_t { NHWC = 0, FLAT = 1, SCALAR = 2, RAW = 3 };
+
 struct Shape {
     std::vector<Dim> dims;
     size_t rank() const { return dims.size(); }
@@ -48,7 +52,7 @@ struct Shape {
         return o;
     }
     int64_t seed_elements() const { return element_count(seed_dims()); }
-    static Shape fixed(const std::vector<int64_t>& e) {
+    static Shape fixed(const std::vector<int64_t>& e, Layout = Layout::RAW) {
         Shape s;
         for (int64_t x : e) s.dims.push_back(Dim::fixed(x));
         return s;

@@ -14,6 +14,8 @@
 #include <cstdint>
 #include <functional>
 #include <map>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -91,6 +93,17 @@ struct ExecStep {
 
 enum class PlanRole : uint8_t { Inference = 0, TrainFwd = 1, TrainBwd = 2 };
 
+/// An enabled (dynamic) dim of a plan input (reference plan.hpp VdimSlot):
+/// vdim `sym` is axis `axis` of input value `slot`; the plan is compiled at `extent`.
+struct VdimSlot {
+    int32_t sym = 0;
+    uint32_t slot = 0;
+    uint32_t axis = 0;
+    int64_t extent = 0;
+};
+
+class Specializer;
+
 struct ExecutionPlan {
     uint64_t uid = 0;   // process-unique id (runtime caches key on it, never on addresses)
     DType dtype = DType::F32;
@@ -102,6 +115,10 @@ struct ExecutionPlan {
     std::vector<uint32_t> input_slots;
     std::vector<uint32_t> output_slots;
     std::vector<std::string> weight_names;
+    // dynamic dims: the runtime re-specialises the plan for other extents
+    // (per call, cached) through `spec`; empty for fixed-shape plans
+    std::vector<VdimSlot> vdims;
+    std::shared_ptr<const Specializer> spec;
 
     int find_value(const std::string& name) const;
     size_t launch_count() const;
@@ -123,6 +140,24 @@ struct VersionPlans {
 VersionPlans compile_version_set(
     const autodiff::VersionSet& versions,
     const std::function<backends::BackendAssignment(const hlir::Graph&)>& assign);
+
+/// Per-binding re-specialisation of plans compiled with enabled vdims: the
+/// source graph with the bound extents substituted runs through the same
+/// infer_shapes -> derive_versions -> compile_version_set pipeline once per
+/// distinct binding; the result is cached (thread-safe) for the plans' lifetime.
+class Specializer {
+public:
+    using Assign = std::function<backends::BackendAssignment(const hlir::Graph&)>;
+    Specializer(hlir::Graph source, Assign assign) : source_(std::move(source)), assign_(std::move(assign)) {}
+    const VersionPlans& plans_for(const std::map<int32_t, int64_t>& binding) const;
+    static const ExecutionPlan& role_plan(const VersionPlans& v, PlanRole r);
+
+private:
+    hlir::Graph source_;
+    Assign assign_;
+    mutable std::mutex mu_;
+    mutable std::map<std::map<int32_t, int64_t>, std::unique_ptr<VersionPlans>> cache_;
+};
 
 // Process-unique plan id (runtime caches key on it).
 uint64_t next_plan_uid();

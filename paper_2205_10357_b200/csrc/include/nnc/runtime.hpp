@@ -27,25 +27,35 @@ namespace nnc::runtime {
 
 class Device;
 
+/// Host weights with per-tensor version stamps (reference runtime.hpp:21-34):
+/// `weights` and `stamps` are public maps, as the reference's. Training keeps
+/// weights device-authoritative; tensor() (and sync()) pull a device-newer
+/// weight back before it is read, and the reference-signature train_step
+/// syncs after its update, so `weights` reads fresh there too.
 class HostModel {
 public:
     HostModel();
+    HostModel(const HostModel& o);
+    HostModel& operator=(const HostModel& o);
     uint64_t uid() const { return uid_; }
     static HostModel from_graph(const hlir::Graph& g);
-    bool has(const std::string& name) const { return weights_.count(name) != 0; }
+    bool has(const std::string& name) const { return weights.count(name) != 0; }
     const Tensor& tensor(const std::string& name) const;   // pulls if device-newer
     uint64_t stamp(const std::string& name) const;
     void set(const std::string& name, Tensor value);      // bumps the stamp
     void bump(const std::string& name);
     std::vector<std::string> names() const;
+    /// Pulls every device-newer weight back into `weights`.
+    void sync() const;
+
+    mutable std::map<std::string, Tensor> weights;
+    std::map<std::string, uint64_t> stamps;
 
     // Device-authoritative bookkeeping (B200 training).
     mutable Device* device_owner = nullptr;
     mutable std::set<std::string> device_newer;
 
 private:
-    mutable std::map<std::string, Tensor> weights_;
-    std::map<std::string, uint64_t> stamps_;
     uint64_t uid_ = 0;
 };
 
@@ -58,6 +68,7 @@ struct SyncStats {
 
 struct ExecOptions {
     int64_t alignment = 64;
+    std::map<int32_t, int64_t> bindings;            // vdim id -> extent (explicit wins)
     std::vector<std::string>* trace = nullptr;
     const std::set<std::string>* materialize = nullptr;
     bool use_graphs = true;           // capture each bound program into a CUDA graph
@@ -124,10 +135,107 @@ private:
 /// Process-wide default device (cuda:0 unless NNC_DEVICE is set).
 Device& default_device();
 
+/// The reference's offload device (runtime.hpp:40-75), on a B200: a
+/// version-stamped weight cache in device memory. sync_weight copies a weight
+/// only when its cached stamp is stale, counting h2d / weight bytes (aligned,
+/// as the reference) and per-weight transfers; execute / train_step route
+/// weights through it and count their input / output copies. Each
+/// OffloadDevice has its own cache (a fresh one re-uploads everything).
+class OffloadDevice {
+public:
+    struct CachedWeight {
+        void* device = nullptr;   // device bytes (the reference keeps a host byte vector)
+        int64_t bytes = 0;
+        uint64_t stamp = 0;
+    };
+    explicit OffloadDevice(Device* device = nullptr);
+    ~OffloadDevice();
+    OffloadDevice(const OffloadDevice&) = delete;
+    OffloadDevice& operator=(const OffloadDevice&) = delete;
+
+    uint8_t* sync_weight(const std::string& name, const Tensor& host, uint64_t stamp, int64_t aligned_bytes);
+    void count_h2d(int64_t bytes) { stats_.h2d_bytes += static_cast<uint64_t>(bytes); }
+    void count_d2h(int64_t bytes) { stats_.d2h_bytes += static_cast<uint64_t>(bytes); }
+    SyncStats sync_stats(bool reset = false);
+    /// Marks a weight as already device-resident (persisted cache state): its
+    /// bytes are placed without counting a transfer.
+    void preseed(const std::string& name, const Tensor& host, uint64_t stamp, int64_t aligned_bytes);
+    const std::map<std::string, CachedWeight>& cache() const { return cache_; }
+    /// Records that the device copy of `name` is current at `stamp` (training
+    /// updates weights on the device; nothing moves).
+    void note_device_current(const std::string& name, uint64_t stamp);
+    Device& device() const { return *dev_; }
+
+private:
+    Device* dev_;
+    std::map<std::string, CachedWeight> cache_;
+    SyncStats stats_;
+};
+
+/// Live values of a run plus exact byte accounting (reference runtime.hpp:92-121).
+/// execute / train_step replay the plan's alloc/free events into a context at
+/// its alignment, so high_water() equals the static planner's estimate
+/// (schedule::plan_timeline / training_timeline); data() is the DEVICE address
+/// of a live value. alloc() reserves device memory the context owns.
+class ExecutionContext {
+public:
+    explicit ExecutionContext(int64_t alignment = 64) : alignment_(alignment) {}
+    ~ExecutionContext();
+    ExecutionContext(const ExecutionContext&) = delete;
+    ExecutionContext& operator=(const ExecutionContext&) = delete;
+
+    int64_t current_bytes() const { return current_; }
+    int64_t high_water() const { return high_; }
+    int64_t alignment() const { return alignment_; }
+    /// Arena capacity; checked when >= 0 (ArenaOverflow).
+    int64_t capacity = -1;
+
+    bool live(const std::string& name) const { return buffers_.count(name) != 0; }
+    uint8_t* data(const std::string& name);
+    uint8_t* alloc(const std::string& name, int64_t bytes);
+    /// Accounts for an externally owned buffer (device weight cache, arena).
+    void adopt(const std::string& name, uint8_t* ptr, int64_t bytes);
+    void release(const std::string& name);
+    void release_all();
+
+private:
+    struct Buffer {
+        uint8_t* ptr = nullptr;
+        int64_t bytes = 0;
+        bool owned = false;
+    };
+    std::map<std::string, Buffer> buffers_;
+    int64_t alignment_;
+    int64_t current_ = 0;
+    int64_t high_ = 0;
+};
+
+/// Runs a plan on the B200 (reference runtime.hpp:126-130, same semantics):
+/// inputs bind free vdims (a plan compiled with an enabled vdim accepts any
+/// extent on that axis: it is re-specialised per binding, and the arena and
+/// CUDA graph are cached per binding; explicit bindings win, conflicts and
+/// fixed-axis mismatches throw ShapeMismatch); weights come from the model,
+/// through `device`'s cache when given. Returns the materialized outputs.
 std::map<std::string, Tensor> execute(const plan::ExecutionPlan& p,
                                       const std::map<std::string, Tensor>& inputs,
-                                      const HostModel& model, Device* device = nullptr,
-                                      const ExecOptions& opts = {});
+                                      const HostModel& model, OffloadDevice* device = nullptr,
+                                      const ExecOptions& opts = {},
+                                      ExecutionContext* shared_ctx = nullptr);
+
+/// B200-native execute on an explicit Device (no offload accounting).
+std::map<std::string, Tensor> execute_on(const plan::ExecutionPlan& p,
+                                         const std::map<std::string, Tensor>& inputs,
+                                         const HostModel& model, Device* device,
+                                         const ExecOptions& opts = {});
+
+/// The plan `p` specialised for the vdim binding these inputs (and explicit
+/// bindings) imply -- `p` itself when they match its compiled extents.
+const plan::ExecutionPlan& plan_for_inputs(const plan::ExecutionPlan& p,
+                                           const std::map<std::string, Tensor>& inputs,
+                                           const std::map<int32_t, int64_t>& bindings = {});
+const plan::VersionPlans& plans_for_inputs(const plan::VersionPlans& plans,
+                                           const std::map<std::string, Tensor>& inputs,
+                                           const std::map<int32_t, int64_t>& bindings = {});
 
 /// Pipelined execute from host buffers. execute_stage uploads the next run's
 /// inputs into one of two device staging slots on the copy stream (the host
@@ -143,14 +251,29 @@ void execute_launch_staged(const plan::ExecutionPlan& p, const HostModel& model,
                            const ExecOptions& opts = {});
 std::map<std::string, Tensor> execute_staged_outputs(const plan::ExecutionPlan& p, Device* device = nullptr);
 
-L1Result l1_loss(const Tensor& pred, const Tensor& target, Device* device = nullptr);
+/// Framework-side kernels (reference runtime.hpp:141-144), run on the device:
+/// loss = sum|p - t|/N in double, grad = sign(p - t)/N; w <- (float)((double)w
+/// - lr*(double)g) with the stamp bumped even at lr = 0 (F32 tensors).
+L1Result l1_loss(const Tensor& pred, const Tensor& target);
+void sgd_step(HostModel& model, const std::map<std::string, Tensor>& grads, double lr);
+L1Result l1_loss_on(const Tensor& pred, const Tensor& target, Device* device);
+void sgd_step_on(HostModel& model, const std::map<std::string, Tensor>& grads, double lr, Device* device);
 
-void sgd_step(HostModel& model, const std::map<std::string, Tensor>& grads, double lr,
-              Device* device = nullptr);
-
+/// One forward / loss / backward / update cycle (reference runtime.hpp:149-152):
+/// the whole step runs as one CUDA graph on the device (runtime::Trainer);
+/// afterwards `model.weights` holds the updated weights (stamps bumped), the
+/// four trace phases are logged, a caller-owned context carries the shared
+/// forward + backward byte accounting, and `device` (if given) counts the
+/// weight / input / loss traffic of its cache protocol.
 double train_step(const plan::VersionPlans& plans, const std::map<std::string, Tensor>& inputs,
-                  const Tensor& target, HostModel& model, double lr, Device* device = nullptr,
-                  const ExecOptions& opts = {});
+                  const Tensor& target, HostModel& model, double lr, OffloadDevice* device = nullptr,
+                  const ExecOptions& opts = {}, ExecutionContext* shared_ctx = nullptr);
+
+/// B200-native training step on an explicit Device: weights stay
+/// device-authoritative (HostModel::tensor pulls lazily).
+double train_step_on(const plan::VersionPlans& plans, const std::map<std::string, Tensor>& inputs,
+                     const Tensor& target, HostModel& model, double lr, Device* device,
+                     const ExecOptions& opts = {});
 
 /// Drops every device program / CUDA graph / trainer cached for these plans.
 // Device memory of a bound program against the static planner: arena_bytes is
@@ -200,6 +323,21 @@ struct DpLayout {
 };
 DpLayout dp_layout(const plan::VersionPlans& plans, HostModel& model, int64_t bucket_elems = int64_t(8) << 20);
 
+/// The backward half of a training step as the Trainer issues it (host-only,
+/// so the exchange / update ordering is testable without a GPU): after
+/// backward launch `after`, fork the comm stream off the compute stream,
+/// all-reduce bucket `bucket` on it (only with a communicator) and apply the
+/// bucket's SGD there once its gradients are final and no later backward
+/// launch reads its weights; the compute stream joins the comm stream after
+/// the last launch.
+struct StepAction {
+    enum Kind : int { Fork = 0, AllReduce = 1, Update = 2, Join = 3 };
+    int64_t after = -1;   // backward launch index the action follows
+    Kind kind = Fork;
+    int64_t bucket = -1;
+};
+std::vector<StepAction> step_schedule(const DpLayout& layout, bool comm, bool do_sgd);
+
 /// Device-resident training step for benchmarking: inputs/target already on the
 /// device (pointers), everything stays on the device; returns nothing (the loss
 /// is left in a device double readable with last_loss()).
@@ -231,6 +369,9 @@ struct Trainer {
     };
     std::vector<LaunchTiming> profile_step(double lr);
     void* input_device_ptr(const std::string& name);
+    /// Replays the step's alloc/free events into `ctx` (byte accounting of a
+    /// caller-owned ExecutionContext; reference train_step's shared context).
+    void account(ExecutionContext& ctx) const;
     /// Device bytes of any Buffer value of the bound step (meaningful for
     /// every value only when the trainer was built with keep_values).
     Tensor value(const std::string& name);

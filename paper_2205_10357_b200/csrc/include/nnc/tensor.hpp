@@ -38,6 +38,8 @@ public:
     Tensor() = default;
     Tensor(DType dt, std::vector<int64_t> dims);   // zero-filled (as the reference's)
     static Tensor from_f32(std::vector<int64_t> dims, std::vector<float> values);
+    static Tensor from_f64(std::vector<int64_t> dims, std::vector<double> values);
+    bool bitwise_equal(const Tensor& other) const;
     // storage left uninitialised: only for tensors fully overwritten right away
     static Tensor uninitialized(DType dt, std::vector<int64_t> dims);
 

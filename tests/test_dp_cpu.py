@@ -105,6 +105,13 @@ def test_dp_bucket_schedule_resnet():
 
 
 def _bucket_worker(rank, world, port, q):
+    """One rank of a data-parallel training step driven by the Trainer's own
+    backward schedule (runtime::step_schedule, the exact action list
+    Trainer::enqueue_step issues): walk the backward launches in order, write
+    each weight gradient at the launch that produces it (NaN poison at any
+    earlier, non-final write), check every weight a launch reads has not been
+    updated yet, and run the fork / all-reduce / update actions where the
+    schedule puts them (gloo standing in for NCCL)."""
     import torch
     import torch.distributed as dist
     import paper_2205_10357_b200 as P
@@ -113,27 +120,55 @@ def _bucket_worker(rank, world, port, q):
     doc = W.c1_small_cnn(2, bn=False)
     x = W.uniform((4, 32, 32, 3), 1, "x")[rank * 2:(rank + 1) * 2]
     t = W.uniform((4, 10), 2, "t", 0.0, 1.0)[rank * 2:(rank + 1) * 2]
-    _, grads = O.OracleModel(doc).gradients({"x": x}, t)
-    s = P.CompiledModel(doc).dp_schedule(4096)
-    region = np.zeros(s["region_elems"], np.float32)
-    for w in s["weights"]:
-        if w["grad_launch"] >= 0:
-            region[w["offset"]:w["offset"] + w["elements"]] = grads[w["name"]].ravel()
-    whole = torch.from_numpy(region.copy())
-    dist.all_reduce(whole, op=dist.ReduceOp.SUM)
-    # the overlapped schedule: each bucket reduced at its close point, in close order
-    bucketed = torch.from_numpy(region.copy())
-    for b in sorted(s["buckets"], key=lambda b: b["close_launch"]):
-        dist.all_reduce(bucketed[b["offset"]:b["offset"] + b["count"]], op=dist.ReduceOp.SUM)
+    om = O.OracleModel(doc)
+    _, grads = om.gradients({"x": x}, t)
+    s = P.CompiledModel(doc).step_schedule(4096, comm=True, sgd=True)
+    woff = {w["name"]: (w["offset"], w["elements"]) for w in s["weights"]}
+    params = np.zeros(s["region_elems"], np.float32)
+    for w, (o, n) in woff.items():
+        params[o:o + n] = om.w[w].ravel()
+    p0 = params.copy()
+    gbuf = torch.zeros(s["region_elems"], dtype=torch.float32)
+    last_write = {}
+    for k, ws in enumerate(s["launch_writes"]):
+        for w in ws:
+            last_write[w] = k
+    lr, scale = 0.05, 1.0 / world
+    updated = np.zeros(s["region_elems"], bool)
+    stale_reads = []
+    acts = {}
+    for a in s["actions"]:
+        acts.setdefault(a["after"], []).append(a)
+    for k in range(s["bwd_launches"]):
+        for w in s["launch_reads"][k]:
+            o, n = woff[w]
+            if updated[o:o + n].any():
+                stale_reads.append((k, w))
+        for w in s["launch_writes"][k]:
+            o, n = woff[w]
+            gbuf[o:o + n] = torch.from_numpy(grads[w].ravel()) if last_write[w] == k else float("nan")
+        for a in acts.get(k, []):
+            if a["kind"] == "allreduce":
+                b = s["buckets"][a["bucket"]]
+                dist.all_reduce(gbuf[b["offset"]:b["offset"] + b["count"]], op=dist.ReduceOp.SUM)
+            elif a["kind"] == "update":
+                b = s["buckets"][a["bucket"]]
+                sl = slice(b["offset"], b["offset"] + b["count"])
+                g = gbuf[sl].numpy().astype(np.float64)
+                params[sl] = (params[sl].astype(np.float64) - lr * (g * scale)).astype(np.float32)
+                updated[sl] = True
     if rank == 0:
-        q.put((s, whole.numpy(), bucketed.numpy()))
+        q.put((s, p0, params, gbuf.numpy().copy(), stale_reads))
     dist.destroy_process_group()
 
 
 @pytest.mark.skipif(not O.available(), reason="oracle/_ref/libnnc_oracle.so not built")
-def test_two_rank_bucketed_allreduce_schedule():
-    """gloo, world 2: reducing the gradient region bucket by bucket at the
-    dp_layout close points gives the same region as one all-reduce of it."""
+def test_two_rank_step_schedule_allreduce_and_update():
+    """gloo, world 2, the Trainer's backward schedule: every bucket is
+    all-reduced only after its last gradient write (no NaN poison survives),
+    no backward launch reads a weight after its bucket was updated, and the
+    updated region equals SGD of the all-reduced gradients, bit for bit
+    (w = (float)((double)w - lr*((double)g_sum * 1/G)), nncb_sgd_dev)."""
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -141,10 +176,23 @@ def test_two_rank_bucketed_allreduce_schedule():
     procs = [ctx.Process(target=_bucket_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    s, whole, bucketed = q.get(timeout=240)
+    s, p0, params, gsum, stale = q.get(timeout=240)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    _check_schedule(s, 1024)
     assert len(s["buckets"]) > 1
-    assert np.array_equal(whole, bucketed)
+    kinds = [a["kind"] for a in s["actions"]]
+    assert kinds.count("allreduce") == len(s["buckets"]) == kinds.count("update") and kinds[-1] == "join"
+    assert not stale, stale
+    assert np.isfinite(gsum).all()
+    want = (p0.astype(np.float64) - 0.05 * (gsum.astype(np.float64) * 0.5)).astype(np.float32)
+    assert np.array_equal(params, want)
+    # the global-batch equivalence of the exchanged gradients
+    doc = W.c1_small_cnn(4, bn=False)
+    m = O.OracleModel(doc)
+    _, g = m.gradients({"x": W.uniform((4, 32, 32, 3), 1, "x")}, W.uniform((4, 10), 2, "t", 0.0, 1.0))
+    for w in s["weights"]:
+        if w["name"] in g:
+            o, n = w["offset"], w["elements"]
+            ref = g[w["name"]].ravel().astype(np.float64)
+            assert np.max(np.abs(gsum[o:o + n] * 0.5 - ref)) <= 1e-5 * max(np.max(np.abs(ref)), 1e-12), w["name"]

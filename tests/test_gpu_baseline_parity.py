@@ -89,8 +89,36 @@ def check_gradients(grads, ograds, tol, skip_zero=True):
     return errs
 
 
+def total_gradient_names(model):
+    """Forward value -> the backward value holding its TOTAL gradient. The
+    autodiff names each consumer's contribution d.<v>.<op> and, for fan-out,
+    the running sums d.<v>.acc<i> (autodiff.cpp:69-78); the total is the last
+    sum, or the single contribution."""
+    d = model.describe
+    wg = set(d["weight_grads"].values())
+    bwd = [v["name"] for v in d["train_bwd"]["values"]]
+    out = {}
+    for v in d["train_fwd"]["values"]:
+        pre = "d." + v["name"] + "."
+        cands = [n for n in bwd if n.startswith(pre) and "." not in n[len(pre):] and n not in wg]
+        accs = [n for n in cands if n[len(pre):].startswith("acc")]
+        if accs:
+            out[v["name"]] = max(accs, key=lambda n: int(n[len(pre) + 3:]))
+        elif len(cands) == 1:
+            out[v["name"]] = cands[0]
+    for o in d["output_grads"]:
+        out[o[2:]] = o
+    return out
+
+
 def device_reader(model):
+    totals = total_gradient_names(model)
+
     def value(name):
+        if name.startswith("d."):
+            name = totals.get(name[2:])
+            if name is None:
+                return None
         try:
             return model.step_value(name)
         except P.NNCError:
