@@ -135,6 +135,10 @@ int nnc_init_comm(int nranks, int rank, const uint8_t id[128]);
  * default assignment (policy 0) or an explicit {"node": backend_int} JSON map
  * (assignment_json != NULL). Returns JSON [[members...], ...]. */
 const char* nnc_group_document(const char* dlb_document, const char* assignment_json);
+/* backends::group_layers with the B200 default assignment on one role graph
+ * of the document's version set (0 inference, 1 train_fwd, 2 train_bwd), as
+ * JSON [{"backend": int, "members": [...]}]. NULL on error.                */
+const char* nnc_group_document_role(const char* doc, int role);
 
 #ifdef __cplusplus
 }

@@ -30,6 +30,9 @@
 #include "nnc/plan.hpp"
 #include "nnc/runtime.hpp"
 #include "nnc/schedule.hpp"
+#include "oracles.hpp"
+
+#include <json.hpp>
 
 using namespace nnc;  // == nncref via -Dnnc=nncref
 
@@ -326,6 +329,31 @@ double ref_init_uniform(uint64_t seed, const char* name, int64_t index, double l
     double v = 0;
     for (int64_t i = 0; i <= index; ++i) v = s.uniform(lo, hi);
     return v;
+}
+
+// The reference harness's partition oracles (tests/harness/oracle_groups.cpp:
+// 117-150) applied to a partition of one role graph of the document's version
+// set: bit 0 = oracle_valid_partition, bit 1 = oracle_maximal_partition; -1 on
+// error. partition_json: [{"backend": int, "members": [...]}] (any backend ids).
+int ref_check_partition(const char* doc, int role, const char* partition_json) {
+    int result = 0;
+    int rc = guarded([&] {
+        auto model = ingest::parse_model(doc);
+        auto g = passes::optimize(model.graph).graph;
+        auto vs = autodiff::derive_versions(g);
+        const hlir::Graph& rg = role == 2 ? vs.train_bwd : role == 1 ? vs.train_fwd : vs.inference;
+        auto j = nlohmann::json::parse(partition_json);
+        std::map<std::string, int> backend_of;
+        testing::Partition part;
+        for (const auto& grp : j) {
+            std::vector<std::string> members = grp.at("members").get<std::vector<std::string>>();
+            for (const auto& m : members) backend_of[m] = grp.at("backend").get<int>();
+            part.push_back(members);
+        }
+        result = (testing::oracle_valid_partition(rg, backend_of, part) ? 1 : 0) |
+                 (testing::oracle_maximal_partition(rg, backend_of, part) ? 2 : 0);
+    });
+    return rc ? -1 : result;
 }
 
 }  // extern "C"

@@ -40,6 +40,7 @@ def lib():
             ("ref_set_weight", I, [P, S, DP, I64]), ("ref_grads", I, [P, DP, I64P, I, DP]),
             ("ref_grad", I, [P, S, DP, I64]), ("ref_train_step", I, [P, DP, I64P, I, D, DP]),
             ("ref_group_document", S, [S, I]),
+            ("ref_check_partition", I, [S, I, S]),
             ("ref_init_uniform", D, [ctypes.c_uint64, S, I64, D, D]),
         ]:
             fn = getattr(l, name)
@@ -148,6 +149,16 @@ def group_document(document: str, policy: int):
     if res is None:
         raise RuntimeError(_err())
     return json.loads(res.decode())
+
+
+def check_partition(document: str, role: int, groups) -> dict:
+    """The reference harness's oracle_valid_partition / oracle_maximal_partition
+    (tests/harness/oracle_groups.cpp:117-150) on one role graph
+    (0 inference, 1 train_fwd, 2 train_bwd) of the document's version set."""
+    r = lib().ref_check_partition(document.encode(), role, json.dumps(groups).encode())
+    if r < 0:
+        raise RuntimeError(_err())
+    return {"valid": bool(r & 1), "maximal": bool(r & 2)}
 
 
 def init_uniform(seed: int, name: str, index: int, lo: float, hi: float) -> float:

@@ -104,6 +104,7 @@ def _load():
         "nnc_comm_unique_id": (I, [ctypes.c_char_p]),
         "nnc_init_comm": (I, [I, I, ctypes.c_char_p]),
         "nnc_group_document": (S, [S, S]),
+        "nnc_group_document_role": (S, [S, I]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(host, name)
@@ -164,6 +165,16 @@ def group_document(document: str, assignment: Optional[Dict[str, int]] = None):
     """backends::group_layers on the optimized inference graph of a DLB document."""
     res = _host.nnc_group_document(document.encode(),
                                    json.dumps(assignment).encode() if assignment is not None else None)
+    if res is None:
+        raise NNCError(_host.nnc_last_status(), _host.nnc_last_error().decode())
+    return json.loads(res.decode())
+
+
+def group_document_role(document: str, role: str = "train_bwd"):
+    """The B200 partition (backends::group_layers, default assignment) of one
+    role graph of the document's version set: [{"backend", "members"}]."""
+    r = {"inference": 0, "train_fwd": 1, "train_bwd": 2}[role]
+    res = _host.nnc_group_document_role(document.encode(), r)
     if res is None:
         raise NNCError(_host.nnc_last_status(), _host.nnc_last_error().decode())
     return json.loads(res.decode())

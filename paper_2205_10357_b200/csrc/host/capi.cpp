@@ -560,4 +560,18 @@ const char* nnc_group_document(const char* doc, const char* assignment_json) {
     return rc ? nullptr : g_buf.c_str();
 }
 
+const char* nnc_group_document_role(const char* doc, int role) {
+    int rc = guarded([&] {
+        auto model = ingest::parse_model(doc);
+        auto g = passes::optimize(model.graph).graph;
+        auto vs = autodiff::derive_versions(g);
+        const hlir::Graph& rg = role == 2 ? vs.train_bwd : role == 1 ? vs.train_fwd : vs.inference;
+        nlohmann::json out = nlohmann::json::array();
+        for (const auto& fg : backends::group_layers(rg, backends::default_assignment(rg)))
+            out.push_back({{"backend", static_cast<int>(fg.backend)}, {"members", fg.members}});
+        g_buf = out.dump();
+    });
+    return rc ? nullptr : g_buf.c_str();
+}
+
 }  // extern "C"

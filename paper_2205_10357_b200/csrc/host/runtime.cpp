@@ -955,6 +955,16 @@ HostModel::HostModel() {
 
 HostModel::HostModel(const HostModel& o) : HostModel() { *this = o; }
 
+void forget_trainers_of(uint64_t model_uid);   // (below, with the trainer cache)
+
+HostModel::~HostModel() {
+    try {
+        forget_trainers_of(uid_);
+        if (device_owner) device_owner->forget_model(uid_);
+    } catch (...) {
+    }
+}
+
 HostModel& HostModel::operator=(const HostModel& o) {
     if (this == &o) return *this;
     o.sync();   // a copy is a value: device-newer weights come with it
@@ -1081,6 +1091,17 @@ void Device::evict_model(HostModel& m) {
         (void)m.tensor(name);   // pulls and clears device_newer
     for (auto it = cache_.begin(); it != cache_.end();) {
         if (it->first.first != m.uid()) {
+            ++it;
+            continue;
+        }
+        if (!it->second.external && it->second.ptr) nncb_free(ctx_, it->second.ptr);
+        it = cache_.erase(it);
+    }
+}
+
+void Device::forget_model(uint64_t model_uid) {
+    for (auto it = cache_.begin(); it != cache_.end();) {
+        if (it->first.first != model_uid) {
             ++it;
             continue;
         }
@@ -1660,9 +1681,14 @@ struct Trainer::Impl {
     double* loss_host = nullptr;          // pinned
     void* loss_ev = nullptr;
 
+    bool model_dying = false;
+
     ~Impl() {
         try {
-            dev->evict_model(*model);   // device-newer weights back to the host before the region goes
+            if (!model_dying)
+                dev->evict_model(*model);   // device-newer weights back to the host before the region goes
+            else
+                dev->forget_model(model->uid());
         } catch (...) {
         }
         if (graph) nncb_graph_destroy(graph);
@@ -2107,6 +2133,17 @@ std::map<std::pair<uint64_t, uint64_t>, std::unique_ptr<Trainer>>& trainers() {
     return m;
 }
 }  // namespace
+
+void forget_trainers_of(uint64_t model_uid) {
+    for (auto it = trainers().begin(); it != trainers().end();) {
+        if (it->first.second != model_uid) {
+            ++it;
+            continue;
+        }
+        if (it->second) it->second->impl->model_dying = true;
+        it = trainers().erase(it);
+    }
+}
 
 Trainer& shared_trainer(const plan::VersionPlans& plans, HostModel& model, Device& dev, const ExecOptions& opts) {
     auto& t = trainers()[{plans.train_fwd.uid, model.uid()}];

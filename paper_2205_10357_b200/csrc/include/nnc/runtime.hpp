@@ -37,6 +37,9 @@ public:
     HostModel();
     HostModel(const HostModel& o);
     HostModel& operator=(const HostModel& o);
+    /// Drops the runtime state tied to this model (its cached trainers and
+    /// device weight copies) -- a HostModel may die before the plans it ran.
+    ~HostModel();
     uint64_t uid() const { return uid_; }
     static HostModel from_graph(const hlir::Graph& g);
     bool has(const std::string& name) const { return weights.count(name) != 0; }
@@ -114,6 +117,8 @@ public:
     void adopt_weight(const HostModel& m, const std::string& name, void* ptr, size_t bytes, uint64_t stamp);
     /// Pulls device-newer weights of `m` back to the host and drops its cache entries.
     void evict_model(HostModel& m);
+    /// Drops the cache entries of a model that is being destroyed (no pull).
+    void forget_model(uint64_t model_uid);
     uint64_t cached_stamp(const HostModel& m, const std::string& name) const;
     std::map<const void*, std::unique_ptr<Program>>& programs() { return programs_; }
     SyncStats& stats() { return stats_; }

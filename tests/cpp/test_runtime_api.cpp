@@ -9,6 +9,10 @@
 //   ExecutionContext high water == estimate    test_runtime.cpp:195-240
 //   training loop: converge, trace, lr = 0     test_runtime.cpp:242-287
 //   enabled batch dim (VdimBinding::enable)    test_runtime.cpp:289-303
+#include <execinfo.h>
+#include <signal.h>
+#include <unistd.h>
+
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -268,7 +272,18 @@ void enabled_batch_dim() {
 
 }  // namespace
 
+void on_fatal(int sig) {
+    void* frames[64];
+    const int n = backtrace(frames, 64);
+    std::fprintf(stderr, "fatal signal %d; backtrace:\n", sig);
+    backtrace_symbols_fd(frames, n, STDERR_FILENO);
+    _exit(128 + sig);
+}
+
 int main() {
+    setvbuf(stdout, nullptr, _IONBF, 0);
+    signal(SIGSEGV, on_fatal);
+    signal(SIGABRT, on_fatal);
     struct Case {
         const char* name;
         void (*fn)();
@@ -281,6 +296,7 @@ int main() {
         {"enabled batch dim: any batch accepted, fixed axes enforced", enabled_batch_dim},
     };
     for (const Case& c : cases) {
+        std::printf("[ RUN ] %s\n", c.name);
         const int before = g_failures;
         try {
             c.fn();

@@ -173,3 +173,21 @@ def test_importing_package_helpers_maps_no_native_library():
             "m = open('/proc/self/maps').read()\n"
             "assert 'libnncb.so' in m and 'libnnc_b200.so' in m\n") % ROOT
     subprocess.run([os.sys.executable, "-c", code], check=True)
+
+
+@pytest.mark.parametrize("name", sorted(DOCS))
+@pytest.mark.parametrize("role", ["inference", "train_fwd", "train_bwd"])
+def test_partitions_pass_reference_harness_oracles(ref, name, role):
+    """the B200 grouping of every role graph -- backward graphs
+    included, whose gradient ops the reference's GEMM_TILED rejects, so no
+    reference group_layers run exists to compare with -- satisfies the
+    reference harness's partition oracles: a valid partition (convex,
+    connected, single-backend groups covering every compute node exactly once)
+    that is maximal (no two adjacent same-backend groups could merge)."""
+    doc = DOCS[name]()
+    groups = P.group_document_role(doc, role)
+    # (the weight-free chain's backward graph is empty: graph-input gradients are
+    # dead code, autodiff.cpp:226-234)
+    assert groups or (name == "chain" and role == "train_bwd")
+    verdict = ref.check_partition(doc, {"inference": 0, "train_fwd": 1, "train_bwd": 2}[role], groups)
+    assert verdict == {"valid": True, "maximal": True}, (role, verdict)
