@@ -86,6 +86,9 @@ int nnc_model_grad(nnc_model* m, const char* weight, float* out, int64_t n);
  * NULL returns only dims/rank). Not for production: the arena grows to the
  * sum of all values. Values living in fused-group registers have no bytes.  */
 int nnc_model_debug_keep_values(nnc_model* m, int on);
+/* Training loss of the model's steps: 0 = L1 (the reference's), 1 = softmax
+ * cross-entropy over the prediction's last axis (targets: probability rows). */
+int nnc_model_set_loss(nnc_model* m, int kind);
 int nnc_model_trainer_value(nnc_model* m, const char* name, float* out, int64_t n, int64_t* dims, int* rank);
 
 /* Data-parallel layout (runtime::dp_layout) as JSON: region order, ~bucket_bytes

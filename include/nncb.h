@@ -233,6 +233,16 @@ int nncb_gemm_last_path(void);
 int nncb_gemm_set_manual_a(int on);
 /* Forces the tcgen05 tile: N width (64/128/256) | (1 << 16) for CTA pairs (cta_group::2); 0 = autotune. */
 int nncb_gemm_force_tile(int code);
+/* GEMM tile choices per shape (they fix the fp32 accumulation order). By
+ * default the choice is deterministic: the committed per-shape table
+ * (kernels/tile_table.inc, tools/tune_tiles.py) plus imported entries, else a
+ * static rule; NNCB_TC_AUTOTUNE=live measures unknown shapes on first use
+ * (on a scratch output). Export/import one "key choice" line per shape, so a
+ * tuned deployment can persist and reload its choices. Mode: 0 static,
+ * 1 table (default), 2 live.                                                */
+int nncb_gemm_tuning_export(char* buf, size_t cap, size_t* needed);
+int nncb_gemm_tuning_import(const char* text);
+int nncb_gemm_tuning_mode(void);
 int nncb_gemm(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b,
               const float* bias, float* out);
 
@@ -287,6 +297,12 @@ int nncb_layernorm_dgamma(nncb_ctx* ctx, const float* x, const float* g, float* 
 /* grad = sign(p - t)/N (sign(0)=0), *loss_dev (double, device) = sum|p-t|/N */
 int nncb_l1_loss(nncb_ctx* ctx, const float* pred, const float* target, float* grad,
                  double* loss_dev, int64_t n);
+/* Softmax cross-entropy over the last axis of logits [rows, C] with
+ * probability-vector targets (extension loss; the reference has only L1):
+ * *loss_dev = -(1/rows) sum_r sum_c t log softmax(z)_c, computed in double;
+ * grad = (softmax(z) - t)/rows. Deterministic (fixed reduction order).     */
+int nncb_softmax_ce(nncb_ctx* ctx, const float* logits, const float* target, float* grad, double* loss_dev,
+                    int64_t rows, int64_t C);
 /* Flat-buffer SGD over the whole parameter region (weights and gradients share
  * one layout): w = (float)((double)w - lr*((double)g*grad_scale)). With
  * grad_scale = 1 this is bit-identical to runtime::sgd_step (runtime.cpp:493). */

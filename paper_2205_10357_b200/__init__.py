@@ -79,6 +79,7 @@ def _load():
         "nnc_model_gradients": (I, [P, FP, I64, DP]),
         "nnc_model_grad": (I, [P, S, FP, I64]),
         "nnc_model_debug_keep_values": (I, [P, I]),
+        "nnc_model_set_loss": (I, [P, I]),
         "nnc_model_trainer_value": (I, [P, S, FP, I64, I64P, ctypes.POINTER(ctypes.c_int)]),
         "nnc_model_trainer_prepare": (I, [P, FP, I64]),
         "nnc_model_trainer_step_device": (I, [P, D]),
@@ -184,14 +185,18 @@ class CompiledModel:
     """A document compiled through optimize -> derive_versions -> compile_version_set,
     holding its HostModel (weights + stamps) on the B200 runtime."""
 
-    def __init__(self, document: str, precision: int = PREC_TF32, dynamic_vdims: Sequence[int] = ()):
+    def __init__(self, document: str, precision: int = PREC_TF32, dynamic_vdims: Sequence[int] = (),
+                 loss: str = "l1"):
         """dynamic_vdims: free vdims (#k) of the document to enable
-        (passes::VdimBinding::enable) -- e.g. (0,) for a dynamic batch."""
+        (passes::VdimBinding::enable) -- e.g. (0,) for a dynamic batch.
+        loss: "l1" (the reference's) or "softmax_ce" (targets are probability rows)."""
         ids = (ctypes.c_int32 * max(len(dynamic_vdims), 1))(*dynamic_vdims)
         h = _host.nnc_model_compile_ex(document.encode(), precision, ids, len(dynamic_vdims))
         if not h:
             raise NNCError(_host.nnc_last_status(), _host.nnc_last_error().decode())
         self._h = h
+        if loss != "l1":
+            _check(_host.nnc_model_set_loss(h, {"l1": 0, "softmax_ce": 1}[loss]))
         self.describe = json.loads(_host.nnc_model_describe(h).decode())
         self.weight_shapes = {k: tuple(v) for k, v in self.describe["weights"].items()}
         inf = self.describe["inference"]

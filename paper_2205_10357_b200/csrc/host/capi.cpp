@@ -342,6 +342,16 @@ int nnc_model_gradients(nnc_model* m, const float* target, int64_t n, double* lo
     return rc;
 }
 
+int nnc_model_set_loss(nnc_model* m, int kind) {
+    return guarded([&] {
+        if (kind != runtime::LOSS_L1 && kind != runtime::LOSS_SOFTMAX_CE)
+            throw Error(Error::Code::BadDocument, "unknown loss kind " + std::to_string(kind));
+        runtime::release(m->plans);   // trainers are bound with their loss
+        m->trainer = nullptr;
+        m->opts.loss = kind;
+    });
+}
+
 int nnc_model_debug_keep_values(nnc_model* m, int on) {
     return guarded([&] {
         runtime::release(m->plans);   // the next training call binds afresh

@@ -1622,6 +1622,32 @@ L1Result l1_loss_on(const Tensor& pred, const Tensor& target, Device* device) {
     return r;
 }
 
+L1Result softmax_ce_loss(const Tensor& pred, const Tensor& target, Device* device) {
+    if (pred.dims() != target.dims() || pred.dtype() != target.dtype() || pred.dims().empty())
+        throw Error(Error::Code::ShapeMismatch, "softmax_ce_loss: operand shapes differ");
+    if (pred.dtype() != DType::F32) throw Error(Error::Code::ShapeMismatch, "softmax_ce_loss: the device computes f32 tensors");
+    Device& dev = device ? *device : default_device();
+    nncb_ctx* ctx = dev.ctx();
+    const size_t bytes = pred.byte_size();
+    void *p = nullptr, *t = nullptr, *g = nullptr, *loss = nullptr;
+    NNC_CHECK(nncb_malloc(ctx, std::max<size_t>(bytes, 16), &p));
+    NNC_CHECK(nncb_malloc(ctx, std::max<size_t>(bytes, 16), &t));
+    NNC_CHECK(nncb_malloc(ctx, std::max<size_t>(bytes, 16), &g));
+    NNC_CHECK(nncb_malloc(ctx, 16, &loss));
+    NNC_CHECK(nncb_h2d(ctx, p, pred.data(), bytes));
+    NNC_CHECK(nncb_h2d(ctx, t, target.data(), bytes));
+    const int64_t C = pred.dims().back();
+    NNC_CHECK(nncb_softmax_ce(ctx, static_cast<float*>(p), static_cast<float*>(t), static_cast<float*>(g),
+                              static_cast<double*>(loss), pred.elements() / C, C));
+    L1Result r;
+    r.grad = Tensor(pred.dtype(), pred.dims());
+    NNC_CHECK(nncb_d2h(ctx, r.grad.data(), g, bytes));
+    NNC_CHECK(nncb_d2h(ctx, &r.loss, loss, sizeof(double)));
+    NNC_CHECK(nncb_sync(ctx));
+    for (void* b : {p, t, g, loss}) nncb_free(ctx, b);
+    return r;
+}
+
 void sgd_step_on(HostModel& model, const std::map<std::string, Tensor>& grads, double lr, Device* device) {
     Device& dev = device ? *device : default_device();
     nncb_ctx* ctx = dev.ctx();
@@ -1719,9 +1745,7 @@ struct Trainer::Impl {
     void enqueue_step(bool do_sgd) {
         nncb_ctx* ctx = dev->ctx();
         prog->enqueue_plan(0, nullptr);
-        int64_t n = element_count(plans->train_fwd.values[plans->train_fwd.find_value(pred)].dims);
-        NNC_CHECK(nncb_l1_loss(ctx, static_cast<float*>(prog->ptr(pred)), static_cast<float*>(target),
-                               static_cast<float*>(prog->ptr(dpred)), static_cast<double*>(loss), n));
+        enqueue_loss();
         const bool comm = nncb_comm_active(ctx) != 0;
         const double scale = 1.0 / static_cast<double>(dev->nranks());
         std::map<int64_t, std::vector<StepAction>> after;
@@ -1748,6 +1772,21 @@ struct Trainer::Impl {
             if (it != after.end())
                 for (const StepAction& a : it->second) issue(a);
         });
+    }
+
+    /// The loss launch(es): prediction + target -> d.pred and the device loss.
+    void enqueue_loss() {
+        nncb_ctx* ctx = dev->ctx();
+        const auto& pd = plans->train_fwd.values[plans->train_fwd.find_value(pred)].dims;
+        const int64_t n = element_count(pd);
+        if (opts.loss == LOSS_SOFTMAX_CE) {
+            const int64_t C = pd.empty() ? 1 : pd.back();
+            NNC_CHECK(nncb_softmax_ce(ctx, static_cast<float*>(prog->ptr(pred)), static_cast<float*>(target),
+                                      static_cast<float*>(prog->ptr(dpred)), static_cast<double*>(loss), n / C, C));
+        } else {
+            NNC_CHECK(nncb_l1_loss(ctx, static_cast<float*>(prog->ptr(pred)), static_cast<float*>(target),
+                                   static_cast<float*>(prog->ptr(dpred)), static_cast<double*>(loss), n));
+        }
     }
 
     void sync_params() {
@@ -1953,10 +1992,10 @@ std::vector<Trainer::LaunchTiming> Trainer::profile_step(double lr) {
         }
         if (pi == 0) {
             int64_t n = element_count(I.plans->train_fwd.values[I.plans->train_fwd.find_value(I.pred)].dims);
-            NNC_CHECK(nncb_l1_loss(ctx, static_cast<float*>(I.prog->ptr(I.pred)), static_cast<float*>(I.target),
-                                   static_cast<float*>(I.prog->ptr(I.dpred)), static_cast<double*>(I.loss), n));
+            I.enqueue_loss();
             ev();
-            out.push_back({"l1_loss", "l1_loss", 0, 12.0 * n, 0});
+            const char* lk = I.opts.loss == LOSS_SOFTMAX_CE ? "softmax_ce_loss" : "l1_loss";
+            out.push_back({lk, lk, 0, 12.0 * n, 0});
         }
     }
     NNC_CHECK(nncb_sgd(ctx, static_cast<float*>(I.params), static_cast<float*>(I.grads), I.region_elems, lr,

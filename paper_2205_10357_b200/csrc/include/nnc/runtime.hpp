@@ -83,7 +83,13 @@ struct ExecOptions {
     // arena bytes (no reuse), so after a step every forward and backward
     // value can be read back (Trainer::value) and checked launch by launch
     bool keep_values = false;
+    // the training loss: L1 (the reference's, runtime.cpp:468-483) or softmax
+    // cross-entropy over the prediction's last axis (extension; targets are
+    // probability vectors)
+    int loss = 0;   // LossKind
 };
+
+enum LossKind : int { LOSS_L1 = 0, LOSS_SOFTMAX_CE = 1 };
 
 struct L1Result {
     double loss = 0;
@@ -262,6 +268,9 @@ std::map<std::string, Tensor> execute_staged_outputs(const plan::ExecutionPlan& 
 L1Result l1_loss(const Tensor& pred, const Tensor& target);
 void sgd_step(HostModel& model, const std::map<std::string, Tensor>& grads, double lr);
 L1Result l1_loss_on(const Tensor& pred, const Tensor& target, Device* device);
+/// Softmax cross-entropy (extension loss) with the same result layout: loss
+/// = -(1/rows) sum t log softmax(pred) over the last axis, grad = (softmax - t)/rows.
+L1Result softmax_ce_loss(const Tensor& pred, const Tensor& target, Device* device = nullptr);
 void sgd_step_on(HostModel& model, const std::map<std::string, Tensor>& grads, double lr, Device* device);
 
 /// One forward / loss / backward / update cycle (reference runtime.hpp:149-152):

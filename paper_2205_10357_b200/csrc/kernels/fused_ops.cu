@@ -866,6 +866,60 @@ __global__ void l1_final_k(const double* __restrict__ partial, int blocks, int64
     *loss = s * (n > 0 ? 1.0 / (double)n : 0.0);
 }
 
+// Softmax cross-entropy over the last axis (extension loss; CPU restatement
+// oracle/restated64.py softmax_ce): per row r of logits z[r, 0:C] with
+// probability-vector targets t, loss_r = -sum_c t_c (z_c - m - log s),
+// s = sum_c exp(z_c - m), m = max_c z_c, and grad = (exp(z - m)/s - t)/rows.
+// One CTA per row; the row's max, exp-sum and loss are reduced in double in a
+// fixed tree (deterministic), the rows' losses summed in order by one thread.
+template <int THREADS>
+__device__ __forceinline__ double block_reduce_d(double v, double* sh, bool is_max) {
+    for (int o = 16; o; o >>= 1) {
+        const double u = __shfl_xor_sync(0xffffffffu, v, o);
+        v = is_max ? fmax(v, u) : v + u;
+    }
+    __syncthreads();
+    if (threadIdx.x % 32 == 0) sh[threadIdx.x / 32] = v;
+    __syncthreads();
+    double r = sh[0];
+    for (int k = 1; k < THREADS / 32; ++k) r = is_max ? fmax(r, sh[k]) : r + sh[k];
+    return r;
+}
+
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) softmax_ce_row_k(const float* __restrict__ z, const float* __restrict__ t,
+                                                             float* __restrict__ grad, double* __restrict__ row_loss,
+                                                             int64_t C, double inv_rows) {
+    __shared__ double sh[THREADS / 32];
+    const int64_t r = blockIdx.x;
+    const float* zr = z + r * C;
+    const float* tr = t + r * C;
+    double m = -INFINITY;
+    for (int64_t c = threadIdx.x; c < C; c += THREADS) m = fmax(m, (double)zr[c]);
+    m = block_reduce_d<THREADS>(m, sh, true);
+    double se = 0, tz = 0, ts = 0;
+    for (int64_t c = threadIdx.x; c < C; c += THREADS) {
+        const double d = (double)zr[c] - m;
+        se += exp(d);
+        tz += (double)tr[c] * d;
+        ts += (double)tr[c];
+    }
+    se = block_reduce_d<THREADS>(se, sh, false);
+    tz = block_reduce_d<THREADS>(tz, sh, false);
+    ts = block_reduce_d<THREADS>(ts, sh, false);
+    const double ls = log(se);
+    for (int64_t c = threadIdx.x; c < C; c += THREADS)
+        grad[r * C + c] = (float)((exp((double)zr[c] - m) / se - (double)tr[c]) * inv_rows);
+    if (threadIdx.x == 0) row_loss[r] = ts * ls - tz;   // -sum t (d - log s)
+}
+
+__global__ void softmax_ce_final_k(const double* __restrict__ row_loss, int64_t rows, double* __restrict__ loss) {
+    if (threadIdx.x != 0) return;
+    double s = 0;
+    for (int64_t r = 0; r < rows; ++r) s += row_loss[r];
+    *loss = rows > 0 ? s / (double)rows : 0.0;
+}
+
 // (float)((double)w - lr*(double)g) with separately rounded double ops, exactly
 // runtime.cpp:493 (no FMA contraction).
 __device__ __forceinline__ float sgd1(float w, float g, double lr, double scale) {
@@ -1091,6 +1145,19 @@ int nncb_l1_loss(nncb_ctx* ctx, const float* pred, const float* target, float* g
     l1_k<<<blocks, threads, 0, ctx->stream>>>(pred, target, grad, partial, n);
     NNCB_LAUNCHED(ctx);
     l1_final_k<<<1, 32, 0, ctx->stream>>>(partial, (int)blocks, n, loss_dev);
+    NNCB_LAUNCHED(ctx);
+    return 0;
+}
+
+int nncb_softmax_ce(nncb_ctx* ctx, const float* logits, const float* target, float* grad, double* loss_dev,
+                    int64_t rows, int64_t C) {
+    if (rows <= 0 || C <= 0) return nncb::fail("nncb_softmax_ce: empty logits");
+    if (rows > (int64_t(1) << 31) - 1) return nncb::fail("nncb_softmax_ce: too many rows");
+    double* row_loss = static_cast<double*>(nncb::scratch(ctx, sizeof(double) * static_cast<size_t>(rows)));
+    if (!row_loss) return nncb::fail("softmax_ce: scratch allocation failed");
+    softmax_ce_row_k<256><<<(unsigned)rows, 256, 0, ctx->stream>>>(logits, target, grad, row_loss, C, 1.0 / (double)rows);
+    NNCB_LAUNCHED(ctx);
+    softmax_ce_final_k<<<1, 32, 0, ctx->stream>>>(row_loss, rows, loss_dev);
     NNCB_LAUNCHED(ctx);
     return 0;
 }

@@ -1829,17 +1829,67 @@ std::atomic<int> g_forced_tile{0};   // nncb_gemm_force_tile: width | pair << 16
 int gemm_tc_route(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const float* bias,
                   float* out, bool* handled);
 
-// Measured tile selection: the first time a GEMM shape is seen outside stream
-// capture, each candidate N-tile width is run and timed with CUDA events on
-// the context's stream (the output is simply rewritten), and the fastest is
-// remembered for the shape. 128-wide tiles (two CTAs per SM) win for some
-// layers and 256-wide (one CTA, half the A re-reads) for others; no static
-// rule separates them. NNCB_TC_AUTOTUNE=0 keeps the static choice.
+// Tile selection. The choice (N-tile width, CTA pair, staging width, K-major
+// weights, halo patches) changes the fp32 accumulation order, so it must be a
+// function of the GEMM shape alone for results to be reproducible across
+// processes and boxes. Modes (NNCB_TC_AUTOTUNE):
+//   unset / "table"  deterministic: the committed per-shape table
+//                    (tile_table.inc, produced by tools/tune_tiles.py from live
+//                    measurements on a B200), plus entries imported with
+//                    nncb_gemm_tuning_import; shapes not in it take the static
+//                    rule. No timing, ever.
+//   "live" / "1"     shapes not in the table are measured on first use outside
+//                    capture: each candidate runs on a SCRATCH output (the
+//                    caller's output and side inputs are never rewritten) and is
+//                    timed with CUDA events; the fastest is remembered.
+//                    nncb_gemm_tuning_export dumps the table.
+//   "0"              the static rule only.
+namespace {
+struct TileEntry {
+    const char* key;
+    int choice;
+};
+const TileEntry kTileTable[] = {
+#include "tile_table.inc"
+    {nullptr, 0},
+};
+int tune_mode() {
+    static const int m = [] {
+        const char* e = getenv("NNCB_TC_AUTOTUNE");
+        if (!e || !strcmp(e, "table")) return 1;
+        if (!strcmp(e, "0")) return 0;
+        return 2;   // live
+    }();
+    return m;
+}
+std::mutex g_tune_mu;
+std::map<std::string, int>& tuned_table() {
+    static std::map<std::string, int> t = [] {
+        std::map<std::string, int> m;
+        for (const TileEntry& e : kTileTable)
+            if (e.key) m[e.key] = e.choice;
+        return m;
+    }();
+    return t;
+}
+size_t gemm_out_elems(const nncb_gemm_desc* d) {
+    switch (d->kind) {
+        case NNCB_DENSE_FWD: return (size_t)(d->batch * d->out_f);
+        case NNCB_DENSE_DGRAD: return (size_t)(d->batch * d->in_f);
+        case NNCB_DENSE_WGRAD: return (size_t)(d->in_f * d->out_f);
+        case NNCB_CONV_FWD: return (size_t)(d->n * d->oh * d->ow * d->co);
+        case NNCB_CONV_DGRAD: return (size_t)(d->n * d->ih * d->iw * d->ci);
+        default: return (size_t)(d->kh * d->kw * d->ci * d->co);
+    }
+}
+}  // namespace
+
 int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const float* bias, float* out,
             bool* handled) {
-    static const bool enabled = !(getenv("NNCB_TC_AUTOTUNE") && atoi(getenv("NNCB_TC_AUTOTUNE")) == 0);
-    static std::mutex mu;
-    static std::map<std::string, int> tuned;
+    const int mode = tune_mode();
+    const bool enabled = mode == 2;
+    std::mutex& mu = g_tune_mu;
+    std::map<std::string, int>& tuned = tuned_table();
     const bool dense = d->kind <= NNCB_DENSE_WGRAD;
     const int64_t N = d->kind == NNCB_DENSE_DGRAD ? d->in_f : d->kind == NNCB_CONV_DGRAD ? d->ci
                       : dense ? d->out_f : d->co;
@@ -1848,9 +1898,9 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
              d->kind, (long long)d->n, (long long)d->ih, (long long)d->iw, (long long)d->ci, (long long)d->co,
              (long long)d->kh, (long long)d->kw, (long long)d->sh, (long long)d->sw, (long long)d->oh,
              (long long)d->ow, (long long)d->pad_top, (long long)d->pad_left, (long long)d->batch,
-             (long long)(d->in_f * 1000003 + d->out_f), d->epilogue, g_manual_a.load() ? 1 : 0);
+             (long long)(d->in_f * 1000003 + d->out_f), d->epilogue & ~NNCB_EPI_A_UNCHANGED, g_manual_a.load() ? 1 : 0);
     int choice = g_forced_tile.load(std::memory_order_relaxed);
-    if (!choice) {
+    if (!choice && mode != 0) {
         std::lock_guard<std::mutex> lk(mu);
         auto it = tuned.find(key);
         if (it != tuned.end()) choice = it->second;
@@ -1889,6 +1939,14 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
             // but 15-20% slower at one CTA per SM -- the kernel-row halo tile is
             // no longer L2-bound at ~79% of the N = 64 MMA ceiling; force_tile only)
         }
+        // candidates write a scratch output: the caller's output (which an
+        // epilogue side input may alias) is only written by the final call
+        float* tmp_out = nullptr;
+        NNCB_CUDA(cudaMalloc(&tmp_out, std::max<size_t>(gemm_out_elems(d), 1) * sizeof(float)));
+        struct FreeTmp {
+            float* p;
+            ~FreeTmp() { cudaFree(p); }
+        } free_tmp{tmp_out};
         cudaEvent_t e0, e1;
         NNCB_CUDA(cudaEventCreate(&e0));
         NNCB_CUDA(cudaEventCreate(&e1));
@@ -1900,7 +1958,7 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
             g_force_tb = (c >> 18) & 1;
             g_force_halo = (c >> 20) & 1 ? 2 : (c >> 19) & 1;
             g_force_bres = (c >> 21) & 1;
-            int rc = gemm_tc_route(ctx, d, a, b, bias, out, handled);   // warm-up (and validity)
+            int rc = gemm_tc_route(ctx, d, a, b, bias, tmp_out, handled);   // warm-up (and validity)
             if (rc || !*handled) {
                 g_force_bn = 0;
                 g_force_pair = 0;
@@ -1913,7 +1971,7 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
                 return rc;
             }
             cudaEventRecord(e0, ctx->stream);
-            for (int r = 0; r < 3 && !rc; ++r) rc = gemm_tc_route(ctx, d, a, b, bias, out, handled);
+            for (int r = 0; r < 3 && !rc; ++r) rc = gemm_tc_route(ctx, d, a, b, bias, tmp_out, handled);
             cudaEventRecord(e1, ctx->stream);
             g_force_bn = 0;
             g_force_pair = 0;
@@ -1936,6 +1994,7 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
         }
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
+        NNCB_CUDA(cudaStreamSynchronize(ctx->stream));   // before the scratch output is freed
         std::lock_guard<std::mutex> lk(mu);
         tuned[key] = choice;
     }
@@ -2304,3 +2363,35 @@ extern "C" int nncb_gemm_force_tile(int code) {
     nncb::g_forced_tile.store(code);
     return 0;
 }
+
+extern "C" int nncb_gemm_tuning_export(char* buf, size_t cap, size_t* needed) {
+    std::string text;
+    {
+        std::lock_guard<std::mutex> lk(nncb::g_tune_mu);
+        for (const auto& [k, c] : nncb::tuned_table()) text += k + " " + std::to_string(c) + "\n";
+    }
+    if (needed) *needed = text.size() + 1;
+    if (buf && cap) {
+        const size_t n = std::min(cap - 1, text.size());
+        memcpy(buf, text.data(), n);
+        buf[n] = 0;
+    }
+    return 0;
+}
+
+extern "C" int nncb_gemm_tuning_import(const char* text) {
+    if (!text) return 0;
+    std::lock_guard<std::mutex> lk(nncb::g_tune_mu);
+    const char* p = text;
+    while (*p) {
+        const char* eol = strchr(p, '\n');
+        std::string line(p, eol ? eol : p + strlen(p));
+        p = eol ? eol + 1 : p + strlen(p);
+        const size_t sp = line.rfind(' ');
+        if (line.empty() || sp == std::string::npos) continue;
+        nncb::tuned_table()[line.substr(0, sp)] = atoi(line.c_str() + sp + 1);
+    }
+    return 0;
+}
+
+extern "C" int nncb_gemm_tuning_mode(void) { return nncb::tune_mode(); }

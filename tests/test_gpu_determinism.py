@@ -1,0 +1,47 @@
+"""Cross-process reproducibility of the tf32 path: the
+GEMM tile choice -- which fixes the fp32 accumulation order -- comes from the
+committed per-shape table or the static rule, never from timing in the
+process, so two processes produce bitwise-identical gradients and losses."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r"""
+import sys
+import numpy as np
+sys.path.insert(0, %r)
+import paper_2205_10357_b200 as P
+from paper_2205_10357_b200 import workloads as W
+assert P._kern.nncb_gemm_tuning_mode() == 1
+out = {}
+for name, doc, xs, ts in [("c1", W.c1_small_cnn(32, bn=True), (32, 32, 32, 3), (32, 10)),
+                          ("rn", W.resnet50(4, bn=True, image=64, classes=16), (4, 64, 64, 3), (4, 16))]:
+    m = P.CompiledModel(doc, precision=P.PREC_TF32)
+    loss, g = m.gradients({"x": W.uniform(xs, 1, "x")}, W.uniform(ts, 2, "t", 0.0, 1.0))
+    out[name + "/loss"] = np.array([loss])
+    for k, v in g.items():
+        out[name + "/" + k] = v
+np.savez(sys.argv[1], **out)
+"""
+
+
+def test_two_processes_give_bitwise_identical_tf32_gradients(tmp_path):
+    env = dict(os.environ)
+    env.pop("NNCB_TC_AUTOTUNE", None)
+    files = []
+    for i in range(2):
+        f = str(tmp_path / f"run{i}.npz")
+        r = subprocess.run([sys.executable, "-c", SCRIPT % ROOT, f], capture_output=True, text=True, timeout=600,
+                           env=env)
+        assert r.returncode == 0, r.stderr[-3000:]
+        files.append(np.load(f))
+    a, b = files
+    assert sorted(a.files) == sorted(b.files) and len(a.files) > 100
+    for k in a.files:
+        assert np.array_equal(a[k], b[k]), k
