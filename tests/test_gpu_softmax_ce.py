@@ -84,6 +84,12 @@ def test_c1_bn_softmax_ce_tf32_step():
                 continue
             err = np.linalg.norm(grads[w] - g) / np.linalg.norm(g)
             assert err < 2e-2, (emulate, w, err)
-    # training with it reduces the loss
-    losses = [m.train_step({"x": x}, t, 0.05) for _ in range(5)]
-    assert losses[-1] < losses[0]
+    # five SGD steps follow the float64 oracle's trajectory (each step's loss
+    # within 2e-2; the update itself is the bit-exact SGD kernel)
+    o = R64.F64Model(doc, {w: m.weight(w) for w in m.weight_shapes})
+    for _ in range(5):
+        loss = m.train_step({"x": x}, t, 0.01)
+        oloss, og = o.gradients({"x": x}, t, loss="softmax_ce")
+        for k, v in og.items():
+            o.w[k] = o.w[k] - 0.01 * v
+        assert abs(loss - oloss) <= 2e-2 * abs(oloss), (loss, oloss)
