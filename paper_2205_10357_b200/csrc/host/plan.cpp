@@ -350,11 +350,48 @@ struct Lowering {
             sum_values[key] = {sg, sgx};
         }
 
+        // Barriers whose inputs all come from outside the group -- training
+        // BatchNorm statistics of a GEMM output, backward reductions of a
+        // gradient produced elsewhere -- are hoisted to the head of the group,
+        // so they do not split its elementwise segment: e.g. the projection
+        // block's two BatchNorms, the add and the ReLU become ONE pass that
+        // reads both GEMM outputs and writes the block output (the first BN's
+        // result never leaves registers).
+        std::unordered_set<std::string> produced_here, hoisted;
+        for (const Node* n : mem)
+            for (const std::string& o : n->outputs) produced_here.insert(o);
+        for (const Node* n : mem) {
+            if (n->op == OpKind::BatchNorm && !n->attrs.inference && !produced_here.count(n->inputs[0])) {
+                int64_t C = dims(n->inputs[0]).back();
+                std::string st = n->outputs.size() == 2 ? n->outputs[1] : n->name + ".stats";
+                if (n->outputs.size() != 2) scratch(st, {2, C});
+                stats_of[n->name] = st;
+                gk.launches.push_back(simple(LaunchKind::BnStats, *n, {n->inputs[0]}, {st}));
+                hoisted.insert(n->name);
+            }
+            auto bit = bundle_of.find(n->name);
+            if (bit != bundle_of.end() && !bn_bundle_sums.count(bit->second)) {
+                const Node* head = bundles[bit->second].front();
+                bool outside = true;
+                for (int k = 0; k < 3; ++k) outside = outside && !produced_here.count(head->inputs[k]);
+                if (outside) {
+                    auto [sg, sgx] = sum_values[bit->second];
+                    gk.launches.push_back(simple(LaunchKind::BnGradReduce, *head,
+                                                 {head->inputs[0], head->inputs[1], head->inputs[2]}, {sg, sgx}));
+                    bn_bundle_sums[bit->second] = {slot(sg), slot(sgx)};
+                }
+            }
+        }
+
         Segment seg;
         for (const Node* n : mem) {
             auto bit = bundle_of.find(n->name);
             if (bit != bundle_of.end() && !bn_bundle_sums.count(bit->second)) {
                 flush(seg, gk);
+                // (reducing every ready bundle here, so that several BatchNorm
+                // grad-input members fed the same gradient share one pass, was
+                // measured slower: the merged program carries ~13 per-channel
+                // operands and ran at 4.4 TB/s against ~6 TB/s for two passes)
                 const Node* head = bundles[bit->second].front();
                 auto [sg, sgx] = sum_values[bit->second];
                 gk.launches.push_back(simple(LaunchKind::BnGradReduce, *head,
@@ -362,7 +399,7 @@ struct Lowering {
                 bn_bundle_sums[bit->second] = {slot(sg), slot(sgx)};
             }
             if (absorbed.count(n->name)) continue;
-            if (n->op == OpKind::BatchNorm && !n->attrs.inference) {
+            if (n->op == OpKind::BatchNorm && !n->attrs.inference && !hoisted.count(n->name)) {
                 flush(seg, gk);
                 int64_t C = dims(n->inputs[0]).back();
                 std::string st = n->outputs.size() == 2 ? n->outputs[1] : n->name + ".stats";
