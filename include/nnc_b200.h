@@ -110,6 +110,10 @@ int      nnc_model_trainer_loss(nnc_model* m, double* loss);
 uint64_t nnc_model_launches_per_step(nnc_model* m);
 /* One eager step with CUDA events around each launch; JSON list of
  * {label, kind, ms, bytes, flops} (algorithmic bytes / flops per launch). */
+/* One eager run of a plan (0 inference, 1 train_fwd) on the fed inputs with CUDA
+ * events around every launch (runtime::profile_run), as JSON
+ * [{label, kind, ms, bytes, flops}] (algorithmic bytes/flops). NULL on error. */
+const char* nnc_model_profile_run(nnc_model* m, int role);
 const char* nnc_model_profile_step(nnc_model* m, double lr);
 uint64_t nnc_model_arena_bytes(nnc_model* m);
 /* Device memory of a bound program (role 0 inference / 1 train_fwd after a run, 2 the trainer):

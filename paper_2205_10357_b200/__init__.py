@@ -86,6 +86,7 @@ def _load():
         "nnc_model_trainer_loss": (I, [P, DP]),
         "nnc_model_launches_per_step": (U64, [P]),
         "nnc_model_profile_step": (S, [P, D]),
+        "nnc_model_profile_run": (S, [P, I]),
         "nnc_model_dp_schedule": (S, [P, I64]),
         "nnc_model_step_schedule": (S, [P, I64, I, I]),
         "nnc_model_arena_bytes": (U64, [P]),
@@ -392,6 +393,14 @@ class CompiledModel:
     def profile_step(self, lr: float = 0.0):
         """Per-launch device times of one eager training step (CUDA events)."""
         res = _host.nnc_model_profile_step(self._h, lr)
+        if res is None:
+            raise NNCError(100, _host.nnc_last_error().decode())
+        return json.loads(res.decode())
+
+    def profile_run(self, inputs: Dict[str, np.ndarray], role: str = "inference"):
+        """Per-launch device times of one eager run of a plan (CUDA events)."""
+        keep = self._borrow(inputs)   # noqa: F841
+        res = _host.nnc_model_profile_run(self._h, 1 if role == "train_fwd" else 0)
         if res is None:
             raise NNCError(100, _host.nnc_last_error().decode())
         return json.loads(res.decode())

@@ -468,6 +468,19 @@ const char* nnc_model_step_schedule(nnc_model* m, int64_t bucket_bytes, int comm
     return rc ? nullptr : g_buf.c_str();
 }
 
+const char* nnc_model_profile_run(nnc_model* m, int role) {
+    int rc = guarded([&] {
+        const plan::ExecutionPlan& p = role == 1 ? m->plans.train_fwd : m->plans.inference;
+        auto t = runtime::profile_run(p, m->inputs, *m->host, nullptr, m->opts);
+        nlohmann::json j = nlohmann::json::array();
+        for (const auto& x : t)
+            j.push_back({{"label", x.label}, {"kind", x.kind}, {"ms", x.ms}, {"bytes", x.bytes}, {"flops", x.flops}});
+        g_buf = j.dump();
+    });
+    drop_views(m);
+    return rc ? nullptr : g_buf.c_str();
+}
+
 const char* nnc_model_profile_step(nnc_model* m, double lr) {
     int rc = guarded([&] {
         if (!m->trainer) throw Error(Error::Code::BadDocument, "trainer not prepared");

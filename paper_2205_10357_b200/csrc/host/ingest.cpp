@@ -208,6 +208,7 @@ struct Converter {
             Attrs a;
             a.eps = at.value("epsilon", 1e-3);
             bool bn = op == "batch_normalization";
+            a.batch_stats = bn && at.value("training", false);
             std::vector<std::string> w{name + ".gamma", name + ".beta"};
             b.initializer(name + ".gamma", weight(name + ".gamma", {c}, c, 1.0));
             b.initializer(name + ".beta", weight(name + ".beta", {c}, c, 0.0));

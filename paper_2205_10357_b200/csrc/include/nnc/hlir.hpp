@@ -99,6 +99,7 @@ struct Attrs {
     std::vector<int64_t> fwd_dims;
     double eps = 1e-3;     // BatchNorm / LayerNorm
     bool inference = false;  // BatchNorm: use moving statistics (inference version)
+    bool batch_stats = false;  // BatchNorm: batch statistics in every version (DLB "training": true)
 };
 
 struct Node {

@@ -239,6 +239,15 @@ std::map<std::string, Tensor> execute_on(const plan::ExecutionPlan& p,
                                          const HostModel& model, Device* device,
                                          const ExecOptions& opts = {});
 
+struct LaunchProfile {
+    std::string label, kind;
+    double ms = 0, bytes = 0, flops = 0;
+};
+/// One eager execute of `p` with CUDA events around every launch on the
+/// compute stream: (label, kind, ms, algorithmic bytes, algorithmic flops).
+std::vector<LaunchProfile> profile_run(const plan::ExecutionPlan& p, const std::map<std::string, Tensor>& inputs,
+                                       const HostModel& model, Device* device = nullptr, const ExecOptions& opts = {});
+
 /// The plan `p` specialised for the vdim binding these inputs (and explicit
 /// bindings) imply -- `p` itself when they match its compiled extents.
 const plan::ExecutionPlan& plan_for_inputs(const plan::ExecutionPlan& p,

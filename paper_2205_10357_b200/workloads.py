@@ -93,14 +93,21 @@ def c1_small_cnn(batch: int = 32, bn: bool = True, seed: int = 7) -> str:
                 [{"name": "x", "dtype": "f32", "shape": [batch, 32, 32, 3]}], ["fc"], nodes, seed)
 
 
-def c2_chain(shape=(256, 128, 128, 64), mode: str = "bn", depth: int = 16, seed: int = 7) -> str:
+def c2_chain(shape=(256, 128, 128, 64), mode: str = "bn", depth: int = 16, seed: int = 7,
+             batch_stats: bool = False) -> str:
+    """batch_stats: the BatchNorms use batch statistics in every version
+    (DLB "training": true) -- the C2 mode-B pass as an inference-role plan,
+    without the SaveSet a training forward writes for its backward."""
     pattern = ["bn", "relu", "mul", "add"] if mode == "bn" else ["relu", "mul", "add", "add"]
     nodes, cur = [], "x"
     for k in range(depth):
         op = pattern[k % 4]
         name = f"e{k}_{op}"
         if op == "bn":
-            nodes.append({"name": name, "op": "batch_normalization", "inputs": [cur], "attrs": {"epsilon": 1e-3}})
+            attrs = {"epsilon": 1e-3}
+            if batch_stats:
+                attrs["training"] = True
+            nodes.append({"name": name, "op": "batch_normalization", "inputs": [cur], "attrs": attrs})
         elif op == "relu":
             nodes.append({"name": name, "op": "relu", "inputs": [cur]})
         else:
