@@ -476,9 +476,10 @@ def main():
         line["mode_a"] = mode_a
         line["config"]["note"] = ("value = mode B: train-mode BN forward (batch statistics, 4 barriers) as a "
                                   "forward-only plan; GB = the executed plan's algorithmic bytes (%.1f B/element: "
-                                  "each barrier materializes its input; 40 B/element would need recompute); "
-                                  "mode_a = inference-BN chain, one fused pass (12 B/element)"
-                                  % (plan_bytes / elems))
+                                  "statistics passes recompute the chain from x, y instead of storing each "
+                                  "barrier's input -- SURVEY 8(d)'s 40; NNC_NO_STATS_RECOMPUTE=1 gives the "
+                                  "materializing plan, 64); mode_a = inference-BN chain, one fused pass "
+                                  "(12 B/element)" % (plan_bytes / elems))
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

@@ -113,6 +113,13 @@ enum nncb_ew_op {
                                tf32 precision mode.                                       */
     NNCB_EW_GELU_FAST = 15,      /* GELU in fp32 (erff): tf32 precision mode only            */
     NNCB_EW_GELU_GRAD_FAST = 16, /* GELU gradient in fp32 (erff/expf): tf32 precision mode only */
+    NNCB_EW_REDUCE_STATS = 17,   /* BatchNorm training statistics of r[a] computed inside a
+                               fused pass (the group's chain recomputed up to the BN input,
+                               nothing stored): per channel sum v and sum v^2 in double,
+                               finalized to slot[s][0:C] = mean, slot[s][C:2C] =
+                               1/sqrt(var + imm) (biased variance), imm = eps. Same
+                               channel-stationary launch requirements as REDUCE_BN_GRAD;
+                               counts toward its at-most-two reductions per program.      */
     NNCB_EW_REDUCE_BN_GRAD = 13, /* BatchNorm backward reduction fused into the group that
                                produces g (replaces nncb_bn_grad_reduce for it):
                                sum_g[c] += g, sum_gx[c] += g*xhat, xhat = (x-mean)*invstd,

@@ -169,7 +169,12 @@ struct Lowering {
         int64_t channels = -1;
     };
 
-    void flush(Segment& seg, GroupKernel& gk) {
+    // stats_bn: instead of the segment's pass, emit a STATISTICS pass for the
+    // training BatchNorm stats_bn whose input the segment computes: the chain
+    // is evaluated from the group's inputs, nothing is stored, and
+    // REDUCE_STATS writes mean / invstd into stats_slot; the segment stays open
+    // (its values are recomputed by the pass that finally stores them).
+    void flush(Segment& seg, GroupKernel& gk, const Node* stats_bn = nullptr, uint32_t stats_slot = 0) {
         if (seg.members.empty()) return;
         std::unordered_set<std::string> in_seg;
         for (const Node* n : seg.members) in_seg.insert(n->name);
@@ -275,6 +280,7 @@ struct Lowering {
                 for (const std::string& c : cit->second)
                     if (!in_seg.count(c)) visible = true;
             uint32_t os = slot(n->outputs[0]);
+            if (stats_bn) continue;   // statistics pass: nothing leaves registers
             if (visible) {
                 nncb_ew_instr st{};
                 st.op = NNCB_EW_STORE;
@@ -286,11 +292,50 @@ struct Lowering {
                 plan.values[os].storage = StorageClass::FusedRegister;
             }
         }
+        if (stats_bn) {
+            nncb_ew_instr red{};
+            red.op = NNCB_EW_REDUCE_STATS;
+            red.dst = red.b = red.c = red.d = red.e = red.f = red.h = -1;
+            red.a = reg_of_value.at(stats_bn->inputs[0]);
+            red.slot = arg(stats_slot, 0, true);
+            red.imm = stats_bn->attrs.eps;
+            L.ew.push_back(red);
+            label += ".stats(" + stats_bn->name + ")";
+        }
         L.ew_regs = next_reg;
         L.label = label;
         L.attrs.out_channels = seg.channels > 0 ? seg.channels : dims(seg.members.front()->outputs[0]).back();
         gk.launches.push_back(std::move(L));
-        seg = Segment{};
+        if (!stats_bn) seg = Segment{};
+    }
+
+    /// Recompute (instead of materialize) the input of a training BatchNorm
+    /// that the open segment computes: a statistics pass re-evaluates the
+    /// chain from the group inputs (SURVEY.md §8(d) C2 mode B: 4 barriers with
+    /// recompute = 40 B/element instead of 64 when every barrier stores its
+    /// input). Applies when the input is used only inside the group, is not
+    /// kept for a backward pass, the chain reads few element-sized inputs, and
+    /// the channel-stationary reduction can run.
+    bool recompute_stats(const Segment& seg, const Node& bn, const std::unordered_set<std::string>& group_members) const {
+        const std::string& x = bn.inputs[0];
+        bool produced = false;
+        std::unordered_set<std::string> outs, ext;
+        for (const Node* m : seg.members) {
+            produced = produced || m->outputs[0] == x;
+            outs.insert(m->outputs[0]);
+        }
+        if (!produced || keep.count(x)) return false;
+        auto cit = consumers.find(x);
+        if (cit != consumers.end())
+            for (const std::string& c : cit->second)
+                if (!group_members.count(c)) return false;
+        for (const Node* m : seg.members)
+            for (const std::string& in : m->inputs)
+                if (!outs.count(in) && element_count(dims(in)) == seg.elems) ext.insert(in);
+        if (ext.size() > 3) return false;
+        const int64_t C = dims(x).back(), e = element_count(dims(x));
+        if (C < 4 || C > 2048 || (C & (C - 1)) || e % 4 != 0) return false;
+        return std::getenv("NNC_NO_STATS_RECOMPUTE") == nullptr;
     }
 
     // ---- BatchNorm statistics / backward bundles --------------------------
@@ -357,7 +402,8 @@ struct Lowering {
         // block's two BatchNorms, the add and the ReLU become ONE pass that
         // reads both GEMM outputs and writes the block output (the first BN's
         // result never leaves registers).
-        std::unordered_set<std::string> produced_here, hoisted;
+        std::unordered_set<std::string> produced_here, hoisted, member_names;
+        for (const Node* n : mem) member_names.insert(n->name);
         for (const Node* n : mem)
             for (const std::string& o : n->outputs) produced_here.insert(o);
         for (const Node* n : mem) {
@@ -400,12 +446,16 @@ struct Lowering {
             }
             if (absorbed.count(n->name)) continue;
             if (n->op == OpKind::BatchNorm && !n->attrs.inference && !hoisted.count(n->name)) {
-                flush(seg, gk);
                 int64_t C = dims(n->inputs[0]).back();
                 std::string st = n->outputs.size() == 2 ? n->outputs[1] : n->name + ".stats";
                 if (n->outputs.size() != 2) scratch(st, {2, C});
                 stats_of[n->name] = st;
-                gk.launches.push_back(simple(LaunchKind::BnStats, *n, {n->inputs[0]}, {st}));
+                if (recompute_stats(seg, *n, member_names)) {
+                    flush(seg, gk, n, slot(st));   // statistics pass; the segment stays open
+                } else {
+                    flush(seg, gk);
+                    gk.launches.push_back(simple(LaunchKind::BnStats, *n, {n->inputs[0]}, {st}));
+                }
             }
             if (is_elementwise(*n)) {
                 int64_t e = element_count(dims(n->outputs[0]));

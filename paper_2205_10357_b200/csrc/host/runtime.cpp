@@ -184,7 +184,7 @@ void launch_cost(const BoundLaunch& b, const Launch& L, const ExecutionPlan& p, 
             for (const auto& in : b.ew_prog.empty() ? L.ew : b.ew_prog) {
                 if (in.op == NNCB_EW_LOAD || in.op == NNCB_EW_STORE) bytes += 4.0 * n;
                 if (in.op == NNCB_EW_LOAD_CH) bytes += 4.0 * c;
-                if (in.op == NNCB_EW_REDUCE_BN_GRAD) bytes += 8.0 * c;
+                if (in.op == NNCB_EW_REDUCE_BN_GRAD || in.op == NNCB_EW_REDUCE_STATS) bytes += 8.0 * c;
             }
             break;
         }

@@ -32,6 +32,9 @@ struct nncb_ew_kernel {
     bool uses_channels = false;
     int n_reduce = 0;                      // REDUCE_BN_GRAD instructions (<= 2)
     int reduce_sg[2] = {-1, -1}, reduce_sgx[2] = {-1, -1};   // their output slots
+    int reduce_stats[2] = {0, 0};          // 1: REDUCE_STATS (mean / invstd into one [2C] slot)
+    double reduce_eps[2] = {0.0, 0.0};
+    int red_blocks = 4;                    // resident blocks per SM the reduction build is budgeted for
 };
 
 void nncb::ew_release(nncb_ew_kernel* k) {
@@ -123,6 +126,18 @@ void emit_body(std::ostringstream& os, const nncb_ew_program& p, int W, bool use
                     os << "  #pragma unroll\n  for (int j = 0; j < " << W << "; ++j) " << d << "[j] = __ldg(" << ptr
                        << " + ch[j]);\n";
                 continue;
+            case NNCB_EW_REDUCE_STATS: {
+                if (!stationary) continue;
+                const std::string r0 = "red" + std::to_string(reduce_index) + "_0",
+                                  r1 = "red" + std::to_string(reduce_index) + "_1";
+                ++reduce_index;
+                char eps[64];   // (in the source: the kernel cache is keyed by it)
+                snprintf(eps, sizeof(eps), "%.17e", in.imm);
+                os << "  /* stats eps " << eps << " */\n";
+                os << "  #pragma unroll\n  for (int j = 0; j < " << W << "; ++j) { const double v = (double)" << a
+                   << "[j]; " << r0 << "[j] += v; " << r1 << "[j] += v * v; }\n";
+                continue;
+            }
             case NNCB_EW_REDUCE_BN_GRAD: {
                 if (!stationary) continue;   // launch guarantees the channel-stationary path
                 const std::string r0 = "red" + std::to_string(reduce_index) + "_0",
@@ -180,7 +195,7 @@ void emit_body(std::ostringstream& os, const nncb_ew_program& p, int W, bool use
 std::vector<int> find_reduces(const nncb_ew_program& p) {
     std::vector<int> r;
     for (int k = 0; k < p.n_instr; ++k)
-        if (p.instr[k].op == NNCB_EW_REDUCE_BN_GRAD) r.push_back(k);
+        if (p.instr[k].op == NNCB_EW_REDUCE_BN_GRAD || p.instr[k].op == NNCB_EW_REDUCE_STATS) r.push_back(k);
     return r;
 }
 
@@ -227,8 +242,14 @@ std::string generate(const nncb_ew_program& p, bool uses_ch) {
     // those programs, e.g. a chain of inference BatchNorms, get a 2-block budget)
     int min_blocks = chregs.size() > 8 ? 2 : chregs.size() >= 3 ? 4 : 0;
     if (env_min_blocks >= 0) min_blocks = env_min_blocks;
-    if (red)   // 16 double accumulator registers per reduction
-        os << "extern \"C\" __global__ void __launch_bounds__(256, " << (nred > 1 ? red2_blocks() : 4)
+    // 16 double accumulator registers per reduction; a statistics pass with
+    // more than 4 per-channel operands (a recomputed BatchNorm chain) gets the
+    // 2-block budget too (at 64 registers the depth-3 pass spilled and ran at
+    // 1.7 TB/s; 4.8 TB/s at 128)
+    bool stats_red = false;
+    for (int k = 0; k < p.n_instr; ++k) stats_red = stats_red || p.instr[k].op == NNCB_EW_REDUCE_STATS;
+    if (red)
+        os << "extern \"C\" __global__ void __launch_bounds__(256, " << (nred > 1 || (stats_red && chregs.size() > 4) ? red2_blocks() : 4)
            << ") nnc_fused_ew(const EwArgs A) {";
     else if (min_blocks > 0)
         os << "extern \"C\" __global__ void __launch_bounds__(256, " << min_blocks << ") nnc_fused_ew(const EwArgs A) {";
@@ -315,7 +336,8 @@ int nvrtc_fail(nvrtcProgram prog, nvrtcResult r, const std::string& src) {
 // (deterministic). For C > 1024 main-kernel block k only covers the channels
 // [(1024 k) % C, +1024).
 __global__ void __launch_bounds__(1024) ew_red_final_k(const double* __restrict__ part, int grid, int C,
-                                                       float* __restrict__ sg, float* __restrict__ sgx) {
+                                                       float* __restrict__ sg, float* __restrict__ sgx,
+                                                       int stats, double rows, double eps) {
     __shared__ double fold[2][128][8];
     // programmatic dependent launch: the reducing grid's partials are
     // complete and visible past this point
@@ -345,8 +367,16 @@ __global__ void __launch_bounds__(1024) ew_red_final_k(const double* __restrict_
         __syncthreads();
     }
     if (ty == 0 && c < C) {
-        sg[c] = static_cast<float>(fold[0][0][tx]);
-        sgx[c] = static_cast<float>(fold[1][0][tx]);
+        if (stats) {   // REDUCE_STATS: BatchNorm mean and 1/sqrt(biased var + eps), from the double sums
+            const double mean = fold[0][0][tx] / rows;
+            double var = fold[1][0][tx] / rows - mean * mean;
+            if (var < 0) var = 0;
+            sg[c] = static_cast<float>(mean);
+            sgx[c] = static_cast<float>(1.0 / sqrt(var + eps));
+        } else {
+            sg[c] = static_cast<float>(fold[0][0][tx]);
+            sgx[c] = static_cast<float>(fold[1][0][tx]);
+        }
     }
 }
 
@@ -406,6 +436,13 @@ int nncb_ew_compile(nncb_ctx* ctx, const nncb_ew_program* p, nncb_ew_kernel** ou
     k->source = src;
     k->n_slots = p->n_slots;
     k->uses_channels = uses_ch;
+    {
+        int nch = 0;
+        for (int q = 0; q < p->n_instr; ++q) nch += p->instr[q].op == NNCB_EW_LOAD_CH;
+        bool stats_red = false;
+        for (int q = 0; q < p->n_instr; ++q) stats_red = stats_red || p->instr[q].op == NNCB_EW_REDUCE_STATS;
+        k->red_blocks = (find_reduces(*p).size() > 1 || (stats_red && nch > 4)) ? red2_blocks() : 4;
+    }
     const std::vector<int> reds = find_reduces(*p);
     if (reds.size() > 2) {
         nncb::ew_release(k);
@@ -414,6 +451,8 @@ int nncb_ew_compile(nncb_ctx* ctx, const nncb_ew_program* p, nncb_ew_kernel** ou
     for (int r : reds) {
         k->reduce_sg[k->n_reduce] = p->instr[r].slot;
         k->reduce_sgx[k->n_reduce] = p->instr[r].e;
+        k->reduce_stats[k->n_reduce] = p->instr[r].op == NNCB_EW_REDUCE_STATS ? 1 : 0;
+        k->reduce_eps[k->n_reduce] = p->instr[r].imm;
         ++k->n_reduce;
     }
     const auto& D = nncb::drv::table();
@@ -475,7 +514,7 @@ int nncb_ew_launch(nncb_ctx* ctx, nncb_ew_kernel* k, void* const* slots, int64_t
         const int64_t g = C / std::gcd<int64_t>(C, 1024);
         static const int64_t per_sm = getenv("NNCB_EW_RED_BLOCKS") ? std::max(1, atoi(getenv("NNCB_EW_RED_BLOCKS"))) : 4;
         // one wave: the two-reduction build is budgeted for red2_blocks() per SM
-        const int64_t resident = k->n_reduce > 1 ? std::min<int64_t>(per_sm, red2_blocks()) : per_sm;
+        const int64_t resident = std::min<int64_t>(per_sm, k->red_blocks);
         const int64_t cap = std::max<int64_t>(g, (resident * static_cast<int64_t>(ctx->sm_count) / g) * g);
         if (grid > cap) grid = static_cast<unsigned>(cap);
         args.part = static_cast<double*>(nncb::scratch(ctx, sizeof(double) * 2 * C * grid * k->n_reduce));
@@ -499,8 +538,11 @@ int nncb_ew_launch(nncb_ctx* ctx, nncb_ew_kernel* k, void* const* slots, int64_t
             attr[0].val.programmaticStreamSerializationAllowed = q == 0 ? 1 : 0;   // the first follows the reducing grid
             cfg.attrs = attr;
             cfg.numAttrs = 1;
+            float* o0 = args.p[k->reduce_sg[q]];
+            float* o1 = k->reduce_stats[q] ? o0 + C : args.p[k->reduce_sgx[q]];
             NNCB_CUDA(cudaLaunchKernelEx(&cfg, ew_red_final_k, static_cast<const double*>(args.part + static_cast<size_t>(q) * grid * 2 * C),
-                                         static_cast<int>(grid), C, args.p[k->reduce_sg[q]], args.p[k->reduce_sgx[q]]));
+                                         static_cast<int>(grid), C, o0, o1, k->reduce_stats[q],
+                                         static_cast<double>(n / C), k->reduce_eps[q]));
             ctx->launches.fetch_add(1, std::memory_order_relaxed);
         }
     }

@@ -221,6 +221,31 @@ def test_c2_train_bn_chain_2_24_elements():
     assert e_gpu <= max(1e-5, e_cpu), (e_gpu, e_cpu)
 
 
+@pytest.mark.parametrize("recompute", [True, False])
+def test_c2_batch_stats_forward_plan_2_24_elements(recompute, monkeypatch):
+    """The benched C2 mode-B plan: the chain's BatchNorms with batch statistics
+    in a forward-only plan. With recompute (default) each statistics barrier
+    re-evaluates the chain from x, y instead of storing it (40 B/element);
+    without, each barrier materializes its input (64 B/element). Both hold the
+    float64 truth to max(1e-5, the float32 CPU restatement's own error)."""
+    if not recompute:
+        monkeypatch.setenv("NNC_NO_STATS_RECOMPUTE", "1")
+    shape = (64, 64, 64, 64)
+    doc = W.c2_chain(shape, mode="bn", batch_stats=True)
+    x = W.uniform(shape, 5, "x")
+    y = W.uniform(shape, 6, "y")
+    m = P.CompiledModel(doc, precision=P.PREC_TF32)
+    out_name = json.loads(doc)["outputs"][0]
+    got = m.run({"x": x, "y": y}, outputs=[out_name])[out_name]
+    truth = R64.F64Model(doc).forward({"x": x, "y": y}, training=True)[out_name]
+    cpu32 = O.OracleModel(doc).forward({"x": x, "y": y}, training=True)[out_name]
+    e_gpu, e_cpu = rel_clamped(got, truth), rel_clamped(cpu32, truth)
+    assert e_gpu <= max(1e-5, e_cpu), (e_gpu, e_cpu)
+    prof = m.profile_run({"x": x, "y": y})
+    per_elem = sum(p["bytes"] for p in prof) / x.size
+    assert abs(per_elem - (40.0 if recompute else 64.0)) < 0.1, per_elem
+
+
 def test_c5_layer_8192x4096_tf32():
     doc = W.mlp(8192, 4096, 1)
     x = W.uniform((8192, 4096), 1, "x")
