@@ -387,7 +387,9 @@ extern "C" {
 int nncb_ew_compile_check(const nncb_ew_program* p) {
     if (p->n_slots > kMaxSlots) return nncb::fail("nncb_ew_compile_check: too many slots");
     bool uses_ch = false;
-    for (int k = 0; k < p->n_instr; ++k) uses_ch = uses_ch || p->instr[k].op == NNCB_EW_LOAD_CH;
+    for (int k = 0; k < p->n_instr; ++k)   // reductions run channel-stationary too
+        uses_ch = uses_ch || p->instr[k].op == NNCB_EW_LOAD_CH || p->instr[k].op == NNCB_EW_REDUCE_STATS ||
+                  p->instr[k].op == NNCB_EW_REDUCE_BN_GRAD;
     std::string src = generate(*p, uses_ch);
     static std::mutex mu;
     static std::set<std::string> checked;
@@ -410,7 +412,9 @@ int nncb_ew_compile_check(const nncb_ew_program* p) {
 int nncb_ew_compile(nncb_ctx* ctx, const nncb_ew_program* p, nncb_ew_kernel** out) {
     if (p->n_slots > kMaxSlots) return nncb::fail("nncb_ew_compile: too many slots");
     bool uses_ch = false;
-    for (int k = 0; k < p->n_instr; ++k) uses_ch = uses_ch || p->instr[k].op == NNCB_EW_LOAD_CH;
+    for (int k = 0; k < p->n_instr; ++k)   // reductions run channel-stationary too
+        uses_ch = uses_ch || p->instr[k].op == NNCB_EW_LOAD_CH || p->instr[k].op == NNCB_EW_REDUCE_STATS ||
+                  p->instr[k].op == NNCB_EW_REDUCE_BN_GRAD;
     std::string src = generate(*p, uses_ch);
     auto hit = ctx->ew_cache.find(src);
     if (hit != ctx->ew_cache.end()) {

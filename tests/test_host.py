@@ -93,8 +93,19 @@ def test_c2_chain_is_one_kernel_per_bn_barrier():
     assert d["inference"]["launch_count"] == 1
     d = P.CompiledModel(W.c2_chain((2, 4, 4, 8), "bn")).describe
     kinds = [l["kind"] for g in d["train_fwd"]["groups"] for l in g["launches"]]
-    # 4 BatchNorm statistics barriers, each followed by one fused pass
-    assert kinds.count("bn_stats") == 4 and kinds.count("ew") == 4
+    # training forward: 4 BatchNorm statistics barriers, each followed by one
+    # fused pass; the BN inputs are saved for backward, so each barrier
+    # materializes its input (the first one, the graph input, is reduced by a
+    # one-load statistics pass)
+    assert kinds.count("bn_stats") == 3 and kinds.count("ew") == 5
+    # forward-only plan with batch statistics (C2 mode B): the 3 inner barriers
+    # recompute the chain in statistics passes; nothing is stored but the output
+    d = P.CompiledModel(W.c2_chain((2, 4, 4, 8), "bn", batch_stats=True)).describe
+    launches = [l for g in d["inference"]["groups"] for l in g["launches"]]
+    assert [l["kind"] for l in launches] == ["ew"] * 5
+    assert sum(".stats" in l["label"] for l in launches) == 4
+    stored = [v["name"] for v in d["inference"]["values"] if v["storage"] == "buffer" and v["category"] != "parameter"]
+    assert sorted(stored) == sorted(["x", "y", "e15_add"] + [f"e{k}_bn.stats" for k in (0, 4, 8, 12)])
 
 
 @pytest.mark.parametrize("doc", [W.c1_small_cnn(2, bn=True), W.mlp(4, 64, 2), W.resnet50(1, bn=True, image=32),
