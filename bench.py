@@ -236,6 +236,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-json", default=None)
+    ap.add_argument("--precision", default="tf32", choices=["tf32", "bf16", "fp32"],
+                    help="GEMM precision: tf32 (default), bf16 operands for compute-bound contractions, exact fp32")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     cfg = CONFIGS[args.config]
@@ -273,7 +275,8 @@ def main():
         P.init_comm(world, rank, uid[0])
 
     doc, inputs, target = make_workload(args.config, batch)
-    model = P.CompiledModel(doc, precision=P.PREC_TF32)
+    prec = {"tf32": P.PREC_TF32, "bf16": P.PREC_BF16, "fp32": P.PREC_FP32}[args.precision]
+    model = P.CompiledModel(doc, precision=prec)
     timer = P.DeviceTimer()
     lr = 1e-4
     clocks = Clocks(local)
@@ -465,7 +468,12 @@ def main():
     line = {
         "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32 (tcgen05 kind::tf32 GEMMs, fp32 accumulate)", "data": "synthetic",
+        "vs_baseline": None, "dtype": {"tf32": "f32 (tcgen05 kind::tf32 GEMMs, fp32 accumulate)",
+                                       "bf16": "f32 storage; tcgen05 kind::f16 on bf16 operand copies for the "
+                                               "compute-bound forward / input-gradient GEMMs, tf32 for the rest; "
+                                               "fp32 accumulate",
+                                       "fp32": "f32 (exact-order fp32 GEMMs)"}[args.precision],
+        "data": "synthetic",
         "config": {"workload": cfg["workload"], "global_batch": batch * world, "batch_per_gpu": batch,
                    "parallelism": f"dp{world}", "l2": "activations >> 126 MB L2; no flush needed"},
         "clocks": clk, "e2e": e2e, "gpu_launches": launches, "roofline": roof, "fused_group_roofline": fused_roof,

@@ -169,6 +169,12 @@ enum nncb_gemm_kind {
 enum nncb_precision {
     NNCB_PREC_TF32 = 0,    /* tcgen05.mma kind::tf32, fp32 accumulate in TMEM (default)    */
     NNCB_PREC_FP32 = 1,    /* exact-order fp32 FFMA path (parity mode)                      */
+    NNCB_PREC_BF16 = 2,    /* tcgen05.mma kind::f16 on bf16 operands, fp32 accumulate in TMEM:
+                              the forward and input-gradient contractions (conv and dense)
+                              with K-major operands (conv: channels per tap % 64 == 0, or a
+                              single tap with K % 8 == 0) convert A and B to bf16 copies
+                              (round to nearest) and multiply those; outputs stay fp32.
+                              Weight gradients and other shapes run the tf32 path.          */
 };
 enum nncb_epilogue {
     NNCB_EPI_BIAS = 1,

@@ -25,6 +25,10 @@ Pinning (tests/test_oracle.py):
     implementation) and against central finite differences (autodiff.cpp:325-400).
 
 Options a parity test may use:
+  emulate = "bf16": the device's bf16 mode -- the forward / input-gradient
+           operands of contractions on the bf16 route (bf16_route: aligned
+           K blocks, arithmetic intensity >= 128) rounded to nearest at bf16,
+           every other tensor-core operand truncated to tf32, fp32 storage;
   emulate = "tf32" (constructor): the arithmetic of the device's tf32 mode,
            restated -- every stored value rounded to float32, and every GEMM
            operand truncated to tf32 (1+8+10 bits: tcgen05 kind::tf32 reads the
@@ -108,6 +112,24 @@ def tf32_trunc(a):
 
 def f32_round(a):
     return np.asarray(a, np.float32).astype(np.float64)
+
+
+def bf16_round(a):
+    """Round to nearest even at bf16 (what the device's fp32 -> bf16 operand
+    conversion does, __float2bfloat16_rn)."""
+    u = np.ascontiguousarray(a, np.float32).view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def bf16_route(K, Ck, N, kind, taps):
+    """The device's NNCB_PREC_BF16 route rule (gemm_tc.cu bf16_eligible): forward
+    and input-gradient contractions with aligned K blocks whose arithmetic
+    intensity K*N / (2*(Ck + N)) reaches 128."""
+    if kind == "wgrad":
+        return False
+    aligned = Ck % 8 == 0 and N % 8 == 0 if taps == 1 else Ck % 64 == 0
+    return aligned and K * N / (2.0 * (Ck + N)) >= 128.0
 
 
 def conv_geom(xd, k, s, same):
@@ -266,7 +288,7 @@ class F64Model:
 
     def __init__(self, document: str, weights: Optional[Dict[str, np.ndarray]] = None,
                  emulate: Optional[str] = None):
-        if emulate not in (None, "tf32"):
+        if emulate not in (None, "tf32", "bf16"):
             raise ValueError(emulate)
         self.emulate = emulate
         d = json.loads(document)
@@ -327,9 +349,14 @@ class F64Model:
         """A stored value: float32-rounded under emulation."""
         return f32_round(a) if self.emulate else a
 
-    def _op(self, a, co):
-        """A GEMM operand of a layer with `co` output channels."""
-        return tf32_trunc(a) if self.emulate == "tf32" and co >= 16 else a
+    def _op(self, a, co, route=None):
+        """A GEMM operand of a layer with `co` output channels; route = (K, Ck,
+        N, kind, taps) of the contraction, for the bf16 mode's route rule."""
+        if not self.emulate or co < 16:
+            return a
+        if self.emulate == "bf16" and route is not None and bf16_route(*route):
+            return bf16_round(a)
+        return tf32_trunc(a)
 
     # ------------------------------------------------------------ per node
     def node_forward(self, n, ins, training: bool, argmax=None):
@@ -342,11 +369,14 @@ class F64Model:
             s = _pair(a, "strides", 1)
             b = self.w.get(name + ".bias") if a.get("use_bias", True) else None
             co = a["filters"]
-            y = conv2d(self._op(x, co), self._op(self.w[name + ".weight"], co), b, s,
+            kh, kw, ci, _ = self.w[name + ".weight"].shape
+            r = (kh * kw * ci, ci, co, "fwd", kh * kw)
+            y = conv2d(self._op(x, co, r), self._op(self.w[name + ".weight"], co, r), b, s,
                        a.get("padding", "valid") == "same")
         elif op == "dense":
             co = a["units"]
-            y = self._op(x, co) @ self._op(self.w[name + ".weight"], co)
+            r = (x.shape[1], x.shape[1], co, "fwd", 1)
+            y = self._op(x, co, r) @ self._op(self.w[name + ".weight"], co, r)
             if a.get("use_bias", True):
                 y = y + self.w[name + ".bias"]
         elif op == "relu":
@@ -419,23 +449,24 @@ class F64Model:
             gin[0] = gy.reshape(x.shape)
         elif op == "dense":
             co = a["units"]
-            xo, go, wo = self._op(x, co), self._op(gy, co), self._op(self.w[name + ".weight"], co)
-            gw[name + ".weight"] = xo.T @ go
+            fin = x.shape[1]
+            rw, rd = (x.shape[0], fin, co, "wgrad", 1), (co, co, fin, "dgrad", 1)
+            gw[name + ".weight"] = self._op(x, co, rw).T @ self._op(gy, co, rw)
             if a.get("use_bias", True):
                 gw[name + ".bias"] = gy.sum(axis=0)
             if need_x:
-                gin[0] = go @ wo.T
+                gin[0] = self._op(gy, co, rd) @ self._op(self.w[name + ".weight"], co, rd).T
         elif op == "conv2d":
             s = _pair(a, "strides", 1)
             same = a.get("padding", "valid") == "same"
             w = self.w[name + ".weight"]
-            co = w.shape[3]
-            xo, go, wo = self._op(x, co), self._op(gy, co), self._op(w, co)
-            gw[name + ".weight"] = conv2d_grad_weight(xo, go, w.shape, s, same)
+            kh, kw, ci, co = w.shape
+            rw, rd = (0, ci, co, "wgrad", kh * kw), (kh * kw * co, co, ci, "dgrad", kh * kw)
+            gw[name + ".weight"] = conv2d_grad_weight(self._op(x, co, rw), self._op(gy, co, rw), w.shape, s, same)
             if a.get("use_bias", True):
                 gw[name + ".bias"] = gy.reshape(-1, co).sum(axis=0)
             if need_x:
-                gin[0] = conv2d_grad_input(go, wo, x.shape, s, same)
+                gin[0] = conv2d_grad_input(self._op(gy, co, rd), self._op(w, co, rd), x.shape, s, same)
         elif op == "max_pooling2d":
             k = _pair(a, "pool_size")
             s = _pair(a, "strides") if "strides" in a else k

@@ -387,7 +387,7 @@ struct Program {
                 }
             }
         }
-        if (precision == NNCB_PREC_TF32) {
+        if (precision != NNCB_PREC_FP32) {   // tensor-core modes (tf32, bf16)
             fuse_bn_statistics();
             fuse_bn_grad_reduce();
             fuse_relu_grad_epilogue();
@@ -829,7 +829,7 @@ struct Program {
                 bool fast = false;
                 for (const auto& in : L.ew)
                     fast = fast || in.op == NNCB_EW_BN_GRAD || in.op == NNCB_EW_GELU || in.op == NNCB_EW_GELU_GRAD;
-                if (fast && precision == NNCB_PREC_TF32 && !std::getenv("NNC_EXACT_BN_GRAD")) {
+                if (fast && precision != NNCB_PREC_FP32 && !std::getenv("NNC_EXACT_BN_GRAD")) {
                     b.ew_prog = L.ew;
                     for (auto& in : b.ew_prog) {
                         if (in.op == NNCB_EW_BN_GRAD) in.op = NNCB_EW_BN_GRAD_FAST;

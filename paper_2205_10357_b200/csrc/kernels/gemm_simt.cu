@@ -239,7 +239,7 @@ extern "C" int nncb_gemm(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a,
     const bool colstats = (d->epilogue & NNCB_EPI_COLSTATS) && d->colstats;
     if (colstats && d->kind != NNCB_CONV_FWD && d->kind != NNCB_DENSE_FWD)
         return nncb::fail("nncb_gemm: column statistics are a forward-GEMM epilogue");
-    if (d->precision == NNCB_PREC_TF32) {
+    if (d->precision == NNCB_PREC_TF32 || d->precision == NNCB_PREC_BF16) {
         bool handled = false;
         int rc = nncb::gemm_tc(ctx, d, a, b, bias, out, &handled);
         g_last_path = 1;

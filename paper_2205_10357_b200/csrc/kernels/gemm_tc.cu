@@ -32,6 +32,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cuda_bf16.h>
+
 #include "driver_api.cuh"
 #include "nncb_internal.cuh"
 
@@ -117,6 +119,12 @@ struct TcParams {
     int ob_w, ob_h, ob_n;   // tma_out 1: a warp's 32-row sub-box of the pixel tile
     int64_t pix_pairs;  // MODE_CONV: pixel-box pairs per phase
     int64_t m_pairs;    // MODE_WGRAD: M-tile pairs
+    // bf16 operands (NNCB_PREC_BF16): tcgen05.mma kind::f16 on bf16 A/B tiles
+    // with fp32 accumulation in TMEM. A 128-byte swizzle row holds kel = 64 K
+    // elements (32 for tf32); one MMA consumes 32 bytes of K in both kinds, so
+    // the smem ring and descriptors are byte-identical.
+    int bf16;
+    int kel;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -261,6 +269,23 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
+}
+
+// kind::f16 with BF16 operands (NNCB_PREC_BF16); the pair form as below
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
 // CTA pair: M=256 MMA issued by the leader over both CTAs' shared memory
@@ -843,7 +868,7 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                     uint8_t* sa; uint64_t* bar;
                     acquire(sa, bar);
                     uint8_t* sb = sa + a_bytes;
-                    const int c0 = cb * BK;
+                    const int c0 = cb * P.kel;
                     if (!MA) ld4(sa, &map_a, bar, c0, xw, yh, T.tn0);
                     if (P.b_mn) {
                         for (int q = 0; q < bcols / 32; ++q) ld2(sb + q * 4096, &map_b, bar, n0 + 32 * q, br + c0);
@@ -904,7 +929,8 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
         // (the 14-bit start-address field, in 16-byte units, cannot carry: smem
         // offsets stay below 256 KB).
         const uint32_t a_mn = (P.mode == MODE_WGRAD && !MA) ? 1u : 0u;
-        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (a_mn << 15) |
+        const uint32_t fmt = P.bf16 ? 1u : 2u;   // A/B format: kind::f16 BF16 = 1, kind::tf32 TF32 = 2
+        const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (a_mn << 15) |
                                (static_cast<uint32_t>(P.b_mn) << 16) | ((static_cast<uint32_t>(P.bn) >> 3) << 17) |
                                ((static_cast<uint32_t>(PAIR ? 2 * BM : BM) >> 4) << 24);
         const uint32_t s0 = smem_u32(smem);
@@ -978,10 +1004,17 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
 #pragma unroll
                     for (int kk = 0; kk < BK / 8; ++kk) {
                         const uint64_t ad = adesc0 + so + kk * a_kstep, bd = bdesc0 + so + kk * b_kstep;
-                        if (PAIR)
-                            mma_tf32_pair(d, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
-                        else
-                            mma_tf32(d, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                        const uint32_t accum = (i > 0 || kk > 0) ? 1u : 0u;
+                        if (P.bf16) {
+                            if (PAIR)
+                                mma_f16_pair(d, ad, bd, idesc, accum);
+                            else
+                                mma_f16(d, ad, bd, idesc, accum);
+                        } else if (PAIR) {
+                            mma_tf32_pair(d, ad, bd, idesc, accum);
+                        } else {
+                            mma_tf32(d, ad, bd, idesc, accum);
+                        }
                     }
                     if (PAIR)
                         mma_commit_pair(&empty[s]);   // frees the stage in both CTAs
@@ -1280,14 +1313,16 @@ __global__ void splitk_reduce4_kernel(const float4* __restrict__ partial, float4
 // ---------------------------------------------------------------------------
 
 bool encode_4d(CUtensorMap* map, const float* base, int64_t c, int64_t w, int64_t h, int64_t n, int bc, int bw,
-               int bh, int bnn, int ew, int eh, bool mn_major, int64_t pitch = 0) {
+               int bh, int bnn, int ew, int eh, bool mn_major, int64_t pitch = 0, int esize = 4) {
     if (pitch == 0) pitch = c;   // elements between consecutive pixels
     cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
-    cuuint64_t strides[3] = {(cuuint64_t)(pitch * 4), (cuuint64_t)(pitch * w * 4), (cuuint64_t)(pitch * w * h * 4)};
+    cuuint64_t strides[3] = {(cuuint64_t)(pitch * esize), (cuuint64_t)(pitch * w * esize),
+                             (cuuint64_t)(pitch * w * h * esize)};
     cuuint32_t box[4] = {(cuuint32_t)bc, (cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)bnn};
     cuuint32_t es[4] = {1, (cuuint32_t)ew, (cuuint32_t)eh, 1};
     CUresult r = nncb::drv::table().tensorMapEncodeTiled(
-        map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box, es,
+        map, esize == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+        const_cast<float*>(base), dims, strides, box, es,
         CU_TENSOR_MAP_INTERLEAVE_NONE, mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
         CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -1296,13 +1331,14 @@ bool encode_4d(CUtensorMap* map, const float* base, int64_t c, int64_t w, int64_
 }
 
 bool encode_2d(CUtensorMap* map, const float* base, int64_t inner, int64_t rows, int box_inner, int box_rows,
-               bool mn_major) {
+               bool mn_major, int esize = 4) {
     cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)(inner * 4)};
+    cuuint64_t strides[1] = {(cuuint64_t)(inner * esize)};
     cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_rows};
     cuuint32_t es[2] = {1, 1};
     CUresult r = nncb::drv::table().tensorMapEncodeTiled(
-        map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+        map, esize == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+        const_cast<float*>(base), dims, strides, box, es,
         CU_TENSOR_MAP_INTERLEAVE_NONE, mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
         CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -1317,6 +1353,7 @@ thread_local int g_dil_w = 1;        // horizontal tap dilation for the next imp
 thread_local int g_force_tb = 0;     // 1: forward convolution with transposed (K-major) weights
 thread_local int g_force_bres = 0;   // 1: halo tiles with resident B (single N tile)
 thread_local int g_force_halo = 0;   // 1: 3x3 stride-1 conv through kernel-row halo patches; 2: full 3x3 patches
+thread_local int g_bf16 = 0;         // the next implicit GEMM's A and B are bf16 copies (NNCB_PREC_BF16 route)
 
 int pick_bn(int64_t n) {
     static const int env_bn = getenv("NNCB_TC_BN") ? atoi(getenv("NNCB_TC_BN")) : 0;   // tuning knob
@@ -1884,8 +1921,107 @@ size_t gemm_out_elems(const nncb_gemm_desc* d) {
 }
 }  // namespace
 
+// fp32 -> bf16 (round to nearest even), 4 elements per thread
+__global__ void f32_to_bf16_k(const float* __restrict__ x, __nv_bfloat16* __restrict__ y, int64_t n) {
+    const int64_t n4 = n / 4;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(x) + i);
+        __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+        uint2 o;
+        o.x = *reinterpret_cast<uint32_t*>(&lo);
+        o.y = *reinterpret_cast<uint32_t*>(&hi);
+        reinterpret_cast<uint2*>(y)[i] = o;
+    }
+    for (int64_t i = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = __float2bfloat16_rn(x[i]);
+}
+
+// W[rows][cols] fp32 -> Wt[cols][rows] bf16 (K-major weights), 32x32 tiles
+__global__ void transpose_bf16_k(const float* __restrict__ w, __nv_bfloat16* __restrict__ wt, int rows, int cols) {
+    __shared__ float tile[32][33];
+    const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+    for (int j = threadIdx.y; j < 32; j += 8) {
+        const int r = by + j, c = bx + threadIdx.x;
+        if (r < rows && c < cols) tile[j][threadIdx.x] = w[static_cast<int64_t>(r) * cols + c];
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += 8) {
+        const int c = bx + j, r = by + threadIdx.x;
+        if (r < rows && c < cols) wt[static_cast<int64_t>(c) * rows + r] = __float2bfloat16_rn(tile[threadIdx.x][j]);
+    }
+}
+
+// NNCB_PREC_BF16: the contraction runs kind::f16 on bf16 copies of its operands
+// when both are K-major (forward and input-gradient contractions) with K blocks
+// of 64 channels per tap (or one tap with K % 8 == 0); otherwise tf32.
+// The route also has to pay: the per-call conversion reads the fp32 operands
+// and writes bf16 copies, so only contractions whose arithmetic intensity
+// (flops per unique fp32 byte, K*N / (2*(Ck + N)) per output pixel) is above
+// the tf32 ridge point take it (measured: 3x3 convs and wide dense layers win;
+// the memory-bound 1x1 convs lose). NNCB_BF16_MIN_INTENSITY overrides (0: all).
+bool bf16_eligible(const nncb_gemm_desc* d) {
+    if (d->epilogue & NNCB_EPI_RELU_GRAD) return false;
+    int64_t K = 0, Ck = 0, N = 0;
+    bool ok = false;
+    switch (d->kind) {
+        case NNCB_DENSE_FWD: K = Ck = d->in_f; N = d->out_f; ok = d->in_f % 8 == 0 && d->out_f % 8 == 0; break;
+        case NNCB_DENSE_DGRAD: K = Ck = d->out_f; N = d->in_f; ok = d->out_f % 8 == 0 && d->in_f % 8 == 0; break;
+        case NNCB_CONV_FWD:
+            Ck = d->ci; K = d->kh * d->kw * d->ci; N = d->co;
+            ok = d->kh * d->kw == 1 ? d->ci % 8 == 0 : d->ci % 64 == 0;
+            break;
+        case NNCB_CONV_DGRAD:
+            Ck = d->co; K = d->kh * d->kw * d->co; N = d->ci;
+            ok = d->kh * d->kw == 1 ? d->co % 8 == 0 : d->co % 64 == 0;
+            break;
+        default: return false;
+    }
+    static const double min_i = getenv("NNCB_BF16_MIN_INTENSITY") ? atof(getenv("NNCB_BF16_MIN_INTENSITY")) : 128.0;
+    return ok && static_cast<double>(K) * N / (2.0 * (Ck + N)) >= min_i;
+}
+
+// Writes the bf16 operand copies into the context's bf16 buffers.
+int bf16_operands(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const void** a16,
+                  const void** b16) {
+    const bool dense = d->kind <= NNCB_DENSE_WGRAD;
+    const bool fwd = d->kind == NNCB_DENSE_FWD || d->kind == NNCB_CONV_FWD;
+    const int64_t na = dense ? d->batch * (fwd ? d->in_f : d->out_f)
+                             : (fwd ? d->n * d->ih * d->iw * d->ci : d->n * d->oh * d->ow * d->co);
+    const int64_t krows = dense ? d->in_f : d->kh * d->kw * d->ci, cols = dense ? d->out_f : d->co;
+    auto* A = static_cast<__nv_bfloat16*>(bf16_buffer(ctx, 0, static_cast<size_t>(na) * 2 + 16));
+    auto* B = static_cast<__nv_bfloat16*>(bf16_buffer(ctx, 1, static_cast<size_t>(krows * cols) * 2 + 16));
+    if (!A || !B) return fail("bf16 gemm: operand buffer allocation failed");
+    f32_to_bf16_k<<<grid_for(ctx, (na + 3) / 4, 256), 256, 0, ctx->stream>>>(a, A, na);
+    NNCB_LAUNCHED(ctx);
+    if (fwd && !dense && d->b_kmajor) {   // the caller's K-major fp32 copy: convert only
+        f32_to_bf16_k<<<grid_for(ctx, (krows * cols + 3) / 4, 256), 256, 0, ctx->stream>>>(d->b_kmajor, B, krows * cols);
+    } else if (fwd) {                    // [K][N] -> K-major [N][K]
+        transpose_bf16_k<<<dim3((unsigned)((cols + 31) / 32), (unsigned)((krows + 31) / 32)), dim3(32, 8), 0,
+                           ctx->stream>>>(b, B, (int)krows, (int)cols);
+    } else {                             // input gradient: the weights are K-major (K = cols) as stored
+        f32_to_bf16_k<<<grid_for(ctx, (krows * cols + 3) / 4, 256), 256, 0, ctx->stream>>>(b, B, krows * cols);
+    }
+    NNCB_LAUNCHED(ctx);
+    *a16 = A;
+    *b16 = B;
+    return 0;
+}
+
 int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const float* bias, float* out,
             bool* handled) {
+    // the bf16 route: operands converted once here; every tile candidate and
+    // the final call below read the copies (g_bf16 scopes the whole call)
+    const bool bf16 = d->precision == NNCB_PREC_BF16 && bf16_eligible(d);
+    if (bf16) {
+        const void *a16 = nullptr, *b16 = nullptr;
+        if (int rc = bf16_operands(ctx, d, a, b, &a16, &b16)) return rc;
+        a = static_cast<const float*>(a16);
+        b = static_cast<const float*>(b16);
+    }
+    struct Bf16Scope {
+        explicit Bf16Scope(bool on) { g_bf16 = on ? 1 : 0; }
+        ~Bf16Scope() { g_bf16 = 0; }
+    } bf16_scope(bf16);
     const int mode = tune_mode();
     const bool enabled = mode == 2;
     std::mutex& mu = g_tune_mu;
@@ -1899,6 +2035,7 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
              (long long)d->kh, (long long)d->kw, (long long)d->sh, (long long)d->sw, (long long)d->oh,
              (long long)d->ow, (long long)d->pad_top, (long long)d->pad_left, (long long)d->batch,
              (long long)(d->in_f * 1000003 + d->out_f), d->epilogue & ~NNCB_EPI_A_UNCHANGED, g_manual_a.load() ? 1 : 0);
+    if (bf16) strncat(key, "|bf16", sizeof(key) - strlen(key) - 1);
     int choice = g_forced_tile.load(std::memory_order_relaxed);
     if (!choice && mode != 0) {
         std::lock_guard<std::mutex> lk(mu);
@@ -2127,6 +2264,7 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
 
     TcParams P;
     memset(&P, 0, sizeof(P));
+    P.kel = BK;
     P.debug = dbg;
     P.dil_w = g_dil_w;
     CUtensorMap ma, mb;
@@ -2148,6 +2286,12 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
         P.N = Nc;
         P.ldc = Nc;
         P.cblocks = static_cast<int>((Ck + 31) / 32);
+        if (g_bf16) {
+            if (manual || (!single_tap && Ck % 64 != 0) || Ck % 8 != 0) return 0;
+            P.bf16 = 1;
+            P.kel = 64;
+            P.cblocks = static_cast<int>((Ck + 63) / 64);
+        }
         if (fwd) {
             P.gn = (int)n; P.gh = (int)oh; P.gw = (int)ow;
             P.out_h = (int)oh; P.out_w = (int)ow; P.out_s = 1;
@@ -2196,7 +2340,7 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
         // (or the space-to-depth stem: 2 taps per row spaced 2, any padding)
         const bool halo33 = kh == 3 && kw == 3 && pt == 1 && pl == 1 && g_dil_w == 1;
         const bool halo_s2d = fwd && kw == 2 && g_dil_w == 2 && kh <= 4;
-        if (g_force_halo && !manual && !P.pair && !(d->epilogue & NNCB_EPI_RELU_GRAD) && (halo33 || halo_s2d) &&
+        if (g_force_halo && !g_bf16 && !manual && !P.pair && !(d->epilogue & NNCB_EPI_RELU_GRAD) && (halo33 || halo_s2d) &&
             sh == 1 && sw == 1 && Ck % 32 == 0 && (fwd ? ow : iw) >= HALO_TW &&
             2 * (HALO_A_BYTES + kw * static_cast<size_t>(P.bn) * BK * 4) + smem_for(P.bn, 0, 8) <= 227 * 1024) {
             // (a two-stage ring must fit: 256-wide tiles do not)
@@ -2225,17 +2369,26 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
         if (fwd && P.halo) {
             if (!encode_4d(&ma, act, ci, iw, ih, n, 32, P.TW + 2, P.TH + (P.halo == 2 ? 2 : 0), 1, 1, 1, false, lda)) return 1;
         } else if (fwd) {
-            if (!manual &&
-                !encode_4d(&ma, act, ci, iw, ih, n, 32, P.TW * (int)sw, P.TH * (int)sh, P.TN, (int)sw, (int)sh, false, lda))
+            if (!manual && !encode_4d(&ma, act, ci, iw, ih, n, P.kel, P.TW * (int)sw, P.TH * (int)sh, P.TN, (int)sw,
+                                      (int)sh, false, lda, P.bf16 ? 2 : 4))
                 return 1;
         } else if (P.halo) {
             if (!encode_4d(&ma, act, co, ow, oh, n, 32, P.TW + 2, P.TH + (P.halo == 2 ? 2 : 0), 1, 1, 1, false)) return 1;
         } else {
-            if (!encode_4d(&ma, act, co, ow, oh, n, 32, P.TW, P.TH, P.TN, 1, 1, false)) return 1;
+            if (!encode_4d(&ma, act, co, ow, oh, n, P.kel, P.TW, P.TH, P.TN, 1, 1, false, 0, P.bf16 ? 2 : 4)) return 1;
         }
         // B: weights [kh*kw*ci, co]
         const int64_t kfull = kh * kw * ci;
-        if (fwd && g_force_tb && !manual && kfull % 4 == 0) {
+        if (P.bf16 && fwd) {
+            // bf16 route: b is the K-major bf16 copy [co][kh*kw*ci] (gemm_tc)
+            P.b_mn = 0;
+            P.bt = 1;
+            if (!encode_2d(&mb, b, kfull, co, P.kel, P.pair ? P.bn / 2 : P.bn, false, 2)) return 1;
+        } else if (P.bf16) {
+            // bf16 route, dgrad: b is the bf16 copy of the weights [kh*kw*ci][co] (K = co)
+            P.b_mn = 0;
+            if (!encode_2d(&mb, b, co, kh * kw * ci, P.kel, P.pair ? P.bn / 2 : P.bn, false, 2)) return 1;
+        } else if (fwd && g_force_tb && !manual && kfull % 4 == 0) {
             // K-major copy [co][kh*kw*ci]: the tensor core reads K-major tf32
             // operands faster than MN-major ones (measured fwd vs dgrad). The
             // caller's copy (b_kmajor, refreshed once per plan) or a per-call one.

@@ -41,6 +41,18 @@ void* wt_buffer(nncb_ctx* ctx, size_t bytes) {
     return ctx->wt;
 }
 
+void* bf16_buffer(nncb_ctx* ctx, int which, size_t bytes) {
+    if (bytes <= ctx->bf16_bytes[which]) return ctx->bf16_buf[which];
+    if (ctx->bf16_buf[which]) ctx->retired.push_back(ctx->bf16_buf[which]);   // captured graphs may use it
+    if (cudaMalloc(&ctx->bf16_buf[which], bytes) != cudaSuccess) {
+        ctx->bf16_buf[which] = nullptr;
+        ctx->bf16_bytes[which] = 0;
+        return nullptr;
+    }
+    ctx->bf16_bytes[which] = bytes;
+    return ctx->bf16_buf[which];
+}
+
 void* workspace(nncb_ctx* ctx, size_t bytes) {
     if (bytes <= ctx->workspace_bytes) return ctx->workspace;
     if (ctx->workspace) ctx->retired.push_back(ctx->workspace);
@@ -110,6 +122,8 @@ int nncb_destroy(nncb_ctx* c) {
     for (void* p : c->retired) cudaFree(p);
     if (c->workspace) cudaFree(c->workspace);
     if (c->wt) cudaFree(c->wt);
+    for (void* p : c->bf16_buf)
+        if (p) cudaFree(p);
     cudaStreamSynchronize(c->comm_stream);
     for (cudaEvent_t e : c->fork_events) cudaEventDestroy(e);
     cudaStreamDestroy(c->stream);

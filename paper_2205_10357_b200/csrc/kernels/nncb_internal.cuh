@@ -39,6 +39,8 @@ struct nncb_ctx {
     void* staging = nullptr;             // pinned upload ring (host_io.cu), created on first large h2d
     void* wt = nullptr;                  // transposed (K-major) forward weights, grown on demand
     size_t wt_bytes = 0;
+    void* bf16_buf[2] = {nullptr, nullptr};   // bf16 operand copies of a NNCB_PREC_BF16 GEMM (A, B)
+    size_t bf16_bytes[2] = {0, 0};
     // fork/join events between the compute and comm streams, reused round
     // robin (created once: nothing is created or destroyed during a capture)
     std::vector<cudaEvent_t> fork_events;
@@ -104,6 +106,7 @@ inline unsigned grid_for(const nncb_ctx* ctx, int64_t work_items, int threads, i
 }
 
 void* scratch(nncb_ctx* ctx, size_t bytes);
+void* bf16_buffer(nncb_ctx* ctx, int which, size_t bytes);
 void* workspace(nncb_ctx* ctx, size_t bytes);
 void ew_release(nncb_ew_kernel* k);
 

@@ -126,7 +126,7 @@ def device_reader(model):
     return value
 
 
-def local_step_parity(model, doc, feed, target, emu_tol, truth_tol, min_values):
+def local_step_parity(model, doc, feed, target, emu_tol, truth_tol, min_values, emulate="tf32"):
     """Launch-by-launch parity of one training step (oracle.restated64.local_parity):
     every forward value, every backward value gradient and every weight
     gradient of the step, each re-derived by the oracle from the device's own
@@ -137,7 +137,7 @@ def local_step_parity(model, doc, feed, target, emu_tol, truth_tol, min_values):
     loss, grads = model.gradients(feed, target)
     read = device_reader(model)
     weights = {w: model.weight(w) for w in model.weight_shapes}
-    emu = R64.local_parity(R64.F64Model(doc, weights, emulate="tf32"), feed, read, grads, target)
+    emu = R64.local_parity(R64.F64Model(doc, weights, emulate=emulate), feed, read, grads, target)
     truth = R64.local_parity(R64.F64Model(doc, weights), feed, read, grads, target)
     n = {k: len(v) for k, v in emu.items()}
     assert n["forward"] >= min_values and n["backward"] >= min_values, n
@@ -183,6 +183,44 @@ def test_c4_resnet50_bn_tf32_training_step_at_224():
     for w, g in grads.items():
         want = (w0[w].astype(np.float64) - lr * g.astype(np.float64)).astype(np.float32)
         assert np.array_equal(m.weight(w), want), w
+
+
+def test_c4_resnet50_bn_bf16_training_step_at_224_launch_by_launch():
+    """The bf16 mode (NNCB_PREC_BF16): compute-bound forward / input-gradient
+    convolutions on tcgen05 kind::f16 with bf16 operand copies, the rest tf32.
+    Every launch of the step against the bf16-emulating oracle (operands rounded
+    exactly as the device converts them) and the float64 truth at the
+    north-star bf16 bound, 2e-2."""
+    batch = 2
+    doc = W.resnet50(batch, bn=True)
+    x = W.uniform((batch, 224, 224, 3), 1, "x")
+    t = W.uniform((batch, 1000), 2, "t", 4.0, 6.0)
+    m = P.CompiledModel(doc, precision=P.PREC_BF16)
+    randomize_norms(m, np.random.default_rng(4))
+    local_step_parity(m, doc, {"x": x}, t, emu_tol=2e-3, truth_tol=TF32_TOL, min_values=100, emulate="bf16")
+
+
+def test_c5_layer_8192x4096_bf16():
+    """One C5 layer in the bf16 mode. The weight gradient passes through the
+    LayerNorm backward, whose rows are orthogonal to the normalized forward
+    values: bf16-rounded forward values move it by ~4e-2 end to end (a
+    conditioning effect, as for the deep graphs), so the kernels are held
+    launch by launch (every value and gradient within 2e-2 of the float64
+    truth on the device's own inputs) and the forward output and loss end to
+    end."""
+    doc = W.mlp(8192, 4096, 1)
+    x = W.uniform((8192, 4096), 1, "x")
+    t = W.uniform((8192, 4096), 2, "t", 4.0, 6.0)
+    m = P.CompiledModel(doc, precision=P.PREC_BF16)
+    randomize_norms(m, np.random.default_rng(5))
+    got = m.run({"x": x})["ln0"]
+    # (norm-relative: bf16 operand rounding moves near-zero LayerNorm outputs by
+    # a few 1e-3 of the row scale, which an elementwise clamped max over-weights)
+    assert rel_norm(got, oracle_for(m, doc, emulate="bf16").forward({"x": x}, training=False)["ln0"]) < 1e-3
+    assert rel_norm(got, oracle_for(m, doc).forward({"x": x}, training=False)["ln0"]) < TF32_TOL
+    loss, _ = local_step_parity(m, doc, {"x": x}, t, emu_tol=2e-3, truth_tol=TF32_TOL, min_values=2, emulate="bf16")
+    oloss = oracle_for(m, doc).gradients({"x": x}, t)[0]
+    assert abs(loss - oloss) <= TF32_TOL * abs(oloss)
 
 
 def test_c1_bn_tf32_with_device_argmax():

@@ -40,6 +40,8 @@ def main():
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--layers", default="")
     ap.add_argument("--colstats", action="store_true", help="forward GEMMs also accumulate BN column statistics")
+    ap.add_argument("--precision", type=int, default=0, help="0 tf32, 1 exact fp32, 2 bf16 operands")
+    ap.add_argument("--dense", default="", help="dense shapes batch:in:out,... instead of conv layers")
     ap.add_argument("--eg", action="store_true", help="dgrad GEMMs run the ReLU-gradient + BN-sums epilogue")
     ap.add_argument("--res", action="store_true", help="with --eg: add a residual gradient")
     ap.add_argument("--tile", default="auto", help="auto | 128 | 256 | p128 | p256 | w128 | t128 | h64 | th128 ... (p = CTA pair, w = wide staging, t = K-major weights, h = halo patches)")
@@ -52,7 +54,22 @@ def main():
                 (0x200000 if "r" in t else 0))
         K.nncb_gemm_force_tile(code)
     total = {}
+    for spec in [x for x in a.dense.split(",") if x]:
+        bsz, fin, fout = (int(v) for v in spec.split(":"))
+        flops = 2.0 * bsz * fin * fout
+        X, Wt, Y = Dev(nbytes=bsz * fin * 4), Dev(nbytes=fin * fout * 4), Dev(nbytes=bsz * fout * 4)
+        for kind in a.kinds.split(","):
+            code, A, B, O = {"fwd": (0, X, Wt, Y), "dgrad": (1, Y, Wt, X), "wgrad": (2, X, Y, Wt)}[kind]
+            d = GemmDesc(kind=code, precision=a.precision, batch=bsz, in_f=fin, out_f=fout)
+            assert K.nncb_gemm(ctx(), ctypes.byref(d), A.p, B.p, None, O.p) == 0, K.nncb_last_error()
+            timer.start()
+            for _ in range(a.reps):
+                K.nncb_gemm(ctx(), ctypes.byref(d), A.p, B.p, None, O.p)
+            ms = timer.stop() / a.reps
+            print(f"dense {spec} {kind:5s} {ms*1000:8.1f} us {flops/ms/1e9:7.1f} TF/s", flush=True)
     for name, h, ci, co, k, s in LAYERS:
+        if a.dense:
+            break
         if a.layers and not any(name.startswith(x) for x in a.layers.split(",")):
             continue
         g = geom(a.batch, h, ci, co, k, s)
@@ -65,7 +82,7 @@ def main():
                 continue   # the stem's input gradient is never needed (and has no tensor-core lowering)
             code, A, B, O = {"fwd": (3, x, w, y), "dgrad": (4, y, w, x), "wgrad": (5, x, y, w)}[kind]
             cs = Dev(nbytes=2 * co * 8) if (a.colstats and kind == "fwd") else None
-            d = GemmDesc(kind=code, precision=0, epilogue=4 if cs else 0, **g)
+            d = GemmDesc(kind=code, precision=a.precision, epilogue=4 if cs else 0, **g)
             if cs:
                 d.colstats = cs.p
             if a.eg and kind == "dgrad":
