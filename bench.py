@@ -236,6 +236,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-json", default=None)
+    ap.add_argument("--no-variants", action="store_true", help="skip the bf16 companion measurement")
     ap.add_argument("--precision", default="tf32", choices=["tf32", "bf16", "fp32"],
                     help="GEMM precision: tf32 (default), bf16 operands for compute-bound contractions, exact fp32")
     args = ap.parse_args()
@@ -446,6 +447,34 @@ def main():
             cpu = cpu_reference(args.config, args.cpu_seconds, min(os.cpu_count() or 1, 32))
         except Exception as exc:  # noqa: BLE001
             cpu = {"value": None, "error": str(exc)[:200]}
+    # the same workload in the bf16 mode (NNCB_PREC_BF16: compute-bound forward /
+    # input-gradient GEMMs on kind::f16 with bf16 operand copies), same timing
+    # rules, on rank 0 of a single-GPU run: reported beside the headline
+    variant = None
+    if (rank == 0 and world == 1 and args.precision == "tf32" and cfg["kind"] in ("train", "infer")
+            and not args.no_variants):
+        del model
+        vm = P.CompiledModel(doc, precision=P.PREC_BF16)
+        if cfg["kind"] == "train":
+            vm.trainer_prepare(inputs, target)
+            vstep = lambda: vm.trainer_step_device(lr)  # noqa: E731
+        else:
+            vm.run(inputs)
+            vstep = lambda: vm.run_device("inference")  # noqa: E731
+        for _ in range(args.warmup):
+            vstep()
+        timer.sync()
+        timer.start()
+        for _ in range(args.steps):
+            vstep()
+        v_ms = timer.stop() / args.steps
+        variant = {"bf16": {"value": units / (v_ms / 1000.0), "unit": unit, "ms_per_step": v_ms,
+                            "dtype": "f32 storage; tcgen05 kind::f16 on bf16 operand copies for the compute-bound "
+                                     "forward / input-gradient GEMMs (arithmetic intensity >= 128), tf32 for the "
+                                     "rest; fp32 accumulate",
+                            "parity": "tests/test_gpu_baseline_parity.py (bf16 rows): launch by launch within 2e-2 "
+                                      "of the float64 truth"}}
+        del vm
     mode_a = None
     if cfg["kind"] == "chain" and rank == 0:
         # SURVEY.md §8(d) C2 mode A: inference BatchNorm (per-channel affine),
@@ -480,6 +509,8 @@ def main():
         "cpu_baseline": cpu,
         "by_kernel_kind": top,
     }
+    if variant:
+        line["precision_variants"] = variant
     if mode_a:
         line["mode_a"] = mode_a
         line["config"]["note"] = ("value = mode B: train-mode BN forward (batch statistics, 4 barriers) as a "

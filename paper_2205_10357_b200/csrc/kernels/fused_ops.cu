@@ -225,6 +225,29 @@ __global__ void avgpool_fwd_k(const float* __restrict__ x, float* __restrict__ y
     }
 }
 
+// Global average pool (1x1 output), 4 channels per thread, 32-bit indices:
+// the window is summed in the same (h, w) order as avgpool_fwd_k (bit-identical)
+// but the 4-wide loads are independent, so the pool streams instead of chaining
+// 64-bit index math per element.
+__global__ void avgpool_fwd_global4_k(const float* __restrict__ x, float* __restrict__ y, uint32_t hw, uint32_t c4,
+                                      uint32_t total4, float scale) {
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total4; t += gridDim.x * blockDim.x) {
+        const uint32_t ch4 = t % c4, b = t / c4;
+        const float4* src = reinterpret_cast<const float4*>(x) + static_cast<size_t>(b) * hw * c4 + ch4;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 7
+        for (uint32_t p = 0; p < hw; ++p) {
+            const float4 v = __ldg(src + static_cast<size_t>(p) * c4);
+            acc.x = __fadd_rn(acc.x, v.x);
+            acc.y = __fadd_rn(acc.y, v.y);
+            acc.z = __fadd_rn(acc.z, v.z);
+            acc.w = __fadd_rn(acc.w, v.w);
+        }
+        reinterpret_cast<float4*>(y)[t] =
+            make_float4(__fmul_rn(acc.x, scale), __fmul_rn(acc.y, scale), __fmul_rn(acc.z, scale), __fmul_rn(acc.w, scale));
+    }
+}
+
 // Output windows containing input row h: o in [o_lo(h), o_hi(h)] where
 // a_start(o) <= h < a_end(o); found by stepping from the proportional guess
 // (adaptive windows overlap by at most one position, so the loops run <= 2
@@ -1014,6 +1037,14 @@ int nncb_avgpool_fwd(nncb_ctx* ctx, int64_t n, int64_t ih, int64_t iw, int64_t c
                      const float* x, float* y) {
     int64_t total = n * oh * ow * c;
     if (total == 0) return 0;
+    if (oh == 1 && ow == 1 && c % 4 == 0 && n * ih * iw * c < (int64_t(1) << 31) &&
+        !((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15)) {
+        const float scale = 1.0f / static_cast<float>(ih * iw);   // = __fdiv_rn(1, window) of the general kernel
+        avgpool_fwd_global4_k<<<nncb::grid_for(ctx, total / 4, 256), 256, 0, ctx->stream>>>(
+            x, y, static_cast<uint32_t>(ih * iw), static_cast<uint32_t>(c / 4), static_cast<uint32_t>(total / 4), scale);
+        NNCB_LAUNCHED(ctx);
+        return 0;
+    }
     avgpool_fwd_k<<<nncb::grid_for(ctx, total, 256), 256, 0, ctx->stream>>>(x, y, n, ih, iw, c, oh, ow);
     NNCB_LAUNCHED(ctx);
     return 0;

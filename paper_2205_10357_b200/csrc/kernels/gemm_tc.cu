@@ -1966,6 +1966,13 @@ bool bf16_eligible(const nncb_gemm_desc* d) {
     switch (d->kind) {
         case NNCB_DENSE_FWD: K = Ck = d->in_f; N = d->out_f; ok = d->in_f % 8 == 0 && d->out_f % 8 == 0; break;
         case NNCB_DENSE_DGRAD: K = Ck = d->out_f; N = d->in_f; ok = d->out_f % 8 == 0 && d->in_f % 8 == 0; break;
+        case NNCB_DENSE_WGRAD:
+            // dW = x^T g over transposed (K-major) bf16 copies: per reduction row the
+            // unique bytes are one row of x and one of g
+            K = 2 * d->in_f; Ck = d->in_f; N = d->out_f;   // intensity in*out / (2*(in + out))
+            ok = d->batch % 8 == 0 && d->in_f % 8 == 0 && d->out_f % 8 == 0;
+            return ok && static_cast<double>(d->in_f) * d->out_f / (2.0 * (d->in_f + d->out_f)) >=
+                             (getenv("NNCB_BF16_MIN_INTENSITY") ? atof(getenv("NNCB_BF16_MIN_INTENSITY")) : 128.0);
         case NNCB_CONV_FWD:
             Ck = d->ci; K = d->kh * d->kw * d->ci; N = d->co;
             ok = d->kh * d->kw == 1 ? d->ci % 8 == 0 : d->ci % 64 == 0;
@@ -1984,6 +1991,20 @@ bool bf16_eligible(const nncb_gemm_desc* d) {
 int bf16_operands(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const void** a16,
                   const void** b16) {
     const bool dense = d->kind <= NNCB_DENSE_WGRAD;
+    if (d->kind == NNCB_DENSE_WGRAD) {   // x [B][in] -> x^T [in][B], g [B][out] -> g^T [out][B]
+        auto* A = static_cast<__nv_bfloat16*>(bf16_buffer(ctx, 0, static_cast<size_t>(d->batch * d->in_f) * 2 + 16));
+        auto* B = static_cast<__nv_bfloat16*>(bf16_buffer(ctx, 1, static_cast<size_t>(d->batch * d->out_f) * 2 + 16));
+        if (!A || !B) return fail("bf16 gemm: operand buffer allocation failed");
+        transpose_bf16_k<<<dim3((unsigned)((d->in_f + 31) / 32), (unsigned)((d->batch + 31) / 32)), dim3(32, 8), 0,
+                           ctx->stream>>>(a, A, (int)d->batch, (int)d->in_f);
+        NNCB_LAUNCHED(ctx);
+        transpose_bf16_k<<<dim3((unsigned)((d->out_f + 31) / 32), (unsigned)((d->batch + 31) / 32)), dim3(32, 8), 0,
+                           ctx->stream>>>(b, B, (int)d->batch, (int)d->out_f);
+        NNCB_LAUNCHED(ctx);
+        *a16 = A;
+        *b16 = B;
+        return 0;
+    }
     const bool fwd = d->kind == NNCB_DENSE_FWD || d->kind == NNCB_CONV_FWD;
     const int64_t na = dense ? d->batch * (fwd ? d->in_f : d->out_f)
                              : (fwd ? d->n * d->ih * d->iw * d->ci : d->n * d->oh * d->ow * d->co);
@@ -2022,6 +2043,20 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
         explicit Bf16Scope(bool on) { g_bf16 = on ? 1 : 0; }
         ~Bf16Scope() { g_bf16 = 0; }
     } bf16_scope(bf16);
+    // a bf16 dense weight gradient is the forward contraction of the transposed
+    // copies: dW[in][out] = (x^T)[in][B] . (g^T)[out][B]^T (both K-major)
+    nncb_gemm_desc wd;
+    if (bf16 && d->kind == NNCB_DENSE_WGRAD) {
+        wd = *d;
+        wd.kind = NNCB_DENSE_FWD;
+        wd.batch = d->in_f;
+        wd.in_f = d->batch;
+        wd.out_f = d->out_f;
+        wd.epilogue = 0;
+        wd.colstats = nullptr;
+        bias = nullptr;
+    }
+    if (bf16 && d->kind == NNCB_DENSE_WGRAD) d = &wd;
     const int mode = tune_mode();
     const bool enabled = mode == 2;
     std::mutex& mu = g_tune_mu;

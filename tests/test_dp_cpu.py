@@ -196,3 +196,34 @@ def test_two_rank_step_schedule_allreduce_and_update():
             o, n = w["offset"], w["elements"]
             ref = g[w["name"]].ravel().astype(np.float64)
             assert np.max(np.abs(gsum[o:o + n] * 0.5 - ref)) <= 1e-5 * max(np.max(np.abs(ref)), 1e-12), w["name"]
+
+
+def test_step_schedule_update_points_resnet():
+    """runtime::step_schedule on the ResNet-50-shaped graph: every bucket is
+    all-reduced at its close point and updated no earlier than the last
+    backward launch that reads any of its weights; without a communicator the
+    same updates fork off the compute stream; without the update nothing but
+    the all-reduces remains; the compute stream always joins last."""
+    import paper_2205_10357_b200 as P
+    m = P.CompiledModel(W.resnet50(2, image=64))
+    s = m.step_schedule(32 << 20, comm=True, sgd=True)
+    woff = {w["name"]: (w["offset"], w["elements"]) for w in s["weights"]}
+    last_read = {}
+    for k, ws in enumerate(s["launch_reads"]):
+        for w in ws:
+            last_read[w] = k
+    for i, b in enumerate(s["buckets"]):
+        touching = [w for w, (o, n) in woff.items() if o < b["offset"] + b["count"] and b["offset"] < o + n]
+        assert b["update_launch"] >= b["close_launch"]
+        assert all(b["update_launch"] >= last_read.get(w, -1) for w in touching)
+        acts = [a for a in s["actions"] if a["bucket"] == i]
+        assert [a["kind"] for a in acts] == ["allreduce", "update"]
+        assert acts[0]["after"] == b["close_launch"] and acts[1]["after"] == b["update_launch"]
+    assert s["actions"][-1]["kind"] == "join"
+    local = m.step_schedule(32 << 20, comm=False, sgd=True)
+    assert [a["kind"] for a in local["actions"] if a["kind"] in ("allreduce", "update")] == \
+        ["update"] * len(s["buckets"])
+    nosgd = m.step_schedule(32 << 20, comm=True, sgd=False)
+    assert [a["kind"] for a in nosgd["actions"] if a["kind"] in ("allreduce", "update")] == \
+        ["allreduce"] * len(s["buckets"])
+    assert m.step_schedule(32 << 20, comm=False, sgd=False)["actions"] == []

@@ -1,6 +1,7 @@
 """The bf16 tensor-core path (NNCB_PREC_BF16: tcgen05.mma kind::f16 on bf16
 operand copies, fp32 accumulation in TMEM) at the kernel level: forward and
-input-gradient contractions of dense layers and convolutions against float64
+input-gradient contractions of dense layers and convolutions, and dense
+weight gradients (over transposed bf16 copies), against float64
 products of the same bf16-rounded operands (what remains is fp32 accumulation
 order), asserting through nncb_gemm_last_path that the tensor-core path ran;
 shapes the route does not take (weight gradients, narrow K blocks) run tf32."""
@@ -66,6 +67,16 @@ def test_conv_fwd_and_dgrad_bf16(n, h, ci, co, k, s):
     g = rng.uniform(-1, 1, (n, oh, ow, co)).astype(np.float32)
     gx = run(GemmDesc(kind=4, precision=BF16, **geo), g, w, (n, h, h, ci))
     assert rel(gx, R64.conv2d_grad_input(bf16(g), bf16(w), x.shape, (s, s), True)) < 1e-5
+
+
+@pytest.mark.parametrize("batch,fin,fout", [(8192, 4096, 4096), (256, 2048, 1000)])
+def test_dense_wgrad_bf16_over_transposed_copies(batch, fin, fout):
+    """dW = x^T g as the forward contraction of K-major bf16 transposes."""
+    rng = np.random.default_rng(fin)
+    x = rng.uniform(-1, 1, (batch, fin)).astype(np.float32)
+    g = rng.uniform(-1, 1, (batch, fout)).astype(np.float32)
+    gw = run(GemmDesc(kind=2, precision=BF16, batch=batch, in_f=fin, out_f=fout), x, g, (fin, fout))
+    assert rel(gw, bf16(x).T @ bf16(g)) < 1e-5
 
 
 def test_wgrad_runs_tf32_under_bf16_precision():

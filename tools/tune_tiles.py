@@ -1,5 +1,6 @@
 """Regenerates paper_2205_10357_b200/csrc/kernels/tile_table.inc: runs the
-BASELINE workloads (C1, C3/C4 ResNet-50-shaped, C5 MLP; C2 has no GEMMs) with
+BASELINE workloads (C1, C3/C4 ResNet-50-shaped, C5 MLP; C2 has no GEMMs), in the
+tf32 and bf16 precisions, with
 NNCB_TC_AUTOTUNE=live on a B200 so every GEMM shape they launch is measured
 (candidates timed on a scratch output), then writes the chosen tile per shape.
 The committed table makes the default (table) mode deterministic across
@@ -22,12 +23,15 @@ def main():
              ("c4", W.resnet50(256, bn=True), {"x": W.uniform((256, 224, 224, 3), 1, "x")}, (256, 1000)),
              ("c5", W.mlp(8192, 4096, 8), {"x": W.uniform((8192, 4096), 1, "x")}, (8192, 4096))]
     for name, doc, inputs, tshape in cases:
-        m = P.CompiledModel(doc, precision=P.PREC_TF32)
-        t = W.uniform(tshape, 2, "t", 0.0, 1.0)
-        m.trainer_prepare(inputs, t)          # first eager step: every training GEMM shape
-        m.run(inputs)                         # inference (C3 for the ResNet-50-shaped graph)
-        print(name, "tuned", flush=True)
-        del m
+        for prec, pname in ((P.PREC_TF32, "tf32"), (P.PREC_BF16, "bf16")):
+            if name == "c1" and pname == "bf16":
+                continue
+            m = P.CompiledModel(doc, precision=prec)
+            t = W.uniform(tshape, 2, "t", 0.0, 1.0)
+            m.trainer_prepare(inputs, t)          # first eager step: every training GEMM shape
+            m.run(inputs)                         # inference (C3 for the ResNet-50-shaped graph)
+            print(name, pname, "tuned", flush=True)
+            del m
     k = P._kern
     k.nncb_gemm_tuning_export.restype = ctypes.c_int
     k.nncb_gemm_tuning_export.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
