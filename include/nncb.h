@@ -199,6 +199,12 @@ enum nncb_epilogue {
      * instead of rebuilt. The library re-derives the copy whenever it cannot
      * match the forward call; the caller vouches only for the bytes.       */
     NNCB_EPI_A_UNCHANGED = 16,
+    /* Inference BatchNorm of the output column, in the epilogue (forward
+     * GEMMs): y = ((acc - bn_mean) * invstd) * bn_gamma + bn_beta with
+     * invstd = (float)(1/sqrt((double)bn_var + bn_eps)) per column -- the
+     * fused group's NNCB_EW_BN_INFER, operation for operation (bitwise equal
+     * to running it as a separate pass); with NNCB_EPI_RELU the ReLU follows. */
+    NNCB_EPI_BN_AFFINE = 32,
 };
 
 typedef struct {
@@ -220,6 +226,12 @@ typedef struct {
      * K-major weights use it instead of transposing per call; routes that
      * lower the weights themselves (space-to-depth, im2col) ignore it.     */
     const float* b_kmajor;
+    /* NNCB_EPI_BN_AFFINE operands: per output column (C floats each)        */
+    const float* bn_mean;
+    const float* bn_var;
+    const float* bn_gamma;
+    const float* bn_beta;
+    double bn_eps;
 } nncb_gemm_desc;
 
 /* One launch transposing many row-major [rows][cols] matrices into [cols][rows]

@@ -125,6 +125,12 @@ struct TcParams {
     // the smem ring and descriptors are byte-identical.
     int bf16;
     int kel;
+    // inference BatchNorm (+ ReLU) of the output column in the epilogue
+    const float* bn_mean;
+    const float* bn_inv;     // (float)(1/sqrt((double)var + eps)), computed per call
+    const float* bn_gamma;
+    const float* bn_beta;
+    int relu;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -1202,6 +1208,18 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                         if (col0 + j < P.N)
                             r[j] = __float_as_uint(__fadd_rn(__uint_as_float(r[j]), __ldg(P.bias + col0 + j)));
                 }
+                if (P.bn_inv && col0 < P.N) {   // inference BatchNorm (+ ReLU): the EW BN_INFER sequence
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (col0 + j < P.N) {
+                            const int cc = static_cast<int>(col0) + j;
+                            float v = __fsub_rn(__uint_as_float(r[j]), __ldg(P.bn_mean + cc));
+                            v = __fmul_rn(__fmul_rn(v, __ldg(P.bn_inv + cc)), __ldg(P.bn_gamma + cc));
+                            v = __fadd_rn(v, __ldg(P.bn_beta + cc));
+                            if (P.relu) v = v > 0.f ? v : 0.f;
+                            r[j] = __float_as_uint(v);
+                        }
+                }
                 if (col0 < P.N && (CS || !P.nostore)) {
                     uint8_t* tile = staging + (warp - 2) * (P.stg_bufs * P.stg_cols * 128);
                     const bool full_cols = col0 + 32 <= P.N && (P.ldc % 4) == 0;
@@ -1354,6 +1372,7 @@ thread_local int g_force_tb = 0;     // 1: forward convolution with transposed (
 thread_local int g_force_bres = 0;   // 1: halo tiles with resident B (single N tile)
 thread_local int g_force_halo = 0;   // 1: 3x3 stride-1 conv through kernel-row halo patches; 2: full 3x3 patches
 thread_local int g_bf16 = 0;         // the next implicit GEMM's A and B are bf16 copies (NNCB_PREC_BF16 route)
+thread_local const float* g_bn_inv = nullptr;   // BN_AFFINE: this call's per-column invstd (device)
 
 int pick_bn(int64_t n) {
     static const int env_bn = getenv("NNCB_TC_BN") ? atoi(getenv("NNCB_TC_BN")) : 0;   // tuning knob
@@ -2028,8 +2047,25 @@ int bf16_operands(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const 
     return 0;
 }
 
+__global__ void bn_invstd_k(const float* __restrict__ var, float* __restrict__ inv, int64_t n, double eps) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x)
+        inv[c] = static_cast<float>(1.0 / sqrt(static_cast<double>(var[c]) + eps));
+}
+
 int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const float* bias, float* out,
             bool* handled) {
+    // inference BatchNorm epilogue: its per-column invstd, once per call
+    struct BnScope {
+        ~BnScope() { g_bn_inv = nullptr; }
+    } bn_scope;
+    if (d->epilogue & NNCB_EPI_BN_AFFINE) {
+        const int64_t C = d->kind <= NNCB_DENSE_WGRAD ? d->out_f : d->co;
+        float* inv = static_cast<float*>(bn_inv_buffer(ctx, static_cast<size_t>(C) * sizeof(float)));
+        if (!inv) return fail("gemm: BN_AFFINE buffer allocation failed");
+        bn_invstd_k<<<grid_for(ctx, C, 256), 256, 0, ctx->stream>>>(d->bn_var, inv, C, d->bn_eps);
+        NNCB_LAUNCHED(ctx);
+        g_bn_inv = inv;
+    }
     // the bf16 route: operands converted once here; every tile candidate and
     // the final call below read the copies (g_bf16 scopes the whole call)
     const bool bf16 = d->precision == NNCB_PREC_BF16 && bf16_eligible(d);
@@ -2221,6 +2257,11 @@ int gemm_tc_route(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const 
         dd.in_f = K;
         dd.out_f = d->co;
         dd.colstats = d->colstats;
+        dd.bn_mean = d->bn_mean;
+        dd.bn_var = d->bn_var;
+        dd.bn_gamma = d->bn_gamma;
+        dd.bn_beta = d->bn_beta;
+        dd.bn_eps = d->bn_eps;
         int rc = gemm_tc_impl(ctx, &dd, cols, ldk, b, bias, out, handled);
         if (!rc && !*handled) return fail("im2col route: dense GEMM rejected");
         return rc;
@@ -2447,6 +2488,14 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
             if (!encode_2d(&mb, b, co, kh * kw * ci, BK, P.pair ? P.bn / 2 : P.bn, false)) return 1;
         }
         P.bias = (fwd && (d->epilogue & NNCB_EPI_BIAS)) ? bias : nullptr;
+        if (fwd && (d->epilogue & NNCB_EPI_BN_AFFINE)) {
+            if (!g_bn_inv) return fail("gemm: BN_AFFINE without its per-call invstd");
+            P.bn_mean = d->bn_mean;
+            P.bn_inv = g_bn_inv;
+            P.bn_gamma = d->bn_gamma;
+            P.bn_beta = d->bn_beta;
+            P.relu = (d->epilogue & NNCB_EPI_RELU) ? 1 : 0;
+        }
         P.out = out;
         P.colstats = (fwd && (d->epilogue & NNCB_EPI_COLSTATS)) ? d->colstats : nullptr;
         if (d->epilogue & NNCB_EPI_RELU_GRAD) {

@@ -53,6 +53,19 @@ void* bf16_buffer(nncb_ctx* ctx, int which, size_t bytes) {
     return ctx->bf16_buf[which];
 }
 
+void* bn_inv_buffer(nncb_ctx* ctx, size_t bytes) {
+    if (bytes <= ctx->bn_inv_bytes) return ctx->bn_inv;
+    if (ctx->bn_inv) ctx->retired.push_back(ctx->bn_inv);
+    const size_t want = bytes < 65536 ? 65536 : bytes;
+    if (cudaMalloc(&ctx->bn_inv, want) != cudaSuccess) {
+        ctx->bn_inv = nullptr;
+        ctx->bn_inv_bytes = 0;
+        return nullptr;
+    }
+    ctx->bn_inv_bytes = want;
+    return ctx->bn_inv;
+}
+
 void* workspace(nncb_ctx* ctx, size_t bytes) {
     if (bytes <= ctx->workspace_bytes) return ctx->workspace;
     if (ctx->workspace) ctx->retired.push_back(ctx->workspace);
@@ -124,6 +137,7 @@ int nncb_destroy(nncb_ctx* c) {
     if (c->wt) cudaFree(c->wt);
     for (void* p : c->bf16_buf)
         if (p) cudaFree(p);
+    if (c->bn_inv) cudaFree(c->bn_inv);
     cudaStreamSynchronize(c->comm_stream);
     for (cudaEvent_t e : c->fork_events) cudaEventDestroy(e);
     cudaStreamDestroy(c->stream);

@@ -17,12 +17,12 @@ timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 6000 -
 # representative 3x3 convolution (s2 block, batch 256) and one fused group
 GEMM="python tools/gemm_bench.py --layers s2b_b --kinds fwd --reps 2"
 $GEMM > "$OUT/gemm_plain.log" 2>&1 || exit 1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc_gemm -s 3 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc_gemm -s 1 -c 1 \
     -o "$OUT/gemm_s2b_b_fwd" $GEMM > "$OUT/ncu_gemm.log" 2>&1
 # the same 3x3 convolution on the bf16 route (tcgen05 kind::f16)
 GEMM16="python tools/gemm_bench.py --layers s2b_b --kinds fwd --reps 2 --precision 2"
 $GEMM16 > "$OUT/gemm16_plain.log" 2>&1 || exit 1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc_gemm -s 3 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc_gemm -s 1 -c 1 \
     -o "$OUT/gemm_s2b_b_fwd_bf16" $GEMM16 > "$OUT/ncu_gemm16.log" 2>&1
 EW="python tools/ew_bench.py --reps 2"
 $EW > "$OUT/ew_plain.log" 2>&1 || exit 1
