@@ -391,6 +391,7 @@ struct Program {
             fuse_bn_statistics();
             fuse_bn_grad_reduce();
             fuse_relu_grad_epilogue();
+            fuse_bn_infer_epilogue();
             if (!std::getenv("NNC_NO_KMAJOR_BATCH")) prepare_kmajor_weights();
         }
         hint_unchanged_activations();
@@ -660,6 +661,86 @@ struct Program {
             f.g->gemm.eg_sums = static_cast<double*>(side_eg) + off;
             off += 2 * f.C;
         }
+    }
+
+    /// An inference BatchNorm (+ ReLU) group that only transforms a forward
+    /// GEMM's output y -- program exactly LOAD y, 4 x LOAD_CH, BN_INFER,
+    /// [RELU], STORE z -- moves into that GEMM's epilogue (NNCB_EPI_BN_AFFINE
+    /// [| NNCB_EPI_RELU], the same fp32 operation sequence): the GEMM writes z
+    /// and the pass over y disappears. y must have no other reader, and no
+    /// launch between the two may touch z's bytes (z is now written earlier).
+    void fuse_bn_infer_epilogue() {
+        if (std::getenv("NNC_NO_BN_INFER_EPILOGUE")) return;
+        const bool debug = std::getenv("NNC_BN_INFER_DEBUG") != nullptr;
+        auto why = [&](const Launch& L, const char* r) {
+            if (debug) std::fprintf(stderr, "bn_infer_epilogue: %s: %s\n", L.label.c_str(), r);
+        };
+        for (size_t pi = 0; pi < steps.size(); ++pi)
+            for (size_t j = 1; j < steps[pi].size(); ++j) {
+                BoundLaunch& e = steps[pi][j];
+                if (e.kind != LaunchKind::Ew || e.skip || !e.ew_prog.empty()) continue;
+                const Launch& L = *sources[pi][j];
+                int n_load = 0, n_ch = 0, n_bn = 0, n_relu = 0, n_store = 0, other = 0;
+                int y_slot = -1, z_slot = -1, bn_reg = -1, relu_reg = -1, store_reg = -1, y_reg = -1;
+                std::map<int, int> ch_slot;   // register -> slot of a LOAD_CH
+                nncb_ew_instr bn{};
+                for (const nncb_ew_instr& in : L.ew) {
+                    switch (in.op) {
+                        case NNCB_EW_LOAD: ++n_load; y_slot = in.slot; y_reg = in.dst; break;
+                        case NNCB_EW_LOAD_CH: ++n_ch; ch_slot[in.dst] = in.slot; break;
+                        case NNCB_EW_BN_INFER: ++n_bn; bn = in; bn_reg = in.dst; break;
+                        case NNCB_EW_RELU: ++n_relu; relu_reg = in.dst; if (in.a != bn_reg) ++other; break;
+                        case NNCB_EW_STORE: ++n_store; z_slot = in.slot; store_reg = in.a; break;
+                        default: ++other; break;
+                    }
+                }
+                if (other || n_load != 1 || n_ch != 4 || n_bn != 1 || n_relu > 1 || n_store != 1) {
+                    if (n_bn) why(L, "program shape");
+                    continue;
+                }
+                if (bn.a != y_reg || !ch_slot.count(bn.b) || !ch_slot.count(bn.c) || !ch_slot.count(bn.d) ||
+                    !ch_slot.count(bn.e)) {
+                    why(L, "operands");
+                    continue;
+                }
+                if (store_reg != (n_relu ? relu_reg : bn_reg)) { why(L, "store"); continue; }
+                const char* y = static_cast<const char*>(e.ptrs[y_slot]);
+                const int64_t ybytes = arg_bytes(pi, j, static_cast<size_t>(y_slot));
+                const int64_t w = last_writer(pi, j, y, ybytes);
+                if (w < 0) { why(L, "no producer"); continue; }
+                BoundLaunch& g = steps[pi][static_cast<size_t>(w)];
+                if (g.kind != LaunchKind::Gemm || g.skip || g.ptrs.back() != e.ptrs[y_slot]) { why(L, "producer not a GEMM"); continue; }
+                if (g.gemm.kind != NNCB_CONV_FWD && g.gemm.kind != NNCB_DENSE_FWD) { why(L, "not forward"); continue; }
+                if (g.gemm.epilogue & (NNCB_EPI_COLSTATS | NNCB_EPI_RELU_GRAD | NNCB_EPI_BN_AFFINE)) { why(L, "epilogue taken"); continue; }
+                // y has no other reader in any bound plan, and is not an output
+                const std::string& yname = plans[pi]->values[L.args[y_slot].slot].name;
+                bool busy = false;
+                for (size_t pk = 0; pk < plans.size() && !busy; ++pk) {
+                    const ExecutionPlan& pp = *plans[pk];
+                    for (uint32_t o : pp.output_slots) busy = busy || pp.values[o].name == yname;
+                    for (size_t k = 0; k < sources[pk].size() && !busy; ++k) {
+                        if (pk == pi && (k == j || k == static_cast<size_t>(w))) continue;
+                        const Launch& Lk = *sources[pk][k];
+                        for (size_t a = 0; a < Lk.args.size(); ++a)
+                            busy = busy || (!Lk.is_out[a] && pp.values[Lk.args[a].slot].name == yname);
+                    }
+                }
+                // z is written earlier now: nothing in between may read or write its bytes
+                const char* z = static_cast<const char*>(e.ptrs[z_slot]);
+                const int64_t zbytes = arg_bytes(pi, j, static_cast<size_t>(z_slot));
+                for (size_t k = static_cast<size_t>(w) + 1; k < j && !busy; ++k)
+                    busy = launch_touches(pi, k, z, zbytes, true) || launch_touches(pi, k, z, zbytes, false);
+                if (busy) { why(L, "y read elsewhere / z touched in between"); continue; }
+                why(L, "fused");
+                g.gemm.epilogue |= NNCB_EPI_BN_AFFINE | (n_relu ? NNCB_EPI_RELU : 0);
+                g.gemm.bn_mean = static_cast<const float*>(e.ptrs[ch_slot[bn.b]]);
+                g.gemm.bn_var = static_cast<const float*>(e.ptrs[ch_slot[bn.c]]);
+                g.gemm.bn_gamma = static_cast<const float*>(e.ptrs[ch_slot[bn.d]]);
+                g.gemm.bn_beta = static_cast<const float*>(e.ptrs[ch_slot[bn.e]]);
+                g.gemm.bn_eps = bn.imm;
+                g.ptrs.back() = e.ptrs[z_slot];
+                e.skip = true;
+            }
     }
 
     void fuse_bn_grad_reduce() {

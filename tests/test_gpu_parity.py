@@ -224,3 +224,31 @@ def test_pipelined_runs_match_sequential():
     assert [list(o) for o in sub] == [[name], [name]]
     assert np.array_equal(sub[1][name], seq[1][name])
     assert m.run_many([]) == []
+
+
+@pytest.mark.parametrize("precision", [P.PREC_TF32, P.PREC_BF16])
+def test_bn_inference_epilogue_is_bitwise_the_separate_pass(precision, monkeypatch):
+    """Inference BatchNorm + ReLU groups that only transform a forward GEMM's
+    output run in that GEMM's epilogue (NNCB_EPI_BN_AFFINE | NNCB_EPI_RELU):
+    the same fp32 operation sequence as the fused group's BN_INFER, so the
+    outputs are bitwise those of the unfused plan, with fewer launches."""
+    doc = W.resnet50(4, bn=True, image=64, classes=16)
+    x = W.uniform((4, 64, 64, 3), 1, "x")
+    outs, counts = [], []
+    for fused in (True, False):
+        if not fused:   # (read when the plan is bound, at its first run)
+            monkeypatch.setenv("NNC_NO_BN_INFER_EPILOGUE", "1")
+        m = P.CompiledModel(doc, precision=precision)
+        rng = np.random.default_rng(9)
+        for name, shape in m.weight_shapes.items():
+            if "moving_variance" in name or name.endswith(".gamma"):
+                m.set_weight(name, rng.uniform(0.5, 1.5, shape).astype(np.float32))
+            elif "moving_mean" in name or name.endswith(".beta"):
+                m.set_weight(name, rng.uniform(-0.5, 0.5, shape).astype(np.float32))
+        outs.append(m.run({"x": x})["fc"])
+        counts.append(len(m.profile_run({"x": x})))
+        del m
+    a, b = outs
+    na, nb = counts
+    assert np.array_equal(a, b)
+    assert na <= nb - 30, (na, nb)   # the stem's and every a / b conv's BN + ReLU pass
