@@ -125,9 +125,14 @@ def bf16_round(a):
 def bf16_route(K, Ck, N, kind, taps):
     """The device's NNCB_PREC_BF16 route rule (gemm_tc.cu bf16_eligible): forward
     and input-gradient contractions with aligned K blocks whose arithmetic
-    intensity K*N / (2*(Ck + N)) reaches 128."""
+    intensity K*N / (2*(Ck + N)) reaches 128; dense weight gradients
+    ("dense_wgrad": K = batch, Ck = in, N = out) when in*out / (2*(in + out))
+    reaches 128 (they run over transposed copies); convolution weight
+    gradients never."""
     if kind == "wgrad":
         return False
+    if kind == "dense_wgrad":
+        return K % 8 == 0 and Ck % 8 == 0 and N % 8 == 0 and Ck * N / (2.0 * (Ck + N)) >= 128.0
     aligned = Ck % 8 == 0 and N % 8 == 0 if taps == 1 else Ck % 64 == 0
     return aligned and K * N / (2.0 * (Ck + N)) >= 128.0
 
@@ -450,7 +455,7 @@ class F64Model:
         elif op == "dense":
             co = a["units"]
             fin = x.shape[1]
-            rw, rd = (x.shape[0], fin, co, "wgrad", 1), (co, co, fin, "dgrad", 1)
+            rw, rd = (x.shape[0], fin, co, "dense_wgrad", 1), (co, co, fin, "dgrad", 1)
             gw[name + ".weight"] = self._op(x, co, rw).T @ self._op(gy, co, rw)
             if a.get("use_bias", True):
                 gw[name + ".bias"] = gy.sum(axis=0)

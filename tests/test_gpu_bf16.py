@@ -4,7 +4,9 @@ input-gradient contractions of dense layers and convolutions, and dense
 weight gradients (over transposed bf16 copies), against float64
 products of the same bf16-rounded operands (what remains is fp32 accumulation
 order), asserting through nncb_gemm_last_path that the tensor-core path ran;
-shapes the route does not take (weight gradients, narrow K blocks) run tf32."""
+shapes the route does not take (convolution weight gradients, narrow K blocks,
+memory-bound contractions below the intensity threshold) run tf32, and are
+checked against tf32-truncated operands."""
 import ctypes
 
 import numpy as np
@@ -35,23 +37,30 @@ def run(desc, A, B, out_shape, bias=None):
     return Od.get(out_shape).astype(np.float64)
 
 
+def operand(a, route):
+    """The operand as the device multiplies it: bf16-rounded on the bf16 route,
+    tf32-truncated on the tf32 one (R64.bf16_route mirrors the device rule)."""
+    return bf16(a) if R64.bf16_route(*route) else R64.tf32_trunc(a)
+
+
 def rel(got, want):
     return float(np.max(np.abs(got - want)) / max(np.max(np.abs(want)), 1e-30))
 
 
-@pytest.mark.parametrize("batch,fin,fout", [(512, 1024, 256), (8192, 4096, 4096), (100, 72, 40)])
+@pytest.mark.parametrize("batch,fin,fout", [(512, 1024, 256), (8192, 4096, 4096), (100, 72, 40), (256, 2048, 1024)])
 def test_dense_fwd_and_dgrad_bf16(batch, fin, fout):
     rng = np.random.default_rng(batch + fin)
     x = rng.uniform(-1, 1, (batch, fin)).astype(np.float32)
     w = rng.uniform(-1, 1, (fin, fout)).astype(np.float32)
     b = rng.uniform(-1, 1, fout).astype(np.float32)
     y = run(GemmDesc(kind=0, precision=BF16, epilogue=1, batch=batch, in_f=fin, out_f=fout), x, w, (batch, fout), b)
-    want = bf16(x) @ bf16(w) + b
-    assert rel(y, want) < 1e-5
+    rf = (fin, fin, fout, "fwd", 1)
+    assert rel(y, operand(x, rf) @ operand(w, rf) + b) < 1e-5
     assert rel(y, x.astype(np.float64) @ w + b) < 2e-2          # against the exact product
     g = rng.uniform(-1, 1, (batch, fout)).astype(np.float32)
     gx = run(GemmDesc(kind=1, precision=BF16, batch=batch, in_f=fin, out_f=fout), g, w, (batch, fin))
-    assert rel(gx, bf16(g) @ bf16(w).T) < 1e-5
+    rd = (fout, fout, fin, "dgrad", 1)
+    assert rel(gx, operand(g, rd) @ operand(w, rd).T) < 1e-5
 
 
 @pytest.mark.parametrize("n,h,ci,co,k,s", [(8, 14, 256, 256, 3, 1), (4, 28, 128, 512, 1, 1), (4, 56, 64, 64, 3, 1),
@@ -63,10 +72,12 @@ def test_conv_fwd_and_dgrad_bf16(n, h, ci, co, k, s):
     oh, ow, ph, pw = R64.conv_geom(x.shape, (k, k), (s, s), True)
     geo = dict(n=n, ih=h, iw=h, ci=ci, co=co, kh=k, kw=k, sh=s, sw=s, oh=oh, ow=ow, pad_top=ph[0], pad_left=pw[0])
     y = run(GemmDesc(kind=3, precision=BF16, **geo), x, w, (n, oh, ow, co))
-    assert rel(y, R64.conv2d(bf16(x), bf16(w), None, (s, s), True)) < 1e-5
+    rf = (k * k * ci, ci, co, "fwd", k * k)
+    assert rel(y, R64.conv2d(operand(x, rf), operand(w, rf), None, (s, s), True)) < 1e-5
     g = rng.uniform(-1, 1, (n, oh, ow, co)).astype(np.float32)
     gx = run(GemmDesc(kind=4, precision=BF16, **geo), g, w, (n, h, h, ci))
-    assert rel(gx, R64.conv2d_grad_input(bf16(g), bf16(w), x.shape, (s, s), True)) < 1e-5
+    rd = (k * k * co, co, ci, "dgrad", k * k)
+    assert rel(gx, R64.conv2d_grad_input(operand(g, rd), operand(w, rd), x.shape, (s, s), True)) < 1e-5
 
 
 @pytest.mark.parametrize("batch,fin,fout", [(8192, 4096, 4096), (256, 2048, 1000)])
@@ -76,7 +87,8 @@ def test_dense_wgrad_bf16_over_transposed_copies(batch, fin, fout):
     x = rng.uniform(-1, 1, (batch, fin)).astype(np.float32)
     g = rng.uniform(-1, 1, (batch, fout)).astype(np.float32)
     gw = run(GemmDesc(kind=2, precision=BF16, batch=batch, in_f=fin, out_f=fout), x, g, (fin, fout))
-    assert rel(gw, bf16(x).T @ bf16(g)) < 1e-5
+    rw = (batch, fin, fout, "dense_wgrad", 1)
+    assert rel(gw, operand(x, rw).T @ operand(g, rw)) < 3e-5   # (a 8192-long fp32 accumulation)
 
 
 def test_wgrad_runs_tf32_under_bf16_precision():
