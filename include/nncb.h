@@ -205,6 +205,10 @@ enum nncb_epilogue {
      * fused group's NNCB_EW_BN_INFER, operation for operation (bitwise equal
      * to running it as a separate pass); with NNCB_EPI_RELU the ReLU follows. */
     NNCB_EPI_BN_AFFINE = 32,
+    /* With NNCB_EPI_BN_AFFINE: residual[row, col] (laid out like the output) is
+     * added to the BatchNorm result before the optional ReLU -- an inference
+     * residual join, relu(bn(acc) + shortcut), in the epilogue.             */
+    NNCB_EPI_RESIDUAL = 64,
 };
 
 typedef struct {
@@ -232,6 +236,8 @@ typedef struct {
     const float* bn_gamma;
     const float* bn_beta;
     double bn_eps;
+    /* NNCB_EPI_RESIDUAL operand                                              */
+    const float* residual;
 } nncb_gemm_desc;
 
 /* One launch transposing many row-major [rows][cols] matrices into [cols][rows]

@@ -680,30 +680,40 @@ struct Program {
                 BoundLaunch& e = steps[pi][j];
                 if (e.kind != LaunchKind::Ew || e.skip || !e.ew_prog.empty()) continue;
                 const Launch& L = *sources[pi][j];
-                int n_load = 0, n_ch = 0, n_bn = 0, n_relu = 0, n_store = 0, other = 0;
-                int y_slot = -1, z_slot = -1, bn_reg = -1, relu_reg = -1, store_reg = -1, y_reg = -1;
-                std::map<int, int> ch_slot;   // register -> slot of a LOAD_CH
-                nncb_ew_instr bn{};
+                // program: LOAD y, 4 x LOAD_CH, BN_INFER(y) [, LOAD r, ADD(bn, r)] [, RELU], STORE z
+                int n_ch = 0, n_bn = 0, n_relu = 0, n_store = 0, n_add = 0, other = 0;
+                int z_slot = -1, bn_reg = -1, relu_reg = -1, store_reg = -1, add_reg = -1;
+                std::map<int, int> load_slot, ch_slot;   // register -> slot of a LOAD / LOAD_CH
+                nncb_ew_instr bn{}, add{};
                 for (const nncb_ew_instr& in : L.ew) {
                     switch (in.op) {
-                        case NNCB_EW_LOAD: ++n_load; y_slot = in.slot; y_reg = in.dst; break;
+                        case NNCB_EW_LOAD: load_slot[in.dst] = in.slot; break;
                         case NNCB_EW_LOAD_CH: ++n_ch; ch_slot[in.dst] = in.slot; break;
                         case NNCB_EW_BN_INFER: ++n_bn; bn = in; bn_reg = in.dst; break;
-                        case NNCB_EW_RELU: ++n_relu; relu_reg = in.dst; if (in.a != bn_reg) ++other; break;
+                        case NNCB_EW_ADD: ++n_add; add = in; add_reg = in.dst; break;
+                        case NNCB_EW_RELU: ++n_relu; relu_reg = in.dst; if (in.a != (n_add ? add_reg : bn_reg)) ++other; break;
                         case NNCB_EW_STORE: ++n_store; z_slot = in.slot; store_reg = in.a; break;
                         default: ++other; break;
                     }
                 }
-                if (other || n_load != 1 || n_ch != 4 || n_bn != 1 || n_relu > 1 || n_store != 1) {
+                if (other || n_ch != 4 || n_bn != 1 || n_add > 1 || n_relu > 1 || n_store != 1 ||
+                    load_slot.size() != static_cast<size_t>(1 + n_add)) {
                     if (n_bn) why(L, "program shape");
                     continue;
                 }
-                if (bn.a != y_reg || !ch_slot.count(bn.b) || !ch_slot.count(bn.c) || !ch_slot.count(bn.d) ||
+                if (!load_slot.count(bn.a) || !ch_slot.count(bn.b) || !ch_slot.count(bn.c) || !ch_slot.count(bn.d) ||
                     !ch_slot.count(bn.e)) {
                     why(L, "operands");
                     continue;
                 }
-                if (store_reg != (n_relu ? relu_reg : bn_reg)) { why(L, "store"); continue; }
+                const int y_slot = load_slot[bn.a];
+                int r_slot = -1;
+                if (n_add) {   // ADD(bn, r) in either order, r an element load
+                    const int other_reg = add.a == bn_reg ? add.b : add.b == bn_reg ? add.a : -1;
+                    if (other_reg < 0 || !load_slot.count(other_reg) || other_reg == bn.a) { why(L, "add operands"); continue; }
+                    r_slot = load_slot[other_reg];
+                }
+                if (store_reg != (n_relu ? relu_reg : n_add ? add_reg : bn_reg)) { why(L, "store"); continue; }
                 const char* y = static_cast<const char*>(e.ptrs[y_slot]);
                 const int64_t ybytes = arg_bytes(pi, j, static_cast<size_t>(y_slot));
                 const int64_t w = last_writer(pi, j, y, ybytes);
@@ -725,14 +735,31 @@ struct Program {
                             busy = busy || (!Lk.is_out[a] && pp.values[Lk.args[a].slot].name == yname);
                     }
                 }
-                // z is written earlier now: nothing in between may read or write its bytes
+                // z is written earlier now: nothing in between may read or write its
+                // bytes; the residual is read earlier: nothing in between may write it
                 const char* z = static_cast<const char*>(e.ptrs[z_slot]);
                 const int64_t zbytes = arg_bytes(pi, j, static_cast<size_t>(z_slot));
-                for (size_t k = static_cast<size_t>(w) + 1; k < j && !busy; ++k)
+                for (size_t k = static_cast<size_t>(w) + 1; k < j && !busy; ++k) {
                     busy = launch_touches(pi, k, z, zbytes, true) || launch_touches(pi, k, z, zbytes, false);
+                    if (r_slot >= 0)
+                        busy = busy || launch_touches(pi, k, static_cast<const char*>(e.ptrs[r_slot]),
+                                                      arg_bytes(pi, j, static_cast<size_t>(r_slot)), true);
+                }
+                if (r_slot >= 0 && (g.gemm.kind != NNCB_CONV_FWD || g.gemm.sh != 1 || g.gemm.sw != 1) &&
+                    g.gemm.kind != NNCB_DENSE_FWD)
+                    busy = true;   // the residual must be laid out like the output
+                // the residual join in the epilogue is opt-in: its per-row residual
+                // loads ran the output-bound 1x1 convs at ~1 TB/s (a TMA side tile,
+                // as the gradient epilogue uses, is the way to make it pay)
+                static const bool residual_on = std::getenv("NNC_BN_INFER_RESIDUAL") != nullptr;
+                if (r_slot >= 0 && !residual_on) {
+                    why(L, "residual join (opt-in: NNC_BN_INFER_RESIDUAL=1)");
+                    continue;
+                }
                 if (busy) { why(L, "y read elsewhere / z touched in between"); continue; }
                 why(L, "fused");
-                g.gemm.epilogue |= NNCB_EPI_BN_AFFINE | (n_relu ? NNCB_EPI_RELU : 0);
+                g.gemm.epilogue |= NNCB_EPI_BN_AFFINE | (n_relu ? NNCB_EPI_RELU : 0) | (n_add ? NNCB_EPI_RESIDUAL : 0);
+                g.gemm.residual = n_add ? static_cast<const float*>(e.ptrs[r_slot]) : nullptr;
                 g.gemm.bn_mean = static_cast<const float*>(e.ptrs[ch_slot[bn.b]]);
                 g.gemm.bn_var = static_cast<const float*>(e.ptrs[ch_slot[bn.c]]);
                 g.gemm.bn_gamma = static_cast<const float*>(e.ptrs[ch_slot[bn.d]]);

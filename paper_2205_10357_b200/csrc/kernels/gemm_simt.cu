@@ -236,12 +236,13 @@ extern "C" int nncb_gemm_last_path(void) { return g_last_path; }
 
 namespace {
 __global__ void affine_relu_k(float* __restrict__ y, const float* __restrict__ mean, const float* __restrict__ var,
-                              const float* __restrict__ gamma, const float* __restrict__ beta, int64_t rows, int64_t C,
-                              double eps, int relu) {
+                              const float* __restrict__ gamma, const float* __restrict__ beta,
+                              const float* __restrict__ res, int64_t rows, int64_t C, double eps, int relu) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * C; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t c = i % C;
         const float inv = static_cast<float>(1.0 / sqrt(static_cast<double>(var[c]) + eps));
         float v = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(y[i], mean[c]), inv), gamma[c]), beta[c]);
+        if (res) v = __fadd_rn(v, res[i]);
         if (relu) v = v > 0.f ? v : 0.f;
         y[i] = v;
     }
@@ -254,7 +255,9 @@ int affine_relu_output(nncb_ctx* ctx, const nncb_gemm_desc* d, float* out) {
     if (d->kind != NNCB_DENSE_FWD && d->kind != NNCB_CONV_FWD) return fail("BN_AFFINE is a forward-GEMM epilogue");
     const int64_t rows = dense ? d->batch : d->n * d->oh * d->ow, C = dense ? d->out_f : d->co;
     affine_relu_k<<<grid_for(ctx, rows * C, 256), 256, 0, ctx->stream>>>(out, d->bn_mean, d->bn_var, d->bn_gamma,
-                                                                        d->bn_beta, rows, C, d->bn_eps,
+                                                                        d->bn_beta,
+                                                                        (d->epilogue & NNCB_EPI_RESIDUAL) ? d->residual : nullptr,
+                                                                        rows, C, d->bn_eps,
                                                                         (d->epilogue & NNCB_EPI_RELU) ? 1 : 0);
     NNCB_LAUNCHED(ctx);
     return 0;

@@ -131,6 +131,7 @@ struct TcParams {
     const float* bn_gamma;
     const float* bn_beta;
     int relu;
+    const float* res;        // residual added after the BatchNorm (inference join)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -1208,17 +1209,52 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                         if (col0 + j < P.N)
                             r[j] = __float_as_uint(__fadd_rn(__uint_as_float(r[j]), __ldg(P.bias + col0 + j)));
                 }
-                if (P.bn_inv && col0 < P.N) {   // inference BatchNorm (+ ReLU): the EW BN_INFER sequence
+                if (P.bn_inv && col0 < P.N) {   // inference BatchNorm (+ residual) (+ ReLU): the EW sequence
+                    const float* rrow = (P.res && valid) ? P.res + (dst - P.out) + col0 : nullptr;
+                    float rv[32];
+                    if (rrow && col0 + 32 <= P.N) {   // the row's 128 residual bytes: 8 independent 16-byte loads
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (col0 + j < P.N) {
-                            const int cc = static_cast<int>(col0) + j;
-                            float v = __fsub_rn(__uint_as_float(r[j]), __ldg(P.bn_mean + cc));
-                            v = __fmul_rn(__fmul_rn(v, __ldg(P.bn_inv + cc)), __ldg(P.bn_gamma + cc));
-                            v = __fadd_rn(v, __ldg(P.bn_beta + cc));
-                            if (P.relu) v = v > 0.f ? v : 0.f;
-                            r[j] = __float_as_uint(v);
+                        for (int q = 0; q < 8; ++q) {
+                            const float4 t4 = __ldg(reinterpret_cast<const float4*>(rrow) + q);
+                            rv[4 * q] = t4.x; rv[4 * q + 1] = t4.y; rv[4 * q + 2] = t4.z; rv[4 * q + 3] = t4.w;
                         }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) rv[j] = (rrow && col0 + j < P.N) ? __ldg(rrow + j) : 0.f;
+                    }
+                    if (col0 + 32 <= P.N) {   // per-column parameters as 16-byte loads (L1 broadcast)
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const int cc = static_cast<int>(col0) + 4 * q;
+                            const float4 m4 = __ldg(reinterpret_cast<const float4*>(P.bn_mean + cc));
+                            const float4 i4 = __ldg(reinterpret_cast<const float4*>(P.bn_inv + cc));
+                            const float4 g4 = __ldg(reinterpret_cast<const float4*>(P.bn_gamma + cc));
+                            const float4 b4 = __ldg(reinterpret_cast<const float4*>(P.bn_beta + cc));
+                            const float mm[4] = {m4.x, m4.y, m4.z, m4.w}, ii[4] = {i4.x, i4.y, i4.z, i4.w};
+                            const float gg[4] = {g4.x, g4.y, g4.z, g4.w}, bb[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const int j = 4 * q + u;
+                                float v = __fsub_rn(__uint_as_float(r[j]), mm[u]);
+                                v = __fadd_rn(__fmul_rn(__fmul_rn(v, ii[u]), gg[u]), bb[u]);
+                                if (rrow) v = __fadd_rn(v, rv[j]);
+                                if (P.relu) v = v > 0.f ? v : 0.f;
+                                r[j] = __float_as_uint(v);
+                            }
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (col0 + j < P.N) {
+                                const int cc = static_cast<int>(col0) + j;
+                                float v = __fsub_rn(__uint_as_float(r[j]), __ldg(P.bn_mean + cc));
+                                v = __fmul_rn(__fmul_rn(v, __ldg(P.bn_inv + cc)), __ldg(P.bn_gamma + cc));
+                                v = __fadd_rn(v, __ldg(P.bn_beta + cc));
+                                if (rrow) v = __fadd_rn(v, rv[j]);
+                                if (P.relu) v = v > 0.f ? v : 0.f;
+                                r[j] = __float_as_uint(v);
+                            }
+                    }
                 }
                 if (col0 < P.N && (CS || !P.nostore)) {
                     uint8_t* tile = staging + (warp - 2) * (P.stg_bufs * P.stg_cols * 128);
@@ -2262,6 +2298,7 @@ int gemm_tc_route(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const 
         dd.bn_gamma = d->bn_gamma;
         dd.bn_beta = d->bn_beta;
         dd.bn_eps = d->bn_eps;
+        dd.residual = d->residual;
         int rc = gemm_tc_impl(ctx, &dd, cols, ldk, b, bias, out, handled);
         if (!rc && !*handled) return fail("im2col route: dense GEMM rejected");
         return rc;
@@ -2495,6 +2532,9 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
             P.bn_gamma = d->bn_gamma;
             P.bn_beta = d->bn_beta;
             P.relu = (d->epilogue & NNCB_EPI_RELU) ? 1 : 0;
+            P.res = (d->epilogue & NNCB_EPI_RESIDUAL) ? d->residual : nullptr;
+            if ((d->epilogue & NNCB_EPI_RESIDUAL) && (!d->residual || P.out_s != 1))
+                return fail("gemm: NNCB_EPI_RESIDUAL needs a residual laid out like the output");
         }
         P.out = out;
         P.colstats = (fwd && (d->epilogue & NNCB_EPI_COLSTATS)) ? d->colstats : nullptr;

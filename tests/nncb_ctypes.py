@@ -17,7 +17,8 @@ class GemmDesc(ctypes.Structure):
                [("colstats", ctypes.c_void_p), ("eg_mask", ctypes.c_void_p), ("eg_res", ctypes.c_void_p),
                 ("eg_x", ctypes.c_void_p), ("eg_stats", ctypes.c_void_p), ("eg_sums", ctypes.c_void_p),
                 ("b_kmajor", ctypes.c_void_p), ("bn_mean", ctypes.c_void_p), ("bn_var", ctypes.c_void_p),
-                ("bn_gamma", ctypes.c_void_p), ("bn_beta", ctypes.c_void_p), ("bn_eps", ctypes.c_double)]
+                ("bn_gamma", ctypes.c_void_p), ("bn_beta", ctypes.c_void_p), ("bn_eps", ctypes.c_double),
+                ("residual", ctypes.c_void_p)]
 
 
 class TransposeJob(ctypes.Structure):
