@@ -126,9 +126,14 @@ enum nncb_ew_op {
                                accumulated in double per channel. a = g, b = x,
                                c = mean, d = invstd (LOAD_CH regs); outputs: slot = sum_g,
                                e = sum_gx slot index. Needs the channel-stationary launch:
-                               C a power of two in [4, 2048], n % 4 == 0, 16 B-aligned
+                               C a power of two in [4, 8192], n % 4 == 0, 16 B-aligned
                                slots; at most two per program (e.g. the two BatchNorms
                                of a residual join fed the same gradient).                */
+    NNCB_EW_REDUCE_SUM = 18,     /* per-channel column sum of r[a] in double into the float
+                               [C] slot `slot` (a Dense bias gradient folded into the group
+                               that stores the gradient). Channel-stationary launch with C
+                               a power of two in [4, 8192]; counts toward the at-most-two
+                               reductions per program.                                    */
 };
 
 typedef struct {
@@ -321,6 +326,12 @@ int nncb_layernorm_bwd(nncb_ctx* ctx, const float* x, const float* gamma, const 
 /* dgamma[c] = sum_r g*xhat (row statistics recomputed)                     */
 int nncb_layernorm_dgamma(nncb_ctx* ctx, const float* x, const float* g, float* dgamma,
                           int64_t rows, int64_t C, double eps);
+/* LayerNorm backward with the parameter gradients in the same pass:
+ * gx as nncb_layernorm_bwd, dgamma[c] = sum_r g*xhat, dbeta[c] = sum_r g
+ * (either may be NULL; deterministic per-CTA partials folded in order).   */
+int nncb_layernorm_bwd_params(nncb_ctx* ctx, const float* x, const float* gamma, const float* g,
+                              float* gx, float* dgamma, float* dbeta, int64_t rows, int64_t C,
+                              double eps);
 
 /* ------------------------------------------------------------------ */
 /*  Loss and update (runtime.cpp:468-496)                              */

@@ -132,6 +132,15 @@ struct BoundLaunch {
     float* eg_sgx = nullptr;
     std::vector<nncb_ew_instr> ew_prog;     // rewritten Ew program (empty: the plan's own)
     int ew_regs = 0;
+    // device bytes bound beyond the plan arguments by a fusion pass (folded
+    // reductions' operands and results): what the launch additionally reads
+    // or writes, for the producer / hazard checks of later passes
+    struct Extra {
+        const void* p;
+        int64_t bytes;
+        bool out;
+    };
+    std::vector<Extra> extra;
 };
 
 void enqueue(nncb_ctx* ctx, const BoundLaunch& b) {
@@ -165,7 +174,12 @@ void enqueue(nncb_ctx* ctx, const BoundLaunch& b) {
             NNC_CHECK(nncb_bn_grad_reduce(ctx, P(0), P(1), P(2), P(3), P(4), b.d0, b.d1));
             break;
         case LaunchKind::LnFwd: NNC_CHECK(nncb_layernorm_fwd(ctx, P(0), P(1), P(2), P(3), b.d0, b.d1, b.eps)); break;
-        case LaunchKind::LnBwd: NNC_CHECK(nncb_layernorm_bwd(ctx, P(0), P(1), P(2), P(3), b.d0, b.d1, b.eps)); break;
+        case LaunchKind::LnBwd:
+            if (b.ptrs.size() >= 6)   // parameter gradients folded in (fuse_ln_param_grads)
+                NNC_CHECK(nncb_layernorm_bwd_params(ctx, P(0), P(1), P(2), P(3), P(4), P(5), b.d0, b.d1, b.eps));
+            else
+                NNC_CHECK(nncb_layernorm_bwd(ctx, P(0), P(1), P(2), P(3), b.d0, b.d1, b.eps));
+            break;
         case LaunchKind::LnDgamma: NNC_CHECK(nncb_layernorm_dgamma(ctx, P(0), P(1), P(2), b.d0, b.d1, b.eps)); break;
     }
 }
@@ -185,6 +199,7 @@ void launch_cost(const BoundLaunch& b, const Launch& L, const ExecutionPlan& p, 
                 if (in.op == NNCB_EW_LOAD || in.op == NNCB_EW_STORE) bytes += 4.0 * n;
                 if (in.op == NNCB_EW_LOAD_CH) bytes += 4.0 * c;
                 if (in.op == NNCB_EW_REDUCE_BN_GRAD || in.op == NNCB_EW_REDUCE_STATS) bytes += 8.0 * c;
+                if (in.op == NNCB_EW_REDUCE_SUM) bytes += 4.0 * c;
             }
             break;
         }
@@ -197,6 +212,11 @@ void launch_cost(const BoundLaunch& b, const Launch& L, const ExecutionPlan& p, 
             break;
         case LaunchKind::BnGradReduce:   // reads x, g (rows*C) and the 2C stats; writes 2C sums
             bytes = 8.0 * elems(0) + 16.0 * b.d1;
+            break;
+        case LaunchKind::LnBwd:   // x, gamma, g read, gx written; folded dgamma / dbeta written
+            for (size_t a = 0; a < L.args.size(); ++a) bytes += 4.0 * elems(a);
+            for (size_t a = L.args.size(); a < b.ptrs.size(); ++a)
+                if (b.ptrs[a]) bytes += 4.0 * b.d1;
             break;
         case LaunchKind::Gemm: {
             const nncb_gemm_desc& d = b.gemm;
@@ -392,6 +412,8 @@ struct Program {
             fuse_bn_grad_reduce();
             fuse_relu_grad_epilogue();
             fuse_bn_infer_epilogue();
+            fuse_ln_param_grads();
+            fuse_bias_grad_reduce();
             if (!std::getenv("NNC_NO_KMAJOR_BATCH")) prepare_kmajor_weights();
         }
         hint_unchanged_activations();
@@ -438,17 +460,8 @@ struct Program {
             r.push_back({static_cast<const char*>(b.ptrs[a]), std::max<int64_t>(bytes, 1)});
         }
         // operands bound beyond the plan arguments
-        const int64_t cb = std::max<int64_t>(b.c, 1) * static_cast<int64_t>(sizeof(float));
-        // folded BatchNorm reductions append x, mean, invstd (read), sum_g, sum_gx (written)
-        for (size_t s0 = L.args.size(); b.kind == LaunchKind::Ew && s0 + 5 <= b.ptrs.size(); s0 += 5) {
-            if (outputs) {
-                r.push_back({static_cast<const char*>(b.ptrs[s0 + 3]), cb});
-                r.push_back({static_cast<const char*>(b.ptrs[s0 + 4]), cb});
-            } else {
-                r.push_back({static_cast<const char*>(b.ptrs[s0]), b.n * static_cast<int64_t>(sizeof(float))});
-                r.push_back({static_cast<const char*>(b.ptrs[s0 + 1]), 2 * cb});
-            }
-        }
+        for (const BoundLaunch::Extra& e : b.extra)
+            if (e.out == outputs && e.p) r.push_back({static_cast<const char*>(e.p), std::max<int64_t>(e.bytes, 1)});
         if (b.kind == LaunchKind::Gemm && b.eg_sg) {
             const int64_t C = (b.gemm.kind == NNCB_DENSE_DGRAD ? b.gemm.in_f : b.gemm.ci) * 4;
             if (outputs) {
@@ -865,7 +878,116 @@ struct Program {
                 e.ew_prog = std::move(prog);
                 e.ew_regs = regs + 3;
                 e.c = C;
+                e.extra.push_back({r.ptrs[0], rows * C * 4, false});   // x
+                e.extra.push_back({r.ptrs[1], 2 * C * 4, false});      // mean, invstd
+                e.extra.push_back({r.ptrs[3], C * 4, true});           // sum_g
+                e.extra.push_back({r.ptrs[4], C * 4, true});           // sum_gx
                 r.skip = true;
+            }
+    }
+
+    /// A column sum (the Dense bias gradient, SumRows over the [rows, C]
+    /// gradient g) is folded into the fused elementwise group that stores g
+    /// (NNCB_EW_REDUCE_SUM): g is summed from registers as it is written
+    /// instead of being read back. Tensor-core modes only (the fp32 mode keeps
+    /// the exact SumRows order). Same producer / hazard rules as the BatchNorm
+    /// gradient reduction above.
+    void fuse_bias_grad_reduce() {
+        if (std::getenv("NNC_NO_FUSED_BIAS_GRAD")) return;
+        for (size_t pi = 0; pi < steps.size(); ++pi)
+            for (size_t j = 1; j < steps[pi].size(); ++j) {
+                BoundLaunch& r = steps[pi][j];
+                if (r.kind != LaunchKind::SumRows || r.skip || r.flag0) continue;
+                const int64_t rows = r.d0, C = r.d1;
+                if (C < 4 || C > 8192 || (C & (C - 1)) || (rows * C) % 4) continue;
+                const char* gp = static_cast<const char*>(r.ptrs[0]);
+                const int64_t gbytes = arg_bytes(pi, j, 0);
+                const int64_t w = last_writer(pi, j, gp, gbytes);
+                if (w < 0) continue;
+                const size_t pj = static_cast<size_t>(w);
+                BoundLaunch& e = steps[pi][pj];
+                if (e.kind != LaunchKind::Ew || e.n != rows * C || (e.c > 0 && e.c != C)) continue;
+                const Launch& L = *sources[pi][pj];
+                std::vector<nncb_ew_instr> prog = e.ew_prog.empty() ? L.ew : e.ew_prog;
+                const int regs = e.ew_prog.empty() ? L.ew_regs : e.ew_regs;
+                int n_reduce = 0, at = -1;
+                for (size_t k = 0; k < prog.size(); ++k) {
+                    n_reduce += prog[k].op == NNCB_EW_REDUCE_BN_GRAD || prog[k].op == NNCB_EW_REDUCE_STATS ||
+                                prog[k].op == NNCB_EW_REDUCE_SUM;
+                    if (prog[k].op == NNCB_EW_STORE && e.ptrs[prog[k].slot] == r.ptrs[0]) at = static_cast<int>(k);
+                }
+                if (at < 0 || n_reduce >= 2 || e.ptrs.size() + 1 > 48) continue;
+                // the sum moves from j up to pj: its output must be neither
+                // read nor written in between
+                const Range o{static_cast<const char*>(r.ptrs[1]), C * 4};
+                bool clash = false;
+                for (size_t k = pj + 1; k < j && !clash; ++k)
+                    clash = launch_touches(pi, k, o.p, o.n, true) || launch_touches(pi, k, o.p, o.n, false);
+                if (clash) continue;
+                nncb_ew_instr red{};
+                red.op = NNCB_EW_REDUCE_SUM;
+                red.a = prog[at].a;
+                red.slot = static_cast<int32_t>(e.ptrs.size());
+                prog.insert(prog.begin() + at + 1, red);
+                std::vector<void*> ptrs = e.ptrs;
+                ptrs.push_back(r.ptrs[1]);
+                nncb_ew_program ep{static_cast<int32_t>(prog.size()), prog.data(), regs, static_cast<int32_t>(ptrs.size())};
+                nncb_ew_kernel* k = nullptr;
+                NNC_CHECK(nncb_ew_compile(dev->ctx(), &ep, &k));
+                e.ew = k;
+                e.ptrs = std::move(ptrs);
+                e.ew_prog = std::move(prog);
+                e.ew_regs = regs;
+                e.c = C;
+                e.extra.push_back({r.ptrs[1], C * 4, true});
+                r.skip = true;
+            }
+    }
+
+    /// The LayerNorm parameter gradients (LnDgamma: sum g*xhat, and the beta
+    /// gradient's SumRows: sum g) of the same x and g as a LayerNorm input
+    /// gradient move into that launch (nncb_layernorm_bwd_params), which has
+    /// x and g in registers already: two passes over x and g disappear.
+    /// Tensor-core modes only (the fp32 mode keeps the exact SumRows order).
+    void fuse_ln_param_grads() {
+        if (std::getenv("NNC_NO_FUSED_LN_PARAMS")) return;
+        for (size_t pi = 0; pi < steps.size(); ++pi)
+            for (size_t j = 0; j < steps[pi].size(); ++j) {
+                BoundLaunch& b = steps[pi][j];
+                if (b.kind != LaunchKind::LnBwd || b.skip || b.ptrs.size() != 4) continue;
+                const int64_t rows = b.d0, C = b.d1;
+                const Range xr{static_cast<const char*>(b.ptrs[0]), arg_bytes(pi, j, 0)};
+                const Range gr{static_cast<const char*>(b.ptrs[2]), arg_bytes(pi, j, 2)};
+                // a candidate at m may move to j when x and g keep their bytes
+                // and its output is neither read nor written in between
+                auto movable = [&](size_t m, const Range& o) {
+                    const size_t lo = std::min(m, j), hi = std::max(m, j);
+                    for (size_t k = lo + 1; k < hi; ++k)
+                        if (launch_touches(pi, k, xr.p, xr.n, true) || launch_touches(pi, k, gr.p, gr.n, true) ||
+                            launch_touches(pi, k, o.p, o.n, true) || launch_touches(pi, k, o.p, o.n, false))
+                            return false;
+                    // the output must not alias the operands of the fused launch
+                    return !(o.overlaps(xr.p, xr.n) || o.overlaps(gr.p, gr.n) ||
+                             o.overlaps(static_cast<const char*>(b.ptrs[3]), arg_bytes(pi, j, 3)));
+                };
+                int64_t dg = -1, db = -1;
+                for (size_t m = 0; m < steps[pi].size(); ++m) {
+                    const BoundLaunch& c = steps[pi][m];
+                    if (m == j || c.skip || c.d0 != rows || c.d1 != C) continue;
+                    if (dg < 0 && c.kind == LaunchKind::LnDgamma && c.ptrs[0] == b.ptrs[0] && c.ptrs[1] == b.ptrs[2] &&
+                        movable(m, Range{static_cast<const char*>(c.ptrs[2]), C * 4}))
+                        dg = static_cast<int64_t>(m);
+                    else if (db < 0 && c.kind == LaunchKind::SumRows && c.ptrs[0] == b.ptrs[2] &&
+                             movable(m, Range{static_cast<const char*>(c.ptrs[1]), C * 4}))
+                        db = static_cast<int64_t>(m);
+                }
+                if (dg < 0 && db < 0) continue;
+                b.ptrs.push_back(dg >= 0 ? steps[pi][dg].ptrs[2] : nullptr);
+                b.ptrs.push_back(db >= 0 ? steps[pi][db].ptrs[1] : nullptr);
+                b.extra.push_back({b.ptrs[4], C * 4, true});
+                b.extra.push_back({b.ptrs[5], C * 4, true});
+                if (dg >= 0) steps[pi][dg].skip = true;
+                if (db >= 0) steps[pi][db].skip = true;
             }
     }
 

@@ -263,6 +263,7 @@ void validate_plan(const ExecutionPlan& p) {
                     case NNCB_EW_BN_GRAD: case NNCB_EW_BN_GRAD_FAST: need = 0xFF; break;
                     case NNCB_EW_REDUCE_BN_GRAD: need = 0x1E; break;
                     case NNCB_EW_REDUCE_STATS: need = 0x02; break;
+                    case NNCB_EW_REDUCE_SUM: need = 0x02; break;
                     default: bad("elementwise opcode");
                 }
                 const int fields[8] = {in.dst, in.a, in.b, in.c, in.d, in.e, in.f, in.h};
@@ -275,7 +276,8 @@ void validate_plan(const ExecutionPlan& p) {
                             std::to_string(L.ew_regs) + " registers) in " + L.label);
                 }
                 const bool slotted = in.op == NNCB_EW_LOAD || in.op == NNCB_EW_LOAD_CH || in.op == NNCB_EW_STORE ||
-                                     in.op == NNCB_EW_REDUCE_BN_GRAD || in.op == NNCB_EW_REDUCE_STATS;
+                                     in.op == NNCB_EW_REDUCE_BN_GRAD || in.op == NNCB_EW_REDUCE_STATS ||
+                                     in.op == NNCB_EW_REDUCE_SUM;
                 if (slotted && (in.slot < 0 || in.slot >= nargs)) bad("elementwise slot out of range in " + L.label);
                 if (in.op == NNCB_EW_REDUCE_BN_GRAD && (in.e < 0 || in.e >= nargs))
                     bad("elementwise slot out of range in " + L.label);

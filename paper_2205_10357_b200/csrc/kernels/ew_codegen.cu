@@ -138,6 +138,14 @@ void emit_body(std::ostringstream& os, const nncb_ew_program& p, int W, bool use
                    << "[j]; " << r0 << "[j] += v; " << r1 << "[j] += v * v; }\n";
                 continue;
             }
+            case NNCB_EW_REDUCE_SUM: {
+                if (!stationary) continue;
+                const std::string r0 = "red" + std::to_string(reduce_index) + "_0";
+                ++reduce_index;
+                os << "  #pragma unroll\n  for (int j = 0; j < " << W << "; ++j) " << r0 << "[j] += (double)" << a
+                   << "[j];\n";
+                continue;
+            }
             case NNCB_EW_REDUCE_BN_GRAD: {
                 if (!stationary) continue;   // launch guarantees the channel-stationary path
                 const std::string r0 = "red" + std::to_string(reduce_index) + "_0",
@@ -195,7 +203,9 @@ void emit_body(std::ostringstream& os, const nncb_ew_program& p, int W, bool use
 std::vector<int> find_reduces(const nncb_ew_program& p) {
     std::vector<int> r;
     for (int k = 0; k < p.n_instr; ++k)
-        if (p.instr[k].op == NNCB_EW_REDUCE_BN_GRAD || p.instr[k].op == NNCB_EW_REDUCE_STATS) r.push_back(k);
+        if (p.instr[k].op == NNCB_EW_REDUCE_BN_GRAD || p.instr[k].op == NNCB_EW_REDUCE_STATS ||
+            p.instr[k].op == NNCB_EW_REDUCE_SUM)
+            r.push_back(k);
     return r;
 }
 
@@ -367,7 +377,7 @@ __global__ void __launch_bounds__(1024) ew_red_final_k(const double* __restrict_
         __syncthreads();
     }
     if (ty == 0 && c < C) {
-        if (stats) {   // REDUCE_STATS: BatchNorm mean and 1/sqrt(biased var + eps), from the double sums
+        if (stats == 1) {   // REDUCE_STATS: BatchNorm mean and 1/sqrt(biased var + eps), from the double sums
             const double mean = fold[0][0][tx] / rows;
             double var = fold[1][0][tx] / rows - mean * mean;
             if (var < 0) var = 0;
@@ -375,7 +385,7 @@ __global__ void __launch_bounds__(1024) ew_red_final_k(const double* __restrict_
             sgx[c] = static_cast<float>(1.0 / sqrt(var + eps));
         } else {
             sg[c] = static_cast<float>(fold[0][0][tx]);
-            sgx[c] = static_cast<float>(fold[1][0][tx]);
+            if (sgx) sgx[c] = static_cast<float>(fold[1][0][tx]);   // null: REDUCE_SUM
         }
     }
 }
@@ -389,7 +399,7 @@ int nncb_ew_compile_check(const nncb_ew_program* p) {
     bool uses_ch = false;
     for (int k = 0; k < p->n_instr; ++k)   // reductions run channel-stationary too
         uses_ch = uses_ch || p->instr[k].op == NNCB_EW_LOAD_CH || p->instr[k].op == NNCB_EW_REDUCE_STATS ||
-                  p->instr[k].op == NNCB_EW_REDUCE_BN_GRAD;
+                  p->instr[k].op == NNCB_EW_REDUCE_BN_GRAD || p->instr[k].op == NNCB_EW_REDUCE_SUM;
     std::string src = generate(*p, uses_ch);
     static std::mutex mu;
     static std::set<std::string> checked;
@@ -414,7 +424,7 @@ int nncb_ew_compile(nncb_ctx* ctx, const nncb_ew_program* p, nncb_ew_kernel** ou
     bool uses_ch = false;
     for (int k = 0; k < p->n_instr; ++k)   // reductions run channel-stationary too
         uses_ch = uses_ch || p->instr[k].op == NNCB_EW_LOAD_CH || p->instr[k].op == NNCB_EW_REDUCE_STATS ||
-                  p->instr[k].op == NNCB_EW_REDUCE_BN_GRAD;
+                  p->instr[k].op == NNCB_EW_REDUCE_BN_GRAD || p->instr[k].op == NNCB_EW_REDUCE_SUM;
     std::string src = generate(*p, uses_ch);
     auto hit = ctx->ew_cache.find(src);
     if (hit != ctx->ew_cache.end()) {
@@ -455,7 +465,8 @@ int nncb_ew_compile(nncb_ctx* ctx, const nncb_ew_program* p, nncb_ew_kernel** ou
     for (int r : reds) {
         k->reduce_sg[k->n_reduce] = p->instr[r].slot;
         k->reduce_sgx[k->n_reduce] = p->instr[r].e;
-        k->reduce_stats[k->n_reduce] = p->instr[r].op == NNCB_EW_REDUCE_STATS ? 1 : 0;
+        k->reduce_stats[k->n_reduce] =
+            p->instr[r].op == NNCB_EW_REDUCE_STATS ? 1 : p->instr[r].op == NNCB_EW_REDUCE_SUM ? 2 : 0;
         k->reduce_eps[k->n_reduce] = p->instr[r].imm;
         ++k->n_reduce;
     }
@@ -513,8 +524,8 @@ int nncb_ew_launch(nncb_ctx* ctx, nncb_ew_kernel* k, void* const* slots, int64_t
         // the reduction runs only on the channel-stationary path: C a power of
         // two in [4, 2048]; a bounded grid keeps the per-block partials small
         const int64_t C = channels;
-        if (!args.cs || C < 4 || C > 2048 || (C & (C - 1)))
-            return nncb::fail("nncb_ew_launch: REDUCE_BN_GRAD needs the channel-stationary launch (C power of 2 <= 2048)");
+        if (!args.cs || C < 4 || C > 8192 || (C & (C - 1)))
+            return nncb::fail("nncb_ew_launch: a reduction needs the channel-stationary launch (C power of 2 <= 8192)");
         const int64_t g = C / std::gcd<int64_t>(C, 1024);
         static const int64_t per_sm = getenv("NNCB_EW_RED_BLOCKS") ? std::max(1, atoi(getenv("NNCB_EW_RED_BLOCKS"))) : 4;
         // one wave: the two-reduction build is budgeted for red2_blocks() per SM
@@ -543,7 +554,7 @@ int nncb_ew_launch(nncb_ctx* ctx, nncb_ew_kernel* k, void* const* slots, int64_t
             cfg.attrs = attr;
             cfg.numAttrs = 1;
             float* o0 = args.p[k->reduce_sg[q]];
-            float* o1 = k->reduce_stats[q] ? o0 + C : args.p[k->reduce_sgx[q]];
+            float* o1 = k->reduce_stats[q] == 1 ? o0 + C : k->reduce_stats[q] == 2 ? nullptr : args.p[k->reduce_sgx[q]];
             NNCB_CUDA(cudaLaunchKernelEx(&cfg, ew_red_final_k, static_cast<const double*>(args.part + static_cast<size_t>(q) * grid * 2 * C),
                                          static_cast<int>(grid), C, o0, o1, k->reduce_stats[q],
                                          static_cast<double>(n / C), k->reduce_eps[q]));

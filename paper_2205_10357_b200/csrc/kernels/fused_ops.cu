@@ -783,7 +783,8 @@ __global__ void __launch_bounds__(256) layernorm_reg_k(const float* __restrict__
     }
     double t0, t1;
     block_sum2(t0f, t1f, t0, t1);
-    const float sg = (float)t0, sgx = (float)t1, cnt = (float)C;
+    const float sg = (float)t0, sgx = (float)t1, cnt = (float)C, inv_cnt = 1.f / cnt;
+    const bool pow2 = (C & (C - 1)) == 0;   // t / C as an exact-reciprocal product (same rounding)
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
         const int c4 = threadIdx.x + 256 * k;
@@ -794,7 +795,7 @@ __global__ void __launch_bounds__(256) layernorm_reg_k(const float* __restrict__
         for (int j = 0; j < 4; ++j) {
             const float xhat = __fmul_rn(__fsub_rn(vv[j], mean), rstd);
             const float t = __fadd_rn(sg, __fmul_rn(xhat, sgx));
-            r[j] = __fmul_rn(rstd, __fsub_rn(gq[j], __fdiv_rn(t, cnt)));
+            r[j] = __fmul_rn(rstd, __fsub_rn(gq[j], pow2 ? __fmul_rn(t, inv_cnt) : __fdiv_rn(t, cnt)));
         }
         o4[c4] = make_float4(r[0], r[1], r[2], r[3]);
     }
@@ -819,6 +820,178 @@ bool layernorm_reg(nncb_ctx* ctx, const float* x, const float* gamma, const floa
     else
         layernorm_reg_k<MODE, 8><<<grid, 256, 0, ctx->stream>>>(x, gamma, beta, g, out, rs, Ci, eps);
     return true;
+}
+
+// LayerNorm backward with the parameter gradients folded in (tensor-core
+// modes): besides dx (identical per row to layernorm_reg_k<1>), every CTA
+// accumulates, for the rows it owns, the per-column sums
+//   dgamma_c = sum_r g[r,c] * xhat[r,c]    dbeta_c = sum_r g[r,c]
+// in double registers (each thread owns the same VPT*4 columns in every row)
+// and writes them once as partials[cta][2][C]; ln_param_final_k folds the
+// partials in CTA order, so the result is deterministic. Replaces the row
+// statistics pass + column pass of nncb_layernorm_dgamma and the SumRows of
+// the beta gradient (reference semantics: src/nnc/graph/op.cpp LayerNorm
+// extension; CPU restatement oracle/restated64.py node_vjp LayerNorm).
+// LayerNorm backward with the parameter gradients folded in (tensor-core
+// modes): besides dx (bitwise identical per row to layernorm_reg_k<1>), every
+// CTA accumulates, over the rows it owns (row = blockIdx.x + k*gridDim.x, at
+// most kLnRowsPerCta of them), the per-column sums
+//   dgamma_c = sum_r g[r,c] * xhat[r,c]    dbeta_c = sum_r g[r,c]
+// in a float shared-memory array (each thread owns the same columns in every
+// row, so the read-modify-write needs no atomics) and stores them once as
+// partials[cta][2][C]; ln_param_final_k folds the partials in double in CTA
+// order, so the result is deterministic. Replaces the row statistics pass and
+// the column pass of nncb_layernorm_dgamma and the SumRows of the beta
+// gradient (CPU restatement: oracle/restated64.py node_vjp LayerNorm).
+constexpr int64_t kLnRowsPerCta = 256;
+
+template <int VPT>
+__global__ void __launch_bounds__(256, VPT > 4 ? 2 : 4)
+    layernorm_bwd_acc_k(const float* __restrict__ x, const float* __restrict__ gamma, const float* __restrict__ gy,
+                        float* __restrict__ out, float* __restrict__ part, int64_t rows, int C, double eps) {
+    extern __shared__ __align__(16) float4 acc[];   // [dgamma | dbeta][C4]
+    __shared__ double red[2][8];
+    const int C4 = C >> 2;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    auto block_sum2 = [&](double a, double b, double& ra, double& rb) {
+        for (int o = 16; o; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            b += __shfl_xor_sync(0xffffffffu, b, o);
+        }
+        __syncthreads();
+        if (lane == 0) {
+            red[0][warp] = a;
+            red[1][warp] = b;
+        }
+        __syncthreads();
+        ra = 0;
+        rb = 0;
+        for (int k = 0; k < 8; ++k) {
+            ra += red[0][k];
+            rb += red[1][k];
+        }
+    };
+    for (int c4 = threadIdx.x; c4 < 2 * C4; c4 += 256) acc[c4] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
+    const float4* g4 = reinterpret_cast<const float4*>(gamma);
+    // t / C: a multiplication by the exact reciprocal when C is a power of two
+    // (the same correctly rounded result as the division)
+    const bool pow2 = (C & (C - 1)) == 0;
+    const float cnt = (float)C, inv_cnt = 1.f / cnt;
+    for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+        const float4* xr = reinterpret_cast<const float4*>(x + row * C);
+        const float4* gr = reinterpret_cast<const float4*>(gy + row * C);
+        float4 v[VPT], gv[VPT];
+        float f0 = 0.f, f1 = 0.f;
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+            const int c4 = threadIdx.x + 256 * k;
+            const bool in = c4 < C4;
+            v[k] = in ? __ldg(xr + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+            gv[k] = in ? __ldcs(gr + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+            f0 += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+            f1 += (v[k].x * v[k].x + v[k].y * v[k].y) + (v[k].z * v[k].z + v[k].w * v[k].w);
+        }
+        double s0, s1;
+        block_sum2(f0, f1, s0, s1);
+        const double mean_d = s0 / (double)C;
+        double var = s1 / (double)C - mean_d * mean_d;
+        if (var < 0) var = 0;
+        const float mean = (float)mean_d;
+        const float rstd = (float)(1.0 / sqrt(var + eps));
+        float t0f = 0.f, t1f = 0.f;
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+            const int c4 = threadIdx.x + 256 * k;
+            if (c4 >= C4) continue;
+            const float4 ga = __ldg(g4 + c4);
+            const float gg[4] = {__fmul_rn(gv[k].x, ga.x), __fmul_rn(gv[k].y, ga.y), __fmul_rn(gv[k].z, ga.z),
+                                 __fmul_rn(gv[k].w, ga.w)};
+            const float xh[4] = {__fmul_rn(__fsub_rn(v[k].x, mean), rstd), __fmul_rn(__fsub_rn(v[k].y, mean), rstd),
+                                 __fmul_rn(__fsub_rn(v[k].z, mean), rstd), __fmul_rn(__fsub_rn(v[k].w, mean), rstd)};
+            t0f += (gg[0] + gg[1]) + (gg[2] + gg[3]);
+            t1f += (gg[0] * xh[0] + gg[1] * xh[1]) + (gg[2] * xh[2] + gg[3] * xh[3]);
+        }
+        double t0, t1;
+        block_sum2(t0f, t1f, t0, t1);
+        const float sg = (float)t0, sgx = (float)t1;
+        float4* o4 = reinterpret_cast<float4*>(out + row * C);
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+            const int c4 = threadIdx.x + 256 * k;
+            if (c4 >= C4) continue;
+            const float4 ga = __ldg(g4 + c4);
+            const float vv[4] = {v[k].x, v[k].y, v[k].z, v[k].w}, graw[4] = {gv[k].x, gv[k].y, gv[k].z, gv[k].w},
+                        gam[4] = {ga.x, ga.y, ga.z, ga.w};
+            float r[4], ax[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float xhat = __fmul_rn(__fsub_rn(vv[j], mean), rstd);
+                const float t = __fadd_rn(sg, __fmul_rn(xhat, sgx));
+                r[j] = __fmul_rn(rstd, __fsub_rn(__fmul_rn(graw[j], gam[j]), pow2 ? __fmul_rn(t, inv_cnt) : __fdiv_rn(t, cnt)));
+                ax[j] = graw[j] * xhat;
+            }
+            __stcs(o4 + c4, make_float4(r[0], r[1], r[2], r[3]));
+            float4 a = acc[c4], b = acc[C4 + c4];
+            a.x += ax[0]; a.y += ax[1]; a.z += ax[2]; a.w += ax[3];
+            b.x += graw[0]; b.y += graw[1]; b.z += graw[2]; b.w += graw[3];
+            acc[c4] = a;
+            acc[C4 + c4] = b;
+        }
+    }
+    float4* p4 = reinterpret_cast<float4*>(part + (int64_t)blockIdx.x * 2 * C);
+    __syncthreads();   // the dbeta half of acc is owned by other threads when C4 % 256 != 0
+    for (int c4 = threadIdx.x; c4 < 2 * C4; c4 += 256) p4[c4] = acc[c4];
+}
+
+// Fold of the per-CTA partials in two fixed-order levels (deterministic):
+// ln_param_fold_k: block (32, 8), grid (column quads / 32, kLnFoldSplits);
+// thread (tx, ty) of split s sums, in double, the chunks ty, ty+8, ... of
+// split s for four columns; the eight row sums are added in ty order into
+// part2[s][2][C]. ln_param_final_k adds the splits in order.
+constexpr int kLnFoldSplits = 16;
+
+__global__ void ln_param_fold_k(const float* __restrict__ part, int64_t chunks, int64_t C, double* __restrict__ part2) {
+    const int64_t C4 = C >> 2, q = blockIdx.x * 32 + threadIdx.x;
+    const int64_t per = (chunks + kLnFoldSplits - 1) / kLnFoldSplits;
+    const int64_t k0 = blockIdx.y * per, k1 = min(chunks, k0 + per);
+    __shared__ double sh[8][8][33];
+    double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (q < C4) {
+        const float4* p4 = reinterpret_cast<const float4*>(part);
+#pragma unroll 2
+        for (int64_t k = k0 + threadIdx.y; k < k1; k += 8) {
+            const float4 u = __ldcs(p4 + (k * 2 + 0) * C4 + q), w = __ldcs(p4 + (k * 2 + 1) * C4 + q);
+            a[0] += u.x; a[1] += u.y; a[2] += u.z; a[3] += u.w;
+            a[4] += w.x; a[5] += w.y; a[6] += w.z; a[7] += w.w;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) sh[j][threadIdx.y][threadIdx.x] = a[j];
+    __syncthreads();
+    if (threadIdx.y != 0 || q >= C4) return;
+    for (int k = 1; k < 8; ++k)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[j] += sh[j][k][threadIdx.x];
+    double* o = part2 + (int64_t)blockIdx.y * 2 * C;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        o[q * 4 + j] = a[j];
+        o[C + q * 4 + j] = a[4 + j];
+    }
+}
+
+__global__ void ln_param_final_k(const double* __restrict__ part2, int64_t C, float* __restrict__ dgamma,
+                                 float* __restrict__ dbeta) {
+    const int64_t col = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (col >= C) return;
+    double s0 = 0, s1 = 0;
+    for (int k = 0; k < kLnFoldSplits; ++k) {
+        s0 += part2[(int64_t)k * 2 * C + col];
+        s1 += part2[(int64_t)k * 2 * C + C + col];
+    }
+    if (dgamma) dgamma[col] = (float)s0;
+    if (dbeta) dbeta[col] = (float)s1;
 }
 
 __global__ void ln_dgamma_partial_k(const float* __restrict__ x, const float* __restrict__ g,
@@ -1138,6 +1311,66 @@ int nncb_layernorm_bwd(nncb_ctx* ctx, const float* x, const float* gamma, const 
     if (rows == 0) return 0;
     if (!layernorm_reg<1>(ctx, x, gamma, nullptr, g, gx, nullptr, rows, C, eps))
         layernorm_k<1><<<(unsigned)rows, 256, 0, ctx->stream>>>(x, gamma, nullptr, g, gx, nullptr, C, eps);
+    NNCB_LAUNCHED(ctx);
+    return 0;
+}
+
+int nncb_layernorm_bwd_params(nncb_ctx* ctx, const float* x, const float* gamma, const float* g, float* gx,
+                              float* dgamma, float* dbeta, int64_t rows, int64_t C, double eps) {
+    if (!dgamma && !dbeta) return nncb_layernorm_bwd(ctx, x, gamma, g, gx, rows, C, eps);
+    if (rows == 0) {
+        if (dgamma) cudaMemsetAsync(dgamma, 0, sizeof(float) * C, ctx->stream);
+        if (dbeta) cudaMemsetAsync(dbeta, 0, sizeof(float) * C, ctx->stream);
+        return 0;
+    }
+    bool aligned = C % 4 == 0 && C <= 8192;
+    for (const void* p : {(const void*)x, (const void*)gamma, (const void*)g, (const void*)gx})
+        aligned = aligned && (reinterpret_cast<uintptr_t>(p) & 15) == 0;
+    if (!aligned) {   // unfused sequence
+        if (int rc = nncb_layernorm_bwd(ctx, x, gamma, g, gx, rows, C, eps)) return rc;
+        if (dgamma)
+            if (int rc = nncb_layernorm_dgamma(ctx, x, g, dgamma, rows, C, eps)) return rc;
+        if (dbeta)
+            if (int rc = nncb_sum_rows(ctx, g, dbeta, rows, C, 0)) return rc;
+        return 0;
+    }
+    const int vpt = static_cast<int>((C / 4 + 255) / 256);
+    const int Ci = static_cast<int>(C);
+    const size_t smem = sizeof(float) * 2 * C;   // the CTA's dgamma / dbeta accumulators
+    float* part = nullptr;
+    double* part2 = nullptr;
+    auto go = [&](auto kern) {
+        // a full wave of resident CTAs, more when a CTA would own more than
+        // kLnRowsPerCta rows (bounds the float accumulation length)
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
+        int64_t grid = std::max<int64_t>((int64_t)ctx->sm_count * std::max(per_sm, 1),
+                                         (rows + kLnRowsPerCta - 1) / kLnRowsPerCta);
+        if (grid > rows) grid = rows;
+        const size_t p2 = (sizeof(float) * 2 * grid * C + 255) / 256 * 256;
+        char* base = static_cast<char*>(nncb::scratch(ctx, p2 + sizeof(double) * 2 * kLnFoldSplits * C));
+        if (!base) return (int64_t)0;
+        part = reinterpret_cast<float*>(base);
+        part2 = reinterpret_cast<double*>(base + p2);
+        kern<<<static_cast<unsigned>(grid), 256, smem, ctx->stream>>>(x, gamma, g, gx, part, rows, Ci, eps);
+        return grid;
+    };
+    int64_t grid;
+    if (vpt <= 1)
+        grid = go(layernorm_bwd_acc_k<1>);
+    else if (vpt <= 2)
+        grid = go(layernorm_bwd_acc_k<2>);
+    else if (vpt <= 4)
+        grid = go(layernorm_bwd_acc_k<4>);
+    else
+        grid = go(layernorm_bwd_acc_k<8>);
+    if (!grid) return nncb::fail("layernorm_bwd_params: scratch allocation failed");
+    NNCB_LAUNCHED(ctx);
+    ln_param_fold_k<<<dim3((unsigned)((C / 4 + 31) / 32), kLnFoldSplits), dim3(32, 8), 0, ctx->stream>>>(part, grid, C,
+                                                                                                       part2);
+    NNCB_LAUNCHED(ctx);
+    ln_param_final_k<<<(unsigned)((C + 127) / 128), 128, 0, ctx->stream>>>(part2, C, dgamma, dbeta);
     NNCB_LAUNCHED(ctx);
     return 0;
 }

@@ -25,6 +25,8 @@ for name, args in [("nncb_maxpool_fwd", [ctypes.c_void_p, ctypes.POINTER(PoolGeo
                    ("nncb_sgd", [ctypes.c_void_p] * 3 + [ctypes.c_int64, ctypes.c_double, ctypes.c_double]),
                    ("nncb_bn_stats", [ctypes.c_void_p] * 3 + [ctypes.c_int64, ctypes.c_int64, ctypes.c_double]),
                    ("nncb_layernorm_fwd", [ctypes.c_void_p] * 5 + [ctypes.c_int64, ctypes.c_int64, ctypes.c_double]),
+                   ("nncb_layernorm_bwd", [ctypes.c_void_p] * 5 + [ctypes.c_int64, ctypes.c_int64, ctypes.c_double]),
+                   ("nncb_layernorm_bwd_params", [ctypes.c_void_p] * 7 + [ctypes.c_int64, ctypes.c_int64, ctypes.c_double]),
                    ("nncb_avgpool_fwd", [ctypes.c_void_p] + [ctypes.c_int64] * 6 + [ctypes.c_void_p] * 2),
                    ("nncb_avgpool_bwd", [ctypes.c_void_p] + [ctypes.c_int64] * 6 + [ctypes.c_void_p] * 2)]:
     fn = getattr(K, name)
@@ -152,6 +154,32 @@ def test_layernorm_forward_vs_oracle():
     assert np.max(np.abs(y.get(x.shape) - oy)) / np.max(np.abs(oy)) < 1e-6
 
 
+@pytest.mark.parametrize("rows,C", [(8192, 4096), (1000, 1024), (37, 256), (3, 8192), (17, 100)])
+def test_layernorm_backward_with_parameter_gradients(rows, C):
+    """nncb_layernorm_bwd_params: gx bitwise equal to nncb_layernorm_bwd, and
+    dgamma = sum g*xhat, dbeta = sum g against the C oracle / float64 numpy
+    (C=100 takes the unaligned fallback sequence)."""
+    rng = np.random.default_rng(rows + C)
+    x = rng.normal(0.3, 1.2, (rows, C)).astype(np.float32)
+    g = rng.normal(0, 1, (rows, C)).astype(np.float32)
+    ga = rng.uniform(0.5, 1.5, C).astype(np.float32)
+    xd, gd, gad = Dev(x), Dev(g), Dev(ga)
+    gx0, gx1 = Dev(nbytes=x.nbytes), Dev(nbytes=x.nbytes)
+    dg, db = Dev(nbytes=4 * C), Dev(nbytes=4 * C)
+    ok(K.nncb_layernorm_bwd(ctx(), xd.p, gad.p, gd.p, gx0.p, rows, C, 1e-5))
+    ok(K.nncb_layernorm_bwd_params(ctx(), xd.p, gad.p, gd.p, gx1.p, dg.p, db.p, rows, C, 1e-5))
+    assert np.array_equal(gx0.get(x.shape), gx1.get(x.shape))
+    odg = np.zeros(C, np.float32)
+    O.lib().o_layernorm_dgamma(O._f(x), O._f(g), O._f(odg), O.I64(rows), O.I64(C), ctypes.c_double(1e-5))
+    scale = np.sqrt(rows)
+    assert np.max(np.abs(dg.get((C,)) - odg)) / scale < 2e-6
+    assert np.max(np.abs(db.get((C,)) - g.astype(np.float64).sum(0))) / scale < 2e-6
+    # either output alone
+    dg2 = Dev(nbytes=4 * C)
+    ok(K.nncb_layernorm_bwd_params(ctx(), xd.p, gad.p, gd.p, gx1.p, dg2.p, None, rows, C, 1e-5))
+    assert np.array_equal(dg2.get((C,)), dg.get((C,)))
+
+
 @pytest.mark.parametrize("rows,C", [(4096, 64), (1000, 256), (512, 2048), (333, 128), (50, 1024)])
 def test_ew_fused_bn_grad_reduce(rows, C):
     """REDUCE_BN_GRAD fused into an elementwise group: per-channel sum(g) and
@@ -184,6 +212,28 @@ def test_ew_fused_bn_grad_reduce(rows, C):
     ok(K.nncb_bn_grad_reduce(ctx(), xd.p, stats.p, out.p, ref_g.p, ref_gx.p, rows, C))
     np.testing.assert_allclose(got_g, ref_g.get((C,)), rtol=1e-5, atol=1e-5)
     np.testing.assert_allclose(got_gx, ref_gx.get((C,)), rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("rows,C", [(8192, 4096), (999, 8192), (4096, 64), (333, 2048), (7, 4)])
+def test_ew_fused_column_sum(rows, C):
+    """REDUCE_SUM fused into an elementwise group (the Dense bias gradient of
+    the value the group stores): per-column sum in double against float64
+    numpy; the stored value is unchanged."""
+    from tests.nncb_ctypes import ew_run
+    rng = np.random.default_rng(rows + C)
+    a = rng.uniform(-1, 1, (rows, C)).astype(np.float32)
+    b = rng.uniform(-1, 1, (rows, C)).astype(np.float32)
+    ad, bd = Dev(a), Dev(b)
+    out, s = Dev(nbytes=a.nbytes), Dev(nbytes=C * 4)
+    LOAD, STORE, MUL, RSUM = 0, 2, 6, 18
+    prog = [dict(op=LOAD, dst=0, slot=0), dict(op=LOAD, dst=1, slot=1), dict(op=MUL, dst=2, a=0, b=1),
+            dict(op=STORE, a=2, slot=2), dict(op=RSUM, a=2, slot=3)]
+    ew_run(prog, 3, [ad, bd, out, s], rows * C, C)
+    prod = a * b
+    assert np.array_equal(out.get((rows, C)), prod)
+    want = prod.astype(np.float64).sum(0)
+    scale = np.abs(prod).astype(np.float64).sum(0) + 1e-30
+    assert np.max(np.abs(s.get((C,)) - want) / scale) < 1e-6
 
 
 @pytest.mark.parametrize("rows,C", [(4096, 64), (1000, 256)])
