@@ -1,8 +1,10 @@
 // passes.cpp -- shape inference, dead-layer elimination, canonicalization.
 // Shape rules follow reference passes.cpp:209-391 (fixed-extent case); the
 // extension ops keep their input shape (BatchNorm/Gelu/LayerNorm) or reduce to
-// [C] (grad-gamma kernels). DCE follows passes.cpp:574-620, canonicalize
-// passes.cpp:704-781.
+// [C] (grad-gamma kernels). Dead-layer elimination and canonicalization give
+// the results of reference passes.cpp:574-620 / 704-781 (same kept nodes,
+// order and initializers) by their own algorithms (backward liveness sweeps,
+// alias resolution, chain roots with reader counts).
 #include "nnc/passes.hpp"
 
 #include <algorithm>
@@ -211,86 +213,127 @@ ShapeInfo infer_shapes(const Graph& input) {
     return info;
 }
 
+// Liveness by backward sweeps over the node list: a node is live when one of
+// its outputs is needed, and its inputs become needed. A graph whose nodes
+// are topologically ordered settles in one sweep; the sweep repeats until
+// nothing changes, so any order is handled. Initializers survive when a live
+// node reads them (input or weight) or the graph returns them.
 Graph eliminate_dead(const Graph& g) {
-    std::unordered_map<std::string, int> producers;
-    for (size_t i = 0; i < g.nodes.size(); ++i)
-        for (const std::string& o : g.nodes[i].outputs) producers[o] = static_cast<int>(i);
-    std::vector<bool> keep(g.nodes.size(), false);
-    std::vector<std::string> work(g.outputs.begin(), g.outputs.end());
-    while (!work.empty()) {
-        std::string v = work.back();
-        work.pop_back();
-        auto it = producers.find(v);
-        if (it == producers.end() || keep[it->second]) continue;
-        keep[it->second] = true;
-        for (const std::string& in : g.nodes[it->second].inputs) work.push_back(in);
+    std::unordered_set<std::string> needed(g.outputs.begin(), g.outputs.end());
+    std::vector<char> live(g.nodes.size(), 0);
+    for (bool grew = true; grew;) {
+        grew = false;
+        for (size_t i = g.nodes.size(); i-- > 0;) {
+            if (live[i]) continue;
+            const Node& n = g.nodes[i];
+            if (std::none_of(n.outputs.begin(), n.outputs.end(), [&](const std::string& v) { return needed.count(v) > 0; }))
+                continue;
+            live[i] = 1;
+            grew = true;
+            needed.insert(n.inputs.begin(), n.inputs.end());
+        }
     }
     Graph out = g;
     out.nodes.clear();
-    for (size_t i = 0; i < g.nodes.size(); ++i)
-        if (keep[i]) out.nodes.push_back(g.nodes[i]);
-    std::unordered_set<std::string> consumed(g.outputs.begin(), g.outputs.end());
-    for (const Node& n : out.nodes) {
-        for (const std::string& v : n.inputs) consumed.insert(v);
-        for (const std::string& v : n.weights) consumed.insert(v);
+    std::unordered_set<std::string> read(g.outputs.begin(), g.outputs.end());
+    for (size_t i = 0; i < g.nodes.size(); ++i) {
+        if (!live[i]) continue;
+        out.nodes.push_back(g.nodes[i]);
+        read.insert(g.nodes[i].inputs.begin(), g.nodes[i].inputs.end());
+        read.insert(g.nodes[i].weights.begin(), g.nodes[i].weights.end());
     }
-    for (auto it = out.initializers.begin(); it != out.initializers.end();)
-        it = consumed.count(it->first) ? std::next(it) : out.initializers.erase(it);
-    out.value_types.clear();
+    std::erase_if(out.initializers, [&](const auto& kv) { return read.count(kv.first) == 0; });
+    out.value_types.clear();   // re-inferred by the caller
     return out;
 }
 
+namespace {
+
+/// Follows an alias map to the value at the end of the chain (bounded, so a
+/// malformed cyclic graph cannot hang the pass).
+std::string resolve_alias(const std::unordered_map<std::string, std::string>& alias, std::string v) {
+    for (size_t hops = 0; hops <= alias.size(); ++hops) {
+        auto it = alias.find(v);
+        if (it == alias.end()) break;
+        v = it->second;
+    }
+    return v;
+}
+
+}  // namespace
+
+// Canonical form: (1) an Identity whose result is not a graph output is
+// removed and its readers read its source (chains resolve through an alias
+// map); (2) a Flatten fed by a Flatten reads the chain's first input instead,
+// and the bypassed inner Flattens are dropped once nothing reads them.
 Graph canonicalize(const Graph& g) {
+    const std::unordered_set<std::string> returned(g.outputs.begin(), g.outputs.end());
     Graph out = g;
     out.value_types.clear();
-    std::unordered_set<std::string> output_set(out.outputs.begin(), out.outputs.end());
-    bool changed = true;
-    while (changed) {
-        changed = false;
-        for (size_t i = 0; i < out.nodes.size(); ++i) {
-            Node& n = out.nodes[i];
-            if (n.op != OpKind::Identity || output_set.count(n.outputs[0])) continue;
-            const std::string from = n.outputs[0], to = n.inputs[0];
-            for (Node& m : out.nodes)
-                for (std::string& in : m.inputs)
-                    if (in == from) in = to;
-            out.nodes.erase(out.nodes.begin() + static_cast<long>(i));
-            changed = true;
-            break;
-        }
+
+    std::unordered_map<std::string, std::string> alias;   // removed Identity result -> its source
+    for (const Node& n : g.nodes)
+        if (n.op == OpKind::Identity && !returned.count(n.outputs[0])) alias.emplace(n.outputs[0], n.inputs[0]);
+    out.nodes.clear();
+    for (const Node& n : g.nodes) {
+        if (n.op == OpKind::Identity && alias.count(n.outputs[0])) continue;
+        Node m = n;
+        for (std::string& in : m.inputs) in = resolve_alias(alias, in);
+        out.nodes.push_back(std::move(m));
     }
+
+    // Flatten chains, judged on the producers as they stand after (1)
+    std::unordered_map<std::string, size_t> made_by;
+    for (size_t i = 0; i < out.nodes.size(); ++i)
+        for (const std::string& o : out.nodes[i].outputs) made_by[o] = i;
+    auto flatten_source = [&](size_t self, const std::string& v) -> const Node* {
+        auto it = made_by.find(v);
+        if (it == made_by.end() || it->second == self || out.nodes[it->second].op != OpKind::Flatten) return nullptr;
+        return &out.nodes[it->second];
+    };
+    std::vector<std::string> root(out.nodes.size());
     std::unordered_set<std::string> bypassed;
-    changed = true;
-    while (changed) {
-        changed = false;
-        std::unordered_map<std::string, const Node*> producer;
-        for (const Node& n : out.nodes)
-            for (const std::string& o : n.outputs) producer[o] = &n;
-        for (Node& n : out.nodes) {
-            if (n.op != OpKind::Flatten) continue;
-            auto it = producer.find(n.inputs[0]);
-            if (it != producer.end() && it->second->op == OpKind::Flatten && it->second != &n) {
-                bypassed.insert(n.inputs[0]);
-                n.inputs[0] = it->second->inputs[0];
-                changed = true;
-            }
+    for (size_t i = 0; i < out.nodes.size(); ++i) {
+        if (out.nodes[i].op != OpKind::Flatten) continue;
+        std::string v = out.nodes[i].inputs[0];
+        for (size_t hops = 0; hops <= out.nodes.size(); ++hops) {
+            const Node* f = flatten_source(i, v);
+            if (!f) break;
+            bypassed.insert(v);
+            v = f->inputs[0];
+        }
+        root[i] = v;
+    }
+    for (size_t i = 0; i < out.nodes.size(); ++i)
+        if (out.nodes[i].op == OpKind::Flatten) out.nodes[i].inputs[0] = root[i];
+
+    // drop bypassed Flattens nobody reads; a removal can orphan the next one
+    std::unordered_map<std::string, int> readers;
+    for (const std::string& v : g.outputs) ++readers[v];
+    for (const Node& n : out.nodes)
+        for (const std::string& v : n.inputs) ++readers[v];
+    std::vector<char> drop(out.nodes.size(), 0);
+    std::vector<size_t> work;
+    for (size_t i = 0; i < out.nodes.size(); ++i)
+        if (out.nodes[i].op == OpKind::Flatten && bypassed.count(out.nodes[i].outputs[0]) &&
+            readers[out.nodes[i].outputs[0]] == 0)
+            work.push_back(i);
+    while (!work.empty()) {
+        const size_t i = work.back();
+        work.pop_back();
+        if (drop[i]) continue;
+        drop[i] = 1;
+        const std::string& src = out.nodes[i].inputs[0];
+        if (--readers[src] == 0) {
+            auto it = made_by.find(src);
+            if (it != made_by.end() && out.nodes[it->second].op == OpKind::Flatten && bypassed.count(src))
+                work.push_back(it->second);
         }
     }
-    changed = true;
-    while (changed) {
-        changed = false;
-        std::unordered_set<std::string> referenced(out.outputs.begin(), out.outputs.end());
-        for (const Node& n : out.nodes)
-            for (const std::string& v : n.inputs) referenced.insert(v);
-        for (size_t i = 0; i < out.nodes.size(); ++i) {
-            const Node& n = out.nodes[i];
-            if (n.op == OpKind::Flatten && bypassed.count(n.outputs[0]) && !referenced.count(n.outputs[0])) {
-                out.nodes.erase(out.nodes.begin() + static_cast<long>(i));
-                changed = true;
-                break;
-            }
-        }
-    }
+    std::vector<Node> kept;
+    for (size_t i = 0; i < out.nodes.size(); ++i)
+        if (!drop[i]) kept.push_back(std::move(out.nodes[i]));
+    out.nodes = std::move(kept);
     return out;
 }
 

@@ -8,6 +8,8 @@ import os
 import re
 import subprocess
 
+import numpy as np
+
 import pytest
 
 import paper_2205_10357_b200 as P
@@ -202,3 +204,50 @@ def test_partitions_pass_reference_harness_oracles(ref, name, role):
     assert groups or (name == "chain" and role == "train_bwd")
     verdict = ref.check_partition(doc, {"inference": 0, "train_fwd": 1, "train_bwd": 2}[role], groups)
     assert verdict == {"valid": True, "maximal": True}, (role, verdict)
+
+
+def _canon_doc(seed):
+    """A dense net with random Identity chains, Flatten chains and dead
+    branches (reference passes.cpp eliminate_dead / canonicalize inputs)."""
+    rng = np.random.default_rng(seed)
+    nodes, cur, k = [], "x", 0
+
+    def add(op, ins, **attrs):
+        nonlocal k
+        k += 1
+        name = f"n{k}_{op}"
+        d = {"name": name, "op": op, "inputs": ins}
+        if attrs:
+            d["attrs"] = attrs
+        nodes.append(d)
+        return name
+
+    cur = add("conv2d", [cur], filters=4, kernel_size=[3, 3], strides=[1, 1], padding="same")
+    for _ in range(int(rng.integers(1, 4))):
+        cur = add("identity", [cur])
+    dead = add("relu", [cur])                      # dead branch
+    add("identity", [dead])
+    for _ in range(int(rng.integers(1, 4))):
+        cur = add("flatten", [cur])
+    side = add("identity", [cur]) if rng.random() < 0.5 else cur
+    cur = add("dense", [side], units=5)
+    for _ in range(int(rng.integers(0, 3))):
+        cur = add("identity", [cur])
+    out2 = add("identity", [cur])                  # a graph output produced by an Identity
+    return json.dumps({"dialect": "dlb", "name": f"canon{seed}", "inputs": [{"name": "x", "shape": [2, 6, 6, 3]}],
+                       "outputs": [cur, out2], "nodes": nodes})
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_canonicalize_and_dead_layer_elimination_match_reference(ref, seed):
+    """Identity splicing, Flatten-chain collapse and dead-layer elimination
+    (restated, not copied) give the reference's plans: the same values in the
+    same order, and the same weights."""
+    doc = _canon_doc(seed)
+    mine = P.CompiledModel(doc).describe
+    r = ref.RefModel(doc, 1).describe
+    assert sorted(mine["weights"]) == sorted(r["weights"])
+    for role in ("inference", "train_fwd"):
+        a = [(v["name"], v["category"]) for v in mine[role]["values"]]
+        b = [(v["name"], v["category"]) for v in r[role]["values"] if not v["name"].endswith(".im2col")]
+        assert a == b, role
