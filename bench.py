@@ -53,6 +53,19 @@ def ncu_summary():
         return json.load(f)
 
 
+TF32_PEAK_FILE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02", "tf32_peak.json")
+
+
+def tf32_peak():
+    """The tf32 dense peak measured with the driver's bf16 recipe (torch 8192^3,
+    allow_tf32; tools/tf32_peak.py, committed under profiles/r02)."""
+    try:
+        with open(TF32_PEAK_FILE) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(PEAKS_FILE) as f:
@@ -237,7 +250,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-json", default=None)
     ap.add_argument("--no-variants", action="store_true", help="skip the bf16 companion measurement")
-    ap.add_argument("--precision", default="tf32", choices=["tf32", "bf16", "fp32"],
+    ap.add_argument("--precision", default="tf32", choices=["tf32", "bf16", "fp32", "tf32x3"],
                     help="GEMM precision: tf32 (default), bf16 operands for compute-bound contractions, exact fp32")
     args = ap.parse_args()
     world, rank, local = dist_setup()
@@ -276,7 +289,7 @@ def main():
         P.init_comm(world, rank, uid[0])
 
     doc, inputs, target = make_workload(args.config, batch)
-    prec = {"tf32": P.PREC_TF32, "bf16": P.PREC_BF16, "fp32": P.PREC_FP32}[args.precision]
+    prec = {"tf32": P.PREC_TF32, "bf16": P.PREC_BF16, "fp32": P.PREC_FP32, "tf32x3": P.PREC_TF32X3}[args.precision]
     model = P.CompiledModel(doc, precision=prec)
     timer = P.DeviceTimer()
     lr = 1e-4
@@ -401,14 +414,31 @@ def main():
         total = sum(a["ms"] for a in fam.values())
         pk, src = peaks()
 
+        t32 = tf32_peak()
+
         def roofline(k, a):
             if a["flops"] > 0:
                 ach = a["flops"] / (a["ms"] / 1000) / 1e12
                 peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
-                return {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                        "traffic": None, "kernel": k, "launches_per_step": a["n"],
-                        "share_of_step": a["ms"] / total,
-                        "peak_source": f"{src} bf16 dense sustained (tf32 runs at half the bf16 rate)"}
+                r = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                     "traffic": None, "kernel": k, "launches_per_step": a["n"],
+                     "share_of_step": a["ms"] / total,
+                     "peak_source": f"{src} bf16 dense sustained (tf32 runs at half the bf16 rate)"}
+                if t32:
+                    # the family computes in tf32: its own measured ceiling, and the
+                    # per-launch roofline time (each GEMM bounded by max(flops / tf32
+                    # peak, algorithmic bytes / HBM) -- many are 1x1 convs that are
+                    # HBM-bound) over the measured time
+                    tp = t32["tf32_tflops_sustained"]
+                    ideal = sum(max(p["flops"] / (tp * 1e12), p["bytes"] / (pk["hbm_gbs"] * 1e9)) for p in prof
+                                if p["kind"].split(":")[0] == k) * 1e3
+                    r.update({"tf32_peak": tp, "frac_of_tf32_peak": ach / tp,
+                              "tf32_peak_source": "profiles/r02/tf32_peak.json (torch fp32 matmul allow_tf32 8192^3, "
+                                                  "back to back 4 s, the MEASURED_PEAKS recipe)",
+                              "roofline_time_frac": ideal / a["ms"],
+                              "roofline_time_note": "sum over launches of max(flops/tf32 peak, bytes/HBM peak) "
+                                                    "divided by the family's measured time"})
+                return r
             ach = a["bytes"] / (a["ms"] / 1000) / 1e9
             return {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
                     "frac": ach / pk["hbm_gbs"], "traffic": None, "kernel": k, "launches_per_step": a["n"],
@@ -447,34 +477,42 @@ def main():
             cpu = cpu_reference(args.config, args.cpu_seconds, min(os.cpu_count() or 1, 32))
         except Exception as exc:  # noqa: BLE001
             cpu = {"value": None, "error": str(exc)[:200]}
-    # the same workload in the bf16 mode (NNCB_PREC_BF16: compute-bound forward /
-    # input-gradient GEMMs on kind::f16 with bf16 operand copies), same timing
-    # rules, on rank 0 of a single-GPU run: reported beside the headline
+    # the same workload in the other tensor-core modes, same timing rules, on
+    # rank 0 of a single-GPU run, reported beside the headline: bf16 operand
+    # copies for the compute-bound forward / input-gradient GEMMs
+    # (NNCB_PREC_BF16), and the split-operand 3xTF32 route (NNCB_PREC_TF32X3)
     variant = None
     if (rank == 0 and world == 1 and args.precision == "tf32" and cfg["kind"] in ("train", "infer")
             and not args.no_variants):
         del model
-        vm = P.CompiledModel(doc, precision=P.PREC_BF16)
-        if cfg["kind"] == "train":
-            vm.trainer_prepare(inputs, target)
-            vstep = lambda: vm.trainer_step_device(lr)  # noqa: E731
-        else:
-            vm.run(inputs)
-            vstep = lambda: vm.run_device("inference")  # noqa: E731
-        for _ in range(args.warmup):
-            vstep()
-        timer.sync()
-        timer.start()
-        for _ in range(args.steps):
-            vstep()
-        v_ms = timer.stop() / args.steps
-        variant = {"bf16": {"value": units / (v_ms / 1000.0), "unit": unit, "ms_per_step": v_ms,
-                            "dtype": "f32 storage; tcgen05 kind::f16 on bf16 operand copies for the compute-bound "
-                                     "forward / input-gradient GEMMs (arithmetic intensity >= 128), tf32 for the "
-                                     "rest; fp32 accumulate",
-                            "parity": "tests/test_gpu_baseline_parity.py (bf16 rows): launch by launch within 2e-2 "
-                                      "of the float64 truth"}}
-        del vm
+        variant = {}
+        for vname, vprec in (("bf16", P.PREC_BF16), ("tf32x3", P.PREC_TF32X3)):
+            vm = P.CompiledModel(doc, precision=vprec)
+            if cfg["kind"] == "train":
+                vm.trainer_prepare(inputs, target)
+                vstep = lambda: vm.trainer_step_device(lr)  # noqa: E731
+            else:
+                vm.run(inputs)
+                vstep = lambda: vm.run_device("inference")  # noqa: E731
+            for _ in range(args.warmup):
+                vstep()
+            timer.sync()
+            timer.start()
+            for _ in range(args.steps):
+                vstep()
+            v_ms = timer.stop() / args.steps
+            variant[vname] = {"value": units / (v_ms / 1000.0), "unit": unit, "ms_per_step": v_ms}
+            del vm
+        variant["bf16"].update({
+            "dtype": "f32 storage; tcgen05 kind::f16 on bf16 operand copies for the compute-bound forward / "
+                     "input-gradient GEMMs (arithmetic intensity >= 128), tf32 for the rest; fp32 accumulate",
+            "parity": "tests/test_gpu_baseline_parity.py (bf16 rows): launch by launch within 2e-2 of the float64 "
+                      "truth"})
+        variant["tf32x3"].update({
+            "dtype": "f32; every GEMM on tcgen05 kind::tf32 over split operands (hi + lo, K concatenated 3x): "
+                     "1e-5-class GEMM error; exact elementwise ops",
+            "parity": "tests/test_gpu_tf32x3.py (kernels vs float64) and tests/test_gpu_baseline_parity.py "
+                      "(tf32x3 row: the C4 step launch by launch against the float64 truth)"})
     mode_a = None
     if cfg["kind"] == "chain" and rank == 0:
         # SURVEY.md §8(d) C2 mode A: inference BatchNorm (per-channel affine),
@@ -501,7 +539,9 @@ def main():
                                        "bf16": "f32 storage; tcgen05 kind::f16 on bf16 operand copies for the "
                                                "compute-bound forward / input-gradient GEMMs, tf32 for the rest; "
                                                "fp32 accumulate",
-                                       "fp32": "f32 (exact-order fp32 GEMMs)"}[args.precision],
+                                       "fp32": "f32 (exact-order fp32 GEMMs)",
+                                       "tf32x3": "f32 (split-operand 3xTF32 tcgen05 GEMMs, fp32 accumulate)"}[
+                                           args.precision],
         "data": "synthetic",
         "config": {"workload": cfg["workload"], "global_batch": batch * world, "batch_per_gpu": batch,
                    "parallelism": f"dp{world}", "l2": "activations >> 126 MB L2; no flush needed"},

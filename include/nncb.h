@@ -180,6 +180,13 @@ enum nncb_precision {
                               single tap with K % 8 == 0) convert A and B to bf16 copies
                               (round to nearest) and multiply those; outputs stay fp32.
                               Weight gradients and other shapes run the tf32 path.          */
+    NNCB_PREC_TF32X3 = 3,  /* fp32-grade tensor-core path ("3xTF32"): every operand v is split
+                              into hi = tf32(v) (low 13 mantissa bits cleared) and lo = v - hi,
+                              and the contraction runs kind::tf32 over K' = 3K with
+                              A' = [A_hi | A_hi | A_lo], B' = [B_hi ; B_lo ; B_hi]
+                              (= A_hi B_hi + A_hi B_lo + A_lo B_hi; dropped terms ~2^-21
+                              relative). K is concatenated along channels (conv fwd /
+                              dgrad, dense) or along the batch (weight gradients).        */
 };
 enum nncb_epilogue {
     NNCB_EPI_BIAS = 1,

@@ -34,6 +34,8 @@ PREC_TF32 = 0   # tcgen05.mma kind::tf32, fp32 accumulation in TMEM
 PREC_FP32 = 1   # exact-order fp32 (bit-identical to the reference CPU kernels)
 PREC_BF16 = 2   # tcgen05.mma kind::f16 on bf16 operand copies for the forward / input-gradient
                 # contractions (K-major operands), fp32 accumulate; weight gradients tf32
+PREC_TF32X3 = 3  # fp32-grade tensor-core path: operands split into tf32 hi + lo parts,
+                 # kind::tf32 over the K-concatenated problem (A_hi B_hi + A_hi B_lo + A_lo B_hi)
 
 
 class NNCError(RuntimeError):
@@ -507,4 +509,4 @@ def init_comm(nranks: int, rank: int, uid: bytes):
 
 
 __all__ = ["load_native", "CompiledModel", "DeviceTimer", "NNCError", "group_document", "comm_unique_id",
-           "init_comm", "PREC_TF32", "PREC_FP32", "PREC_BF16", "HOST_LIB", "KERNEL_LIB"]
+           "init_comm", "PREC_TF32", "PREC_FP32", "PREC_BF16", "PREC_TF32X3", "HOST_LIB", "KERNEL_LIB"]

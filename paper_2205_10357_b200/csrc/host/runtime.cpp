@@ -414,7 +414,8 @@ struct Program {
             fuse_bn_infer_epilogue();
             fuse_ln_param_grads();
             fuse_bias_grad_reduce();
-            if (!std::getenv("NNC_NO_KMAJOR_BATCH")) prepare_kmajor_weights();
+            // (the 3xTF32 route builds its own split weight copies)
+            if (!std::getenv("NNC_NO_KMAJOR_BATCH") && precision != NNCB_PREC_TF32X3) prepare_kmajor_weights();
         }
         hint_unchanged_activations();
     }
@@ -1059,7 +1060,8 @@ struct Program {
                 bool fast = false;
                 for (const auto& in : L.ew)
                     fast = fast || in.op == NNCB_EW_BN_GRAD || in.op == NNCB_EW_GELU || in.op == NNCB_EW_GELU_GRAD;
-                if (fast && precision != NNCB_PREC_FP32 && !std::getenv("NNC_EXACT_BN_GRAD")) {
+                if (fast && (precision == NNCB_PREC_TF32 || precision == NNCB_PREC_BF16) &&
+                    !std::getenv("NNC_EXACT_BN_GRAD")) {
                     b.ew_prog = L.ew;
                     for (auto& in : b.ew_prog) {
                         if (in.op == NNCB_EW_BN_GRAD) in.op = NNCB_EW_BN_GRAD_FAST;

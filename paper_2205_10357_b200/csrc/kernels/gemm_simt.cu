@@ -274,6 +274,11 @@ extern "C" int nncb_gemm(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a,
         int rc = nncb::gemm_tc(ctx, d, a, b, bias, out, &handled);
         g_last_path = 1;
         if (rc || handled) return rc;
+    } else if (d->precision == NNCB_PREC_TF32X3) {
+        bool handled = false;
+        int rc = nncb::gemm_tc_x3(ctx, d, a, b, bias, out, &handled);
+        g_last_path = 1;
+        if (rc || handled) return rc;
     }
     if (d->epilogue & NNCB_EPI_RELU_GRAD)
         return nncb::fail("nncb_gemm: NNCB_EPI_RELU_GRAD is a tensor-core epilogue (tf32 precision, TMA-eligible shape)");

@@ -43,6 +43,7 @@ from paper_2205_10357_b200 import workloads as W
 
 pytestmark = pytest.mark.gpu
 TF32_TOL = 2e-2   # north star: "2e-2 for bf16 GEMM paths" (tf32 is wider than bf16)
+X3_TOL = 1e-4     # 3xTF32: the tensor core's fp32 accumulation (linear in K) bounds it
 
 
 def rel_norm(got, want):
@@ -198,6 +199,20 @@ def test_c4_resnet50_bn_bf16_training_step_at_224_launch_by_launch():
     m = P.CompiledModel(doc, precision=P.PREC_BF16)
     randomize_norms(m, np.random.default_rng(4))
     local_step_parity(m, doc, {"x": x}, t, emu_tol=2e-3, truth_tol=TF32_TOL, min_values=100, emulate="bf16")
+
+
+def test_c4_resnet50_bn_tf32x3_training_step_at_224_launch_by_launch():
+    """The split-operand 3xTF32 mode (NNCB_PREC_TF32X3: every GEMM on
+    kind::tf32 over hi/lo operand parts, exact elementwise ops): every launch
+    of the C4 step against the float64 truth directly, at a 1e-5-class bound
+    (X3_TOL) -- two orders below the tf32 mode's truncation error."""
+    batch = 2
+    doc = W.resnet50(batch, bn=True)
+    x = W.uniform((batch, 224, 224, 3), 1, "x")
+    t = W.uniform((batch, 1000), 2, "t", 4.0, 6.0)
+    m = P.CompiledModel(doc, precision=P.PREC_TF32X3)
+    randomize_norms(m, np.random.default_rng(4))
+    local_step_parity(m, doc, {"x": x}, t, emu_tol=X3_TOL, truth_tol=X3_TOL, min_values=100, emulate=None)
 
 
 def test_c5_layer_8192x4096_bf16():
