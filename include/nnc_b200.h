@@ -11,6 +11,7 @@
  *   nnc_model_run         runtime::execute (ref runtime.cpp:314-462)
  *   nnc_model_train_step  runtime::train_step (ref runtime.cpp:498-537)
  *   nnc_group_document    backends::group_layers (ref backends.cpp:321-400)
+ *   nnc_model_tune        backends::tune_with_report (ref backends.cpp:73-176)
  *
  * Conventions: int status (0 = OK; otherwise 1 + nnc::Error::Code, or 100 for
  * other failures) with nnc_last_error(); tensors are float32, row-major NHWC;
@@ -115,6 +116,15 @@ uint64_t nnc_model_launches_per_step(nnc_model* m);
  * [{label, kind, ms, bytes, flops}] (algorithmic bytes/flops). NULL on error. */
 const char* nnc_model_profile_run(nnc_model* m, int role);
 const char* nnc_model_profile_step(nnc_model* m, double lr);
+/* Measured layer-wise tuning (backends::tune_with_report, ref backends.cpp:
+ * 73-176) of the model's three role graphs before first execution: every
+ * compute node timed in isolation on seed-shaped random inputs (median of
+ * `trials` after `warmup`; GEMM nodes once per tensor-core tile candidate),
+ * the chosen tiles attached to the plans (plan::attach_tuning, saved with
+ * them in SOLP). injected_json (optional) {"node": {"b200_gemm"|"b200_fused":
+ * cost}} skips the device (CostModel::injected_from). Returns the report as
+ * JSON {role: {records, tiles, text}, attached_launches}; NULL on error.   */
+const char* nnc_model_tune(nnc_model* m, int warmup, int trials, const char* injected_json);
 uint64_t nnc_model_arena_bytes(nnc_model* m);
 /* Device memory of a bound program (role 0 inference / 1 train_fwd after a run, 2 the trainer):
    arena address span, live-bytes high water and plan::estimate_peak at the same 256-byte alignment. */

@@ -224,7 +224,11 @@ enum nncb_epilogue {
 };
 
 typedef struct {
-    int32_t kind, precision, epilogue, _pad;
+    int32_t kind, precision, epilogue;
+    /* tensor-core tile choice for this call (a code from nncb_gemm_candidates,
+     * e.g. persisted by the layer-wise tuner in the plan); 0 = the table /
+     * static rule. A code the shape's route rejects falls back to 0.        */
+    int32_t tile;
     /* conv geometry, as kernels::ConvGeom (kernels.hpp:20-25) */
     int64_t n, ih, iw, ci, co, kh, kw, sh, sw, oh, ow, pad_top, pad_left;
     /* dense geometry */
@@ -286,6 +290,15 @@ int nncb_gemm_force_tile(int code);
 int nncb_gemm_tuning_export(char* buf, size_t cap, size_t* needed);
 int nncb_gemm_tuning_import(const char* text);
 int nncb_gemm_tuning_mode(void);
+/* Layer-wise tuning support (backends::tune_with_report): the tensor-core tile
+ * codes worth timing for this contraction (*n set; codes written up to cap;
+ * 0 candidates when the shape has no tensor-core route), and the median
+ * device time of `trials` calls with tile `code` after `warmup` calls (CUDA
+ * events on the compute stream; `out` is overwritten).                    */
+int nncb_gemm_candidates(const nncb_gemm_desc* d, int32_t* codes, int cap, int* n);
+int nncb_gemm_time_tile(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b,
+                        const float* bias, float* out, int32_t code, int warmup, int trials,
+                        float* median_ms);
 int nncb_gemm(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b,
               const float* bias, float* out);
 

@@ -91,6 +91,7 @@ def _load():
         "nnc_model_launches_per_step": (U64, [P]),
         "nnc_model_profile_step": (S, [P, D]),
         "nnc_model_profile_run": (S, [P, I]),
+        "nnc_model_tune": (S, [P, I, I, S]),
         "nnc_model_dp_schedule": (S, [P, I64]),
         "nnc_model_step_schedule": (S, [P, I64, I, I]),
         "nnc_model_arena_bytes": (U64, [P]),
@@ -408,6 +409,19 @@ class CompiledModel:
         if res is None:
             raise NNCError(100, _host.nnc_last_error().decode())
         return json.loads(res.decode())
+
+    def tune(self, warmup: int = 1, trials: int = 5, injected: Optional[dict] = None) -> dict:
+        """Measured layer-wise tuning (backends::tune_with_report) of the three
+        role graphs before first execution; the chosen GEMM tiles are attached
+        to the plans (and saved with them). `injected` = {node: {"b200_gemm" |
+        "b200_fused": cost}} skips the device. Returns the report."""
+        inj = json.dumps(injected).encode() if injected is not None else None
+        res = _host.nnc_model_tune(self._h, warmup, trials, inj)
+        if res is None:
+            raise NNCError(_host.nnc_last_status(), _host.nnc_last_error().decode())
+        report = json.loads(res.decode())
+        self.describe = json.loads(_host.nnc_model_describe(self._h).decode())   # plans now carry tiles
+        return report
 
     def dp_schedule(self, bucket_bytes: int = 32 << 20) -> dict:
         """Data-parallel region layout and all-reduce bucket schedule (host-only)."""

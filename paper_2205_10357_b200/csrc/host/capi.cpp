@@ -64,7 +64,7 @@ void describe_plan(std::ostringstream& os, const plan::ExecutionPlan& p) {
         for (size_t k = 0; k < g.launches.size(); ++k) {
             const auto& L = g.launches[k];
             os << (k ? "," : "") << "{\"kind\":" << jstr(plan::launch_kind_name(L.kind)) << ",\"label\":" << jstr(L.label)
-               << ",\"instrs\":" << L.ew.size() << ",\"args\":[";
+               << ",\"instrs\":" << L.ew.size() << ",\"tile\":" << L.tile << ",\"args\":[";
             for (size_t a = 0; a < L.args.size(); ++a)
                 os << (a ? "," : "") << "[" << jstr(p.values[L.args[a].slot].name) << "," << L.args[a].offset << ","
                    << (L.is_out[a] ? 1 : 0) << "]";
@@ -565,6 +565,46 @@ int nnc_comm_unique_id(uint8_t id[128]) {
 
 int nnc_init_comm(int nranks, int rank, const uint8_t id[128]) {
     return guarded([&] { runtime::default_device().init_comm(nranks, rank, id); });
+}
+
+const char* nnc_model_tune(nnc_model* m, int warmup, int trials, const char* injected_json) {
+    const char* out = nullptr;
+    int rc = guarded([&] {
+        backends::CostModel cm;
+        cm.warmup = warmup;
+        cm.trials = trials;
+        cm.gemm_precision = m->opts.gemm_precision;
+        if (injected_json && *injected_json) {   // {"node": {"b200_gemm": us, "b200_fused": us}, ...}
+            std::map<std::pair<std::string, backends::BackendId>, double> costs;
+            const nlohmann::json spec = nlohmann::json::parse(injected_json);
+            for (const auto& [node, per] : spec.items())
+                for (const auto& [bk, c] : per.items())
+                    costs[{node, bk == "b200_gemm" ? backends::BackendId::B200_GEMM : backends::BackendId::B200_FUSED}] =
+                        c.get<double>();
+            cm = backends::CostModel::injected_from(std::move(costs));
+        }
+        nlohmann::json j;
+        size_t attached = 0;
+        for (const auto& [role, g] : {std::pair<const char*, const hlir::Graph*>{"inference", &m->versions.inference},
+                                      {"train_fwd", &m->versions.train_fwd},
+                                      {"train_bwd", &m->versions.train_bwd}}) {
+            backends::TuningReport r = backends::tune_with_report(*g, cm);
+            nlohmann::json recs = nlohmann::json::array();
+            for (const auto& x : r.records)
+                recs.push_back({{"node", x.node}, {"backend", backends::backend_name(x.backend)}, {"tile", x.tile},
+                                {"cost_us", x.cost}, {"chosen", x.chosen}});
+            j[role] = {{"records", recs}, {"tiles", r.tiles}, {"text", r.render_text()}};
+            plan::ExecutionPlan& p = std::string(role) == "inference" ? m->plans.inference
+                                     : std::string(role) == "train_fwd" ? m->plans.train_fwd
+                                                                        : m->plans.train_bwd;
+            attached += plan::attach_tuning(p, r);
+        }
+        j["attached_launches"] = attached;
+        m->trainer = nullptr;   // rebinds with the tuned plans
+        m->desc = j.dump();
+        out = m->desc.c_str();
+    });
+    return rc ? nullptr : out;
 }
 
 const char* nnc_group_document(const char* doc, const char* assignment_json) {

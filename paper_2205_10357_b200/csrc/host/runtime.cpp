@@ -1079,6 +1079,7 @@ struct Program {
             case LaunchKind::Gemm: {
                 nncb_gemm_desc& d = b.gemm;
                 d.precision = precision;
+                d.tile = L.tile;
                 switch (L.op) {
                     case hlir::OpKind::Conv2D:
                         d.kind = NNCB_CONV_FWD;

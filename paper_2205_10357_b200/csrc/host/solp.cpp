@@ -23,7 +23,7 @@ namespace {
 
 constexpr char kMagic[4] = {'S', 'O', 'L', 'P'};
 constexpr char kSetMagic[4] = {'S', 'O', 'L', 'V'};
-constexpr uint32_t kVersion = 0xB2000001u;   // B200 descriptor layout, revision 1
+constexpr uint32_t kVersion = 0xB2000002u;   // B200 descriptor layout, revision 2 (per-launch GEMM tile)
 
 struct Writer {
     std::vector<uint8_t> out;
@@ -175,6 +175,7 @@ void write_plan(Writer& w, const ExecutionPlan& p) {
             w.u32(static_cast<uint32_t>(L.op));
             write_attrs(w, L.attrs);
             w.u8(L.relu_epilogue ? 1 : 0);
+            w.i32(L.tile);
         }
     }
     w.u32(static_cast<uint32_t>(p.exec_steps.size()));
@@ -358,6 +359,7 @@ ExecutionPlan read_plan(Reader& r) {
             L.op = static_cast<hlir::OpKind>(r.u32());
             L.attrs = read_attrs(r);
             L.relu_epilogue = r.u8() != 0;
+            L.tile = r.i32();
             gk.launches.push_back(std::move(L));
         }
         p.groups.push_back(std::move(gk));

@@ -66,6 +66,10 @@ struct Launch {
     hlir::OpKind op = hlir::OpKind::Identity;
     hlir::Attrs attrs;
     bool relu_epilogue = false;
+    // Gemm: the tensor-core tile chosen by measured layer-wise tuning
+    // (backends::tune_with_report, attached with attach_tuning); 0 = the
+    // kernel library's deterministic table / static rule
+    int32_t tile = 0;
 };
 
 struct GroupKernel {
@@ -140,6 +144,12 @@ struct VersionPlans {
 VersionPlans compile_version_set(
     const autodiff::VersionSet& versions,
     const std::function<backends::BackendAssignment(const hlir::Graph&)>& assign);
+
+/// Persists measured tile choices into a plan: every GEMM launch whose node
+/// the report tuned carries the chosen tile code (Launch::tile, saved in SOLP).
+/// Returns the number of launches updated.
+size_t attach_tuning(ExecutionPlan& p, const backends::TuningReport& report);
+size_t attach_tuning(VersionPlans& v, const backends::TuningReport& report);
 
 /// Per-binding re-specialisation of plans compiled with enabled vdims: the
 /// source graph with the bound extents substituted runs through the same

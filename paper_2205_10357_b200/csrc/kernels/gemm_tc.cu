@@ -23,6 +23,7 @@
 // -> registers -> bias -> 128-bit global stores). A 4-stage smem ring with
 // full/empty mbarriers couples TMA and MMA; tcgen05.commit releases stages.
 // Operand tiles use the 128-byte swizzle (TMA and UMMA descriptors agree).
+#include <algorithm>
 #include <atomic>
 #include <vector>
 #include <string>
@@ -2171,6 +2172,43 @@ __global__ void bn_invstd_k(const float* __restrict__ var, float* __restrict__ i
         inv[c] = static_cast<float>(1.0 / sqrt(static_cast<double>(var[c]) + eps));
 }
 
+// The tile codes the live tuner (and backends::tune_with_report) times for a
+// contraction with N output columns.
+std::vector<int> tile_candidates(const nncb_gemm_desc* d, int64_t N) {
+    // bit 16: CTA pair (cta_group::2, 256-row tiles over two SMs)
+    static const bool pairs = !(getenv("NNCB_TC_PAIR") && atoi(getenv("NNCB_TC_PAIR")) == 0);
+    std::vector<int> cands = N <= 64 ? std::vector<int>{64} : N <= 128 ? std::vector<int>{64, 128}
+                                                                        : std::vector<int>{128, 256};
+    if (pairs) {
+        cands.push_back(0x10000 | (N <= 64 ? 64 : 128));
+        if (N > 128) cands.push_back(0x10000 | 256);
+    }
+    cands.push_back(0x20000 | (N <= 64 ? 64 : 128));   // bit 17: full-width staging at 2 CTAs/SM
+    if (d->kind == NNCB_CONV_FWD || d->kind == NNCB_DENSE_FWD) {   // bit 18: K-major (transposed) weights
+        const size_t nb = cands.size();
+        for (size_t ci_ = 0; ci_ < nb; ++ci_) cands.push_back(cands[ci_] | 0x40000);
+    }
+    static const bool halo_on = !(getenv("NNCB_TC_HALO") && atoi(getenv("NNCB_TC_HALO")) == 0);
+    const bool halo_fwd = d->kind == NNCB_CONV_FWD && d->ci % 32 == 0 && d->ow >= HALO_TW;
+    // the space-to-depth stem (packed: its lowered conv has 2 taps per row spaced 2)
+    const bool halo_stem = d->kind == NNCB_CONV_FWD && d->ci % 32 != 0 && d->sh == 2 && d->sw == 2 &&
+                           4 * d->ci <= 16 && d->kw == 7 && d->kh == 7 && d->ow >= HALO_TW;
+    const bool halo_dgrad = d->kind == NNCB_CONV_DGRAD && d->co % 32 == 0 && d->iw >= HALO_TW;
+    if (halo_on && !(d->epilogue & NNCB_EPI_RELU_GRAD) &&
+        (halo_stem || ((halo_fwd || halo_dgrad) && d->kh == 3 && d->kw == 3 && d->sh == 1 && d->sw == 1 &&
+                       d->pad_top == 1 && d->pad_left == 1))) {   // bit 19: halo patches
+        const size_t nb = cands.size();
+        for (size_t ci_ = 0; ci_ < nb; ++ci_)
+            if (!(cands[ci_] & 0x30000)) cands.push_back(cands[ci_] | 0x80000);   // 1-CTA tiles, default staging
+        // (bit 20, full 3x3 patches: correct but measured no faster than
+        // kernel-row patches at one CTA per SM; force_tile only)
+        // (bit 21, resident B for 64-wide single-N-tile halo convs: correct,
+        // but 15-20% slower at one CTA per SM -- the kernel-row halo tile is
+        // no longer L2-bound at ~79% of the N = 64 MMA ceiling; force_tile only)
+    }
+    return cands;
+}
+
 int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const float* bias, float* out,
             bool* handled) {
     // inference BatchNorm epilogue: its per-column invstd, once per call
@@ -2227,6 +2265,8 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
              (long long)(d->in_f * 1000003 + d->out_f), d->epilogue & ~NNCB_EPI_A_UNCHANGED, g_manual_a.load() ? 1 : 0);
     if (bf16) strncat(key, "|bf16", sizeof(key) - strlen(key) - 1);
     int choice = g_forced_tile.load(std::memory_order_relaxed);
+    const bool per_call = !choice && d->tile != 0;   // the plan's persisted choice
+    if (per_call) choice = d->tile;
     if (!choice && mode != 0) {
         std::lock_guard<std::mutex> lk(mu);
         auto it = tuned.find(key);
@@ -2235,37 +2275,7 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(ctx->stream, &cap);
     if (!choice && enabled && cap == cudaStreamCaptureStatusNone) {
-        // bit 16: CTA pair (cta_group::2, 256-row tiles over two SMs)
-        static const bool pairs = !(getenv("NNCB_TC_PAIR") && atoi(getenv("NNCB_TC_PAIR")) == 0);
-        std::vector<int> cands = N <= 64 ? std::vector<int>{64} : N <= 128 ? std::vector<int>{64, 128}
-                                                                            : std::vector<int>{128, 256};
-        if (pairs) {
-            cands.push_back(0x10000 | (N <= 64 ? 64 : 128));
-            if (N > 128) cands.push_back(0x10000 | 256);
-        }
-        cands.push_back(0x20000 | (N <= 64 ? 64 : 128));   // bit 17: full-width staging at 2 CTAs/SM
-        if (d->kind == NNCB_CONV_FWD || d->kind == NNCB_DENSE_FWD) {   // bit 18: K-major (transposed) weights
-            const size_t nb = cands.size();
-            for (size_t ci_ = 0; ci_ < nb; ++ci_) cands.push_back(cands[ci_] | 0x40000);
-        }
-        static const bool halo_on = !(getenv("NNCB_TC_HALO") && atoi(getenv("NNCB_TC_HALO")) == 0);
-        const bool halo_fwd = d->kind == NNCB_CONV_FWD && d->ci % 32 == 0 && d->ow >= HALO_TW;
-        // the space-to-depth stem (packed: its lowered conv has 2 taps per row spaced 2)
-        const bool halo_stem = d->kind == NNCB_CONV_FWD && d->ci % 32 != 0 && d->sh == 2 && d->sw == 2 &&
-                               4 * d->ci <= 16 && d->kw == 7 && d->kh == 7 && d->ow >= HALO_TW;
-        const bool halo_dgrad = d->kind == NNCB_CONV_DGRAD && d->co % 32 == 0 && d->iw >= HALO_TW;
-        if (halo_on && !(d->epilogue & NNCB_EPI_RELU_GRAD) &&
-            (halo_stem || ((halo_fwd || halo_dgrad) && d->kh == 3 && d->kw == 3 && d->sh == 1 && d->sw == 1 &&
-                           d->pad_top == 1 && d->pad_left == 1))) {   // bit 19: halo patches
-            const size_t nb = cands.size();
-            for (size_t ci_ = 0; ci_ < nb; ++ci_)
-                if (!(cands[ci_] & 0x30000)) cands.push_back(cands[ci_] | 0x80000);   // 1-CTA tiles, default staging
-            // (bit 20, full 3x3 patches: correct but measured no faster than
-            // kernel-row patches at one CTA per SM; force_tile only)
-            // (bit 21, resident B for 64-wide single-N-tile halo convs: correct,
-            // but 15-20% slower at one CTA per SM -- the kernel-row halo tile is
-            // no longer L2-bound at ~79% of the N = 64 MMA ceiling; force_tile only)
-        }
+        const std::vector<int> cands = tile_candidates(d, N);
         // candidates write a scratch output: the caller's output (which an
         // epilogue side input may alias) is only written by the final call
         float* tmp_out = nullptr;
@@ -2331,13 +2341,18 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
     g_force_tb = (choice >> 18) & 1;
     g_force_halo = (choice >> 20) & 1 ? 2 : (choice >> 19) & 1;
     g_force_bres = (choice >> 21) & 1;
-    const int rc = gemm_tc_route(ctx, d, a, b, bias, out, handled);
+    int rc = gemm_tc_route(ctx, d, a, b, bias, out, handled);
     g_force_bn = 0;
     g_force_pair = 0;
     g_force_wide = 0;
     g_force_tb = 0;
     g_force_halo = 0;
     g_force_bres = 0;
+    if (!rc && !*handled && per_call) {   // a persisted code this route rejects: the default choice
+        nncb_gemm_desc d0 = *d;
+        d0.tile = 0;
+        return gemm_tc(ctx, &d0, a, b, bias, out, handled);
+    }
     return rc;
 }
 
@@ -2755,3 +2770,44 @@ extern "C" int nncb_gemm_tuning_import(const char* text) {
 }
 
 extern "C" int nncb_gemm_tuning_mode(void) { return nncb::tune_mode(); }
+
+extern "C" int nncb_gemm_candidates(const nncb_gemm_desc* d, int32_t* codes, int cap, int* n) {
+    if (!d || !n) return nncb::fail("nncb_gemm_candidates: null argument");
+    std::vector<int> c;
+    if (d->precision != NNCB_PREC_FP32 && !(d->kind == NNCB_CONV_DGRAD && d->kh * d->kw > 1 && d->ci % 32)) {
+        const bool dense = d->kind <= NNCB_DENSE_WGRAD;
+        const int64_t N = d->kind == NNCB_DENSE_DGRAD ? d->in_f : d->kind == NNCB_CONV_DGRAD ? d->ci
+                          : dense ? d->out_f : d->co;
+        c = nncb::tile_candidates(d, N);
+    }
+    *n = static_cast<int>(c.size());
+    for (int i = 0; i < *n && i < cap && codes; ++i) codes[i] = c[i];
+    return 0;
+}
+
+extern "C" int nncb_gemm_time_tile(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b,
+                                   const float* bias, float* out, int32_t code, int warmup, int trials,
+                                   float* median_ms) {
+    if (!d || !median_ms || trials < 1) return nncb::fail("nncb_gemm_time_tile: bad argument");
+    nncb_gemm_desc x = *d;
+    x.tile = code;
+    for (int i = 0; i < warmup; ++i)
+        if (int rc = nncb_gemm(ctx, &x, a, b, bias, out)) return rc;
+    std::vector<float> ms(static_cast<size_t>(trials));
+    cudaEvent_t e0, e1;
+    NNCB_CUDA(cudaEventCreate(&e0));
+    NNCB_CUDA(cudaEventCreate(&e1));
+    int rc = 0;
+    for (int t = 0; t < trials && !rc; ++t) {
+        cudaEventRecord(e0, ctx->stream);
+        rc = nncb_gemm(ctx, &x, a, b, bias, out);
+        cudaEventRecord(e1, ctx->stream);
+        if (!rc && cudaEventSynchronize(e1) == cudaSuccess) cudaEventElapsedTime(&ms[static_cast<size_t>(t)], e0, e1);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (rc) return rc;
+    std::sort(ms.begin(), ms.end());
+    *median_ms = ms[ms.size() / 2];
+    return 0;
+}

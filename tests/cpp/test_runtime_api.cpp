@@ -9,6 +9,7 @@
 //   ExecutionContext high water == estimate    test_runtime.cpp:195-240
 //   training loop: converge, trace, lr = 0     test_runtime.cpp:242-287
 //   enabled batch dim (VdimBinding::enable)    test_runtime.cpp:289-303
+//   tune_with_report / CostModel / attach      backends.hpp:35-73, backends.cpp:73-176
 #include <execinfo.h>
 #include <signal.h>
 #include <unistd.h>
@@ -280,6 +281,52 @@ void on_fatal(int sig) {
     _exit(128 + sig);
 }
 
+// measured layer-wise tuning as a reference caller uses it (backends.hpp:35-73):
+// injected costs are total and deterministic; measured tuning times every GEMM
+// tile, and the tuned plans (tiles attached) compute what the untuned ones do
+void tuning_report_and_tuned_plans() {
+    auto model = ingest::parse_model(c1_doc(R"("shape":[8,16,16,3])"));
+    Graph g = passes::optimize(model.graph).graph;
+    std::map<std::pair<std::string, backends::BackendId>, double> costs;
+    for (const Node& n : g.nodes)
+        for (backends::BackendId b : {backends::BackendId::B200_FUSED, backends::BackendId::B200_GEMM})
+            if (backends::supports(b, n.op)) costs[{n.name, b}] = 1.0;
+    backends::TuningReport inj = backends::tune_with_report(g, backends::CostModel::injected_from(costs));
+    CHECK(inj.assignment == backends::default_assignment(g));
+    CHECK(inj.render_csv().rfind("node,backend,tile,cost_us,chosen\n", 0) == 0);
+    costs.erase(costs.begin());
+    {
+        bool bad_document = false;
+        try {
+            backends::tune_with_report(g, backends::CostModel::injected_from(costs));
+        } catch (const Error& e) {
+            bad_document = e.code() == Error::Code::BadDocument;
+        }
+        CHECK(bad_document);
+    }
+
+    backends::TuningReport rep = backends::tune_with_report(g, backends::CostModel::measured());
+    size_t gemm_records = 0;
+    for (const auto& r : rep.records) gemm_records += r.backend == backends::BackendId::B200_GEMM;
+    CHECK(gemm_records > 2);   // c1, c2, fc: several tile candidates each
+    auto versions = autodiff::derive_versions(g);
+    auto plans = plan::compile_version_set(versions, [](const Graph& gg) { return backends::default_assignment(gg); });
+    auto tuned = plans;
+    CHECK(plan::attach_tuning(tuned.inference, rep) > 0);
+    HostModel host = HostModel::from_graph(g);
+    std::map<std::string, Tensor> in{{"x", uniform({8, 16, 16, 3}, 3)}};
+    auto a = execute(plans.inference, in, host);
+    auto b = execute(tuned.inference, in, host);
+    const Tensor& ya = a.at("fc");
+    const Tensor& yb = b.at("fc");
+    double num = 0, den = 0;
+    for (int64_t i = 0; i < ya.elements(); ++i) {
+        num += (ya.get(i) - yb.get(i)) * (ya.get(i) - yb.get(i));
+        den += ya.get(i) * ya.get(i);
+    }
+    CHECK(std::sqrt(num / den) < 1e-2);
+}
+
 int main() {
     setvbuf(stdout, nullptr, _IONBF, 0);
     signal(SIGSEGV, on_fatal);
@@ -294,6 +341,7 @@ int main() {
         {"arena instrumentation equals the schedule estimate", arena_instrumentation_equals_estimate},
         {"training loop: dense(1->1) converges and traces the four steps", training_loop_converges_and_traces},
         {"enabled batch dim: any batch accepted, fixed axes enforced", enabled_batch_dim},
+        {"layer-wise tuning: injected report, measured tiles, tuned plans", tuning_report_and_tuned_plans},
     };
     for (const Case& c : cases) {
         std::printf("[ RUN ] %s\n", c.name);

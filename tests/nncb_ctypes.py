@@ -11,7 +11,7 @@ _P, _I, _I64, _D, _S = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_d
 
 
 class GemmDesc(ctypes.Structure):
-    _fields_ = [(n, ctypes.c_int32) for n in ("kind", "precision", "epilogue", "_pad")] + \
+    _fields_ = [(n, ctypes.c_int32) for n in ("kind", "precision", "epilogue", "tile")] + \
                [(n, ctypes.c_int64) for n in ("n", "ih", "iw", "ci", "co", "kh", "kw", "sh", "sw", "oh", "ow",
                                               "pad_top", "pad_left", "batch", "in_f", "out_f")] + \
                [("colstats", ctypes.c_void_p), ("eg_mask", ctypes.c_void_p), ("eg_res", ctypes.c_void_p),

@@ -23,4 +23,4 @@ def test_reference_cpp_api_on_the_b200():
     r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count("[PASS]") == 6
+    assert r.stdout.count("[PASS]") == 7
