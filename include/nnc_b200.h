@@ -91,6 +91,11 @@ int nnc_model_debug_keep_values(nnc_model* m, int on);
  * cross-entropy over the prediction's last axis (targets: probability rows). */
 int nnc_model_set_loss(nnc_model* m, int kind);
 int nnc_model_trainer_value(nnc_model* m, const char* name, float* out, int64_t n, int64_t* dims, int* rank);
+/* The same for runs (nnc_model_run with keep_values on): a value of the last
+ * run of a plan (0 inference, 1 train_fwd), for launch-by-launch parity of
+ * inference plans.                                                        */
+int nnc_model_run_value(nnc_model* m, int role, const char* name, float* out, int64_t n,
+                        int64_t* dims, int* rank);
 
 /* Data-parallel layout (runtime::dp_layout) as JSON: region order, ~bucket_bytes
  * all-reduce buckets and the backward launch after which each can start.

@@ -558,6 +558,29 @@ class F64Model:
         return lv, grads
 
 
+def local_forward_parity(model: "F64Model", feed, device_value, training: bool = False):
+    """Launch-by-launch parity of a forward pass (inference plans: BatchNorm
+    from moving statistics when training is False): every node re-evaluated
+    from the device's own inputs, as local_parity's forward half. Returns
+    {value: err} with err = ||dev - oracle|| / ||oracle||."""
+    res = {}
+    v = {k: model._st(np.asarray(x, np.float64)) for k, x in feed.items()}
+    for n in model.nodes:
+        name = n["name"]
+        ins = [v[i] for i in n.get("inputs", [])]
+        am = device_value(name + ".argmax") if n["op"] == "max_pooling2d" else None
+        y, _ = model.node_forward(n, ins, training, am)
+        dv = device_value(name)
+        if dv is not None:
+            b = np.asarray(y, np.float64)
+            nb = np.linalg.norm(b)
+            d = np.asarray(dv, np.float64).reshape(b.shape)
+            res[name] = float(np.linalg.norm(d - b) / nb) if nb > 0 else float(np.linalg.norm(d))
+            y = d
+        v[name] = y
+    return res
+
+
 def local_parity(model: "F64Model", feed, device_value, device_grads, target, loss="l1"):
     """Launch-by-launch parity of one training step: every node is re-evaluated
     by the oracle FROM THE DEVICE'S OWN INPUTS (forward values, max-pool

@@ -85,6 +85,7 @@ def _load():
         "nnc_model_debug_keep_values": (I, [P, I]),
         "nnc_model_set_loss": (I, [P, I]),
         "nnc_model_trainer_value": (I, [P, S, FP, I64, I64P, ctypes.POINTER(ctypes.c_int)]),
+        "nnc_model_run_value": (I, [P, I, S, FP, I64, I64P, ctypes.POINTER(ctypes.c_int)]),
         "nnc_model_trainer_prepare": (I, [P, FP, I64]),
         "nnc_model_trainer_step_device": (I, [P, D]),
         "nnc_model_trainer_loss": (I, [P, DP]),
@@ -370,6 +371,17 @@ class CompiledModel:
         """Bind the training step without arena reuse so every value survives
         the step (then read them with step_value)."""
         _check(_host.nnc_model_debug_keep_values(self._h, 1 if on else 0))
+
+    def run_value(self, name: str, role: str = "inference") -> np.ndarray:
+        """A value of the last run() (debug_keep_values(True) first): launch-by-launch
+        parity of inference plans."""
+        r = 1 if role == "train_fwd" else 0
+        dims = (ctypes.c_int64 * 8)()
+        rank = ctypes.c_int()
+        _check(_host.nnc_model_run_value(self._h, r, name.encode(), None, 0, dims, ctypes.byref(rank)))
+        arr = np.empty(tuple(dims[: rank.value]), dtype=np.float32)
+        _check(_host.nnc_model_run_value(self._h, r, name.encode(), _fptr(arr), arr.size, dims, ctypes.byref(rank)))
+        return arr
 
     def step_value(self, name: str) -> np.ndarray:
         """Device contents of a value of the last training step (forward or

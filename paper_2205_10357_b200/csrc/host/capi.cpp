@@ -360,6 +360,19 @@ int nnc_model_debug_keep_values(nnc_model* m, int on) {
     });
 }
 
+int nnc_model_run_value(nnc_model* m, int role, const char* name, float* out, int64_t n, int64_t* dims, int* rank) {
+    return guarded([&] {
+        const plan::ExecutionPlan& p0 = role == 1 ? m->plans.train_fwd : m->plans.inference;
+        Tensor v = runtime::last_run_value(runtime::plan_for_inputs(p0, m->inputs, m->opts.bindings), name);
+        if (rank) {
+            *rank = static_cast<int>(v.dims().size());
+            for (size_t i = 0; i < v.dims().size() && i < 8; ++i) dims[i] = v.dims()[i];
+        }
+        if (!out) return;
+        if (v.elements() != n) throw Error(Error::Code::ShapeMismatch, std::string("value size mismatch: ") + name);
+        std::memcpy(out, v.data(), v.byte_size());
+    });
+}
 int nnc_model_trainer_value(nnc_model* m, const char* name, float* out, int64_t n, int64_t* dims, int* rank) {
     return guarded([&] {
         runtime::Trainer& t = runtime::shared_trainer(m->plans, *m->host, runtime::default_device(), m->opts);

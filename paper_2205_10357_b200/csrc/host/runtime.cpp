@@ -472,6 +472,14 @@ struct Program {
         }
         return r;
     }
+    /// Whether a launch of plan `pi` writes any byte of [q, q+m) (fusion passes
+    /// may redirect or absorb a value's producer: a plan value whose producer
+    /// was folded away is never written).
+    bool written_by_plan(size_t pi, const char* q, int64_t m) const {
+        for (size_t k = 0; k < steps[pi].size(); ++k)
+            if (launch_touches(pi, k, q, m, true)) return true;
+        return false;
+    }
     bool launch_touches(size_t pi, size_t k, const char* q, int64_t m, bool outputs) const {
         for (const Range& r : launch_ranges(pi, k, outputs))
             if (r.overlaps(q, m)) return true;
@@ -1510,18 +1518,52 @@ ExecCache& bound_cache(const ExecutionPlan& p, const HostModel& model, Device& d
     std::map<std::string, void*> wptrs;
     for (const std::string& w : p.weight_names)
         wptrs[w] = weights ? (*weights)(w) : dev.weight_buffer(model, w, model.tensor(w), model.stamp(w));
-    if (!slot || slot->weight_ptrs != wptrs || slot->prog->precision != opts.gemm_precision) {
+    if (!slot || slot->weight_ptrs != wptrs || slot->prog->precision != opts.gemm_precision ||
+        slot->prog->keep_values != opts.keep_values) {
         slot = std::make_unique<ExecCache>();
         slot->prog = std::make_unique<Program>();
         slot->prog->dev = &dev;
         slot->prog->plans = {&p};
         slot->prog->precision = opts.gemm_precision;
+        slot->prog->keep_values = opts.keep_values;
         slot->prog->bind([&](const std::string& w) { return wptrs.at(w); },
                          [](const std::string&) -> void* { return nullptr; });
         slot->weight_ptrs = wptrs;
     }
     return *slot;
 }
+
+}  // namespace
+
+/// A value of the last execute of `p` on `device` (parity debugging): the
+/// program must have been bound with ExecOptions::keep_values, so no later
+/// launch of the run reused the value's arena bytes.
+Tensor last_run_value(const ExecutionPlan& p, const std::string& name, Device* device) {
+    Device& dev = device ? *device : default_device();
+    auto it = exec_caches().find({&dev, p.uid});
+    if (it == exec_caches().end() || !it->second)
+        throw Error(Error::Code::ShapeMismatch, "last_run_value: the plan has not run on this device");
+    Program& prog = *it->second->prog;
+    if (!prog.keep_values)
+        throw Error(Error::Code::ShapeMismatch, "last_run_value: bind with ExecOptions::keep_values");
+    const int s = p.find_value(name);
+    if (s < 0) throw Error(Error::Code::ShapeMismatch, "no value " + name + " in the plan");
+    const plan::ValueEntry& v = p.values[s];
+    if (v.storage != StorageClass::Buffer)
+        throw Error(Error::Code::ShapeMismatch, name + " lives in registers of a fused group");
+    Tensor t(p.dtype, v.dims);
+    bool fed = false;
+    for (uint32_t is : p.input_slots) fed = fed || p.values[is].name == name;
+    if (!fed && v.category != plan::MemCategory::Input && v.category != plan::MemCategory::Parameter &&
+        !prog.written_by_plan(0, static_cast<const char*>(prog.ptr(name)), static_cast<int64_t>(t.byte_size())))
+        throw Error(Error::Code::ShapeMismatch, name + " is never written: its producer was fused into another launch");
+    NNC_CHECK(nncb_sync(dev.ctx()));
+    NNC_CHECK(nncb_d2h(dev.ctx(), t.data(), prog.ptr(name), t.byte_size()));
+    NNC_CHECK(nncb_sync(dev.ctx()));
+    return t;
+}
+
+namespace {
 
 // first run eagerly (sizes scratch, compiles kernels); later runs replay a graph
 void run_bound(ExecCache& c, const ExecutionPlan& p, const ExecOptions& opts) {
@@ -2326,13 +2368,24 @@ void* Trainer::input_device_ptr(const std::string& name) { return impl->prog->pt
 
 Tensor Trainer::value(const std::string& name) {
     Impl& I = *impl;
-    for (const ExecutionPlan* p : I.prog->plans) {
+    for (size_t pi = 0; pi < I.prog->plans.size(); ++pi) {
+        const ExecutionPlan* p = I.prog->plans[pi];
         const int s = p->find_value(name);
         if (s < 0) continue;
         const plan::ValueEntry& v = p->values[s];
         if (v.storage != StorageClass::Buffer)
             throw Error(Error::Code::ShapeMismatch, name + " lives in registers of a fused group");
         Tensor t(p->dtype, v.dims);
+        bool fed = false;   // a graph input (also when the plan saves it for backward)
+        for (uint32_t is : p->input_slots) fed = fed || p->values[is].name == name;
+        if (!fed && v.category != plan::MemCategory::Input && v.category != plan::MemCategory::Parameter) {
+            bool written = false;
+            for (size_t q = 0; q < I.prog->plans.size() && !written; ++q)
+                written = I.prog->written_by_plan(q, static_cast<const char*>(I.prog->ptr(name)),
+                                                  static_cast<int64_t>(t.byte_size()));
+            if (!written)
+                throw Error(Error::Code::ShapeMismatch, name + " is never written: its producer was fused into another launch");
+        }
         NNC_CHECK(nncb_sync(I.dev->ctx()));
         NNC_CHECK(nncb_d2h(I.dev->ctx(), t.data(), I.prog->ptr(name), t.byte_size()));
         NNC_CHECK(nncb_sync(I.dev->ctx()));

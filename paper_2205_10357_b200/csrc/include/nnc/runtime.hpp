@@ -239,6 +239,10 @@ std::map<std::string, Tensor> execute_on(const plan::ExecutionPlan& p,
                                          const HostModel& model, Device* device,
                                          const ExecOptions& opts = {});
 
+/// A value of the last execute of `p` on `device` (parity debugging; the
+/// program must be bound with ExecOptions::keep_values, i.e. no arena reuse).
+Tensor last_run_value(const plan::ExecutionPlan& p, const std::string& name, Device* device = nullptr);
+
 struct LaunchProfile {
     std::string label, kind;
     double ms = 0, bytes = 0, flops = 0;

@@ -27,6 +27,9 @@ What is checked, and the north-star tolerances it is held to:
     kernels): forward within max(1e-5, the float32 CPU restatement's own error)
     of the float64 truth, SURVEY.md §8(c)'s protocol.
   * C5: one Dense(4096)+GELU+LayerNorm layer at batch 8192 (tf32): 2e-2.
+  * C3: ResNet-50-shaped inference at 224x224 (BatchNorm folded into the GEMM
+    epilogues), tf32 and bf16, launch by launch: within 2e-3 of the emulating
+    oracle and 2e-2 of the float64 truth.
   * A pre-activation residual graph (BatchNorm fed by an elementwise add, the
     arena reusing GEMM output addresses), which exercises the producer matching
     of the BN-statistics and BN-gradient-reduction fusions.
@@ -213,6 +216,54 @@ def test_c4_resnet50_bn_tf32x3_training_step_at_224_launch_by_launch():
     m = P.CompiledModel(doc, precision=P.PREC_TF32X3)
     randomize_norms(m, np.random.default_rng(4))
     local_step_parity(m, doc, {"x": x}, t, emu_tol=X3_TOL, truth_tol=X3_TOL, min_values=100, emulate=None)
+
+
+@pytest.mark.parametrize("precision,emulate", [(P.PREC_TF32, "tf32"), (P.PREC_BF16, "bf16")])
+def test_c3_resnet50_inference_at_224_launch_by_launch(precision, emulate):
+    """C3: ResNet-50-shaped inference (BatchNorm from moving statistics, folded
+    into the GEMM epilogues; fused residual joins) at 224x224, launch by
+    launch: the run bound without arena reuse, every materialized value read
+    back and re-derived by the oracle from the device's own inputs -- within
+    2e-3 of the precision-emulating oracle and 2e-2 of the float64 truth.
+    The moving statistics are calibrated to this batch's float64 training
+    statistics, so activations stay normalized through the depth."""
+    batch = 4
+    doc = W.resnet50(batch, bn=True)
+    x = W.uniform((batch, 224, 224, 3), 1, "x")
+    m = P.CompiledModel(doc, precision=precision)
+    randomize_norms(m, np.random.default_rng(5))
+    cal = oracle_for(m, doc)
+    cal.forward({"x": x}, training=True)
+    for key, st in cal.saved.items():
+        if not key.endswith(".stats"):
+            continue
+        mean, inv = np.asarray(st, np.float64).reshape(2, -1)
+        bn = key[: -len(".stats")]
+        eps = next(n.get("attrs", {}).get("epsilon", 1e-3) for n in cal.nodes if n["name"] == bn)
+        m.set_weight(bn + ".moving_mean", np.asarray(mean, np.float32))
+        m.set_weight(bn + ".moving_variance", np.asarray(1.0 / np.square(inv) - eps, np.float32))
+    m.debug_keep_values(True)
+    y = m.run({"x": x})["fc"]
+
+    def value(name):
+        try:
+            return m.run_value(name)
+        except P.NNCError:
+            return None   # fused-group registers / not materialized: the oracle's local value stands in
+
+    emu = R64.local_forward_parity(oracle_for(m, doc, emulate=emulate), {"x": x}, value)
+    truth = R64.local_forward_parity(oracle_for(m, doc), {"x": x}, value)
+    assert len(emu) >= 50, len(emu)
+    bad_e = {k: e for k, e in emu.items() if not e < 2e-3}
+    bad_t = {k: e for k, e in truth.items() if not e < TF32_TOL}
+    print("c3 launch by launch: %d values, worst vs emulated %.3g, vs f64 truth %.3g" %
+          (len(emu), max(emu.values()), max(truth.values())))
+    assert not bad_e, bad_e
+    assert not bad_t, bad_t
+    # end to end (recorded: deep fixed-statistics forwards amplify per-layer rounding)
+    e2e = rel_norm(y, oracle_for(m, doc).forward({"x": x}, training=False)["fc"])
+    print("c3 logits end to end vs f64 truth %.3g" % e2e)
+    m.debug_keep_values(False)
 
 
 def test_c5_layer_8192x4096_bf16():
