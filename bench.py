@@ -346,6 +346,12 @@ def main():
     launches = timer.launches() - l0
     if cfg["kind"] == "train":   # graph replays are not counted by the host-side counter
         launches = max(launches, model.launches_per_step() * args.steps)
+    else:
+        # inference / chain runs replay a CUDA graph: count one eager run's
+        # kernel launches (profile_run enqueues every launch of the plan)
+        la = timer.launches()
+        model.profile_run(inputs, "inference")
+        launches = max(launches, (timer.launches() - la) * args.steps)
     ms = max_over_ranks(ms)
     ms_per_step = ms / args.steps
     value = units / (ms_per_step / 1000.0)
