@@ -94,6 +94,7 @@ struct TcParams {
     int tma_store;      // epilogue through smem + TMA store (else direct stores)
     int stages;         // smem ring depth (sized so 2 CTAs fit per SM when N is small)
     int nostore;        // tuning knob: skip the output stores (epilogue cost probe)
+    unsigned long long* trace;   // probe (NNCB_TC_TRACE): per CTA / local tile event timestamps
     int stg_cols;       // epilogue transpose width per pass: 32, 16 or 8 columns (4/2/1 KB per warp)
     int stg_bufs;       // staging tiles per warp: 2 lets a pass's TMA store overlap staging of the next
     // --- halo (3x3 stride-1 forward): one (TW+2) x TH input patch per (32-channel
@@ -312,6 +313,27 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
                  ::"r"(smem_u32(bar)), "h"(static_cast<uint16_t>(3))
                  : "memory");
 }
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// Probe (NNCB_TC_TRACE, tools/tc_trace.py): event timestamps per CTA and local
+// tile -- 0 MMA tile start, 1 MMA commit, 2 epilogue sees the accumulator,
+// 3 its TMEM release, 4/5 epilogue warps 2/9 done, 6 producer tile start.
+// Compiled in only with -DNNCB_TC_TRACE_PROBE (it costs the register-capped
+// builds stack space); `make PROBE=1` builds it.
+#ifdef NNCB_TC_TRACE_PROBE
+#define TC_TRACE(local, ev)                                                                                   \
+    do {                                                                                                      \
+        if (P.trace && (local) < 64) P.trace[(static_cast<int64_t>(blockIdx.x) * 64 + (local)) * 8 + (ev)] = gtimer(); \
+    } while (0)
+#else
+#define TC_TRACE(local, ev) \
+    do {                    \
+    } while (0)
+#endif
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile(
@@ -840,8 +862,10 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                     }
                 }
         }
-        for (int64_t t = t_begin; t < P.tiles; t += t_step) {
+        uint32_t plocal = 0;
+        for (int64_t t = t_begin; t < P.tiles; t += t_step, ++plocal) {
             const Tile T = decode(t);
+            TC_TRACE(plocal, 6);
             if (P.mode == MODE_CONV && P.halo) {
                 // k-step (kernel row dh, channel block cb): the (TW+2) x TH patch at
                 // (tw0 - 1, th0 - 1 + dh) and the row's three taps' weights
@@ -960,6 +984,7 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
             // every tile takes an accumulator turn (tiles without K steps commit
             // immediately and the epilogue writes zeros), so phases stay in step
             if (local >= 2) mbar_wait(&tmem_empty[acc], ((local / 2) - 1) & 1);
+            if (lane == 0) TC_TRACE(local, 0);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t d = tmem_base + acc * static_cast<uint32_t>(P.bn);
             for (int i = 0; i < T.nk; ++i) {
@@ -1037,6 +1062,7 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                 else
                     mma_commit(&tmem_full[acc]);
             }
+            if (lane == 0) TC_TRACE(local, 1);
             __syncwarp();
         }
     } else if (MA && warp >= 10) {
@@ -1161,6 +1187,7 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                 }
             }
             mbar_wait(&tmem_full[acc], (local / 2) & 1);
+            if (warp == 2 && lane == 0) TC_TRACE(local, 2);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             float* dst = nullptr;
             bool valid = false;
@@ -1198,6 +1225,7 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                                          : "memory");
                     }
                     arrived = true;
+                    if (warp == 2 && lane == 0) TC_TRACE(local, 3);
                 }
                 const int64_t col0 = T.n0 + c * 32;
                 if (T.nk == 0) {
@@ -1282,6 +1310,8 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                     }
                 }
             }
+            if (warp == 2 && lane == 0) TC_TRACE(local, 4);
+            if (warp == 9 && lane == 0) TC_TRACE(local, 5);
             if (!arrived && lane == 0) {   // a warp without a chunk in this tile still arrives once
                 if (PAIR)
                     mbar_arrive_cluster(mapa_u32(&tmem_empty[acc], 0));
@@ -1715,6 +1745,32 @@ int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CU
     if (P.eg) per_sm = 1;      // the gradient epilogue needs the 168-register build
     unsigned grid = static_cast<unsigned>(std::min<int64_t>(P.tiles, static_cast<int64_t>(ctx->sm_count) * per_sm));
     const unsigned threads = manual ? THREADS + 128 : THREADS;
+    // probe (NNCB_TC_TRACE=path): per-CTA tile event timestamps of each launch on
+    // this path, appended to `path` (tools/tc_trace.py reads them)
+    static const char* trace_path = getenv("NNCB_TC_TRACE");
+    static unsigned long long* trace_buf = nullptr;
+    const size_t trace_bytes = static_cast<size_t>(grid) * 64 * 8 * sizeof(unsigned long long);
+    if (trace_path) {
+        if (!trace_buf) NNCB_CUDA(cudaMalloc(&trace_buf, 2 * 148 * 64 * 8 * sizeof(unsigned long long)));
+        NNCB_CUDA(cudaMemsetAsync(trace_buf, 0, trace_bytes, ctx->stream));
+        P.trace = trace_buf;
+    }
+    struct TraceDump {
+        const char* path; unsigned long long* buf; size_t bytes; nncb_ctx* ctx; const TcParams& P; unsigned grid; int per_sm;
+        ~TraceDump() {
+            if (!path) return;
+            std::vector<unsigned long long> h(bytes / 8);
+            cudaStreamSynchronize(ctx->stream);
+            cudaMemcpy(h.data(), buf, bytes, cudaMemcpyDeviceToHost);
+            if (FILE* f = fopen(path, "ab")) {
+                const long long hdr[6] = {static_cast<long long>(grid), static_cast<long long>(P.tiles), P.bn, P.stages,
+                                          P.stg_bufs, per_sm};
+                fwrite(hdr, sizeof(hdr), 1, f);
+                fwrite(h.data(), 8, h.size(), f);
+                fclose(f);
+            }
+        }
+    } trace_dump{trace_path, trace_buf, trace_bytes, ctx, P, grid, per_sm};
     if (P.colstats && manual)
         tc_gemm_kernel<true, true, 1, false><<<grid, threads, smem, ctx->stream>>>(ma, mb, mc, P, em);
     else if (manual)
