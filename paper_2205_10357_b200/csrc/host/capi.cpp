@@ -598,6 +598,8 @@ const char* nnc_model_tune(nnc_model* m, int warmup, int trials, const char* inj
         }
         nlohmann::json j;
         size_t attached = 0;
+        runtime::release(m->plans);   // bound programs / trainers of the untuned plans
+        m->trainer = nullptr;
         for (const auto& [role, g] : {std::pair<const char*, const hlir::Graph*>{"inference", &m->versions.inference},
                                       {"train_fwd", &m->versions.train_fwd},
                                       {"train_bwd", &m->versions.train_bwd}}) {
