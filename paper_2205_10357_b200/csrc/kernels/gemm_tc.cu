@@ -109,6 +109,10 @@ struct TcParams {
     uint32_t bres_bytes;
     int halo_kw;        // halo 1: taps per kernel row (3; 2 for the space-to-depth stem, spaced dil_w rows)
     double* colstats;   // fused BatchNorm statistics: [0,N) sum, [N,2N) sum of squares
+    // order-independent accumulation of colstats: per column two fixed-point
+    // (2^-40) sums split in 32-bit limbs, [sum hi | sum lo | sq hi | sq lo][N],
+    // then a CTA ticket counter; the last CTA converts to the doubles above
+    unsigned long long* cs_fixed;
     // --- manual A (channel counts that do not fill a 32-wide TMA block) -----
     // Builder warps gather A straight from the NHWC activation into the
     // K-major 128B-swizzled stage layout: no im2col matrix in HBM.
@@ -334,6 +338,24 @@ __device__ __forceinline__ unsigned long long gtimer() {
     do {                    \
     } while (0)
 #endif
+
+// Order-independent column sums: v is added as round-toward-zero fixed point
+// with 40 fraction bits, split into a high part (v / 2^-8, integer) and a low
+// 32-bit part, each accumulated by 64-bit integer atomics (exact, so the
+// total does not depend on the order in which CTAs and warps flush). |sum| <
+// 2^55; each contribution loses < 2^-40 (below every float32 BatchNorm
+// statistic's resolution here).
+__device__ __forceinline__ void fixed_add(unsigned long long* hi, unsigned long long* lo, double v) {
+    const double t = v * 1099511627776.0;                  // 2^40
+    const double h = floor(t * 2.3283064365386963e-10);   // floor(t / 2^32)
+    const double l = t - h * 4294967296.0;                 // [0, 2^32): exact
+    atomicAdd(hi, static_cast<unsigned long long>(static_cast<long long>(h)));
+    atomicAdd(lo, static_cast<unsigned long long>(l));
+}
+__device__ __forceinline__ double fixed_value(unsigned long long hi, unsigned long long lo) {
+    return static_cast<double>(static_cast<long long>(hi)) * 0.00390625 +   // 2^-8
+           static_cast<double>(lo) * 9.094947017729282e-13;                // 2^-40
+}
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile(
@@ -1327,8 +1349,11 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                     for (int k = 0; k < 4; ++k) {
                         const int64_t col = T.n0 + (half + 2 * k) * 32 + lane;
                         if (half + 2 * k < nchunks && col < P.N && cs_sum[k] != 0.0) {
-                            atomicAdd(P.colstats + col, cs_sum[k]);
-                            atomicAdd(P.colstats + P.N + col, cs_sq[k]);
+                            // integer limbs: the sum is the same in any order (deterministic)
+                            unsigned long long* f = P.cs_fixed;
+                            const int64_t N = P.N;
+                            fixed_add(f + col, f + N + col, cs_sum[k]);
+                            fixed_add(f + 2 * N + col, f + 3 * N + col, cs_sq[k]);
                         }
                         cs_sum[k] = 0.0;
                         cs_sq[k] = 0.0;
@@ -1338,6 +1363,26 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
         }
         if (P.tma_out && lane == 0)   // every TMA store issued by this warp has completed
             asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        if (CS) {
+            // the last CTA to finish converts the fixed-point column sums
+            volatile uint32_t* cs_last = tmem_slot + 1;   // a free word beside the TMEM address slot
+            asm volatile("bar.sync 1, 256;" ::: "memory");   // the 8 epilogue warps' flushes are issued
+            if (warp == 2 && lane == 0) {
+                __threadfence();
+                const unsigned long long ticket = atomicAdd(P.cs_fixed + 4 * P.N, 1ull);
+                *cs_last = ticket == gridDim.x - 1 ? 1u : 0u;
+            }
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            if (*cs_last) {
+                __threadfence();
+                const int64_t N = P.N;
+                for (int64_t c = threadIdx.x - 64; c < N; c += 256) {
+                    const unsigned long long* f = P.cs_fixed;
+                    P.colstats[c] = fixed_value(__ldcg(f + c), __ldcg(f + N + c));
+                    P.colstats[N + c] = fixed_value(__ldcg(f + 2 * N + c), __ldcg(f + 3 * N + c));
+                }
+            }
+        }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     if (PAIR)
@@ -2702,7 +2747,12 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
             P.eg_stats = d->eg_stats;
             P.colstats = d->eg_sums;   // the CS build accumulates the dy sums
         }
-        if (P.colstats) NNCB_CUDA(cudaMemsetAsync(P.colstats, 0, sizeof(double) * 2 * Nc, ctx->stream));
+        if (P.colstats) {   // fixed-point accumulators + CTA ticket; the kernel's last CTA writes colstats
+            const size_t fb = sizeof(unsigned long long) * (4 * static_cast<size_t>(Nc) + 1);
+            P.cs_fixed = static_cast<unsigned long long*>(colstats_fixed_buffer(ctx, fb));
+            if (!P.cs_fixed) return fail("gemm: column-statistics buffer allocation failed");
+            NNCB_CUDA(cudaMemsetAsync(P.cs_fixed, 0, fb, ctx->stream));
+        }
         P.n_tiles = (Nc + P.bn - 1) / P.bn;
         P.pix_tiles = tiles;
         P.pix_pairs = (tiles + 1) / 2;

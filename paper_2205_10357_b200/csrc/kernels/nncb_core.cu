@@ -66,6 +66,19 @@ void* bn_inv_buffer(nncb_ctx* ctx, size_t bytes) {
     return ctx->bn_inv;
 }
 
+void* colstats_fixed_buffer(nncb_ctx* ctx, size_t bytes) {
+    if (bytes <= ctx->cs_fixed_bytes) return ctx->cs_fixed;
+    if (ctx->cs_fixed) ctx->retired.push_back(ctx->cs_fixed);   // captured graphs may use it
+    const size_t want = bytes < (1u << 16) ? (1u << 16) : bytes;
+    if (cudaMalloc(&ctx->cs_fixed, want) != cudaSuccess) {
+        ctx->cs_fixed = nullptr;
+        ctx->cs_fixed_bytes = 0;
+        return nullptr;
+    }
+    ctx->cs_fixed_bytes = want;
+    return ctx->cs_fixed;
+}
+
 void* workspace(nncb_ctx* ctx, size_t bytes) {
     if (bytes <= ctx->workspace_bytes) return ctx->workspace;
     if (ctx->workspace) ctx->retired.push_back(ctx->workspace);
@@ -138,6 +151,7 @@ int nncb_destroy(nncb_ctx* c) {
     for (void* p : c->bf16_buf)
         if (p) cudaFree(p);
     if (c->bn_inv) cudaFree(c->bn_inv);
+    if (c->cs_fixed) cudaFree(c->cs_fixed);
     cudaStreamSynchronize(c->comm_stream);
     for (cudaEvent_t e : c->fork_events) cudaEventDestroy(e);
     cudaStreamDestroy(c->stream);

@@ -43,6 +43,8 @@ struct nncb_ctx {
     size_t bf16_bytes[2] = {0, 0};
     void* bn_inv = nullptr;              // per-call invstd of a BN_AFFINE epilogue
     size_t bn_inv_bytes = 0;
+    void* cs_fixed = nullptr;            // fixed-point column-statistics accumulators of a GEMM epilogue
+    size_t cs_fixed_bytes = 0;
     // fork/join events between the compute and comm streams, reused round
     // robin (created once: nothing is created or destroyed during a capture)
     std::vector<cudaEvent_t> fork_events;
@@ -110,6 +112,7 @@ inline unsigned grid_for(const nncb_ctx* ctx, int64_t work_items, int threads, i
 void* scratch(nncb_ctx* ctx, size_t bytes);
 void* bf16_buffer(nncb_ctx* ctx, int which, size_t bytes);
 void* bn_inv_buffer(nncb_ctx* ctx, size_t bytes);
+void* colstats_fixed_buffer(nncb_ctx* ctx, size_t bytes);
 int affine_relu_output(nncb_ctx* ctx, const nncb_gemm_desc* d, float* out);
 void* workspace(nncb_ctx* ctx, size_t bytes);
 void ew_release(nncb_ew_kernel* k);
