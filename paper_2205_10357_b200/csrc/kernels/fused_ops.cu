@@ -570,19 +570,45 @@ __global__ void bn_finalize_k(const double* __restrict__ cs, float* __restrict__
     stats[C + c] = (float)(1.0 / sqrt(var + eps));
 }
 
-// colstats accumulation from a materialized output (used when the GEMM ran on
-// the exact path): cs[c] += sum_r y, cs[C+c] += sum_r y^2.
-__global__ void colstats_k(const float* __restrict__ y, double* __restrict__ cs, int64_t rows, int64_t C) {
-    int64_t c = blockIdx.x * 32 + threadIdx.x;
+// colstats from a materialized output (used when the GEMM ran on the exact
+// path): cs[c] = sum_r y, cs[C+c] = sum_r y^2, in double. Chunk y of the rows
+// writes its partials to part[y][2C] (block (32, 8), rows strided by 8 within
+// the chunk, the 8 row sums folded in order); colstats_fold_k adds the chunks
+// in order -- deterministic, no atomics.
+__global__ void colstats_k(const float* __restrict__ y, double* __restrict__ part, int64_t rows, int64_t C,
+                           int64_t rpc) {
+    const int64_t c = blockIdx.x * 32 + threadIdx.x;
+    const int64_t r0 = blockIdx.y * rpc, r1 = min(rows, r0 + rpc);
+    double s0 = 0, s1 = 0;
+    if (c < C)
+        for (int64_t r = r0 + threadIdx.y; r < r1; r += 8) {
+            const double v = y[r * C + c];
+            s0 += v;
+            s1 += v * v;
+        }
+    __shared__ double sh[2][8][33];
+    sh[0][threadIdx.y][threadIdx.x] = s0;
+    sh[1][threadIdx.y][threadIdx.x] = s1;
+    __syncthreads();
+    if (threadIdx.y != 0 || c >= C) return;
+    for (int k = 1; k < 8; ++k) {
+        s0 += sh[0][k][threadIdx.x];
+        s1 += sh[1][k][threadIdx.x];
+    }
+    part[blockIdx.y * 2 * C + c] = s0;
+    part[blockIdx.y * 2 * C + C + c] = s1;
+}
+
+__global__ void colstats_fold_k(const double* __restrict__ part, int64_t chunks, int64_t C, double* __restrict__ cs) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= C) return;
     double s0 = 0, s1 = 0;
-    for (int64_t r = blockIdx.y * (int64_t)blockDim.y + threadIdx.y; r < rows; r += (int64_t)gridDim.y * blockDim.y) {
-        double v = y[r * C + c];
-        s0 += v;
-        s1 += v * v;
+    for (int64_t k = 0; k < chunks; ++k) {
+        s0 += part[k * 2 * C + c];
+        s1 += part[k * 2 * C + C + c];
     }
-    atomicAdd(cs + c, s0);
-    atomicAdd(cs + C + c, s1);
+    cs[c] = s0;
+    cs[C + c] = s1;
 }
 
 __global__ void cumsum_k(const float* __restrict__ x, float* __restrict__ y, int64_t outer, int64_t len, int64_t inner,
@@ -1161,9 +1187,14 @@ __global__ void sgd_k(float* __restrict__ w, const float* __restrict__ g, int64_
 
 namespace nncb {
 int colstats_from_output(nncb_ctx* ctx, const float* y, double* cs, int64_t rows, int64_t C) {
-    NNCB_CUDA(cudaMemsetAsync(cs, 0, sizeof(double) * 2 * C, ctx->stream));
-    dim3 grid((unsigned)((C + 31) / 32), (unsigned)std::min<int64_t>(1024, (rows + 255) / 256));
-    colstats_k<<<grid, dim3(32, 8), 0, ctx->stream>>>(y, cs, rows, C);
+    if (C <= 0) return 0;
+    const int64_t chunks = std::max<int64_t>(1, std::min<int64_t>(1024, (rows + 255) / 256));
+    const int64_t rpc = (rows + chunks - 1) / chunks;
+    double* part = static_cast<double*>(scratch(ctx, sizeof(double) * 2 * C * chunks));
+    if (!part) return fail("colstats: scratch allocation failed");
+    colstats_k<<<dim3((unsigned)((C + 31) / 32), (unsigned)chunks), dim3(32, 8), 0, ctx->stream>>>(y, part, rows, C, rpc);
+    NNCB_LAUNCHED(ctx);
+    colstats_fold_k<<<(unsigned)((C + 127) / 128), 128, 0, ctx->stream>>>(part, chunks, C, cs);
     NNCB_LAUNCHED(ctx);
     return 0;
 }

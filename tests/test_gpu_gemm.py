@@ -105,10 +105,14 @@ def test_dense(b, i, o):
     check(tc, ex)
 
 
-@pytest.mark.parametrize("shape", [(2, 14, 14, 64, 64, 3, 1), (2, 32, 32, 3, 64, 7, 2), (3, 7, 7, 128, 96, 1, 1)])
-def test_conv_fwd_fused_column_statistics(shape):
+@pytest.mark.parametrize("precision", [0, 1])
+@pytest.mark.parametrize("shape", [(2, 14, 14, 64, 64, 3, 1), (2, 32, 32, 3, 64, 7, 2), (3, 7, 7, 128, 96, 1, 1),
+                                   (16, 28, 28, 128, 256, 1, 1)])
+def test_conv_fwd_fused_column_statistics(shape, precision):
     """NNCB_EPI_COLSTATS: per-channel sum / sum of squares of the conv output
-    accumulated in the tcgen05 epilogue (BatchNorm statistics), vs the output."""
+    accumulated in the tcgen05 epilogue (fixed-point integer atomics) or, on
+    the exact path, by a deterministic pass over the output -- vs the output,
+    and bitwise identical when the call is repeated."""
     import ctypes
     n, ih, iw, ci, co, k, s = shape
     g = conv_geom(n, ih, iw, ci, co, k, s)
@@ -118,12 +122,15 @@ def test_conv_fwd_fused_column_statistics(shape):
     xd, wd = Dev(x), Dev(w)
     cs = Dev(nbytes=2 * co * 8)
     out = Dev(nbytes=n * g["oh"] * g["ow"] * co * 4)
-    d = GemmDesc(kind=CONV_FWD, precision=0, epilogue=4, colstats=cs.p.value, **g)
+    d = GemmDesc(kind=CONV_FWD, precision=precision, epilogue=4, colstats=cs.p.value, **g)
     gemm(d, xd, wd, None, out)
     y = out.get((n * g["oh"] * g["ow"], co)).astype(np.float64)
     got = np.frombuffer(cs.get((4 * co,)).tobytes(), np.float64)
     assert np.allclose(got[:co], y.sum(0), rtol=1e-5, atol=1e-3)
     assert np.allclose(got[co:], (y * y).sum(0), rtol=1e-5, atol=1e-3)
+    gemm(d, xd, wd, None, out)
+    again = np.frombuffer(cs.get((4 * co,)).tobytes(), np.float64)
+    assert np.array_equal(got, again)
 
 
 SMALL_C = [c for c in CONVS if c[3] % 32 != 0 and c[5] > 1]
