@@ -254,6 +254,15 @@ typedef struct {
     double bn_eps;
     /* NNCB_EPI_RESIDUAL operand                                              */
     const float* residual;
+    /* Weight gradients (NNCB_CONV_WGRAD / NNCB_DENSE_WGRAD) with sgd_w set:
+     * the SGD update of those weights from the gradient this call writes,
+     * w = (float)((double)w - (*sgd_lr) * sgd_scale * (double)dW) (reference
+     * runtime.cpp:485-496), fused into the split-K fold that produces dW (or
+     * issued by the call right after it on the other routes). Valid when no
+     * later launch reads the old weights.                                    */
+    float* sgd_w;
+    const double* sgd_lr;
+    double sgd_scale;
 } nncb_gemm_desc;
 
 /* One launch transposing many row-major [rows][cols] matrices into [cols][rows]

@@ -132,6 +132,9 @@ struct BoundLaunch {
     float* eg_sgx = nullptr;
     std::vector<nncb_ew_instr> ew_prog;     // rewritten Ew program (empty: the plan's own)
     int ew_regs = 0;
+    // weight gradient whose weights the training step updates in the same
+    // call (nncb_gemm_desc::sgd_w, the update fused into the split-K fold)
+    float* sgd_w = nullptr;
     // device bytes bound beyond the plan arguments by a fusion pass (folded
     // reductions' operands and results): what the launch additionally reads
     // or writes, for the producer / hazard checks of later passes
@@ -143,12 +146,20 @@ struct BoundLaunch {
     std::vector<Extra> extra;
 };
 
-void enqueue(nncb_ctx* ctx, const BoundLaunch& b) {
+void enqueue(nncb_ctx* ctx, const BoundLaunch& b, const double* sgd_lr = nullptr, double sgd_scale = 1.0) {
     if (b.skip) return;
     auto P = [&](size_t i) { return static_cast<float*>(b.ptrs.at(i)); };
     switch (b.kind) {
         case LaunchKind::Ew: NNC_CHECK(nncb_ew_launch(ctx, b.ew, b.ptrs.data(), b.n, b.c)); break;
         case LaunchKind::Gemm:
+            if (b.sgd_w && sgd_lr) {   // the training step's update of these weights, fused into the call
+                nncb_gemm_desc d = b.gemm;
+                d.sgd_w = b.sgd_w;
+                d.sgd_lr = sgd_lr;
+                d.sgd_scale = sgd_scale;
+                NNC_CHECK(nncb_gemm(ctx, &d, P(0), P(1), b.flag0 ? P(2) : nullptr, P(b.ptrs.size() - 1)));
+                break;
+            }
             NNC_CHECK(nncb_gemm(ctx, &b.gemm, P(0), P(1), b.flag0 ? P(2) : nullptr, P(b.ptrs.size() - 1)));
             if (b.eg_sg)
                 NNC_CHECK(nncb_colsums_to_float(ctx, b.gemm.eg_sums, b.eg_sg, b.eg_sgx,
@@ -1171,14 +1182,14 @@ struct Program {
         return b;
     }
 
-    void enqueue_plan(size_t pi, std::vector<std::string>* trace,
-                      const std::function<void(size_t)>& after = nullptr) const {
+    void enqueue_plan(size_t pi, std::vector<std::string>* trace, const std::function<void(size_t)>& after = nullptr,
+                      const double* sgd_lr = nullptr, double sgd_scale = 1.0) const {
         const auto& labels = step_labels[pi];
         size_t li = 0;
         plan_prologue(pi);
         for (size_t k = 0; k < steps[pi].size(); ++k) {
             while (trace && li < labels.size() && labels[li].first == k) trace->push_back("exec:" + labels[li++].second);
-            enqueue(dev->ctx(), steps[pi][k]);
+            enqueue(dev->ctx(), steps[pi][k], sgd_lr, sgd_scale);
             if (after) after(k);
         }
         while (trace && li < labels.size()) trace->push_back("exec:" + labels[li++].second);
@@ -2020,6 +2031,12 @@ struct Trainer::Impl {
     void* graph = nullptr;
     void* graph_nosgd = nullptr;
     DpLayout layout;                                      // region order and all-reduce buckets
+    // weights updated inside their weight-gradient call at G = 1 (the
+    // reference's update fused into the backward, runtime.cpp:485-496), and
+    // per bucket the element ranges the bucket update still covers
+    std::set<std::string> fused_sgd;
+    std::vector<std::vector<std::pair<int64_t, int64_t>>> bucket_rest;
+    bool fused_planned = false;
     uint64_t launches_per_step = 0;
     bool warmed = false;
     // pipelined stepping (stage / launch_staged / staged_loss): two staging slots
@@ -2070,12 +2087,67 @@ struct Trainer::Impl {
     /// compute stream. The compute stream joins the comm stream at the end
     /// (before the next step's forward reads the weights). The learning rate
     /// is read from device memory, so the captured graph survives lr changes.
+    /// G = 1: a weight whose gradient is written last by a weight-gradient
+    /// GEMM, after every backward launch that reads the weight, is updated by
+    /// that call (the update fused into its split-K fold); the bucket updates
+    /// cover the remaining weights. NNC_NO_FUSED_SGD=1 keeps bucket updates only.
+    void plan_fused_sgd() {
+        fused_planned = true;
+        fused_sgd.clear();
+        if (!std::getenv("NNC_NO_FUSED_SGD") && prog->steps.size() > 1) {
+            auto& bwd = prog->steps[1];
+            for (const std::string& w : layout.weights) {
+                const int64_t k = layout.grad_launch.count(w) ? layout.grad_launch.at(w) : -1;
+                if (k < 0 || k >= static_cast<int64_t>(bwd.size())) continue;
+                BoundLaunch& b = bwd[static_cast<size_t>(k)];
+                if (b.skip || b.kind != LaunchKind::Gemm ||
+                    (b.gemm.kind != NNCB_CONV_WGRAD && b.gemm.kind != NNCB_DENSE_WGRAD))
+                    continue;
+                float* g = static_cast<float*>(grads) + layout.offset.at(w);
+                if (b.ptrs.back() != g) continue;   // the call writes this weight's final gradient
+                auto rd = layout.read_launch.find(w);
+                if (rd != layout.read_launch.end() && rd->second >= k) continue;   // a later launch reads the weights
+                b.sgd_w = static_cast<float*>(params) + layout.offset.at(w);
+                fused_sgd.insert(w);
+            }
+        }
+        if (std::getenv("NNC_FUSED_SGD_DEBUG")) {
+            int64_t fe = 0, te = 0;
+            for (const std::string& w : layout.weights)
+                if (layout.grad_launch.at(w) >= 0) {
+                    te += layout.elements.at(w);
+                    if (fused_sgd.count(w)) fe += layout.elements.at(w);
+                }
+            std::fprintf(stderr, "[fused sgd] %zu of %zu weights (%lld of %lld elements) updated in their weight-gradient call\n",
+                         fused_sgd.size(), layout.weights.size(), (long long)fe, (long long)te);
+        }
+        bucket_rest.assign(layout.buckets.size(), {});
+        for (size_t bi = 0; bi < layout.buckets.size(); ++bi) {
+            const DpBucket& bk = layout.buckets[bi];
+            int64_t cur = bk.offset;
+            const int64_t end = bk.offset + bk.count;
+            std::vector<std::pair<int64_t, int64_t>> gaps;   // fused weights' ranges inside the bucket
+            for (const std::string& w : fused_sgd) {
+                const int64_t o = layout.offset.at(w), n = (layout.elements.at(w) + 63) / 64 * 64;
+                if (o < end && bk.offset < o + n) gaps.push_back({std::max(o, bk.offset), std::min(o + n, end)});
+            }
+            std::sort(gaps.begin(), gaps.end());
+            for (const auto& [a, e] : gaps) {
+                if (a > cur) bucket_rest[bi].push_back({cur, a - cur});
+                cur = std::max(cur, e);
+            }
+            if (cur < end) bucket_rest[bi].push_back({cur, end - cur});
+        }
+    }
+
     void enqueue_step(bool do_sgd) {
         nncb_ctx* ctx = dev->ctx();
         prog->enqueue_plan(0, nullptr);
         enqueue_loss();
         const bool comm = nncb_comm_active(ctx) != 0;
         const double scale = 1.0 / static_cast<double>(dev->nranks());
+        const bool fused = do_sgd && !comm;
+        if (fused && !fused_planned) plan_fused_sgd();
         std::map<int64_t, std::vector<StepAction>> after;
         for (const StepAction& a : step_schedule(layout, comm, do_sgd)) after[a.after].push_back(a);
         auto issue = [&](const StepAction& a) {
@@ -2089,17 +2161,26 @@ struct Trainer::Impl {
                 }
                 case StepAction::Update: {
                     const DpBucket& bk = layout.buckets[a.bucket];
+                    if (fused) {   // the weights not updated by their weight-gradient call
+                        for (const auto& [o, n] : bucket_rest[static_cast<size_t>(a.bucket)])
+                            NNC_CHECK(nncb_sgd_dev(ctx, NNCB_STREAM_COMM, static_cast<float*>(params) + o,
+                                                   static_cast<float*>(grads) + o, n, lr_dev, scale));
+                        break;
+                    }
                     NNC_CHECK(nncb_sgd_dev(ctx, NNCB_STREAM_COMM, static_cast<float*>(params) + bk.offset,
                                            static_cast<float*>(grads) + bk.offset, bk.count, lr_dev, scale));
                     break;
                 }
             }
         };
-        prog->enqueue_plan(1, nullptr, [&](size_t k) {
-            auto it = after.find(static_cast<int64_t>(k));
-            if (it != after.end())
-                for (const StepAction& a : it->second) issue(a);
-        });
+        prog->enqueue_plan(
+            1, nullptr,
+            [&](size_t k) {
+                auto it = after.find(static_cast<int64_t>(k));
+                if (it != after.end())
+                    for (const StepAction& a : it->second) issue(a);
+            },
+            fused && !fused_sgd.empty() ? lr_dev : nullptr, scale);
     }
 
     /// The loss launch(es): prediction + target -> d.pred and the device loss.

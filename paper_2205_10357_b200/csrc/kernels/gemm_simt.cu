@@ -264,8 +264,25 @@ int affine_relu_output(nncb_ctx* ctx, const nncb_gemm_desc* d, float* out) {
 }
 }  // namespace nncb
 
+int nncb_gemm_core(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const float* bias,
+                   float* out);
+
+// Weight gradients with sgd_w: the update is fused into the split-K fold when
+// the tensor-core route produced dW that way, else applied right after.
 extern "C" int nncb_gemm(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const float* bias,
                          float* out) {
+    nncb::take_sgd_applied();
+    const int rc = nncb_gemm_core(ctx, d, a, b, bias, out);
+    const bool fused = nncb::take_sgd_applied();
+    if (rc || !d->sgd_w || fused) return rc;
+    if (d->kind != NNCB_CONV_WGRAD && d->kind != NNCB_DENSE_WGRAD) return 0;
+    if (!d->sgd_lr) return nncb::fail("nncb_gemm: sgd_w needs sgd_lr");
+    const int64_t count = d->kind == NNCB_DENSE_WGRAD ? d->in_f * d->out_f : d->kh * d->kw * d->ci * d->co;
+    return nncb_sgd_dev(ctx, NNCB_STREAM_COMPUTE, d->sgd_w, out, count, d->sgd_lr, d->sgd_scale);
+}
+
+int nncb_gemm_core(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const float* bias,
+                   float* out) {
     const bool colstats = (d->epilogue & NNCB_EPI_COLSTATS) && d->colstats;
     if (colstats && d->kind != NNCB_CONV_FWD && d->kind != NNCB_DENSE_FWD)
         return nncb::fail("nncb_gemm: column statistics are a forward-GEMM epilogue");

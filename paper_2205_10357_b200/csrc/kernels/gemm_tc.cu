@@ -1411,6 +1411,50 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ partial, float* _
 // Split-K fold, 4 outputs per thread (float4) and four independent chains
 // over the splits (k mod 4), combined as (c0 + c1) + (c2 + c3): a fixed,
 // deterministic order with a quarter of the dependent-add latency.
+__device__ __forceinline__ float sgd_update(float w, float g, double lr, double scale) {
+    // the expression of fused_ops.cu sgd1, no contraction: (double)w - lr * ((double)g * scale)
+    return (float)__dsub_rn((double)w, __dmul_rn(lr, __dmul_rn((double)g, scale)));
+}
+
+// The split-K fold of a weight gradient with the SGD update of those weights
+// fused in: out = dW (same fixed order as splitk_reduce4_kernel), and
+// w = sgd_update(w, dW) -- the expression of sgd_dev_k, so the weights are
+// bitwise those of the separate update.
+__global__ void splitk_reduce4_sgd_kernel(const float4* __restrict__ partial, float4* __restrict__ out, int64_t count4,
+                                          int splits, float4* __restrict__ w, const double* __restrict__ lr_dev,
+                                          double scale) {
+    nncb::pdl_wait();
+    const double lr = *lr_dev;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count4; i += (int64_t)gridDim.x * blockDim.x) {
+        float4 c[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c[j] = j < splits ? __ldg(partial + j * count4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int k = 4; k < splits; k += 4) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (k + j < splits) {
+                    const float4 v = __ldg(partial + (k + j) * count4 + i);
+                    c[j].x = __fadd_rn(c[j].x, v.x);
+                    c[j].y = __fadd_rn(c[j].y, v.y);
+                    c[j].z = __fadd_rn(c[j].z, v.z);
+                    c[j].w = __fadd_rn(c[j].w, v.w);
+                }
+        }
+        float4 r;
+        r.x = __fadd_rn(__fadd_rn(c[0].x, c[1].x), __fadd_rn(c[2].x, c[3].x));
+        r.y = __fadd_rn(__fadd_rn(c[0].y, c[1].y), __fadd_rn(c[2].y, c[3].y));
+        r.z = __fadd_rn(__fadd_rn(c[0].z, c[1].z), __fadd_rn(c[2].z, c[3].z));
+        r.w = __fadd_rn(__fadd_rn(c[0].w, c[1].w), __fadd_rn(c[2].w, c[3].w));
+        out[i] = r;
+        float4 wv = w[i];
+        wv.x = sgd_update(wv.x, r.x, lr, scale);
+        wv.y = sgd_update(wv.y, r.y, lr, scale);
+        wv.z = sgd_update(wv.z, r.z, lr, scale);
+        wv.w = sgd_update(wv.w, r.w, lr, scale);
+        w[i] = wv;
+    }
+}
+
 __global__ void splitk_reduce4_kernel(const float4* __restrict__ partial, float4* __restrict__ out, int64_t count4,
                                       int splits) {
     nncb::pdl_wait();   // programmatic dependent of the split-K GEMM
@@ -1483,6 +1527,7 @@ thread_local int g_dil_w = 1;        // horizontal tap dilation for the next imp
 thread_local int g_force_tb = 0;     // 1: forward convolution with transposed (K-major) weights
 thread_local int g_force_bres = 0;   // 1: halo tiles with resident B (single N tile)
 thread_local int g_force_halo = 0;   // 1: 3x3 stride-1 conv through kernel-row halo patches; 2: full 3x3 patches
+thread_local bool g_sgd_applied = false;   // the last weight-gradient call applied its SGD update (fused fold)
 thread_local int g_bf16 = 0;         // the next implicit GEMM's A and B are bf16 copies (NNCB_PREC_BF16 route)
 thread_local const float* g_bn_inv = nullptr;   // BN_AFFINE: this call's per-column invstd (device)
 
@@ -1994,6 +2039,7 @@ int gemm_tc_s2d(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const fl
     }
     nncb_gemm_desc dd = *d;
     dd.b_kmajor = nullptr;   // the lowered conv has its own weight layout
+    dd.sgd_w = nullptr;      // its dW is scattered back afterwards: the caller applies the update
     dd.ih = H2; dd.iw = W2; dd.ci = 32; dd.kh = kh2; dd.kw = kwt; dd.sh = 1; dd.sw = 1;
     dd.pad_top = 0; dd.pad_left = 0;
     g_dil_w = pack ? 2 : 1;
@@ -2396,7 +2442,9 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
             g_force_tb = (c >> 18) & 1;
             g_force_halo = (c >> 20) & 1 ? 2 : (c >> 19) & 1;
             g_force_bres = (c >> 21) & 1;
-            int rc = gemm_tc_route(ctx, d, a, b, bias, tmp_out, handled);   // warm-up (and validity)
+            nncb_gemm_desc dt = *d;
+            dt.sgd_w = nullptr;   // candidates never update weights
+            int rc = gemm_tc_route(ctx, &dt, a, b, bias, tmp_out, handled);   // warm-up (and validity)
             if (rc || !*handled) {
                 g_force_bn = 0;
                 g_force_pair = 0;
@@ -2409,7 +2457,7 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
                 return rc;
             }
             cudaEventRecord(e0, ctx->stream);
-            for (int r = 0; r < 3 && !rc; ++r) rc = gemm_tc_route(ctx, d, a, b, bias, tmp_out, handled);
+            for (int r = 0; r < 3 && !rc; ++r) rc = gemm_tc_route(ctx, &dt, a, b, bias, tmp_out, handled);
             cudaEventRecord(e1, ctx->stream);
             g_force_bn = 0;
             g_force_pair = 0;
@@ -2809,7 +2857,14 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
     if (int rc = launch(ctx, ma, mb, mc, P)) return rc;
     if (P.splits > 1) {
         int64_t count = P.M * P.N;
-        if (count % 4 == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0)
+        const bool sgd = d->sgd_w && d->sgd_lr && (d->kind == NNCB_CONV_WGRAD || d->kind == NNCB_DENSE_WGRAD) &&
+                         (reinterpret_cast<uintptr_t>(d->sgd_w) & 15) == 0;
+        if (sgd && count % 4 == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+            NNCB_CUDA(launch_pdl(splitk_reduce4_sgd_kernel, dim3(grid_for(ctx, count / 4, 256)), dim3(256), ctx->stream,
+                                 reinterpret_cast<const float4*>(P.partial), reinterpret_cast<float4*>(out), count / 4,
+                                 P.splits, reinterpret_cast<float4*>(d->sgd_w), d->sgd_lr, d->sgd_scale));
+            g_sgd_applied = true;
+        } else if (count % 4 == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0)
             NNCB_CUDA(launch_pdl(splitk_reduce4_kernel, dim3(grid_for(ctx, count / 4, 256)), dim3(256), ctx->stream,
                                  reinterpret_cast<const float4*>(P.partial), reinterpret_cast<float4*>(out), count / 4,
                                  P.splits));
@@ -2876,6 +2931,14 @@ extern "C" int nncb_gemm_tuning_import(const char* text) {
 }
 
 extern "C" int nncb_gemm_tuning_mode(void) { return nncb::tune_mode(); }
+
+namespace nncb {
+bool take_sgd_applied() {
+    const bool v = g_sgd_applied;
+    g_sgd_applied = false;
+    return v;
+}
+}  // namespace nncb
 
 extern "C" int nncb_gemm_candidates(const nncb_gemm_desc* d, int32_t* codes, int cap, int* n) {
     if (!d || !n) return nncb::fail("nncb_gemm_candidates: null argument");

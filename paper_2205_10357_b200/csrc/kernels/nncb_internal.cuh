@@ -124,6 +124,9 @@ int gemm_simt(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const floa
               float* out);
 int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const float* bias,
             float* out, bool* handled);
+// whether the last weight-gradient GEMM on this thread applied its fused SGD
+// update (and clears the flag)
+bool take_sgd_applied();
 // NNCB_PREC_TF32X3: split operands, tf32 GEMM over the K-concatenated problem
 int gemm_tc_x3(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float* b, const float* bias,
                float* out, bool* handled);

@@ -18,7 +18,8 @@ class GemmDesc(ctypes.Structure):
                 ("eg_x", ctypes.c_void_p), ("eg_stats", ctypes.c_void_p), ("eg_sums", ctypes.c_void_p),
                 ("b_kmajor", ctypes.c_void_p), ("bn_mean", ctypes.c_void_p), ("bn_var", ctypes.c_void_p),
                 ("bn_gamma", ctypes.c_void_p), ("bn_beta", ctypes.c_void_p), ("bn_eps", ctypes.c_double),
-                ("residual", ctypes.c_void_p)]
+                ("residual", ctypes.c_void_p), ("sgd_w", ctypes.c_void_p), ("sgd_lr", ctypes.c_void_p),
+                ("sgd_scale", ctypes.c_double)]
 
 
 class TransposeJob(ctypes.Structure):
