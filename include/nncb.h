@@ -383,6 +383,11 @@ int nncb_sgd(nncb_ctx* ctx, float* w, const float* g, int64_t n, double lr, doub
  * right after its all-reduce, overlapping the rest of the backward pass).  */
 int nncb_sgd_dev(nncb_ctx* ctx, int stream, float* w, const float* g, int64_t n, const double* lr_dev,
                  double grad_scale);
+/* The same update over n_ranges element ranges of w / g in one launch:
+ * ranges_dev = device [offset0, count0, offset1, count1, ...] (int64,
+ * offsets 16-byte aligned); max_count sizes the grid.                      */
+int nncb_sgd_dev_ranges(nncb_ctx* ctx, int stream, float* w, const float* g, const int64_t* ranges_dev,
+                        int n_ranges, int64_t max_count, const double* lr_dev, double grad_scale);
 
 /* ------------------------------------------------------------------ */
 /*  Data-parallel collectives (NCCL over NVLink/NVSwitch)               */

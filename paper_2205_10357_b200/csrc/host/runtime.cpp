@@ -2036,6 +2036,8 @@ struct Trainer::Impl {
     // per bucket the element ranges the bucket update still covers
     std::set<std::string> fused_sgd;
     std::vector<std::vector<std::pair<int64_t, int64_t>>> bucket_rest;
+    void* rest_ranges = nullptr;                 // device [offset, count] pairs of every bucket's rest
+    std::vector<int64_t> rest_first, rest_max;   // per bucket: first pair index, largest count
     bool fused_planned = false;
     uint64_t launches_per_step = 0;
     bool warmed = false;
@@ -2074,7 +2076,7 @@ struct Trainer::Impl {
         }
         if (loss_ev) nncb_event_destroy(loss_ev);
         if (loss_host) nncb_host_free(loss_host);
-        for (void* p : {params, grads, target, loss, static_cast<void*>(lr_dev)})
+        for (void* p : {params, grads, target, loss, static_cast<void*>(lr_dev), rest_ranges})
             if (p) nncb_free(ctx, p);
     }
 
@@ -2138,6 +2140,26 @@ struct Trainer::Impl {
             }
             if (cur < end) bucket_rest[bi].push_back({cur, end - cur});
         }
+        // one multi-range update launch per bucket: the ranges live on the device
+        std::vector<int64_t> flat;
+        rest_first.assign(layout.buckets.size(), 0);
+        rest_max.assign(layout.buckets.size(), 0);
+        for (size_t bi = 0; bi < bucket_rest.size(); ++bi) {
+            rest_first[bi] = static_cast<int64_t>(flat.size() / 2);
+            for (const auto& [o, n] : bucket_rest[bi]) {
+                flat.push_back(o);
+                flat.push_back(n);
+                rest_max[bi] = std::max(rest_max[bi], n);
+            }
+        }
+        nncb_ctx* ctx = dev->ctx();
+        if (rest_ranges) nncb_free(ctx, rest_ranges);
+        rest_ranges = nullptr;
+        if (!flat.empty()) {
+            NNC_CHECK(nncb_malloc(ctx, flat.size() * sizeof(int64_t), &rest_ranges));
+            NNC_CHECK(nncb_h2d(ctx, rest_ranges, flat.data(), flat.size() * sizeof(int64_t)));
+            NNC_CHECK(nncb_sync(ctx));
+        }
     }
 
     void enqueue_step(bool do_sgd) {
@@ -2146,8 +2168,7 @@ struct Trainer::Impl {
         enqueue_loss();
         const bool comm = nncb_comm_active(ctx) != 0;
         const double scale = 1.0 / static_cast<double>(dev->nranks());
-        const bool fused = do_sgd && !comm;
-        if (fused && !fused_planned) plan_fused_sgd();
+        const bool fused = do_sgd && !comm && fused_planned;
         std::map<int64_t, std::vector<StepAction>> after;
         for (const StepAction& a : step_schedule(layout, comm, do_sgd)) after[a.after].push_back(a);
         auto issue = [&](const StepAction& a) {
@@ -2161,10 +2182,13 @@ struct Trainer::Impl {
                 }
                 case StepAction::Update: {
                     const DpBucket& bk = layout.buckets[a.bucket];
-                    if (fused) {   // the weights not updated by their weight-gradient call
-                        for (const auto& [o, n] : bucket_rest[static_cast<size_t>(a.bucket)])
-                            NNC_CHECK(nncb_sgd_dev(ctx, NNCB_STREAM_COMM, static_cast<float*>(params) + o,
-                                                   static_cast<float*>(grads) + o, n, lr_dev, scale));
+                    if (fused) {   // the weights not updated by their weight-gradient call, one launch
+                        const size_t bi = static_cast<size_t>(a.bucket);
+                        if (!bucket_rest[bi].empty())
+                            NNC_CHECK(nncb_sgd_dev_ranges(
+                                ctx, NNCB_STREAM_COMM, static_cast<float*>(params), static_cast<float*>(grads),
+                                static_cast<const int64_t*>(rest_ranges) + 2 * rest_first[bi],
+                                static_cast<int>(bucket_rest[bi].size()), rest_max[bi], lr_dev, scale));
                         break;
                     }
                     NNC_CHECK(nncb_sgd_dev(ctx, NNCB_STREAM_COMM, static_cast<float*>(params) + bk.offset,
@@ -2363,6 +2387,7 @@ Trainer::Trainer(const plan::VersionPlans& plans, HostModel& model, Device& dev,
                      if (it == weight_of_grad.end()) return nullptr;
                      return static_cast<float*>(I.grads) + I.w_off.at(it->second);
                  });
+    I.plan_fused_sgd();   // before any capture (it uploads the bucket ranges); used only at G = 1
 }
 
 Trainer::~Trainer() = default;

@@ -1457,11 +1457,45 @@ int nncb_softmax_ce(nncb_ctx* ctx, const float* logits, const float* target, flo
     return 0;
 }
 
+// SGD over several element ranges of the flat regions in one launch:
+// blockIdx.y picks the range (ranges[2r] offset, ranges[2r+1] count, both in
+// elements, offsets 16-byte aligned), blockIdx.x strides within it.
+__global__ void sgd_ranges_k(float* __restrict__ w, const float* __restrict__ g, const int64_t* __restrict__ ranges,
+                             const double* __restrict__ lr_dev, double scale) {
+    const double lr = *lr_dev;
+    const int64_t off = ranges[2 * blockIdx.y], n = ranges[2 * blockIdx.y + 1];
+    float* wr = w + off;
+    const float* gr = g + off;
+    const int64_t nv = n >> 2, stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += stride) {
+        float4 wv = reinterpret_cast<float4*>(wr)[v];
+        const float4 gv = __ldg(reinterpret_cast<const float4*>(gr) + v);
+        wv.x = sgd1(wv.x, gv.x, lr, scale);
+        wv.y = sgd1(wv.y, gv.y, lr, scale);
+        wv.z = sgd1(wv.z, gv.z, lr, scale);
+        wv.w = sgd1(wv.w, gv.w, lr, scale);
+        reinterpret_cast<float4*>(wr)[v] = wv;
+    }
+    for (int64_t i = (nv << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+        wr[i] = sgd1(wr[i], gr[i], lr, scale);
+}
+
 int nncb_sgd(nncb_ctx* ctx, float* w, const float* g, int64_t n, double lr, double grad_scale) {
     if (n <= 0) return 0;
     if ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(g)) & 15)
         return nncb::fail("nncb_sgd: buffers must be 16-byte aligned");
     sgd_k<<<nncb::grid_for(ctx, (n + 3) / 4, 256), 256, 0, ctx->stream>>>(w, g, n, lr, grad_scale);
+    NNCB_LAUNCHED(ctx);
+    return 0;
+}
+
+int nncb_sgd_dev_ranges(nncb_ctx* ctx, int stream, float* w, const float* g, const int64_t* ranges_dev,
+                        int n_ranges, int64_t max_count, const double* lr_dev, double grad_scale) {
+    if (n_ranges <= 0) return 0;
+    if (n_ranges > 65535) return nncb::fail("nncb_sgd_dev_ranges: too many ranges");
+    const unsigned gx = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(64, (max_count / 4 + 255) / 256)));
+    sgd_ranges_k<<<dim3(gx, static_cast<unsigned>(n_ranges)), 256, 0, nncb::stream_of(ctx, stream)>>>(
+        w, g, ranges_dev, lr_dev, grad_scale);
     NNCB_LAUNCHED(ctx);
     return 0;
 }
