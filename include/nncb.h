@@ -263,6 +263,12 @@ typedef struct {
     float* sgd_w;
     const double* sgd_lr;
     double sgd_scale;
+    /* With NNCB_EPI_COLSTATS and colstats_finalize set: the call also writes
+     * the BatchNorm statistics of its output, colstats_finalize[0:N] = mean,
+     * [N:2N] = 1/sqrt(biased var + colstats_eps), exactly as nncb_bn_finalize
+     * computes them from the column sums (the finalize launch folded in).   */
+    float* colstats_finalize;
+    double colstats_eps;
 } nncb_gemm_desc;
 
 /* One launch transposing many row-major [rows][cols] matrices into [cols][rows]

@@ -1048,6 +1048,20 @@ struct Program {
                     doubles += 2 * bn.d1;
                     fused.push_back(&g);
                     fused.push_back(&bn);
+                    // the finalize itself folds into the GEMM (its last CTA) when the
+                    // statistics' bytes are untouched between the two launches
+                    {
+                        const Range st{static_cast<const char*>(bn.ptrs[1]), 2 * bn.d1 * 4};
+                        bool clash = std::getenv("NNC_NO_FUSED_BN_FINALIZE") != nullptr;
+                        for (size_t k = static_cast<size_t>(once) + 1; k < j && !clash; ++k)
+                            clash = launch_touches(pi, k, st.p, st.n, true) || launch_touches(pi, k, st.p, st.n, false);
+                        if (!clash) {
+                            g.gemm.colstats_finalize = static_cast<float*>(bn.ptrs[1]);
+                            g.gemm.colstats_eps = bn.eps;
+                            g.extra.push_back({bn.ptrs[1], 2 * bn.d1 * 4, true});
+                            bn.skip = true;
+                        }
+                    }
                     break;
                 }
             }

@@ -563,11 +563,12 @@ __global__ void bn_finalize_k(const double* __restrict__ cs, float* __restrict__
     nncb::pdl_wait();   // launched as a programmatic dependent of the producing GEMM / reduction
     int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= C) return;
-    double mean = cs[c] / (double)rows;
-    double var = cs[C + c] / (double)rows - mean * mean;
+    // (the same expression, uncontracted, as the GEMM's folded finalize: gemm_tc.cu bn_stats_from_sums)
+    const double mean = __ddiv_rn(cs[c], (double)rows);
+    double var = __dsub_rn(__ddiv_rn(cs[C + c], (double)rows), __dmul_rn(mean, mean));
     if (var < 0) var = 0;
     stats[c] = (float)mean;
-    stats[C + c] = (float)(1.0 / sqrt(var + eps));
+    stats[C + c] = (float)__ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(var, eps)));
 }
 
 // colstats from a materialized output (used when the GEMM ran on the exact

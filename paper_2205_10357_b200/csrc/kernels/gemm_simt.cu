@@ -306,7 +306,9 @@ int nncb_gemm_core(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const
     if (colstats) {
         const bool dense = d->kind == NNCB_DENSE_FWD;
         const int64_t rows = dense ? d->batch : d->n * d->oh * d->ow, C = dense ? d->out_f : d->co;
-        return nncb::colstats_from_output(ctx, out, d->colstats, rows, C);
+        if (int rc = nncb::colstats_from_output(ctx, out, d->colstats, rows, C)) return rc;
+        if (d->colstats_finalize) return nncb_bn_finalize(ctx, d->colstats, d->colstats_finalize, rows, C, d->colstats_eps);
+        return 0;
     }
     return 0;
 }

@@ -113,6 +113,9 @@ struct TcParams {
     // (2^-40) sums split in 32-bit limbs, [sum hi | sum lo | sq hi | sq lo][N],
     // then a CTA ticket counter; the last CTA converts to the doubles above
     unsigned long long* cs_fixed;
+    float* cs_stats;    // NNCB_EPI_COLSTATS + colstats_finalize: the last CTA also writes mean / invstd
+    double cs_eps;
+    int64_t cs_rows;
     // --- manual A (channel counts that do not fill a 32-wide TMA block) -----
     // Builder warps gather A straight from the NHWC activation into the
     // K-major 128B-swizzled stage layout: no im2col matrix in HBM.
@@ -1378,8 +1381,17 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                 const int64_t N = P.N;
                 for (int64_t c = threadIdx.x - 64; c < N; c += 256) {
                     const unsigned long long* f = P.cs_fixed;
-                    P.colstats[c] = fixed_value(__ldcg(f + c), __ldcg(f + N + c));
-                    P.colstats[N + c] = fixed_value(__ldcg(f + 2 * N + c), __ldcg(f + 3 * N + c));
+                    const double s0 = fixed_value(__ldcg(f + c), __ldcg(f + N + c));
+                    const double s1 = fixed_value(__ldcg(f + 2 * N + c), __ldcg(f + 3 * N + c));
+                    P.colstats[c] = s0;
+                    P.colstats[N + c] = s1;
+                    if (P.cs_stats) {   // the BatchNorm finalize, as fused_ops.cu bn_finalize_k
+                        const double mean = __ddiv_rn(s0, (double)P.cs_rows);
+                        double var = __dsub_rn(__ddiv_rn(s1, (double)P.cs_rows), __dmul_rn(mean, mean));
+                        if (var < 0) var = 0;
+                        P.cs_stats[c] = (float)mean;
+                        P.cs_stats[N + c] = (float)__ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(var, P.cs_eps)));
+                    }
                 }
             }
         }
@@ -2540,6 +2552,8 @@ int gemm_tc_route(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const 
         dd.in_f = K;
         dd.out_f = d->co;
         dd.colstats = d->colstats;
+        dd.colstats_finalize = d->colstats_finalize;
+        dd.colstats_eps = d->colstats_eps;
         dd.bn_mean = d->bn_mean;
         dd.bn_var = d->bn_var;
         dd.bn_gamma = d->bn_gamma;
@@ -2794,6 +2808,11 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
             P.eg_x = d->eg_x;
             P.eg_stats = d->eg_stats;
             P.colstats = d->eg_sums;   // the CS build accumulates the dy sums
+        }
+        if (P.colstats && !P.eg && d->colstats_finalize) {
+            P.cs_stats = d->colstats_finalize;
+            P.cs_eps = d->colstats_eps;
+            P.cs_rows = d->kind == NNCB_DENSE_FWD ? d->batch : d->n * d->oh * d->ow;
         }
         if (P.colstats) {   // fixed-point accumulators + CTA ticket; the kernel's last CTA writes colstats
             const size_t fb = sizeof(unsigned long long) * (4 * static_cast<size_t>(Nc) + 1);

@@ -19,7 +19,8 @@ class GemmDesc(ctypes.Structure):
                 ("b_kmajor", ctypes.c_void_p), ("bn_mean", ctypes.c_void_p), ("bn_var", ctypes.c_void_p),
                 ("bn_gamma", ctypes.c_void_p), ("bn_beta", ctypes.c_void_p), ("bn_eps", ctypes.c_double),
                 ("residual", ctypes.c_void_p), ("sgd_w", ctypes.c_void_p), ("sgd_lr", ctypes.c_void_p),
-                ("sgd_scale", ctypes.c_double)]
+                ("sgd_scale", ctypes.c_double), ("colstats_finalize", ctypes.c_void_p),
+                ("colstats_eps", ctypes.c_double)]
 
 
 class TransposeJob(ctypes.Structure):
