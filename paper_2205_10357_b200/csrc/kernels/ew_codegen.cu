@@ -20,6 +20,7 @@
 #include <numeric>
 #include <set>
 #include <sstream>
+#include <map>
 
 #include "driver_api.cuh"
 #include "nncb_internal.cuh"
@@ -35,6 +36,7 @@ struct nncb_ew_kernel {
     int reduce_stats[2] = {0, 0};          // 1: REDUCE_STATS (mean / invstd into one [2C] slot)
     double reduce_eps[2] = {0.0, 0.0};
     int red_blocks = 4;                    // resident blocks per SM the reduction build is budgeted for
+    int ring_bytes = 0;                    // dynamic shared memory of the cp.async load ring (0: none)
 };
 
 void nncb::ew_release(nncb_ew_kernel* k) {
@@ -94,9 +96,53 @@ __device__ __forceinline__ float bn_grad_fast_(float x, float g, float m, float 
 
 std::string reg(int r) { return "r" + std::to_string(r); }
 
+bool writes_reg(int op) {
+    return op != NNCB_EW_STORE && op != NNCB_EW_REDUCE_STATS && op != NNCB_EW_REDUCE_SUM &&
+           op != NNCB_EW_REDUCE_BN_GRAD;
+}
+
+// Channel-stationary programs: a per-channel variance read only as the `v`
+// operand of inference BatchNorms (one eps) is turned into invstd once, in the
+// prologue, with the very expression bn_infer_ evaluates per element, and
+// those BatchNorms become bn_apply_ (bitwise the same result, one double
+// sqrt + divide per thread instead of per element). Conservative: any other
+// use or redefinition of the register keeps the per-element form.
+// Returns: instruction index -> pre-inverted; fills reg -> eps.
+std::vector<char> hoisted_invstd(const nncb_ew_program& p, std::map<int, double>& regs) {
+    std::vector<char> flag(p.n_instr, 0);
+    for (int k = 0; k < p.n_instr; ++k) {
+        if (p.instr[k].op != NNCB_EW_LOAD_CH) continue;
+        const int r = p.instr[k].dst;
+        bool ok = true, seen = false;
+        double eps = 0;
+        std::vector<int> users;
+        for (int q = 0; q < p.n_instr && ok; ++q) {
+            if (q == k) continue;
+            const nncb_ew_instr& in = p.instr[q];
+            if (writes_reg(in.op) && in.dst == r) { ok = false; break; }
+            const bool as_var = in.op == NNCB_EW_BN_INFER && in.c == r && in.a != r && in.b != r && in.d != r &&
+                                in.e != r;
+            if (as_var) {
+                if (seen && in.imm != eps) ok = false;
+                eps = in.imm, seen = true;
+                users.push_back(q);
+            } else if (in.a == r || in.b == r || in.c == r || in.d == r || in.e == r || in.f == r || in.h == r) {
+                ok = false;
+            }
+        }
+        if (!ok || !seen) continue;
+        regs[r] = eps;
+        for (int q : users) flag[q] = 1;
+    }
+    return flag;
+}
+
 // Emits the body for W lanes (W = 4: float4 path, W = 1: scalar tail).
-void emit_body(std::ostringstream& os, const nncb_ew_program& p, int W, bool uses_ch, bool stationary = false) {
-    int reduce_index = 0;
+void emit_body(std::ostringstream& os, const nncb_ew_program& p, int W, bool uses_ch, bool stationary = false,
+               bool ring = false) {
+    int reduce_index = 0, load_index = 0;
+    std::map<int, double> inv_regs;
+    const std::vector<char> pre_inverted = stationary ? hoisted_invstd(p, inv_regs) : std::vector<char>(p.n_instr, 0);
     os << "  float ";
     for (int r = 0; r < p.n_regs; ++r) os << (r ? ", " : "") << reg(r) << "[" << W << "]";
     os << ";\n";
@@ -112,7 +158,10 @@ void emit_body(std::ostringstream& os, const nncb_ew_program& p, int W, bool use
         std::string ptr = "A.p[" + std::to_string(in.slot) + "]";
         switch (in.op) {
             case NNCB_EW_LOAD:
-                if (W == 4)
+                if (ring) {   // staged by the cp.async ring (rs: this thread's slot of the stage)
+                    os << "  { const float4 t = rs[" << 256 * load_index++ << "]; " << d << "[0]=t.x; " << d
+                       << "[1]=t.y; " << d << "[2]=t.z; " << d << "[3]=t.w; }\n";
+                } else if (W == 4)
                     os << "  { float4 t = __ldg(reinterpret_cast<const float4*>(" << ptr << " + i)); " << d
                        << "[0]=t.x; " << d << "[1]=t.y; " << d << "[2]=t.z; " << d << "[3]=t.w; }\n";
                 else
@@ -180,6 +229,10 @@ void emit_body(std::ostringstream& os, const nncb_ew_program& p, int W, bool use
                 expr = "bn_apply_(" + a + "[j], " + b + "[j], " + c + "[j], " + dd + "[j], " + e + "[j])";
                 break;
             case NNCB_EW_BN_INFER: {
+                if (pre_inverted[k]) {   // c holds invstd (prologue, see hoisted_invstd)
+                    expr = "bn_apply_(" + a + "[j], " + b + "[j], " + c + "[j], " + dd + "[j], " + e + "[j])";
+                    break;
+                }
                 char eps[64];
                 snprintf(eps, sizeof(eps), "%.17e", in.imm);
                 expr = "bn_infer_(" + a + "[j], " + b + "[j], " + c + "[j], " + dd + "[j], " + e + "[j], " +
@@ -216,6 +269,32 @@ int red2_blocks() {
     return b;
 }
 
+// The channel-stationary loop stages the element-wise LOAD streams through a
+// per-thread ring of cp.async (LDGSTS) copies in shared memory: the loads in
+// flight no longer cost registers, so the register-heavy programs (many
+// per-channel operands on the 2-block budget) keep several element vectors in
+// flight per thread. Stages: as many as fit 48 KB per block (32 KB beside a
+// reduction's 16 KB static buffer), 3..8; 0 = no ring (more than 4 streams, or
+// NNCB_EW_RING=0). Each thread reads back only its own slots, so no block
+// barrier is needed.
+int ring_stages(const nncb_ew_program& p) {
+    static const int env = getenv("NNCB_EW_RING") ? atoi(getenv("NNCB_EW_RING")) : -1;
+    if (env == 0) return 0;
+    int nl = 0;
+    for (int k = 0; k < p.n_instr; ++k) nl += p.instr[k].op == NNCB_EW_LOAD;
+    if (nl == 0) return 0;
+    const int budget = (find_reduces(p).empty() ? 48 : 32) / 4;   // stage-streams of 4 KB
+    int S = std::min(8, budget / nl);
+    if (env > 0) S = std::min(S, env);
+    return S >= 3 ? S : 0;
+}
+
+int load_streams(const nncb_ew_program& p) {
+    int nl = 0;
+    for (int k = 0; k < p.n_instr; ++k) nl += p.instr[k].op == NNCB_EW_LOAD;
+    return nl;
+}
+
 std::string generate(const nncb_ew_program& p, bool uses_ch) {
     std::ostringstream os;
     const int nred = static_cast<int>(find_reduces(p).size());
@@ -234,10 +313,11 @@ std::string generate(const nncb_ew_program& p, bool uses_ch) {
         // multiple of C, so a thread's 4 channels never change; per-channel
         // operands are loaded once (float4) into registers before the loop.
         os << "__device__ __forceinline__ void body4s(const EwArgs& A, i64 i";
+        if (ring_stages(p)) os << ", const float4* rs";
         for (int k : chregs) os << ", const float (&pc" << p.instr[k].dst << ")[4]";
         for (int q = 0; q < nred; ++q) os << ", double (&red" << q << "_0)[4], double (&red" << q << "_1)[4]";
         os << ") {\n";
-        emit_body(os, p, 4, uses_ch, true);
+        emit_body(os, p, 4, uses_ch, true, ring_stages(p) > 0);
         os << "}\n";
     }
     // reduction groups carry 16 registers of double accumulators: cap at 64
@@ -282,15 +362,57 @@ std::string generate(const nncb_ew_program& p, bool uses_ch) {
                << "] + c0)); pc" << in.dst << "[0]=t.x; pc" << in.dst << "[1]=t.y; pc" << in.dst << "[2]=t.z; pc"
                << in.dst << "[3]=t.w; }\n";
         }
+        std::map<int, double> inv_regs;
+        hoisted_invstd(p, inv_regs);
+        for (const auto& [r, e] : inv_regs) {
+            char eps[64];
+            snprintf(eps, sizeof(eps), "%.17e", e);
+            os << "    #pragma unroll\n    for (int j = 0; j < 4; ++j) pc" << r << "[j] = (float)(1.0 / sqrt((double)pc" << r
+               << "[j] + " << eps << "));\n";
+        }
         std::string args;
         for (int k : chregs) args += ", pc" + std::to_string(p.instr[k].dst);
         for (int q = 0; q < nred; ++q) {
             args += ", red" + std::to_string(q) + "_0, red" + std::to_string(q) + "_1";
             os << "    double red" << q << "_0[4] = {0, 0, 0, 0}, red" << q << "_1[4] = {0, 0, 0, 0};\n";
         }
+        // A statistics pass on the 2-block budget (a recomputed BatchNorm
+        // chain) runs at 16 warps per SM: four element vectors per iteration
+        // put twice the loads in flight at the same occupancy, same
+        // accumulation order (C2 mode B 5.57 -> 6.05 TB/s; the same unroll on
+        // the apply passes measured neutral on C4 and 25% slower on C2 mode A).
+        // NNCB_EW_UNROLL=2|4 overrides.
+        static const int env_unroll = getenv("NNCB_EW_UNROLL") ? atoi(getenv("NNCB_EW_UNROLL")) : 0;
+        const int unroll = env_unroll == 2 || env_unroll == 4 ? env_unroll
+                         : red && stats_red && chregs.size() > 4 ? 4 : 2;
+        if (const int S = ring_stages(p)) {
+            const int NL = load_streams(p);
+            std::vector<int> lslots;
+            for (int k = 0; k < p.n_instr; ++k)
+                if (p.instr[k].op == NNCB_EW_LOAD) lslots.push_back(p.instr[k].slot);
+            os << "    extern __shared__ float4 ring[];   // [" << S << " stages][" << NL << " streams][256 threads]\n"
+               << "    const unsigned rbase = (unsigned)__cvta_generic_to_shared(ring + threadIdx.x);\n"
+               << "    auto issue = [&](i64 w, int st) {\n      if (w < nvec) {\n";
+            for (int q = 0; q < NL; ++q)
+                os << "        asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\" :: \"r\"(rbase + (unsigned)((st * "
+                   << NL << " + " << q << ") * 4096)), \"l\"(A.p[" << lslots[q] << "] + (w << 2)) : \"memory\");\n";
+            os << "      }\n      asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n    };\n";
+            os << "    #pragma unroll\n    for (int st = 0; st < " << S << "; ++st) issue(v + st * stride, st);\n";
+            os << "    for (int st = 0; v < nvec; v += stride) {\n"
+               << "      asm volatile(\"cp.async.wait_group " << S - 1 << ";\" ::: \"memory\");\n"
+               << "      body4s(A, v << 2, ring + st * " << NL * 256 << " + threadIdx.x" << args << ");\n"
+               << "      issue(v + " << S << " * stride, st);\n"
+               << "      st = st + 1 == " << S << " ? 0 : st + 1;\n    }\n"
+               << "    asm volatile(\"cp.async.wait_all;\" ::: \"memory\");\n";
+        } else {
+        if (unroll == 4)
+            os << "    for (; v + 3 * stride < nvec; v += 4 * stride) { body4s(A, v << 2" << args
+               << "); body4s(A, (v + stride) << 2" << args << "); body4s(A, (v + 2 * stride) << 2" << args
+               << "); body4s(A, (v + 3 * stride) << 2" << args << "); }\n";
         os << "    for (; v + stride < nvec; v += 2 * stride) { body4s(A, v << 2" << args << "); body4s(A, (v + stride) << 2"
            << args << "); }\n";
         os << "    if (v < nvec) body4s(A, v << 2" << args << ");\n";
+        }
         if (red) {
             // Per-block partials, deterministic: for C <= 1024 (a power of two)
             // threads t and t + C/4 share channels and thread q < C/4 folds its
@@ -326,6 +448,13 @@ std::string generate(const nncb_ew_program& p, bool uses_ch) {
   for (i64 i = (nvec << 2) + (i64)blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += stride) body1(A, i);
 }
 )";
+    // NNCB_EW_DUMP=dir: write every generated program to dir/ew_<hash>.cu
+    if (const char* dir = getenv("NNCB_EW_DUMP")) {
+        const std::string src = os.str();
+        char path[512];
+        snprintf(path, sizeof(path), "%s/ew_%016zx.cu", dir, std::hash<std::string>{}(src));
+        if (FILE* f = fopen(path, "w")) fputs(src.c_str(), f), fclose(f);
+    }
     return os.str();
 }
 
@@ -456,6 +585,7 @@ int nncb_ew_compile(nncb_ctx* ctx, const nncb_ew_program* p, nncb_ew_kernel** ou
         bool stats_red = false;
         for (int q = 0; q < p->n_instr; ++q) stats_red = stats_red || p->instr[q].op == NNCB_EW_REDUCE_STATS;
         k->red_blocks = (find_reduces(*p).size() > 1 || (stats_red && nch > 4)) ? red2_blocks() : 4;
+        if (uses_ch) k->ring_bytes = ring_stages(*p) * load_streams(*p) * 4096;
     }
     const std::vector<int> reds = find_reduces(*p);
     if (reds.size() > 2) {
@@ -536,7 +666,7 @@ int nncb_ew_launch(nncb_ctx* ctx, nncb_ew_kernel* k, void* const* slots, int64_t
         if (!args.part) return nncb::fail("nncb_ew_launch: reduction scratch allocation failed");
     }
     void* params[] = {&args};
-    CUresult r = nncb::drv::table().launchKernel(k->fn, grid, 1, 1, 256, 1, 1, 0,
+    CUresult r = nncb::drv::table().launchKernel(k->fn, grid, 1, 1, 256, 1, 1, args.cs ? k->ring_bytes : 0,
                                                  reinterpret_cast<CUstream>(ctx->stream), params, nullptr);
     if (r != CUDA_SUCCESS)
         return nncb::fail(std::string("cuLaunchKernel(fused ew): ") + nncb::drv::error_string(r));
