@@ -858,11 +858,13 @@ struct Program {
                     n_reduce += prog[k].op == NNCB_EW_REDUCE_BN_GRAD;
                     if (prog[k].op == NNCB_EW_STORE && e.ptrs[prog[k].slot] == r.ptrs[2]) at = static_cast<int>(k);
                 }
-                // one reduction per group: a second one (residual joins) needs a
-                // 2-block register budget and measured slower than the standalone pass
-                // NNC_BN_GRAD_REDUCE_MAX=2 folds the second reduction of a residual
-                // join too: measured neutral on C4 at 2 or 3 resident blocks
-                static const int max_reduce = std::getenv("NNC_BN_GRAD_REDUCE_MAX") ? std::atoi(std::getenv("NNC_BN_GRAD_REDUCE_MAX")) : 1;
+                // at most two reductions per group: the second one (the residual
+                // join of a projection block, both BatchNorms fed the same
+                // gradient) puts the group on the 2-block register budget; with
+                // its loads staged through the cp.async ring it beats the
+                // standalone pass (C4 +1%; it measured neutral before the ring).
+                // NNC_BN_GRAD_REDUCE_MAX=1 keeps one.
+                static const int max_reduce = std::getenv("NNC_BN_GRAD_REDUCE_MAX") ? std::atoi(std::getenv("NNC_BN_GRAD_REDUCE_MAX")) : 2;
                 if (n_reduce >= max_reduce || at < 0 || e.ptrs.size() + 5 > 48) continue;
                 const int s0 = static_cast<int>(e.ptrs.size());
                 std::vector<void*> ptrs = e.ptrs;

@@ -16,6 +16,7 @@ struct Table {
     PFN_cuModuleGetFunction_v2000 moduleGetFunction = nullptr;
     PFN_cuLaunchKernel_v4000 launchKernel = nullptr;
     PFN_cuTensorMapEncodeTiled_v12000 tensorMapEncodeTiled = nullptr;
+    PFN_cuFuncSetAttribute_v9000 funcSetAttribute = nullptr;
     bool ok = false;
 };
 
@@ -32,7 +33,8 @@ inline const Table& table() {
                get("cuModuleUnload", reinterpret_cast<void**>(&r.moduleUnload)) &&
                get("cuModuleGetFunction", reinterpret_cast<void**>(&r.moduleGetFunction)) &&
                get("cuLaunchKernel", reinterpret_cast<void**>(&r.launchKernel)) &&
-               get("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&r.tensorMapEncodeTiled));
+               get("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&r.tensorMapEncodeTiled)) &&
+               get("cuFuncSetAttribute", reinterpret_cast<void**>(&r.funcSetAttribute));
         return r;
     }();
     return t;

@@ -277,13 +277,48 @@ int red2_blocks() {
 // reduction's 16 KB static buffer), 3..8; 0 = no ring (more than 4 streams, or
 // NNCB_EW_RING=0). Each thread reads back only its own slots, so no block
 // barrier is needed.
+// Resident blocks per SM a program's register budget is built for (0: the
+// compiler's default).
+// * reductions carry 16 registers of double accumulators: 64 registers (four
+//   blocks, one wave, see nncb_ew_launch); two reductions, or a statistics
+//   pass with more than 4 per-channel operands (a recomputed BatchNorm chain),
+//   get the 2-block budget (at 64 registers the depth-3 pass spilled and ran at
+//   1.7 TB/s; 4.8 TB/s at 128)
+// * programs with many per-channel operands (BatchNorm apply / gradient) hold
+//   them in registers on the channel-stationary path; 64 registers (4 blocks)
+//   keep enough loads in flight (measured: 5.1 -> 6.1 TB/s for the BN input
+//   gradient); more than 8 per-channel float4 operands do not fit 64
+//   registers: those (a chain of inference BatchNorms) get a 2-block budget.
+//   NNCB_EW_MINBLOCKS overrides.
+int resident_blocks(const nncb_ew_program& p) {
+    int nch = 0;
+    bool stats_red = false;
+    for (int k = 0; k < p.n_instr; ++k) {
+        nch += p.instr[k].op == NNCB_EW_LOAD_CH;
+        stats_red = stats_red || p.instr[k].op == NNCB_EW_REDUCE_STATS;
+    }
+    const size_t nred = find_reduces(p).size();
+    if (nred > 0) return nred > 1 || (stats_red && nch > 4) ? red2_blocks() : 4;
+    static const int env_min_blocks = getenv("NNCB_EW_MINBLOCKS") ? atoi(getenv("NNCB_EW_MINBLOCKS")) : -1;
+    if (env_min_blocks >= 0) return env_min_blocks;
+    return nch > 8 ? 2 : nch >= 3 ? 4 : 0;
+}
+
 int ring_stages(const nncb_ew_program& p) {
     static const int env = getenv("NNCB_EW_RING") ? atoi(getenv("NNCB_EW_RING")) : -1;
     if (env == 0) return 0;
     int nl = 0;
     for (int k = 0; k < p.n_instr; ++k) nl += p.instr[k].op == NNCB_EW_LOAD;
     if (nl == 0) return 0;
-    const int budget = (find_reduces(p).empty() ? 48 : 32) / 4;   // stage-streams of 4 KB
+    // shared memory per block: 48 KB; 100 KB (opt-in size) for a group with
+    // two reductions on the 2-block budget (the residual join's backward: +1%
+    // on C4, where the C2 statistics passes measured 3% slower with it); a
+    // reduction's static partial buffer takes 16 KB of it. NNCB_EW_RING_KB2
+    // overrides the size for every 2-block program.
+    static const int kb2 = getenv("NNCB_EW_RING_KB2") ? atoi(getenv("NNCB_EW_RING_KB2")) : 0;
+    const bool wide = resident_blocks(p) == 2 && (kb2 > 0 || find_reduces(p).size() > 1);
+    const int kb = (wide ? (kb2 > 0 ? kb2 : 100) : 48) - (find_reduces(p).empty() ? 0 : 16);
+    const int budget = kb / 4;   // stage-streams of 4 KB
     int S = std::min(8, budget / nl);
     if (env > 0) S = std::min(S, env);
     return S >= 3 ? S : 0;
@@ -320,31 +355,12 @@ std::string generate(const nncb_ew_program& p, bool uses_ch) {
         emit_body(os, p, 4, uses_ch, true, ring_stages(p) > 0);
         os << "}\n";
     }
-    // reduction groups carry 16 registers of double accumulators: cap at 64
-    // registers so four blocks stay resident (one wave, see nncb_ew_launch)
-    // Programs with many per-channel operands (BatchNorm apply / gradient) hold
-    // them in registers on the channel-stationary path; capping at 64 registers
-    // (4 resident blocks) keeps enough loads in flight to stream at HBM rate
-    // (measured: 5.1 -> 6.1 TB/s for the BN input gradient). Light programs keep
-    // the default. NNCB_EW_MINBLOCKS overrides.
-    static const int env_min_blocks = getenv("NNCB_EW_MINBLOCKS") ? atoi(getenv("NNCB_EW_MINBLOCKS")) : -1;
-    // (more than 8 per-channel float4 operands would not fit 64 registers:
-    // those programs, e.g. a chain of inference BatchNorms, get a 2-block budget)
-    int min_blocks = chregs.size() > 8 ? 2 : chregs.size() >= 3 ? 4 : 0;
-    if (env_min_blocks >= 0) min_blocks = env_min_blocks;
-    // 16 double accumulator registers per reduction; a statistics pass with
-    // more than 4 per-channel operands (a recomputed BatchNorm chain) gets the
-    // 2-block budget too (at 64 registers the depth-3 pass spilled and ran at
-    // 1.7 TB/s; 4.8 TB/s at 128)
-    bool stats_red = false;
-    for (int k = 0; k < p.n_instr; ++k) stats_red = stats_red || p.instr[k].op == NNCB_EW_REDUCE_STATS;
-    if (red)
-        os << "extern \"C\" __global__ void __launch_bounds__(256, " << (nred > 1 || (stats_red && chregs.size() > 4) ? red2_blocks() : 4)
-           << ") nnc_fused_ew(const EwArgs A) {";
-    else if (min_blocks > 0)
-        os << "extern \"C\" __global__ void __launch_bounds__(256, " << min_blocks << ") nnc_fused_ew(const EwArgs A) {";
+    if (const int blocks = resident_blocks(p))
+        os << "extern \"C\" __global__ void __launch_bounds__(256, " << blocks << ") nnc_fused_ew(const EwArgs A) {";
     else
         os << "extern \"C\" __global__ void __launch_bounds__(256) nnc_fused_ew(const EwArgs A) {";
+    bool stats_red = false;
+    for (int k = 0; k < p.n_instr; ++k) stats_red = stats_red || p.instr[k].op == NNCB_EW_REDUCE_STATS;
     // reduction groups: the finalize kernel is a programmatic dependent
     // launch; let it be scheduled while this grid drains (it waits on
     // griddepcontrol.wait for this grid's completion and memory)
@@ -579,14 +595,8 @@ int nncb_ew_compile(nncb_ctx* ctx, const nncb_ew_program* p, nncb_ew_kernel** ou
     k->source = src;
     k->n_slots = p->n_slots;
     k->uses_channels = uses_ch;
-    {
-        int nch = 0;
-        for (int q = 0; q < p->n_instr; ++q) nch += p->instr[q].op == NNCB_EW_LOAD_CH;
-        bool stats_red = false;
-        for (int q = 0; q < p->n_instr; ++q) stats_red = stats_red || p->instr[q].op == NNCB_EW_REDUCE_STATS;
-        k->red_blocks = (find_reduces(*p).size() > 1 || (stats_red && nch > 4)) ? red2_blocks() : 4;
-        if (uses_ch) k->ring_bytes = ring_stages(*p) * load_streams(*p) * 4096;
-    }
+    k->red_blocks = find_reduces(*p).empty() ? 4 : resident_blocks(*p);
+    if (uses_ch) k->ring_bytes = ring_stages(*p) * load_streams(*p) * 4096;
     const std::vector<int> reds = find_reduces(*p);
     if (reds.size() > 2) {
         nncb::ew_release(k);
@@ -607,6 +617,8 @@ int nncb_ew_compile(nncb_ctx* ctx, const nncb_ew_program* p, nncb_ew_kernel** ou
     }
     CUresult cr = D.moduleLoadData(&k->module, cubin.data());
     if (cr == CUDA_SUCCESS) cr = D.moduleGetFunction(&k->fn, k->module, "nnc_fused_ew");
+    if (cr == CUDA_SUCCESS && k->ring_bytes > 0)   // (with a reduction's static 16 KB it may pass 48 KB)
+        cr = D.funcSetAttribute(k->fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, k->ring_bytes);
     if (cr != CUDA_SUCCESS) {
         nncb::ew_release(k);
         return nncb::fail(std::string("cuModuleLoadData: ") + nncb::drv::error_string(cr));

@@ -184,7 +184,7 @@ def test_relu_grad_epilogue_fusion_matches_separate_pass(monkeypatch):
     loss_b, grads_b = b.gradients({"x": x}, t)
     b.trainer_prepare({"x": x}, t)
     n_b = len(b.profile_step(0.0))
-    assert n_b < n_a - 30, (n_a, n_b)
+    assert n_b <= n_a - 30, (n_a, n_b)
     assert abs(loss_b - loss_a) <= 1e-3 * abs(loss_a)
     for w, g in grads_a.items():
         assert rel_err(grads_b[w], g) < 2e-2, w
