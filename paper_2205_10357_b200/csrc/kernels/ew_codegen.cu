@@ -312,12 +312,13 @@ int ring_stages(const nncb_ew_program& p) {
     if (nl == 0) return 0;
     // shared memory per block: 48 KB; 100 KB (opt-in size) for a group with
     // two reductions on the 2-block budget (the residual join's backward: +1%
-    // on C4, where the C2 statistics passes measured 3% slower with it); a
-    // reduction's static partial buffer takes 16 KB of it. NNCB_EW_RING_KB2
-    // overrides the size for every 2-block program.
+    // on C4, where the C2 statistics passes measured 3% slower with it). A
+    // reduction's 16 KB of per-thread partials reuse the ring after the loop.
+    // NNCB_EW_RING_KB2 overrides the size for every 2-block program.
     static const int kb2 = getenv("NNCB_EW_RING_KB2") ? atoi(getenv("NNCB_EW_RING_KB2")) : 0;
     const bool wide = resident_blocks(p) == 2 && (kb2 > 0 || find_reduces(p).size() > 1);
-    const int kb = (wide ? (kb2 > 0 ? kb2 : 100) : 48) - (find_reduces(p).empty() ? 0 : 16);
+    static const int kbr = getenv("NNCB_EW_RING_KBR") ? atoi(getenv("NNCB_EW_RING_KBR")) : 48;
+    const int kb = wide ? (kb2 > 0 ? kb2 : 100) : find_reduces(p).empty() ? 48 : kbr;
     const int budget = kb / 4;   // stage-streams of 4 KB
     int S = std::min(8, budget / nl);
     if (env > 0) S = std::min(S, env);
@@ -434,7 +435,13 @@ std::string generate(const nncb_ew_program& p, bool uses_ch) {
             // threads t and t + C/4 share channels and thread q < C/4 folds its
             // group in t order; for C > 1024 each thread owns its 4 channels.
             // Reduction q writes the slice A.part + q * gridDim.x * 2C.
-            os << "    __shared__ double rs[256][8];\n    const int t = threadIdx.x;\n    const int C = (int)A.C;\n";
+            // (with a load ring, the partials reuse its shared memory once every
+            // thread has left the loop)
+            if (ring_stages(p))
+                os << "    __syncthreads();\n    double (*rs)[8] = reinterpret_cast<double (*)[8]>(ring);\n";
+            else
+                os << "    __shared__ double rs[256][8];\n";
+            os << "    const int t = threadIdx.x;\n    const int C = (int)A.C;\n";
             for (int q = 0; q < nred; ++q) {
                 const std::string r0 = "red" + std::to_string(q) + "_0", r1 = "red" + std::to_string(q) + "_1";
                 os << "    {\n    if (" << q << " > 0) __syncthreads();\n"
@@ -595,8 +602,12 @@ int nncb_ew_compile(nncb_ctx* ctx, const nncb_ew_program* p, nncb_ew_kernel** ou
     k->source = src;
     k->n_slots = p->n_slots;
     k->uses_channels = uses_ch;
-    k->red_blocks = find_reduces(*p).empty() ? 4 : resident_blocks(*p);
-    if (uses_ch) k->ring_bytes = ring_stages(*p) * load_streams(*p) * 4096;
+    const bool reds_empty = find_reduces(*p).empty();
+    k->red_blocks = reds_empty ? 4 : resident_blocks(*p);
+    if (uses_ch && ring_stages(*p)) {
+        k->ring_bytes = ring_stages(*p) * load_streams(*p) * 4096;
+        if (!reds_empty) k->ring_bytes = std::max(k->ring_bytes, 256 * 8 * 8);   // the partials' reuse
+    }
     const std::vector<int> reds = find_reduces(*p);
     if (reds.size() > 2) {
         nncb::ew_release(k);
@@ -617,7 +628,7 @@ int nncb_ew_compile(nncb_ctx* ctx, const nncb_ew_program* p, nncb_ew_kernel** ou
     }
     CUresult cr = D.moduleLoadData(&k->module, cubin.data());
     if (cr == CUDA_SUCCESS) cr = D.moduleGetFunction(&k->fn, k->module, "nnc_fused_ew");
-    if (cr == CUDA_SUCCESS && k->ring_bytes > 0)   // (with a reduction's static 16 KB it may pass 48 KB)
+    if (cr == CUDA_SUCCESS && k->ring_bytes > 48 * 1024)
         cr = D.funcSetAttribute(k->fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, k->ring_bytes);
     if (cr != CUDA_SUCCESS) {
         nncb::ew_release(k);
