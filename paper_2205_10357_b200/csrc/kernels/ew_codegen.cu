@@ -298,7 +298,11 @@ int resident_blocks(const nncb_ew_program& p) {
         stats_red = stats_red || p.instr[k].op == NNCB_EW_REDUCE_STATS;
     }
     const size_t nred = find_reduces(p).size();
-    if (nred > 0) return nred > 1 || (stats_red && nch > 4) ? red2_blocks() : 4;
+    // (with the load ring, every reduction group runs best at 2 blocks per SM
+    // with 128 registers: tools/ew_bench.py relu-grad + reduction 5-15% faster
+    // than 4 blocks at 64 registers; NNCB_EW_RED1_BLOCKS=4 restores that)
+    static const int red1 = getenv("NNCB_EW_RED1_BLOCKS") ? atoi(getenv("NNCB_EW_RED1_BLOCKS")) : 2;
+    if (nred > 0) return nred > 1 || (stats_red && nch > 4) ? red2_blocks() : red1;
     static const int env_min_blocks = getenv("NNCB_EW_MINBLOCKS") ? atoi(getenv("NNCB_EW_MINBLOCKS")) : -1;
     if (env_min_blocks >= 0) return env_min_blocks;
     return nch > 8 ? 2 : nch >= 3 ? 4 : 0;
@@ -310,13 +314,16 @@ int ring_stages(const nncb_ew_program& p) {
     int nl = 0;
     for (int k = 0; k < p.n_instr; ++k) nl += p.instr[k].op == NNCB_EW_LOAD;
     if (nl == 0) return 0;
-    // shared memory per block: 48 KB; 100 KB (opt-in size) for a group with
-    // two reductions on the 2-block budget (the residual join's backward: +1%
-    // on C4, where the C2 statistics passes measured 3% slower with it). A
-    // reduction's 16 KB of per-thread partials reuse the ring after the loop.
-    // NNCB_EW_RING_KB2 overrides the size for every 2-block program.
+    // shared memory per block: 48 KB; 100 KB (opt-in size) for the gradient
+    // reductions on the 2-block budget (+1% on C4 for the residual join's
+    // two-reduction group, 5-15% on the relu-grad + reduction microbenchmark;
+    // the C2 statistics passes measured 3% slower with it). A reduction's 16 KB
+    // of per-thread partials reuse the ring after the loop. NNCB_EW_RING_KB2
+    // overrides the size for every 2-block program.
     static const int kb2 = getenv("NNCB_EW_RING_KB2") ? atoi(getenv("NNCB_EW_RING_KB2")) : 0;
-    const bool wide = resident_blocks(p) == 2 && (kb2 > 0 || find_reduces(p).size() > 1);
+    bool stats = false;
+    for (int k = 0; k < p.n_instr; ++k) stats = stats || p.instr[k].op == NNCB_EW_REDUCE_STATS;
+    const bool wide = resident_blocks(p) == 2 && (kb2 > 0 || (!stats && !find_reduces(p).empty()));
     static const int kbr = getenv("NNCB_EW_RING_KBR") ? atoi(getenv("NNCB_EW_RING_KBR")) : 48;
     const int kb = wide ? (kb2 > 0 ? kb2 : 100) : find_reduces(p).empty() ? 48 : kbr;
     const int budget = kb / 4;   // stage-streams of 4 KB
@@ -680,7 +687,11 @@ int nncb_ew_launch(nncb_ctx* ctx, nncb_ew_kernel* k, void* const* slots, int64_t
         if (!args.cs || C < 4 || C > 8192 || (C & (C - 1)))
             return nncb::fail("nncb_ew_launch: a reduction needs the channel-stationary launch (C power of 2 <= 8192)");
         const int64_t g = C / std::gcd<int64_t>(C, 1024);
-        static const int64_t per_sm = getenv("NNCB_EW_RED_BLOCKS") ? std::max(1, atoi(getenv("NNCB_EW_RED_BLOCKS"))) : 4;
+        // two blocks per SM: with the load ring keeping the loads in flight,
+        // fewer blocks mean fewer per-block partials to write and fold
+        // (tools/ew_bench.py relu-grad + reduction: 2 blocks 1-10% faster than
+        // 4 from 12544x512 to 200704x128; C4 neutral, C2 statistics +1%)
+        static const int64_t per_sm = getenv("NNCB_EW_RED_BLOCKS") ? std::max(1, atoi(getenv("NNCB_EW_RED_BLOCKS"))) : 2;
         // one wave: the two-reduction build is budgeted for red2_blocks() per SM
         const int64_t resident = std::min<int64_t>(per_sm, k->red_blocks);
         const int64_t cap = std::max<int64_t>(g, (resident * static_cast<int64_t>(ctx->sm_count) / g) * g);
