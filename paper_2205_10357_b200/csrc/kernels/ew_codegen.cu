@@ -284,11 +284,11 @@ int red2_blocks() {
 //   pass with more than 4 per-channel operands (a recomputed BatchNorm chain),
 //   get the 2-block budget (at 64 registers the depth-3 pass spilled and ran at
 //   1.7 TB/s; 4.8 TB/s at 128)
-// * programs with many per-channel operands (BatchNorm apply / gradient) hold
-//   them in registers on the channel-stationary path; 64 registers (4 blocks)
-//   keep enough loads in flight (measured: 5.1 -> 6.1 TB/s for the BN input
-//   gradient); more than 8 per-channel float4 operands do not fit 64
-//   registers: those (a chain of inference BatchNorms) get a 2-block budget.
+// * programs with 3+ per-channel operands (BatchNorm apply / gradient) hold
+//   them in registers on the channel-stationary path: 128 registers (2
+//   blocks). Before the load ring, 64 registers (4 blocks) were needed to keep
+//   enough loads in flight (5.1 -> 6.1 TB/s for the BN input gradient); with
+//   the ring the 2-block budget measured +1% on the C4 step.
 //   NNCB_EW_MINBLOCKS overrides.
 int resident_blocks(const nncb_ew_program& p) {
     int nch = 0;
@@ -305,7 +305,7 @@ int resident_blocks(const nncb_ew_program& p) {
     if (nred > 0) return nred > 1 || (stats_red && nch > 4) ? red2_blocks() : red1;
     static const int env_min_blocks = getenv("NNCB_EW_MINBLOCKS") ? atoi(getenv("NNCB_EW_MINBLOCKS")) : -1;
     if (env_min_blocks >= 0) return env_min_blocks;
-    return nch > 8 ? 2 : nch >= 3 ? 4 : 0;
+    return nch >= 3 ? 2 : 0;
 }
 
 int ring_stages(const nncb_ew_program& p) {
