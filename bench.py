@@ -470,7 +470,8 @@ def main():
             fused_roof = roofline("ew (generated fused groups)", fam["ew"])
         # DRAM traffic per launch from the committed `ncu --set full` capture of
         # a representative launch of each family, beside its algorithmic bytes
-        for r, fk in ((roof, "gemm" if top_k == "gemm" else top_k), (fused_roof, "ew")):
+        ew_key = "ew_c2" if args.config == "c2" else "ew"   # the C2 statistics pass capture
+        for r, fk in ((roof, ew_key if top_k == "ew" else top_k), (fused_roof, ew_key)):
             summ = ncu_summary().get(fk) if r else None
             if summ:
                 r["traffic"] = summ["dram_read_bytes"] + summ["dram_write_bytes"]

@@ -24,7 +24,7 @@ def num(d, k, scale=1.0):
     return float(v.replace(",", "")) * (mult if scale == 1.0 else scale)
 
 
-g, e = raw("gemm_s2b_b_fwd"), raw("ew_relu_grad_reduce")
+g, e, e2 = raw("gemm_s2b_b_fwd"), raw("ew_relu_grad_reduce"), raw("ew_c2_stats_pass")
 summ = {
     "gemm": {"kernel": g["Kernel Name"][0].strip(),
              "launch": "conv fwd 3x3 s1, 256->256 ch, 14x14, batch 256 (ResNet-50 stage-2 block b), tools/gemm_bench.py",
@@ -44,6 +44,15 @@ summ = {
            "dram_throughput_pct": float(e["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"][0]),
            "registers": float(e["launch__registers_per_thread"][0]),
            "report": f"profiles/{rnd}/ew_relu_grad_reduce_raw.csv"},
+    "ew_c2": {"kernel": "nnc_fused_ew (C2 recomputed-statistics pass, REDUCE_STATS)",
+              "launch": "C2 chain statistics pass over x, y [256,128,128,64] (reads 2 x 1.07 GB, stores nothing), "
+                        "tools/c2_profile.py",
+              "duration_us": float(e2["gpu__time_duration.sum"][0]),
+              "dram_read_bytes": num(e2, "dram__bytes_read.sum"), "dram_write_bytes": num(e2, "dram__bytes_write.sum"),
+              "algorithmic_bytes": 2 * 256 * 128 * 128 * 64 * 4,
+              "dram_throughput_pct": float(e2["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"][0]),
+              "registers": float(e2["launch__registers_per_thread"][0]),
+              "report": f"profiles/{rnd}/ew_c2_stats_pass_raw.csv"},
     "note": ("ncu --set full --clock-control none (serialised, cold per-kernel caches): compare shares and traffic, "
              "not absolute times. Writes still resident in the 126 MB L2 at kernel end are not counted in "
              "dram_write_bytes."),
