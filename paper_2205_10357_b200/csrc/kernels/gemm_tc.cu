@@ -872,11 +872,13 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
             if (++slot == STAGES) { slot = 0; phase ^= 1u; }
         };
         if (P.bres && t_begin < P.tiles) {
-            // every (channel block, tap) B tile once, [cb][tap] order
+            // every (channel block, tap) B tile once, [cb][tap] order (taps:
+            // kernel rows x taps per row -- 3 x 3, or the stem's 4 x 2)
+            const int nres = P.ntaps[0] * P.halo_kw;
             mbar_expect_tx(bres_bar, P.bres_bytes);
             for (int cb = 0; cb < P.cblocks; ++cb)
-                for (int j = 0; j < 9; ++j) {
-                    uint8_t* sb = bres_base + (cb * 9 + j) * bt_bytes;
+                for (int j = 0; j < nres; ++j) {
+                    uint8_t* sb = bres_base + (cb * nres + j) * bt_bytes;
                     const int br = P.brow[j], c0 = cb * BK;
                     if (P.b_mn) {
                         for (int q = 0; q < bcols / 32; ++q) tma_load_2d(sb + q * 4096, &map_b, bres_bar, 32 * q, br + c0);
@@ -1019,18 +1021,21 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                 if (++slot == STAGES) { slot = 0; phase ^= 1u; }
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 if (leader && P.bres) {
-                    // B from the resident copy: tile (cb, dh * 3 + dw)
+                    // B from the resident copy: tile (cb, dh * halo_kw + dw)
                     const uint64_t so = static_cast<uint64_t>(s) * stage16;
-                    const int cb = i % P.cblocks, dh = i / P.cblocks;
+                    const int cb = i % P.cblocks, dh = i / P.cblocks, nres = P.ntaps[0] * P.halo_kw;
 #pragma unroll
-                    for (int dw = 0; dw < 3; ++dw)
+                    for (int dw = 0; dw < 3; ++dw) {
+                        if (dw >= P.halo_kw) break;
 #pragma unroll
                         for (int kk = 0; kk < BK / 8; ++kk) {
-                            const uint64_t ad = adesc0 + so + dw * (128 >> 4) + kk * a_kstep;
-                            const uint64_t bd = bresdesc0 + static_cast<uint64_t>((cb * 9 + dh * 3 + dw) * bt_bytes >> 4) +
+                            const uint64_t ad = adesc0 + so + dw * P.dil_w * (128 >> 4) + kk * a_kstep;
+                            const uint64_t bd = bresdesc0 +
+                                                static_cast<uint64_t>((cb * nres + dh * P.halo_kw + dw) * bt_bytes >> 4) +
                                                 kk * b_kstep;
                             mma_tf32(d, ad, bd, idesc, (i > 0 || dw > 0 || kk > 0) ? 1u : 0u);
                         }
+                    }
                     mma_commit(&empty[s]);
                 } else if (leader && P.halo == 2) {
                     const uint64_t so = static_cast<uint64_t>(s) * stage16;
@@ -1812,6 +1817,33 @@ int launch(nncb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CU
         const size_t smem = static_cast<size_t>(P.stages) * sbh + smem_for(P.bn, 0, P.stg_cols) + P.bres_bytes;
         encode_tma_out(&mc, P);
         const unsigned grid = static_cast<unsigned>(std::min<int64_t>(P.tiles, static_cast<int64_t>(ctx->sm_count) * per));
+#ifdef NNCB_TC_TRACE_PROBE
+        // probe builds: the halo launches' per-tile events too (NNCB_TC_TRACE)
+        static const char* htrace_path = getenv("NNCB_TC_TRACE");
+        static unsigned long long* htrace_buf = nullptr;
+        const size_t htrace_bytes = static_cast<size_t>(grid) * 64 * 8 * sizeof(unsigned long long);
+        if (htrace_path) {
+            if (!htrace_buf) NNCB_CUDA(cudaMalloc(&htrace_buf, 2 * 148 * 64 * 8 * sizeof(unsigned long long)));
+            NNCB_CUDA(cudaMemsetAsync(htrace_buf, 0, htrace_bytes, ctx->stream));
+            P.trace = htrace_buf;
+        }
+        struct HTraceDump {
+            const char* path; unsigned long long* buf; size_t bytes; nncb_ctx* ctx; const TcParams& P; unsigned grid; int per;
+            ~HTraceDump() {
+                if (!path) return;
+                std::vector<unsigned long long> h(bytes / 8);
+                cudaStreamSynchronize(ctx->stream);
+                cudaMemcpy(h.data(), buf, bytes, cudaMemcpyDeviceToHost);
+                if (FILE* f = fopen(path, "ab")) {
+                    const long long hdr[6] = {static_cast<long long>(grid), static_cast<long long>(P.tiles), P.bn,
+                                              P.stages, P.stg_bufs, per};
+                    fwrite(hdr, sizeof(hdr), 1, f);
+                    fwrite(h.data(), 8, h.size(), f);
+                    fclose(f);
+                }
+            }
+        } htrace_dump{htrace_path, htrace_buf, htrace_bytes, ctx, P, grid, per};
+#endif
         if (per == 2 && P.colstats)
             tc_gemm_kernel<true, false, 2, false><<<grid, THREADS, smem, ctx->stream>>>(ma, mb, mc, P, em);
         else if (per == 2)
@@ -2362,8 +2394,12 @@ std::vector<int> tile_candidates(const nncb_gemm_desc* d, int64_t N) {
         // (bit 20, full 3x3 patches: correct but measured no faster than
         // kernel-row patches at one CTA per SM; force_tile only)
         // (bit 21, resident B for 64-wide single-N-tile halo convs: correct,
-        // but 15-20% slower at one CTA per SM -- the kernel-row halo tile is
-        // no longer L2-bound at ~79% of the N = 64 MMA ceiling; force_tile only)
+        // but 15-20% slower on the 3x3 convs at one CTA per SM -- the
+        // kernel-row halo tile is no longer L2-bound at ~79% of the N = 64 MMA
+        // ceiling; force_tile only there. The stem's lowered conv keeps its
+        // eight B tiles resident 3-4% faster (its main loop waits on the patch
+        // loads at two stages per CTA): a candidate.)
+        if (halo_stem) cands.push_back(0x280000 | 0x40000 | 64);
     }
     return cands;
 }
@@ -2501,7 +2537,8 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
     g_force_wide = (choice >> 17) & 1;
     g_force_tb = (choice >> 18) & 1;
     g_force_halo = (choice >> 20) & 1 ? 2 : (choice >> 19) & 1;
-    g_force_bres = (choice >> 21) & 1;
+    static const bool no_bres = getenv("NNCB_TC_NO_BRES") != nullptr;   // A/B knob: resident B off
+    g_force_bres = no_bres ? 0 : (choice >> 21) & 1;
     int rc = gemm_tc_route(ctx, d, a, b, bias, out, handled);
     g_force_bn = 0;
     g_force_pair = 0;
@@ -2726,8 +2763,8 @@ int gemm_tc_impl(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, int64_t
             P.TW = HALO_TW;
             P.halo_kw = static_cast<int>(kw);
             P.ntaps[0] = full ? 1 : static_cast<int>(kh);   // k-steps per channel block: one per kernel row, or one
-            const size_t bres = 9 * static_cast<size_t>(P.cblocks) * P.bn * BK * 4;
-            if (g_force_bres && halo33 && !full && Nc <= P.bn &&
+            const size_t bres = static_cast<size_t>(P.ntaps[0] * P.halo_kw) * P.cblocks * P.bn * BK * 4;
+            if (g_force_bres && !full && Nc <= P.bn &&
                 bres + 2 * HALO_A_BYTES + smem_for(P.bn, 0, 8) <= 227 * 1024) {
                 P.bres = 1;
                 P.bres_bytes = static_cast<uint32_t>(bres);

@@ -429,10 +429,11 @@ def test_dgrad_halo_relu_grad_epilogue():
 
 
 @pytest.mark.parametrize("shape", [(2, 32, 32, 3, 64, 7, 2), (2, 17, 23, 3, 32, 7, 2), (4, 64, 64, 3, 64, 7, 2)])
-@pytest.mark.parametrize("tile", [0x80000 | 64, 0x80000 | 0x40000 | 64])
+@pytest.mark.parametrize("tile", [0x80000 | 64, 0x80000 | 0x40000 | 64, 0x280000 | 64, 0x280000 | 0x40000 | 64])
 def test_stem_space_to_depth_halo(shape, tile):
     """The space-to-depth stem's lowered conv (4 kernel rows x 2 taps spaced 2)
-    through halo patches, against the exact path."""
+    through halo patches, against the exact path (bit 21: its eight B tiles
+    resident in shared memory)."""
     n, ih, iw, ci, co, k, s = shape
     g = conv_geom(n, ih, iw, ci, co, k, s)
     if g["ow"] < 8:
