@@ -288,7 +288,9 @@ int red2_blocks() {
 //   them in registers on the channel-stationary path: 128 registers (2
 //   blocks). Before the load ring, 64 registers (4 blocks) were needed to keep
 //   enough loads in flight (5.1 -> 6.1 TB/s for the BN input gradient); with
-//   the ring the 2-block budget measured +1% on the C4 step.
+//   the ring the 2-block budget measured +1% on the C4 step. More than 8
+//   per-channel operands (a chain of BatchNorms: the C2 apply pass) take the
+//   whole register file (C2 mode B +1.5%; C3/C4/C5 have none).
 //   NNCB_EW_MINBLOCKS overrides.
 int resident_blocks(const nncb_ew_program& p) {
     int nch = 0;
@@ -305,7 +307,7 @@ int resident_blocks(const nncb_ew_program& p) {
     if (nred > 0) return nred > 1 || (stats_red && nch > 4) ? red2_blocks() : red1;
     static const int env_min_blocks = getenv("NNCB_EW_MINBLOCKS") ? atoi(getenv("NNCB_EW_MINBLOCKS")) : -1;
     if (env_min_blocks >= 0) return env_min_blocks;
-    return nch >= 3 ? 2 : 0;
+    return nch > 8 ? 1 : nch >= 3 ? 2 : 0;
 }
 
 int ring_stages(const nncb_ew_program& p) {
