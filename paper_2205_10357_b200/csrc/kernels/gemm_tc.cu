@@ -1269,18 +1269,11 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                             r[j] = __float_as_uint(__fadd_rn(__uint_as_float(r[j]), __ldg(P.bias + col0 + j)));
                 }
                 if (P.bn_inv && col0 < P.N) {   // inference BatchNorm (+ residual) (+ ReLU): the EW sequence
+                    // Four columns at a time: their parameters and the row's
+                    // residual as 16-byte loads, consumed at once, so no 32-wide
+                    // residual array is live (the 96-register 2-CTA builds
+                    // spilled it: BN_AFFINE convs ran up to 2.3x slower).
                     const float* rrow = (P.res && valid) ? P.res + (dst - P.out) + col0 : nullptr;
-                    float rv[32];
-                    if (rrow && col0 + 32 <= P.N) {   // the row's 128 residual bytes: 8 independent 16-byte loads
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            const float4 t4 = __ldg(reinterpret_cast<const float4*>(rrow) + q);
-                            rv[4 * q] = t4.x; rv[4 * q + 1] = t4.y; rv[4 * q + 2] = t4.z; rv[4 * q + 3] = t4.w;
-                        }
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) rv[j] = (rrow && col0 + j < P.N) ? __ldg(rrow + j) : 0.f;
-                    }
                     if (col0 + 32 <= P.N) {   // per-column parameters as 16-byte loads (L1 broadcast)
 #pragma unroll
                         for (int q = 0; q < 8; ++q) {
@@ -1289,14 +1282,17 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                             const float4 i4 = __ldg(reinterpret_cast<const float4*>(P.bn_inv + cc));
                             const float4 g4 = __ldg(reinterpret_cast<const float4*>(P.bn_gamma + cc));
                             const float4 b4 = __ldg(reinterpret_cast<const float4*>(P.bn_beta + cc));
+                            const float4 r4 = rrow ? __ldg(reinterpret_cast<const float4*>(rrow) + q)
+                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
                             const float mm[4] = {m4.x, m4.y, m4.z, m4.w}, ii[4] = {i4.x, i4.y, i4.z, i4.w};
                             const float gg[4] = {g4.x, g4.y, g4.z, g4.w}, bb[4] = {b4.x, b4.y, b4.z, b4.w};
+                            const float rr[4] = {r4.x, r4.y, r4.z, r4.w};
 #pragma unroll
                             for (int u = 0; u < 4; ++u) {
                                 const int j = 4 * q + u;
                                 float v = __fsub_rn(__uint_as_float(r[j]), mm[u]);
                                 v = __fadd_rn(__fmul_rn(__fmul_rn(v, ii[u]), gg[u]), bb[u]);
-                                if (rrow) v = __fadd_rn(v, rv[j]);
+                                if (rrow) v = __fadd_rn(v, rr[u]);
                                 if (P.relu) v = v > 0.f ? v : 0.f;
                                 r[j] = __float_as_uint(v);
                             }
@@ -1309,7 +1305,7 @@ __global__ void __launch_bounds__(MA ? THREADS + 128 : THREADS, MINB)
                                 float v = __fsub_rn(__uint_as_float(r[j]), __ldg(P.bn_mean + cc));
                                 v = __fmul_rn(__fmul_rn(v, __ldg(P.bn_inv + cc)), __ldg(P.bn_gamma + cc));
                                 v = __fadd_rn(v, __ldg(P.bn_beta + cc));
-                                if (rrow) v = __fadd_rn(v, rv[j]);
+                                if (rrow) v = __fadd_rn(v, __ldg(rrow + j));
                                 if (P.relu) v = v > 0.f ? v : 0.f;
                                 r[j] = __float_as_uint(v);
                             }

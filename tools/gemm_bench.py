@@ -43,6 +43,7 @@ def main():
     ap.add_argument("--precision", type=int, default=0, help="0 tf32, 1 exact fp32, 2 bf16 operands")
     ap.add_argument("--dense", default="", help="dense shapes batch:in:out,... instead of conv layers")
     ap.add_argument("--eg", action="store_true", help="dgrad GEMMs run the ReLU-gradient + BN-sums epilogue")
+    ap.add_argument("--bn", action="store_true", help="forward GEMMs run the inference BatchNorm + ReLU epilogue")
     ap.add_argument("--res", action="store_true", help="with --eg: add a residual gradient")
     ap.add_argument("--tile", default="auto", help="auto | 128 | 256 | p128 | p256 | w128 | t128 | h64 | th128 ... (p = CTA pair, w = wide staging, t = K-major weights, h = halo patches)")
     a = ap.parse_args()
@@ -85,6 +86,11 @@ def main():
             d = GemmDesc(kind=code, precision=a.precision, epilogue=4 if cs else 0, **g)
             if cs:
                 d.colstats = cs.p
+            if a.bn and kind == "fwd":
+                bnp = [Dev(np.full(co, v, np.float32)) for v in (0.1, 1.0, 0.9, 0.05)]
+                d.epilogue |= 32 | 2
+                d.bn_mean, d.bn_var, d.bn_gamma, d.bn_beta = (t.p for t in bnp)
+                d.bn_eps = 1e-5
             if a.eg and kind == "dgrad":
                 eg = [Dev(nbytes=a.batch * h * h * ci * 4) for _ in range(3)] + [Dev(nbytes=2 * ci * 4), Dev(nbytes=2 * ci * 8)]
                 d.epilogue = 8
