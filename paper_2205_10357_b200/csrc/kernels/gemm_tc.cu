@@ -2138,6 +2138,7 @@ int tune_mode() {
         const char* e = getenv("NNCB_TC_AUTOTUNE");
         if (!e || !strcmp(e, "table")) return 1;
         if (!strcmp(e, "0")) return 0;
+        if (!strcmp(e, "fresh")) return 3;   // live, ignoring the committed table (tools/tune_tiles.py)
         return 2;   // live
     }();
     return m;
@@ -2146,6 +2147,7 @@ std::mutex g_tune_mu;
 std::map<std::string, int>& tuned_table() {
     static std::map<std::string, int> t = [] {
         std::map<std::string, int> m;
+        if (tune_mode() == 3) return m;   // fresh: every shape measured anew
         for (const TileEntry& e : kTileTable)
             if (e.key) m[e.key] = e.choice;
         return m;
@@ -2442,7 +2444,7 @@ int gemm_tc(nncb_ctx* ctx, const nncb_gemm_desc* d, const float* a, const float*
     }
     if (bf16 && d->kind == NNCB_DENSE_WGRAD) d = &wd;
     const int mode = tune_mode();
-    const bool enabled = mode == 2;
+    const bool enabled = mode >= 2;
     std::mutex& mu = g_tune_mu;
     std::map<std::string, int>& tuned = tuned_table();
     const bool dense = d->kind <= NNCB_DENSE_WGRAD;

@@ -1,7 +1,8 @@
 """Regenerates paper_2205_10357_b200/csrc/kernels/tile_table.inc: runs the
 BASELINE workloads (C1, C3/C4 ResNet-50-shaped, C5 MLP; C2 has no GEMMs), in the
 tf32 and bf16 precisions, with
-NNCB_TC_AUTOTUNE=live on a B200 so every GEMM shape they launch is measured
+NNCB_TC_AUTOTUNE=fresh on a B200 so every GEMM shape they launch is measured
+(the committed table is not consulted)
 (candidates timed on a scratch output), then writes the chosen tile per shape.
 The committed table makes the default (table) mode deterministic across
 processes and boxes. Run under gpurun:  python tools/tune_tiles.py [out.inc]"""
@@ -9,7 +10,7 @@ import ctypes
 import os
 import sys
 
-os.environ["NNCB_TC_AUTOTUNE"] = "live"
+os.environ["NNCB_TC_AUTOTUNE"] = "fresh"   # live, without consulting the committed table
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2205_10357_b200 as P  # noqa: E402
 from paper_2205_10357_b200 import workloads as W  # noqa: E402
