@@ -45,3 +45,33 @@ def test_two_processes_give_bitwise_identical_tf32_gradients(tmp_path):
     assert sorted(a.files) == sorted(b.files) and len(a.files) > 100
     for k in a.files:
         assert np.array_equal(a[k], b[k]), k
+
+
+FRESH = r"""
+import ctypes, sys
+sys.path.insert(0, %r)
+import paper_2205_10357_b200 as P
+from paper_2205_10357_b200 import workloads as W
+k = P._kern
+assert k.nncb_gemm_tuning_mode() == 3
+m = P.CompiledModel(W.c1_small_cnn(32, bn=True), precision=P.PREC_TF32)
+m.run({"x": W.uniform((32, 32, 32, 3), 1, "x")})
+k.nncb_gemm_tuning_export.restype = ctypes.c_int
+k.nncb_gemm_tuning_export.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
+n = ctypes.c_size_t()
+k.nncb_gemm_tuning_export(None, 0, ctypes.byref(n))
+buf = ctypes.create_string_buffer(n.value)
+assert k.nncb_gemm_tuning_export(buf, n.value, ctypes.byref(n)) == 0
+print(buf.value.decode().count("\n"))
+"""
+
+
+def test_fresh_tuning_measures_shapes_without_the_committed_table():
+    """NNCB_TC_AUTOTUNE=fresh (what tools/tune_tiles.py runs): the committed
+    table is not consulted, so the C1 inference shapes -- all of which the
+    table holds -- are measured in the process and exported."""
+    env = dict(os.environ, NNCB_TC_AUTOTUNE="fresh")
+    r = subprocess.run([sys.executable, "-c", FRESH % ROOT], capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    measured = int(r.stdout.strip().splitlines()[-1])
+    assert 0 < measured < 20, measured   # only this process's shapes, not the committed table's 168
